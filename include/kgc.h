@@ -1,0 +1,184 @@
+/*
+ * kgc.h -- C ABI of the B200-native TransE completion join (libkgc.so).
+ *
+ * What it computes.  Knowledge-graph completion, Definition 1 of arXiv
+ * 2307.12059, for TransE:
+ *
+ *     R(eps) = { (h, r, t) in [0,N) x [0,R) x [0,N) :  || E_h + Rel_r - E_t ||_p <= eps }
+ *
+ * with p = norm in {1, 2}, L2 the non-squared Euclidean norm, the bound
+ * inclusive, self edges (h == t) included, every relation vector independent.
+ * ``eps`` is the DISTANCE threshold theta: a caller holding a score threshold
+ * s* (score >= s*) passes eps = -s* because dist3 = -score.
+ *
+ * How: the triple problem is recast as a binary similarity join
+ * q = h + r against t; pivot distances and sorting
+ * give contiguous surviving tail-tile ranges per query
+ * tile by Lemma 1 and Lemma 2, so whole tiles are skipped;
+ * surviving tiles are verified on the GPU (tcgen05 TF32 tensor-core filter
+ * with a rigorous guard band for L2, FP32 SIMT for L1) and every candidate is
+ * re-checked in FP64 before it is emitted ("verify if the
+ * results are valid").  The filtering is lossless: the
+ * result set is the brute-force set.
+ *
+ * Conventions for every call:
+ *   - int-returning calls return a kgc_status (0 = OK, < 0 = error); the
+ *     message of the last error is available from kgc_last_error().
+ *   - No call keeps a pointer passed by the caller after it returns.
+ *   - A context is not thread-safe: one context per host thread.
+ *   - Pointers may be host (pageable or pinned) or device memory of the
+ *     context's device; the library detects which with
+ *     cudaPointerGetAttributes.
+ */
+#ifndef KGC_H_
+#define KGC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define KGC_ABI_VERSION 1
+
+/* Opaque context: owns device buffers, the stream, per-join statistics. */
+typedef struct kgc_ctx kgc_ctx;
+
+typedef enum {
+    KGC_OK = 0,
+    KGC_EINVAL = -1,   /* bad argument: NULL pointer, N<0, R<0, d<1 or d>KGC_MAX_DIM, norm not 1/2, eps<0 or non-finite */
+    KGC_EDATA = -2,    /* a non-finite value in E or Rel */
+    KGC_ENOMEM = -3,   /* device or host allocation failed */
+    KGC_ECUDA = -4,    /* CUDA runtime error (message in kgc_last_error) */
+    KGC_ENODEV = -5,   /* no CUDA device / not an sm_100 device */
+    KGC_ESTATE = -6    /* call out of order (e.g. kgc_results before any successful kgc_join) */
+} kgc_status;
+
+#define KGC_MAX_DIM 1024
+
+/* One result record, 16 bytes.  dist is the non-squared L_p distance
+ * computed in FP64 and rounded to float. */
+typedef struct {
+    int32_t h, r, t;
+    float dist;
+} kgc_triplet;
+
+/* Options for kgc_create.  Fill with kgc_default_options() first. */
+typedef struct {
+    int32_t device;           /* CUDA device ordinal; -1 = the current device                      */
+    int32_t rank, world;      /* this context computes shard `rank` of `world` of the work list     */
+                              /* (query tiles split by predicted cost; results stay sharded)       */
+    int32_t prune;            /* 1 = Lemma 1/2 tile pruning (default); 0 = every tile (naive control,*/
+                              /*     PAPER.md:473 "naive GPU approach")                            */
+    int32_t pivot;            /* 0 = zero vector (default); 1 = mean of the tails      */
+    int32_t l2_engine;        /* 0 = auto (= 1); 1 = tcgen05 TF32 filter; 2 = FP32 SIMT filter      */
+    int32_t chunk_tiles;      /* max tail tiles per work item (load-balance granularity); 0 = auto */
+    int32_t reserved;
+    int64_t result_capacity;  /* initial result-buffer capacity in triplets; 0 = auto (grows)       */
+    void*   stream;           /* cudaStream_t to run on; NULL = a stream the context creates       */
+} kgc_options;
+
+/* Per-join statistics (of the last successful kgc_join). */
+typedef struct {
+    int64_t N, R;
+    int32_t d, norm;
+    float eps;
+    int32_t rank, world;
+    double triplets;              /* N*N*R candidate triplets (PAPER.md:460 counts 14951^2 x 2690) */
+    int64_t query_tile_rows;      /* rows per query tile (128)                                     */
+    int64_t tail_tile_rows;       /* rows per tail tile (256 for the L2 engine, 128 for L1)        */
+    int64_t query_tiles;          /* per relation                                                  */
+    int64_t tail_tiles;
+    int64_t tile_pairs_total;     /* R * query_tiles * tail_tiles                                  */
+    int64_t tile_pairs_surviving; /* after Lemma 1/2 pruning, all shards                           */
+    int64_t tile_pairs_mine;      /* processed by this context's shard                             */
+    int64_t work_items_mine;
+    int64_t candidates;           /* pairs that passed the GPU filter (this shard)                 */
+    int64_t results;              /* triplets emitted (this shard)                                 */
+    int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved inside kgc_join                     */
+    int32_t launches;             /* kernels launched by the last kgc_join                         */
+    int32_t reruns;               /* capacity-overflow reruns                                      */
+    /* device time per phase (CUDA events on the context's stream), milliseconds */
+    float ms_total, ms_h2d, ms_keys, ms_sort, ms_ranges, ms_stage, ms_tiles, ms_recheck;
+} kgc_stats_t;
+
+/* Fill *opt with defaults: device -1, rank 0, world 1, prune 1, pivot 0,
+ * l2_engine 0, chunk_tiles 0, result_capacity 0, stream NULL. */
+void kgc_default_options(kgc_options* opt);
+
+/* Create a context.  opt == NULL means defaults.  Returns KGC_ENODEV when no
+ * sm_100 device is present.  *out is set to NULL on error. */
+int kgc_create(kgc_ctx** out, const kgc_options* opt);
+
+/* Run the join R(eps) above.
+ *   E   : N x d float32, row-major, contiguous (entity embeddings)
+ *   Rel : R x d float32, row-major, contiguous (relation embeddings)
+ *   norm: 1 or 2; eps: distance threshold >= 0, finite.
+ * N == 0 or R == 0 is valid and yields 0 results (E / Rel may then be NULL).
+ * Blocks until the result count is known.  On error the previous results are
+ * dropped and the context stays usable. */
+int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t N, int64_t R, int32_t d,
+             int32_t norm, float eps);
+
+/* Copy min(count, capacity) result records of the last join into `out`
+ * (host or device memory, caller-owned) and return the total count (>= 0),
+ * or a negative kgc_status.  out may be NULL to query the count.  Record
+ * order is unspecified (each triplet appears exactly once). */
+int64_t kgc_results(kgc_ctx* ctx, kgc_triplet* out, int64_t capacity);
+
+/* Statistics of the last successful join. */
+int kgc_stats(const kgc_ctx* ctx, kgc_stats_t* out);
+
+/* Message of the last error on this context ("" if none).  Owned by the
+ * context; valid until the next call on it.  ctx == NULL gives the last
+ * kgc_create error. */
+const char* kgc_last_error(const kgc_ctx* ctx);
+
+/* Use `stream` (a cudaStream_t) for subsequent joins; NULL = the context's own. */
+int kgc_set_stream(kgc_ctx* ctx, void* stream);
+
+/* Release every resource of the context.  NULL is a no-op. */
+void kgc_destroy(kgc_ctx* ctx);
+
+/* Inspection hooks for tests: copy an intermediate array of the last join to
+ * host memory `out` (capacity `bytes`); returns the number of bytes the array
+ * has (copies min of the two), or a negative kgc_status.
+ *   KGC_INSPECT_TAIL_KEYS   float[N]     d(t, p) per tail, original order (K1)
+ *   KGC_INSPECT_QUERY_KEYS  float[R*N]   d(h + r, p), [r][h] (K1)
+ *   KGC_INSPECT_TAIL_PERM   int32[N]     sorted position -> tail index (K2)
+ *   KGC_INSPECT_QUERY_PERM  int32[R*N]   per relation, sorted position -> head (K2)
+ *   KGC_INSPECT_TILE_RANGES int32[R*QT*2] surviving tail-tile range [sb, eb] per query tile (K3)
+ *   KGC_INSPECT_QUERY_COST  int64[R*QT]  exclusive prefix of surviving tiles per query tile (K3)  */
+enum {
+    KGC_INSPECT_TAIL_KEYS = 1,
+    KGC_INSPECT_QUERY_KEYS = 2,
+    KGC_INSPECT_TAIL_PERM = 3,
+    KGC_INSPECT_QUERY_PERM = 4,
+    KGC_INSPECT_TILE_RANGES = 5,
+    KGC_INSPECT_QUERY_COST = 6
+};
+int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes);
+
+/* Pure host function (no device needed): the shard of query tiles owned by
+ * `rank` of `world`, given the exclusive prefix sums `cum` (length n) of the
+ * per-query-tile surviving-tile counts and their grand total.  Query tile q
+ * belongs to rank min(world-1, floor(world * cum[q] / total)) (total == 0:
+ * everything to rank 0).  Writes the half-open range [*begin, *end) and
+ * returns its cost (surviving tiles), or KGC_EINVAL.  The device uses the
+ * same rule. */
+int64_t kgc_shard_range(const int64_t* cum, int64_t n, int64_t total, int32_t rank, int32_t world,
+                        int64_t* begin, int64_t* end);
+
+/* ABI version compiled into the library (== KGC_ABI_VERSION). */
+int kgc_abi_version(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* KGC_H_ */

@@ -1,0 +1,587 @@
+// kgc_api.cu -- host runtime and C ABI of libkgc (include/kgc.h).
+//
+// One kgc_join runs the whole hot path on the context's stream:
+//   a1 stage inputs (H2D when the caller passes host pointers)
+//   a2 K1 pivot distances (tails once; queries per relation)
+//   a3 K2 sorts
+//   a4 K3 tile ranges (Lemma 1 + 2), shard split, work items   -> sync #1
+//   stage operand tiles
+//   a5/a6 K4 (L2, tcgen05) or K5 (L1 / L2 SIMT) over the work items
+//   a7/a8 K6+K7 FP64 re-check and compaction                    -> sync #2
+// Device buffers grow monotonically and are reused across joins.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/kgc.h"
+#include "kgc_internal.h"
+
+using namespace kgc;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+};
+
+enum Phase { EV_START, EV_H2D, EV_KEYS, EV_SORT, EV_RANGES, EV_STAGE, EV_TILES, EV_VERIFY, EV_COUNT };
+
+}  // namespace
+
+struct kgc_ctx {
+    kgc_options opt{};
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::string err;
+    DevBuf E, Rel, pivot, kt, kq, mm_t, mm_q, sk0, sv0, sk1, sv1, counts, scan_tmp, qperm, qskey, tperm, tskey, tmin,
+        tmax, cmax, cmin, ranges, cost, cum, nitem, item_off, items, Qp, qs, Tp, T2, tstile, cand, res, ctr;
+    long long cand_cap = 0, res_cap = 0;
+    long long n_results = -1;
+    kgc_stats_t st{};
+    cudaEvent_t ev[EV_COUNT] = {};
+    int launches = 0;
+    // geometry of the last join (for kgc_inspect)
+    long long N = 0, R = 0;
+    int QT = 0, TT = 0, BN = 0;
+    bool have_join = false;
+};
+
+static std::string g_create_err;
+
+static void set_err(kgc_ctx* c, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) {                                                                   \
+            set_err(ctx, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+            return e_ == cudaErrorMemoryAllocation ? KGC_ENOMEM : KGC_ECUDA;                       \
+        }                                                                                          \
+    } while (0)
+
+#define LAUNCHED(n)                                                                                \
+    do {                                                                                           \
+        ctx->launches += (n);                                                                      \
+        cudaError_t e_ = cudaGetLastError();                                                       \
+        if (e_ != cudaSuccess) {                                                                   \
+            set_err(ctx, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__); \
+            return KGC_ECUDA;                                                                      \
+        }                                                                                          \
+    } while (0)
+
+static cudaError_t ensure(DevBuf& b, size_t bytes) {
+    if (bytes <= b.n && b.p) return cudaSuccess;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.n = 0;
+    size_t nb = bytes + bytes / 8 + 256;
+    cudaError_t e = cudaMalloc(&b.p, nb);
+    if (e == cudaSuccess) b.n = nb;
+    return e;
+}
+
+template <typename T>
+static T* P(DevBuf& b) {
+    return reinterpret_cast<T*>(b.p);
+}
+
+static bool is_device_ptr(const void* p, int device) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) && (a.device == device);
+}
+
+extern "C" {
+
+int kgc_abi_version(void) { return KGC_ABI_VERSION; }
+
+void kgc_default_options(kgc_options* o) {
+    if (!o) return;
+    memset(o, 0, sizeof *o);
+    o->device = -1;
+    o->rank = 0;
+    o->world = 1;
+    o->prune = 1;
+    o->pivot = 0;
+    o->l2_engine = 0;
+    o->chunk_tiles = 0;
+    o->result_capacity = 0;
+    o->stream = nullptr;
+}
+
+int kgc_create(kgc_ctx** out, const kgc_options* opt) {
+    if (!out) return KGC_EINVAL;
+    *out = nullptr;
+    kgc_options o;
+    if (opt) o = *opt; else kgc_default_options(&o);
+    if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
+        o.l2_engine > 2 || o.chunk_tiles < 0 || o.result_capacity < 0) {
+        g_create_err = "kgc_create: invalid options";
+        return KGC_EINVAL;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        g_create_err = "kgc_create: no CUDA device";
+        return KGC_ENODEV;
+    }
+    int dev = o.device;
+    if (dev < 0) cudaGetDevice(&dev);
+    if (dev >= ndev) {
+        g_create_err = "kgc_create: device ordinal out of range";
+        return KGC_EINVAL;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10 || prop.minor != 0) {
+        cudaGetLastError();
+        g_create_err = "kgc_create: libkgc is built for sm_100a (B200); device " + std::to_string(dev) + " is sm_" +
+                       std::to_string(prop.major) + std::to_string(prop.minor);
+        return KGC_ENODEV;
+    }
+    kgc_ctx* ctx = new kgc_ctx();
+    ctx->opt = o;
+    ctx->device = dev;
+    ctx->num_sms = prop.multiProcessorCount;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+    if (o.stream) {
+        ctx->stream = reinterpret_cast<cudaStream_t>(o.stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+            g_create_err = "kgc_create: cudaStreamCreate failed";
+            delete ctx;
+            return KGC_ECUDA;
+        }
+        ctx->stream = ctx->own_stream;
+    }
+    for (auto& e : ctx->ev) cudaEventCreate(&e);
+    cudaSetDevice(prev);
+    *out = ctx;
+    return KGC_OK;
+}
+
+void kgc_destroy(kgc_ctx* ctx) {
+    if (!ctx) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    DevBuf* bufs[] = {&ctx->E,     &ctx->Rel,    &ctx->pivot,  &ctx->kt,    &ctx->kq,     &ctx->mm_t,   &ctx->mm_q,
+                      &ctx->sk0,   &ctx->sv0,    &ctx->sk1,    &ctx->sv1,   &ctx->counts, &ctx->scan_tmp,
+                      &ctx->qperm, &ctx->qskey,  &ctx->tperm,  &ctx->tskey, &ctx->tmin,   &ctx->tmax,   &ctx->cmax,
+                      &ctx->cmin,  &ctx->ranges, &ctx->cost,   &ctx->cum,   &ctx->nitem,  &ctx->item_off,
+                      &ctx->items, &ctx->Qp,     &ctx->qs,     &ctx->Tp,    &ctx->T2,     &ctx->tstile, &ctx->cand,
+                      &ctx->res,   &ctx->ctr};
+    for (DevBuf* b : bufs)
+        if (b->p) cudaFree(b->p);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    cudaSetDevice(prev);
+    delete ctx;
+}
+
+const char* kgc_last_error(const kgc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+int kgc_set_stream(kgc_ctx* ctx, void* stream) {
+    if (!ctx) return KGC_EINVAL;
+    ctx->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : ctx->own_stream;
+    if (!ctx->stream) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(ctx->device);
+        cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+        cudaSetDevice(prev);
+        ctx->stream = ctx->own_stream;
+    }
+    return KGC_OK;
+}
+
+int64_t kgc_shard_range(const int64_t* cum, int64_t n, int64_t total, int32_t rank, int32_t world, int64_t* begin,
+                        int64_t* end) {
+    if (!cum || !begin || !end || n < 0 || total < 0 || world < 1 || rank < 0 || rank >= world) return KGC_EINVAL;
+    int64_t b = n, e = 0, cost = 0;
+    for (int64_t q = 0; q < n; ++q) {
+        int64_t owner = 0;
+        if (total > 0) {
+            int64_t o = (int64_t)world * cum[q] / total;
+            owner = o < world - 1 ? o : world - 1;
+        }
+        if (owner == rank) {
+            if (q < b) b = q;
+            e = q + 1;
+            int64_t next = q + 1 < n ? cum[q + 1] : total;
+            cost += next - cum[q];
+        }
+    }
+    if (b > e) b = e = 0;
+    *begin = b;
+    *end = e;
+    return cost;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ join
+static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long long N, long long R, int d, int norm,
+                     float eps) {
+    cudaStream_t s = ctx->stream;
+    ctx->launches = 0;
+    kgc_stats_t& st = ctx->st;
+    memset(&st, 0, sizeof st);
+    st.N = N;
+    st.R = R;
+    st.d = d;
+    st.norm = norm;
+    st.eps = eps;
+    st.rank = ctx->opt.rank;
+    st.world = ctx->opt.world;
+    st.triplets = (double)N * (double)N * (double)R;
+
+    const bool tc = norm == 2 && ctx->opt.l2_engine != 2 && ((d + 7) / 8) * 8 <= TC_MAX_KPAD;
+    if (norm == 2 && ctx->opt.l2_engine == 1 && !tc) {
+        set_err(ctx, "l2_engine=1 (tcgen05) supports d <= %d", TC_MAX_KPAD);
+        return KGC_EINVAL;
+    }
+    const int Kpad = ((d + 7) / 8) * 8;
+    const int BN = tc ? BN_TC : BN_SIMT;
+    const int QT = (int)((N + BM - 1) / BM);
+    const int TT = (int)((N + BN - 1) / BN);
+    const long long nq = R * (long long)QT;
+    const int chunk = ctx->opt.chunk_tiles > 0 ? ctx->opt.chunk_tiles : (tc ? 16 : 8);
+    ctx->N = N;
+    ctx->R = R;
+    ctx->QT = QT;
+    ctx->TT = TT;
+    ctx->BN = BN;
+    st.query_tile_rows = BM;
+    st.tail_tile_rows = BN;
+    st.query_tiles = QT;
+    st.tail_tiles = TT;
+    st.tile_pairs_total = nq * TT;
+
+    CK(cudaEventRecord(ctx->ev[EV_START], s));
+    // ---- a1: inputs on the device
+    const float* E = E_in;
+    const float* Rel = Rel_in;
+    if (!is_device_ptr(E_in, ctx->device)) {
+        CK(ensure(ctx->E, (size_t)N * d * 4));
+        CK(cudaMemcpyAsync(ctx->E.p, E_in, (size_t)N * d * 4, cudaMemcpyDefault, s));
+        E = P<float>(ctx->E);
+        st.h2d_bytes += (int64_t)N * d * 4;
+    }
+    if (!is_device_ptr(Rel_in, ctx->device)) {
+        CK(ensure(ctx->Rel, (size_t)R * d * 4));
+        CK(cudaMemcpyAsync(ctx->Rel.p, Rel_in, (size_t)R * d * 4, cudaMemcpyDefault, s));
+        Rel = P<float>(ctx->Rel);
+        st.h2d_bytes += (int64_t)R * d * 4;
+    }
+    CK(cudaEventRecord(ctx->ev[EV_H2D], s));
+
+    // ---- allocations for the preprocessing
+    const size_t NR = (size_t)N * R;
+    const size_t nsort = std::max(NR, (size_t)N);
+    CK(ensure(ctx->ctr, sizeof(DevCounters)));
+    CK(ensure(ctx->kt, (size_t)N * 4));
+    CK(ensure(ctx->kq, NR * 4));
+    CK(ensure(ctx->mm_t, 2 * 4));
+    CK(ensure(ctx->mm_q, (size_t)R * 2 * 4));
+    CK(ensure(ctx->sk0, nsort * 4));
+    CK(ensure(ctx->sv0, nsort * 4));
+    CK(ensure(ctx->sk1, nsort * 4));
+    CK(ensure(ctx->sv1, nsort * 4));
+    CK(ensure(ctx->counts, std::max(radix_counts_len(R, N), radix_counts_len(1, N)) * 4));
+    const size_t scan_n = std::max({radix_counts_len(R, N), (size_t)nq, (size_t)1});
+    CK(ensure(ctx->scan_tmp, scan_tmp_bytes(scan_n)));
+    CK(ensure(ctx->qperm, NR * 4));
+    CK(ensure(ctx->qskey, NR * 4));
+    CK(ensure(ctx->tperm, (size_t)N * 4));
+    CK(ensure(ctx->tskey, (size_t)N * 4));
+    CK(ensure(ctx->tmin, (size_t)TT * 4));
+    CK(ensure(ctx->tmax, (size_t)TT * 4));
+    CK(ensure(ctx->cmax, (size_t)TT * 4));
+    CK(ensure(ctx->cmin, (size_t)TT * 4));
+    CK(ensure(ctx->ranges, (size_t)nq * 8));
+    CK(ensure(ctx->cost, (size_t)nq * 8));
+    CK(ensure(ctx->cum, (size_t)nq * 8));
+    CK(ensure(ctx->nitem, (size_t)nq * 4));
+    CK(ensure(ctx->item_off, (size_t)nq * 4));
+    DevCounters hc{};
+    hc.tq_begin = INT_MAX;
+    hc.tq_end = 0;
+    CK(cudaMemcpyAsync(ctx->ctr.p, &hc, sizeof hc, cudaMemcpyHostToDevice, s));
+    DevCounters* dctr = P<DevCounters>(ctx->ctr);
+
+    const double* pivot = nullptr;
+    if (ctx->opt.pivot == 1) {
+        CK(ensure(ctx->pivot, (size_t)d * 8));
+        launch_pivot_mean(E, N, d, P<double>(ctx->pivot), s);
+        LAUNCHED(1);
+        pivot = P<double>(ctx->pivot);
+    }
+    // ---- a2: K1 keys
+    launch_tail_keys(E, N, d, norm, pivot, P<float>(ctx->kt), P<unsigned>(ctx->mm_t), &dctr->nonfinite, s);
+    LAUNCHED(2);
+    launch_query_keys(E, Rel, N, R, d, norm, pivot, P<float>(ctx->kq), P<unsigned>(ctx->mm_q), &dctr->nonfinite, s);
+    LAUNCHED(2);
+    CK(cudaEventRecord(ctx->ev[EV_KEYS], s));
+    // ---- a3: K2 sorts (tails once, queries per relation)
+    radix_sort_segments(P<float>(ctx->kt), P<unsigned>(ctx->mm_t), 1, N, P<unsigned>(ctx->sk0), P<unsigned>(ctx->sv0),
+                        P<unsigned>(ctx->sk1), P<unsigned>(ctx->sv1), P<int>(ctx->counts), P<int>(ctx->tperm),
+                        P<float>(ctx->tskey), ctx->scan_tmp.p, ctx->scan_tmp.n, s, &ctx->launches);
+    LAUNCHED(0);
+    radix_sort_segments(P<float>(ctx->kq), P<unsigned>(ctx->mm_q), R, N, P<unsigned>(ctx->sk0), P<unsigned>(ctx->sv0),
+                        P<unsigned>(ctx->sk1), P<unsigned>(ctx->sv1), P<int>(ctx->counts), P<int>(ctx->qperm),
+                        P<float>(ctx->qskey), ctx->scan_tmp.p, ctx->scan_tmp.n, s, &ctx->launches);
+    LAUNCHED(0);
+    CK(cudaEventRecord(ctx->ev[EV_SORT], s));
+    // ---- a4: K3 tile ranges, shard split, work items
+    launch_tail_tile_bounds(P<float>(ctx->tskey), N, BN, TT, P<float>(ctx->tmin), P<float>(ctx->tmax),
+                            P<float>(ctx->cmax), P<float>(ctx->cmin), s, &ctx->launches);
+    LAUNCHED(0);
+    launch_query_ranges(P<float>(ctx->qskey), N, R, QT, TT, P<float>(ctx->cmax), P<float>(ctx->cmin), eps,
+                        ctx->opt.prune, P<int2>(ctx->ranges), P<long long>(ctx->cost), s);
+    LAUNCHED(1);
+    scan_exclusive_i64(P<long long>(ctx->cost), P<long long>(ctx->cum), (size_t)nq, &dctr->total_cost,
+                       ctx->scan_tmp.p, s, &ctx->launches);
+    LAUNCHED(0);
+    launch_shard_items(P<int2>(ctx->ranges), P<long long>(ctx->cost), P<long long>(ctx->cum), nq, ctx->opt.rank,
+                       ctx->opt.world, chunk, dctr, P<int>(ctx->nitem), P<int>(ctx->item_off), nullptr,
+                       ctx->scan_tmp.p, s, &ctx->launches, 0);
+    LAUNCHED(0);
+    // sync #1: plan totals
+    struct {
+        DevCounters c;
+        int last_n, last_off;
+    } h1{};
+    CK(cudaMemcpyAsync(&h1.c, ctx->ctr.p, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&h1.last_n, P<int>(ctx->nitem) + (nq - 1), 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&h1.last_off, P<int>(ctx->item_off) + (nq - 1), 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h1.c.nonfinite) {
+        set_err(ctx, "non-finite value in E or Rel");
+        return KGC_EDATA;
+    }
+    const long long n_items = (long long)h1.last_off + h1.last_n;
+    st.tile_pairs_surviving = h1.c.total_cost;
+    st.tile_pairs_mine = h1.c.my_cost;
+    st.work_items_mine = n_items;
+    const int tq0 = h1.c.tq_begin == INT_MAX ? 0 : h1.c.tq_begin;
+    const int tq1 = h1.c.tq_begin == INT_MAX ? 0 : h1.c.tq_end;
+    if (n_items > 0) {
+        CK(ensure(ctx->items, (size_t)n_items * 16));
+        launch_shard_items(P<int2>(ctx->ranges), P<long long>(ctx->cost), P<long long>(ctx->cum), nq, ctx->opt.rank,
+                           ctx->opt.world, chunk, dctr, P<int>(ctx->nitem), P<int>(ctx->item_off),
+                           P<int4>(ctx->items), ctx->scan_tmp.p, s, &ctx->launches, 1);
+        LAUNCHED(0);
+    }
+    CK(cudaEventRecord(ctx->ev[EV_RANGES], s));
+
+    // ---- stage operand tiles (tails: all; queries: this shard's range)
+    if (n_items > 0) {
+        CK(ensure(ctx->Tp, (size_t)TT * BN * Kpad * 4));
+        CK(ensure(ctx->T2, (size_t)TT * BN * 4));
+        CK(ensure(ctx->tstile, (size_t)TT * 8));
+        CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * BM * Kpad * 4));
+        CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * BM * 16));
+        launch_stage_tails(E, P<int>(ctx->tperm), N, d, Kpad, BN, TT, tc ? 1 : 0, P<float>(ctx->Tp), P<float>(ctx->T2),
+                           P<float2>(ctx->tstile), s);
+        LAUNCHED(1);
+        launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, tq0, tq1, tc ? 1 : 0, norm, eps,
+                             P<float>(ctx->Qp), P<float4>(ctx->qs), s);
+        LAUNCHED(1);
+    }
+    CK(cudaEventRecord(ctx->ev[EV_STAGE], s));
+
+    // ---- a5/a6 tiles, a7/a8 verify (rerun on capacity overflow)
+    if (ctx->cand_cap == 0) ctx->cand_cap = 1 << 20;
+    if (ctx->res_cap == 0) ctx->res_cap = ctx->opt.result_capacity > 0 ? ctx->opt.result_capacity : (1 << 20);
+    long long cand_n = 0, res_n = 0;
+    for (int attempt = 0;; ++attempt) {
+        CK(ensure(ctx->cand, (size_t)ctx->cand_cap * 8));
+        CK(ensure(ctx->res, (size_t)ctx->res_cap * 16));
+        CK(cudaMemsetAsync(&dctr->cand, 0, 16, s));  // cand + res counters
+        if (attempt > 0) CK(cudaEventRecord(ctx->ev[EV_STAGE], s));
+        TileParams tp{};
+        tp.Qp = P<float>(ctx->Qp);
+        tp.qs = P<float4>(ctx->qs);
+        tp.Tp = P<float>(ctx->Tp);
+        tp.T2 = P<float>(ctx->T2);
+        tp.tstile = P<float2>(ctx->tstile);
+        tp.items = P<int4>(ctx->items);
+        tp.n_items = n_items;
+        tp.Kpad = Kpad;
+        tp.tq0 = tq0;
+        tp.N = (int)N;
+        tp.theta = eps;
+        tp.eta = (float)((Kpad / 8) * 3.814697265625e-06);  // Ksteps * 2^-18
+        tp.cand = P<int2>(ctx->cand);
+        tp.cand_count = &dctr->cand;
+        tp.cand_cap = ctx->cand_cap;
+        if (n_items > 0) {
+            if (tc) launch_tiles_tc(tp, ctx->num_sms, s);
+            else launch_tiles_simt(tp, norm, ctx->num_sms, s);
+            LAUNCHED(1);
+        }
+        CK(cudaEventRecord(ctx->ev[EV_TILES], s));
+        if (n_items > 0) {
+            launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, P<int>(ctx->qperm), P<int>(ctx->tperm), E,
+                          Rel, N, QT, d, norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p), &dctr->res,
+                          ctx->res_cap, ctx->num_sms, s);
+            LAUNCHED(1);
+        }
+        CK(cudaEventRecord(ctx->ev[EV_VERIFY], s));
+        unsigned long long hcnt[2];
+        CK(cudaMemcpyAsync(hcnt, &dctr->cand, 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        cand_n = (long long)hcnt[0];
+        res_n = (long long)hcnt[1];
+        if (cand_n > ctx->cand_cap) {
+            ctx->cand_cap = cand_n + cand_n / 4 + 1024;
+            st.reruns++;
+            continue;
+        }
+        if (res_n > ctx->res_cap) {
+            ctx->res_cap = res_n + res_n / 4 + 1024;
+            st.reruns++;
+            continue;
+        }
+        break;
+    }
+    st.candidates = cand_n;
+    st.results = res_n;
+    st.launches = ctx->launches;
+    float ms[EV_COUNT] = {};
+    for (int i = 1; i < EV_COUNT; ++i) cudaEventElapsedTime(&ms[i], ctx->ev[i - 1], ctx->ev[i]);
+    st.ms_h2d = ms[EV_H2D];
+    st.ms_keys = ms[EV_KEYS];
+    st.ms_sort = ms[EV_SORT];
+    st.ms_ranges = ms[EV_RANGES];
+    st.ms_stage = ms[EV_STAGE];
+    st.ms_tiles = ms[EV_TILES];
+    st.ms_recheck = ms[EV_VERIFY];
+    cudaEventElapsedTime(&st.ms_total, ctx->ev[EV_START], ctx->ev[EV_VERIFY]);
+    ctx->n_results = res_n;
+    ctx->have_join = true;
+    return KGC_OK;
+}
+
+extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t N, int64_t R, int32_t d, int32_t norm,
+                        float eps) {
+    if (!ctx) return KGC_EINVAL;
+    ctx->err.clear();
+    ctx->n_results = -1;
+    ctx->have_join = false;
+    if (N < 0 || R < 0 || d < 1 || d > KGC_MAX_DIM || (norm != 1 && norm != 2) || !(eps >= 0.f) ||
+        !std::isfinite(eps)) {
+        set_err(ctx, "kgc_join: invalid argument (N=%lld R=%lld d=%d norm=%d eps=%g)", (long long)N, (long long)R, d,
+                norm, (double)eps);
+        return KGC_EINVAL;
+    }
+    if (N > INT_MAX / 2 || (double)R * (double)((N + BM - 1) / BM) * BM > 2.0e9) {
+        set_err(ctx, "kgc_join: N*R too large for 32-bit row ids");
+        return KGC_EINVAL;
+    }
+    if (N == 0 || R == 0) {
+        memset(&ctx->st, 0, sizeof ctx->st);
+        ctx->st.N = N;
+        ctx->st.R = R;
+        ctx->st.d = d;
+        ctx->st.norm = norm;
+        ctx->st.eps = eps;
+        ctx->st.rank = ctx->opt.rank;
+        ctx->st.world = ctx->opt.world;
+        ctx->n_results = 0;
+        ctx->have_join = true;
+        return KGC_OK;
+    }
+    if (!E || !Rel) {
+        set_err(ctx, "kgc_join: NULL E or Rel");
+        return KGC_EINVAL;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->device);
+    int rc = join_impl(ctx, E, Rel, N, R, d, norm, eps);
+    if (rc != KGC_OK) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaGetLastError();
+    }
+    cudaSetDevice(prev);
+    return rc;
+}
+
+extern "C" int64_t kgc_results(kgc_ctx* ctx, kgc_triplet* out, int64_t capacity) {
+    if (!ctx || capacity < 0) return KGC_EINVAL;
+    if (ctx->n_results < 0) {
+        set_err(ctx, "kgc_results: no successful join");
+        return KGC_ESTATE;
+    }
+    long long n = std::min<long long>(ctx->n_results, capacity);
+    if (out && n > 0) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(ctx->device);
+        cudaError_t e = cudaMemcpyAsync(out, ctx->res.p, (size_t)n * 16, cudaMemcpyDefault, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        cudaSetDevice(prev);
+        if (e != cudaSuccess) {
+            set_err(ctx, "kgc_results: copy failed: %s", cudaGetErrorString(e));
+            return KGC_ECUDA;
+        }
+        if (!is_device_ptr(out, ctx->device)) ctx->st.d2h_bytes += n * 16;
+    }
+    return ctx->n_results;
+}
+
+extern "C" int kgc_stats(const kgc_ctx* ctx, kgc_stats_t* out) {
+    if (!ctx || !out) return KGC_EINVAL;
+    if (!ctx->have_join) return KGC_ESTATE;
+    *out = ctx->st;
+    return KGC_OK;
+}
+
+extern "C" int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes) {
+    if (!ctx || bytes < 0) return KGC_EINVAL;
+    if (!ctx->have_join || ctx->N == 0 || ctx->R == 0) return KGC_ESTATE;
+    const void* src = nullptr;
+    int64_t n = 0;
+    switch (what) {
+        case KGC_INSPECT_TAIL_KEYS: src = ctx->kt.p; n = ctx->N * 4; break;
+        case KGC_INSPECT_QUERY_KEYS: src = ctx->kq.p; n = ctx->N * ctx->R * 4; break;
+        case KGC_INSPECT_TAIL_PERM: src = ctx->tperm.p; n = ctx->N * 4; break;
+        case KGC_INSPECT_QUERY_PERM: src = ctx->qperm.p; n = ctx->N * ctx->R * 4; break;
+        case KGC_INSPECT_TILE_RANGES: src = ctx->ranges.p; n = ctx->R * (int64_t)ctx->QT * 8; break;
+        case KGC_INSPECT_QUERY_COST: src = ctx->cum.p; n = ctx->R * (int64_t)ctx->QT * 8; break;
+        default: return KGC_EINVAL;
+    }
+    if (out && bytes > 0) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(ctx->device);
+        cudaError_t e = cudaMemcpyAsync(out, src, (size_t)std::min(n, bytes), cudaMemcpyDefault, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        cudaSetDevice(prev);
+        if (e != cudaSuccess) return KGC_ECUDA;
+    }
+    return n;
+}

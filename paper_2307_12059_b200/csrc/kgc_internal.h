@@ -1,0 +1,87 @@
+// kgc_internal.h -- internal (non-ABI) declarations shared by the libkgc
+// translation units: tile geometry, kernel launchers, parameter blocks.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kgc {
+
+constexpr int BM = 128;          // query rows per tile (= TMEM lanes = UMMA M)
+constexpr int BN_TC = 256;       // tail rows per tile, tensor-core engine (UMMA N)
+constexpr int BN_SIMT = 128;     // tail rows per tile, SIMT engines
+constexpr int SORT_IPB = 2048;   // radix-sort items per block (256 threads x 8)
+constexpr int TC_MAX_KPAD = 256; // tensor-core engine supports d <= 256
+
+// Counters block in device memory (zeroed per join).
+struct DevCounters {
+    unsigned long long cand;      // candidates appended by the tile kernels
+    unsigned long long res;       // results appended by the verify kernel
+    unsigned int nonfinite;       // != 0 if E or Rel holds a non-finite value
+    unsigned int pad0;
+    long long total_cost;         // surviving tile pairs, all shards
+    long long my_cost;            // surviving tile pairs, this shard
+    int tq_begin, tq_end;         // query-tile range of this shard [begin, end)
+    long long n_items;            // work items of this shard
+};
+
+struct TileParams {
+    const float* Qp;        // staged query tiles of this shard
+    const float4* qs;       // per staged query row: {Q2, Qn, Qd, thr}
+    const float* Tp;        // staged tail tiles
+    const float* T2;        // per staged tail row ||t||^2 (3e38 for padding rows)
+    const float2* tstile;   // per tail tile {max ||t||, max ||t - tf32(t)||}
+    const int4* items;      // {tq, j0, j1, 0}
+    long long n_items;
+    int Kpad;
+    int tq0;                // first staged query tile
+    int N;                  // tails (valid columns are < N)
+    float theta;
+    float eta;              // tensor-core accumulation error coefficient
+    int2* cand;
+    unsigned long long* cand_count;
+    long long cand_cap;
+};
+
+// ---- launchers (prep.cu) ----
+void launch_tail_keys(const float* E, long long N, int d, int norm, const double* pivot, float* kt,
+                      unsigned int* minmax_seg, unsigned int* nonfinite, cudaStream_t s);
+void launch_query_keys(const float* E, const float* Rel, long long N, long long R, int d, int norm,
+                       const double* pivot, float* kq, unsigned int* minmax, unsigned int* nonfinite,
+                       cudaStream_t s);
+void launch_pivot_mean(const float* E, long long N, int d, double* pivot, cudaStream_t s);
+int  radix_sort_segments(const float* keys, const unsigned int* minmax, long long S, long long L,
+                         unsigned int* k0, unsigned int* v0, unsigned int* k1, unsigned int* v1, int* counts,
+                         int* perm_out, float* skeys_out, void* scan_tmp, size_t scan_tmp_bytes,
+                         cudaStream_t s, int* launches);
+size_t radix_counts_len(long long S, long long L);
+size_t scan_tmp_bytes(size_t n);
+void scan_exclusive_i32(const int* in, int* out, size_t n, void* tmp, cudaStream_t s, int* launches);
+void scan_exclusive_i64(const long long* in, long long* out, size_t n, long long* total, void* tmp,
+                        cudaStream_t s, int* launches);
+void launch_tail_tile_bounds(const float* tskey, long long N, int BN, int TT, float* tmin, float* tmax,
+                             float* cmax, float* cmin, cudaStream_t s, int* launches);
+void launch_query_ranges(const float* qskey, long long N, long long R, int QT, int TT, const float* cmax,
+                         const float* cmin, float theta, int prune, int2* ranges, long long* cost,
+                         cudaStream_t s);
+void launch_shard_items(const int2* ranges, const long long* cost, const long long* cum, long long nq,
+                        int rank, int world, int chunk, DevCounters* ctr, int* nitem, int* item_off,
+                        int4* items, void* tmp, cudaStream_t s, int* launches, int phase);
+void launch_stage_tails(const float* E, const int* tperm, long long N, int d, int Kpad, int BN, int TT,
+                        int tc_layout, float* Tp, float* T2, float2* tstile, cudaStream_t s);
+void launch_stage_queries(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad,
+                          int QT, int tq0, int tq1, int tc_layout, int norm, float theta, float* Qp,
+                          float4* qs, cudaStream_t s);
+
+// ---- tile engines ----
+int  tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);
+void launch_tiles_tc(const TileParams& p, int num_sms, cudaStream_t s);
+void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t s);
+
+// ---- verification (verify.cu) ----
+struct KgcTripletDev { int h, r, t; float dist; };
+void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap,
+                   const int* qperm, const int* tperm, const float* E, const float* Rel, long long N, int QT,
+                   int d, int norm, float theta, KgcTripletDev* out, unsigned long long* res_count,
+                   long long res_cap, int num_sms, cudaStream_t s);
+
+}  // namespace kgc

@@ -1,0 +1,733 @@
+// prep.cu -- the preprocessing steps of the join:
+//   K1  pivot distances of every query q = h + r and every tail t
+//       (Fig. algo1 lines 3-6; connector_1 = h + r)
+//   K2  per-relation sort of the query keys and one sort of the tail keys
+//       (lines 7-10; "the sorting is not heavy"; tails once)
+//   K3  per query tile, the contiguous range of surviving tail tiles
+//       (Lemma 1 PAPER.md:202-210 + Lemma 2 PAPER.md:282-305 at tile granularity)
+//   and the staging of operand tiles in the layouts the tile engines read.
+#include <cfloat>
+#include <climits>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace kgc {
+
+static inline unsigned grid_for(long long n, int threads, long long cap = 148LL * 64) {
+    long long g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+// ============================================================== K1: keys
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_min_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_max_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__global__ void init_minmax_kernel(unsigned int* mm, long long nseg) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nseg; i += (long long)gridDim.x * blockDim.x) {
+        mm[2 * i] = __float_as_uint(FLT_MAX);
+        mm[2 * i + 1] = 0u;
+    }
+}
+
+// d(t, p) = ||t - p||_norm in FP64, stored RN to float.  One warp per tail.
+template <int NORM, bool PIV>
+__global__ void tail_keys_kernel(const float* __restrict__ E, long long N, int d, const double* __restrict__ pivot,
+                                 float* __restrict__ kt, unsigned int* minmax_seg, unsigned int* nonfinite) {
+    const int lane = threadIdx.x & 31;
+    long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    float kmin = FLT_MAX, kmax = 0.f;
+    bool bad = false;
+    for (long long row = warp; row < N; row += nwarps) {
+        double s = 0.0;
+        const float* e = E + row * d;
+        for (int k = lane; k < d; k += 32) {
+            float v = e[k];
+            bad |= !isfinite(v);
+            double x = (double)v - (PIV ? pivot[k] : 0.0);
+            s += NORM == 1 ? fabs(x) : x * x;
+        }
+        s = warp_sum_d(s);
+        float key = __double2float_rn(NORM == 2 ? sqrt(s) : s);
+        if (lane == 0) kt[row] = key;
+        kmin = fminf(kmin, key);
+        kmax = fmaxf(kmax, key);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(nonfinite, 1u);
+    if (lane == 0) {
+        atomicMin(&minmax_seg[0], __float_as_uint(kmin));
+        atomicMax(&minmax_seg[1], __float_as_uint(kmax));
+    }
+}
+
+// d(h + r, p) for every (h, r): a block holds 32 entity rows and 16 relation
+// rows in shared memory; warp w handles relations w and w + 8, lane = entity.
+constexpr int QK_ENT = 32, QK_REL = 16;
+template <int NORM, bool PIV>
+__global__ void __launch_bounds__(256) query_keys_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
+                                                         long long N, long long R, int d,
+                                                         const double* __restrict__ pivot, float* __restrict__ kq,
+                                                         unsigned int* minmax, unsigned int* nonfinite) {
+    extern __shared__ float qk_smem[];
+    const int S = (d & 1) ? d : d + 1;  // odd row stride: conflict-free column reads
+    float* Es = qk_smem;                 // [QK_ENT][S]
+    float* Rs = qk_smem + QK_ENT * S;    // [QK_REL][d]
+    const long long h0 = (long long)blockIdx.x * QK_ENT;
+    const long long r0 = (long long)blockIdx.y * QK_REL;
+    for (int x = threadIdx.x; x < QK_ENT * d; x += blockDim.x) {
+        int i = x / d, k = x % d;
+        Es[i * S + k] = (h0 + i < N) ? E[(h0 + i) * d + k] : 0.f;
+    }
+    bool bad = false;
+    for (int x = threadIdx.x; x < QK_REL * d; x += blockDim.x) {
+        int i = x / d, k = x % d;
+        float v = (r0 + i < R) ? Rel[(r0 + i) * d + k] : 0.f;
+        bad |= !isfinite(v);
+        Rs[i * d + k] = v;
+    }
+    if (blockIdx.x == 0 && __syncthreads_or(bad)) {
+        if (threadIdx.x == 0) atomicOr(nonfinite, 1u);
+    } else {
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long h = h0 + lane;
+    for (int rl = w; rl < QK_REL; rl += 8) {
+        const long long r = r0 + rl;
+        if (r >= R) break;
+        double s = 0.0;
+        const float* es = Es + lane * S;
+        const float* rs = Rs + rl * d;
+        for (int k = 0; k < d; ++k) {
+            double x = (double)es[k] + (double)rs[k];  // connector_1(h, r) = h + r
+            if (PIV) x -= pivot[k];
+            s += NORM == 1 ? fabs(x) : x * x;
+        }
+        float key = __double2float_rn(NORM == 2 ? sqrt(s) : s);
+        bool valid = h < N;
+        if (valid) kq[r * N + h] = key;
+        float mn = warp_min_f(valid ? key : FLT_MAX);
+        float mx = warp_max_f(valid ? key : 0.f);
+        if (lane == 0) {
+            atomicMin(&minmax[2 * r], __float_as_uint(mn));
+            atomicMax(&minmax[2 * r + 1], __float_as_uint(mx));
+        }
+    }
+}
+
+// Column means of E in FP64 (pivot option "mean of tails").
+__global__ void pivot_mean_kernel(const float* __restrict__ E, long long N, int d, double* pivot) {
+    int k = blockIdx.x;
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < N; i += blockDim.x) s += (double)E[i * d + k];
+    __shared__ double red[256];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) pivot[k] = N > 0 ? red[0] / (double)N : 0.0;
+}
+
+void launch_pivot_mean(const float* E, long long N, int d, double* pivot, cudaStream_t s) {
+    pivot_mean_kernel<<<d, 256, 0, s>>>(E, N, d, pivot);
+}
+
+void launch_tail_keys(const float* E, long long N, int d, int norm, const double* pivot, float* kt,
+                      unsigned int* minmax_seg, unsigned int* nonfinite, cudaStream_t s) {
+    init_minmax_kernel<<<1, 32, 0, s>>>(minmax_seg, 1);
+    unsigned g = grid_for(N * 32, 256);
+    if (norm == 1) {
+        if (pivot) tail_keys_kernel<1, true><<<g, 256, 0, s>>>(E, N, d, pivot, kt, minmax_seg, nonfinite);
+        else tail_keys_kernel<1, false><<<g, 256, 0, s>>>(E, N, d, pivot, kt, minmax_seg, nonfinite);
+    } else {
+        if (pivot) tail_keys_kernel<2, true><<<g, 256, 0, s>>>(E, N, d, pivot, kt, minmax_seg, nonfinite);
+        else tail_keys_kernel<2, false><<<g, 256, 0, s>>>(E, N, d, pivot, kt, minmax_seg, nonfinite);
+    }
+}
+
+void launch_query_keys(const float* E, const float* Rel, long long N, long long R, int d, int norm,
+                       const double* pivot, float* kq, unsigned int* minmax, unsigned int* nonfinite,
+                       cudaStream_t s) {
+    init_minmax_kernel<<<grid_for(R, 256), 256, 0, s>>>(minmax, R);
+    const int S = (d & 1) ? d : d + 1;
+    size_t smem = (size_t)(QK_ENT * S + QK_REL * d) * sizeof(float);
+    dim3 grid((unsigned)((N + QK_ENT - 1) / QK_ENT), (unsigned)((R + QK_REL - 1) / QK_REL));
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, 256, smem, s>>>(E, Rel, N, R, d, pivot, kq, minmax, nonfinite);
+    };
+    if (norm == 1) {
+        if (pivot) go(query_keys_kernel<1, true>); else go(query_keys_kernel<1, false>);
+    } else {
+        if (pivot) go(query_keys_kernel<2, true>); else go(query_keys_kernel<2, false>);
+    }
+}
+
+// ============================================================== scans
+constexpr int SCAN_T = 256, SCAN_I = 8, SCAN_B = SCAN_T * SCAN_I;
+
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* total) {
+    __shared__ T warp_tot[SCAN_T / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    T inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T n = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += n;
+    }
+    if (lane == 31) warp_tot[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        T x = lane < SCAN_T / 32 ? warp_tot[lane] : T(0);
+        T xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T n = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += n;
+        }
+        if (lane < SCAN_T / 32) warp_tot[lane] = xi - x;
+        if (lane == SCAN_T / 32 - 1) *total = xi;
+    }
+    __syncthreads();
+    T r = warp_tot[w] + inc - v;
+    __syncthreads();
+    return r;
+}
+
+template <typename T>
+__global__ void scan_reduce_kernel(const T* __restrict__ in, size_t n, T* partial) {
+    size_t base = (size_t)blockIdx.x * SCAN_B + (size_t)threadIdx.x * SCAN_I;
+    T s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_I; ++i)
+        if (base + i < n) s += in[base + i];
+    __shared__ T tot;
+    block_excl_scan<T>(s, &tot);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+template <typename T>
+__global__ void scan_partials_kernel(T* partial, size_t nb, T* grand_total) {
+    __shared__ T carry;
+    __shared__ T tot;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (size_t base = 0; base < nb; base += SCAN_T) {
+        size_t i = base + threadIdx.x;
+        T v = i < nb ? partial[i] : T(0);
+        T ex = block_excl_scan<T>(v, &tot);
+        if (i < nb) partial[i] = ex + carry;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && grand_total) *grand_total = carry;
+}
+
+template <typename T>
+__global__ void scan_final_kernel(const T* __restrict__ in, T* __restrict__ out, size_t n, const T* partial) {
+    size_t base = (size_t)blockIdx.x * SCAN_B + (size_t)threadIdx.x * SCAN_I;
+    T v[SCAN_I];
+    T s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_I; ++i) {
+        v[i] = base + i < n ? in[base + i] : T(0);
+        s += v[i];
+    }
+    __shared__ T tot;
+    T ex = block_excl_scan<T>(s, &tot) + partial[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < SCAN_I; ++i) {
+        if (base + i < n) out[base + i] = ex;
+        ex += v[i];
+    }
+}
+
+size_t scan_tmp_bytes(size_t n) { return ((n + SCAN_B - 1) / SCAN_B + 2) * sizeof(long long) + 256; }
+
+template <typename T>
+static void scan_exclusive(const T* in, T* out, size_t n, T* total, void* tmp, cudaStream_t s, int* launches) {
+    size_t nb = (n + SCAN_B - 1) / SCAN_B;
+    if (nb == 0) nb = 1;
+    T* partial = reinterpret_cast<T*>(tmp);
+    scan_reduce_kernel<T><<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, partial);
+    scan_partials_kernel<T><<<1, SCAN_T, 0, s>>>(partial, nb, total);
+    scan_final_kernel<T><<<(unsigned)nb, SCAN_T, 0, s>>>(in, out, n, partial);
+    if (launches) *launches += 3;
+}
+
+void scan_exclusive_i32(const int* in, int* out, size_t n, void* tmp, cudaStream_t s, int* launches) {
+    scan_exclusive<int>(in, out, n, nullptr, tmp, s, launches);
+}
+void scan_exclusive_i64(const long long* in, long long* out, size_t n, long long* total, void* tmp,
+                        cudaStream_t s, int* launches) {
+    scan_exclusive<long long>(in, out, n, total, tmp, s, launches);
+}
+
+// ============================================================== K2: sort
+// Segmented, stable LSD radix sort of S segments of L keys on a 16-bit
+// quantisation of the float key inside its segment's [min, max] (two 8-bit
+// passes).  Ties keep ascending original index, so the order is
+// deterministic (identical on every rank).  Order only affects how tight the
+// tile bounds are, never correctness: K3 uses the actual key min/max of every
+// tile.
+__global__ void radix_prep_kernel(const float* __restrict__ keys, const unsigned int* __restrict__ minmax,
+                                  long long S, long long L, unsigned int* k0, unsigned int* v0) {
+    long long n = S * L;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long s = idx / L, i = idx - s * L;
+        float kmin = __uint_as_float(minmax[2 * s]), kmax = __uint_as_float(minmax[2 * s + 1]);
+        float range = kmax - kmin;
+        unsigned q = 0;
+        if (range > 0.f) {
+            float x = (keys[idx] - kmin) * (65536.0f / range);
+            x = fminf(fmaxf(x, 0.f), 65535.f);
+            q = (unsigned)x;
+        }
+        k0[idx] = q;
+        v0[idx] = (unsigned)i;
+    }
+}
+
+__global__ void radix_hist_kernel(const unsigned int* __restrict__ kin, long long L, int B, int shift, int* counts) {
+    __shared__ int h[256];
+    const long long s = blockIdx.y;
+    const int b = blockIdx.x;
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    long long base = (long long)b * SORT_IPB;
+#pragma unroll
+    for (int k = 0; k < SORT_IPB / 256; ++k) {
+        long long i = base + k * 256 + threadIdx.x;
+        if (i < L) atomicAdd(&h[(kin[s * L + i] >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    counts[(s * 256 + threadIdx.x) * B + b] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(256) radix_scatter_kernel(const unsigned int* __restrict__ kin,
+                                                            const unsigned int* __restrict__ vin,
+                                                            unsigned int* __restrict__ kout,
+                                                            unsigned int* __restrict__ vout,
+                                                            const int* __restrict__ offs, long long L, int B,
+                                                            int shift) {
+    __shared__ int run[256];
+    __shared__ int wcnt[8][257];
+    const long long s = blockIdx.y;
+    const int b = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    run[threadIdx.x] = 0;
+    const long long base = (long long)b * SORT_IPB;
+    const int boff = offs[(s * 256 + threadIdx.x) * B + b];
+    __shared__ int blk_off[256];
+    blk_off[threadIdx.x] = boff;
+    for (int round = 0; round < SORT_IPB / 256; ++round) {
+        long long i = base + round * 256 + threadIdx.x;
+        bool valid = i < L;
+        unsigned key = valid ? kin[s * L + i] : 0u;
+        int dg = valid ? (int)((key >> shift) & 255u) : 256;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) wcnt[ww][threadIdx.x] = 0;
+        __syncthreads();
+        unsigned peers = __match_any_sync(0xffffffffu, dg);
+        int lrank = __popc(peers & lanemask_lt());
+        if (valid && lrank == 0) wcnt[w][dg] = __popc(peers);
+        __syncthreads();
+        {
+            int sum = run[threadIdx.x];
+#pragma unroll
+            for (int ww = 0; ww < 8; ++ww) {
+                int c = wcnt[ww][threadIdx.x];
+                wcnt[ww][threadIdx.x] = sum;
+                sum += c;
+            }
+            run[threadIdx.x] = sum;
+        }
+        __syncthreads();
+        if (valid) {
+            long long dst = (long long)blk_off[dg] + wcnt[w][dg] + lrank;
+            kout[dst] = key;
+            vout[dst] = vin[s * L + i];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void radix_final_kernel(const unsigned int* __restrict__ v, const float* __restrict__ keys, long long S,
+                                   long long L, int* perm, float* skeys) {
+    long long n = S * L;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long s = idx / L;
+        unsigned src = v[idx];
+        perm[idx] = (int)src;
+        skeys[idx] = keys[s * L + src];
+    }
+}
+
+size_t radix_counts_len(long long S, long long L) {
+    long long B = (L + SORT_IPB - 1) / SORT_IPB;
+    return (size_t)(S * 256 * (B > 0 ? B : 1));
+}
+
+int radix_sort_segments(const float* keys, const unsigned int* minmax, long long S, long long L, unsigned int* k0,
+                        unsigned int* v0, unsigned int* k1, unsigned int* v1, int* counts, int* perm_out,
+                        float* skeys_out, void* scan_tmp, size_t /*scan_tmp_bytes*/, cudaStream_t s,
+                        int* launches) {
+    if (S <= 0 || L <= 0) return 0;
+    const int B = (int)((L + SORT_IPB - 1) / SORT_IPB);
+    const size_t nc = (size_t)S * 256 * B;
+    radix_prep_kernel<<<grid_for(S * L, 256), 256, 0, s>>>(keys, minmax, S, L, k0, v0);
+    dim3 g((unsigned)B, (unsigned)S);
+    for (int pass = 0; pass < 2; ++pass) {
+        const unsigned int* ki = pass == 0 ? k0 : k1;
+        const unsigned int* vi = pass == 0 ? v0 : v1;
+        unsigned int* ko = pass == 0 ? k1 : k0;
+        unsigned int* vo = pass == 0 ? v1 : v0;
+        radix_hist_kernel<<<g, 256, 0, s>>>(ki, L, B, pass * 8, counts);
+        scan_exclusive_i32(counts, counts, nc, scan_tmp, s, launches);
+        radix_scatter_kernel<<<g, 256, 0, s>>>(ki, vi, ko, vo, counts, L, B, pass * 8);
+    }
+    radix_final_kernel<<<grid_for(S * L, 256), 256, 0, s>>>(v0, keys, S, L, perm_out, skeys_out);
+    if (launches) *launches += 6;
+    return 0;
+}
+
+// ============================================================== K3: ranges
+// Per tail tile j: [tmin_j, tmax_j] of its sorted keys; cmax = running max of
+// tmax, cmin = running min of tmin from the right.  Both are monotone, so the
+// tiles that can hold a tail within theta of a query-tile key interval form a
+// contiguous range found by binary search (Lemma 2's s_i <= s_{i+1},
+// e_i <= e_{i+1}, at tile granularity).
+__global__ void tail_tile_minmax_kernel(const float* __restrict__ tskey, long long N, int BN, int TT, float* tmin,
+                                        float* tmax) {
+    const int lane = threadIdx.x & 31;
+    long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long j = warp; j < TT; j += nwarps) {
+        float mn = FLT_MAX, mx = -FLT_MAX;
+        long long b = j * BN, e = min((long long)N, b + BN);
+        for (long long i = b + lane; i < e; i += 32) {
+            float k = tskey[i];
+            mn = fminf(mn, k);
+            mx = fmaxf(mx, k);
+        }
+        mn = warp_min_f(mn);
+        mx = warp_max_f(mx);
+        if (lane == 0) {
+            tmin[j] = mn;
+            tmax[j] = mx;
+        }
+    }
+}
+
+__global__ void tail_tile_cum_kernel(const float* tmin, const float* tmax, int TT, float* cmax, float* cmin) {
+    if (threadIdx.x == 0) {
+        float m = -FLT_MAX;
+        for (int j = 0; j < TT; ++j) {
+            m = fmaxf(m, tmax[j]);
+            cmax[j] = m;
+        }
+    } else if (threadIdx.x == 32) {
+        float m = FLT_MAX;
+        for (int j = TT - 1; j >= 0; --j) {
+            m = fminf(m, tmin[j]);
+            cmin[j] = m;
+        }
+    }
+}
+
+void launch_tail_tile_bounds(const float* tskey, long long N, int BN, int TT, float* tmin, float* tmax, float* cmax,
+                             float* cmin, cudaStream_t s, int* launches) {
+    tail_tile_minmax_kernel<<<grid_for((long long)TT * 32, 256), 256, 0, s>>>(tskey, N, BN, TT, tmin, tmax);
+    tail_tile_cum_kernel<<<1, 64, 0, s>>>(tmin, tmax, TT, cmax, cmin);
+    if (launches) *launches += 2;
+}
+
+// Pruning margin: keys are FP64 norms rounded to float (relative error
+// <= 2^-24); theta is widened by 2^-14 relative and the key bounds by 2^-20
+// relative so that no pair with dist3 <= theta is ever pruned (DESIGN.md
+// "Floating-point rigor of pruning").
+__global__ void query_ranges_kernel(const float* __restrict__ qskey, long long N, long long R, int QT, int TT,
+                                    const float* __restrict__ cmax, const float* __restrict__ cmin, float theta,
+                                    int prune, int2* ranges, long long* cost) {
+    const int lane = threadIdx.x & 31;
+    long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long nq = R * (long long)QT;
+    for (long long tq = warp; tq < nq; tq += nwarps) {
+        long long r = tq / QT, qt = tq - r * QT;
+        long long b = qt * BM, e = min(N, b + BM);
+        float mn = FLT_MAX, mx = -FLT_MAX;
+        for (long long i = b + lane; i < e; i += 32) {
+            float k = qskey[r * N + i];
+            mn = fminf(mn, k);
+            mx = fmaxf(mx, k);
+        }
+        mn = warp_min_f(mn);
+        mx = warp_max_f(mx);
+        if (lane == 0) {
+            int sb = 0, eb = TT - 1;
+            if (prune) {
+                const float th = theta * (1.0f + 6.103515625e-05f);                // theta (1 + 2^-14)
+                const float lo = mn - th - fabsf(mn) * 9.5367431640625e-07f;      // - |key| 2^-20
+                const float hi = mx + th + fabsf(mx) * 9.5367431640625e-07f;
+                int a = 0, z = TT;  // first j with cmax[j] >= lo
+                while (a < z) {
+                    int m = (a + z) >> 1;
+                    if (cmax[m] >= lo) z = m; else a = m + 1;
+                }
+                sb = a;
+                a = 0; z = TT;      // first j with cmin[j] > hi
+                while (a < z) {
+                    int m = (a + z) >> 1;
+                    if (cmin[m] > hi) z = m; else a = m + 1;
+                }
+                eb = a - 1;
+            }
+            ranges[tq] = make_int2(sb, eb);
+            cost[tq] = eb >= sb ? (long long)(eb - sb + 1) : 0LL;
+        }
+    }
+}
+
+void launch_query_ranges(const float* qskey, long long N, long long R, int QT, int TT, const float* cmax,
+                         const float* cmin, float theta, int prune, int2* ranges, long long* cost, cudaStream_t s) {
+    query_ranges_kernel<<<grid_for(R * QT * 32, 256), 256, 0, s>>>(qskey, N, R, QT, TT, cmax, cmin, theta, prune,
+                                                                    ranges, cost);
+}
+
+// Shard assignment: query tile q belongs to rank min(W-1, W*cum[q]/total)
+// (cum = exclusive prefix of surviving-tile counts) -- identical to the host
+// function kgc_shard_range().  Work items of at most `chunk` tail tiles.
+__global__ void shard_count_kernel(const long long* __restrict__ cost, const long long* __restrict__ cum,
+                                   long long nq, int rank, int world, int chunk, DevCounters* ctr, int* nitem) {
+    const long long total = ctr->total_cost;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq; q += (long long)gridDim.x * blockDim.x) {
+        int owner = 0;
+        if (total > 0) {
+            long long o = (long long)world * cum[q] / total;
+            owner = (int)(o < world - 1 ? o : world - 1);
+        }
+        int n = 0;
+        if (owner == rank) {
+            atomicMin(&ctr->tq_begin, (int)q);
+            atomicMax(&ctr->tq_end, (int)q + 1);
+            long long c = cost[q];
+            atomicAdd((unsigned long long*)&ctr->my_cost, (unsigned long long)c);
+            n = (int)((c + chunk - 1) / chunk);
+        }
+        nitem[q] = n;
+    }
+}
+
+__global__ void shard_emit_kernel(const int2* __restrict__ ranges, const int* __restrict__ nitem,
+                                  const int* __restrict__ off, long long nq, int chunk, DevCounters* ctr,
+                                  int4* items) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq; q += (long long)gridDim.x * blockDim.x) {
+        int n = nitem[q];
+        int o = off[q];
+        if (q == nq - 1) ctr->n_items = (long long)o + n;
+        int2 rg = ranges[q];
+        for (int k = 0; k < n; ++k) {
+            int j0 = rg.x + k * chunk;
+            int j1 = min(rg.y, j0 + chunk - 1);
+            items[o + k] = make_int4((int)q, j0, j1, 0);
+        }
+    }
+}
+
+void launch_shard_items(const int2* ranges, const long long* cost, const long long* cum, long long nq, int rank,
+                        int world, int chunk, DevCounters* ctr, int* nitem, int* item_off, int4* items, void* tmp,
+                        cudaStream_t s, int* launches, int phase) {
+    if (phase == 0) {
+        shard_count_kernel<<<grid_for(nq, 256), 256, 0, s>>>(cost, cum, nq, rank, world, chunk, ctr, nitem);
+        scan_exclusive_i32(nitem, item_off, (size_t)nq, tmp, s, launches);
+        if (launches) *launches += 1;
+    } else {
+        shard_emit_kernel<<<grid_for(nq, 256), 256, 0, s>>>(ranges, nitem, item_off, nq, chunk, ctr, items);
+        if (launches) *launches += 1;
+    }
+}
+
+// ============================================================== staging
+// Operand tiles in HBM in exactly the shared-memory layout the engines read,
+// so one bulk TMA copy moves a whole (chunk of a) tile:
+//   tensor-core layout (UMMA K-major, no swizzle): element (i, k) of a ROWS-row
+//     tile at float offset ((k/4) * (ROWS/8) + i/8) * 32 + (i%8) * 4 + k%4;
+//   SIMT layout: element (i, k) at k * ROWS + i.
+// Zero padding for rows >= N and k >= d.  Query values q = fl32(h + r).
+// Row scalars (FP64 sums of the fp32 values): ||v||^2, ||v||, ||v - tf32(v)||
+// (truncation residual, which bounds the round-to-nearest residual too), ||v||_1.
+__device__ __forceinline__ float tf32_trunc(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
+
+struct RowStat {
+    double s2, sd2, s1;
+};
+
+template <bool TC>
+__device__ __forceinline__ size_t stage_off(int i, int k, int ROWS) {
+    if (TC) return ((size_t)(k >> 2) * (ROWS >> 3) + (i >> 3)) * 32 + (i & 7) * 4 + (k & 3);
+    return (size_t)k * ROWS + i;
+}
+
+// grid: one block per tile; 256 threads.  `rel` == nullptr for tails.
+template <bool TC>
+__global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
+                                                    const int* __restrict__ perm, long long N, int d, int Kpad,
+                                                    int ROWS, int QT, int tile0, int norm, float theta,
+                                                    float* __restrict__ out, float4* __restrict__ qs,
+                                                    float* __restrict__ T2, float2* __restrict__ tstile) {
+    const int tile = tile0 + blockIdx.x;
+    long long r = 0, t_in_rel = tile;
+    if (Rel) {
+        r = tile / QT;
+        t_in_rel = tile - r * QT;
+    }
+    const int* pr = perm + (Rel ? r * N : 0);
+    const float* rel = Rel ? Rel + r * d : nullptr;
+    float* dst = out + (size_t)blockIdx.x * ROWS * Kpad;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __shared__ float sTn[8], sTd[8];
+    float tn_max = 0.f, td_max = 0.f;
+
+    // rows handled by warp w; TC: lanes over k (4 consecutive k per lane),
+    // SIMT: lanes over rows.
+    if (TC) {
+        for (int i = w; i < ROWS; i += 8) {
+            long long p = t_in_rel * ROWS + i;
+            bool valid = p < N;
+            long long h = valid ? pr[p] : 0;
+            RowStat st{0, 0, 0};
+            for (int kq = lane; kq < (Kpad >> 2); kq += 32) {
+                float4 v;
+                float* vv = reinterpret_cast<float*>(&v);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    int k = kq * 4 + c;
+                    float x = 0.f;
+                    if (valid && k < d) x = rel ? __fadd_rn(E[h * d + k], rel[k]) : E[h * d + k];
+                    vv[c] = x;
+                    double xd = x, rd = (double)(x - tf32_trunc(x));
+                    st.s2 += xd * xd;
+                    st.sd2 += rd * rd;
+                    st.s1 += fabs(xd);
+                }
+                *reinterpret_cast<float4*>(dst + stage_off<true>(i, kq * 4, ROWS)) = v;
+            }
+            st.s2 = warp_sum_d(st.s2);
+            st.sd2 = warp_sum_d(st.sd2);
+            st.s1 = warp_sum_d(st.s1);
+            if (lane == 0) {
+                float Qn = f2up(sqrt(st.s2)), Qd = f2up(sqrt(st.sd2));
+                if (rel) {
+                    float thr;
+                    if (norm == 1) {
+                        thr = f2up(((double)theta + st.s1 * 2.384185791015625e-07) * (1.0 + (d + 2) * 1.1920928955078125e-07) *
+                                   (1.0 + 9.5367431640625e-07));
+                    } else {
+                        double thf = (double)theta * (1.0 + 2.44140625e-04) + 2.384185791015625e-07 * sqrt(st.s2);
+                        thr = f2up(thf * thf * (1.0 + (d + 3) * 1.1920928955078125e-07) * (1.0 + 9.5367431640625e-07));
+                    }
+                    qs[(size_t)blockIdx.x * ROWS + i] =
+                        valid ? make_float4(__double2float_rn(st.s2), Qn, Qd, thr) : make_float4(3e38f, 0.f, 0.f, -1.f);
+                } else {
+                    T2[(size_t)tile * ROWS + i] = valid ? __double2float_rn(st.s2) : 3e38f;
+                    if (valid) {
+                        tn_max = fmaxf(tn_max, Qn);
+                        td_max = fmaxf(td_max, Qd);
+                    }
+                }
+            }
+        }
+    } else {
+        for (int g = w; g < ROWS / 32; g += 8) {
+            int i = g * 32 + lane;
+            long long p = t_in_rel * ROWS + i;
+            bool valid = p < N;
+            long long h = valid ? pr[p] : 0;
+            RowStat st{0, 0, 0};
+            for (int k = 0; k < Kpad; ++k) {
+                float x = 0.f;
+                if (valid && k < d) x = rel ? __fadd_rn(E[h * d + k], rel[k]) : E[h * d + k];
+                dst[stage_off<false>(i, k, ROWS)] = x;
+                double xd = x;
+                st.s2 += xd * xd;
+                st.s1 += fabs(xd);
+            }
+            if (rel) {
+                float thr;
+                if (norm == 1) {
+                    thr = f2up(((double)theta + st.s1 * 2.384185791015625e-07) * (1.0 + (d + 2) * 1.1920928955078125e-07) *
+                               (1.0 + 9.5367431640625e-07));
+                } else {
+                    double thf = (double)theta * (1.0 + 2.44140625e-04) + 2.384185791015625e-07 * sqrt(st.s2);
+                    thr = f2up(thf * thf * (1.0 + (d + 3) * 1.1920928955078125e-07) * (1.0 + 9.5367431640625e-07));
+                }
+                qs[(size_t)blockIdx.x * ROWS + i] =
+                    valid ? make_float4(__double2float_rn(st.s2), f2up(sqrt(st.s2)), 0.f, thr)
+                          : make_float4(3e38f, 0.f, 0.f, -1.f);
+            }
+        }
+    }
+    if (!Rel && TC) {
+        tn_max = warp_max_f(tn_max);
+        td_max = warp_max_f(td_max);
+        if (lane == 0) {
+            sTn[w] = tn_max;
+            sTd[w] = td_max;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float a = 0.f, b = 0.f;
+            for (int x = 0; x < 8; ++x) {
+                a = fmaxf(a, sTn[x]);
+                b = fmaxf(b, sTd[x]);
+            }
+            tstile[tile] = make_float2(a, b);
+        }
+    }
+}
+
+void launch_stage_tails(const float* E, const int* tperm, long long N, int d, int Kpad, int BN, int TT, int tc_layout,
+                        float* Tp, float* T2, float2* tstile, cudaStream_t s) {
+    if (TT <= 0) return;
+    if (tc_layout)
+        stage_kernel<true><<<TT, 256, 0, s>>>(E, nullptr, tperm, N, d, Kpad, BN, 1, 0, 2, 0.f, Tp, nullptr, T2, tstile);
+    else
+        stage_kernel<false><<<TT, 256, 0, s>>>(E, nullptr, tperm, N, d, Kpad, BN, 1, 0, 2, 0.f, Tp, nullptr, T2, tstile);
+}
+
+void launch_stage_queries(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad, int QT,
+                          int tq0, int tq1, int tc_layout, int norm, float theta, float* Qp, float4* qs,
+                          cudaStream_t s) {
+    if (tq1 <= tq0) return;
+    if (tc_layout)
+        stage_kernel<true><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, BM, QT, tq0, norm, theta, Qp, qs,
+                                                     nullptr, nullptr);
+    else
+        stage_kernel<false><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, BM, QT, tq0, norm, theta, Qp, qs,
+                                                      nullptr, nullptr);
+}
+
+}  // namespace kgc

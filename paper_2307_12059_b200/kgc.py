@@ -1,0 +1,266 @@
+"""Thin ctypes binding of libkgc (include/kgc.h) -- argument marshalling only.
+
+Every step of the join runs in the CUDA kernels of libkgc.so; this module
+only converts Python / numpy / torch arguments into pointers and sizes.
+There is no fallback: if libkgc.so is missing or cannot be loaded, importing
+the library raises.
+
+Same names as the C ABI: kgc_default_options, kgc_create, kgc_join,
+kgc_results, kgc_stats, kgc_last_error, kgc_set_stream, kgc_destroy,
+kgc_inspect, kgc_shard_range, kgc_abi_version.  ``Join`` is a small
+convenience wrapper around one context.
+"""
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libkgc.so"
+
+KGC_OK, KGC_EINVAL, KGC_EDATA, KGC_ENOMEM, KGC_ECUDA, KGC_ENODEV, KGC_ESTATE = 0, -1, -2, -3, -4, -5, -6
+STATUS_NAMES = {0: "KGC_OK", -1: "KGC_EINVAL", -2: "KGC_EDATA", -3: "KGC_ENOMEM", -4: "KGC_ECUDA",
+                -5: "KGC_ENODEV", -6: "KGC_ESTATE"}
+KGC_MAX_DIM = 1024
+INSPECT = {"tail_keys": 1, "query_keys": 2, "tail_perm": 3, "query_perm": 4, "tile_ranges": 5, "query_cost": 6}
+
+TRIPLET_DTYPE = np.dtype([("h", np.int32), ("r", np.int32), ("t", np.int32), ("dist", np.float32)])
+
+
+class kgc_options(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("prune", ctypes.c_int32), ("pivot", ctypes.c_int32), ("l2_engine", ctypes.c_int32),
+                ("chunk_tiles", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("result_capacity", ctypes.c_int64), ("stream", ctypes.c_void_p)]
+
+
+class kgc_stats_t(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("R", ctypes.c_int64), ("d", ctypes.c_int32), ("norm", ctypes.c_int32),
+                ("eps", ctypes.c_float), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("triplets", ctypes.c_double), ("query_tile_rows", ctypes.c_int64),
+                ("tail_tile_rows", ctypes.c_int64), ("query_tiles", ctypes.c_int64), ("tail_tiles", ctypes.c_int64),
+                ("tile_pairs_total", ctypes.c_int64), ("tile_pairs_surviving", ctypes.c_int64),
+                ("tile_pairs_mine", ctypes.c_int64), ("work_items_mine", ctypes.c_int64),
+                ("candidates", ctypes.c_int64), ("results", ctypes.c_int64), ("h2d_bytes", ctypes.c_int64),
+                ("d2h_bytes", ctypes.c_int64), ("launches", ctypes.c_int32), ("reruns", ctypes.c_int32),
+                ("ms_total", ctypes.c_float), ("ms_h2d", ctypes.c_float), ("ms_keys", ctypes.c_float),
+                ("ms_sort", ctypes.c_float), ("ms_ranges", ctypes.c_float), ("ms_stage", ctypes.c_float),
+                ("ms_tiles", ctypes.c_float), ("ms_recheck", ctypes.c_float)]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+EXPORTS = ["kgc_abi_version", "kgc_default_options", "kgc_create", "kgc_join", "kgc_results", "kgc_stats",
+           "kgc_last_error", "kgc_set_stream", "kgc_destroy", "kgc_inspect", "kgc_shard_range"]
+
+_lib = None
+
+
+def load_library(path: str | Path | None = None):
+    """Load libkgc.so (raises OSError if it is missing: no fallback path exists)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise OSError(f"libkgc.so not found at {p}; build it with `python -m paper_2307_12059_b200._build`")
+    L = ctypes.CDLL(str(p))
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    L.kgc_abi_version.restype = ctypes.c_int
+    L.kgc_default_options.argtypes = [ctypes.POINTER(kgc_options)]
+    L.kgc_default_options.restype = None
+    L.kgc_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(kgc_options)]
+    L.kgc_create.restype = ctypes.c_int
+    L.kgc_join.argtypes = [vp, vp, vp, i64, i64, i32, i32, ctypes.c_float]
+    L.kgc_join.restype = ctypes.c_int
+    L.kgc_results.argtypes = [vp, vp, i64]
+    L.kgc_results.restype = i64
+    L.kgc_stats.argtypes = [vp, ctypes.POINTER(kgc_stats_t)]
+    L.kgc_stats.restype = ctypes.c_int
+    L.kgc_last_error.argtypes = [vp]
+    L.kgc_last_error.restype = ctypes.c_char_p
+    L.kgc_set_stream.argtypes = [vp, vp]
+    L.kgc_set_stream.restype = ctypes.c_int
+    L.kgc_destroy.argtypes = [vp]
+    L.kgc_destroy.restype = None
+    L.kgc_inspect.argtypes = [vp, i32, vp, i64]
+    L.kgc_inspect.restype = i64
+    L.kgc_shard_range.argtypes = [vp, i64, i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.kgc_shard_range.restype = i64
+    if path is None:
+        _lib = L
+    return L
+
+
+class KgcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+# ----------------------------------------------------------- raw C names
+
+def kgc_abi_version() -> int:
+    return load_library().kgc_abi_version()
+
+
+def kgc_default_options(**overrides) -> kgc_options:
+    o = kgc_options()
+    load_library().kgc_default_options(ctypes.byref(o))
+    for k, v in overrides.items():
+        setattr(o, k, v)
+    return o
+
+
+def kgc_last_error(ctx=None) -> str:
+    s = load_library().kgc_last_error(ctx)
+    return s.decode() if s else ""
+
+
+def kgc_create(options: kgc_options | None = None, **overrides):
+    o = options if options is not None else kgc_default_options(**overrides)
+    ctx = ctypes.c_void_p()
+    rc = load_library().kgc_create(ctypes.byref(ctx), ctypes.byref(o))
+    if rc != KGC_OK:
+        raise KgcError(rc, kgc_last_error(None))
+    return ctx
+
+
+def _ptr(x):
+    """Pointer of a numpy array or torch tensor (host or device), contiguous float32/int."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):          # torch tensor
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return ctypes.c_void_p(x.data_ptr())
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return ctypes.c_void_p(x.ctypes.data)
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def _check_f32(x, name):
+    dt = getattr(x, "dtype", None)
+    if dt is None:
+        return
+    if str(dt) not in ("float32", "torch.float32"):
+        raise TypeError(f"{name} must be float32, got {dt}")
+
+
+def kgc_join(ctx, E, Rel, N: int, R: int, d: int, norm: int, eps: float) -> None:
+    _check_f32(E, "E")
+    _check_f32(Rel, "Rel")
+    rc = load_library().kgc_join(ctx, _ptr(E), _ptr(Rel), int(N), int(R), int(d), int(norm), float(eps))
+    if rc != KGC_OK:
+        raise KgcError(rc, kgc_last_error(ctx))
+
+
+def kgc_results(ctx, out=None, capacity: int | None = None) -> int:
+    cap = 0 if out is None else (capacity if capacity is not None else
+                                 (out.shape[0] if hasattr(out, "shape") else 0))
+    n = load_library().kgc_results(ctx, _ptr(out), int(cap))
+    if n < 0:
+        raise KgcError(int(n), kgc_last_error(ctx))
+    return int(n)
+
+
+def kgc_stats(ctx) -> dict:
+    st = kgc_stats_t()
+    rc = load_library().kgc_stats(ctx, ctypes.byref(st))
+    if rc != KGC_OK:
+        raise KgcError(rc, kgc_last_error(ctx))
+    return st.as_dict()
+
+
+def kgc_set_stream(ctx, stream) -> None:
+    ptr = stream if isinstance(stream, int) or stream is None else getattr(stream, "cuda_stream", stream)
+    rc = load_library().kgc_set_stream(ctx, ctypes.c_void_p(ptr) if ptr else None)
+    if rc != KGC_OK:
+        raise KgcError(rc, kgc_last_error(ctx))
+
+
+def kgc_destroy(ctx) -> None:
+    if ctx:
+        load_library().kgc_destroy(ctx)
+
+
+def kgc_inspect(ctx, what: str) -> np.ndarray:
+    code = INSPECT[what]
+    n = load_library().kgc_inspect(ctx, code, None, 0)
+    if n < 0:
+        raise KgcError(int(n), kgc_last_error(ctx))
+    dtype = {"tail_keys": np.float32, "query_keys": np.float32, "tail_perm": np.int32, "query_perm": np.int32,
+             "tile_ranges": np.int32, "query_cost": np.int64}[what]
+    out = np.empty(n // np.dtype(dtype).itemsize, dtype=dtype)
+    rc = load_library().kgc_inspect(ctx, code, out.ctypes.data, n)
+    if rc < 0:
+        raise KgcError(int(rc), kgc_last_error(ctx))
+    return out
+
+
+def kgc_shard_range(cum, total: int, rank: int, world: int):
+    """Pure host function: the query-tile shard [begin, end) of `rank` and its cost."""
+    cum = np.ascontiguousarray(cum, dtype=np.int64)
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    cost = load_library().kgc_shard_range(cum.ctypes.data, cum.shape[0], int(total), int(rank), int(world),
+                                          ctypes.byref(b), ctypes.byref(e))
+    if cost < 0:
+        raise KgcError(int(cost), "kgc_shard_range: invalid argument")
+    return int(b.value), int(e.value), int(cost)
+
+
+# ----------------------------------------------------------- convenience
+
+class Join:
+    """One libkgc context.  ``run(E, Rel, norm, eps)`` joins and returns the
+    result count; ``results()`` returns a numpy structured array (h, r, t, dist)."""
+
+    def __init__(self, **options):
+        stream = options.pop("stream", None)
+        self.ctx = kgc_create(**options)
+        if stream is not None:
+            kgc_set_stream(self.ctx, stream)
+
+    def run(self, E, Rel, norm: int, eps: float) -> int:
+        N, d = (int(E.shape[0]), int(E.shape[1])) if E is not None and len(E.shape) == 2 else (0, 1)
+        R = int(Rel.shape[0]) if Rel is not None else 0
+        if Rel is not None and len(Rel.shape) == 2 and R and int(Rel.shape[1]) != d:
+            raise ValueError("E and Rel dimensions differ")
+        kgc_join(self.ctx, E, Rel, N, R, d, norm, eps)
+        return kgc_results(self.ctx)
+
+    def results(self, out=None):
+        n = kgc_results(self.ctx)
+        if out is None:
+            out = np.empty(n, dtype=TRIPLET_DTYPE)
+        kgc_results(self.ctx, out, n)
+        return out
+
+    def stats(self) -> dict:
+        return kgc_stats(self.ctx)
+
+    def inspect(self, what: str) -> np.ndarray:
+        return kgc_inspect(self.ctx, what)
+
+    def close(self):
+        if self.ctx:
+            kgc_destroy(self.ctx)
+            self.ctx = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
