@@ -232,36 +232,27 @@ def group_candidates(s, e, max_group_size: int):
 # --------------------------------------------------------------------------
 
 def calibrate_theta(E, Rel, norm: int, hit_rate: float, rows, rel_norms_guard: bool = True,
-                    min_gap_rel: float = 4e-4, threads: int = 0):
-    """theta at the requested hit rate over the sampled rows (FP64 dist3), moved
-    to the middle of the nearest gap at least ``min_gap_rel * theta`` wide that
-    holds no sampled distance and no self-edge distance ||r_j||_p (reading R14),
-    then rounded to float32.  Returns (theta_f32, info)."""
+                    tie_guard_rel: float = 2e-4, threads: int = 0):
+    """theta at the requested hit rate over the sampled rows (FP64 dist3): the
+    midpoint of the k-th and (k+1)-th smallest sampled distances, k = round(hit
+    rate x sample size), moved below any self-edge distance ||r_j||_p closer
+    than ``tie_guard_rel * theta`` (N-fold ties, reading R14), then rounded to
+    float32.  Returns (theta_f32, info)."""
     D = dist_rows(E, Rel, norm, rows, threads).ravel()
-    k = max(1, int(round(hit_rate * D.size)))
+    k = min(max(1, int(round(hit_rate * D.size))), D.size - 1) if D.size > 1 else 1
     D.sort()
-    q = D[k - 1]
-    guard = []
+    theta = 0.5 * (D[k - 1] + D[k]) if D.size > 1 else float(D[0])
     if rel_norms_guard:
         Rel64 = np.asarray(Rel, np.float64)
-        guard = list(np.abs(Rel64).sum(1) if norm == 1 else np.sqrt((Rel64 ** 2).sum(1)))
-    pts = np.sort(np.concatenate([D[max(0, k - 5000): k + 5000], np.asarray(guard, np.float64)]))
-    best = None
-    # candidate gaps between consecutive points near the quantile
-    lo = np.searchsorted(pts, q * 0.9)
-    hi = np.searchsorted(pts, q * 1.1)
-    for a in range(max(0, lo), min(len(pts) - 1, hi + 1)):
-        g0, g1 = pts[a], pts[a + 1]
-        mid = 0.5 * (g0 + g1)
-        if g1 - g0 >= 2 * min_gap_rel * mid:
-            cand = (abs(mid - q), mid)
-            if best is None or cand < best:
-                best = cand
-    if best is None:
-        raise RuntimeError("no gap found near the requested quantile")
-    theta = float(np.float32(best[1]))
+        guard = np.abs(Rel64).sum(1) if norm == 1 else np.sqrt((Rel64 ** 2).sum(1))
+        for _ in range(100):
+            close = np.abs(guard - theta) <= tie_guard_rel * theta
+            if not close.any():
+                break
+            theta = float(guard[close].min()) * (1.0 - 2.0 * tie_guard_rel)
+    theta = float(np.float32(theta))
     n_hits = int(np.searchsorted(D, theta, side="right"))
-    return theta, {"quantile": float(q), "sample_hits": n_hits, "sample_pairs": int(D.size),
+    return theta, {"k": k, "sample_hits": n_hits, "sample_pairs": int(D.size),
                    "hit_rate_sample": n_hits / D.size}
 
 
