@@ -100,14 +100,18 @@ __global__ void __launch_bounds__(256, 2) tiles_simt_kernel(TileParams p) {
 #pragma unroll
                     for (int b = 0; b < 8; ++b) hit |= (unsigned long long)(acc[a][b] <= thr[a]) << (a * 8 + b);
                 if (__any_sync(0xffffffffu, hit != 0)) {
-#pragma unroll 1
-                    for (int ab = 0; ab < 64; ++ab) {
-                        const int a = ab >> 3, b = ab & 7;
-                        const int col = j * BN_SIMT + tx * 8 + b;
-                        const bool pr = ((hit >> ab) & 1ull) && col < p.N;
-                        const unsigned long long slot = warp_append(pr, p.cand_count);
-                        if (pr && slot < (unsigned long long)p.cand_cap)
-                            p.cand[slot] = make_int2(w.x * BM + ty * 8 + a, col);
+                    // columns past the last tail are padding
+                    const int colb = j * BN_SIMT + tx * 8;
+#pragma unroll
+                    for (int b = 0; b < 8; ++b)
+                        if (colb + b >= p.N) hit &= ~(0x0101010101010101ull << b);
+                    unsigned long long slot = warp_reserve(__popcll(hit), p.cand_count);
+                    while (hit) {
+                        const int ab = __ffsll(hit) - 1;
+                        if (slot < (unsigned long long)p.cand_cap)
+                            p.cand[slot] = make_int2(w.x * BM + ty * 8 + (ab >> 3), colb + (ab & 7));
+                        ++slot;
+                        hit &= hit - 1;
                     }
                 }
 #pragma unroll

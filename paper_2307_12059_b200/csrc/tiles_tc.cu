@@ -9,11 +9,11 @@
 // FP64 re-check (verify.cu) decides -- the filtering stays lossless
 // (PAPER.md:349-351).
 //
-// Persistent kernel, one CTA per SM, 192 threads:
+// Persistent kernel, one CTA per SM, 320 threads:
 //   warp 0      producer: 1-D bulk TMA (cp.async.bulk) of the staged query
 //               tile (resident for a work item) and of K-chunks of tail tiles
 //   warp 1      TMEM allocation + single-thread tcgen05.mma issue
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> band test -> candidates
+//   warps 2..9  epilogue: tcgen05.ld 32x32b.x32 -> band test -> candidates
 // TMEM holds two 128 x 256 FP32 accumulators (all 512 columns) so the
 // epilogue of tile j overlaps the MMAs of tile j + 1.
 #include <cstdio>
@@ -22,7 +22,7 @@
 
 namespace kgc {
 
-constexpr int TC_THREADS = 192;
+constexpr int TC_THREADS = 320;  // 2 control warps + 8 epilogue warps
 constexpr uint32_t LBO_A = (BM / 8) * 128;     // bytes between K-adjacent core matrices, query tile
 constexpr uint32_t LBO_B = (BN_TC / 8) * 128;  // same, tail tile
 constexpr uint32_t SBO = 128;                  // bytes between M/N-adjacent core matrices
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
             mbar_init(&a_full[i], 1);
             mbar_init(&a_empty[i], 1);
             mbar_init(&acc_full[i], 1);
-            mbar_init(&acc_empty[i], 4);
+            mbar_init(&acc_empty[i], 8);
         }
         for (int i = 0; i < b_stages; ++i) {
             mbar_init(&b_full[i], 1);
@@ -154,7 +154,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
         }
     } else {
         // ---------------------------------------------------- epilogue
-        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        // 8 warps: warp w reads TMEM lane quadrant (w % 4) (hardware rule) and
+        // column half (w - 2) / 4 of the 128 x 256 accumulator.
+        const int q = warp & 3;
+        const int col0 = ((warp - 2) >> 2) * (BN_TC / 2);
         const int i = q * 32 + lane;
         int acc = 0;
         uint32_t accph = 0;
@@ -172,37 +175,61 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
                 const float eb = Qd * Tm + Qn * Tdm + Qd * Tdm + p.eta * (Qn + Qd) * (Tm + Tdm);
                 const float sl = 4.76837158203125e-07f * (Qn + Tm) * (Qn + Tm);  // 8u (Qn + Tm)^2, fp32 evaluation
                 const float R = thf * thf + 2.0f * eb + sl;
+                // candidate iff 2 acc - ||t||^2 >= c
                 const float c = Q2 - R - 9.5367431640625e-07f * (Q2 + R);
                 mbar_wait(&acc_full[acc], accph);
                 tc_fence_after();
-                const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_TC);
-                const float4* t2 = reinterpret_cast<const float4*>(p.T2 + (size_t)j * BN_TC);
-#pragma unroll 1
-                for (int ch = 0; ch < BN_TC / 32; ++ch) {
-                    float v[32];
-                    tmem_ld32(tbase + ch * 32, v);
-                    uint32_t hit = 0;
+                const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_TC + col0);
+                const float* t2row = p.T2 + (size_t)j * BN_TC + col0;
+                uint32_t ra[32], rb[32];
+                auto process = [&](const uint32_t (&r)[32], int ch) {
+                    const float4* t2 = reinterpret_cast<const float4*>(t2row + ch * 32);
+                    float m0 = -3.0e38f, m1 = -3.0e38f, m2 = -3.0e38f, m3 = -3.0e38f;
 #pragma unroll
                     for (int u4 = 0; u4 < 8; ++u4) {
-                        const float4 tt = __ldg(t2 + ch * 8 + u4);
-                        hit |= (uint32_t)(fmaf(2.0f, v[4 * u4 + 0], -tt.x) >= c) << (4 * u4 + 0);
-                        hit |= (uint32_t)(fmaf(2.0f, v[4 * u4 + 1], -tt.y) >= c) << (4 * u4 + 1);
-                        hit |= (uint32_t)(fmaf(2.0f, v[4 * u4 + 2], -tt.z) >= c) << (4 * u4 + 2);
-                        hit |= (uint32_t)(fmaf(2.0f, v[4 * u4 + 3], -tt.w) >= c) << (4 * u4 + 3);
+                        const float4 tt = __ldg(t2 + u4);
+                        m0 = fmaxf(m0, fmaf(2.0f, __uint_as_float(r[4 * u4 + 0]), -tt.x));
+                        m1 = fmaxf(m1, fmaf(2.0f, __uint_as_float(r[4 * u4 + 1]), -tt.y));
+                        m2 = fmaxf(m2, fmaf(2.0f, __uint_as_float(r[4 * u4 + 2]), -tt.z));
+                        m3 = fmaxf(m3, fmaf(2.0f, __uint_as_float(r[4 * u4 + 3]), -tt.w));
                     }
-                    if (__any_sync(0xffffffffu, hit != 0)) {
-#pragma unroll 1
-                        for (int u = 0; u < 32; ++u) {
-                            const bool pr = (hit >> u) & 1u;
-                            const unsigned long long slot = warp_append(pr, p.cand_count);
-                            if (pr && slot < (unsigned long long)p.cand_cap)
-                                p.cand[slot] = make_int2(rowid, j * BN_TC + ch * 32 + u);
+                    const float m = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+                    if (__any_sync(0xffffffffu, m >= c)) {
+                        uint32_t hit = 0;
+#pragma unroll
+                        for (int u4 = 0; u4 < 8; ++u4) {
+                            const float4 tt = __ldg(t2 + u4);
+                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 0]), -tt.x) >= c) << (4 * u4 + 0);
+                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 1]), -tt.y) >= c) << (4 * u4 + 1);
+                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 2]), -tt.z) >= c) << (4 * u4 + 2);
+                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 3]), -tt.w) >= c) << (4 * u4 + 3);
+                        }
+                        unsigned long long slot = warp_reserve(__popc(hit), p.cand_count);
+                        const int colb = j * BN_TC + col0 + ch * 32;
+                        while (hit) {
+                            const int u = __ffs(hit) - 1;
+                            if (slot < (unsigned long long)p.cand_cap) p.cand[slot] = make_int2(rowid, colb + u);
+                            ++slot;
+                            hit &= hit - 1;
                         }
                     }
-                }
+                };
+                // software-pipelined TMEM loads: chunk ch + 1 is in flight while ch is tested
+                tmem_ld32_nowait(tbase + 0, ra);
+                tmem_wait_ld();
+                tmem_ld32_nowait(tbase + 32, rb);
+                process(ra, 0);
+                tmem_wait_ld();
+                tmem_ld32_nowait(tbase + 64, ra);
+                process(rb, 1);
+                tmem_wait_ld();
+                tmem_ld32_nowait(tbase + 96, rb);
+                process(ra, 2);
+                tmem_wait_ld();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty[acc]);
+                process(rb, 3);
                 if (++acc == 2) { acc = 0; accph ^= 1; }
             }
         }

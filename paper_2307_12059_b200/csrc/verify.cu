@@ -6,75 +6,102 @@
 // PAPER.md:369).  Each candidate (sorted query row, sorted tail) is mapped
 // back through the permutations (h = pi_r[i], t = pi_T[j]) and its distance
 // dist3(h, r, t) = ||h + r - t||_p is recomputed from the
-// ORIGINAL fp32 embeddings in FP64 (one warp per candidate, lanes over k,
-// warp-shuffle tree).  Kept iff dist <= theta (inclusive);
-// emitted as {h, r, t, (float)dist} with one atomic per warp.
+// ORIGINAL fp32 embeddings in FP64 (8 lanes per candidate, lanes over k,
+// shuffle tree).  Kept iff dist <= theta (inclusive); emitted as
+// {h, r, t, (float)dist} with one atomic per warp per 32 candidates.
 #include "common.cuh"
 
 namespace kgc {
 
-__device__ __forceinline__ double warp_sum_dd(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
+template <int NORM, bool VEC4>
+__device__ __forceinline__ double partial_dist(const float* __restrict__ eh, const float* __restrict__ er,
+                                               const float* __restrict__ et, int d, int s) {
+    double acc = 0.0;
+    if (VEC4) {
+        for (int k = s * 4; k < d; k += 32) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(eh + k));
+            const float4 b = __ldg(reinterpret_cast<const float4*>(er + k));
+            const float4 c = __ldg(reinterpret_cast<const float4*>(et + k));
+            const double x0 = ((double)a.x + (double)b.x) - (double)c.x;  // (h + r) - t, FP64
+            const double x1 = ((double)a.y + (double)b.y) - (double)c.y;
+            const double x2 = ((double)a.z + (double)b.z) - (double)c.z;
+            const double x3 = ((double)a.w + (double)b.w) - (double)c.w;
+            if (NORM == 1) acc += fabs(x0) + fabs(x1) + fabs(x2) + fabs(x3);
+            else acc += x0 * x0 + x1 * x1 + x2 * x2 + x3 * x3;
+        }
+    } else {
+        for (int k = s; k < d; k += 8) {
+            const double x = ((double)__ldg(eh + k) + (double)__ldg(er + k)) - (double)__ldg(et + k);
+            acc += NORM == 1 ? fabs(x) : x * x;
+        }
+    }
+    return acc;
 }
 
+// One warp verifies 32 candidates per round: 8 lanes per candidate (4 at a
+// time), FP64 partial sums reduced over the 8 lanes, one atomic per round.
+template <int NORM, bool VEC4>
 __global__ void __launch_bounds__(256) verify_kernel(const int2* __restrict__ cand,
                                                      const unsigned long long* __restrict__ cand_count,
                                                      long long cand_cap, const int* __restrict__ qperm,
                                                      const int* __restrict__ tperm, const float* __restrict__ E,
                                                      const float* __restrict__ Rel, long long N, int QT, int d,
-                                                     int norm, double theta, KgcTripletDev* __restrict__ out,
+                                                     double theta, KgcTripletDev* __restrict__ out,
                                                      unsigned long long* res_count, long long res_cap) {
     long long nc = (long long)*cand_count;
     if (nc > cand_cap) nc = cand_cap;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, g = lane >> 3, s = lane & 7;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const long long rows_per_rel = (long long)QT * BM;
-    for (long long g = warp; g * 32 < nc; g += nwarps) {
-        const long long idx = g * 32 + lane;
-        bool valid = idx < nc;
-        int h = 0, r = 0, t = 0;
-        if (valid) {
-            const int2 cv = cand[idx];
-            const long long rr = cv.x / rows_per_rel;
-            const long long pos = cv.x - rr * rows_per_rel;
-            valid = pos < N && cv.y < N;
+    for (long long base = warp * 32; base < nc; base += nwarps * 32) {
+        uint32_t keep = 0;
+        int hs[8], rs[8], ts[8];
+        float ds[8];
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+            const long long idx = base + it * 4 + g;
+            bool valid = idx < nc;
+            int h = 0, r = 0, t = 0;
             if (valid) {
-                r = (int)rr;
-                h = qperm[rr * N + pos];
-                t = tperm[cv.y];
+                const int2 cv = cand[idx];
+                const long long rr = cv.x / rows_per_rel;
+                const long long pos = cv.x - rr * rows_per_rel;
+                valid = pos < N && cv.y < N;
+                if (valid) {
+                    r = (int)rr;
+                    h = qperm[rr * N + pos];
+                    t = tperm[cv.y];
+                }
             }
+            double acc = valid ? partial_dist<NORM, VEC4>(E + (long long)h * d, Rel + (long long)r * d,
+                                                          E + (long long)t * d, d, s)
+                               : 0.0;
+            acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+            const double dist = NORM == 2 ? sqrt(acc) : acc;
+            keep |= (uint32_t)(valid && dist <= theta) << it;
+            hs[it] = h;
+            rs[it] = r;
+            ts[it] = t;
+            ds[it] = (float)dist;
         }
-        const int n_here = (int)min(32LL, nc - g * 32);
-        double mine = 0.0;
-        for (int c = 0; c < n_here; ++c) {
-            const int hc = __shfl_sync(0xffffffffu, h, c);
-            const int rc = __shfl_sync(0xffffffffu, r, c);
-            const int tc = __shfl_sync(0xffffffffu, t, c);
-            const float* eh = E + (long long)hc * d;
-            const float* er = Rel + (long long)rc * d;
-            const float* et = E + (long long)tc * d;
-            double s = 0.0;
-            for (int k = lane; k < d; k += 32) {
-                const double q = (double)eh[k] + (double)er[k];   // connector_1(h, r) = h + r
-                const double x = q - (double)et[k];              // - connector_2(t, r) = t
-                s += norm == 1 ? fabs(x) : x * x;
+        if (s != 0) keep = 0;
+        unsigned long long slot = warp_reserve(__popc(keep), res_count);
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+            if (keep & (1u << it)) {
+                if (slot < (unsigned long long)res_cap) {
+                    KgcTripletDev o;
+                    o.h = hs[it];
+                    o.r = rs[it];
+                    o.t = ts[it];
+                    o.dist = ds[it];
+                    out[slot] = o;
+                }
+                ++slot;
             }
-            s = warp_sum_dd(s);
-            if (lane == c) mine = s;
-        }
-        const double dist = norm == 2 ? sqrt(mine) : mine;
-        const bool keep = valid && dist <= theta;
-        const unsigned long long slot = warp_append(keep, res_count);
-        if (keep && slot < (unsigned long long)res_cap) {
-            KgcTripletDev o;
-            o.h = h;
-            o.r = r;
-            o.t = t;
-            o.dist = (float)dist;
-            out[slot] = o;
         }
     }
 }
@@ -83,8 +110,11 @@ void launch_verify(const int2* cand, const unsigned long long* cand_count, long 
                    const int* tperm, const float* E, const float* Rel, long long N, int QT, int d, int norm,
                    float theta, KgcTripletDev* out, unsigned long long* res_count, long long res_cap, int num_sms,
                    cudaStream_t s) {
-    verify_kernel<<<num_sms * 8, 256, 0, s>>>(cand, cand_count, cand_cap, qperm, tperm, E, Rel, N, QT, d, norm,
-                                              (double)theta, out, res_count, res_cap);
+    const bool vec4 = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(E) | reinterpret_cast<uintptr_t>(Rel)) % 16 == 0);
+    auto kern = norm == 1 ? (vec4 ? verify_kernel<1, true> : verify_kernel<1, false>)
+                          : (vec4 ? verify_kernel<2, true> : verify_kernel<2, false>);
+    kern<<<num_sms * 8, 256, 0, s>>>(cand, cand_count, cand_cap, qperm, tperm, E, Rel, N, QT, d, (double)theta, out,
+                                     res_count, res_cap);
 }
 
 }  // namespace kgc
