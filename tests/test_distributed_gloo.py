@@ -1,0 +1,105 @@
+"""N > 1 host logic on CPU: two processes (gloo, world_size 2) split the query
+tiles with libkgc's kgc_shard_range (the rule the device uses), each joins its
+own shard, counts are all-reduced as bench.py does, and the union of the
+shards equals the single-process join (sharding invariance).
+
+The per-rank join here is the oracle restricted to the rank's query rows (no
+GPU on this box); the GPU sharding itself is covered by
+tests/test_gpu_parity.py::test_sharding_invariance.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+BM, BN = 128, 128
+
+
+def _plan(E, Rel, norm, eps):
+    """Per relation: queries sorted by pivot distance (zero pivot), query tiles of
+    BM rows, surviving tail tiles by Lemma 1 at tile granularity; returns the
+    sorted head order per relation and the per-query-tile surviving-tile counts."""
+    from oracle import oracle
+    N, R = E.shape[0], Rel.shape[0]
+    p = np.zeros(E.shape[1])
+    _, skt = oracle.sort_side(oracle.pivot_distances(E, p, norm))
+    TT = (N + BN - 1) // BN
+    tmin = np.array([skt[j * BN:(j + 1) * BN].min() for j in range(TT)])
+    tmax = np.array([skt[j * BN:(j + 1) * BN].max() for j in range(TT)])
+    QT = (N + BM - 1) // BM
+    order, cost = [], []
+    for r in range(R):
+        perm, skq = oracle.sort_side(oracle.pivot_distances(oracle.connector1(E, Rel[r]), p, norm))
+        order.append(perm)
+        for qt in range(QT):
+            rows = skq[qt * BM:(qt + 1) * BM]
+            ok = (tmax >= rows.min() - eps) & (tmin <= rows.max() + eps)
+            cost.append(int(ok.sum()))
+    return order, np.array(cost, np.int64), QT
+
+
+def _worker(rank, world, port, E, Rel, norm, eps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle
+        from paper_2307_12059_b200 import kgc
+        N, R = E.shape[0], Rel.shape[0]
+        order, cost, QT = _plan(E, Rel, norm, eps)
+        cum = np.concatenate([[0], np.cumsum(cost)[:-1]])
+        total = int(cost.sum())
+        b, e, my_cost = kgc.kgc_shard_range(cum, total, rank, world)
+        rows = []
+        for tq in range(b, e):
+            r, qt = divmod(tq, QT)
+            for h in order[r][qt * BM:(qt + 1) * BM]:
+                rows.append(int(h) * R + r)
+        res = oracle.join(E, Rel, norm, eps, rows=np.sort(np.array(rows, np.int64))) if rows else \
+            np.zeros(0, oracle.TRIPLET_DTYPE)
+        counts = torch.tensor([res.size, my_cost], dtype=torch.int64)
+        dist.all_reduce(counts)                      # as bench.py does after every step
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (b, e, [tuple(x) for x in zip(res["h"], res["r"], res["t"])]))
+        if rank == 0:
+            q.put((int(counts[0]), int(counts[1]), total, gathered))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("norm", [1, 2])
+def test_two_rank_shards_union_equals_full_join(norm):
+    from oracle import oracle
+    from synth import generate
+    E, Rel = generate(700, 5, 16, seed=50)
+    D = np.sort(oracle.dist_rows(E, Rel, norm).ravel())
+    eps = float(np.float32(0.5 * (D[2000] + D[2001])))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, E, Rel, norm, eps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    n_all, cost_all, total, gathered = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = oracle.join(E, Rel, norm, eps)
+    full_set = set(zip(full["h"].tolist(), full["r"].tolist(), full["t"].tolist()))
+    shards = [set(g[2]) for g in gathered]
+    assert not (shards[0] & shards[1])
+    assert shards[0] | shards[1] == full_set
+    assert n_all == len(full_set)
+    assert cost_all == total
+    (b0, e0, _), (b1, e1, _) = gathered
+    assert b0 == 0 and e0 == b1          # contiguous split of the query tiles
