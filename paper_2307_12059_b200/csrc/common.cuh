@@ -15,6 +15,17 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// One lane of a converged warp (PTX elect.sync).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -174,6 +185,20 @@ __device__ __forceinline__ unsigned long long warp_reserve(uint32_t n, unsigned 
     if (lane == 31 && total) base = atomicAdd(counter, (unsigned long long)total);
     base = __shfl_sync(0xffffffffu, base, 31);
     return base + (incl - n);
+}
+
+// Contiguous, cost-balanced block of work items for CTA b of G: the first item
+// whose exclusive tile prefix reaches floor(total * b / G) (b == G gives n).
+__device__ __forceinline__ long long balanced_begin(const long long* __restrict__ cum, long long n, long long total,
+                                                    long long b, long long G) {
+    if (b >= G) return n;
+    const long long target = total * b / G;
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        const long long m = (lo + hi) >> 1;
+        if (cum[m] >= target) hi = m; else lo = m + 1;
+    }
+    return lo;
 }
 
 // float -> float rounded towards +inf from a double

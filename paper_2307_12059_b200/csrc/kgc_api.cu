@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -41,7 +42,8 @@ struct kgc_ctx {
     cudaStream_t own_stream = nullptr;
     std::string err;
     DevBuf E, Rel, pivot, kt, kq, mm_t, mm_q, sk0, sv0, sk1, sv1, counts, scan_tmp, qperm, qskey, tperm, tskey, tmin,
-        tmax, cmax, cmin, ranges, cost, cum, nitem, item_off, items, Qp, qs, Tp, T2, tstile, cand, res, ctr;
+        tmax, cmax, cmin, ranges, cost, cum, nitem, item_off, items, item_tiles, item_cum, Qp, qs, Tp, T2, tstile, cand,
+        res, ctr;
     long long cand_cap = 0, res_cap = 0;
     long long n_results = -1;
     kgc_stats_t st{};
@@ -189,7 +191,7 @@ void kgc_destroy(kgc_ctx* ctx) {
                       &ctx->sk0,   &ctx->sv0,    &ctx->sk1,    &ctx->sv1,   &ctx->counts, &ctx->scan_tmp,
                       &ctx->qperm, &ctx->qskey,  &ctx->tperm,  &ctx->tskey, &ctx->tmin,   &ctx->tmax,   &ctx->cmax,
                       &ctx->cmin,  &ctx->ranges, &ctx->cost,   &ctx->cum,   &ctx->nitem,  &ctx->item_off,
-                      &ctx->items, &ctx->Qp,     &ctx->qs,     &ctx->Tp,    &ctx->T2,     &ctx->tstile, &ctx->cand,
+                      &ctx->items, &ctx->item_tiles, &ctx->item_cum, &ctx->Qp,     &ctx->qs,     &ctx->Tp,    &ctx->T2,     &ctx->tstile, &ctx->cand,
                       &ctx->res,   &ctx->ctr};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
@@ -267,7 +269,11 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const int QT = (int)((N + BM - 1) / BM);
     const int TT = (int)((N + BN - 1) / BN);
     const long long nq = R * (long long)QT;
-    const int chunk = ctx->opt.chunk_tiles > 0 ? ctx->opt.chunk_tiles : (tc ? 16 : 8);
+    int chunk = ctx->opt.chunk_tiles > 0 ? ctx->opt.chunk_tiles : (tc ? 16 : 8);
+    if (tc && ctx->opt.chunk_tiles == 0) {
+        int as = 0, bs = 0, kc = 0;
+        if (tc_smem_bytes(((d + 7) / 8) * 8, &as, &bs, &kc) > 0 && as == 1) chunk = 64;  // amortise A rebuilds
+    }
     ctx->N = N;
     ctx->R = R;
     ctx->QT = QT;
@@ -365,7 +371,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                        ctx->scan_tmp.p, s, &ctx->launches);
     LAUNCHED(0);
     launch_shard_items(P<int2>(ctx->ranges), P<long long>(ctx->cost), P<long long>(ctx->cum), nq, ctx->opt.rank,
-                       ctx->opt.world, chunk, dctr, P<int>(ctx->nitem), P<int>(ctx->item_off), nullptr,
+                       ctx->opt.world, chunk, dctr, P<int>(ctx->nitem), P<int>(ctx->item_off), nullptr, nullptr,
                        ctx->scan_tmp.p, s, &ctx->launches, 0);
     LAUNCHED(0);
     // sync #1: plan totals
@@ -389,9 +395,15 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const int tq1 = h1.c.tq_begin == INT_MAX ? 0 : h1.c.tq_end;
     if (n_items > 0) {
         CK(ensure(ctx->items, (size_t)n_items * 16));
+        CK(ensure(ctx->item_tiles, (size_t)n_items * 8));
+        CK(ensure(ctx->item_cum, (size_t)n_items * 8));
+        CK(ensure(ctx->scan_tmp, scan_tmp_bytes((size_t)n_items)));
         launch_shard_items(P<int2>(ctx->ranges), P<long long>(ctx->cost), P<long long>(ctx->cum), nq, ctx->opt.rank,
                            ctx->opt.world, chunk, dctr, P<int>(ctx->nitem), P<int>(ctx->item_off),
-                           P<int4>(ctx->items), ctx->scan_tmp.p, s, &ctx->launches, 1);
+                           P<int4>(ctx->items), P<long long>(ctx->item_tiles), ctx->scan_tmp.p, s, &ctx->launches, 1);
+        LAUNCHED(0);
+        scan_exclusive_i64(P<long long>(ctx->item_tiles), P<long long>(ctx->item_cum), (size_t)n_items, nullptr,
+                           ctx->scan_tmp.p, s, &ctx->launches);
         LAUNCHED(0);
     }
     CK(cudaEventRecord(ctx->ev[EV_RANGES], s));
@@ -401,14 +413,16 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(ensure(ctx->Tp, (size_t)TT * BN * Kpad * 4));
         CK(ensure(ctx->T2, (size_t)TT * BN * 4));
         CK(ensure(ctx->tstile, (size_t)TT * 8));
-        CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * BM * Kpad * 4));
-        CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * BM * 16));
         launch_stage_tails(E, P<int>(ctx->tperm), N, d, Kpad, BN, TT, tc ? 1 : 0, P<float>(ctx->Tp), P<float>(ctx->T2),
                            P<float2>(ctx->tstile), s);
         LAUNCHED(1);
-        launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, tq0, tq1, tc ? 1 : 0, norm, eps,
-                             P<float>(ctx->Qp), P<float4>(ctx->qs), s);
-        LAUNCHED(1);
+        if (!tc) {  // the tensor-core engine forms its query tiles on the fly
+            CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * BM * Kpad * 4));
+            CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * BM * 16));
+            launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, tq0, tq1, 0, norm, eps,
+                                 P<float>(ctx->Qp), P<float4>(ctx->qs), s);
+            LAUNCHED(1);
+        }
     }
     CK(cudaEventRecord(ctx->ev[EV_STAGE], s));
 
@@ -429,6 +443,12 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.tstile = P<float2>(ctx->tstile);
         tp.items = P<int4>(ctx->items);
         tp.n_items = n_items;
+        tp.item_cum = P<long long>(ctx->item_cum);
+        tp.total_tiles = h1.c.my_cost;
+        {   // tuning knob for experiments: KGC_SCHED_TC / KGC_SCHED_SIMT = 0 (round-robin) | 1 (balanced blocks)
+            const char* e = getenv(tc ? "KGC_SCHED_TC" : "KGC_SCHED_SIMT");
+            tp.sched = e ? atoi(e) : (tc ? 0 : 1);
+        }
         tp.Kpad = Kpad;
         tp.tq0 = tq0;
         tp.N = (int)N;
@@ -437,6 +457,11 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.cand = P<int2>(ctx->cand);
         tp.cand_count = &dctr->cand;
         tp.cand_cap = ctx->cand_cap;
+        tp.E = E;
+        tp.Rel = Rel;
+        tp.qperm = P<int>(ctx->qperm);
+        tp.d = d;
+        tp.QT = QT;
         if (n_items > 0) {
             if (tc) launch_tiles_tc(tp, ctx->num_sms, s);
             else launch_tiles_simt(tp, norm, ctx->num_sms, s);

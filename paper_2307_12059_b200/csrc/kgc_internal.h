@@ -32,6 +32,9 @@ struct TileParams {
     const float2* tstile;   // per tail tile {max ||t||, max ||t - tf32(t)||}
     const int4* items;      // {tq, j0, j1, 0}
     long long n_items;
+    const long long* item_cum;  // exclusive prefix of item tile counts (cost-balanced CTA ranges)
+    long long total_tiles;
+    int sched;                  // 0 = round-robin items, 1 = contiguous cost-balanced blocks
     int Kpad;
     int tq0;                // first staged query tile
     int N;                  // tails (valid columns are < N)
@@ -40,6 +43,12 @@ struct TileParams {
     int2* cand;
     unsigned long long* cand_count;
     long long cand_cap;
+    // tensor-core engine: query tiles are formed on the fly from these
+    const float* E;
+    const float* Rel;
+    const int* qperm;
+    int d;
+    int QT;
 };
 
 // ---- launchers (prep.cu) ----
@@ -65,7 +74,7 @@ void launch_query_ranges(const float* qskey, long long N, long long R, int QT, i
                          cudaStream_t s);
 void launch_shard_items(const int2* ranges, const long long* cost, const long long* cum, long long nq,
                         int rank, int world, int chunk, DevCounters* ctr, int* nitem, int* item_off,
-                        int4* items, void* tmp, cudaStream_t s, int* launches, int phase);
+                        int4* items, long long* item_tiles, void* tmp, cudaStream_t s, int* launches, int phase);
 void launch_stage_tails(const float* E, const int* tperm, long long N, int d, int Kpad, int BN, int TT,
                         int tc_layout, float* Tp, float* T2, float2* tstile, cudaStream_t s);
 void launch_stage_queries(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad,

@@ -543,7 +543,7 @@ __global__ void shard_count_kernel(const long long* __restrict__ cost, const lon
 
 __global__ void shard_emit_kernel(const int2* __restrict__ ranges, const int* __restrict__ nitem,
                                   const int* __restrict__ off, long long nq, int chunk, DevCounters* ctr,
-                                  int4* items) {
+                                  int4* items, long long* item_tiles) {
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq; q += (long long)gridDim.x * blockDim.x) {
         int n = nitem[q];
         int o = off[q];
@@ -553,19 +553,21 @@ __global__ void shard_emit_kernel(const int2* __restrict__ ranges, const int* __
             int j0 = rg.x + k * chunk;
             int j1 = min(rg.y, j0 + chunk - 1);
             items[o + k] = make_int4((int)q, j0, j1, 0);
+            item_tiles[o + k] = j1 - j0 + 1;
         }
     }
 }
 
 void launch_shard_items(const int2* ranges, const long long* cost, const long long* cum, long long nq, int rank,
-                        int world, int chunk, DevCounters* ctr, int* nitem, int* item_off, int4* items, void* tmp,
-                        cudaStream_t s, int* launches, int phase) {
+                        int world, int chunk, DevCounters* ctr, int* nitem, int* item_off, int4* items,
+                        long long* item_tiles, void* tmp, cudaStream_t s, int* launches, int phase) {
     if (phase == 0) {
         shard_count_kernel<<<grid_for(nq, 256), 256, 0, s>>>(cost, cum, nq, rank, world, chunk, ctr, nitem);
         scan_exclusive_i32(nitem, item_off, (size_t)nq, tmp, s, launches);
         if (launches) *launches += 1;
     } else {
-        shard_emit_kernel<<<grid_for(nq, 256), 256, 0, s>>>(ranges, nitem, item_off, nq, chunk, ctr, items);
+        shard_emit_kernel<<<grid_for(nq, 256), 256, 0, s>>>(ranges, nitem, item_off, nq, chunk, ctr, items,
+                                                            item_tiles);
         if (launches) *launches += 1;
     }
 }

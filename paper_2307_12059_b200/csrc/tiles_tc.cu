@@ -9,9 +9,11 @@
 // FP64 re-check (verify.cu) decides -- the filtering stays lossless
 // (PAPER.md:349-351).
 //
-// Persistent kernel, one CTA per SM, 320 threads:
-//   warp 0      producer: 1-D bulk TMA (cp.async.bulk) of the staged query
-//               tile (resident for a work item) and of K-chunks of tail tiles
+// Persistent kernel, one CTA per SM, 448 threads:
+//   warp 0      producer: 1-D bulk TMA (cp.async.bulk) of K-chunks of the
+//               staged tail tiles
+//   warps 10-13 builders: form the query tile q = fl32(h + r) of the next
+//               work item in shared memory (UMMA layout) + its row scalars
 //   warp 1      TMEM allocation + single-thread tcgen05.mma issue
 //   warps 2..9  epilogue: tcgen05.ld 32x32b.x32 -> band test -> candidates
 // TMEM holds two 128 x 256 FP32 accumulators (all 512 columns) so the
@@ -22,14 +24,27 @@
 
 namespace kgc {
 
-constexpr int TC_THREADS = 320;  // 2 control warps + 8 epilogue warps
+#ifdef KGC_PROF_TC
+// debug build only: cycles each role spends blocked in each barrier wait
+__device__ unsigned long long g_tc_prof[16];
+#define TC_WAIT(slot, bar, par)                                    \
+    do {                                                           \
+        const long long t0_ = clock64();                           \
+        mbar_wait(bar, par);                                       \
+        atomicAdd(&g_tc_prof[slot], (unsigned long long)(clock64() - t0_)); \
+    } while (0)
+#else
+#define TC_WAIT(slot, bar, par) mbar_wait(bar, par)
+#endif
+constexpr int TC_THREADS = 448;  // 2 control warps + 8 epilogue warps + 4 builder warps
+constexpr int TC_BUILDER_WARP0 = 10;
 constexpr uint32_t LBO_A = (BM / 8) * 128;     // bytes between K-adjacent core matrices, query tile
 constexpr uint32_t LBO_B = (BN_TC / 8) * 128;  // same, tail tile
 constexpr uint32_t SBO = 128;                  // bytes between M/N-adjacent core matrices
 constexpr uint32_t IDESC = idesc_tf32(BM, BN_TC);
 
 int tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
-    const int budget = 227 * 1024 - 512;
+    const int budget = 227 * 1024 - 512 - 2 * BM * 16;
     const int A = BM * Kpad * 4;
     for (int KC : {32, 16, 8}) {
         const int B = BN_TC * KC * 4;
@@ -42,7 +57,7 @@ int tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
                 *a_stages = as;
                 *b_stages = bs;
                 *kc = KC;
-                int bytes = as * A + bs * B + 256;
+                int bytes = as * A + bs * B + 256 + as * BM * 16;
                 // >= 117 KB keeps one CTA per SM, so the 512-column TMEM
                 // allocation never waits on a co-resident CTA.
                 return bytes < 117 * 1024 ? 117 * 1024 : bytes;
@@ -56,7 +71,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
     extern __shared__ __align__(1024) uint8_t smem[];
     const int Kpad = p.Kpad;
     const uint32_t A_FLOATS = BM * Kpad;
-    const uint32_t A_BYTES = A_FLOATS * 4;
     const int nkc = (Kpad + KC - 1) / KC;
     float* As = reinterpret_cast<float*>(smem);
     float* Bs = As + (size_t)a_stages * A_FLOATS;
@@ -68,12 +82,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
     uint64_t* acc_full = b_empty + b_stages;
     uint64_t* acc_empty = acc_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    float4* qrow = reinterpret_cast<float4*>(bars + 32);  // [a_stages][BM] {||q||^2, ||q||, ||q - tf32(q)||, 0}
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // this CTA's contiguous, cost-balanced block of work items (every role walks it)
+    const long long it_begin = p.sched ? balanced_begin(p.item_cum, p.n_items, p.total_tiles, blockIdx.x, gridDim.x)
+                                       : (long long)blockIdx.x;
+    const long long it_end = p.sched ? balanced_begin(p.item_cum, p.n_items, p.total_tiles, blockIdx.x + 1, gridDim.x)
+                                     : p.n_items;
+    const long long it_step = p.sched ? 1 : gridDim.x;
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&a_full[i], 1);
-            mbar_init(&a_empty[i], 1);
+            mbar_init(&a_full[i], BM);        // one arrival per builder thread (one row each)
+            mbar_init(&a_empty[i], 1 + 8);    // MMA commit + the 8 epilogue warps (row scalars read)
             mbar_init(&acc_full[i], 1);
             mbar_init(&acc_empty[i], 8);
         }
@@ -91,26 +112,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
 
     if (warp == 0) {
         if (lane == 0) {
-            // ------------------------------------------------ producer
-            int ai = 0, bi = 0;
-            uint32_t aph = 0, bph = 0;
-            for (long long it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+            // ------------------------------------------------ producer (tail tiles)
+            int bi = 0;
+            uint32_t bph = 0;
+            for (long long it = it_begin; it < it_end; it += it_step) {
                 const int4 w = p.items[it];
-                mbar_wait(&a_empty[ai], aph ^ 1);
-                mbar_arrive_expect_tx(&a_full[ai], A_BYTES);
-                const float* src = p.Qp + (size_t)(w.x - p.tq0) * A_FLOATS;
-                float* dst = As + (size_t)ai * A_FLOATS;
-                for (uint32_t off = 0; off < A_BYTES; off += 32768u) {
-                    uint32_t n = A_BYTES - off < 32768u ? A_BYTES - off : 32768u;
-                    bulk_g2s(dst + off / 4, src + off / 4, n, &a_full[ai]);
-                }
-                if (++ai == a_stages) { ai = 0; aph ^= 1; }
                 for (int j = w.y; j <= w.z; ++j) {
                     const float* tsrc = p.Tp + (size_t)j * BN_TC * Kpad;
                     for (int c = 0; c < nkc; ++c) {
                         const int klen = Kpad - c * KC < KC ? Kpad - c * KC : KC;
                         const uint32_t bytes = (uint32_t)klen * BN_TC * 4;
-                        mbar_wait(&b_empty[bi], bph ^ 1);
+                        TC_WAIT(0, &b_empty[bi], bph ^ 1);
                         mbar_arrive_expect_tx(&b_full[bi], bytes);
                         bulk_g2s(Bs + (size_t)bi * BN_TC * KC, tsrc + (size_t)c * KC * BN_TC, bytes, &b_full[bi]);
                         if (++bi == b_stages) { bi = 0; bph ^= 1; }
@@ -119,51 +131,66 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ------------------------------------------------ MMA issuer
-            int ai = 0, bi = 0, acc = 0;
-            uint32_t aph = 0, bph = 0, accph = 0;
-            for (long long it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-                const int4 w = p.items[it];
-                mbar_wait(&a_full[ai], aph);
+        // ---------------------------------------------------- MMA issuer
+        // The whole warp walks the schedule (so every operand of tcgen05.mma is
+        // warp-uniform and lives in uniform registers); one elected lane issues.
+        int ai = 0, bi = 0, acc = 0;
+        uint32_t aph = 0, bph = 0, accph = 0;
+        for (long long it = it_begin; it < it_end; it += it_step) {
+            const int4 w = p.items[it];
+            TC_WAIT(1, &a_full[ai], aph);
+            tc_fence_after();
+            const uint64_t a_desc0 = umma_desc_kmajor(smem_u32(As + (size_t)ai * A_FLOATS), LBO_A, SBO);
+            for (int j = w.y; j <= w.z; ++j) {
+                TC_WAIT(2, &acc_empty[acc], accph ^ 1);
                 tc_fence_after();
-                const uint32_t a_base = smem_u32(As + (size_t)ai * A_FLOATS);
-                for (int j = w.y; j <= w.z; ++j) {
-                    mbar_wait(&acc_empty[acc], accph ^ 1);
+                const uint32_t d_tmem = tmem + (uint32_t)(acc * BN_TC);
+                for (int c = 0; c < nkc; ++c) {
+                    TC_WAIT(3, &b_full[bi], bph);
                     tc_fence_after();
-                    const uint32_t d_tmem = tmem + (uint32_t)(acc * BN_TC);
-                    for (int c = 0; c < nkc; ++c) {
-                        mbar_wait(&b_full[bi], bph);
-                        tc_fence_after();
-                        const uint32_t b_base = smem_u32(Bs + (size_t)bi * BN_TC * KC);
-                        const int klen = Kpad - c * KC < KC ? Kpad - c * KC : KC;
-                        for (int s = 0; s < klen / 8; ++s) {
-                            const uint64_t ad = umma_desc_kmajor(a_base + (uint32_t)(c * KC / 4 + 2 * s) * LBO_A, LBO_A, SBO);
-                            const uint64_t bd = umma_desc_kmajor(b_base + (uint32_t)(2 * s) * LBO_B, LBO_B, SBO);
-                            mma_tf32(d_tmem, ad, bd, IDESC, (c | s) != 0);
+                    const uint64_t b_desc0 = umma_desc_kmajor(smem_u32(Bs + (size_t)bi * BN_TC * KC), LBO_B, SBO);
+                    const int nsteps = (Kpad - c * KC < KC ? Kpad - c * KC : KC) / 8;
+                    // descriptor start address advances by 2 core matrices (K = 8) per step
+                    const uint64_t a_desc = a_desc0 + (uint64_t)((uint32_t)(c * KC / 4) * (LBO_A >> 4));
+                    if (elect_one()) {
+#pragma unroll
+                        for (int s = 0; s < 4; ++s) {
+                            if (s < nsteps)
+                                mma_tf32(d_tmem, a_desc + (uint64_t)(2 * s * (LBO_A >> 4)),
+                                         b_desc0 + (uint64_t)(2 * s * (LBO_B >> 4)), IDESC, (c | s) != 0);
                         }
+                        for (int s = 4; s < nsteps; ++s)  // KC > 32 is not configured; kept for safety
+                            mma_tf32(d_tmem, a_desc + (uint64_t)(2 * s * (LBO_A >> 4)),
+                                     b_desc0 + (uint64_t)(2 * s * (LBO_B >> 4)), IDESC, 1u);
                         mma_commit(&b_empty[bi]);
-                        if (++bi == b_stages) { bi = 0; bph ^= 1; }
                     }
-                    mma_commit(&acc_full[acc]);
-                    if (++acc == 2) { acc = 0; accph ^= 1; }
+                    __syncwarp();
+                    if (++bi == b_stages) { bi = 0; bph ^= 1; }
                 }
-                mma_commit(&a_empty[ai]);
-                if (++ai == a_stages) { ai = 0; aph ^= 1; }
+                if (elect_one()) mma_commit(&acc_full[acc]);
+                __syncwarp();
+                if (++acc == 2) { acc = 0; accph ^= 1; }
             }
+            if (elect_one()) mma_commit(&a_empty[ai]);
+            __syncwarp();
+            if (++ai == a_stages) { ai = 0; aph ^= 1; }
         }
-    } else {
+    } else if (warp < TC_BUILDER_WARP0) {
         // ---------------------------------------------------- epilogue
         // 8 warps: warp w reads TMEM lane quadrant (w % 4) (hardware rule) and
         // column half (w - 2) / 4 of the 128 x 256 accumulator.
         const int q = warp & 3;
         const int col0 = ((warp - 2) >> 2) * (BN_TC / 2);
         const int i = q * 32 + lane;
-        int acc = 0;
-        uint32_t accph = 0;
-        for (long long it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+        int acc = 0, ai = 0;
+        uint32_t accph = 0, aph = 0;
+        for (long long it = it_begin; it < it_end; it += it_step) {
             const int4 w = p.items[it];
-            const float4 qv = p.qs[(size_t)(w.x - p.tq0) * BM + i];
+            TC_WAIT(4, &a_full[ai], aph);
+            const float4 qv = qrow[ai * BM + i];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a_empty[ai]);
+            if (++ai == a_stages) { ai = 0; aph ^= 1; }
             const float Q2 = qv.x, Qn = qv.y, Qd = qv.z;
             const int rowid = w.x * BM + i;
             // theta_f covers q = fl32(h + r) vs the exact h + r (|dq_k| <= 2^-24 |q_k|)
@@ -176,8 +203,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
                 const float sl = 4.76837158203125e-07f * (Qn + Tm) * (Qn + Tm);  // 8u (Qn + Tm)^2, fp32 evaluation
                 const float R = thf * thf + 2.0f * eb + sl;
                 // candidate iff 2 acc - ||t||^2 >= c
-                const float c = Q2 - R - 9.5367431640625e-07f * (Q2 + R);
-                mbar_wait(&acc_full[acc], accph);
+                // Q2 is an FP32 sum: |Q2 - ||q||^2| <= (Kpad + 4) 2^-23 Q2 (builder)
+                const float c = Q2 - R - (float)(p.Kpad + 4) * 1.1920928955078125e-07f * Q2 - 9.5367431640625e-07f * (Q2 + R);
+                TC_WAIT(5, &acc_full[acc], accph);
                 tc_fence_after();
                 const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_TC + col0);
                 const float* t2row = p.T2 + (size_t)j * BN_TC + col0;
@@ -234,12 +262,92 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
             }
         }
     }
+    if (warp >= TC_BUILDER_WARP0) {
+        // ---------------------------------------------------- builders
+        // Form the query tile q = fl32(h + r) (connector_1) for
+        // the 128 sorted queries of the item directly in the UMMA layout,
+        // one row per thread (32 rows per warp -> 512 contiguous bytes per
+        // float4 store), plus the row scalars the epilogue's bound needs.
+        const int i = (warp - TC_BUILDER_WARP0) * 32 + lane;
+        const bool vec4 = (p.d % 4 == 0) && ((reinterpret_cast<uintptr_t>(p.E) | reinterpret_cast<uintptr_t>(p.Rel)) % 16 == 0);
+        int ai = 0;
+        uint32_t aph = 0;
+        for (long long it = it_begin; it < it_end; it += it_step) {
+            const int4 w = p.items[it];
+            const int r = w.x / p.QT;
+            const long long pos = (long long)(w.x - r * p.QT) * BM + i;
+            const bool valid = pos < p.N;
+            const long long h = valid ? p.qperm[(long long)r * p.N + pos] : 0;
+            const float* e = p.E + h * p.d;
+            const float* rr = p.Rel + (long long)r * p.d;
+            TC_WAIT(6, &a_empty[ai], aph ^ 1);
+            float* A = As + (size_t)ai * A_FLOATS;
+            // row statistics in FP32; every use below carries the (Kpad + 4) 2^-23
+            // relative error bound of a Kpad-term FP32 sum of non-negative terms
+            float s2 = 0.f, sd2 = 0.f;
+            const int nq = Kpad >> 2;
+            // 8 float4 loads of E and Rel in flight per thread before the stores
+            for (int kq0 = 0; kq0 < nq; kq0 += 8) {
+                float4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int kq = kq0 + u, k = kq * 4;
+                    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (valid && kq < nq) {
+                        if (vec4 && k < p.d) {
+                            const float4 a = __ldg(reinterpret_cast<const float4*>(e + k));
+                            const float4 b = __ldg(reinterpret_cast<const float4*>(rr + k));
+                            v[u] = make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                                               __fadd_rn(a.w, b.w));
+                        } else {
+                            float* vv = reinterpret_cast<float*>(&v[u]);
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                if (k + c < p.d) vv[c] = __fadd_rn(__ldg(e + k + c), __ldg(rr + k + c));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int kq = kq0 + u;
+                    if (kq < nq) {
+                        const float* vv = reinterpret_cast<const float*>(&v[u]);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const float rd = vv[c] - __uint_as_float(__float_as_uint(vv[c]) & 0xFFFFE000u);  // exact
+                            s2 = fmaf(vv[c], vv[c], s2);
+                            sd2 = fmaf(rd, rd, sd2);
+                        }
+                        *reinterpret_cast<float4*>(A + ((size_t)kq * (BM / 8) + (i >> 3)) * 32 + (i & 7) * 4) = v[u];
+                    }
+                }
+            }
+            const float gam = 1.0f + (float)(Kpad + 4) * 1.1920928955078125e-07f;
+            qrow[ai * BM + i] = valid ? make_float4(s2, __fsqrt_ru(__fmul_ru(s2, gam)), __fsqrt_ru(__fmul_ru(sd2, gam)), 0.f)
+                                      : make_float4(3e38f, 0.f, 0.f, 0.f);
+            fence_proxy_async_smem();  // generic-proxy smem writes -> visible to tcgen05.mma
+            mbar_arrive(&a_full[ai]);
+            if (++ai == a_stages) { ai = 0; aph ^= 1; }
+        }
+    }
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
 }
+
+#ifdef KGC_PROF_TC
+}  // namespace kgc
+extern "C" __attribute__((visibility("default"))) void kgc_debug_tc_prof(unsigned long long* out16, int reset) {
+    if (out16) cudaMemcpyFromSymbol(out16, kgc::g_tc_prof, 16 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(kgc::g_tc_prof, z, sizeof z);
+    }
+}
+namespace kgc {
+#endif
 
 void launch_tiles_tc(const TileParams& p, int num_sms, cudaStream_t s) {
     if (p.n_items <= 0) return;
