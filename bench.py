@@ -198,7 +198,8 @@ def run_ours(args, cfg, thresholds):
         E_h, Rel_h = Et.cpu().numpy(), Rt.cpu().numpy()
     torch.cuda.synchronize()
 
-    joins = {n: kgc.Join(device=local, rank=rank, world=world, stream=stream.cuda_stream) for n in args.norms}
+    joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, stream=stream.cuda_stream)
+             for n in args.norms}
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     counts = torch.zeros(len(args.norms), dtype=torch.int64, device=dev)
 
@@ -288,8 +289,8 @@ def run_ours(args, cfg, thresholds):
         R_pin = torch.from_numpy(Rel_h).pin_memory()
         out_pin = {n: torch.empty((max(1, stats_last[n]["results"]) * 2, 4), dtype=torch.int32).pin_memory()
                    for n in args.norms}
-        e2e_joins = {n: kgc.Join(device=local, rank=rank, world=world, stream=stream.cuda_stream)
-                     for n in args.norms}
+        e2e_joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots,
+                                 stream=stream.cuda_stream) for n in args.norms}
         h2d = d2h = 0
 
         def e2e_step():
@@ -357,6 +358,7 @@ def run_ours(args, cfg, thresholds):
             "data": "synthetic",
             "config": {"workload": wl, "N": N, "R": R, "d": d, "norms": args.norms, "eps": eps, "hit_rate": args.hit,
                        "parallelism": f"query-tile shards x{world}, tails replicated",
+                       "pivots": args.pivots,
                        "l2_cache": "flushed (512 MiB write) before every timed step, outside the timed events"},
             "result_triplets_per_step": results_total,
             "result_triplets_per_s": results_total / (ms_per_step / 1e3),
@@ -386,6 +388,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=256, help="(h,r) rows per reference step")
+    ap.add_argument("--pivots", type=int, default=1, help="1 = the paper's single pivot; 2..8 = multi-pivot pruning")
     args = ap.parse_args()
     args.norms = [int(x) for x in args.norms.split(",")]
     cfg = CONFIGS[args.config]

@@ -76,7 +76,9 @@ typedef struct {
     int32_t pivot;            /* 0 = zero vector (default); 1 = mean of the tails      */
     int32_t l2_engine;        /* 0 = auto (= 1); 1 = tcgen05 TF32 filter; 2 = FP32 SIMT filter      */
     int32_t chunk_tiles;      /* max tail tiles per work item (load-balance granularity); 0 = auto */
-    int32_t reserved;
+    int32_t pivots;           /* 0/1 = one pivot (default); 2..8 = multi-pivot tile     */
+                              /* pruning (L_inf over K pivot distances; needs d <= 256, */
+                              /* prune = 1; otherwise one pivot is used)                           */
     int64_t result_capacity;  /* initial result-buffer capacity in triplets; 0 = auto (grows)       */
     void*   stream;           /* cudaStream_t to run on; NULL = a stream the context creates       */
 } kgc_options;
@@ -103,10 +105,12 @@ typedef struct {
     int32_t reruns;               /* capacity-overflow reruns                                      */
     /* device time per phase (CUDA events on the context's stream), milliseconds */
     float ms_total, ms_h2d, ms_keys, ms_sort, ms_ranges, ms_stage, ms_tiles, ms_recheck;
+    int32_t pivots_used;          /* 1, or K of the multi-pivot pruning                            */
+    int32_t reserved;
 } kgc_stats_t;
 
 /* Fill *opt with defaults: device -1, rank 0, world 1, prune 1, pivot 0,
- * l2_engine 0, chunk_tiles 0, result_capacity 0, stream NULL. */
+ * l2_engine 0, chunk_tiles 0, pivots 1, result_capacity 0, stream NULL. */
 void kgc_default_options(kgc_options* opt);
 
 /* Create a context.  opt == NULL means defaults.  Returns KGC_ENODEV when no
@@ -151,14 +155,19 @@ void kgc_destroy(kgc_ctx* ctx);
  *   KGC_INSPECT_TAIL_PERM   int32[N]     sorted position -> tail index (K2)
  *   KGC_INSPECT_QUERY_PERM  int32[R*N]   per relation, sorted position -> head (K2)
  *   KGC_INSPECT_TILE_RANGES int32[R*QT*2] surviving tail-tile range [sb, eb] per query tile (K3)
- *   KGC_INSPECT_QUERY_COST  int64[R*QT]  exclusive prefix of surviving tiles per query tile (K3)  */
+ *   KGC_INSPECT_QUERY_COST  int64[R*QT]  exclusive prefix of surviving tiles per query tile (K3)
+ *   KGC_INSPECT_TILE_LIST   int32[mine]  multi-pivot: this shard's surviving tail tiles, query tile by
+ *                                        query tile (offset of tile q = cost prefix[q] - prefix[first])
+ * With multi-pivot pruning (pivots_used = K > 1) the key arrays hold K floats
+ * per row: TAIL_KEYS float[N][K], QUERY_KEYS float[R][N][K]. */
 enum {
     KGC_INSPECT_TAIL_KEYS = 1,
     KGC_INSPECT_QUERY_KEYS = 2,
     KGC_INSPECT_TAIL_PERM = 3,
     KGC_INSPECT_QUERY_PERM = 4,
     KGC_INSPECT_TILE_RANGES = 5,
-    KGC_INSPECT_QUERY_COST = 6
+    KGC_INSPECT_QUERY_COST = 6,
+    KGC_INSPECT_TILE_LIST = 7
 };
 int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes);
 

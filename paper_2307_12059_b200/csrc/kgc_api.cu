@@ -43,7 +43,7 @@ struct kgc_ctx {
     std::string err;
     DevBuf E, Rel, pivot, kt, kq, mm_t, mm_q, sk0, sv0, sk1, sv1, counts, scan_tmp, qperm, qskey, tperm, tskey, tmin,
         tmax, cmax, cmin, ranges, cost, cum, nitem, item_off, items, item_tiles, item_cum, Qp, qs, Tp, T2, tstile, cand,
-        res, ctr;
+        res, ctr, mpP, mpkt, mpkq, mpmm_t, mpmm_q, mpc0, mpc1, tbmin, tbmax, qbmin, qbmax, tile_list;
     long long cand_cap = 0, res_cap = 0;
     long long n_results = -1;
     kgc_stats_t st{};
@@ -52,6 +52,8 @@ struct kgc_ctx {
     // geometry of the last join (for kgc_inspect)
     long long N = 0, R = 0;
     int QT = 0, TT = 0, BN = 0;
+    int K = 1;                  // pivots used by the last join
+    long long list_len = 0;     // multi-pivot tile-list length of this shard
     bool have_join = false;
 };
 
@@ -101,6 +103,9 @@ static T* P(DevBuf& b) {
     return reinterpret_cast<T*>(b.p);
 }
 
+// Relative margin covering the FP32 pivot keys.
+static float mp_relm(int d) { return (float)(d + 8) * 1.1920928955078125e-07f; }
+
 static bool is_device_ptr(const void* p, int device) {
     if (!p) return false;
     cudaPointerAttributes a;
@@ -125,6 +130,7 @@ void kgc_default_options(kgc_options* o) {
     o->pivot = 0;
     o->l2_engine = 0;
     o->chunk_tiles = 0;
+    o->pivots = 1;
     o->result_capacity = 0;
     o->stream = nullptr;
 }
@@ -135,7 +141,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 2 || o.chunk_tiles < 0 || o.result_capacity < 0) {
+        o.l2_engine > 2 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -192,7 +198,8 @@ void kgc_destroy(kgc_ctx* ctx) {
                       &ctx->qperm, &ctx->qskey,  &ctx->tperm,  &ctx->tskey, &ctx->tmin,   &ctx->tmax,   &ctx->cmax,
                       &ctx->cmin,  &ctx->ranges, &ctx->cost,   &ctx->cum,   &ctx->nitem,  &ctx->item_off,
                       &ctx->items, &ctx->item_tiles, &ctx->item_cum, &ctx->Qp,     &ctx->qs,     &ctx->Tp,    &ctx->T2,     &ctx->tstile, &ctx->cand,
-                      &ctx->res,   &ctx->ctr};
+                      &ctx->res,   &ctx->ctr,  &ctx->mpP,   &ctx->mpkt,  &ctx->mpkq,  &ctx->mpmm_t, &ctx->mpmm_q,
+                      &ctx->mpc0,  &ctx->mpc1, &ctx->tbmin, &ctx->tbmax, &ctx->qbmin, &ctx->qbmax, &ctx->tile_list};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& e : ctx->ev)
@@ -344,35 +351,93 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         LAUNCHED(1);
         pivot = P<double>(ctx->pivot);
     }
-    // ---- a2: K1 keys
-    launch_tail_keys(E, N, d, norm, pivot, P<float>(ctx->kt), P<unsigned>(ctx->mm_t), &dctr->nonfinite, s);
-    LAUNCHED(2);
-    launch_query_keys(E, Rel, N, R, d, norm, pivot, P<float>(ctx->kq), P<unsigned>(ctx->mm_q), &dctr->nonfinite, s);
-    LAUNCHED(2);
-    CK(cudaEventRecord(ctx->ev[EV_KEYS], s));
-    // ---- a3: K2 sorts (tails once, queries per relation)
-    radix_sort_segments(P<float>(ctx->kt), P<unsigned>(ctx->mm_t), 1, N, P<unsigned>(ctx->sk0), P<unsigned>(ctx->sv0),
-                        P<unsigned>(ctx->sk1), P<unsigned>(ctx->sv1), P<int>(ctx->counts), P<int>(ctx->tperm),
-                        P<float>(ctx->tskey), ctx->scan_tmp.p, ctx->scan_tmp.n, s, &ctx->launches);
-    LAUNCHED(0);
-    radix_sort_segments(P<float>(ctx->kq), P<unsigned>(ctx->mm_q), R, N, P<unsigned>(ctx->sk0), P<unsigned>(ctx->sv0),
-                        P<unsigned>(ctx->sk1), P<unsigned>(ctx->sv1), P<int>(ctx->counts), P<int>(ctx->qperm),
-                        P<float>(ctx->qskey), ctx->scan_tmp.p, ctx->scan_tmp.n, s, &ctx->launches);
-    LAUNCHED(0);
-    CK(cudaEventRecord(ctx->ev[EV_SORT], s));
-    // ---- a4: K3 tile ranges, shard split, work items
-    launch_tail_tile_bounds(P<float>(ctx->tskey), N, BN, TT, P<float>(ctx->tmin), P<float>(ctx->tmax),
-                            P<float>(ctx->cmax), P<float>(ctx->cmin), s, &ctx->launches);
-    LAUNCHED(0);
-    launch_query_ranges(P<float>(ctx->qskey), N, R, QT, TT, P<float>(ctx->cmax), P<float>(ctx->cmin), eps,
-                        ctx->opt.prune, P<int2>(ctx->ranges), P<long long>(ctx->cost), s);
-    LAUNCHED(1);
+    const int K = (ctx->opt.pivots >= 2 && ctx->opt.prune && d <= MP_MAX_DIM) ? ctx->opt.pivots : 1;
+    ctx->K = K;
+    st.pivots_used = K;
+    if (K == 1) {
+        // ---- a2: K1 keys (one pivot, FP64 -> float)
+        launch_tail_keys(E, N, d, norm, pivot, P<float>(ctx->kt), P<unsigned>(ctx->mm_t), &dctr->nonfinite, s);
+        LAUNCHED(2);
+        launch_query_keys(E, Rel, N, R, d, norm, pivot, P<float>(ctx->kq), P<unsigned>(ctx->mm_q), &dctr->nonfinite,
+                          s);
+        LAUNCHED(2);
+        CK(cudaEventRecord(ctx->ev[EV_KEYS], s));
+        // ---- a3: K2 sorts (tails once, queries per relation)
+        radix_sort_segments(P<float>(ctx->kt), P<unsigned>(ctx->mm_t), 1, N, P<unsigned>(ctx->sk0),
+                            P<unsigned>(ctx->sv0), P<unsigned>(ctx->sk1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
+                            P<int>(ctx->tperm), P<float>(ctx->tskey), ctx->scan_tmp.p, ctx->scan_tmp.n, s,
+                            &ctx->launches);
+        LAUNCHED(0);
+        radix_sort_segments(P<float>(ctx->kq), P<unsigned>(ctx->mm_q), R, N, P<unsigned>(ctx->sk0),
+                            P<unsigned>(ctx->sv0), P<unsigned>(ctx->sk1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
+                            P<int>(ctx->qperm), P<float>(ctx->qskey), ctx->scan_tmp.p, ctx->scan_tmp.n, s,
+                            &ctx->launches);
+        LAUNCHED(0);
+        CK(cudaEventRecord(ctx->ev[EV_SORT], s));
+        // ---- a4: K3 tile ranges (Lemma 1 + 2 at tile granularity)
+        launch_tail_tile_bounds(P<float>(ctx->tskey), N, BN, TT, P<float>(ctx->tmin), P<float>(ctx->tmax),
+                                P<float>(ctx->cmax), P<float>(ctx->cmin), s, &ctx->launches);
+        LAUNCHED(0);
+        launch_query_ranges(P<float>(ctx->qskey), N, R, QT, TT, P<float>(ctx->cmax), P<float>(ctx->cmin), eps,
+                            ctx->opt.prune, P<int2>(ctx->ranges), P<long long>(ctx->cost), s);
+        LAUNCHED(1);
+    } else {
+        // ---- a2: K pivot distances per row (FP32)
+        CK(ensure(ctx->mpP, (size_t)K * d * 4));
+        CK(ensure(ctx->mpkt, (size_t)N * K * 4));
+        CK(ensure(ctx->mpkq, NR * K * 4));
+        CK(ensure(ctx->mpmm_t, (size_t)K * 8));
+        CK(ensure(ctx->mpmm_q, (size_t)R * K * 8));
+        CK(ensure(ctx->mpc0, nsort * 8));
+        CK(ensure(ctx->mpc1, nsort * 8));
+        CK(ensure(ctx->tbmin, (size_t)TT * K * 4));
+        CK(ensure(ctx->tbmax, (size_t)TT * K * 4));
+        CK(ensure(ctx->qbmin, (size_t)nq * K * 4));
+        CK(ensure(ctx->qbmax, (size_t)nq * K * 4));
+        launch_pick_pivots(E, N, d, norm, K, pivot, P<float>(ctx->mpP), s);
+        LAUNCHED(1);
+        launch_mp_keys(E, nullptr, N, 1, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkt), P<unsigned>(ctx->mpmm_t),
+                       &dctr->nonfinite, s);
+        LAUNCHED(2);
+        launch_mp_keys(E, Rel, N, R, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q),
+                       &dctr->nonfinite, s);
+        LAUNCHED(2);
+        CK(cudaEventRecord(ctx->ev[EV_KEYS], s));
+        // ---- a3: Morton-order sorts (tiles compact in pivot space)
+        const int bits = 64 / K;
+        launch_mp_morton(P<float>(ctx->mpkt), P<unsigned>(ctx->mpmm_t), 1, N, K, bits,
+                         P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
+        LAUNCHED(1);
+        radix_sort_u64_segments(1, N, K * bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
+                                P<unsigned long long>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
+                                ctx->scan_tmp.p, s, &ctx->launches);
+        LAUNCHED(0);
+        CK(cudaMemcpyAsync(ctx->tperm.p, ctx->sv0.p, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
+        launch_mp_morton(P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q), R, N, K, bits,
+                         P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
+        LAUNCHED(1);
+        radix_sort_u64_segments(R, N, K * bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
+                                P<unsigned long long>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
+                                ctx->scan_tmp.p, s, &ctx->launches);
+        LAUNCHED(0);
+        CK(cudaMemcpyAsync(ctx->qperm.p, ctx->sv0.p, NR * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaEventRecord(ctx->ev[EV_SORT], s));
+        // ---- a4: K-dim tile boxes and the L_inf test of every tile pair
+        launch_mp_boxes(P<float>(ctx->mpkt), P<unsigned>(ctx->tperm), 1, N, BN, TT, K, P<float>(ctx->tbmin),
+                        P<float>(ctx->tbmax), s);
+        launch_mp_boxes(P<float>(ctx->mpkq), P<unsigned>(ctx->qperm), R, N, BM, QT, K, P<float>(ctx->qbmin),
+                        P<float>(ctx->qbmax), s);
+        LAUNCHED(2);
+        launch_mp_count(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tbmin), P<float>(ctx->tbmax), nq, TT,
+                        K, eps, mp_relm(d), 1, P<int2>(ctx->ranges), P<long long>(ctx->cost), s);
+        LAUNCHED(1);
+    }
     scan_exclusive_i64(P<long long>(ctx->cost), P<long long>(ctx->cum), (size_t)nq, &dctr->total_cost,
                        ctx->scan_tmp.p, s, &ctx->launches);
     LAUNCHED(0);
     launch_shard_items(P<int2>(ctx->ranges), P<long long>(ctx->cost), P<long long>(ctx->cum), nq, ctx->opt.rank,
                        ctx->opt.world, chunk, dctr, P<int>(ctx->nitem), P<int>(ctx->item_off), nullptr, nullptr,
-                       ctx->scan_tmp.p, s, &ctx->launches, 0);
+                       ctx->scan_tmp.p, s, &ctx->launches, 0, 0);
     LAUNCHED(0);
     // sync #1: plan totals
     struct {
@@ -393,6 +458,14 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     st.work_items_mine = n_items;
     const int tq0 = h1.c.tq_begin == INT_MAX ? 0 : h1.c.tq_begin;
     const int tq1 = h1.c.tq_begin == INT_MAX ? 0 : h1.c.tq_end;
+    ctx->list_len = 0;
+    if (n_items > 0 && K > 1) {
+        ctx->list_len = h1.c.my_cost;
+        CK(ensure(ctx->tile_list, (size_t)h1.c.my_cost * 4 + 4));
+        launch_mp_emit(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tbmin), P<float>(ctx->tbmax),
+                       P<long long>(ctx->cum), dctr, nq, TT, K, eps, mp_relm(d), 1, P<int>(ctx->tile_list), s);
+        LAUNCHED(1);
+    }
     if (n_items > 0) {
         CK(ensure(ctx->items, (size_t)n_items * 16));
         CK(ensure(ctx->item_tiles, (size_t)n_items * 8));
@@ -400,7 +473,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(ensure(ctx->scan_tmp, scan_tmp_bytes((size_t)n_items)));
         launch_shard_items(P<int2>(ctx->ranges), P<long long>(ctx->cost), P<long long>(ctx->cum), nq, ctx->opt.rank,
                            ctx->opt.world, chunk, dctr, P<int>(ctx->nitem), P<int>(ctx->item_off),
-                           P<int4>(ctx->items), P<long long>(ctx->item_tiles), ctx->scan_tmp.p, s, &ctx->launches, 1);
+                           P<int4>(ctx->items), P<long long>(ctx->item_tiles), ctx->scan_tmp.p, s, &ctx->launches, 1,
+                           K > 1 ? 1 : 0);
         LAUNCHED(0);
         scan_exclusive_i64(P<long long>(ctx->item_tiles), P<long long>(ctx->item_cum), (size_t)n_items, nullptr,
                            ctx->scan_tmp.p, s, &ctx->launches);
@@ -442,6 +516,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.T2 = P<float>(ctx->T2);
         tp.tstile = P<float2>(ctx->tstile);
         tp.items = P<int4>(ctx->items);
+        tp.tile_list = P<int>(ctx->tile_list);
         tp.n_items = n_items;
         tp.item_cum = P<long long>(ctx->item_cum);
         tp.total_tiles = h1.c.my_cost;
@@ -591,8 +666,9 @@ extern "C" int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t by
     const void* src = nullptr;
     int64_t n = 0;
     switch (what) {
-        case KGC_INSPECT_TAIL_KEYS: src = ctx->kt.p; n = ctx->N * 4; break;
-        case KGC_INSPECT_QUERY_KEYS: src = ctx->kq.p; n = ctx->N * ctx->R * 4; break;
+        case KGC_INSPECT_TAIL_KEYS: src = ctx->K > 1 ? ctx->mpkt.p : ctx->kt.p; n = ctx->N * 4 * ctx->K; break;
+        case KGC_INSPECT_QUERY_KEYS: src = ctx->K > 1 ? ctx->mpkq.p : ctx->kq.p; n = ctx->N * ctx->R * 4 * ctx->K; break;
+        case KGC_INSPECT_TILE_LIST: src = ctx->tile_list.p; n = ctx->list_len * 4; break;
         case KGC_INSPECT_TAIL_PERM: src = ctx->tperm.p; n = ctx->N * 4; break;
         case KGC_INSPECT_QUERY_PERM: src = ctx->qperm.p; n = ctx->N * ctx->R * 4; break;
         case KGC_INSPECT_TILE_RANGES: src = ctx->ranges.p; n = ctx->R * (int64_t)ctx->QT * 8; break;

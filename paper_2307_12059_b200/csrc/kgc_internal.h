@@ -11,6 +11,9 @@ constexpr int BN_TC = 256;       // tail rows per tile, tensor-core engine (UMMA
 constexpr int BN_SIMT = 128;     // tail rows per tile, SIMT engines
 constexpr int SORT_IPB = 2048;   // radix-sort items per block (256 threads x 8)
 constexpr int TC_MAX_KPAD = 256; // tensor-core engine supports d <= 256
+constexpr int MP_MAX = 8;        // multi-pivot pruning: at most 8 pivots
+constexpr int MP_SAMPLE = 4096;  // tails sampled for the farthest-point pivot choice
+constexpr int MP_MAX_DIM = 256;  // multi-pivot pruning supports d <= 256
 
 // Counters block in device memory (zeroed per join).
 struct DevCounters {
@@ -30,7 +33,8 @@ struct TileParams {
     const float* Tp;        // staged tail tiles
     const float* T2;        // per staged tail row ||t||^2 (3e38 for padding rows)
     const float2* tstile;   // per tail tile {max ||t||, max ||t - tf32(t)||}
-    const int4* items;      // {tq, j0, j1, 0}
+    const int4* items;      // {tq, j0, j1, list_off}: tiles j0..j1 (list_off < 0) or list[list_off + j0..j1]
+    const int* tile_list;   // multi-pivot surviving tail tiles of this shard
     long long n_items;
     const long long* item_cum;  // exclusive prefix of item tile counts (cost-balanced CTA ranges)
     long long total_tiles;
@@ -74,12 +78,36 @@ void launch_query_ranges(const float* qskey, long long N, long long R, int QT, i
                          cudaStream_t s);
 void launch_shard_items(const int2* ranges, const long long* cost, const long long* cum, long long nq,
                         int rank, int world, int chunk, DevCounters* ctr, int* nitem, int* item_off,
-                        int4* items, long long* item_tiles, void* tmp, cudaStream_t s, int* launches, int phase);
+                        int4* items, long long* item_tiles, void* tmp, cudaStream_t s, int* launches, int phase,
+                        int list_mode);
 void launch_stage_tails(const float* E, const int* tperm, long long N, int d, int Kpad, int BN, int TT,
                         int tc_layout, float* Tp, float* T2, float2* tstile, cudaStream_t s);
 void launch_stage_queries(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad,
                           int QT, int tq0, int tq1, int tc_layout, int norm, float theta, float* Qp,
                           float4* qs, cudaStream_t s);
+
+// ---- multi-pivot pruning (pivots.cu) ----
+void radix_sort_u64_segments(long long S, long long L, int bits, unsigned long long* k0, unsigned int* v0,
+                             unsigned long long* k1, unsigned int* v1, int* counts, void* scan_tmp, cudaStream_t s,
+                             int* launches);
+void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, const double* p0, float* P,
+                        cudaStream_t s);
+void launch_mp_keys(const float* E, const float* Rel, long long N, long long nseg, int d, int norm, int K,
+                    const float* P, float* keys, unsigned int* minmax, unsigned int* nonfinite, cudaStream_t s);
+void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
+                      unsigned long long* code, unsigned int* idx, cudaStream_t s);
+void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg, long long L, int ROWS, int ntile,
+                     int K, float* bmin, float* bmax, cudaStream_t s);
+void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,
+                     int TT, int K, float theta, float relm, int prune, int2* ranges, long long* cost, cudaStream_t s);
+void launch_mp_emit(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax,
+                    const long long* cum, const DevCounters* ctr, long long nq, int TT, int K, float theta, float relm,
+                    int prune, int* list, cudaStream_t s);
+
+// Tail tile of position j of item w (contiguous range or multi-pivot list).
+__device__ __forceinline__ int item_tile(const int4& w, int j, const int* __restrict__ list) {
+    return w.w < 0 ? j : __ldg(list + w.w + j);
+}
 
 // ---- tile engines ----
 int  tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);

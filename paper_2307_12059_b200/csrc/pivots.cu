@@ -1,0 +1,340 @@
+// pivots.cu -- multi-pivot tile pruning ("tighter tile
+// bounds"): K pivots instead of one.  Lemma 1 holds for
+// every pivot, so a (query, tail) pair can be a hit only if
+// |d(p_k, q) - d(p_k, t)| <= theta for ALL k -- the L_inf bound over pivot
+// distances of Chen et al. that the paper cites.  At tile
+// granularity: a tile pair survives iff, for every pivot, the key intervals of
+// the two tiles are within theta of each other.
+//
+// Pieces (all on the device, deterministic):
+//   pick_pivots   p_0 = zero (or mean) vector, p_1..p_{K-1} = farthest-point
+//                 traversal over a fixed sample of tails (a heuristic: it only
+//                 decides how much is pruned, never what is returned)
+//   mp_keys       d(p_k, x) for every query q = fl32(h + r) and tail, FP32
+//                 (relative error <= (d + 4) 2^-24, covered by the test margin)
+//   mp_morton     64-bit Morton code of the K quantised keys, so that the
+//                 radix-sorted tiles are compact in pivot space
+//   mp_boxes      per tile and pivot: [min, max] of its rows' keys
+//   mp_count / mp_emit  per query tile: count, then list, the surviving tail tiles
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace kgc {
+
+static inline unsigned grid_for_mp(long long n, int threads, long long cap = 148LL * 64) {
+    long long g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+// --------------------------------------------------------------- pivots
+template <int NORM>
+__device__ __forceinline__ float dist_f32(const float* __restrict__ a, const float* __restrict__ b, int d) {
+    float s = 0.f;
+    for (int k = 0; k < d; ++k) {
+        const float x = a[k] - b[k];
+        s = NORM == 1 ? s + fabsf(x) : fmaf(x, x, s);
+    }
+    return s;  // squared for L2 (monotone: fine for argmax)
+}
+
+template <int NORM>
+__global__ void __launch_bounds__(1024) pick_pivots_kernel(const float* __restrict__ E, long long N, int d, int K,
+                                                           const double* __restrict__ p0, float* __restrict__ P) {
+    __shared__ float mind[MP_SAMPLE];
+    __shared__ float bv[32];
+    __shared__ int bi[32];
+    __shared__ int chosen;
+    const int S = (int)(N < MP_SAMPLE ? N : MP_SAMPLE);
+    for (int k = threadIdx.x; k < d; k += blockDim.x) P[k] = p0 ? (float)p0[k] : 0.f;
+    __syncthreads();
+    for (int s = threadIdx.x; s < S; s += blockDim.x) {
+        const long long row = (long long)s * N / S;
+        mind[s] = dist_f32<NORM>(E + row * d, P, d);
+    }
+    __syncthreads();
+    for (int kk = 1; kk < K; ++kk) {
+        float best = -1.f;
+        int besti = 0;
+        for (int s = threadIdx.x; s < S; s += blockDim.x)
+            if (mind[s] > best) { best = mind[s]; besti = s; }
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+            if (ov > best || (ov == best && oi < besti)) { best = ov; besti = oi; }
+        }
+        if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = best; bi[threadIdx.x >> 5] = besti; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float b = -1.f;
+            int ix = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+                if (bv[w] > b || (bv[w] == b && bi[w] < ix)) { b = bv[w]; ix = bi[w]; }
+            chosen = ix;
+        }
+        __syncthreads();
+        const long long row = (long long)chosen * N / S;
+        float* pk = P + (size_t)kk * d;
+        for (int k = threadIdx.x; k < d; k += blockDim.x) pk[k] = E[row * d + k];
+        __syncthreads();
+        for (int s = threadIdx.x; s < S; s += blockDim.x) {
+            const long long r2 = (long long)s * N / S;
+            mind[s] = fminf(mind[s], dist_f32<NORM>(E + r2 * d, pk, d));
+        }
+        __syncthreads();
+    }
+}
+
+// ----------------------------------------------------------------- keys
+// QUERY: block = 32 entities x 16 relations (warp w: relations w, w + 8);
+// tails: block = 128 threads = 128 entities (warp w: entities w*32 + lane), one segment.
+template <int NORM, bool QUERY>
+__global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
+                                                      long long N, long long nseg, int d, int K,
+                                                      const float* __restrict__ P, float* __restrict__ keys,
+                                                      unsigned int* minmax, unsigned int* nonfinite) {
+    extern __shared__ float mk_smem[];
+    const int S = (d & 1) ? d : d + 1;
+    constexpr int ENT = QUERY ? 32 : 128;
+    float* Es = mk_smem;                                   // [ENT][S]
+    float* Ps = Es + ENT * S;                              // [K][d]
+    float* Rs = Ps + K * d;                                // [16][d] (queries)
+    const long long h0 = (long long)blockIdx.x * ENT;
+    const long long r0 = QUERY ? (long long)blockIdx.y * 16 : 0;
+    bool bad = false;
+    for (int x = threadIdx.x; x < ENT * d; x += blockDim.x) {
+        const int i = x / d, k = x % d;
+        const float v = (h0 + i < N) ? E[(h0 + i) * d + k] : 0.f;
+        if (!QUERY) bad |= !isfinite(v);
+        Es[i * S + k] = v;
+    }
+    for (int x = threadIdx.x; x < K * d; x += blockDim.x) Ps[x] = P[x];
+    if (QUERY) {
+        for (int x = threadIdx.x; x < 16 * d; x += blockDim.x) {
+            const int i = x / d, k = x % d;
+            const float v = (r0 + i < nseg) ? Rel[(r0 + i) * d + k] : 0.f;
+            bad |= !isfinite(v);
+            Rs[i * d + k] = v;
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int rl = QUERY ? w : 0; rl < (QUERY ? 16 : 1); rl += 8) {
+        const long long r = r0 + rl;
+        if (QUERY && r >= nseg) break;
+        const int eloc = QUERY ? lane : w * 32 + lane;
+        const long long h = h0 + eloc;
+        const float* es = Es + eloc * S;
+        const float* rs = QUERY ? Rs + rl * d : nullptr;
+        float acc[MP_MAX];
+#pragma unroll
+        for (int k = 0; k < MP_MAX; ++k) acc[k] = 0.f;
+        for (int dd = 0; dd < d; ++dd) {
+            const float q = QUERY ? __fadd_rn(es[dd], rs[dd]) : es[dd];  // connector_1(h, r) = h + r
+#pragma unroll
+            for (int k = 0; k < MP_MAX; ++k) {
+                if (k < K) {
+                    const float x = q - Ps[k * d + dd];
+                    acc[k] = NORM == 1 ? acc[k] + fabsf(x) : fmaf(x, x, acc[k]);
+                }
+            }
+        }
+        const bool valid = h < N;
+#pragma unroll
+        for (int k = 0; k < MP_MAX; ++k) {
+            if (k < K) {
+                const float key = NORM == 2 ? sqrtf(acc[k]) : acc[k];
+                if (valid) keys[((size_t)r * N + h) * K + k] = key;
+                float mn = valid ? key : FLT_MAX, mx = valid ? key : 0.f;
+                for (int o = 16; o > 0; o >>= 1) {
+                    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                }
+                if (lane == 0) {
+                    atomicMin(&minmax[((size_t)r * K + k) * 2], __float_as_uint(mn));
+                    atomicMax(&minmax[((size_t)r * K + k) * 2 + 1], __float_as_uint(mx));
+                }
+            }
+        }
+    }
+}
+
+__global__ void mp_init_minmax_kernel(unsigned int* mm, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        mm[2 * i] = __float_as_uint(FLT_MAX);
+        mm[2 * i + 1] = 0u;
+    }
+}
+
+// -------------------------------------------------------------- Morton
+__global__ void mp_morton_kernel(const float* __restrict__ keys, const unsigned int* __restrict__ minmax, long long nseg,
+                                 long long L, int K, int bits, unsigned long long* __restrict__ code,
+                                 unsigned int* __restrict__ idx) {
+    const long long n = nseg * L;
+    const float scale_max = (float)((1u << bits) - 1);
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+        const long long s = t / L, i = t - s * L;
+        unsigned q[MP_MAX];
+#pragma unroll
+        for (int k = 0; k < MP_MAX; ++k) {
+            q[k] = 0;
+            if (k < K) {
+                const float lo = __uint_as_float(minmax[(s * K + k) * 2]);
+                const float hi = __uint_as_float(minmax[(s * K + k) * 2 + 1]);
+                const float rg = hi - lo;
+                if (rg > 0.f) {
+                    float x = (keys[t * K + k] - lo) / rg * scale_max;
+                    x = fminf(fmaxf(x, 0.f), scale_max);
+                    q[k] = (unsigned)x;
+                }
+            }
+        }
+        unsigned long long c = 0;
+        for (int b = bits - 1; b >= 0; --b)
+#pragma unroll
+            for (int k = 0; k < MP_MAX; ++k)
+                if (k < K) c = (c << 1) | ((q[k] >> b) & 1u);
+        code[t] = c;
+        idx[t] = (unsigned)i;
+    }
+}
+
+// --------------------------------------------------------------- boxes
+// One warp per tile: [min, max] per pivot of the keys of its (sorted) rows.
+__global__ void mp_boxes_kernel(const float* __restrict__ keys, const unsigned int* __restrict__ perm, long long nseg,
+                                long long L, int ROWS, int ntile, int K, float* __restrict__ bmin,
+                                float* __restrict__ bmax) {
+    const int lane = threadIdx.x & 31;
+    const long long nt = nseg * ntile;
+    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < nt;
+         w += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const long long s = w / ntile, tl = w - s * ntile;
+        const long long b = tl * ROWS, e = min(L, b + ROWS);
+        float mn[MP_MAX], mx[MP_MAX];
+#pragma unroll
+        for (int k = 0; k < MP_MAX; ++k) { mn[k] = FLT_MAX; mx[k] = -FLT_MAX; }
+        for (long long i = b + lane; i < e; i += 32) {
+            const float* kr = keys + ((size_t)s * L + perm[s * L + i]) * K;
+#pragma unroll
+            for (int k = 0; k < MP_MAX; ++k)
+                if (k < K) { mn[k] = fminf(mn[k], kr[k]); mx[k] = fmaxf(mx[k], kr[k]); }
+        }
+#pragma unroll
+        for (int k = 0; k < MP_MAX; ++k) {
+            if (k < K) {
+                float a = mn[k], z = mx[k];
+                for (int o = 16; o > 0; o >>= 1) {
+                    a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+                    z = fmaxf(z, __shfl_xor_sync(0xffffffffu, z, o));
+                }
+                if (lane == 0) { bmin[w * K + k] = a; bmax[w * K + k] = z; }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------ test and lists
+// Tile pair survives iff for every pivot k the intervals are within th_k,
+// th_k = theta (1 + 2^-14) + relm (|qmax_k| + |tmax_k|), relm covering the
+// FP32 key error.
+__device__ __forceinline__ bool mp_survives(const float* qmn, const float* qmx, const float* __restrict__ tmn,
+                                            const float* __restrict__ tmx, int K, float theta, float relm) {
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < MP_MAX; ++k) {
+        if (k < K) {
+            const float th = theta * (1.0f + 6.103515625e-05f) + relm * (fabsf(qmx[k]) + fabsf(tmx[k]));
+            ok &= !(tmx[k] < qmn[k] - th || tmn[k] > qmx[k] + th);
+        }
+    }
+    return ok;
+}
+
+__global__ void mp_count_kernel(const float* __restrict__ qbmin, const float* __restrict__ qbmax,
+                                const float* __restrict__ tbmin, const float* __restrict__ tbmax, long long nq, int TT,
+                                int K, float theta, float relm, int prune, int2* ranges, long long* cost) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq; q += (long long)gridDim.x * blockDim.x) {
+        float qmn[MP_MAX], qmx[MP_MAX];
+#pragma unroll
+        for (int k = 0; k < MP_MAX; ++k)
+            if (k < K) { qmn[k] = qbmin[q * K + k]; qmx[k] = qbmax[q * K + k]; }
+        int c = 0;
+        if (prune) {
+            for (int j = 0; j < TT; ++j) c += mp_survives(qmn, qmx, tbmin + (size_t)j * K, tbmax + (size_t)j * K, K, theta, relm);
+        } else {
+            c = TT;
+        }
+        ranges[q] = make_int2(0, c - 1);  // positions in this query tile's list
+        cost[q] = c;
+    }
+}
+
+__global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __restrict__ qbmax,
+                               const float* __restrict__ tbmin, const float* __restrict__ tbmax,
+                               const long long* __restrict__ cum, const DevCounters* ctr, int TT, int K, float theta,
+                               float relm, int prune, int* __restrict__ list) {
+    const int tq0 = ctr->tq_begin, tq1 = ctr->tq_end;
+    if (tq0 >= tq1) return;
+    const long long base = cum[tq0];
+    for (long long q = tq0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < tq1;
+         q += (long long)gridDim.x * blockDim.x) {
+        float qmn[MP_MAX], qmx[MP_MAX];
+#pragma unroll
+        for (int k = 0; k < MP_MAX; ++k)
+            if (k < K) { qmn[k] = qbmin[q * K + k]; qmx[k] = qbmax[q * K + k]; }
+        long long o = cum[q] - base;
+        for (int j = 0; j < TT; ++j)
+            if (!prune || mp_survives(qmn, qmx, tbmin + (size_t)j * K, tbmax + (size_t)j * K, K, theta, relm)) list[o++] = j;
+    }
+}
+
+// ------------------------------------------------------------ launchers
+void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, const double* p0, float* P,
+                        cudaStream_t s) {
+    if (norm == 1) pick_pivots_kernel<1><<<1, 1024, 0, s>>>(E, N, d, K, p0, P);
+    else pick_pivots_kernel<2><<<1, 1024, 0, s>>>(E, N, d, K, p0, P);
+}
+
+void launch_mp_keys(const float* E, const float* Rel, long long N, long long nseg, int d, int norm, int K,
+                    const float* P, float* keys, unsigned int* minmax, unsigned int* nonfinite, cudaStream_t s) {
+    const bool query = Rel != nullptr;
+    mp_init_minmax_kernel<<<grid_for_mp(nseg * K, 256), 256, 0, s>>>(minmax, nseg * K);
+    const int S = (d & 1) ? d : d + 1;
+    const int ent = query ? 32 : 128;
+    const size_t smem = (size_t)(ent * S + K * d + (query ? 16 * d : 0)) * sizeof(float);
+    dim3 grid((unsigned)((N + ent - 1) / ent), query ? (unsigned)((nseg + 15) / 16) : 1u);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, query ? 256 : 128, smem, s>>>(E, Rel, N, nseg, d, K, P, keys, minmax, nonfinite);
+    };
+    if (norm == 1) { if (query) go(mp_keys_kernel<1, true>); else go(mp_keys_kernel<1, false>); }
+    else { if (query) go(mp_keys_kernel<2, true>); else go(mp_keys_kernel<2, false>); }
+}
+
+void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
+                      unsigned long long* code, unsigned int* idx, cudaStream_t s) {
+    mp_morton_kernel<<<grid_for_mp(nseg * L, 256), 256, 0, s>>>(keys, minmax, nseg, L, K, bits, code, idx);
+}
+
+void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg, long long L, int ROWS, int ntile,
+                     int K, float* bmin, float* bmax, cudaStream_t s) {
+    mp_boxes_kernel<<<grid_for_mp(nseg * ntile * 32, 256), 256, 0, s>>>(keys, perm, nseg, L, ROWS, ntile, K, bmin,
+                                                                         bmax);
+}
+
+void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,
+                     int TT, int K, float theta, float relm, int prune, int2* ranges, long long* cost, cudaStream_t s) {
+    mp_count_kernel<<<grid_for_mp(nq, 128), 128, 0, s>>>(qbmin, qbmax, tbmin, tbmax, nq, TT, K, theta, relm, prune,
+                                                          ranges, cost);
+}
+
+void launch_mp_emit(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax,
+                    const long long* cum, const DevCounters* ctr, long long nq, int TT, int K, float theta, float relm,
+                    int prune, int* list, cudaStream_t s) {
+    mp_emit_kernel<<<grid_for_mp(nq, 128), 128, 0, s>>>(qbmin, qbmax, tbmin, tbmax, cum, ctr, TT, K, theta, relm, prune,
+                                                         list);
+}
+
+}  // namespace kgc

@@ -309,7 +309,8 @@ __global__ void radix_prep_kernel(const float* __restrict__ keys, const unsigned
     }
 }
 
-__global__ void radix_hist_kernel(const unsigned int* __restrict__ kin, long long L, int B, int shift, int* counts) {
+template <typename KeyT>
+__global__ void radix_hist_kernel(const KeyT* __restrict__ kin, long long L, int B, int shift, int* counts) {
     __shared__ int h[256];
     const long long s = blockIdx.y;
     const int b = blockIdx.x;
@@ -319,15 +320,16 @@ __global__ void radix_hist_kernel(const unsigned int* __restrict__ kin, long lon
 #pragma unroll
     for (int k = 0; k < SORT_IPB / 256; ++k) {
         long long i = base + k * 256 + threadIdx.x;
-        if (i < L) atomicAdd(&h[(kin[s * L + i] >> shift) & 255u], 1);
+        if (i < L) atomicAdd(&h[(unsigned)(kin[s * L + i] >> shift) & 255u], 1);
     }
     __syncthreads();
     counts[(s * 256 + threadIdx.x) * B + b] = h[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(256) radix_scatter_kernel(const unsigned int* __restrict__ kin,
+template <typename KeyT>
+__global__ void __launch_bounds__(256) radix_scatter_kernel(const KeyT* __restrict__ kin,
                                                             const unsigned int* __restrict__ vin,
-                                                            unsigned int* __restrict__ kout,
+                                                            KeyT* __restrict__ kout,
                                                             unsigned int* __restrict__ vout,
                                                             const int* __restrict__ offs, long long L, int B,
                                                             int shift) {
@@ -344,8 +346,8 @@ __global__ void __launch_bounds__(256) radix_scatter_kernel(const unsigned int* 
     for (int round = 0; round < SORT_IPB / 256; ++round) {
         long long i = base + round * 256 + threadIdx.x;
         bool valid = i < L;
-        unsigned key = valid ? kin[s * L + i] : 0u;
-        int dg = valid ? (int)((key >> shift) & 255u) : 256;
+        KeyT key = valid ? kin[s * L + i] : KeyT(0);
+        int dg = valid ? (int)((unsigned)(key >> shift) & 255u) : 256;
 #pragma unroll
         for (int ww = 0; ww < 8; ++ww) wcnt[ww][threadIdx.x] = 0;
         __syncthreads();
@@ -404,13 +406,36 @@ int radix_sort_segments(const float* keys, const unsigned int* minmax, long long
         const unsigned int* vi = pass == 0 ? v0 : v1;
         unsigned int* ko = pass == 0 ? k1 : k0;
         unsigned int* vo = pass == 0 ? v1 : v0;
-        radix_hist_kernel<<<g, 256, 0, s>>>(ki, L, B, pass * 8, counts);
+        radix_hist_kernel<unsigned int><<<g, 256, 0, s>>>(ki, L, B, pass * 8, counts);
         scan_exclusive_i32(counts, counts, nc, scan_tmp, s, launches);
-        radix_scatter_kernel<<<g, 256, 0, s>>>(ki, vi, ko, vo, counts, L, B, pass * 8);
+        radix_scatter_kernel<unsigned int><<<g, 256, 0, s>>>(ki, vi, ko, vo, counts, L, B, pass * 8);
     }
     radix_final_kernel<<<grid_for(S * L, 256), 256, 0, s>>>(v0, keys, S, L, perm_out, skeys_out);
     if (launches) *launches += 6;
     return 0;
+}
+
+// Stable LSD sort of S segments of L 64-bit keys (already in k0, values =
+// in-segment indices in v0) on the low `bits` bits; sorted values end in v0.
+void radix_sort_u64_segments(long long S, long long L, int bits, unsigned long long* k0, unsigned int* v0,
+                             unsigned long long* k1, unsigned int* v1, int* counts, void* scan_tmp, cudaStream_t s,
+                             int* launches) {
+    if (S <= 0 || L <= 0) return;
+    const int B = (int)((L + SORT_IPB - 1) / SORT_IPB);
+    const size_t nc = (size_t)S * 256 * B;
+    dim3 g((unsigned)B, (unsigned)S);
+    int passes = (bits + 7) / 8;
+    if (passes & 1) ++passes;  // even pass count: the result lands back in (k0, v0)
+    for (int pass = 0; pass < passes; ++pass) {
+        const unsigned long long* ki = (pass & 1) ? k1 : k0;
+        const unsigned int* vi = (pass & 1) ? v1 : v0;
+        unsigned long long* ko = (pass & 1) ? k0 : k1;
+        unsigned int* vo = (pass & 1) ? v0 : v1;
+        radix_hist_kernel<unsigned long long><<<g, 256, 0, s>>>(ki, L, B, pass * 8, counts);
+        scan_exclusive_i32(counts, counts, nc, scan_tmp, s, launches);
+        radix_scatter_kernel<unsigned long long><<<g, 256, 0, s>>>(ki, vi, ko, vo, counts, L, B, pass * 8);
+        if (launches) *launches += 2;
+    }
 }
 
 // ============================================================== K3: ranges
@@ -543,16 +568,17 @@ __global__ void shard_count_kernel(const long long* __restrict__ cost, const lon
 
 __global__ void shard_emit_kernel(const int2* __restrict__ ranges, const int* __restrict__ nitem,
                                   const int* __restrict__ off, long long nq, int chunk, DevCounters* ctr,
-                                  int4* items, long long* item_tiles) {
+                                  int4* items, long long* item_tiles, const long long* __restrict__ cum, int list_mode) {
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq; q += (long long)gridDim.x * blockDim.x) {
         int n = nitem[q];
         int o = off[q];
         if (q == nq - 1) ctr->n_items = (long long)o + n;
         int2 rg = ranges[q];
+        const int loff = (list_mode && n > 0) ? (int)(cum[q] - cum[ctr->tq_begin]) : -1;
         for (int k = 0; k < n; ++k) {
             int j0 = rg.x + k * chunk;
             int j1 = min(rg.y, j0 + chunk - 1);
-            items[o + k] = make_int4((int)q, j0, j1, 0);
+            items[o + k] = make_int4((int)q, j0, j1, loff);
             item_tiles[o + k] = j1 - j0 + 1;
         }
     }
@@ -560,14 +586,14 @@ __global__ void shard_emit_kernel(const int2* __restrict__ ranges, const int* __
 
 void launch_shard_items(const int2* ranges, const long long* cost, const long long* cum, long long nq, int rank,
                         int world, int chunk, DevCounters* ctr, int* nitem, int* item_off, int4* items,
-                        long long* item_tiles, void* tmp, cudaStream_t s, int* launches, int phase) {
+                        long long* item_tiles, void* tmp, cudaStream_t s, int* launches, int phase, int list_mode) {
     if (phase == 0) {
         shard_count_kernel<<<grid_for(nq, 256), 256, 0, s>>>(cost, cum, nq, rank, world, chunk, ctr, nitem);
         scan_exclusive_i32(nitem, item_off, (size_t)nq, tmp, s, launches);
         if (launches) *launches += 1;
     } else {
         shard_emit_kernel<<<grid_for(nq, 256), 256, 0, s>>>(ranges, nitem, item_off, nq, chunk, ctr, items,
-                                                            item_tiles);
+                                                            item_tiles, cum, list_mode);
         if (launches) *launches += 1;
     }
 }

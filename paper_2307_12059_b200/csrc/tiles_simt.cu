@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(256, 2) tiles_simt_kernel(TileParams p) {
         float* dst = St + (size_t)s * SIMT_KC * (BM + BN_SIMT);
         mbar_arrive_expect_tx(&full[s], qbytes + tbytes);
         bulk_g2s(dst, p.Qp + (size_t)(ci.w.x - p.tq0) * BM * Kpad + (size_t)ci.c * SIMT_KC * BM, qbytes, &full[s]);
-        bulk_g2s(dst + SIMT_KC * BM, p.Tp + (size_t)ci.j * BN_SIMT * Kpad + (size_t)ci.c * SIMT_KC * BN_SIMT, tbytes,
+        bulk_g2s(dst + SIMT_KC * BM,
+                 p.Tp + (size_t)item_tile(ci.w, ci.j, p.tile_list) * BN_SIMT * Kpad + (size_t)ci.c * SIMT_KC * BN_SIMT, tbytes,
                  &full[s]);
     };
 
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(256, 2) tiles_simt_kernel(TileParams p) {
             }
         }
         if (cs.c == nkc - 1) {
-            const int j = cs.j;
+            const int j = item_tile(cs.w, cs.j, p.tile_list);
             unsigned long long hit = 0;
 #pragma unroll
             for (int a = 0; a < 8; ++a)

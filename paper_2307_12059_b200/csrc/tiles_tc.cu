@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
             for (long long it = it_begin; it < it_end; it += it_step) {
                 const int4 w = p.items[it];
                 for (int j = w.y; j <= w.z; ++j) {
-                    const float* tsrc = p.Tp + (size_t)j * BN_TC * Kpad;
+                    const float* tsrc = p.Tp + (size_t)item_tile(w, j, p.tile_list) * BN_TC * Kpad;
                     for (int c = 0; c < nkc; ++c) {
                         const int klen = Kpad - c * KC < KC ? Kpad - c * KC : KC;
                         const uint32_t bytes = (uint32_t)klen * BN_TC * 4;
@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
             const int rowid = w.x * BM + i;
             // theta_f covers q = fl32(h + r) vs the exact h + r (|dq_k| <= 2^-24 |q_k|)
             const float thf = p.theta * (1.0f + 2.44140625e-04f) + 2.384185791015625e-07f * Qn;
-            for (int j = w.y; j <= w.z; ++j) {
+            for (int jj = w.y; jj <= w.z; ++jj) {
+                const int j = item_tile(w, jj, p.tile_list);
                 const float2 tv = p.tstile[j];
                 const float Tm = tv.x, Tdm = tv.y;
                 // |acc - q.t| <= Qd Tm + Qn Tdm + Qd Tdm + eta (Qn + Qd)(Tm + Tdm)

@@ -23,7 +23,8 @@ KGC_OK, KGC_EINVAL, KGC_EDATA, KGC_ENOMEM, KGC_ECUDA, KGC_ENODEV, KGC_ESTATE = 0
 STATUS_NAMES = {0: "KGC_OK", -1: "KGC_EINVAL", -2: "KGC_EDATA", -3: "KGC_ENOMEM", -4: "KGC_ECUDA",
                 -5: "KGC_ENODEV", -6: "KGC_ESTATE"}
 KGC_MAX_DIM = 1024
-INSPECT = {"tail_keys": 1, "query_keys": 2, "tail_perm": 3, "query_perm": 4, "tile_ranges": 5, "query_cost": 6}
+INSPECT = {"tail_keys": 1, "query_keys": 2, "tail_perm": 3, "query_perm": 4, "tile_ranges": 5, "query_cost": 6,
+           "tile_list": 7}
 
 TRIPLET_DTYPE = np.dtype([("h", np.int32), ("r", np.int32), ("t", np.int32), ("dist", np.float32)])
 
@@ -31,7 +32,7 @@ TRIPLET_DTYPE = np.dtype([("h", np.int32), ("r", np.int32), ("t", np.int32), ("d
 class kgc_options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("prune", ctypes.c_int32), ("pivot", ctypes.c_int32), ("l2_engine", ctypes.c_int32),
-                ("chunk_tiles", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("chunk_tiles", ctypes.c_int32), ("pivots", ctypes.c_int32),
                 ("result_capacity", ctypes.c_int64), ("stream", ctypes.c_void_p)]
 
 
@@ -46,7 +47,8 @@ class kgc_stats_t(ctypes.Structure):
                 ("d2h_bytes", ctypes.c_int64), ("launches", ctypes.c_int32), ("reruns", ctypes.c_int32),
                 ("ms_total", ctypes.c_float), ("ms_h2d", ctypes.c_float), ("ms_keys", ctypes.c_float),
                 ("ms_sort", ctypes.c_float), ("ms_ranges", ctypes.c_float), ("ms_stage", ctypes.c_float),
-                ("ms_tiles", ctypes.c_float), ("ms_recheck", ctypes.c_float)]
+                ("ms_tiles", ctypes.c_float), ("ms_recheck", ctypes.c_float), ("pivots_used", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -196,7 +198,7 @@ def kgc_inspect(ctx, what: str) -> np.ndarray:
     if n < 0:
         raise KgcError(int(n), kgc_last_error(ctx))
     dtype = {"tail_keys": np.float32, "query_keys": np.float32, "tail_perm": np.int32, "query_perm": np.int32,
-             "tile_ranges": np.int32, "query_cost": np.int64}[what]
+             "tile_ranges": np.int32, "query_cost": np.int64, "tile_list": np.int32}[what]
     out = np.empty(n // np.dtype(dtype).itemsize, dtype=dtype)
     rc = load_library().kgc_inspect(ctx, code, out.ctypes.data, n)
     if rc < 0:

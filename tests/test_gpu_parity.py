@@ -240,3 +240,97 @@ def test_full_size_sampled(cfg, norm, hit, S):
     rep = check_parity(E, Rel, norm, eps, res, rows=rows)
     assert rep["tight"] > 0
     assert st["tile_pairs_surviving"] < st["tile_pairs_total"]
+
+
+# ------------------------------------------------- multi-pivot pruning (§8(f) row 2)
+@pytest.mark.parametrize("K", [2, 4, 8])
+@pytest.mark.parametrize("norm", [1, 2])
+def test_multipivot_parity_c1(K, norm):
+    E, Rel = generate_config("c1")
+    eps = theta_for(E, Rel, norm, 1e-3)
+    res, st = gpu_join(E, Rel, norm, eps, pivots=K)
+    assert st["pivots_used"] == K
+    check_parity(E, Rel, norm, eps, res)
+
+
+@pytest.mark.parametrize("N,R,d", [(7, 3, 5), (300, 5, 100), (1000, 4, 200), (513, 2, 256), (700, 3, 50)])
+@pytest.mark.parametrize("norm", [1, 2])
+def test_multipivot_ragged(N, R, d, norm):
+    E, Rel = generate(N, R, d, seed=N + 7 * d, dist="cluster")
+    eps = theta_for(E, Rel, norm, 0.01)
+    engines = ["tc", "simt"] if norm == 2 else ["simt"]
+    for eng in engines:
+        res, st = gpu_join(E, Rel, norm, eps, pivots=8, **ENGINES[eng])
+        check_parity(E, Rel, norm, eps, res)
+
+
+@pytest.mark.parametrize("norm", [1, 2])
+def test_multipivot_equals_single_pivot(norm):
+    """Same set with 1 and 8 pivots (the tiles differ, so the surviving-tile
+    counts are not ordered pair by pair; both prune)."""
+    E, Rel = generate(6000, 6, 64, seed=41)
+    eps = theta_for(E, Rel, norm, 1e-3)
+    a, sa = gpu_join(E, Rel, norm, eps, pivots=1)
+    b, sb = gpu_join(E, Rel, norm, eps, pivots=8)
+    assert keyset(a) == keyset(b)
+    assert sb["pivots_used"] == 8 and sa["pivots_used"] == 1
+    assert sb["tile_pairs_surviving"] < sb["tile_pairs_total"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multipivot_sharding_invariance(world):
+    E, Rel = generate(3000, 7, 48, seed=42)
+    eps = theta_for(E, Rel, 2, 1e-3)
+    full, _ = gpu_join(E, Rel, 2, eps, pivots=8)
+    parts = [gpu_join(E, Rel, 2, eps, rank=r, world=world, pivots=8)[0] for r in range(world)]
+    sets = [keyset(p) for p in parts]
+    assert sum(len(s) for s in sets) == len(set().union(*sets))
+    assert set().union(*sets) == keyset(full)
+
+
+@pytest.mark.parametrize("norm", [1, 2])
+def test_multipivot_tile_lists_complete(norm):
+    """Every (query, tail) pair that passes the K-pivot L_inf test of Lemma 1
+    (|d(p_k,q) - d(p_k,t)| <= eps for all k) lies in a surviving tile of its
+    query tile's list; keys within their documented FP32 bound of FP64."""
+    from paper_2307_12059_b200 import kgc
+    E, Rel = generate(2500, 3, 32, seed=43)
+    N, R, K = 2500, 3, 8
+    eps = theta_for(E, Rel, norm, 1e-3)
+    with kgc.Join(pivots=K) as j:
+        j.run(E, Rel, norm, eps)
+        kt = j.inspect("tail_keys").reshape(N, K)
+        kq = j.inspect("query_keys").reshape(R, N, K)
+        tperm = j.inspect("tail_perm")
+        qperm = j.inspect("query_perm").reshape(R, N)
+        cum = j.inspect("query_cost")
+        lst = j.inspect("tile_list")
+        st = j.stats()
+    BM, BN = st["query_tile_rows"], st["tail_tile_rows"]
+    QT = st["query_tiles"]
+    assert np.array_equal(np.sort(tperm), np.arange(N))
+    skt = kt[tperm]
+    for r in range(R):
+        assert np.array_equal(np.sort(qperm[r]), np.arange(N))
+        skq = kq[r][qperm[r]]
+        for qt in range(QT):
+            tq = r * QT + qt
+            hi = cum[tq + 1] if tq + 1 < len(cum) else len(lst) + cum[0]
+            tiles = set(lst[cum[tq] - cum[0]: hi - cum[0]].tolist())
+            rows = skq[qt * BM:(qt + 1) * BM]
+            ok = np.ones((rows.shape[0], N), bool)
+            for k in range(K):
+                ok &= np.abs(rows[:, None, k] - skt[None, :, k]) <= eps
+            need = set((np.nonzero(ok.any(axis=0))[0] // BN).tolist())
+            assert need <= tiles
+
+
+@pytest.mark.parametrize("cfg,norm,hit,S", [("c2", 2, 1e-4, 1200), ("c2", 1, 1e-4, 1200), ("c3", 2, 1e-5, 800)])
+def test_multipivot_full_size_sampled(cfg, norm, hit, S):
+    E, Rel = generate_config(cfg)
+    N, R = E.shape[0], Rel.shape[0]
+    rows = sample_rows(N, R, S, seed=8)
+    eps = theta_for(E, Rel, norm, hit, rows=rows)
+    res, st = gpu_join(E, Rel, norm, eps, pivots=8)
+    rep = check_parity(E, Rel, norm, eps, res, rows=rows)
+    assert rep["tight"] > 0
