@@ -81,6 +81,9 @@ typedef struct {
                               /* prune = 1; otherwise one pivot is used)                           */
     int64_t result_capacity;  /* initial result-buffer capacity in triplets; 0 = auto (grows)       */
     void*   stream;           /* cudaStream_t to run on; NULL = a stream the context creates       */
+    int32_t l1_engine;        /* 0 = auto (= 2); 1 = FP16x2 SIMT filter with rigorous band (used   */
+                              /* only when every |E|, |Rel| value <= 1000, else 2); 2 = FP32 SIMT   */
+    int32_t reserved2;
 } kgc_options;
 
 /* Per-join statistics (of the last successful kgc_join). */
@@ -106,11 +109,12 @@ typedef struct {
     /* device time per phase (CUDA events on the context's stream), milliseconds */
     float ms_total, ms_h2d, ms_keys, ms_sort, ms_ranges, ms_stage, ms_tiles, ms_recheck;
     int32_t pivots_used;          /* 1, or K of the multi-pivot pruning                            */
-    int32_t reserved;
+    int32_t engine;               /* tile engine used: 1 tcgen05 TF32, 2 FP32 SIMT, 3 FP16x2 SIMT    */
 } kgc_stats_t;
 
 /* Fill *opt with defaults: device -1, rank 0, world 1, prune 1, pivot 0,
- * l2_engine 0, chunk_tiles 0, pivots 1, result_capacity 0, stream NULL. */
+ * l2_engine 0, chunk_tiles 0, pivots 1, result_capacity 0, stream NULL,
+ * l1_engine 0. */
 void kgc_default_options(kgc_options* opt);
 
 /* Create a context.  opt == NULL means defaults.  Returns KGC_ENODEV when no

@@ -106,6 +106,12 @@ static T* P(DevBuf& b) {
 // Relative margin covering the FP32 pivot keys.
 static float mp_relm(int d) { return (float)(d + 8) * 1.1920928955078125e-07f; }
 
+static float __uint_as_float_host(unsigned int u) {
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
 static bool is_device_ptr(const void* p, int device) {
     if (!p) return false;
     cudaPointerAttributes a;
@@ -131,6 +137,7 @@ void kgc_default_options(kgc_options* o) {
     o->l2_engine = 0;
     o->chunk_tiles = 0;
     o->pivots = 1;
+    o->l1_engine = 0;
     o->result_capacity = 0;
     o->stream = nullptr;
 }
@@ -141,7 +148,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 2 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX) {
+        o.l2_engine > 2 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 2) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -351,6 +358,10 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         LAUNCHED(1);
         pivot = P<double>(ctx->pivot);
     }
+    if (norm == 1 && ctx->opt.l1_engine == 1) {
+        launch_absmax(E, N * d, Rel, R * d, &dctr->absmax_bits, s);
+        LAUNCHED(1);
+    }
     const int K = (ctx->opt.pivots >= 2 && ctx->opt.prune && d <= MP_MAX_DIM) ? ctx->opt.pivots : 1;
     ctx->K = K;
     st.pivots_used = K;
@@ -483,19 +494,35 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     CK(cudaEventRecord(ctx->ev[EV_RANGES], s));
 
     // ---- stage operand tiles (tails: all; queries: this shard's range)
+    // FP16x2 L1 engine only on request (l1_engine = 1) and when every |value| <= 1000 (FP16 range and
+    // partial sums safe).  Measured on B200 it is no faster than FP32: HADD2 issues at half the FADD rate,
+    // so two elements per instruction buy nothing (scripts/micro/l1_inner.cu).
+    const bool half = norm == 1 && ctx->opt.l1_engine == 1 && __uint_as_float_host(h1.c.absmax_bits) <= 1000.0f;
+    st.engine = tc ? 1 : (half ? 3 : 2);
+    const float gam = 1.0f + 10.0f * 4.8828125e-04f + (float)(d / 8 + 4) * 1.1920928955078125e-07f;
     if (n_items > 0) {
         CK(ensure(ctx->Tp, (size_t)TT * BN * Kpad * 4));
         CK(ensure(ctx->T2, (size_t)TT * BN * 4));
         CK(ensure(ctx->tstile, (size_t)TT * 8));
-        launch_stage_tails(E, P<int>(ctx->tperm), N, d, Kpad, BN, TT, tc ? 1 : 0, P<float>(ctx->Tp), P<float>(ctx->T2),
-                           P<float2>(ctx->tstile), s);
-        LAUNCHED(1);
-        if (!tc) {  // the tensor-core engine forms its query tiles on the fly
-            CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * BM * Kpad * 4));
+        if (half) {
+            CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * BM * Kpad * 2));
             CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * BM * 16));
-            launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, tq0, tq1, 0, norm, eps,
-                                 P<float>(ctx->Qp), P<float4>(ctx->qs), s);
+            launch_stage_half(E, nullptr, P<int>(ctx->tperm), N, d, Kpad, BN, 1, 0, TT, eps, gam, ctx->Tp.p, nullptr,
+                              P<float>(ctx->T2), s);
+            launch_stage_half(E, Rel, P<int>(ctx->qperm), N, d, Kpad, BM, QT, tq0, tq1 - tq0, eps, gam, ctx->Qp.p,
+                              P<float4>(ctx->qs), nullptr, s);
+            LAUNCHED(2);
+        } else {
+            launch_stage_tails(E, P<int>(ctx->tperm), N, d, Kpad, BN, TT, tc ? 1 : 0, P<float>(ctx->Tp),
+                               P<float>(ctx->T2), P<float2>(ctx->tstile), s);
             LAUNCHED(1);
+            if (!tc) {  // the tensor-core engine forms its query tiles on the fly
+                CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * BM * Kpad * 4));
+                CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * BM * 16));
+                launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, tq0, tq1, 0, norm, eps,
+                                     P<float>(ctx->Qp), P<float4>(ctx->qs), s);
+                LAUNCHED(1);
+            }
         }
     }
     CK(cudaEventRecord(ctx->ev[EV_STAGE], s));
@@ -528,6 +555,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.tq0 = tq0;
         tp.N = (int)N;
         tp.theta = eps;
+        tp.gam = gam;
+        tp.Rt = P<float>(ctx->T2);
         tp.eta = (float)((Kpad / 8) * 3.814697265625e-06);  // Ksteps * 2^-18
         tp.cand = P<int2>(ctx->cand);
         tp.cand_count = &dctr->cand;
@@ -539,6 +568,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.QT = QT;
         if (n_items > 0) {
             if (tc) launch_tiles_tc(tp, ctx->num_sms, s);
+            else if (half) launch_tiles_half_l1(tp, ctx->num_sms, s);
             else launch_tiles_simt(tp, norm, ctx->num_sms, s);
             LAUNCHED(1);
         }

@@ -25,6 +25,8 @@ struct DevCounters {
     long long my_cost;            // surviving tile pairs, this shard
     int tq_begin, tq_end;         // query-tile range of this shard [begin, end)
     long long n_items;            // work items of this shard
+    unsigned int absmax_bits;     // max |value| over E and Rel (float bits), for the FP16 engine
+    unsigned int pad1;
 };
 
 struct TileParams {
@@ -44,6 +46,8 @@ struct TileParams {
     int N;                  // tails (valid columns are < N)
     float theta;
     float eta;              // tensor-core accumulation error coefficient
+    float gam;              // FP16 engine: relative error factor (1 + gamma)
+    const float* Rt;        // FP16 engine: per staged tail row residual
     int2* cand;
     unsigned long long* cand_count;
     long long cand_cap;
@@ -85,6 +89,12 @@ void launch_stage_tails(const float* E, const int* tperm, long long N, int d, in
 void launch_stage_queries(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad,
                           int QT, int tq0, int tq1, int tc_layout, int norm, float theta, float* Qp,
                           float4* qs, cudaStream_t s);
+// FP16x2 L1 engine staging: tiles of half2 words, element (i, k-pair p) at p * ROWS + i;
+// per row the exact residual R = sum_k |v_k - fp16(v_k)| (rounded up)
+void launch_stage_half(const float* E, const float* Rel, const int* perm, long long N, int d, int Kpad, int ROWS,
+                       int QT, int tile0, int ntiles, float theta, float gam, void* out, float4* qs, float* rt,
+                       cudaStream_t s);
+void launch_absmax(const float* E, long long nE, const float* Rel, long long nR, unsigned int* out, cudaStream_t s);
 
 // ---- multi-pivot pruning (pivots.cu) ----
 void radix_sort_u64_segments(long long S, long long L, int bits, unsigned long long* k0, unsigned int* v0,
@@ -113,6 +123,8 @@ __device__ __forceinline__ int item_tile(const int4& w, int j, const int* __rest
 int  tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);
 void launch_tiles_tc(const TileParams& p, int num_sms, cudaStream_t s);
 void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t s);
+void launch_tiles_half_l1(const TileParams& p, int num_sms, cudaStream_t s);
+constexpr int HALF_FLUSH_PAIRS = 8;  // FP16x2 engine: flush to FP32 every 16 dims
 
 // ---- verification (verify.cu) ----
 struct KgcTripletDev { int h, r, t; float dist; };

@@ -88,8 +88,11 @@ __global__ void __launch_bounds__(1024) pick_pivots_kernel(const float* __restri
 }
 
 // ----------------------------------------------------------------- keys
-// QUERY: block = 32 entities x 16 relations (warp w: relations w, w + 8);
-// tails: block = 128 threads = 128 entities (warp w: entities w*32 + lane), one segment.
+// QUERY: a block walks MK_CH chunks of 32 entities against 16 relations (warp
+// w: relations w, w + 8; lane = entity); tails: 128 threads, MK_CH chunks of
+// 128 entities (warp w: entities w*32 + lane).  Key min/max per (segment,
+// pivot) are kept per warp across chunks: one atomic pair per warp at the end.
+constexpr int MK_CH = 8;
 template <int NORM, bool QUERY>
 __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
                                                       long long N, long long nseg, int d, int K,
@@ -98,18 +101,12 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
     extern __shared__ float mk_smem[];
     const int S = (d & 1) ? d : d + 1;
     constexpr int ENT = QUERY ? 32 : 128;
+    constexpr int NU = QUERY ? 2 : 1;                     // relations per warp
     float* Es = mk_smem;                                   // [ENT][S]
     float* Ps = Es + ENT * S;                              // [K][d]
     float* Rs = Ps + K * d;                                // [16][d] (queries)
-    const long long h0 = (long long)blockIdx.x * ENT;
     const long long r0 = QUERY ? (long long)blockIdx.y * 16 : 0;
     bool bad = false;
-    for (int x = threadIdx.x; x < ENT * d; x += blockDim.x) {
-        const int i = x / d, k = x % d;
-        const float v = (h0 + i < N) ? E[(h0 + i) * d + k] : 0.f;
-        if (!QUERY) bad |= !isfinite(v);
-        Es[i * S + k] = v;
-    }
     for (int x = threadIdx.x; x < K * d; x += blockDim.x) Ps[x] = P[x];
     if (QUERY) {
         for (int x = threadIdx.x; x < 16 * d; x += blockDim.x) {
@@ -119,42 +116,74 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
             Rs[i * d + k] = v;
         }
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int rl = QUERY ? w : 0; rl < (QUERY ? 16 : 1); rl += 8) {
-        const long long r = r0 + rl;
-        if (QUERY && r >= nseg) break;
-        const int eloc = QUERY ? lane : w * 32 + lane;
-        const long long h = h0 + eloc;
-        const float* es = Es + eloc * S;
-        const float* rs = QUERY ? Rs + rl * d : nullptr;
-        float acc[MP_MAX];
+    float mn[NU][MP_MAX], mx[NU][MP_MAX];
 #pragma unroll
-        for (int k = 0; k < MP_MAX; ++k) acc[k] = 0.f;
-        for (int dd = 0; dd < d; ++dd) {
-            const float q = QUERY ? __fadd_rn(es[dd], rs[dd]) : es[dd];  // connector_1(h, r) = h + r
+    for (int u = 0; u < NU; ++u)
 #pragma unroll
-            for (int k = 0; k < MP_MAX; ++k) {
-                if (k < K) {
-                    const float x = q - Ps[k * d + dd];
-                    acc[k] = NORM == 1 ? acc[k] + fabsf(x) : fmaf(x, x, acc[k]);
+        for (int k = 0; k < MP_MAX; ++k) { mn[u][k] = FLT_MAX; mx[u][k] = 0.f; }
+    for (int ch = 0; ch < MK_CH; ++ch) {
+        const long long h0 = ((long long)blockIdx.x * MK_CH + ch) * ENT;
+        if (h0 >= N) break;
+        __syncthreads();
+        for (int x = threadIdx.x; x < ENT * d; x += blockDim.x) {
+            const int i = x / d, k = x % d;
+            const float v = (h0 + i < N) ? E[(h0 + i) * d + k] : 0.f;
+            if (!QUERY) bad |= !isfinite(v);
+            Es[i * S + k] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+            const int rl = QUERY ? w + 8 * u : 0;
+            const long long r = r0 + rl;
+            if (QUERY && r >= nseg) break;
+            const int eloc = QUERY ? lane : w * 32 + lane;
+            const long long h = h0 + eloc;
+            const float* es = Es + eloc * S;
+            const float* rs = QUERY ? Rs + rl * d : nullptr;
+            float acc[MP_MAX];
+#pragma unroll
+            for (int k = 0; k < MP_MAX; ++k) acc[k] = 0.f;
+            for (int dd = 0; dd < d; ++dd) {
+                const float q = QUERY ? __fadd_rn(es[dd], rs[dd]) : es[dd];  // connector_1(h, r) = h + r
+#pragma unroll
+                for (int k = 0; k < MP_MAX; ++k) {
+                    if (k < K) {
+                        const float x = q - Ps[k * d + dd];
+                        acc[k] = NORM == 1 ? acc[k] + fabsf(x) : fmaf(x, x, acc[k]);
+                    }
+                }
+            }
+            if (h < N) {
+#pragma unroll
+                for (int k = 0; k < MP_MAX; ++k) {
+                    if (k < K) {
+                        const float key = NORM == 2 ? sqrtf(acc[k]) : acc[k];
+                        keys[((size_t)r * N + h) * K + k] = key;
+                        mn[u][k] = fminf(mn[u][k], key);
+                        mx[u][k] = fmaxf(mx[u][k], key);
+                    }
                 }
             }
         }
-        const bool valid = h < N;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const long long r = r0 + (QUERY ? w + 8 * u : 0);
+        if (QUERY && r >= nseg) break;
 #pragma unroll
         for (int k = 0; k < MP_MAX; ++k) {
             if (k < K) {
-                const float key = NORM == 2 ? sqrtf(acc[k]) : acc[k];
-                if (valid) keys[((size_t)r * N + h) * K + k] = key;
-                float mn = valid ? key : FLT_MAX, mx = valid ? key : 0.f;
+                float a = mn[u][k], z = mx[u][k];
                 for (int o = 16; o > 0; o >>= 1) {
-                    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                    a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+                    z = fmaxf(z, __shfl_xor_sync(0xffffffffu, z, o));
                 }
                 if (lane == 0) {
-                    atomicMin(&minmax[((size_t)r * K + k) * 2], __float_as_uint(mn));
-                    atomicMax(&minmax[((size_t)r * K + k) * 2 + 1], __float_as_uint(mx));
+                    atomicMin(&minmax[((size_t)r * K + k) * 2], __float_as_uint(a));
+                    atomicMax(&minmax[((size_t)r * K + k) * 2 + 1], __float_as_uint(z));
                 }
             }
         }
@@ -304,7 +333,8 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
     const int S = (d & 1) ? d : d + 1;
     const int ent = query ? 32 : 128;
     const size_t smem = (size_t)(ent * S + K * d + (query ? 16 * d : 0)) * sizeof(float);
-    dim3 grid((unsigned)((N + ent - 1) / ent), query ? (unsigned)((nseg + 15) / 16) : 1u);
+    dim3 grid((unsigned)((N + (long long)ent * MK_CH - 1) / ((long long)ent * MK_CH)),
+              query ? (unsigned)((nseg + 15) / 16) : 1u);
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, query ? 256 : 128, smem, s>>>(E, Rel, N, nseg, d, K, P, keys, minmax, nonfinite);

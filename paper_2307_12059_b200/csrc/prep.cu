@@ -10,6 +10,8 @@
 #include <climits>
 #include <cstdio>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace kgc {
@@ -76,9 +78,11 @@ __global__ void tail_keys_kernel(const float* __restrict__ E, long long N, int d
     }
 }
 
-// d(h + r, p) for every (h, r): a block holds 32 entity rows and 16 relation
-// rows in shared memory; warp w handles relations w and w + 8, lane = entity.
-constexpr int QK_ENT = 32, QK_REL = 16;
+// d(h + r, p) for every (h, r): a block walks QK_CH chunks of 32 entity rows
+// (in shared memory) against 16 relation rows; warp w handles relations w and
+// w + 8, lane = entity.  Per-relation key min/max are kept per warp across the
+// chunks, so each warp issues one atomic pair per relation (not per chunk).
+constexpr int QK_ENT = 32, QK_REL = 16, QK_CH = 8;
 template <int NORM, bool PIV>
 __global__ void __launch_bounds__(256) query_keys_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
                                                          long long N, long long R, int d,
@@ -88,12 +92,7 @@ __global__ void __launch_bounds__(256) query_keys_kernel(const float* __restrict
     const int S = (d & 1) ? d : d + 1;  // odd row stride: conflict-free column reads
     float* Es = qk_smem;                 // [QK_ENT][S]
     float* Rs = qk_smem + QK_ENT * S;    // [QK_REL][d]
-    const long long h0 = (long long)blockIdx.x * QK_ENT;
     const long long r0 = (long long)blockIdx.y * QK_REL;
-    for (int x = threadIdx.x; x < QK_ENT * d; x += blockDim.x) {
-        int i = x / d, k = x % d;
-        Es[i * S + k] = (h0 + i < N) ? E[(h0 + i) * d + k] : 0.f;
-    }
     bool bad = false;
     for (int x = threadIdx.x; x < QK_REL * d; x += blockDim.x) {
         int i = x / d, k = x % d;
@@ -103,30 +102,48 @@ __global__ void __launch_bounds__(256) query_keys_kernel(const float* __restrict
     }
     if (blockIdx.x == 0 && __syncthreads_or(bad)) {
         if (threadIdx.x == 0) atomicOr(nonfinite, 1u);
-    } else {
-        __syncthreads();
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const long long h = h0 + lane;
-    for (int rl = w; rl < QK_REL; rl += 8) {
-        const long long r = r0 + rl;
-        if (r >= R) break;
-        double s = 0.0;
-        const float* es = Es + lane * S;
-        const float* rs = Rs + rl * d;
-        for (int k = 0; k < d; ++k) {
-            double x = (double)es[k] + (double)rs[k];  // connector_1(h, r) = h + r
-            if (PIV) x -= pivot[k];
-            s += NORM == 1 ? fabs(x) : x * x;
+    float mn[2] = {FLT_MAX, FLT_MAX}, mx[2] = {0.f, 0.f};
+    for (int ch = 0; ch < QK_CH; ++ch) {
+        const long long h0 = ((long long)blockIdx.x * QK_CH + ch) * QK_ENT;
+        if (h0 >= N) break;
+        __syncthreads();  // previous chunk fully consumed
+        for (int x = threadIdx.x; x < QK_ENT * d; x += blockDim.x) {
+            int i = x / d, k = x % d;
+            Es[i * S + k] = (h0 + i < N) ? E[(h0 + i) * d + k] : 0.f;
         }
-        float key = __double2float_rn(NORM == 2 ? sqrt(s) : s);
-        bool valid = h < N;
-        if (valid) kq[r * N + h] = key;
-        float mn = warp_min_f(valid ? key : FLT_MAX);
-        float mx = warp_max_f(valid ? key : 0.f);
+        __syncthreads();
+        const long long h = h0 + lane;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int rl = w + 8 * u;
+            const long long r = r0 + rl;
+            if (r >= R) break;
+            double s = 0.0;
+            const float* es = Es + lane * S;
+            const float* rs = Rs + rl * d;
+            for (int k = 0; k < d; ++k) {
+                double x = (double)es[k] + (double)rs[k];  // connector_1(h, r) = h + r
+                if (PIV) x -= pivot[k];
+                s += NORM == 1 ? fabs(x) : x * x;
+            }
+            float key = __double2float_rn(NORM == 2 ? sqrt(s) : s);
+            if (h < N) {
+                kq[r * N + h] = key;
+                mn[u] = fminf(mn[u], key);
+                mx[u] = fmaxf(mx[u], key);
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const long long r = r0 + w + 8 * u;
+        if (r >= R) break;
+        const float a = warp_min_f(mn[u]), z = warp_max_f(mx[u]);
         if (lane == 0) {
-            atomicMin(&minmax[2 * r], __float_as_uint(mn));
-            atomicMax(&minmax[2 * r + 1], __float_as_uint(mx));
+            atomicMin(&minmax[2 * r], __float_as_uint(a));
+            atomicMax(&minmax[2 * r + 1], __float_as_uint(z));
         }
     }
 }
@@ -169,7 +186,7 @@ void launch_query_keys(const float* E, const float* Rel, long long N, long long 
     init_minmax_kernel<<<grid_for(R, 256), 256, 0, s>>>(minmax, R);
     const int S = (d & 1) ? d : d + 1;
     size_t smem = (size_t)(QK_ENT * S + QK_REL * d) * sizeof(float);
-    dim3 grid((unsigned)((N + QK_ENT - 1) / QK_ENT), (unsigned)((R + QK_REL - 1) / QK_REL));
+    dim3 grid((unsigned)((N + QK_ENT * QK_CH - 1) / (QK_ENT * QK_CH)), (unsigned)((R + QK_REL - 1) / QK_REL));
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, 256, smem, s>>>(E, Rel, N, R, d, pivot, kq, minmax, nonfinite);
@@ -735,6 +752,74 @@ __global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ E,
             tstile[tile] = make_float2(a, b);
         }
     }
+}
+
+// ------------------------------------------------------------ FP16x2 staging
+// L1 FP16x2 engine operands: half2 words (dims 2p, 2p + 1) at p * ROWS + i.
+// Per row: R = sum_k |v_k - fp16(v_k)| (each difference exact in FP32, sum
+// rounded up) -- the exact price of the FP16 rounding in the L1 bound
+// (DESIGN.md "FP16x2 L1 engine").  Queries: qs.w = (theta + 2^-23 ||q||_1 + R) gam
+// (rounded up); tails: rt = R gam (rounded up).  One thread per row.
+__global__ void __launch_bounds__(128) stage_half_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
+                                                         const int* __restrict__ perm, long long N, int d, int Kpad,
+                                                         int ROWS, int QT, int tile0, float theta, float gam,
+                                                         __half2* __restrict__ out, float4* __restrict__ qs,
+                                                         float* __restrict__ rt) {
+    const int tile = tile0 + blockIdx.x;
+    long long r = 0, t_in_rel = tile;
+    if (Rel) {
+        r = tile / QT;
+        t_in_rel = tile - r * QT;
+    }
+    const int* pr = perm + (Rel ? r * N : 0);
+    const float* rel = Rel ? Rel + r * d : nullptr;
+    __half2* dst = out + (size_t)blockIdx.x * ROWS * (Kpad / 2);
+    for (int i = threadIdx.x; i < ROWS; i += blockDim.x) {
+        const long long p = t_in_rel * ROWS + i;
+        const bool valid = p < N;
+        const long long h = valid ? pr[p] : 0;
+        float res = 0.f, l1 = 0.f;
+        for (int kp = 0; kp < Kpad / 2; ++kp) {
+            float v[2] = {0.f, 0.f};
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int k = 2 * kp + c;
+                if (valid && k < d) v[c] = rel ? __fadd_rn(E[h * d + k], rel[k]) : E[h * d + k];
+            }
+            const __half2 hv = __floats2half2_rn(v[0], v[1]);
+            const float2 back = __half22float2(hv);
+            res = __fadd_ru(res, __fadd_ru(fabsf(v[0] - back.x), fabsf(v[1] - back.y)));
+            l1 = __fadd_ru(l1, __fadd_ru(fabsf(v[0]), fabsf(v[1])));
+            dst[(size_t)kp * ROWS + i] = hv;
+        }
+        if (rel) {
+            const float thr = __fmul_ru(__fadd_ru(__fadd_ru(theta, __fmul_ru(l1, 1.1920928955078125e-07f)), res), gam);
+            qs[(size_t)blockIdx.x * ROWS + i] = valid ? make_float4(0.f, 0.f, res, thr) : make_float4(0.f, 0.f, 0.f, -1.f);
+        } else {
+            rt[(size_t)tile * ROWS + i] = valid ? __fmul_ru(res, gam) : 0.f;
+        }
+    }
+}
+
+void launch_stage_half(const float* E, const float* Rel, const int* perm, long long N, int d, int Kpad, int ROWS,
+                       int QT, int tile0, int ntiles, float theta, float gam, void* out, float4* qs, float* rt,
+                       cudaStream_t s) {
+    if (ntiles <= 0) return;
+    stage_half_kernel<<<ntiles, 128, 0, s>>>(E, Rel, perm, N, d, Kpad, ROWS, QT, tile0, theta, gam,
+                                             reinterpret_cast<__half2*>(out), qs, rt);
+}
+
+__global__ void absmax_kernel(const float* __restrict__ E, long long nE, const float* __restrict__ Rel, long long nR,
+                              unsigned int* out) {
+    float m = 0.f;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nE + nR; i += (long long)gridDim.x * blockDim.x)
+        m = fmaxf(m, fabsf(i < nE ? E[i] : Rel[i - nE]));
+    m = warp_max_f(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+void launch_absmax(const float* E, long long nE, const float* Rel, long long nR, unsigned int* out, cudaStream_t s) {
+    absmax_kernel<<<grid_for(nE + nR, 256, 148 * 4), 256, 0, s>>>(E, nE, Rel, nR, out);
 }
 
 void launch_stage_tails(const float* E, const int* tperm, long long N, int d, int Kpad, int BN, int TT, int tc_layout,

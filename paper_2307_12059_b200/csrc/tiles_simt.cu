@@ -11,6 +11,8 @@
 // two CTAs per SM).  A pair whose FP32 distance is within the row's
 // rigorous bound (stage kernel) becomes a
 // candidate; the FP64 re-check (verify.cu) decides.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace kgc {
@@ -181,6 +183,172 @@ __global__ void __launch_bounds__(256, 2) tiles_simt_kernel(TileParams p) {
         }
         cs.next(p, nkc);
     }
+}
+
+// ------------------------------------------------------------------------
+// FP16x2 L1 engine.  Same tiling, ring and scheduling as above, operands are
+// half2 words (two consecutive dims) and the inner step is
+//     acc2 = acc2 + |q2 - t2|      (HADD2 with the |.| operand modifier:
+// one instruction per element instead of FADD + FADD|.|), flushed into FP32
+// every HALF_FLUSH_PAIRS pairs (16 dims).  A pair is a candidate iff the FP32
+// sum <= thr_row + rt_col, the rigorous bound of DESIGN.md "FP16x2 L1 engine";
+// the FP64 re-check decides.
+constexpr int HKC = 16;  // pairs (= 32 dims) per stage
+
+__global__ void __launch_bounds__(256, 1) tiles_half_l1_kernel(TileParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int KP = p.Kpad / 2;                         // pairs per row
+    const int nkc = (KP + HKC - 1) / HKC;
+    uint32_t* St = reinterpret_cast<uint32_t*>(smem);  // [stage][HKC][BM + BN] half2 words
+    uint64_t* full = reinterpret_cast<uint64_t*>(St + SIMT_NS * HKC * (BM + BN_SIMT));
+    int* released = reinterpret_cast<int*>(full + SIMT_NS);
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int ty = tid >> 4, tx = tid & 15;
+    if (tid == 0) {
+        for (int s = 0; s < SIMT_NS; ++s) {
+            mbar_init(&full[s], 1);
+            released[s] = 0;
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const uint32_t* Qw = reinterpret_cast<const uint32_t*>(p.Qp);
+    const uint32_t* Tw = reinterpret_cast<const uint32_t*>(p.Tp);
+    auto issue = [&](const ChunkIter& ci, long long g) {
+        const int s = (int)(g % SIMT_NS);
+        const int klen = KP - ci.c * HKC < HKC ? KP - ci.c * HKC : HKC;
+        const uint32_t qbytes = (uint32_t)klen * BM * 4, tbytes = (uint32_t)klen * BN_SIMT * 4;
+        uint32_t* dst = St + (size_t)s * HKC * (BM + BN_SIMT);
+        mbar_arrive_expect_tx(&full[s], qbytes + tbytes);
+        bulk_g2s(dst, Qw + (size_t)(ci.w.x - p.tq0) * BM * KP + (size_t)ci.c * HKC * BM, qbytes, &full[s]);
+        bulk_g2s(dst + HKC * BM, Tw + (size_t)item_tile(ci.w, ci.j, p.tile_list) * BN_SIMT * KP + (size_t)ci.c * HKC * BN_SIMT,
+                 tbytes, &full[s]);
+    };
+
+    ChunkIter cs;
+    cs.start(p);
+    if (tid == 0) {
+        ChunkIter pr = cs;
+        for (long long gp = 0; gp < SIMT_NS && pr.valid(p); ++gp) {
+            issue(pr, gp);
+            pr.next(p, nkc);
+        }
+    }
+
+    float thr[8];
+    float accf[8][8];
+    __half2 acc2[8][8];
+    const __half2 hz = __float2half2_rn(0.f);
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) { accf[a][b] = 0.f; acc2[a][b] = hz; }
+    long long cur_item = -1;
+
+    auto flush = [&]() {
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const float2 f = __half22float2(acc2[a][b]);
+                accf[a][b] += f.x + f.y;
+                acc2[a][b] = hz;
+            }
+    };
+
+    for (long long g = 0; cs.valid(p); ++g) {
+        if (cs.it != cur_item) {
+            cur_item = cs.it;
+#pragma unroll
+            for (int a = 0; a < 8; ++a) thr[a] = p.qs[(size_t)(cs.w.x - p.tq0) * BM + ty * 8 + a].w;
+        }
+        const int s = (int)(g % SIMT_NS);
+        mbar_wait(&full[s], (uint32_t)(g / SIMT_NS) & 1u);
+        const int klen = KP - cs.c * HKC < HKC ? KP - cs.c * HKC : HKC;
+        const uint32_t* qk = St + (size_t)s * HKC * (BM + BN_SIMT) + ty * 8;
+        const uint32_t* tk = St + (size_t)s * HKC * (BM + BN_SIMT) + HKC * BM + tx * 8;
+        for (int k0 = 0; k0 < klen; k0 += HALF_FLUSH_PAIRS) {
+            const int kend = k0 + HALF_FLUSH_PAIRS < klen ? k0 + HALF_FLUSH_PAIRS : klen;
+#pragma unroll 2
+            for (int k = k0; k < kend; ++k) {
+                const uint4 qa = *reinterpret_cast<const uint4*>(qk + k * BM);
+                const uint4 qb = *reinterpret_cast<const uint4*>(qk + k * BM + 4);
+                const uint4 ta = *reinterpret_cast<const uint4*>(tk + k * BN_SIMT);
+                const uint4 tb = *reinterpret_cast<const uint4*>(tk + k * BN_SIMT + 4);
+                const uint32_t qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+                const uint32_t tv[8] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
+#pragma unroll
+                for (int a = 0; a < 8; ++a) {
+                    const __half2 q2 = *reinterpret_cast<const __half2*>(&qv[a]);
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const __half2 t2 = *reinterpret_cast<const __half2*>(&tv[b]);
+                        acc2[a][b] = __hadd2(acc2[a][b], __habs2(__hsub2(q2, t2)));
+                    }
+                }
+            }
+            flush();
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&released[s], 1) == 7) {
+                released[s] = 0;
+                ChunkIter nx = cs;
+#pragma unroll 1
+                for (int x = 0; x < SIMT_NS && nx.valid(p); ++x) nx.next(p, nkc);
+                if (nx.valid(p)) {
+                    fence_proxy_async_smem();
+                    issue(nx, g + SIMT_NS);
+                }
+            }
+        }
+        if (cs.c == nkc - 1) {
+            const int j = item_tile(cs.w, cs.j, p.tile_list);
+            const int colb = j * BN_SIMT + tx * 8;
+            const float4 r0 = __ldg(reinterpret_cast<const float4*>(p.Rt + colb));
+            const float4 r1 = __ldg(reinterpret_cast<const float4*>(p.Rt + colb + 4));
+            const float rtc[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+            unsigned long long hit = 0;
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
+                    hit |= (unsigned long long)(accf[a][b] <= __fadd_ru(thr[a], rtc[b])) << (a * 8 + b);
+            if (__any_sync(0xffffffffu, hit != 0)) {
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
+                    if (colb + b >= p.N) hit &= ~(0x0101010101010101ull << b);
+                unsigned long long slot = warp_reserve(__popcll(hit), p.cand_count);
+                while (hit) {
+                    const int ab = __ffsll(hit) - 1;
+                    if (slot < (unsigned long long)p.cand_cap)
+                        p.cand[slot] = make_int2(cs.w.x * BM + ty * 8 + (ab >> 3), colb + (ab & 7));
+                    ++slot;
+                    hit &= hit - 1;
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int b = 0; b < 8; ++b) accf[a][b] = 0.f;
+        }
+        cs.next(p, nkc);
+    }
+}
+
+void launch_tiles_half_l1(const TileParams& p, int num_sms, cudaStream_t s) {
+    if (p.n_items <= 0) return;
+    const size_t smem = (size_t)SIMT_NS * HKC * (BM + BN_SIMT) * 4 + 64;
+    cudaFuncSetAttribute(tiles_half_l1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiles_half_l1_kernel, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+    long long g = (long long)num_sms * per_sm;
+    if (g > p.n_items) g = p.n_items;
+    tiles_half_l1_kernel<<<(unsigned)g, 256, smem, s>>>(p);
 }
 
 void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t s) {

@@ -38,8 +38,12 @@ __device__ __forceinline__ double partial_dist(const float* __restrict__ eh, con
     return acc;
 }
 
-// One warp verifies 32 candidates per round: 8 lanes per candidate (4 at a
-// time), FP64 partial sums reduced over the 8 lanes, one atomic per round.
+// One warp verifies 32 candidates per round: 8 lanes per candidate, each
+// 8-lane group takes 8 CONSECUTIVE candidates (the tile engines append the
+// candidates of one query row contiguously), keeps that row's E_h and Rel_r
+// in registers while the row repeats (VEC4 path, d <= 256), and reloads only
+// E_t.  FP64 partial sums are reduced over the 8 lanes; one atomic per round.
+constexpr int VMAXM = 8;  // float4 chunks per lane cached (d <= 256)
 template <int NORM, bool VEC4>
 __global__ void __launch_bounds__(256) verify_kernel(const int2* __restrict__ cand,
                                                      const unsigned long long* __restrict__ cand_count,
@@ -54,15 +58,19 @@ __global__ void __launch_bounds__(256) verify_kernel(const int2* __restrict__ ca
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const long long rows_per_rel = (long long)QT * BM;
+    const bool cache = VEC4 && d <= 32 * VMAXM;
+    const int M = (d + 31) / 32;
     for (long long base = warp * 32; base < nc; base += nwarps * 32) {
         uint32_t keep = 0;
         int hs[8], rs[8], ts[8];
         float ds[8];
+        int cached = -1;
+        float4 chv[VMAXM], crv[VMAXM];
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
-            const long long idx = base + it * 4 + g;
+            const long long idx = base + g * 8 + it;
             bool valid = idx < nc;
-            int h = 0, r = 0, t = 0;
+            int h = 0, r = 0, t = 0, rowid = -1;
             if (valid) {
                 const int2 cv = cand[idx];
                 const long long rr = cv.x / rows_per_rel;
@@ -72,11 +80,44 @@ __global__ void __launch_bounds__(256) verify_kernel(const int2* __restrict__ ca
                     r = (int)rr;
                     h = qperm[rr * N + pos];
                     t = tperm[cv.y];
+                    rowid = cv.x;
                 }
             }
-            double acc = valid ? partial_dist<NORM, VEC4>(E + (long long)h * d, Rel + (long long)r * d,
-                                                          E + (long long)t * d, d, s)
-                               : 0.0;
+            double acc = 0.0;
+            if (valid) {
+                const float* eh = E + (long long)h * d;
+                const float* er = Rel + (long long)r * d;
+                const float* et = E + (long long)t * d;
+                if (cache) {
+                    if (rowid != cached) {
+                        cached = rowid;
+#pragma unroll
+                        for (int m = 0; m < VMAXM; ++m) {
+                            const int k = s * 4 + 32 * m;
+                            if (m < M && k < d) {
+                                chv[m] = __ldg(reinterpret_cast<const float4*>(eh + k));
+                                crv[m] = __ldg(reinterpret_cast<const float4*>(er + k));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int m = 0; m < VMAXM; ++m) {
+                        const int k = s * 4 + 32 * m;
+                        if (m < M && k < d) {
+                            const float4 a = chv[m], b = crv[m];
+                            const float4 c = __ldg(reinterpret_cast<const float4*>(et + k));
+                            const double x0 = ((double)a.x + (double)b.x) - (double)c.x;  // (h + r) - t, FP64
+                            const double x1 = ((double)a.y + (double)b.y) - (double)c.y;
+                            const double x2 = ((double)a.z + (double)b.z) - (double)c.z;
+                            const double x3 = ((double)a.w + (double)b.w) - (double)c.w;
+                            if (NORM == 1) acc += fabs(x0) + fabs(x1) + fabs(x2) + fabs(x3);
+                            else acc += x0 * x0 + x1 * x1 + x2 * x2 + x3 * x3;
+                        }
+                    }
+                } else {
+                    acc = partial_dist<NORM, VEC4>(eh, er, et, d, s);
+                }
+            }
             acc += __shfl_xor_sync(0xffffffffu, acc, 4);
             acc += __shfl_xor_sync(0xffffffffu, acc, 2);
             acc += __shfl_xor_sync(0xffffffffu, acc, 1);

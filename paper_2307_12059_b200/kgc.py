@@ -33,7 +33,8 @@ class kgc_options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("prune", ctypes.c_int32), ("pivot", ctypes.c_int32), ("l2_engine", ctypes.c_int32),
                 ("chunk_tiles", ctypes.c_int32), ("pivots", ctypes.c_int32),
-                ("result_capacity", ctypes.c_int64), ("stream", ctypes.c_void_p)]
+                ("result_capacity", ctypes.c_int64), ("stream", ctypes.c_void_p), ("l1_engine", ctypes.c_int32),
+                ("reserved2", ctypes.c_int32)]
 
 
 class kgc_stats_t(ctypes.Structure):
@@ -48,7 +49,7 @@ class kgc_stats_t(ctypes.Structure):
                 ("ms_total", ctypes.c_float), ("ms_h2d", ctypes.c_float), ("ms_keys", ctypes.c_float),
                 ("ms_sort", ctypes.c_float), ("ms_ranges", ctypes.c_float), ("ms_stage", ctypes.c_float),
                 ("ms_tiles", ctypes.c_float), ("ms_recheck", ctypes.c_float), ("pivots_used", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("engine", ctypes.c_int32)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

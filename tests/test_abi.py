@@ -44,7 +44,7 @@ def test_abi_version(lib):
 def test_struct_sizes_match_header():
     from paper_2307_12059_b200 import kgc
     assert kgc.TRIPLET_DTYPE.itemsize == 16
-    assert ctypes.sizeof(kgc.kgc_options) == 48
+    assert ctypes.sizeof(kgc.kgc_options) == 56
     # kgc_stats_t: compile a tiny C program against the header to get its size
     import subprocess
     import tempfile

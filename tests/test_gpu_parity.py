@@ -334,3 +334,36 @@ def test_multipivot_full_size_sampled(cfg, norm, hit, S):
     res, st = gpu_join(E, Rel, norm, eps, pivots=8)
     rep = check_parity(E, Rel, norm, eps, res, rows=rows)
     assert rep["tight"] > 0
+
+
+# ------------------------------------------------- FP16x2 L1 engine
+@pytest.mark.parametrize("eng", [1, 2])
+def test_l1_engines_parity(eng):
+    E, Rel = generate_config("c1")
+    eps = theta_for(E, Rel, 1, 1e-3)
+    res, st = gpu_join(E, Rel, 1, eps, l1_engine=eng)
+    assert st["engine"] == (3 if eng == 1 else 2)
+    check_parity(E, Rel, 1, eps, res)
+
+
+def test_l1_half_engine_falls_back_on_large_values():
+    """|values| > 1000 leave the FP16 range margin: the FP16 engine request falls back to FP32."""
+    E, Rel = generate(900, 3, 40, seed=44)
+    E = (E * np.float32(3000.0)).astype(np.float32)
+    Rel = (Rel * np.float32(3000.0)).astype(np.float32)
+    eps = theta_for(E, Rel, 1, 1e-3)
+    res, st = gpu_join(E, Rel, 1, eps, l1_engine=1)
+    assert st["engine"] == 2
+    check_parity(E, Rel, 1, eps, res)
+
+
+def test_l1_half_engine_tiny_values_and_planted_zeros():
+    """Subnormal-range FP16 values and exact translations (distance 0)."""
+    rng = np.random.default_rng(45)
+    E = (rng.standard_normal((600, 24)) * 1e-5).astype(np.float32)
+    Rel = (rng.standard_normal((3, 24)) * 1e-5).astype(np.float32)
+    E[1] = E[0] + Rel[0]
+    eps = theta_for(E, Rel, 1, 1e-3)
+    res, st = gpu_join(E, Rel, 1, eps, l1_engine=1)
+    assert st["engine"] == 3
+    check_parity(E, Rel, 1, eps, res)
