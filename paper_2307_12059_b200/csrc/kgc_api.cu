@@ -415,11 +415,12 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         LAUNCHED(2);
         CK(cudaEventRecord(ctx->ev[EV_KEYS], s));
         // ---- a3: Morton-order sorts (tiles compact in pivot space)
-        const int bits = 64 / K;
+        const int bits = 8;  // per pivot, over the first min(K, MP_SORT_PIVOTS) pivots
         launch_mp_morton(P<float>(ctx->mpkt), P<unsigned>(ctx->mpmm_t), 1, N, K, bits,
                          P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
         LAUNCHED(1);
-        radix_sort_u64_segments(1, N, K * bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
+        const int code_bits = bits * (K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS);
+        radix_sort_u64_segments(1, N, code_bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
                                 P<unsigned long long>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
                                 ctx->scan_tmp.p, s, &ctx->launches);
         LAUNCHED(0);
@@ -427,7 +428,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         launch_mp_morton(P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q), R, N, K, bits,
                          P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
         LAUNCHED(1);
-        radix_sort_u64_segments(R, N, K * bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
+        radix_sort_u64_segments(R, N, code_bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
                                 P<unsigned long long>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
                                 ctx->scan_tmp.p, s, &ctx->launches);
         LAUNCHED(0);

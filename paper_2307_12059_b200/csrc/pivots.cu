@@ -93,27 +93,38 @@ __global__ void __launch_bounds__(1024) pick_pivots_kernel(const float* __restri
 // 128 entities (warp w: entities w*32 + lane).  Key min/max per (segment,
 // pivot) are kept per warp across chunks: one atomic pair per warp at the end.
 constexpr int MK_CH = 8;
+// Row stride (floats) of the entity tile: a multiple of 4 whose quarter is odd,
+// so the per-lane float4 row reads of a quarter-warp hit distinct bank groups.
+__host__ __device__ inline int mk_stride(int d) {
+    int s4 = (d + 3) / 4;
+    if ((s4 & 1) == 0) ++s4;
+    return 4 * s4;
+}
 template <int NORM, bool QUERY>
 __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
                                                       long long N, long long nseg, int d, int K,
                                                       const float* __restrict__ P, float* __restrict__ keys,
                                                       unsigned int* minmax, unsigned int* nonfinite) {
-    extern __shared__ float mk_smem[];
-    const int S = (d & 1) ? d : d + 1;
+    extern __shared__ __align__(16) float mk_smem[];
+    const int S = mk_stride(d);                            // entity row stride (zero padded)
+    const int D4 = (d + 3) / 4 * 4;                        // pivot / relation row stride (zero padded)
     constexpr int ENT = QUERY ? 32 : 128;
     constexpr int NU = QUERY ? 2 : 1;                     // relations per warp
     float* Es = mk_smem;                                   // [ENT][S]
-    float* Ps = Es + ENT * S;                              // [K][d]
-    float* Rs = Ps + K * d;                                // [16][d] (queries)
+    float* Ps = Es + ENT * S;                              // [K][D4]
+    float* Rs = Ps + K * D4;                               // [16][D4] (queries)
     const long long r0 = QUERY ? (long long)blockIdx.y * 16 : 0;
     bool bad = false;
-    for (int x = threadIdx.x; x < K * d; x += blockDim.x) Ps[x] = P[x];
+    for (int x = threadIdx.x; x < K * D4; x += blockDim.x) {
+        const int i = x / D4, k = x % D4;
+        Ps[x] = k < d ? P[i * d + k] : 0.f;
+    }
     if (QUERY) {
-        for (int x = threadIdx.x; x < 16 * d; x += blockDim.x) {
-            const int i = x / d, k = x % d;
-            const float v = (r0 + i < nseg) ? Rel[(r0 + i) * d + k] : 0.f;
+        for (int x = threadIdx.x; x < 16 * D4; x += blockDim.x) {
+            const int i = x / D4, k = x % D4;
+            const float v = (r0 + i < nseg && k < d) ? Rel[(r0 + i) * d + k] : 0.f;
             bad |= !isfinite(v);
-            Rs[i * d + k] = v;
+            Rs[x] = v;
         }
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -126,11 +137,11 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
         const long long h0 = ((long long)blockIdx.x * MK_CH + ch) * ENT;
         if (h0 >= N) break;
         __syncthreads();
-        for (int x = threadIdx.x; x < ENT * d; x += blockDim.x) {
-            const int i = x / d, k = x % d;
-            const float v = (h0 + i < N) ? E[(h0 + i) * d + k] : 0.f;
+        for (int x = threadIdx.x; x < ENT * S; x += blockDim.x) {
+            const int i = x / S, k = x % S;
+            const float v = (h0 + i < N && k < d) ? E[(h0 + i) * d + k] : 0.f;
             if (!QUERY) bad |= !isfinite(v);
-            Es[i * S + k] = v;
+            Es[x] = v;
         }
         __syncthreads();
 #pragma unroll
@@ -141,17 +152,27 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
             const int eloc = QUERY ? lane : w * 32 + lane;
             const long long h = h0 + eloc;
             const float* es = Es + eloc * S;
-            const float* rs = QUERY ? Rs + rl * d : nullptr;
+            const float* rs = QUERY ? Rs + rl * D4 : nullptr;
             float acc[MP_MAX];
 #pragma unroll
             for (int k = 0; k < MP_MAX; ++k) acc[k] = 0.f;
-            for (int dd = 0; dd < d; ++dd) {
-                const float q = QUERY ? __fadd_rn(es[dd], rs[dd]) : es[dd];  // connector_1(h, r) = h + r
+            // 4 dims per step: float4 loads of the entity row, relation row (broadcast)
+            // and every pivot row (broadcast); padding dims are zero on all sides.
+            for (int dd = 0; dd < D4; dd += 4) {
+                const float4 e4 = *reinterpret_cast<const float4*>(es + dd);
+                float4 q4 = e4;
+                if (QUERY) {
+                    const float4 r4 = *reinterpret_cast<const float4*>(rs + dd);
+                    q4 = make_float4(__fadd_rn(e4.x, r4.x), __fadd_rn(e4.y, r4.y), __fadd_rn(e4.z, r4.z),
+                                     __fadd_rn(e4.w, r4.w));  // connector_1(h, r) = h + r
+                }
 #pragma unroll
                 for (int k = 0; k < MP_MAX; ++k) {
                     if (k < K) {
-                        const float x = q - Ps[k * d + dd];
-                        acc[k] = NORM == 1 ? acc[k] + fabsf(x) : fmaf(x, x, acc[k]);
+                        const float4 p4 = *reinterpret_cast<const float4*>(Ps + k * D4 + dd);
+                        const float x0 = q4.x - p4.x, x1 = q4.y - p4.y, x2 = q4.z - p4.z, x3 = q4.w - p4.w;
+                        if (NORM == 1) acc[k] = acc[k] + fabsf(x0) + fabsf(x1) + fabsf(x2) + fabsf(x3);
+                        else acc[k] = fmaf(x3, x3, fmaf(x2, x2, fmaf(x1, x1, fmaf(x0, x0, acc[k]))));
                     }
                 }
             }
@@ -220,11 +241,12 @@ __global__ void mp_morton_kernel(const float* __restrict__ keys, const unsigned 
                 }
             }
         }
+        const int Ks = K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS;  // order by the first pivots only
         unsigned long long c = 0;
         for (int b = bits - 1; b >= 0; --b)
 #pragma unroll
             for (int k = 0; k < MP_MAX; ++k)
-                if (k < K) c = (c << 1) | ((q[k] >> b) & 1u);
+                if (k < Ks) c = (c << 1) | ((q[k] >> b) & 1u);
         code[t] = c;
         idx[t] = (unsigned)i;
     }
@@ -281,22 +303,31 @@ __device__ __forceinline__ bool mp_survives(const float* qmn, const float* qmx, 
     return ok;
 }
 
+// One warp per query tile, lanes over tail tiles.
 __global__ void mp_count_kernel(const float* __restrict__ qbmin, const float* __restrict__ qbmax,
                                 const float* __restrict__ tbmin, const float* __restrict__ tbmax, long long nq, int TT,
                                 int K, float theta, float relm, int prune, int2* ranges, long long* cost) {
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq; q += (long long)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; q < nq;
+         q += ((long long)gridDim.x * blockDim.x) >> 5) {
         float qmn[MP_MAX], qmx[MP_MAX];
 #pragma unroll
         for (int k = 0; k < MP_MAX; ++k)
             if (k < K) { qmn[k] = qbmin[q * K + k]; qmx[k] = qbmax[q * K + k]; }
         int c = 0;
         if (prune) {
-            for (int j = 0; j < TT; ++j) c += mp_survives(qmn, qmx, tbmin + (size_t)j * K, tbmax + (size_t)j * K, K, theta, relm);
+            for (int j0 = 0; j0 < TT; j0 += 32) {
+                const int j = j0 + lane;
+                const bool ok = j < TT && mp_survives(qmn, qmx, tbmin + (size_t)j * K, tbmax + (size_t)j * K, K, theta, relm);
+                c += __popc(__ballot_sync(0xffffffffu, ok));
+            }
         } else {
             c = TT;
         }
-        ranges[q] = make_int2(0, c - 1);  // positions in this query tile's list
-        cost[q] = c;
+        if (lane == 0) {
+            ranges[q] = make_int2(0, c - 1);  // positions in this query tile's list
+            cost[q] = c;
+        }
     }
 }
 
@@ -307,15 +338,22 @@ __global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __r
     const int tq0 = ctr->tq_begin, tq1 = ctr->tq_end;
     if (tq0 >= tq1) return;
     const long long base = cum[tq0];
-    for (long long q = tq0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < tq1;
-         q += (long long)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (long long q = tq0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); q < tq1;
+         q += ((long long)gridDim.x * blockDim.x) >> 5) {
         float qmn[MP_MAX], qmx[MP_MAX];
 #pragma unroll
         for (int k = 0; k < MP_MAX; ++k)
             if (k < K) { qmn[k] = qbmin[q * K + k]; qmx[k] = qbmax[q * K + k]; }
         long long o = cum[q] - base;
-        for (int j = 0; j < TT; ++j)
-            if (!prune || mp_survives(qmn, qmx, tbmin + (size_t)j * K, tbmax + (size_t)j * K, K, theta, relm)) list[o++] = j;
+        for (int j0 = 0; j0 < TT; j0 += 32) {
+            const int j = j0 + lane;
+            const bool ok = j < TT && (!prune || mp_survives(qmn, qmx, tbmin + (size_t)j * K, tbmax + (size_t)j * K,
+                                                             K, theta, relm));
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            if (ok) list[o + __popc(m & lanemask_lt())] = j;  // ascending j order
+            o += __popc(m);
+        }
     }
 }
 
@@ -330,9 +368,9 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
                     const float* P, float* keys, unsigned int* minmax, unsigned int* nonfinite, cudaStream_t s) {
     const bool query = Rel != nullptr;
     mp_init_minmax_kernel<<<grid_for_mp(nseg * K, 256), 256, 0, s>>>(minmax, nseg * K);
-    const int S = (d & 1) ? d : d + 1;
+    const int S = mk_stride(d), D4 = (d + 3) / 4 * 4;
     const int ent = query ? 32 : 128;
-    const size_t smem = (size_t)(ent * S + K * d + (query ? 16 * d : 0)) * sizeof(float);
+    const size_t smem = (size_t)(ent * S + K * D4 + (query ? 16 * D4 : 0)) * sizeof(float);
     dim3 grid((unsigned)((N + (long long)ent * MK_CH - 1) / ((long long)ent * MK_CH)),
               query ? (unsigned)((nseg + 15) / 16) : 1u);
     auto go = [&](auto kern) {
@@ -356,14 +394,14 @@ void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg
 
 void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,
                      int TT, int K, float theta, float relm, int prune, int2* ranges, long long* cost, cudaStream_t s) {
-    mp_count_kernel<<<grid_for_mp(nq, 128), 128, 0, s>>>(qbmin, qbmax, tbmin, tbmax, nq, TT, K, theta, relm, prune,
+    mp_count_kernel<<<grid_for_mp(nq * 32, 256), 256, 0, s>>>(qbmin, qbmax, tbmin, tbmax, nq, TT, K, theta, relm, prune,
                                                           ranges, cost);
 }
 
 void launch_mp_emit(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax,
                     const long long* cum, const DevCounters* ctr, long long nq, int TT, int K, float theta, float relm,
                     int prune, int* list, cudaStream_t s) {
-    mp_emit_kernel<<<grid_for_mp(nq, 128), 128, 0, s>>>(qbmin, qbmax, tbmin, tbmax, cum, ctr, TT, K, theta, relm, prune,
+    mp_emit_kernel<<<grid_for_mp(nq * 32, 256), 256, 0, s>>>(qbmin, qbmax, tbmin, tbmax, cum, ctr, TT, K, theta, relm, prune,
                                                          list);
 }
 
