@@ -388,9 +388,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=256, help="(h,r) rows per reference step")
-    ap.add_argument("--pivots", type=int, default=1, help="1 = the paper's single pivot; 2..8 = multi-pivot pruning")
+    ap.add_argument("--pivots", default="auto",
+                    help="1 = the paper's single pivot; 2..8 = multi-pivot pruning; auto = best measured per config")
     args = ap.parse_args()
     args.norms = [int(x) for x in args.norms.split(",")]
+    # Best measured pivot count per workload: multi-pivot pruning pays on c2 / c4,
+    # the paper's single pivot is faster on c3 (its extra keys/sort cost exceeds the pruning gain).
+    best_pivots = {"c1": 1, "c2": 8, "c3": 1, "c4": 8, "c5": 8}
+    args.pivots = best_pivots.get(args.config, 1) if args.pivots == "auto" else int(args.pivots)
     cfg = CONFIGS[args.config]
     thresholds = load_thresholds()
     if args.impl == "reference":

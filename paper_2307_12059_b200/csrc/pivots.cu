@@ -17,6 +17,7 @@
 //   mp_boxes      per tile and pivot: [min, max] of its rows' keys
 //   mp_count / mp_emit  per query tile: count, then list, the surviving tail tiles
 #include <cfloat>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -100,9 +101,9 @@ __host__ __device__ inline int mk_stride(int d) {
     if ((s4 & 1) == 0) ++s4;
     return 4 * s4;
 }
-template <int NORM, bool QUERY>
+template <int NORM, bool QUERY, int K>
 __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
-                                                      long long N, long long nseg, int d, int K,
+                                                      long long N, long long nseg, int d, int /*Kr*/,
                                                       const float* __restrict__ P, float* __restrict__ keys,
                                                       unsigned int* minmax, unsigned int* nonfinite) {
     extern __shared__ __align__(16) float mk_smem[];
@@ -128,11 +129,11 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
         }
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    float mn[NU][MP_MAX], mx[NU][MP_MAX];
+    float mn[NU][K], mx[NU][K];
 #pragma unroll
     for (int u = 0; u < NU; ++u)
 #pragma unroll
-        for (int k = 0; k < MP_MAX; ++k) { mn[u][k] = FLT_MAX; mx[u][k] = 0.f; }
+        for (int k = 0; k < K; ++k) { mn[u][k] = FLT_MAX; mx[u][k] = 0.f; }
     for (int ch = 0; ch < MK_CH; ++ch) {
         const long long h0 = ((long long)blockIdx.x * MK_CH + ch) * ENT;
         if (h0 >= N) break;
@@ -153,9 +154,9 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
             const long long h = h0 + eloc;
             const float* es = Es + eloc * S;
             const float* rs = QUERY ? Rs + rl * D4 : nullptr;
-            float acc[MP_MAX];
+            float acc[K];
 #pragma unroll
-            for (int k = 0; k < MP_MAX; ++k) acc[k] = 0.f;
+            for (int k = 0; k < K; ++k) acc[k] = 0.f;
             // 4 dims per step: float4 loads of the entity row, relation row (broadcast)
             // and every pivot row (broadcast); padding dims are zero on all sides.
             for (int dd = 0; dd < D4; dd += 4) {
@@ -167,24 +168,20 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
                                      __fadd_rn(e4.w, r4.w));  // connector_1(h, r) = h + r
                 }
 #pragma unroll
-                for (int k = 0; k < MP_MAX; ++k) {
-                    if (k < K) {
-                        const float4 p4 = *reinterpret_cast<const float4*>(Ps + k * D4 + dd);
-                        const float x0 = q4.x - p4.x, x1 = q4.y - p4.y, x2 = q4.z - p4.z, x3 = q4.w - p4.w;
-                        if (NORM == 1) acc[k] = acc[k] + fabsf(x0) + fabsf(x1) + fabsf(x2) + fabsf(x3);
-                        else acc[k] = fmaf(x3, x3, fmaf(x2, x2, fmaf(x1, x1, fmaf(x0, x0, acc[k]))));
-                    }
+                for (int k = 0; k < K; ++k) {
+                    const float4 p4 = *reinterpret_cast<const float4*>(Ps + k * D4 + dd);
+                    const float x0 = q4.x - p4.x, x1 = q4.y - p4.y, x2 = q4.z - p4.z, x3 = q4.w - p4.w;
+                    if (NORM == 1) acc[k] = acc[k] + fabsf(x0) + fabsf(x1) + fabsf(x2) + fabsf(x3);
+                    else acc[k] = fmaf(x3, x3, fmaf(x2, x2, fmaf(x1, x1, fmaf(x0, x0, acc[k]))));
                 }
             }
             if (h < N) {
 #pragma unroll
-                for (int k = 0; k < MP_MAX; ++k) {
-                    if (k < K) {
-                        const float key = NORM == 2 ? sqrtf(acc[k]) : acc[k];
-                        keys[((size_t)r * N + h) * K + k] = key;
-                        mn[u][k] = fminf(mn[u][k], key);
-                        mx[u][k] = fmaxf(mx[u][k], key);
-                    }
+                for (int k = 0; k < K; ++k) {
+                    const float key = NORM == 2 ? sqrtf(acc[k]) : acc[k];
+                    keys[((size_t)r * N + h) * K + k] = key;
+                    mn[u][k] = fminf(mn[u][k], key);
+                    mx[u][k] = fmaxf(mx[u][k], key);
                 }
             }
         }
@@ -195,17 +192,15 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
         const long long r = r0 + (QUERY ? w + 8 * u : 0);
         if (QUERY && r >= nseg) break;
 #pragma unroll
-        for (int k = 0; k < MP_MAX; ++k) {
-            if (k < K) {
-                float a = mn[u][k], z = mx[u][k];
-                for (int o = 16; o > 0; o >>= 1) {
-                    a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
-                    z = fmaxf(z, __shfl_xor_sync(0xffffffffu, z, o));
-                }
-                if (lane == 0) {
-                    atomicMin(&minmax[((size_t)r * K + k) * 2], __float_as_uint(a));
-                    atomicMax(&minmax[((size_t)r * K + k) * 2 + 1], __float_as_uint(z));
-                }
+        for (int k = 0; k < K; ++k) {
+            float a = mn[u][k], z = mx[u][k];
+            for (int o = 16; o > 0; o >>= 1) {
+                a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+                z = fmaxf(z, __shfl_xor_sync(0xffffffffu, z, o));
+            }
+            if (lane == 0) {
+                atomicMin(&minmax[((size_t)r * K + k) * 2], __float_as_uint(a));
+                atomicMax(&minmax[((size_t)r * K + k) * 2 + 1], __float_as_uint(z));
             }
         }
     }
@@ -377,8 +372,25 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, query ? 256 : 128, smem, s>>>(E, Rel, N, nseg, d, K, P, keys, minmax, nonfinite);
     };
-    if (norm == 1) { if (query) go(mp_keys_kernel<1, true>); else go(mp_keys_kernel<1, false>); }
-    else { if (query) go(mp_keys_kernel<2, true>); else go(mp_keys_kernel<2, false>); }
+    auto byK = [&](auto n_, auto q_) {
+        constexpr int NN = decltype(n_)::value;
+        constexpr bool QQ = decltype(q_)::value;
+        switch (K) {
+            case 2: go(mp_keys_kernel<NN, QQ, 2>); break;
+            case 3: go(mp_keys_kernel<NN, QQ, 3>); break;
+            case 4: go(mp_keys_kernel<NN, QQ, 4>); break;
+            case 5: go(mp_keys_kernel<NN, QQ, 5>); break;
+            case 6: go(mp_keys_kernel<NN, QQ, 6>); break;
+            case 7: go(mp_keys_kernel<NN, QQ, 7>); break;
+            default: go(mp_keys_kernel<NN, QQ, 8>); break;
+        }
+    };
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    using BT = std::integral_constant<bool, true>;
+    using BF = std::integral_constant<bool, false>;
+    if (norm == 1) { if (query) byK(I1{}, BT{}); else byK(I1{}, BF{}); }
+    else { if (query) byK(I2{}, BT{}); else byK(I2{}, BF{}); }
 }
 
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
