@@ -12,7 +12,7 @@ constexpr int BN_SIMT = 128;     // tail rows per tile, SIMT engines
 constexpr int SORT_IPB = 2048;   // radix-sort items per block (256 threads x 8)
 constexpr int TC_MAX_KPAD = 256; // tensor-core engine supports d <= 256
 constexpr int MP_MAX = 8;        // multi-pivot pruning: at most 8 pivots
-constexpr int MP_SAMPLE = 4096;  // tails sampled for the farthest-point pivot choice
+
 constexpr int MP_MAX_DIM = 256;  // multi-pivot pruning supports d <= 256
 constexpr int MP_SORT_PIVOTS = 4; // Morton order over the first 4 pivots (8 bits each: 32-bit code)
 

@@ -41,26 +41,46 @@ __device__ __forceinline__ float dist_f32(const float* __restrict__ a, const flo
     return s;  // squared for L2 (monotone: fine for argmax)
 }
 
+// Farthest-point traversal over S sample tails held in shared memory (row
+// stride d|1: conflict-free across threads), one sample per thread.
 template <int NORM>
 __global__ void __launch_bounds__(1024) pick_pivots_kernel(const float* __restrict__ E, long long N, int d, int K,
-                                                           const double* __restrict__ p0, float* __restrict__ P) {
-    __shared__ float mind[MP_SAMPLE];
+                                                           int S, const double* __restrict__ p0,
+                                                           float* __restrict__ P) {
+    extern __shared__ float pp_smem[];
+    const int st = d | 1;
+    float* X = pp_smem;                      // [S][st] sample rows
+    float* piv = X + (size_t)S * st;         // [d] current pivot
     __shared__ float bv[32];
     __shared__ int bi[32];
     __shared__ int chosen;
-    const int S = (int)(N < MP_SAMPLE ? N : MP_SAMPLE);
-    for (int k = threadIdx.x; k < d; k += blockDim.x) P[k] = p0 ? (float)p0[k] : 0.f;
-    __syncthreads();
-    for (int s = threadIdx.x; s < S; s += blockDim.x) {
-        const long long row = (long long)s * N / S;
-        mind[s] = dist_f32<NORM>(E + row * d, P, d);
+    for (int x = threadIdx.x; x < S * d; x += blockDim.x) {
+        const int sidx = x / d, k = x % d;
+        const long long row = (long long)sidx * N / S;
+        X[sidx * st + k] = E[row * d + k];
+    }
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+        const float v = p0 ? (float)p0[k] : 0.f;
+        P[k] = v;
+        piv[k] = v;
     }
     __syncthreads();
+    const int sidx = threadIdx.x;
+    auto dist_to_piv = [&]() {
+        float sum = 0.f;
+        if (sidx < S) {
+            const float* xr = X + sidx * st;
+            for (int k = 0; k < d; ++k) {
+                const float x = xr[k] - piv[k];
+                sum = NORM == 1 ? sum + fabsf(x) : fmaf(x, x, sum);
+            }
+        }
+        return sum;  // squared for L2 (monotone: fine for argmax)
+    };
+    float mind = sidx < S ? dist_to_piv() : -1.f;
     for (int kk = 1; kk < K; ++kk) {
-        float best = -1.f;
-        int besti = 0;
-        for (int s = threadIdx.x; s < S; s += blockDim.x)
-            if (mind[s] > best) { best = mind[s]; besti = s; }
+        float best = mind;
+        int besti = sidx;
         for (int o = 16; o > 0; o >>= 1) {
             const float ov = __shfl_xor_sync(0xffffffffu, best, o);
             const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
@@ -69,21 +89,21 @@ __global__ void __launch_bounds__(1024) pick_pivots_kernel(const float* __restri
         if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = best; bi[threadIdx.x >> 5] = besti; }
         __syncthreads();
         if (threadIdx.x == 0) {
-            float b = -1.f;
+            float b = -2.f;
             int ix = 0;
             for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
                 if (bv[w] > b || (bv[w] == b && bi[w] < ix)) { b = bv[w]; ix = bi[w]; }
             chosen = ix;
         }
         __syncthreads();
-        const long long row = (long long)chosen * N / S;
         float* pk = P + (size_t)kk * d;
-        for (int k = threadIdx.x; k < d; k += blockDim.x) pk[k] = E[row * d + k];
-        __syncthreads();
-        for (int s = threadIdx.x; s < S; s += blockDim.x) {
-            const long long r2 = (long long)s * N / S;
-            mind[s] = fminf(mind[s], dist_f32<NORM>(E + r2 * d, pk, d));
+        for (int k = threadIdx.x; k < d; k += blockDim.x) {
+            const float v = X[chosen * st + k];
+            pk[k] = v;
+            piv[k] = v;
         }
+        __syncthreads();
+        if (sidx < S) mind = fminf(mind, dist_to_piv());
         __syncthreads();
     }
 }
@@ -355,8 +375,15 @@ __global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __r
 // ------------------------------------------------------------ launchers
 void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, const double* p0, float* P,
                         cudaStream_t s) {
-    if (norm == 1) pick_pivots_kernel<1><<<1, 1024, 0, s>>>(E, N, d, K, p0, P);
-    else pick_pivots_kernel<2><<<1, 1024, 0, s>>>(E, N, d, K, p0, P);
+    // sample size: at most 1024 tails and ~200 KB of shared memory
+    long long S = (200 * 1024 / 4 - d) / (d | 1);
+    if (S > 1024) S = 1024;
+    if (S > N) S = N;
+    if (S < 1) S = 1;
+    const size_t smem = ((size_t)S * (d | 1) + d) * sizeof(float);
+    auto kern = norm == 1 ? pick_pivots_kernel<1> : pick_pivots_kernel<2>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<1, 1024, smem, s>>>(E, N, d, K, (int)S, p0, P);
 }
 
 void launch_mp_keys(const float* E, const float* Rel, long long N, long long nseg, int d, int norm, int K,
