@@ -83,7 +83,10 @@ typedef struct {
     void*   stream;           /* cudaStream_t to run on; NULL = a stream the context creates       */
     int32_t l1_engine;        /* 0 = auto (= 2); 1 = FP16x2 SIMT filter with rigorous band (used   */
                               /* only when every |E|, |Rel| value <= 1000, else 2); 2 = FP32 SIMT   */
-    int32_t reserved2;
+    int32_t split;            /* world > 1: 0 = rank-local (default: rank k takes query tiles       */
+                              /* [k nq/W, (k+1) nq/W) and preprocesses only the relations they      */
+                              /* touch; tails are replicated); 1 = global cost-balanced split (every */
+                              /* rank preprocesses everything, shards by surviving-tile counts)     */
 } kgc_options;
 
 /* Per-join statistics (of the last successful kgc_join). */
@@ -114,7 +117,7 @@ typedef struct {
 
 /* Fill *opt with defaults: device -1, rank 0, world 1, prune 1, pivot 0,
  * l2_engine 0, chunk_tiles 0, pivots 1, result_capacity 0, stream NULL,
- * l1_engine 0. */
+ * l1_engine 0, split 0. */
 void kgc_default_options(kgc_options* opt);
 
 /* Create a context.  opt == NULL means defaults.  Returns KGC_ENODEV when no
@@ -175,9 +178,9 @@ enum {
 };
 int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes);
 
-/* Pure host function (no device needed): the shard of query tiles owned by
- * `rank` of `world`, given the exclusive prefix sums `cum` (length n) of the
- * per-query-tile surviving-tile counts and their grand total.  Query tile q
+/* Pure host function (no device needed), used by split = 1: the shard of
+ * query tiles owned by `rank` of `world`, given the exclusive prefix sums
+ * `cum` (length n) of the per-query-tile surviving-tile counts and their grand total.  Query tile q
  * belongs to rank min(world-1, floor(world * cum[q] / total)) (total == 0:
  * everything to rank 0).  Writes the half-open range [*begin, *end) and
  * returns its cost (surviving tiles), or KGC_EINVAL.  The device uses the

@@ -138,6 +138,7 @@ void kgc_default_options(kgc_options* o) {
     o->chunk_tiles = 0;
     o->pivots = 1;
     o->l1_engine = 0;
+    o->split = 0;
     o->result_capacity = 0;
     o->stream = nullptr;
 }
@@ -148,7 +149,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 2 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 2) {
+        o.l2_engine > 2 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 2 || o.split < 0 || o.split > 1) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -258,20 +259,24 @@ int64_t kgc_shard_range(const int64_t* cum, int64_t n, int64_t total, int32_t ra
 }  // extern "C"
 
 // ------------------------------------------------------------------ join
+// R, Rel_in: the relations this context preprocesses (rank-local split: a
+// sub-range starting at global relation r_off); [force_lo, force_hi): the
+// query tiles (in local numbering) this rank joins, or -1 for the
+// cost-balanced rule over all of them.
 static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long long N, long long R, int d, int norm,
-                     float eps) {
+                     float eps, int r_off, long long force_lo, long long force_hi, long long R_global) {
     cudaStream_t s = ctx->stream;
     ctx->launches = 0;
     kgc_stats_t& st = ctx->st;
     memset(&st, 0, sizeof st);
     st.N = N;
-    st.R = R;
+    st.R = R_global;
     st.d = d;
     st.norm = norm;
     st.eps = eps;
     st.rank = ctx->opt.rank;
     st.world = ctx->opt.world;
-    st.triplets = (double)N * (double)N * (double)R;
+    st.triplets = (double)N * (double)N * (double)R_global;
 
     const bool tc = norm == 2 && ctx->opt.l2_engine != 2 && ((d + 7) / 8) * 8 <= TC_MAX_KPAD;
     if (norm == 2 && ctx->opt.l2_engine == 1 && !tc) {
@@ -449,7 +454,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     LAUNCHED(0);
     launch_shard_items(P<int2>(ctx->ranges), P<long long>(ctx->cost), P<long long>(ctx->cum), nq, ctx->opt.rank,
                        ctx->opt.world, chunk, dctr, P<int>(ctx->nitem), P<int>(ctx->item_off), nullptr, nullptr,
-                       ctx->scan_tmp.p, s, &ctx->launches, 0, 0);
+                       ctx->scan_tmp.p, s, &ctx->launches, 0, 0, force_lo, force_hi);
     LAUNCHED(0);
     // sync #1: plan totals
     struct {
@@ -486,7 +491,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         launch_shard_items(P<int2>(ctx->ranges), P<long long>(ctx->cost), P<long long>(ctx->cum), nq, ctx->opt.rank,
                            ctx->opt.world, chunk, dctr, P<int>(ctx->nitem), P<int>(ctx->item_off),
                            P<int4>(ctx->items), P<long long>(ctx->item_tiles), ctx->scan_tmp.p, s, &ctx->launches, 1,
-                           K > 1 ? 1 : 0);
+                           K > 1 ? 1 : 0, force_lo, force_hi);
         LAUNCHED(0);
         scan_exclusive_i64(P<long long>(ctx->item_tiles), P<long long>(ctx->item_cum), (size_t)n_items, nullptr,
                            ctx->scan_tmp.p, s, &ctx->launches);
@@ -577,7 +582,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         if (n_items > 0) {
             launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, P<int>(ctx->qperm), P<int>(ctx->tperm), E,
                           Rel, N, QT, d, norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p), &dctr->res,
-                          ctx->res_cap, ctx->num_sms, s);
+                          ctx->res_cap, ctx->num_sms, s, r_off);
             LAUNCHED(1);
         }
         CK(cudaEventRecord(ctx->ev[EV_VERIFY], s));
@@ -652,7 +657,27 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(ctx->device);
-    int rc = join_impl(ctx, E, Rel, N, R, d, norm, eps);
+    int rc;
+    if (ctx->opt.world > 1 && ctx->opt.split == 0) {
+        // rank-local split: equal query-tile ranges, preprocessing restricted to the relations they touch
+        const long long QT = (N + BM - 1) / BM, nq = R * QT;
+        const long long a = nq * ctx->opt.rank / ctx->opt.world, b = nq * (ctx->opt.rank + 1) / ctx->opt.world;
+        if (a >= b) {
+            memset(&ctx->st, 0, sizeof ctx->st);
+            ctx->st.N = N; ctx->st.R = R; ctx->st.d = d; ctx->st.norm = norm; ctx->st.eps = eps;
+            ctx->st.rank = ctx->opt.rank; ctx->st.world = ctx->opt.world;
+            ctx->st.triplets = (double)N * (double)N * (double)R;
+            ctx->n_results = 0;
+            ctx->have_join = true;
+            rc = KGC_OK;
+        } else {
+            const long long r_lo = a / QT, r_hi = (b - 1) / QT + 1;
+            rc = join_impl(ctx, E, Rel + r_lo * d, N, r_hi - r_lo, d, norm, eps, (int)r_lo, a - r_lo * QT,
+                           b - r_lo * QT, R);
+        }
+    } else {
+        rc = join_impl(ctx, E, Rel, N, R, d, norm, eps, 0, -1, -1, R);
+    }
     if (rc != KGC_OK) {
         cudaStreamSynchronize(ctx->stream);
         cudaGetLastError();

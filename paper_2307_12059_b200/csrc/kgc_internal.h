@@ -84,7 +84,7 @@ void launch_query_ranges(const float* qskey, long long N, long long R, int QT, i
 void launch_shard_items(const int2* ranges, const long long* cost, const long long* cum, long long nq,
                         int rank, int world, int chunk, DevCounters* ctr, int* nitem, int* item_off,
                         int4* items, long long* item_tiles, void* tmp, cudaStream_t s, int* launches, int phase,
-                        int list_mode);
+                        int list_mode, long long force_lo, long long force_hi);
 void launch_stage_tails(const float* E, const int* tperm, long long N, int d, int Kpad, int BN, int TT,
                         int tc_layout, float* Tp, float* T2, float2* tstile, cudaStream_t s);
 void launch_stage_queries(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad,
@@ -132,6 +132,6 @@ struct KgcTripletDev { int h, r, t; float dist; };
 void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap,
                    const int* qperm, const int* tperm, const float* E, const float* Rel, long long N, int QT,
                    int d, int norm, float theta, KgcTripletDev* out, unsigned long long* res_count,
-                   long long res_cap, int num_sms, cudaStream_t s);
+                   long long res_cap, int num_sms, cudaStream_t s, int r_off);
 
 }  // namespace kgc

@@ -563,11 +563,14 @@ void launch_query_ranges(const float* qskey, long long N, long long R, int QT, i
 // (cum = exclusive prefix of surviving-tile counts) -- identical to the host
 // function kgc_shard_range().  Work items of at most `chunk` tail tiles.
 __global__ void shard_count_kernel(const long long* __restrict__ cost, const long long* __restrict__ cum,
-                                   long long nq, int rank, int world, int chunk, DevCounters* ctr, int* nitem) {
+                                   long long nq, int rank, int world, int chunk, DevCounters* ctr, int* nitem,
+                                   long long force_lo, long long force_hi) {
     const long long total = ctr->total_cost;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq; q += (long long)gridDim.x * blockDim.x) {
         int owner = 0;
-        if (total > 0) {
+        if (force_lo >= 0) {
+            owner = (q >= force_lo && q < force_hi) ? rank : rank + 1;  // rank-local split: a fixed range
+        } else if (total > 0) {
             long long o = (long long)world * cum[q] / total;
             owner = (int)(o < world - 1 ? o : world - 1);
         }
@@ -603,9 +606,11 @@ __global__ void shard_emit_kernel(const int2* __restrict__ ranges, const int* __
 
 void launch_shard_items(const int2* ranges, const long long* cost, const long long* cum, long long nq, int rank,
                         int world, int chunk, DevCounters* ctr, int* nitem, int* item_off, int4* items,
-                        long long* item_tiles, void* tmp, cudaStream_t s, int* launches, int phase, int list_mode) {
+                        long long* item_tiles, void* tmp, cudaStream_t s, int* launches, int phase, int list_mode,
+                        long long force_lo, long long force_hi) {
     if (phase == 0) {
-        shard_count_kernel<<<grid_for(nq, 256), 256, 0, s>>>(cost, cum, nq, rank, world, chunk, ctr, nitem);
+        shard_count_kernel<<<grid_for(nq, 256), 256, 0, s>>>(cost, cum, nq, rank, world, chunk, ctr, nitem, force_lo,
+                                                             force_hi);
         scan_exclusive_i32(nitem, item_off, (size_t)nq, tmp, s, launches);
         if (launches) *launches += 1;
     } else {

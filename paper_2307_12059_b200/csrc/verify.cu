@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) verify_kernel(const int2* __restrict__ ca
                                                      const int* __restrict__ tperm, const float* __restrict__ E,
                                                      const float* __restrict__ Rel, long long N, int QT, int d,
                                                      double theta, KgcTripletDev* __restrict__ out,
-                                                     unsigned long long* res_count, long long res_cap) {
+                                                     unsigned long long* res_count, long long res_cap, int r_off) {
     long long nc = (long long)*cand_count;
     if (nc > cand_cap) nc = cand_cap;
     const int lane = threadIdx.x & 31, g = lane >> 3, s = lane & 7;
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) verify_kernel(const int2* __restrict__ ca
                 if (slot < (unsigned long long)res_cap) {
                     KgcTripletDev o;
                     o.h = hs[it];
-                    o.r = rs[it];
+                    o.r = rs[it] + r_off;  // relation index in the caller's Rel
                     o.t = ts[it];
                     o.dist = ds[it];
                     out[slot] = o;
@@ -150,12 +150,12 @@ __global__ void __launch_bounds__(256) verify_kernel(const int2* __restrict__ ca
 void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap, const int* qperm,
                    const int* tperm, const float* E, const float* Rel, long long N, int QT, int d, int norm,
                    float theta, KgcTripletDev* out, unsigned long long* res_count, long long res_cap, int num_sms,
-                   cudaStream_t s) {
+                   cudaStream_t s, int r_off) {
     const bool vec4 = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(E) | reinterpret_cast<uintptr_t>(Rel)) % 16 == 0);
     auto kern = norm == 1 ? (vec4 ? verify_kernel<1, true> : verify_kernel<1, false>)
                           : (vec4 ? verify_kernel<2, true> : verify_kernel<2, false>);
     kern<<<num_sms * 8, 256, 0, s>>>(cand, cand_count, cand_cap, qperm, tperm, E, Rel, N, QT, d, (double)theta, out,
-                                     res_count, res_cap);
+                                     res_count, res_cap, r_off);
 }
 
 }  // namespace kgc

@@ -13,7 +13,7 @@ int main(int argc, char** argv) {
     std::vector<float> E(N * d), Rl(R * d);
     FILE* f = fopen(argv[1], "rb"); fread(E.data(), 4, E.size(), f); fclose(f);
     f = fopen(argv[2], "rb"); fread(Rl.data(), 4, Rl.size(), f); fclose(f);
-    kgc_ctx* ctx; kgc_options o; kgc_default_options(&o); o.l2_engine = 1;
+    kgc_ctx* ctx; kgc_options o; kgc_default_options(&o); o.l2_engine = 1; o.pivots = getenv("PIVOTS") ? atoi(getenv("PIVOTS")) : 1;
     if (kgc_create(&ctx, &o)) { printf("create: %s\n", kgc_last_error(nullptr)); return 1; }
     for (int rep = 0; rep < 2; ++rep) {
         kgc_debug_tc_prof(nullptr, 1);
@@ -22,7 +22,7 @@ int main(int argc, char** argv) {
         kgc_debug_tc_prof(h, 0);
         kgc_stats_t st; kgc_stats(ctx, &st);
         const char* nm[] = {"producer b_empty", "mma a_full", "mma acc_empty", "mma b_full", "epi a_full", "epi acc_full", "builder a_empty"};
-        const double waiters[] = {1, 1, 1, 1, 256, 256, 128};
+        const double waiters[] = {1, 32, 32, 32, 256, 256, 128};
         double cyc = st.ms_tiles * 1e-3 * 1.965e9;
         printf("rep %d: tiles %.3f ms (~%.3g cycles/CTA), results %lld\n", rep, st.ms_tiles, cyc, (long long)st.results);
         for (int i = 0; i < 7; ++i) printf("  %-18s %6.1f%% of kernel time per waiting thread\n", nm[i], 100.0 * h[i] / waiters[i] / 148 / cyc);

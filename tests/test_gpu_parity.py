@@ -82,15 +82,28 @@ def test_pivot_invariance(norm):
     check_parity(E, Rel, norm, eps, b)
 
 
-@pytest.mark.parametrize("world", [2, 3, 5])
-def test_sharding_invariance(world):
-    """Union of the shards of `world` contexts == the 1-context set, shards disjoint."""
+@pytest.mark.parametrize("world,split", [(2, 0), (3, 0), (5, 0), (8, 0), (2, 1), (3, 1), (5, 1)])
+def test_sharding_invariance(world, split):
+    """Union of the shards of `world` contexts == the 1-context set, shards disjoint
+    (split 0: rank-local preprocessing of a query-tile range; 1: global cost split)."""
     E, Rel = generate(3000, 7, 48, seed=33)
     eps = theta_for(E, Rel, 2, 1e-3)
     full, _ = gpu_join(E, Rel, 2, eps)
-    parts = [gpu_join(E, Rel, 2, eps, rank=r, world=world)[0] for r in range(world)]
+    parts = [gpu_join(E, Rel, 2, eps, rank=r, world=world, split=split)[0] for r in range(world)]
     sets = [keyset(p) for p in parts]
     assert sum(len(s) for s in sets) == len(set().union(*sets))
+    assert set().union(*sets) == keyset(full)
+
+
+@pytest.mark.parametrize("norm", [1, 2])
+def test_rank_local_split_host_inputs(norm):
+    """Rank-local shards with HOST inputs (the Rel sub-range is copied) == full set."""
+    E, Rel = generate(1500, 9, 24, seed=46)
+    eps = theta_for(E, Rel, norm, 1e-3)
+    full, _ = gpu_join(E, Rel, norm, eps)
+    parts = [gpu_join(E, Rel, norm, eps, device_inputs=False, rank=r, world=4)[0] for r in range(4)]
+    sets = [keyset(p) for p in parts]
+    assert sum(len(s) for s in sets) == len(set().union(*sets)) == len(keyset(full))
     assert set().union(*sets) == keyset(full)
 
 
@@ -277,7 +290,7 @@ def test_multipivot_equals_single_pivot(norm):
     assert sb["tile_pairs_surviving"] < sb["tile_pairs_total"]
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_multipivot_sharding_invariance(world):
     E, Rel = generate(3000, 7, 48, seed=42)
     eps = theta_for(E, Rel, 2, 1e-3)
