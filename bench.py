@@ -375,6 +375,53 @@ def run_ours(args, cfg, thresholds):
     return 0
 
 
+def run_emulated_ranks(args, cfg, thresholds):
+    """Every shard of a W-rank run, one after the other on one GPU (device time per
+    shard, CUDA events, L2 flushed before each).  The data path has no collective,
+    so max over shards projects the N=W step time (NCCL count all-reduce excluded)."""
+    import torch
+
+    from paper_2307_12059_b200 import kgc
+    W = args.emulate_ranks
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream()
+    N, R, d = cfg.N, cfg.R, cfg.d
+    eps = {n: float(thresholds[args.config][f"L{n}@{args.hit:g}"]["theta"]) for n in args.norms}
+    E_h, Rel_h = generate_config(args.config)
+    Et, Rt = torch.from_numpy(E_h).to(dev), torch.from_numpy(Rel_h).to(dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    out = {"emulated_ranks": W, "config": args.config, "pivots": args.pivots, "shard_ms": []}
+    for rank in range(W):
+        joins = {n: kgc.Join(device=0, rank=rank, world=W, pivots=args.pivots, stream=stream.cuda_stream)
+                 for n in args.norms}
+        for _ in range(max(1, args.warmup)):
+            for n in args.norms:
+                joins[n].run(Et, Rt, n, eps[n])
+        times = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for n in args.norms:
+                joins[n].run(Et, Rt, n, eps[n])
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        out["shard_ms"].append(statistics.mean(times))
+        if rank == 0:
+            out["rank0_phases"] = {f"L{n}": {k: round(v, 3) for k, v in joins[n].stats().items()
+                                             if k.startswith("ms_") or k in ("launches", "work_items_mine",
+                                                                             "tile_pairs_mine")}
+                                   for n in args.norms}
+        for j in joins.values():
+            j.close()
+    ms = max(out["shard_ms"])
+    out["projected_ms_per_step"] = ms
+    out["projected_value"] = float(N) * N * R * len(args.norms) / (ms / 1e3)
+    print(json.dumps(out), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -388,6 +435,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=256, help="(h,r) rows per reference step")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="diagnostic: on ONE GPU run each of W shards in turn and print the per-shard device times "
+                         "(projects the N=W device time; not the official line)")
     ap.add_argument("--pivots", default="auto",
                     help="1 = the paper's single pivot; 2..8 = multi-pivot pruning; auto = best measured per config")
     args = ap.parse_args()
@@ -400,6 +450,8 @@ def main():
     thresholds = load_thresholds()
     if args.impl == "reference":
         return run_reference(args, cfg, thresholds)
+    if args.emulate_ranks:
+        return run_emulated_ranks(args, cfg, thresholds)
     return run_ours(args, cfg, thresholds)
 
 

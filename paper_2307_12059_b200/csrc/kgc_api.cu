@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/kgc.h"
 #include "kgc_internal.h"
@@ -43,7 +44,7 @@ struct kgc_ctx {
     std::string err;
     DevBuf E, Rel, pivot, kt, kq, mm_t, mm_q, sk0, sv0, sk1, sv1, counts, scan_tmp, qperm, qskey, tperm, tskey, tmin,
         tmax, cmax, cmin, ranges, cost, cum, nitem, item_off, items, item_tiles, item_cum, Qp, qs, Tp, T2, tstile, cand,
-        res, ctr, mpP, mpkt, mpkq, mpmm_t, mpmm_q, mpc0, mpc1, tbmin, tbmax, qbmin, qbmax, tile_list;
+        res, ctr, est_hist, est_cost, mpP, mpkt, mpkq, mpmm_t, mpmm_q, mpc0, mpc1, tbmin, tbmax, qbmin, qbmax, tile_list;
     long long cand_cap = 0, res_cap = 0;
     long long n_results = -1;
     kgc_stats_t st{};
@@ -206,7 +207,7 @@ void kgc_destroy(kgc_ctx* ctx) {
                       &ctx->qperm, &ctx->qskey,  &ctx->tperm,  &ctx->tskey, &ctx->tmin,   &ctx->tmax,   &ctx->cmax,
                       &ctx->cmin,  &ctx->ranges, &ctx->cost,   &ctx->cum,   &ctx->nitem,  &ctx->item_off,
                       &ctx->items, &ctx->item_tiles, &ctx->item_cum, &ctx->Qp,     &ctx->qs,     &ctx->Tp,    &ctx->T2,     &ctx->tstile, &ctx->cand,
-                      &ctx->res,   &ctx->ctr,  &ctx->mpP,   &ctx->mpkt,  &ctx->mpkq,  &ctx->mpmm_t, &ctx->mpmm_q,
+                      &ctx->res,   &ctx->ctr,  &ctx->est_hist, &ctx->est_cost, &ctx->mpP,   &ctx->mpkt,  &ctx->mpkq,  &ctx->mpmm_t, &ctx->mpmm_q,
                       &ctx->mpc0,  &ctx->mpc1, &ctx->tbmin, &ctx->tbmax, &ctx->qbmin, &ctx->qbmax, &ctx->tile_list};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
@@ -621,6 +622,63 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     return KGC_OK;
 }
 
+// Query-tile range [a, b) of this rank: cumulative estimated cost, each
+// relation's estimate spread evenly over its QT query tiles.
+static int split_range(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long long N, long long R, int d, int norm,
+                       float eps, long long QT, long long* a, long long* b, const float** E_dev, const float** Rel_dev,
+                       long long* h2d) {
+    cudaStream_t s = ctx->stream;
+    const float* E = E_in;
+    const float* Rel = Rel_in;
+    *h2d = 0;
+    if (!is_device_ptr(E_in, ctx->device)) {
+        CK(ensure(ctx->E, (size_t)N * d * 4));
+        CK(cudaMemcpyAsync(ctx->E.p, E_in, (size_t)N * d * 4, cudaMemcpyDefault, s));
+        E = P<float>(ctx->E);
+        *h2d += (long long)N * d * 4;
+    }
+    if (!is_device_ptr(Rel_in, ctx->device)) {
+        CK(ensure(ctx->Rel, (size_t)R * d * 4));
+        CK(cudaMemcpyAsync(ctx->Rel.p, Rel_in, (size_t)R * d * 4, cudaMemcpyDefault, s));
+        Rel = P<float>(ctx->Rel);
+        *h2d += (long long)R * d * 4;
+    }
+    *E_dev = E;
+    *Rel_dev = Rel;
+    CK(ensure(ctx->kt, (size_t)N * 4));
+    CK(ensure(ctx->mm_t, 2 * 4));
+    CK(ensure(ctx->est_hist, 4096 * 4));
+    CK(ensure(ctx->est_cost, (size_t)R * 8));
+    launch_split_estimate(E, Rel, N, R, d, norm, eps, P<float>(ctx->kt), P<unsigned>(ctx->mm_t),
+                          P<unsigned>(ctx->est_hist), P<double>(ctx->est_cost), s);
+    LAUNCHED(5);
+    std::vector<double> cost((size_t)R);
+    CK(cudaMemcpyAsync(cost.data(), ctx->est_cost.p, (size_t)R * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double total = 0.0;
+    for (double c : cost) total += c;
+    const int W = ctx->opt.world, k = ctx->opt.rank;
+    // first query tile whose cumulative cost before it reaches t: relation-granular scan,
+    // then uniform within the relation
+    auto first_at = [&](double t) -> long long {
+        double acc = 0.0;
+        for (long long r = 0; r < R; ++r) {
+            const double c = cost[(size_t)r];
+            if (acc + c > t) {
+                long long qt = (long long)std::ceil((t - acc) / c * (double)QT);
+                if (qt < 0) qt = 0;
+                if (qt > QT) qt = QT;
+                return r * QT + qt;
+            }
+            acc += c;
+        }
+        return R * QT;
+    };
+    *a = k == 0 ? 0 : first_at(total * k / W);
+    *b = k == W - 1 ? R * QT : first_at(total * (k + 1) / W);
+    return KGC_OK;
+}
+
 extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t N, int64_t R, int32_t d, int32_t norm,
                         float eps) {
     if (!ctx) return KGC_EINVAL;
@@ -657,23 +715,27 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(ctx->device);
-    int rc;
+    int rc = KGC_OK;
     if (ctx->opt.world > 1 && ctx->opt.split == 0) {
-        // rank-local split: equal query-tile ranges, preprocessing restricted to the relations they touch
+        // Rank-local split: query-tile ranges balanced by an estimated per-relation cost
+        // (launch_split_estimate); each rank then preprocesses only the relations its range touches.
         const long long QT = (N + BM - 1) / BM, nq = R * QT;
-        const long long a = nq * ctx->opt.rank / ctx->opt.world, b = nq * (ctx->opt.rank + 1) / ctx->opt.world;
-        if (a >= b) {
+        long long a = 0, b = 0, h2d = 0;
+        const float *Ed = E, *Rd = Rel;
+        rc = split_range(ctx, E, Rel, N, R, d, norm, eps, QT, &a, &b, &Ed, &Rd, &h2d);
+        if (rc == KGC_OK && a >= b) {
             memset(&ctx->st, 0, sizeof ctx->st);
             ctx->st.N = N; ctx->st.R = R; ctx->st.d = d; ctx->st.norm = norm; ctx->st.eps = eps;
             ctx->st.rank = ctx->opt.rank; ctx->st.world = ctx->opt.world;
             ctx->st.triplets = (double)N * (double)N * (double)R;
             ctx->n_results = 0;
             ctx->have_join = true;
-            rc = KGC_OK;
-        } else {
+        } else if (rc == KGC_OK) {
+            (void)nq;
             const long long r_lo = a / QT, r_hi = (b - 1) / QT + 1;
-            rc = join_impl(ctx, E, Rel + r_lo * d, N, r_hi - r_lo, d, norm, eps, (int)r_lo, a - r_lo * QT,
+            rc = join_impl(ctx, Ed, Rd + r_lo * d, N, r_hi - r_lo, d, norm, eps, (int)r_lo, a - r_lo * QT,
                            b - r_lo * QT, R);
+            ctx->st.h2d_bytes += h2d;
         }
     } else {
         rc = join_impl(ctx, E, Rel, N, R, d, norm, eps, 0, -1, -1, R);

@@ -95,6 +95,8 @@ void launch_stage_queries(const float* E, const float* Rel, const int* qperm, lo
 void launch_stage_half(const float* E, const float* Rel, const int* perm, long long N, int d, int Kpad, int ROWS,
                        int QT, int tile0, int ntiles, float theta, float gam, void* out, float4* qs, float* rt,
                        cudaStream_t s);
+void launch_split_estimate(const float* E, const float* Rel, long long N, long long R, int d, int norm, float theta,
+                           float* kt, unsigned int* mm, unsigned int* hist, double* cost, cudaStream_t s);
 void launch_absmax(const float* E, long long nE, const float* Rel, long long nR, unsigned int* out, cudaStream_t s);
 
 // ---- multi-pivot pruning (pivots.cu) ----

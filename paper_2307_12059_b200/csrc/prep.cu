@@ -759,6 +759,95 @@ __global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ E,
     }
 }
 
+// ------------------------------------------------------ split cost estimate
+// For the rank-local multi-GPU split: estimated surviving work per relation
+// from Lemma 1 at element level with the zero pivot -- a histogram of tail
+// keys ||t||_p (ESTB bins) and S sampled queries per relation; cost_r =
+// (N / S) * sum over samples of #tails with |key(q) - key(t)| <= theta (bin
+// resolution).  Integer histogram + fixed-order per-relation sums: identical
+// on every rank.  Only steers load balance; never what is computed.
+constexpr int ESTB = 4096, EST_S = 256;
+
+__global__ void est_tail_keys_kernel(const float* __restrict__ E, long long N, int d, int norm, float* kt,
+                                     unsigned int* mm) {
+    float mn = FLT_MAX, mx = 0.f;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+        float s = 0.f;
+        for (int k = 0; k < d; ++k) {
+            const float v = E[i * d + k];
+            s = norm == 1 ? s + fabsf(v) : fmaf(v, v, s);
+        }
+        const float key = norm == 2 ? sqrtf(s) : s;
+        kt[i] = key;
+        mn = fminf(mn, key);
+        mx = fmaxf(mx, key);
+    }
+    mn = warp_min_f(mn);
+    mx = warp_max_f(mx);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], __float_as_uint(mn));
+        atomicMax(&mm[1], __float_as_uint(mx));
+    }
+}
+
+__global__ void est_hist_kernel(const float* __restrict__ kt, long long N, const unsigned int* mm, unsigned int* hist) {
+    const float lo = __uint_as_float(mm[0]), hi = __uint_as_float(mm[1]);
+    const float sc = hi > lo ? (float)ESTB / (hi - lo) : 0.f;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+        int b = (int)((kt[i] - lo) * sc);
+        b = b < 0 ? 0 : (b >= ESTB ? ESTB - 1 : b);
+        atomicAdd(&hist[b], 1u);
+    }
+}
+
+// one block per relation; thread s < EST_S takes head h = s N / EST_S
+__global__ void est_relation_cost_kernel(const float* __restrict__ E, const float* __restrict__ Rel, long long N,
+                                         int d, int norm, float theta, const unsigned int* mm,
+                                         const unsigned int* __restrict__ hist, double* cost) {
+    __shared__ unsigned int cum[ESTB + 1];
+    __shared__ double part[EST_S];
+    const long long r = blockIdx.x;
+    const float lo = __uint_as_float(mm[0]), hi = __uint_as_float(mm[1]);
+    const float sc = hi > lo ? (float)ESTB / (hi - lo) : 0.f;
+    if (threadIdx.x == 0) {  // inclusive prefix, fixed order
+        unsigned int c = 0;
+        cum[0] = 0;
+        for (int b = 0; b < ESTB; ++b) { c += hist[b]; cum[b + 1] = c; }
+    }
+    __syncthreads();
+    const int s = threadIdx.x;
+    double cnt = 0.0;
+    if (s < EST_S && N > 0) {
+        const long long h = (long long)s * N / EST_S;
+        float acc = 0.f;
+        for (int k = 0; k < d; ++k) {
+            const float v = E[h * d + k] + Rel[r * d + k];
+            acc = norm == 1 ? acc + fabsf(v) : fmaf(v, v, acc);
+        }
+        const float key = norm == 2 ? sqrtf(acc) : acc;
+        int b0 = (int)floorf((key - theta - lo) * sc), b1 = (int)floorf((key + theta - lo) * sc);
+        b0 = b0 < 0 ? 0 : (b0 > ESTB ? ESTB : b0);
+        b1 = b1 < -1 ? -1 : (b1 >= ESTB ? ESTB - 1 : b1);
+        cnt = b1 >= b0 ? (double)(cum[b1 + 1] - cum[b0]) : 0.0;
+    }
+    if (s < EST_S) part[s] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < EST_S; ++i) t += part[i];
+        cost[r] = t * (double)N / EST_S + 1.0;  // +1: never a zero-cost relation
+    }
+}
+
+void launch_split_estimate(const float* E, const float* Rel, long long N, long long R, int d, int norm, float theta,
+                           float* kt, unsigned int* mm, unsigned int* hist, double* cost, cudaStream_t s) {
+    init_minmax_kernel<<<1, 32, 0, s>>>(mm, 1);
+    cudaMemsetAsync(hist, 0, ESTB * sizeof(unsigned int), s);
+    est_tail_keys_kernel<<<grid_for(N, 256), 256, 0, s>>>(E, N, d, norm, kt, mm);
+    est_hist_kernel<<<grid_for(N, 256), 256, 0, s>>>(kt, N, mm, hist);
+    est_relation_cost_kernel<<<(unsigned)R, EST_S, 0, s>>>(E, Rel, N, d, norm, theta, mm, hist, cost);
+}
+
 // ------------------------------------------------------------ FP16x2 staging
 // L1 FP16x2 engine operands: half2 words (dims 2p, 2p + 1) at p * ROWS + i.
 // Per row: R = sum_k |v_k - fp16(v_k)| (each difference exact in FP32, sum
