@@ -96,8 +96,8 @@ typedef struct {
     float eps;
     int32_t rank, world;
     double triplets;              /* N*N*R candidate triplets (PAPER.md:460 counts 14951^2 x 2690) */
-    int64_t query_tile_rows;      /* rows per query tile (128)                                     */
-    int64_t tail_tile_rows;       /* rows per tail tile (256 for the L2 engine, 128 for L1)        */
+    int64_t query_tile_rows;      /* rows per query tile (128 tensor cores / FP16x2, 64 FP32 SIMT) */
+    int64_t tail_tile_rows;       /* rows per tail tile (256 tensor cores, 128 FP16x2, 64 FP32 SIMT) */
     int64_t query_tiles;          /* per relation                                                  */
     int64_t tail_tiles;
     int64_t tile_pairs_total;     /* R * query_tiles * tail_tiles                                  */

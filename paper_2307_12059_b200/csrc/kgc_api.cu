@@ -104,6 +104,15 @@ static T* P(DevBuf& b) {
     return reinterpret_cast<T*>(b.p);
 }
 
+// Engine choice and the plan's query-tile height (tensor cores / FP16x2: 128, FP32 SIMT: 64).
+static bool use_tc(const kgc_ctx* ctx, int norm, int d) {
+    return norm == 2 && ctx->opt.l2_engine != 2 && ((d + 7) / 8) * 8 <= TC_MAX_KPAD;
+}
+static int plan_bq(const kgc_ctx* ctx, int norm, int d) {
+    if (use_tc(ctx, norm, d)) return BM;
+    return (norm == 1 && ctx->opt.l1_engine == 1) ? BN_HALF : SIMT_T;
+}
+
 // Relative margin covering the FP32 pivot keys.
 static float mp_relm(int d) { return (float)(d + 8) * 1.1920928955078125e-07f; }
 
@@ -279,14 +288,17 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     st.world = ctx->opt.world;
     st.triplets = (double)N * (double)N * (double)R_global;
 
-    const bool tc = norm == 2 && ctx->opt.l2_engine != 2 && ((d + 7) / 8) * 8 <= TC_MAX_KPAD;
+    const bool tc = use_tc(ctx, norm, d);
     if (norm == 2 && ctx->opt.l2_engine == 1 && !tc) {
         set_err(ctx, "l2_engine=1 (tcgen05) supports d <= %d", TC_MAX_KPAD);
         return KGC_EINVAL;
     }
     const int Kpad = ((d + 7) / 8) * 8;
-    const int BN = tc ? BN_TC : BN_SIMT;
-    const int QT = (int)((N + BM - 1) / BM);
+    // tile geometry of the plan: tensor cores 128 x 256; FP16x2 L1 128 x 128; FP32 SIMT 64 x 64
+    const bool half_req = norm == 1 && ctx->opt.l1_engine == 1;
+    const int bq = plan_bq(ctx, norm, d);
+    const int BN = tc ? BN_TC : (half_req ? BN_HALF : SIMT_T);
+    const int QT = (int)((N + bq - 1) / bq);
     const int TT = (int)((N + BN - 1) / BN);
     const long long nq = R * (long long)QT;
     int chunk = ctx->opt.chunk_tiles > 0 ? ctx->opt.chunk_tiles : (tc ? 16 : 8);
@@ -299,7 +311,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     ctx->QT = QT;
     ctx->TT = TT;
     ctx->BN = BN;
-    st.query_tile_rows = BM;
+    st.query_tile_rows = bq;
     st.tail_tile_rows = BN;
     st.query_tiles = QT;
     st.tail_tiles = TT;
@@ -395,7 +407,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         launch_tail_tile_bounds(P<float>(ctx->tskey), N, BN, TT, P<float>(ctx->tmin), P<float>(ctx->tmax),
                                 P<float>(ctx->cmax), P<float>(ctx->cmin), s, &ctx->launches);
         LAUNCHED(0);
-        launch_query_ranges(P<float>(ctx->qskey), N, R, QT, TT, P<float>(ctx->cmax), P<float>(ctx->cmin), eps,
+        launch_query_ranges(P<float>(ctx->qskey), N, R, QT, TT, bq, P<float>(ctx->cmax), P<float>(ctx->cmin), eps,
                             ctx->opt.prune, P<int2>(ctx->ranges), P<long long>(ctx->cost), s);
         LAUNCHED(1);
     } else {
@@ -443,7 +455,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         // ---- a4: K-dim tile boxes and the L_inf test of every tile pair
         launch_mp_boxes(P<float>(ctx->mpkt), P<unsigned>(ctx->tperm), 1, N, BN, TT, K, P<float>(ctx->tbmin),
                         P<float>(ctx->tbmax), s);
-        launch_mp_boxes(P<float>(ctx->mpkq), P<unsigned>(ctx->qperm), R, N, BM, QT, K, P<float>(ctx->qbmin),
+        launch_mp_boxes(P<float>(ctx->mpkq), P<unsigned>(ctx->qperm), R, N, bq, QT, K, P<float>(ctx->qbmin),
                         P<float>(ctx->qbmax), s);
         LAUNCHED(2);
         launch_mp_count(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tbmin), P<float>(ctx->tbmax), nq, TT,
@@ -504,7 +516,11 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     // FP16x2 L1 engine only on request (l1_engine = 1) and when every |value| <= 1000 (FP16 range and
     // partial sums safe).  Measured on B200 it is no faster than FP32: HADD2 issues at half the FADD rate,
     // so two elements per instruction buy nothing (scripts/micro/l1_inner.cu).
-    const bool half = norm == 1 && ctx->opt.l1_engine == 1 && __uint_as_float_host(h1.c.absmax_bits) <= 1000.0f;
+    const bool half = half_req && __uint_as_float_host(h1.c.absmax_bits) <= 1000.0f;
+    if (half_req && !half) {
+        set_err(ctx, "l1_engine=1 (FP16x2) needs every |E|, |Rel| value <= 1000; use l1_engine 0 or 2");
+        return KGC_EINVAL;
+    }
     st.engine = tc ? 1 : (half ? 3 : 2);
     const float gam = 1.0f + 10.0f * 4.8828125e-04f + (float)(d / 8 + 4) * 1.1920928955078125e-07f;
     if (n_items > 0) {
@@ -512,11 +528,11 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(ensure(ctx->T2, (size_t)TT * BN * 4));
         CK(ensure(ctx->tstile, (size_t)TT * 8));
         if (half) {
-            CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * BM * Kpad * 2));
-            CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * BM * 16));
+            CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * bq * Kpad * 2));
+            CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * bq * 16));
             launch_stage_half(E, nullptr, P<int>(ctx->tperm), N, d, Kpad, BN, 1, 0, TT, eps, gam, ctx->Tp.p, nullptr,
                               P<float>(ctx->T2), s);
-            launch_stage_half(E, Rel, P<int>(ctx->qperm), N, d, Kpad, BM, QT, tq0, tq1 - tq0, eps, gam, ctx->Qp.p,
+            launch_stage_half(E, Rel, P<int>(ctx->qperm), N, d, Kpad, bq, QT, tq0, tq1 - tq0, eps, gam, ctx->Qp.p,
                               P<float4>(ctx->qs), nullptr, s);
             LAUNCHED(2);
         } else {
@@ -524,9 +540,9 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                                P<float>(ctx->T2), P<float2>(ctx->tstile), s);
             LAUNCHED(1);
             if (!tc) {  // the tensor-core engine forms its query tiles on the fly
-                CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * BM * Kpad * 4));
-                CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * BM * 16));
-                launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, tq0, tq1, 0, norm, eps,
+                CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * bq * Kpad * 4));
+                CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * bq * 16));
+                launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, bq, tq0, tq1, 0, norm, eps,
                                      P<float>(ctx->Qp), P<float4>(ctx->qs), s);
                 LAUNCHED(1);
             }
@@ -559,6 +575,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             tp.sched = e ? atoi(e) : (tc ? 0 : 1);
         }
         tp.Kpad = Kpad;
+        tp.bq = bq;
+        tp.bn = BN;
         tp.tq0 = tq0;
         tp.N = (int)N;
         tp.theta = eps;
@@ -582,7 +600,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(cudaEventRecord(ctx->ev[EV_TILES], s));
         if (n_items > 0) {
             launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, P<int>(ctx->qperm), P<int>(ctx->tperm), E,
-                          Rel, N, QT, d, norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p), &dctr->res,
+                          Rel, N, QT, bq, d, norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p), &dctr->res,
                           ctx->res_cap, ctx->num_sms, s, r_off);
             LAUNCHED(1);
         }
@@ -691,7 +709,7 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
                 norm, (double)eps);
         return KGC_EINVAL;
     }
-    if (N > INT_MAX / 2 || (double)R * (double)((N + BM - 1) / BM) * BM > 2.0e9) {
+    if (N > INT_MAX / 2 || (double)R * (double)((N + SIMT_T - 1) / SIMT_T + 1) * BM > 2.0e9) {  // rowid fits int32
         set_err(ctx, "kgc_join: N*R too large for 32-bit row ids");
         return KGC_EINVAL;
     }
@@ -719,7 +737,8 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
     if (ctx->opt.world > 1 && ctx->opt.split == 0) {
         // Rank-local split: query-tile ranges balanced by an estimated per-relation cost
         // (launch_split_estimate); each rank then preprocesses only the relations its range touches.
-        const long long QT = (N + BM - 1) / BM, nq = R * QT;
+        const long long bq = plan_bq(ctx, norm, d);
+        const long long QT = (N + bq - 1) / bq, nq = R * QT;
         long long a = 0, b = 0, h2d = 0;
         const float *Ed = E, *Rd = Rel;
         rc = split_range(ctx, E, Rel, N, R, d, norm, eps, QT, &a, &b, &Ed, &Rd, &h2d);

@@ -8,7 +8,8 @@ namespace kgc {
 
 constexpr int BM = 128;          // query rows per tile (= TMEM lanes = UMMA M)
 constexpr int BN_TC = 256;       // tail rows per tile, tensor-core engine (UMMA N)
-constexpr int BN_SIMT = 128;     // tail rows per tile, SIMT engines
+constexpr int BN_HALF = 128;     // tile rows (query and tail), FP16x2 L1 engine
+constexpr int SIMT_T = 64;       // tile rows (query and tail), FP32 SIMT engines
 constexpr int SORT_IPB = 2048;   // radix-sort items per block (256 threads x 8)
 constexpr int TC_MAX_KPAD = 256; // tensor-core engine supports d <= 256
 constexpr int MP_MAX = 8;        // multi-pivot pruning: at most 8 pivots
@@ -43,6 +44,7 @@ struct TileParams {
     long long total_tiles;
     int sched;                  // 0 = round-robin items, 1 = contiguous cost-balanced blocks
     int Kpad;
+    int bq, bn;             // query / tail tile rows of the plan
     int tq0;                // first staged query tile
     int N;                  // tails (valid columns are < N)
     float theta;
@@ -78,7 +80,7 @@ void scan_exclusive_i64(const long long* in, long long* out, size_t n, long long
                         cudaStream_t s, int* launches);
 void launch_tail_tile_bounds(const float* tskey, long long N, int BN, int TT, float* tmin, float* tmax,
                              float* cmax, float* cmin, cudaStream_t s, int* launches);
-void launch_query_ranges(const float* qskey, long long N, long long R, int QT, int TT, const float* cmax,
+void launch_query_ranges(const float* qskey, long long N, long long R, int QT, int TT, int bq, const float* cmax,
                          const float* cmin, float theta, int prune, int2* ranges, long long* cost,
                          cudaStream_t s);
 void launch_shard_items(const int2* ranges, const long long* cost, const long long* cum, long long nq,
@@ -88,7 +90,7 @@ void launch_shard_items(const int2* ranges, const long long* cost, const long lo
 void launch_stage_tails(const float* E, const int* tperm, long long N, int d, int Kpad, int BN, int TT,
                         int tc_layout, float* Tp, float* T2, float2* tstile, cudaStream_t s);
 void launch_stage_queries(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad,
-                          int QT, int tq0, int tq1, int tc_layout, int norm, float theta, float* Qp,
+                          int QT, int bq, int tq0, int tq1, int tc_layout, int norm, float theta, float* Qp,
                           float4* qs, cudaStream_t s);
 // FP16x2 L1 engine staging: tiles of half2 words, element (i, k-pair p) at p * ROWS + i;
 // per row the exact residual R = sum_k |v_k - fp16(v_k)| (rounded up)
@@ -133,7 +135,7 @@ constexpr int HALF_FLUSH_PAIRS = 8;  // FP16x2 engine: flush to FP32 every 16 di
 struct KgcTripletDev { int h, r, t; float dist; };
 void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap,
                    const int* qperm, const int* tperm, const float* E, const float* Rel, long long N, int QT,
-                   int d, int norm, float theta, KgcTripletDev* out, unsigned long long* res_count,
+                   int bq, int d, int norm, float theta, KgcTripletDev* out, unsigned long long* res_count,
                    long long res_cap, int num_sms, cudaStream_t s, int r_off);
 
 }  // namespace kgc

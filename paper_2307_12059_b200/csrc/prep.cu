@@ -511,15 +511,15 @@ void launch_tail_tile_bounds(const float* tskey, long long N, int BN, int TT, fl
 // relative so that no pair with dist3 <= theta is ever pruned (DESIGN.md
 // "Floating-point rigor of pruning").
 __global__ void query_ranges_kernel(const float* __restrict__ qskey, long long N, long long R, int QT, int TT,
-                                    const float* __restrict__ cmax, const float* __restrict__ cmin, float theta,
-                                    int prune, int2* ranges, long long* cost) {
+                                    int bq, const float* __restrict__ cmax, const float* __restrict__ cmin,
+                                    float theta, int prune, int2* ranges, long long* cost) {
     const int lane = threadIdx.x & 31;
     long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const long long nq = R * (long long)QT;
     for (long long tq = warp; tq < nq; tq += nwarps) {
         long long r = tq / QT, qt = tq - r * QT;
-        long long b = qt * BM, e = min(N, b + BM);
+        long long b = qt * bq, e = min(N, b + bq);
         float mn = FLT_MAX, mx = -FLT_MAX;
         for (long long i = b + lane; i < e; i += 32) {
             float k = qskey[r * N + i];
@@ -553,9 +553,9 @@ __global__ void query_ranges_kernel(const float* __restrict__ qskey, long long N
     }
 }
 
-void launch_query_ranges(const float* qskey, long long N, long long R, int QT, int TT, const float* cmax,
+void launch_query_ranges(const float* qskey, long long N, long long R, int QT, int TT, int bq, const float* cmax,
                          const float* cmin, float theta, int prune, int2* ranges, long long* cost, cudaStream_t s) {
-    query_ranges_kernel<<<grid_for(R * QT * 32, 256), 256, 0, s>>>(qskey, N, R, QT, TT, cmax, cmin, theta, prune,
+    query_ranges_kernel<<<grid_for(R * QT * 32, 256), 256, 0, s>>>(qskey, N, R, QT, TT, bq, cmax, cmin, theta, prune,
                                                                     ranges, cost);
 }
 
@@ -926,14 +926,14 @@ void launch_stage_tails(const float* E, const int* tperm, long long N, int d, in
 }
 
 void launch_stage_queries(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad, int QT,
-                          int tq0, int tq1, int tc_layout, int norm, float theta, float* Qp, float4* qs,
+                          int bq, int tq0, int tq1, int tc_layout, int norm, float theta, float* Qp, float4* qs,
                           cudaStream_t s) {
     if (tq1 <= tq0) return;
     if (tc_layout)
-        stage_kernel<true><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, BM, QT, tq0, norm, theta, Qp, qs,
+        stage_kernel<true><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, bq, QT, tq0, norm, theta, Qp, qs,
                                                      nullptr, nullptr);
     else
-        stage_kernel<false><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, BM, QT, tq0, norm, theta, Qp, qs,
+        stage_kernel<false><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, bq, QT, tq0, norm, theta, Qp, qs,
                                                       nullptr, nullptr);
 }
 

@@ -2,13 +2,13 @@
 // pipes (SURVEY §8(a) row a6, and the L2 "SIMT" control engine).
 //
 // L1 (TransE ||h + r - t||_1) has no dense-contraction form, so
-// it runs as register-tiled |q - t| accumulation: a 128-query x 128-tail
-// tile per CTA, 256 threads, an 8 x 8 micro-tile per thread (FADD + FADD|.|
-// per element and k).  Query and tail K-chunks stream through a 3-stage
-// ring fed by 1-D bulk TMA copies (full barriers with transaction counts; the
-// last warp to release a stage refills it, so there is no CTA-wide barrier
-// and no blocking producer in the main loop; shared memory independent of d,
-// two CTAs per SM).  A pair whose FP32 distance is within the row's
+// it runs as register-tiled |q - t| accumulation: a 64-query x 64-tail tile
+// per CTA (small tiles prune better), 64 threads, an 8 x 8 micro-tile per
+// thread (FADD + FADD|.| per element and k).  Query and tail K-chunks stream
+// through a double buffer fed by 1-D bulk TMA copies (full barriers with
+// transaction counts; the last warp to release a stage refills it, so there is
+// no CTA-wide barrier and no blocking producer in the main loop; shared memory
+// independent of d, 7 CTAs per SM).  A pair whose FP32 distance is within the row's
 // rigorous bound (stage kernel) becomes a
 // candidate; the FP64 re-check (verify.cu) decides.
 #include <cuda_fp16.h>
@@ -56,18 +56,25 @@ struct ChunkIter {
     }
 };
 
-template <int NORM>
-__global__ void __launch_bounds__(256, 2) tiles_simt_kernel(TileParams p) {
+// TBM x TBN tile, 256 threads in a (TBM/TM) x (TBN/TN) grid, TM x TN register
+// micro-tile per thread.
+template <int NORM, int TBM, int TBN, int TM, int TN, int KC = SIMT_KC, int NSTAGE = SIMT_NS>
+__global__ void __launch_bounds__((TBM / TM) * (TBN / TN)) tiles_simt_kernel(TileParams p) {
+    constexpr int NT = (TBM / TM) * (TBN / TN);
+    static_assert(NT % 32 == 0 && NT <= 256 && TM * TN <= 64, "tile shape");
+    constexpr int SIMT_KC = KC;
+    constexpr int SIMT_NS = NSTAGE;
+    constexpr int GX = TBN / TN;  // threads along the tail dimension
     extern __shared__ __align__(128) uint8_t smem[];
     const int Kpad = p.Kpad;
     const int nkc = (Kpad + SIMT_KC - 1) / SIMT_KC;
-    // stage s: query chunk [SIMT_KC][BM] followed by tail chunk [SIMT_KC][BN]
+    // stage s: query chunk [SIMT_KC][TBM] followed by tail chunk [SIMT_KC][TBN]
     float* St = reinterpret_cast<float*>(smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(St + SIMT_NS * SIMT_KC * (BM + BN_SIMT));
+    uint64_t* full = reinterpret_cast<uint64_t*>(St + SIMT_NS * SIMT_KC * (TBM + TBN));
     int* released = reinterpret_cast<int*>(full + SIMT_NS);  // warps done with each stage
 
     const int tid = threadIdx.x, lane = tid & 31;
-    const int ty = tid >> 4, tx = tid & 15;
+    const int ty = tid / GX, tx = tid % GX;
     if (tid == 0) {
         for (int s = 0; s < SIMT_NS; ++s) {
             mbar_init(&full[s], 1);
@@ -77,18 +84,16 @@ __global__ void __launch_bounds__(256, 2) tiles_simt_kernel(TileParams p) {
     }
     __syncthreads();
 
-    // Both operands stream in K-chunks (the query chunk is re-read per tail
-    // tile from L2), so shared memory does not grow with d.
     // Called by one thread once stage (g % SIMT_NS) is free.
     auto issue = [&](const ChunkIter& ci, long long g) {
         const int s = (int)(g % SIMT_NS);
         const int klen = Kpad - ci.c * SIMT_KC < SIMT_KC ? Kpad - ci.c * SIMT_KC : SIMT_KC;
-        const uint32_t qbytes = (uint32_t)klen * BM * 4, tbytes = (uint32_t)klen * BN_SIMT * 4;
-        float* dst = St + (size_t)s * SIMT_KC * (BM + BN_SIMT);
+        const uint32_t qbytes = (uint32_t)klen * TBM * 4, tbytes = (uint32_t)klen * TBN * 4;
+        float* dst = St + (size_t)s * SIMT_KC * (TBM + TBN);
         mbar_arrive_expect_tx(&full[s], qbytes + tbytes);
-        bulk_g2s(dst, p.Qp + (size_t)(ci.w.x - p.tq0) * BM * Kpad + (size_t)ci.c * SIMT_KC * BM, qbytes, &full[s]);
-        bulk_g2s(dst + SIMT_KC * BM,
-                 p.Tp + (size_t)item_tile(ci.w, ci.j, p.tile_list) * BN_SIMT * Kpad + (size_t)ci.c * SIMT_KC * BN_SIMT, tbytes,
+        bulk_g2s(dst, p.Qp + (size_t)(ci.w.x - p.tq0) * TBM * Kpad + (size_t)ci.c * SIMT_KC * TBM, qbytes, &full[s]);
+        bulk_g2s(dst + SIMT_KC * TBM,
+                 p.Tp + (size_t)item_tile(ci.w, ci.j, p.tile_list) * TBN * Kpad + (size_t)ci.c * SIMT_KC * TBN, tbytes,
                  &full[s]);
     };
 
@@ -102,37 +107,42 @@ __global__ void __launch_bounds__(256, 2) tiles_simt_kernel(TileParams p) {
         }
     }
 
-    float thr[8];
-    float acc[8][8];
+    float thr[TM];
+    float acc[TM][TN];
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < TM; ++a)
 #pragma unroll
-        for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+        for (int b = 0; b < TN; ++b) acc[a][b] = 0.f;
     long long cur_item = -1;
 
     for (long long g = 0; cs.valid(p); ++g) {
         if (cs.it != cur_item) {
             cur_item = cs.it;
 #pragma unroll
-            for (int a = 0; a < 8; ++a) thr[a] = p.qs[(size_t)(cs.w.x - p.tq0) * BM + ty * 8 + a].w;
+            for (int a = 0; a < TM; ++a) thr[a] = p.qs[(size_t)(cs.w.x - p.tq0) * TBM + ty * TM + a].w;
         }
         const int s = (int)(g % SIMT_NS);
         mbar_wait(&full[s], (uint32_t)(g / SIMT_NS) & 1u);
         const int klen = Kpad - cs.c * SIMT_KC < SIMT_KC ? Kpad - cs.c * SIMT_KC : SIMT_KC;
-        const float* qk = St + (size_t)s * SIMT_KC * (BM + BN_SIMT) + ty * 8;
-        const float* tk = St + (size_t)s * SIMT_KC * (BM + BN_SIMT) + SIMT_KC * BM + tx * 8;
+        const float* qk = St + (size_t)s * SIMT_KC * (TBM + TBN) + ty * TM;
+        const float* tk = St + (size_t)s * SIMT_KC * (TBM + TBN) + SIMT_KC * TBM + tx * TN;
 #pragma unroll 4
         for (int k = 0; k < klen; ++k) {
-            const float4 qa = *reinterpret_cast<const float4*>(qk + k * BM);
-            const float4 qb = *reinterpret_cast<const float4*>(qk + k * BM + 4);
-            const float4 ta = *reinterpret_cast<const float4*>(tk + k * BN_SIMT);
-            const float4 tb = *reinterpret_cast<const float4*>(tk + k * BN_SIMT + 4);
-            const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-            const float tv[8] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
+            float qv[TM], tv[TN];
 #pragma unroll
-            for (int a = 0; a < 8; ++a)
+            for (int a = 0; a < TM; a += 4) {
+                const float4 v = *reinterpret_cast<const float4*>(qk + k * TBM + a);
+                qv[a] = v.x; qv[a + 1] = v.y; qv[a + 2] = v.z; qv[a + 3] = v.w;
+            }
 #pragma unroll
-                for (int b = 0; b < 8; ++b) {
+            for (int b = 0; b < TN; b += 4) {
+                const float4 v = *reinterpret_cast<const float4*>(tk + k * TBN + b);
+                tv[b] = v.x; tv[b + 1] = v.y; tv[b + 2] = v.z; tv[b + 3] = v.w;
+            }
+#pragma unroll
+            for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TN; ++b) {
                     const float df = qv[a] - tv[b];
                     if (NORM == 1) acc[a][b] += fabsf(df);
                     else acc[a][b] = fmaf(df, df, acc[a][b]);
@@ -143,7 +153,7 @@ __global__ void __launch_bounds__(256, 2) tiles_simt_kernel(TileParams p) {
         __syncwarp();
         if (lane == 0) {
             __threadfence_block();
-            if (atomicAdd(&released[s], 1) == 7) {
+            if (atomicAdd(&released[s], 1) == NT / 32 - 1) {
                 released[s] = 0;
                 ChunkIter nx = cs;
 #pragma unroll 1
@@ -158,28 +168,30 @@ __global__ void __launch_bounds__(256, 2) tiles_simt_kernel(TileParams p) {
             const int j = item_tile(cs.w, cs.j, p.tile_list);
             unsigned long long hit = 0;
 #pragma unroll
-            for (int a = 0; a < 8; ++a)
+            for (int a = 0; a < TM; ++a)
 #pragma unroll
-                for (int b = 0; b < 8; ++b) hit |= (unsigned long long)(acc[a][b] <= thr[a]) << (a * 8 + b);
+                for (int b = 0; b < TN; ++b) hit |= (unsigned long long)(acc[a][b] <= thr[a]) << (a * TN + b);
             if (__any_sync(0xffffffffu, hit != 0)) {
                 // columns past the last tail are padding
-                const int colb = j * BN_SIMT + tx * 8;
+                const int colb = j * TBN + tx * TN;
 #pragma unroll
-                for (int b = 0; b < 8; ++b)
-                    if (colb + b >= p.N) hit &= ~(0x0101010101010101ull << b);
+                for (int b = 0; b < TN; ++b)
+                    if (colb + b >= p.N)
+#pragma unroll
+                        for (int a = 0; a < TM; ++a) hit &= ~(1ull << (a * TN + b));
                 unsigned long long slot = warp_reserve(__popcll(hit), p.cand_count);
                 while (hit) {
                     const int ab = __ffsll(hit) - 1;
                     if (slot < (unsigned long long)p.cand_cap)
-                        p.cand[slot] = make_int2(cs.w.x * BM + ty * 8 + (ab >> 3), colb + (ab & 7));
+                        p.cand[slot] = make_int2(cs.w.x * TBM + ty * TM + ab / TN, colb + ab % TN);
                     ++slot;
                     hit &= hit - 1;
                 }
             }
 #pragma unroll
-            for (int a = 0; a < 8; ++a)
+            for (int a = 0; a < TM; ++a)
 #pragma unroll
-                for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+                for (int b = 0; b < TN; ++b) acc[a][b] = 0.f;
         }
         cs.next(p, nkc);
     }
@@ -200,7 +212,7 @@ __global__ void __launch_bounds__(256, 1) tiles_half_l1_kernel(TileParams p) {
     const int KP = p.Kpad / 2;                         // pairs per row
     const int nkc = (KP + HKC - 1) / HKC;
     uint32_t* St = reinterpret_cast<uint32_t*>(smem);  // [stage][HKC][BM + BN] half2 words
-    uint64_t* full = reinterpret_cast<uint64_t*>(St + SIMT_NS * HKC * (BM + BN_SIMT));
+    uint64_t* full = reinterpret_cast<uint64_t*>(St + SIMT_NS * HKC * (BN_HALF + BN_HALF));
     int* released = reinterpret_cast<int*>(full + SIMT_NS);
 
     const int tid = threadIdx.x, lane = tid & 31;
@@ -219,11 +231,11 @@ __global__ void __launch_bounds__(256, 1) tiles_half_l1_kernel(TileParams p) {
     auto issue = [&](const ChunkIter& ci, long long g) {
         const int s = (int)(g % SIMT_NS);
         const int klen = KP - ci.c * HKC < HKC ? KP - ci.c * HKC : HKC;
-        const uint32_t qbytes = (uint32_t)klen * BM * 4, tbytes = (uint32_t)klen * BN_SIMT * 4;
-        uint32_t* dst = St + (size_t)s * HKC * (BM + BN_SIMT);
+        const uint32_t qbytes = (uint32_t)klen * BN_HALF * 4, tbytes = (uint32_t)klen * BN_HALF * 4;
+        uint32_t* dst = St + (size_t)s * HKC * (BN_HALF + BN_HALF);
         mbar_arrive_expect_tx(&full[s], qbytes + tbytes);
-        bulk_g2s(dst, Qw + (size_t)(ci.w.x - p.tq0) * BM * KP + (size_t)ci.c * HKC * BM, qbytes, &full[s]);
-        bulk_g2s(dst + HKC * BM, Tw + (size_t)item_tile(ci.w, ci.j, p.tile_list) * BN_SIMT * KP + (size_t)ci.c * HKC * BN_SIMT,
+        bulk_g2s(dst, Qw + (size_t)(ci.w.x - p.tq0) * BN_HALF * KP + (size_t)ci.c * HKC * BN_HALF, qbytes, &full[s]);
+        bulk_g2s(dst + HKC * BN_HALF, Tw + (size_t)item_tile(ci.w, ci.j, p.tile_list) * BN_HALF * KP + (size_t)ci.c * HKC * BN_HALF,
                  tbytes, &full[s]);
     };
 
@@ -262,21 +274,21 @@ __global__ void __launch_bounds__(256, 1) tiles_half_l1_kernel(TileParams p) {
         if (cs.it != cur_item) {
             cur_item = cs.it;
 #pragma unroll
-            for (int a = 0; a < 8; ++a) thr[a] = p.qs[(size_t)(cs.w.x - p.tq0) * BM + ty * 8 + a].w;
+            for (int a = 0; a < 8; ++a) thr[a] = p.qs[(size_t)(cs.w.x - p.tq0) * BN_HALF + ty * 8 + a].w;
         }
         const int s = (int)(g % SIMT_NS);
         mbar_wait(&full[s], (uint32_t)(g / SIMT_NS) & 1u);
         const int klen = KP - cs.c * HKC < HKC ? KP - cs.c * HKC : HKC;
-        const uint32_t* qk = St + (size_t)s * HKC * (BM + BN_SIMT) + ty * 8;
-        const uint32_t* tk = St + (size_t)s * HKC * (BM + BN_SIMT) + HKC * BM + tx * 8;
+        const uint32_t* qk = St + (size_t)s * HKC * (BN_HALF + BN_HALF) + ty * 8;
+        const uint32_t* tk = St + (size_t)s * HKC * (BN_HALF + BN_HALF) + HKC * BN_HALF + tx * 8;
         for (int k0 = 0; k0 < klen; k0 += HALF_FLUSH_PAIRS) {
             const int kend = k0 + HALF_FLUSH_PAIRS < klen ? k0 + HALF_FLUSH_PAIRS : klen;
 #pragma unroll 2
             for (int k = k0; k < kend; ++k) {
-                const uint4 qa = *reinterpret_cast<const uint4*>(qk + k * BM);
-                const uint4 qb = *reinterpret_cast<const uint4*>(qk + k * BM + 4);
-                const uint4 ta = *reinterpret_cast<const uint4*>(tk + k * BN_SIMT);
-                const uint4 tb = *reinterpret_cast<const uint4*>(tk + k * BN_SIMT + 4);
+                const uint4 qa = *reinterpret_cast<const uint4*>(qk + k * BN_HALF);
+                const uint4 qb = *reinterpret_cast<const uint4*>(qk + k * BN_HALF + 4);
+                const uint4 ta = *reinterpret_cast<const uint4*>(tk + k * BN_HALF);
+                const uint4 tb = *reinterpret_cast<const uint4*>(tk + k * BN_HALF + 4);
                 const uint32_t qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
                 const uint32_t tv[8] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
 #pragma unroll
@@ -307,7 +319,7 @@ __global__ void __launch_bounds__(256, 1) tiles_half_l1_kernel(TileParams p) {
         }
         if (cs.c == nkc - 1) {
             const int j = item_tile(cs.w, cs.j, p.tile_list);
-            const int colb = j * BN_SIMT + tx * 8;
+            const int colb = j * BN_HALF + tx * 8;
             const float4 r0 = __ldg(reinterpret_cast<const float4*>(p.Rt + colb));
             const float4 r1 = __ldg(reinterpret_cast<const float4*>(p.Rt + colb + 4));
             const float rtc[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
@@ -325,7 +337,7 @@ __global__ void __launch_bounds__(256, 1) tiles_half_l1_kernel(TileParams p) {
                 while (hit) {
                     const int ab = __ffsll(hit) - 1;
                     if (slot < (unsigned long long)p.cand_cap)
-                        p.cand[slot] = make_int2(cs.w.x * BM + ty * 8 + (ab >> 3), colb + (ab & 7));
+                        p.cand[slot] = make_int2(cs.w.x * BN_HALF + ty * 8 + (ab >> 3), colb + (ab & 7));
                     ++slot;
                     hit &= hit - 1;
                 }
@@ -341,7 +353,7 @@ __global__ void __launch_bounds__(256, 1) tiles_half_l1_kernel(TileParams p) {
 
 void launch_tiles_half_l1(const TileParams& p, int num_sms, cudaStream_t s) {
     if (p.n_items <= 0) return;
-    const size_t smem = (size_t)SIMT_NS * HKC * (BM + BN_SIMT) * 4 + 64;
+    const size_t smem = (size_t)SIMT_NS * HKC * (BN_HALF + BN_HALF) * 4 + 64;
     cudaFuncSetAttribute(tiles_half_l1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiles_half_l1_kernel, 256, smem);
@@ -351,17 +363,27 @@ void launch_tiles_half_l1(const TileParams& p, int num_sms, cudaStream_t s) {
     tiles_half_l1_kernel<<<(unsigned)g, 256, smem, s>>>(p);
 }
 
-void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t s) {
-    if (p.n_items <= 0) return;
-    const size_t smem = (size_t)SIMT_NS * SIMT_KC * (BM + BN_SIMT) * 4 + 64;
-    auto kern = norm == 1 ? tiles_simt_kernel<1> : tiles_simt_kernel<2>;
+template <int NORM, int TM, int TN, int KC, int NS = SIMT_NS>
+static void launch_simt_variant(const TileParams& p, int num_sms, cudaStream_t s) {
+    constexpr int NT = (SIMT_T / TM) * (SIMT_T / TN);
+    const size_t smem = (size_t)NS * KC * (SIMT_T + SIMT_T) * 4 + 128;
+    auto kern = tiles_simt_kernel<NORM, SIMT_T, SIMT_T, TM, TN, KC, NS>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
     if (per_sm < 1) per_sm = 1;
     long long g = (long long)num_sms * per_sm;
     if (g > p.n_items) g = p.n_items;
-    kern<<<(unsigned)g, 256, smem, s>>>(p);
+    kern<<<(unsigned)g, NT, smem, s>>>(p);
+}
+
+void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t s) {
+    if (p.n_items <= 0) return;
+    // 64 x 64 tiles, 64 threads with 8 x 8 micro-tiles, 32-wide K-chunks, double buffer:
+    // 32 KB of shared memory -> 7 CTAs per SM (register-limited).  Measured best of the
+    // micro-tile / chunk / depth sweep on c2 L1.
+    if (norm == 1) launch_simt_variant<1, 8, 8, 32, 2>(p, num_sms, s);
+    else launch_simt_variant<2, 8, 8, 32, 2>(p, num_sms, s);
 }
 
 }  // namespace kgc

@@ -49,15 +49,15 @@ __global__ void __launch_bounds__(256) verify_kernel(const int2* __restrict__ ca
                                                      const unsigned long long* __restrict__ cand_count,
                                                      long long cand_cap, const int* __restrict__ qperm,
                                                      const int* __restrict__ tperm, const float* __restrict__ E,
-                                                     const float* __restrict__ Rel, long long N, int QT, int d,
-                                                     double theta, KgcTripletDev* __restrict__ out,
+                                                     const float* __restrict__ Rel, long long N, int QT, int bq,
+                                                     int d, double theta, KgcTripletDev* __restrict__ out,
                                                      unsigned long long* res_count, long long res_cap, int r_off) {
     long long nc = (long long)*cand_count;
     if (nc > cand_cap) nc = cand_cap;
     const int lane = threadIdx.x & 31, g = lane >> 3, s = lane & 7;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    const long long rows_per_rel = (long long)QT * BM;
+    const long long rows_per_rel = (long long)QT * bq;
     const bool cache = VEC4 && d <= 32 * VMAXM;
     const int M = (d + 31) / 32;
     for (long long base = warp * 32; base < nc; base += nwarps * 32) {
@@ -148,13 +148,13 @@ __global__ void __launch_bounds__(256) verify_kernel(const int2* __restrict__ ca
 }
 
 void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap, const int* qperm,
-                   const int* tperm, const float* E, const float* Rel, long long N, int QT, int d, int norm,
+                   const int* tperm, const float* E, const float* Rel, long long N, int QT, int bq, int d, int norm,
                    float theta, KgcTripletDev* out, unsigned long long* res_count, long long res_cap, int num_sms,
                    cudaStream_t s, int r_off) {
     const bool vec4 = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(E) | reinterpret_cast<uintptr_t>(Rel)) % 16 == 0);
     auto kern = norm == 1 ? (vec4 ? verify_kernel<1, true> : verify_kernel<1, false>)
                           : (vec4 ? verify_kernel<2, true> : verify_kernel<2, false>);
-    kern<<<num_sms * 8, 256, 0, s>>>(cand, cand_count, cand_cap, qperm, tperm, E, Rel, N, QT, d, (double)theta, out,
+    kern<<<num_sms * 8, 256, 0, s>>>(cand, cand_count, cand_cap, qperm, tperm, E, Rel, N, QT, bq, d, (double)theta, out,
                                      res_count, res_cap, r_off);
 }
 

@@ -359,13 +359,18 @@ def test_l1_engines_parity(eng):
     check_parity(E, Rel, 1, eps, res)
 
 
-def test_l1_half_engine_falls_back_on_large_values():
-    """|values| > 1000 leave the FP16 range margin: the FP16 engine request falls back to FP32."""
+def test_l1_half_engine_rejects_large_values():
+    """|values| > 1000 leave the FP16 range margin: an explicit FP16x2 request is
+    refused (EINVAL); the default engine (FP32) handles the data."""
+    from paper_2307_12059_b200 import kgc
     E, Rel = generate(900, 3, 40, seed=44)
     E = (E * np.float32(3000.0)).astype(np.float32)
     Rel = (Rel * np.float32(3000.0)).astype(np.float32)
     eps = theta_for(E, Rel, 1, 1e-3)
-    res, st = gpu_join(E, Rel, 1, eps, l1_engine=1)
+    with pytest.raises(kgc.KgcError) as ei:
+        gpu_join(E, Rel, 1, eps, l1_engine=1)
+    assert ei.value.status == kgc.KGC_EINVAL
+    res, st = gpu_join(E, Rel, 1, eps)
     assert st["engine"] == 2
     check_parity(E, Rel, 1, eps, res)
 
