@@ -262,7 +262,9 @@ def run_ours(args, cfg, thresholds):
             tc = st["tail_tile_rows"] == 256
             peak = peaks["bf16_tflops"] * (1.1 / 2.25) if tc else \
                 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12 * 2
-            kernels.append({"kernel": "tiles_tc_kernel (L2, tcgen05 kind::tf32)" if tc else "tiles_simt_kernel<2>",
+            kname = ("tiles_tc2_kernel (L2, tcgen05.mma.cta_group::2 kind::tf32)" if st["engine"] == 4 else
+                     "tiles_tc_kernel (L2, tcgen05 kind::tf32)") if tc else "tiles_simt_kernel<2>"
+            kernels.append({"kernel": kname,
                             "bound": "tensor" if tc else "alu", "ms": t_tiles * 1e3,
                             "achieved": flops / t_tiles / 1e12, "peak": peak, "unit": "TFLOP/s",
                             "peak_note": (f"{peak_src} bf16 burst {peaks['bf16_tflops']} x nominal tf32/bf16 "

@@ -74,7 +74,9 @@ typedef struct {
     int32_t prune;            /* 1 = Lemma 1/2 tile pruning (default); 0 = every tile (naive control,*/
                               /*     PAPER.md:473 "naive GPU approach")                            */
     int32_t pivot;            /* 0 = zero vector (default); 1 = mean of the tails      */
-    int32_t l2_engine;        /* 0 = auto (= 1); 1 = tcgen05 TF32 filter; 2 = FP32 SIMT filter      */
+    int32_t l2_engine;        /* 0 = auto (3 when N * pad8(d) * 4 > 48 MiB, else 1; 2 if d > 256);  */
+                              /* 1 = tcgen05 TF32 filter; 2 = FP32 SIMT filter; 3 = tcgen05 TF32 on */
+                              /* CTA pairs (cta_group::2, 256-row query tiles)                     */
     int32_t chunk_tiles;      /* max tail tiles per work item (load-balance granularity); 0 = auto */
     int32_t pivots;           /* 0/1 = one pivot (default); 2..8 = multi-pivot tile     */
                               /* pruning (L_inf over K pivot distances; needs d <= 256, */
@@ -112,7 +114,8 @@ typedef struct {
     /* device time per phase (CUDA events on the context's stream), milliseconds */
     float ms_total, ms_h2d, ms_keys, ms_sort, ms_ranges, ms_stage, ms_tiles, ms_recheck;
     int32_t pivots_used;          /* 1, or K of the multi-pivot pruning                            */
-    int32_t engine;               /* tile engine used: 1 tcgen05 TF32, 2 FP32 SIMT, 3 FP16x2 SIMT    */
+    int32_t engine;               /* tile engine used: 1 tcgen05 TF32, 2 FP32 SIMT, 3 FP16x2 SIMT,   */
+                                  /* 4 tcgen05 TF32 on CTA pairs                                      */
 } kgc_stats_t;
 
 /* Fill *opt with defaults: device -1, rank 0, world 1, prune 1, pivot 0,

@@ -108,9 +108,28 @@ static T* P(DevBuf& b) {
 static bool use_tc(const kgc_ctx* ctx, int norm, int d) {
     return norm == 2 && ctx->opt.l2_engine != 2 && ((d + 7) / 8) * 8 <= TC_MAX_KPAD;
 }
-static int plan_bq(const kgc_ctx* ctx, int norm, int d) {
+// Tensor cores on CTA pairs (cta_group::2, 256-row query tiles): l2_engine 3,
+// or automatically once the staged tails outgrow a fraction of L2 (48 MiB),
+// where the 1-CTA kernel waits on tail bytes (measured: c4 +9%, c5 +11%
+// tile-kernel throughput; on c2 the coarser query tiles prune less and the
+// pair kernel is 8% slower).
+static bool use_tc2(const kgc_ctx* ctx, int norm, int d, long long N) {
+    if (!use_tc(ctx, norm, d)) return false;
+    if (ctx->opt.l2_engine == 3) return true;
+    if (ctx->opt.l2_engine != 0) return false;
+    const char* e = getenv("KGC_TC2");  // experiment knob: force the automatic choice
+    if (e) return atoi(e) != 0;
+    return (double)N * (double)(((d + 7) / 8) * 8) * 4.0 > 48.0 * 1048576.0;
+}
+// FP32 SIMT tile edge (experiment knob KGC_SIMT_T = 32 | 64)
+static int simt_t() {
+    const char* e = getenv("KGC_SIMT_T");
+    return (e && atoi(e) == 32) ? 32 : SIMT_T;
+}
+static int plan_bq(const kgc_ctx* ctx, int norm, int d, long long N) {
+    if (use_tc2(ctx, norm, d, N)) return 2 * BM;
     if (use_tc(ctx, norm, d)) return BM;
-    return (norm == 1 && ctx->opt.l1_engine == 1) ? BN_HALF : SIMT_T;
+    return (norm == 1 && ctx->opt.l1_engine == 1) ? BN_HALF : simt_t();
 }
 
 // Relative margin covering the FP32 pivot keys.
@@ -159,7 +178,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 2 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 2 || o.split < 0 || o.split > 1) {
+        o.l2_engine > 3 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 2 || o.split < 0 || o.split > 1) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -289,22 +308,24 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     st.triplets = (double)N * (double)N * (double)R_global;
 
     const bool tc = use_tc(ctx, norm, d);
-    if (norm == 2 && ctx->opt.l2_engine == 1 && !tc) {
-        set_err(ctx, "l2_engine=1 (tcgen05) supports d <= %d", TC_MAX_KPAD);
+    const bool tc2 = use_tc2(ctx, norm, d, N);
+    if (norm == 2 && (ctx->opt.l2_engine == 1 || ctx->opt.l2_engine == 3) && !tc) {
+        set_err(ctx, "l2_engine=%d (tcgen05) supports d <= %d", ctx->opt.l2_engine, TC_MAX_KPAD);
         return KGC_EINVAL;
     }
     const int Kpad = ((d + 7) / 8) * 8;
     // tile geometry of the plan: tensor cores 128 x 256; FP16x2 L1 128 x 128; FP32 SIMT 64 x 64
     const bool half_req = norm == 1 && ctx->opt.l1_engine == 1;
-    const int bq = plan_bq(ctx, norm, d);
-    const int BN = tc ? BN_TC : (half_req ? BN_HALF : SIMT_T);
+    const int bq = plan_bq(ctx, norm, d, N);
+    const int BN = tc ? BN_TC : (half_req ? BN_HALF : simt_t());
     const int QT = (int)((N + bq - 1) / bq);
     const int TT = (int)((N + BN - 1) / BN);
     const long long nq = R * (long long)QT;
     int chunk = ctx->opt.chunk_tiles > 0 ? ctx->opt.chunk_tiles : (tc ? 16 : 8);
     if (tc && ctx->opt.chunk_tiles == 0) {
         int as = 0, bs = 0, kc = 0;
-        if (tc_smem_bytes(((d + 7) / 8) * 8, &as, &bs, &kc) > 0 && as == 1) chunk = 64;  // amortise A rebuilds
+        const int sb = tc2 ? tc2_smem_bytes(Kpad, &as, &bs, &kc) : tc_smem_bytes(Kpad, &as, &bs, &kc);
+        if (sb > 0 && as == 1) chunk = 64;  // amortise A rebuilds
     }
     ctx->N = N;
     ctx->R = R;
@@ -521,7 +542,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         set_err(ctx, "l1_engine=1 (FP16x2) needs every |E|, |Rel| value <= 1000; use l1_engine 0 or 2");
         return KGC_EINVAL;
     }
-    st.engine = tc ? 1 : (half ? 3 : 2);
+    st.engine = tc2 ? 4 : (tc ? 1 : (half ? 3 : 2));
     const float gam = 1.0f + 10.0f * 4.8828125e-04f + (float)(d / 8 + 4) * 1.1920928955078125e-07f;
     if (n_items > 0) {
         CK(ensure(ctx->Tp, (size_t)TT * BN * Kpad * 4));
@@ -536,7 +557,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                               P<float4>(ctx->qs), nullptr, s);
             LAUNCHED(2);
         } else {
-            launch_stage_tails(E, P<int>(ctx->tperm), N, d, Kpad, BN, TT, tc ? 1 : 0, P<float>(ctx->Tp),
+            launch_stage_tails(E, P<int>(ctx->tperm), N, d, Kpad, BN, TT, tc2 ? 2 : (tc ? 1 : 0), P<float>(ctx->Tp),
                                P<float>(ctx->T2), P<float2>(ctx->tstile), s);
             LAUNCHED(1);
             if (!tc) {  // the tensor-core engine forms its query tiles on the fly
@@ -574,6 +595,10 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             const char* e = getenv(tc ? "KGC_SCHED_TC" : "KGC_SCHED_SIMT");
             tp.sched = e ? atoi(e) : (tc ? 0 : 1);
         }
+        {
+            const char* e = getenv("KGC_T2_PREFETCH");
+            tp.t2pf = e ? atoi(e) : 1;
+        }
         tp.Kpad = Kpad;
         tp.bq = bq;
         tp.bn = BN;
@@ -592,7 +617,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.d = d;
         tp.QT = QT;
         if (n_items > 0) {
-            if (tc) launch_tiles_tc(tp, ctx->num_sms, s);
+            if (tc2) launch_tiles_tc2(tp, ctx->num_sms, s);
+            else if (tc) launch_tiles_tc(tp, ctx->num_sms, s);
             else if (half) launch_tiles_half_l1(tp, ctx->num_sms, s);
             else launch_tiles_simt(tp, norm, ctx->num_sms, s);
             LAUNCHED(1);
@@ -737,7 +763,7 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
     if (ctx->opt.world > 1 && ctx->opt.split == 0) {
         // Rank-local split: query-tile ranges balanced by an estimated per-relation cost
         // (launch_split_estimate); each rank then preprocesses only the relations its range touches.
-        const long long bq = plan_bq(ctx, norm, d);
+        const long long bq = plan_bq(ctx, norm, d, N);
         const long long QT = (N + bq - 1) / bq, nq = R * QT;
         long long a = 0, b = 0, h2d = 0;
         const float *Ed = E, *Rd = Rel;

@@ -42,6 +42,7 @@ struct TileParams {
     long long n_items;
     const long long* item_cum;  // exclusive prefix of item tile counts (cost-balanced CTA ranges)
     long long total_tiles;
+    int t2pf;                   // tensor-core epilogues: prefetch ||t||^2 lines into L1 (experiment knob)
     int sched;                  // 0 = round-robin items, 1 = contiguous cost-balanced blocks
     int Kpad;
     int bq, bn;             // query / tail tile rows of the plan
@@ -127,6 +128,8 @@ __device__ __forceinline__ int item_tile(const int4& w, int j, const int* __rest
 // ---- tile engines ----
 int  tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);
 void launch_tiles_tc(const TileParams& p, int num_sms, cudaStream_t s);
+int  tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);
+void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s);
 void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t s);
 void launch_tiles_half_l1(const TileParams& p, int num_sms, cudaStream_t s);
 constexpr int HALF_FLUSH_PAIRS = 8;  // FP16x2 engine: flush to FP32 every 16 dims

@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ E,
                                                     const int* __restrict__ perm, long long N, int d, int Kpad,
                                                     int ROWS, int QT, int tile0, int norm, float theta,
                                                     float* __restrict__ out, float4* __restrict__ qs,
-                                                    float* __restrict__ T2, float2* __restrict__ tstile) {
+                                                    float* __restrict__ T2, float2* __restrict__ tstile, int split) {
     const int tile = tile0 + blockIdx.x;
     long long r = 0, t_in_rel = tile;
     if (Rel) {
@@ -683,7 +683,8 @@ __global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ E,
                     st.sd2 += rd * rd;
                     st.s1 += fabs(xd);
                 }
-                *reinterpret_cast<float4*>(dst + stage_off<true>(i, kq * 4, ROWS)) = v;
+                // UMMA layout per block of `split` rows (split = 128: one block per CTA of a pair)
+                *reinterpret_cast<float4*>(dst + (size_t)(i / split) * split * Kpad + stage_off<true>(i % split, kq * 4, split)) = v;
             }
             st.s2 = warp_sum_d(st.s2);
             st.sd2 = warp_sum_d(st.sd2);
@@ -920,9 +921,11 @@ void launch_stage_tails(const float* E, const int* tperm, long long N, int d, in
                         float* Tp, float* T2, float2* tstile, cudaStream_t s) {
     if (TT <= 0) return;
     if (tc_layout)
-        stage_kernel<true><<<TT, 256, 0, s>>>(E, nullptr, tperm, N, d, Kpad, BN, 1, 0, 2, 0.f, Tp, nullptr, T2, tstile);
+        stage_kernel<true><<<TT, 256, 0, s>>>(E, nullptr, tperm, N, d, Kpad, BN, 1, 0, 2, 0.f, Tp, nullptr, T2, tstile,
+                                              tc_layout == 2 ? BN / 2 : BN);
     else
-        stage_kernel<false><<<TT, 256, 0, s>>>(E, nullptr, tperm, N, d, Kpad, BN, 1, 0, 2, 0.f, Tp, nullptr, T2, tstile);
+        stage_kernel<false><<<TT, 256, 0, s>>>(E, nullptr, tperm, N, d, Kpad, BN, 1, 0, 2, 0.f, Tp, nullptr, T2, tstile,
+                                               BN);
 }
 
 void launch_stage_queries(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad, int QT,
@@ -931,10 +934,10 @@ void launch_stage_queries(const float* E, const float* Rel, const int* qperm, lo
     if (tq1 <= tq0) return;
     if (tc_layout)
         stage_kernel<true><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, bq, QT, tq0, norm, theta, Qp, qs,
-                                                     nullptr, nullptr);
+                                                     nullptr, nullptr, bq);
     else
         stage_kernel<false><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, bq, QT, tq0, norm, theta, Qp, qs,
-                                                      nullptr, nullptr);
+                                                      nullptr, nullptr, bq);
 }
 
 }  // namespace kgc

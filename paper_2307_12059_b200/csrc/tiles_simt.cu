@@ -363,11 +363,11 @@ void launch_tiles_half_l1(const TileParams& p, int num_sms, cudaStream_t s) {
     tiles_half_l1_kernel<<<(unsigned)g, 256, smem, s>>>(p);
 }
 
-template <int NORM, int TM, int TN, int KC, int NS = SIMT_NS>
+template <int NORM, int TM, int TN, int KC, int NS = SIMT_NS, int T = SIMT_T>
 static void launch_simt_variant(const TileParams& p, int num_sms, cudaStream_t s) {
-    constexpr int NT = (SIMT_T / TM) * (SIMT_T / TN);
-    const size_t smem = (size_t)NS * KC * (SIMT_T + SIMT_T) * 4 + 128;
-    auto kern = tiles_simt_kernel<NORM, SIMT_T, SIMT_T, TM, TN, KC, NS>;
+    constexpr int NT = (T / TM) * (T / TN);
+    const size_t smem = (size_t)NS * KC * (T + T) * 4 + 128;
+    auto kern = tiles_simt_kernel<NORM, T, T, TM, TN, KC, NS>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
@@ -382,6 +382,11 @@ void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t 
     // 64 x 64 tiles, 64 threads with 8 x 8 micro-tiles, 32-wide K-chunks, double buffer:
     // 32 KB of shared memory -> 7 CTAs per SM (register-limited).  Measured best of the
     // micro-tile / chunk / depth sweep on c2 L1.
+    if (p.bq == 32) {  // 32 x 32 tiles (experiment: finer pruning), 64 threads with 4 x 4 micro-tiles
+        if (norm == 1) launch_simt_variant<1, 4, 4, 32, 2, 32>(p, num_sms, s);
+        else launch_simt_variant<2, 4, 4, 32, 2, 32>(p, num_sms, s);
+        return;
+    }
     if (norm == 1) launch_simt_variant<1, 8, 8, 32, 2>(p, num_sms, s);
     else launch_simt_variant<2, 8, 8, 32, 2>(p, num_sms, s);
 }

@@ -206,10 +206,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
                 // candidate iff 2 acc - ||t||^2 >= c
                 // Q2 is an FP32 sum: |Q2 - ||q||^2| <= (Kpad + 4) 2^-23 Q2 (builder)
                 const float c = Q2 - R - (float)(p.Kpad + 4) * 1.1920928955078125e-07f * Q2 - 9.5367431640625e-07f * (Q2 + R);
+                // ||t||^2 of this tile's and the next tile's columns into L1 ahead of use
+                // (4 lines each); each chunk's loads would otherwise be an L2 round trip
+                const float* t2row = p.T2 + (size_t)j * BN_TC + col0;
+                if (p.t2pf && lane < 4) prefetch_l1(t2row + lane * 32);
+                else if (p.t2pf && lane < 8 && jj < w.z)
+                    prefetch_l1(p.T2 + (size_t)item_tile(w, jj + 1, p.tile_list) * BN_TC + col0 + (lane - 4) * 32);
                 TC_WAIT(5, &acc_full[acc], accph);
                 tc_fence_after();
                 const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_TC + col0);
-                const float* t2row = p.T2 + (size_t)j * BN_TC + col0;
                 uint32_t ra[32], rb[32];
                 auto process = [&](const uint32_t (&r)[32], int ch) {
                     const float4* t2 = reinterpret_cast<const float4*>(t2row + ch * 32);

@@ -1,0 +1,406 @@
+// tiles_tc2.cu -- K4 on CTA pairs: the L2 surviving-tile contraction with
+// tcgen05.mma.cta_group::2 (the M = 256 form of
+// tiles_tc.cu).
+//
+// Same arithmetic and guard band as tiles_tc.cu (D^2 = ||q||^2 + ||t||^2 -
+// 2 q.t; TF32 band + FP64 re-check keep the filter lossless,
+// PAPER.md:349-351).  What changes is the data movement: a cluster of two
+// CTAs on two SMs works on one 256-row query tile (128 rows per CTA, built
+// in each CTA's shared memory) against the same 256-row tail tiles, and
+// each CTA streams only HALF of every tail tile (its 128 rows; the tails
+// are staged as two 128-row UMMA blocks per tile).  The even CTA issues
+// M = 256, N = 256, K = 8 MMAs that read A and B from both CTAs' shared
+// memory; each CTA's TMEM receives its own 128 x 256 accumulator.  Per SM,
+// tail bytes per MAC halve relative to tiles_tc.cu -- the B-operand wait
+// that bounds the 1-CTA kernel on large N.
+//
+// Cross-CTA signalling (all mbarriers live at the same offsets in both CTAs):
+//   a_full   (even CTA: 256 arrivals) builders of both CTAs; odd-CTA
+//            builders arrive remotely (release.cluster) after their
+//            proxy fence.
+//   b_full   (even CTA: 2 arrivals) its producer's expect_tx + a relay
+//            thread of the odd CTA that waits for the odd CTA's own bulk
+//            copy and forwards the completion (1-D bulk copies complete
+//            only on a barrier of the destination CTA).
+//   b_empty, a_empty, acc_full: tcgen05.commit multicast to both CTAs.
+//   acc_empty (even CTA: 16 arrivals) the 8 epilogue warps of each CTA.
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace kgc {
+
+#ifdef KGC_PROF_TC
+// debug build only: cycles each role spends blocked in each barrier wait
+__device__ unsigned long long g_tc2_prof[16];
+#define TC2_WAIT(slot, bar, par)                                   \
+    do {                                                           \
+        const long long t0_ = clock64();                           \
+        mbar_wait(bar, par);                                       \
+        atomicAdd(&g_tc2_prof[slot], (unsigned long long)(clock64() - t0_)); \
+    } while (0)
+#else
+#define TC2_WAIT(slot, bar, par) mbar_wait(bar, par)
+#endif
+
+constexpr int TC2_THREADS = 448;  // same roles as tiles_tc.cu
+constexpr int TC2_BUILDER_WARP0 = 10;
+constexpr int HALF = BN_TC / 2;                 // tail rows per CTA
+constexpr uint32_t LBO_A2 = (BM / 8) * 128;     // 128 query rows per CTA
+constexpr uint32_t LBO_B2 = (HALF / 8) * 128;   // 128 tail rows per CTA
+constexpr uint32_t SBO2 = 128;
+constexpr uint32_t IDESC2 = idesc_tf32(2 * BM, BN_TC);  // M = 256, N = 256
+
+int tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
+    const int budget = 227 * 1024 - 512 - 2 * BM * 16;
+    const int A = BM * Kpad * 4;
+    // prefer two A stages when the B ring still buffers >= 64 K-values
+    for (int as = 2; as >= 1; --as) {
+        for (int KC : {32, 16, 8}) {
+            const int B = HALF * KC * 4;
+            const int rem = budget - as * A;
+            if (rem <= 0) continue;
+            int bs = rem / B;
+            if (bs > 6) bs = 6;
+            if (bs >= 2 && (bs * KC >= 64 || as == 1)) {
+                *a_stages = as;
+                *b_stages = bs;
+                *kc = KC;
+                const int bytes = as * A + bs * B + 512 + as * BM * 16;
+                return bytes < 117 * 1024 ? 117 * 1024 : bytes;  // one CTA per SM
+            }
+        }
+    }
+    return -1;
+}
+
+__global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p, int a_stages, int b_stages, int KC) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int Kpad = p.Kpad;
+    const uint32_t A_FLOATS = BM * Kpad;
+    const int nkc = (Kpad + KC - 1) / KC;
+    float* As = reinterpret_cast<float*>(smem);
+    float* Bs = As + (size_t)a_stages * A_FLOATS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Bs + (size_t)b_stages * HALF * KC);
+    uint64_t* a_full = bars;
+    uint64_t* a_empty = bars + 2;
+    uint64_t* acc_full = bars + 4;
+    uint64_t* acc_empty = bars + 6;
+    uint64_t* b_full = bars + 8;
+    uint64_t* b_empty = b_full + b_stages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 40);
+    float4* qrow = reinterpret_cast<float4*>(bars + 64);  // [a_stages][BM] {||q||^2, ||q||, ||q - tf32(q)||, 0}
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = cluster_ctarank();
+    const bool leader = crank == 0;
+    const long long cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const long long it_begin = p.sched ? balanced_begin(p.item_cum, p.n_items, p.total_tiles, cid, ncl) : cid;
+    const long long it_end = p.sched ? balanced_begin(p.item_cum, p.n_items, p.total_tiles, cid + 1, ncl) : p.n_items;
+    const long long it_step = p.sched ? 1 : ncl;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&a_full[i], leader ? 2 * BM : BM);
+            mbar_init(&a_empty[i], 1 + 8);
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 16);
+        }
+        for (int i = 0; i < b_stages; ++i) {
+            mbar_init(&b_full[i], leader ? 2 : 1);
+            mbar_init(&b_empty[i], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+    tc_fence_before();
+    cluster_sync_all();  // barrier inits + the TMEM address visible in both CTAs
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ producer: this CTA's half of each tail tile
+            int bi = 0;
+            uint32_t bph = 0;
+            for (long long it = it_begin; it < it_end; it += it_step) {
+                const int4 w = p.items[it];
+                for (int j = w.y; j <= w.z; ++j) {
+                    const float* tsrc = p.Tp + ((size_t)item_tile(w, j, p.tile_list) * BN_TC + crank * HALF) * Kpad;
+                    for (int c = 0; c < nkc; ++c) {
+                        const int klen = Kpad - c * KC < KC ? Kpad - c * KC : KC;
+                        const uint32_t bytes = (uint32_t)klen * HALF * 4;
+                        TC2_WAIT(0, &b_empty[bi], bph ^ 1);
+                        mbar_arrive_expect_tx(&b_full[bi], bytes);
+                        bulk_g2s(Bs + (size_t)bi * HALF * KC, tsrc + (size_t)c * KC * HALF, bytes, &b_full[bi]);
+                        if (++bi == b_stages) { bi = 0; bph ^= 1; }
+                    }
+                }
+            }
+            for (int k = 0; k < b_stages; ++k) {  // drain: the last commits have landed
+                mbar_wait(&b_empty[bi], bph ^ 1);
+                if (++bi == b_stages) { bi = 0; bph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {
+            // ------------------------------------------------ MMA issuer (even CTA)
+            int ai = 0, bi = 0, acc = 0;
+            uint32_t aph = 0, bph = 0, accph = 0;
+            for (long long it = it_begin; it < it_end; it += it_step) {
+                const int4 w = p.items[it];
+                TC2_WAIT(1, &a_full[ai], aph);
+                tc_fence_after();
+                const uint64_t a_desc0 = umma_desc_kmajor(smem_u32(As + (size_t)ai * A_FLOATS), LBO_A2, SBO2);
+                for (int j = w.y; j <= w.z; ++j) {
+                    TC2_WAIT(2, &acc_empty[acc], accph ^ 1);
+                    tc_fence_after();
+                    const uint32_t d_tmem = tmem + (uint32_t)(acc * BN_TC);
+                    for (int c = 0; c < nkc; ++c) {
+                        TC2_WAIT(3, &b_full[bi], bph);
+                        tc_fence_after();
+                        const uint64_t b_desc0 = umma_desc_kmajor(smem_u32(Bs + (size_t)bi * HALF * KC), LBO_B2, SBO2);
+                        const int nsteps = (Kpad - c * KC < KC ? Kpad - c * KC : KC) / 8;
+                        const uint64_t a_desc = a_desc0 + (uint64_t)((uint32_t)(c * KC / 4) * (LBO_A2 >> 4));
+                        if (elect_one()) {
+#pragma unroll
+                            for (int s = 0; s < 4; ++s) {
+                                if (s < nsteps)
+                                    mma_tf32_pair(d_tmem, a_desc + (uint64_t)(2 * s * (LBO_A2 >> 4)),
+                                                  b_desc0 + (uint64_t)(2 * s * (LBO_B2 >> 4)), IDESC2, (c | s) != 0);
+                            }
+                            mma_commit_pair(&b_empty[bi], 3);
+                        }
+                        __syncwarp();
+                        if (++bi == b_stages) { bi = 0; bph ^= 1; }
+                    }
+                    if (elect_one()) mma_commit_pair(&acc_full[acc], 3);
+                    __syncwarp();
+                    if (++acc == 2) { acc = 0; accph ^= 1; }
+                }
+                if (elect_one()) mma_commit_pair(&a_empty[ai], 3);
+                __syncwarp();
+                if (++ai == a_stages) { ai = 0; aph ^= 1; }
+            }
+            for (int k = 0; k < 2; ++k) {  // drain: both CTAs' epilogues released the accumulators
+                mbar_wait(&acc_empty[acc], accph ^ 1);
+                if (++acc == 2) { acc = 0; accph ^= 1; }
+            }
+        } else if (lane == 0) {
+            // ------------------------------------------------ relay (odd CTA): forward B-chunk completions
+            int bi = 0;
+            uint32_t bph = 0;
+            for (long long it = it_begin; it < it_end; it += it_step) {
+                const int4 w = p.items[it];
+                for (int j = w.y; j <= w.z; ++j) {
+                    for (int c = 0; c < nkc; ++c) {
+                        TC2_WAIT(7, &b_full[bi], bph);
+                        mbar_arrive_cluster(&b_full[bi], 0);
+                        if (++bi == b_stages) { bi = 0; bph ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp < TC2_BUILDER_WARP0) {
+        // ---------------------------------------------------- epilogue (both CTAs, own 128 rows)
+        const int q = warp & 3;
+        const int col0 = ((warp - 2) >> 2) * (BN_TC / 2);
+        const int i = q * 32 + lane;
+        int acc = 0, ai = 0;
+        uint32_t accph = 0, aph = 0;
+        for (long long it = it_begin; it < it_end; it += it_step) {
+            const int4 w = p.items[it];
+            TC2_WAIT(4, &a_full[ai], aph);
+            const float4 qv = qrow[ai * BM + i];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a_empty[ai]);
+            if (++ai == a_stages) { ai = 0; aph ^= 1; }
+            const float Q2 = qv.x, Qn = qv.y, Qd = qv.z;
+            const int rowid = w.x * (2 * BM) + (int)crank * BM + i;
+            const float thf = p.theta * (1.0f + 2.44140625e-04f) + 2.384185791015625e-07f * Qn;
+            for (int jj = w.y; jj <= w.z; ++jj) {
+                const int j = item_tile(w, jj, p.tile_list);
+                const float2 tv = p.tstile[j];
+                const float Tm = tv.x, Tdm = tv.y;
+                // guard band exactly as tiles_tc.cu
+                const float eb = Qd * Tm + Qn * Tdm + Qd * Tdm + p.eta * (Qn + Qd) * (Tm + Tdm);
+                const float sl = 4.76837158203125e-07f * (Qn + Tm) * (Qn + Tm);
+                const float R = thf * thf + 2.0f * eb + sl;
+                const float c = Q2 - R - (float)(p.Kpad + 4) * 1.1920928955078125e-07f * Q2 - 9.5367431640625e-07f * (Q2 + R);
+                // ||t||^2 of this tile's and the next tile's columns into L1 ahead of use
+                // (4 lines each); each chunk's loads would otherwise be an L2 round trip
+                const float* t2row = p.T2 + (size_t)j * BN_TC + col0;
+                if (p.t2pf && lane < 4) prefetch_l1(t2row + lane * 32);
+                else if (p.t2pf && lane < 8 && jj < w.z)
+                    prefetch_l1(p.T2 + (size_t)item_tile(w, jj + 1, p.tile_list) * BN_TC + col0 + (lane - 4) * 32);
+                TC2_WAIT(5, &acc_full[acc], accph);
+                tc_fence_after();
+                const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_TC + col0);
+                uint32_t ra[32], rb[32];
+                auto process = [&](const uint32_t (&r)[32], int ch) {
+                    const float4* t2 = reinterpret_cast<const float4*>(t2row + ch * 32);
+                    float m0 = -3.0e38f, m1 = -3.0e38f, m2 = -3.0e38f, m3 = -3.0e38f;
+#pragma unroll
+                    for (int u4 = 0; u4 < 8; ++u4) {
+                        const float4 tt = __ldg(t2 + u4);
+                        m0 = fmaxf(m0, fmaf(2.0f, __uint_as_float(r[4 * u4 + 0]), -tt.x));
+                        m1 = fmaxf(m1, fmaf(2.0f, __uint_as_float(r[4 * u4 + 1]), -tt.y));
+                        m2 = fmaxf(m2, fmaf(2.0f, __uint_as_float(r[4 * u4 + 2]), -tt.z));
+                        m3 = fmaxf(m3, fmaf(2.0f, __uint_as_float(r[4 * u4 + 3]), -tt.w));
+                    }
+                    const float m = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+                    if (__any_sync(0xffffffffu, m >= c)) {
+                        uint32_t hit = 0;
+#pragma unroll
+                        for (int u4 = 0; u4 < 8; ++u4) {
+                            const float4 tt = __ldg(t2 + u4);
+                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 0]), -tt.x) >= c) << (4 * u4 + 0);
+                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 1]), -tt.y) >= c) << (4 * u4 + 1);
+                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 2]), -tt.z) >= c) << (4 * u4 + 2);
+                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 3]), -tt.w) >= c) << (4 * u4 + 3);
+                        }
+                        unsigned long long slot = warp_reserve(__popc(hit), p.cand_count);
+                        const int colb = j * BN_TC + col0 + ch * 32;
+                        while (hit) {
+                            const int u = __ffs(hit) - 1;
+                            if (slot < (unsigned long long)p.cand_cap) p.cand[slot] = make_int2(rowid, colb + u);
+                            ++slot;
+                            hit &= hit - 1;
+                        }
+                    }
+                };
+                tmem_ld32_nowait(tbase + 0, ra);
+                tmem_wait_ld();
+                tmem_ld32_nowait(tbase + 32, rb);
+                process(ra, 0);
+                tmem_wait_ld();
+                tmem_ld32_nowait(tbase + 64, ra);
+                process(rb, 1);
+                tmem_wait_ld();
+                tmem_ld32_nowait(tbase + 96, rb);
+                process(ra, 2);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (leader) mbar_arrive(&acc_empty[acc]);
+                    else mbar_arrive_cluster(&acc_empty[acc], 0);
+                }
+                process(rb, 3);
+                if (++acc == 2) { acc = 0; accph ^= 1; }
+            }
+        }
+    }
+    if (warp >= TC2_BUILDER_WARP0) {
+        // ---------------------------------------------------- builders: this CTA's 128 query rows
+        const int i = (warp - TC2_BUILDER_WARP0) * 32 + lane;
+        const bool vec4 = (p.d % 4 == 0) && ((reinterpret_cast<uintptr_t>(p.E) | reinterpret_cast<uintptr_t>(p.Rel)) % 16 == 0);
+        int ai = 0;
+        uint32_t aph = 0;
+        for (long long it = it_begin; it < it_end; it += it_step) {
+            const int4 w = p.items[it];
+            const int r = w.x / p.QT;
+            const long long pos = (long long)(w.x - r * p.QT) * (2 * BM) + crank * BM + i;
+            const bool valid = pos < p.N;
+            const long long h = valid ? p.qperm[(long long)r * p.N + pos] : 0;
+            const float* e = p.E + h * p.d;
+            const float* rr = p.Rel + (long long)r * p.d;
+            TC2_WAIT(6, &a_empty[ai], aph ^ 1);
+            float* A = As + (size_t)ai * A_FLOATS;
+            float s2 = 0.f, sd2 = 0.f;
+            const int nq = Kpad >> 2;
+            for (int kq0 = 0; kq0 < nq; kq0 += 8) {
+                float4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int kq = kq0 + u, k = kq * 4;
+                    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (valid && kq < nq) {
+                        if (vec4 && k < p.d) {
+                            const float4 a = __ldg(reinterpret_cast<const float4*>(e + k));
+                            const float4 b = __ldg(reinterpret_cast<const float4*>(rr + k));
+                            v[u] = make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                                               __fadd_rn(a.w, b.w));
+                        } else {
+                            float* vv = reinterpret_cast<float*>(&v[u]);
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                if (k + c < p.d) vv[c] = __fadd_rn(__ldg(e + k + c), __ldg(rr + k + c));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int kq = kq0 + u;
+                    if (kq < nq) {
+                        const float* vv = reinterpret_cast<const float*>(&v[u]);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const float rd = vv[c] - __uint_as_float(__float_as_uint(vv[c]) & 0xFFFFE000u);  // exact
+                            s2 = fmaf(vv[c], vv[c], s2);
+                            sd2 = fmaf(rd, rd, sd2);
+                        }
+                        *reinterpret_cast<float4*>(A + ((size_t)kq * (BM / 8) + (i >> 3)) * 32 + (i & 7) * 4) = v[u];
+                    }
+                }
+            }
+            const float gam = 1.0f + (float)(Kpad + 4) * 1.1920928955078125e-07f;
+            qrow[ai * BM + i] = valid ? make_float4(s2, __fsqrt_ru(__fmul_ru(s2, gam)), __fsqrt_ru(__fmul_ru(sd2, gam)), 0.f)
+                                      : make_float4(3e38f, 0.f, 0.f, 0.f);
+            fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the pair's tcgen05.mma
+            mbar_arrive(&a_full[ai]);
+            if (!leader) mbar_arrive_cluster(&a_full[ai], 0);
+            if (++ai == a_stages) { ai = 0; aph ^= 1; }
+        }
+        for (int k = 0; k < a_stages; ++k) {  // drain: the last a_empty commits have landed
+            mbar_wait(&a_empty[ai], aph ^ 1);
+            if (++ai == a_stages) { ai = 0; aph ^= 1; }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();  // no CTA leaves while its partner may still signal it
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair(tmem, 512);
+    }
+}
+
+#ifdef KGC_PROF_TC
+}  // namespace kgc
+extern "C" __attribute__((visibility("default"))) void kgc_debug_tc2_prof(unsigned long long* out16, int reset) {
+    if (out16) cudaMemcpyFromSymbol(out16, kgc::g_tc2_prof, 16 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(kgc::g_tc2_prof, z, sizeof z);
+    }
+}
+namespace kgc {
+#endif
+
+void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s) {
+    if (p.n_items <= 0) return;
+    int as, bs, kc;
+    const int smem = tc2_smem_bytes(p.Kpad, &as, &bs, &kc);
+    cudaFuncSetAttribute(tiles_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(TC2_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(num_sms & ~1);
+    int max_clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, tiles_tc2_kernel, &cfg) != cudaSuccess || max_clusters <= 0) {
+        cudaGetLastError();
+        max_clusters = num_sms / 2;
+    }
+    long long g = p.n_items < max_clusters ? p.n_items : max_clusters;
+    cfg.gridDim = dim3((unsigned)(2 * g));
+    cudaLaunchKernelEx(&cfg, tiles_tc2_kernel, p, as, bs, kc);
+}
+
+}  // namespace kgc

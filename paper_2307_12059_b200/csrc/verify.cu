@@ -13,136 +13,92 @@
 
 namespace kgc {
 
+// One warp verifies 32 candidates per round.  Stage 1: lane l loads
+// candidate base + l and maps it through the permutations (one independent
+// load chain per lane, all 32 in flight together).  Stage 2: the 8 lanes of
+// group g compute the distances of candidates g*8 .. g*8+7 (lanes over k,
+// FP64 partial sums, 3-step shuffle tree); the sum of candidate c lands back
+// in lane c.  Stage 3: warp-aggregated append of the kept candidates in
+// candidate order.  No data-dependent branches in stage 2, so the compiler
+// overlaps the loads of consecutive candidates; E_h and Rel_r repeat across
+// consecutive candidates of one query row and hit L1.
 template <int NORM, bool VEC4>
-__device__ __forceinline__ double partial_dist(const float* __restrict__ eh, const float* __restrict__ er,
-                                               const float* __restrict__ et, int d, int s) {
-    double acc = 0.0;
-    if (VEC4) {
-        for (int k = s * 4; k < d; k += 32) {
-            const float4 a = __ldg(reinterpret_cast<const float4*>(eh + k));
-            const float4 b = __ldg(reinterpret_cast<const float4*>(er + k));
-            const float4 c = __ldg(reinterpret_cast<const float4*>(et + k));
-            const double x0 = ((double)a.x + (double)b.x) - (double)c.x;  // (h + r) - t, FP64
-            const double x1 = ((double)a.y + (double)b.y) - (double)c.y;
-            const double x2 = ((double)a.z + (double)b.z) - (double)c.z;
-            const double x3 = ((double)a.w + (double)b.w) - (double)c.w;
-            if (NORM == 1) acc += fabs(x0) + fabs(x1) + fabs(x2) + fabs(x3);
-            else acc += x0 * x0 + x1 * x1 + x2 * x2 + x3 * x3;
-        }
-    } else {
-        for (int k = s; k < d; k += 8) {
-            const double x = ((double)__ldg(eh + k) + (double)__ldg(er + k)) - (double)__ldg(et + k);
-            acc += NORM == 1 ? fabs(x) : x * x;
-        }
-    }
-    return acc;
-}
-
-// One warp verifies 32 candidates per round: 8 lanes per candidate, each
-// 8-lane group takes 8 CONSECUTIVE candidates (the tile engines append the
-// candidates of one query row contiguously), keeps that row's E_h and Rel_r
-// in registers while the row repeats (VEC4 path, d <= 256), and reloads only
-// E_t.  FP64 partial sums are reduced over the 8 lanes; one atomic per round.
-constexpr int VMAXM = 8;  // float4 chunks per lane cached (d <= 256)
-template <int NORM, bool VEC4>
-__global__ void __launch_bounds__(256) verify_kernel(const int2* __restrict__ cand,
-                                                     const unsigned long long* __restrict__ cand_count,
-                                                     long long cand_cap, const int* __restrict__ qperm,
-                                                     const int* __restrict__ tperm, const float* __restrict__ E,
-                                                     const float* __restrict__ Rel, long long N, int QT, int bq,
-                                                     int d, double theta, KgcTripletDev* __restrict__ out,
-                                                     unsigned long long* res_count, long long res_cap, int r_off) {
+__global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__ cand,
+                                                        const unsigned long long* __restrict__ cand_count,
+                                                        long long cand_cap, const int* __restrict__ qperm,
+                                                        const int* __restrict__ tperm, const float* __restrict__ E,
+                                                        const float* __restrict__ Rel, long long N, int QT, int bq,
+                                                        int d, double theta, KgcTripletDev* __restrict__ out,
+                                                        unsigned long long* res_count, long long res_cap, int r_off) {
     long long nc = (long long)*cand_count;
     if (nc > cand_cap) nc = cand_cap;
     const int lane = threadIdx.x & 31, g = lane >> 3, s = lane & 7;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const long long rows_per_rel = (long long)QT * bq;
-    const bool cache = VEC4 && d <= 32 * VMAXM;
-    const int M = (d + 31) / 32;
     for (long long base = warp * 32; base < nc; base += nwarps * 32) {
-        uint32_t keep = 0;
-        int hs[8], rs[8], ts[8];
-        float ds[8];
-        int cached = -1;
-        float4 chv[VMAXM], crv[VMAXM];
+        // ---- stage 1: this lane's candidate
+        const long long idx = base + lane;
+        bool valid = idx < nc;
+        int h = 0, r = 0, t = 0;
+        if (valid) {
+            const int2 cv = cand[idx];
+            const long long rr = cv.x / rows_per_rel;
+            const long long pos = cv.x - rr * rows_per_rel;
+            valid = pos < N && cv.y < N;
+            if (valid) {
+                r = (int)rr;
+                h = qperm[rr * N + pos];
+                t = tperm[cv.y];
+            }
+        }
+        // ---- stage 2: distances, 8 lanes per candidate
+        double mine = 0.0;
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
-            const long long idx = base + g * 8 + it;
-            bool valid = idx < nc;
-            int h = 0, r = 0, t = 0, rowid = -1;
-            if (valid) {
-                const int2 cv = cand[idx];
-                const long long rr = cv.x / rows_per_rel;
-                const long long pos = cv.x - rr * rows_per_rel;
-                valid = pos < N && cv.y < N;
-                if (valid) {
-                    r = (int)rr;
-                    h = qperm[rr * N + pos];
-                    t = tperm[cv.y];
-                    rowid = cv.x;
-                }
-            }
+            const int src = g * 8 + it;
+            const int hh = __shfl_sync(0xffffffffu, h, src);
+            const int rq = __shfl_sync(0xffffffffu, r, src);
+            const int tt = __shfl_sync(0xffffffffu, t, src);
+            const float* eh = E + (long long)hh * d;
+            const float* er = Rel + (long long)rq * d;
+            const float* et = E + (long long)tt * d;
             double acc = 0.0;
-            if (valid) {
-                const float* eh = E + (long long)h * d;
-                const float* er = Rel + (long long)r * d;
-                const float* et = E + (long long)t * d;
-                if (cache) {
-                    if (rowid != cached) {
-                        cached = rowid;
-#pragma unroll
-                        for (int m = 0; m < VMAXM; ++m) {
-                            const int k = s * 4 + 32 * m;
-                            if (m < M && k < d) {
-                                chv[m] = __ldg(reinterpret_cast<const float4*>(eh + k));
-                                crv[m] = __ldg(reinterpret_cast<const float4*>(er + k));
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int m = 0; m < VMAXM; ++m) {
-                        const int k = s * 4 + 32 * m;
-                        if (m < M && k < d) {
-                            const float4 a = chv[m], b = crv[m];
-                            const float4 c = __ldg(reinterpret_cast<const float4*>(et + k));
-                            const double x0 = ((double)a.x + (double)b.x) - (double)c.x;  // (h + r) - t, FP64
-                            const double x1 = ((double)a.y + (double)b.y) - (double)c.y;
-                            const double x2 = ((double)a.z + (double)b.z) - (double)c.z;
-                            const double x3 = ((double)a.w + (double)b.w) - (double)c.w;
-                            if (NORM == 1) acc += fabs(x0) + fabs(x1) + fabs(x2) + fabs(x3);
-                            else acc += x0 * x0 + x1 * x1 + x2 * x2 + x3 * x3;
-                        }
-                    }
-                } else {
-                    acc = partial_dist<NORM, VEC4>(eh, er, et, d, s);
+            if (VEC4) {
+#pragma unroll 2
+                for (int k = s * 4; k < d; k += 32) {
+                    const float4 a = __ldg(reinterpret_cast<const float4*>(eh + k));
+                    const float4 b = __ldg(reinterpret_cast<const float4*>(er + k));
+                    const float4 c = __ldg(reinterpret_cast<const float4*>(et + k));
+                    const double x0 = ((double)a.x + (double)b.x) - (double)c.x;  // (h + r) - t, FP64
+                    const double x1 = ((double)a.y + (double)b.y) - (double)c.y;
+                    const double x2 = ((double)a.z + (double)b.z) - (double)c.z;
+                    const double x3 = ((double)a.w + (double)b.w) - (double)c.w;
+                    if (NORM == 1) acc += fabs(x0) + fabs(x1) + fabs(x2) + fabs(x3);
+                    else acc += x0 * x0 + x1 * x1 + x2 * x2 + x3 * x3;
+                }
+            } else {
+                for (int k = s; k < d; k += 8) {
+                    const double x = ((double)__ldg(eh + k) + (double)__ldg(er + k)) - (double)__ldg(et + k);
+                    acc += NORM == 1 ? fabs(x) : x * x;
                 }
             }
             acc += __shfl_xor_sync(0xffffffffu, acc, 4);
             acc += __shfl_xor_sync(0xffffffffu, acc, 2);
             acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-            const double dist = NORM == 2 ? sqrt(acc) : acc;
-            keep |= (uint32_t)(valid && dist <= theta) << it;
-            hs[it] = h;
-            rs[it] = r;
-            ts[it] = t;
-            ds[it] = (float)dist;
+            if (s == it) mine = acc;  // lane g*8 + it owns candidate g*8 + it
         }
-        if (s != 0) keep = 0;
-        unsigned long long slot = warp_reserve(__popc(keep), res_count);
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-            if (keep & (1u << it)) {
-                if (slot < (unsigned long long)res_cap) {
-                    KgcTripletDev o;
-                    o.h = hs[it];
-                    o.r = rs[it] + r_off;  // relation index in the caller's Rel
-                    o.t = ts[it];
-                    o.dist = ds[it];
-                    out[slot] = o;
-                }
-                ++slot;
-            }
+        // ---- stage 3: keep iff dist <= theta (inclusive); append in candidate order
+        const double dist = NORM == 2 ? sqrt(mine) : mine;
+        const bool keep = valid && dist <= theta;
+        const unsigned long long slot = warp_append(keep, res_count);
+        if (keep && slot < (unsigned long long)res_cap) {
+            KgcTripletDev o;
+            o.h = h;
+            o.r = r + r_off;  // relation index in the caller's Rel
+            o.t = t;
+            o.dist = (float)dist;
+            out[slot] = o;
         }
     }
 }

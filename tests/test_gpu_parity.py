@@ -10,7 +10,7 @@ from tests.gpu_util import check_parity, gpu_join, keyset, theta_for
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = {"tc": dict(l2_engine=1), "simt": dict(l2_engine=2)}
+ENGINES = {"tc": dict(l2_engine=1), "simt": dict(l2_engine=2), "tc2": dict(l2_engine=3)}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -23,7 +23,7 @@ def _cuda():
 
 
 # ------------------------------------------------------------ C1, full oracle
-@pytest.mark.parametrize("engine", ["tc", "simt"])
+@pytest.mark.parametrize("engine", ["tc", "simt", "tc2"])
 def test_c1_l2_full(engine):
     E, Rel = generate_config("c1")
     eps = theta_for(E, Rel, 2, 1e-3)
@@ -53,7 +53,7 @@ SHAPES = [(1, 1, 1), (7, 3, 5), (129, 2, 9), (257, 3, 33), (300, 5, 100), (1000,
 def test_ragged_shapes(N, R, d, norm, dist):
     E, Rel = generate(N, R, d, seed=N + R + d, dist=dist)
     eps = theta_for(E, Rel, norm, 0.01 if N > 10 else 0.3)
-    engines = ["tc", "simt"] if norm == 2 and d <= 256 else ["simt"]
+    engines = ["tc", "simt", "tc2"] if norm == 2 and d <= 256 else ["simt"]
     for eng in engines:
         res, _ = gpu_join(E, Rel, norm, eps, **ENGINES[eng])
         check_parity(E, Rel, norm, eps, res)
@@ -271,7 +271,7 @@ def test_multipivot_parity_c1(K, norm):
 def test_multipivot_ragged(N, R, d, norm):
     E, Rel = generate(N, R, d, seed=N + 7 * d, dist="cluster")
     eps = theta_for(E, Rel, norm, 0.01)
-    engines = ["tc", "simt"] if norm == 2 else ["simt"]
+    engines = ["tc", "simt", "tc2"] if norm == 2 else ["simt"]
     for eng in engines:
         res, st = gpu_join(E, Rel, norm, eps, pivots=8, **ENGINES[eng])
         check_parity(E, Rel, norm, eps, res)
@@ -385,3 +385,50 @@ def test_l1_half_engine_tiny_values_and_planted_zeros():
     res, st = gpu_join(E, Rel, 1, eps, l1_engine=1)
     assert st["engine"] == 3
     check_parity(E, Rel, 1, eps, res)
+
+
+# ------------------------------------------------- tcgen05 on CTA pairs (l2_engine 3)
+def test_tc2_engine_reported_and_tiles_256():
+    E, Rel = generate(1000, 3, 64, seed=5)
+    eps = theta_for(E, Rel, 2, 1e-2)
+    res, st = gpu_join(E, Rel, 2, eps, l2_engine=3)
+    assert st["engine"] == 4 and st["query_tile_rows"] == 256 and st["tail_tile_rows"] == 256
+    check_parity(E, Rel, 2, eps, res)
+
+
+@pytest.mark.parametrize("pivots", [1, 8])
+@pytest.mark.parametrize("world", [1, 3])
+def test_tc2_matches_tc(pivots, world):
+    """Same result set from the 1-CTA and the CTA-pair tensor-core engines, also per shard."""
+    E, Rel = generate(5000, 5, 100, seed=77)
+    eps = theta_for(E, Rel, 2, 1e-3, rows=sample_rows(5000, 5, 2000, seed=1))
+    for r in range(world):
+        a, _ = gpu_join(E, Rel, 2, eps, pivots=pivots, rank=r, world=world, l2_engine=1)
+        b, sb = gpu_join(E, Rel, 2, eps, pivots=pivots, rank=r, world=world, l2_engine=3)
+        assert sb["engine"] == 4
+        if world == 1:
+            assert keyset(a) == keyset(b)
+    full_a, _ = gpu_join(E, Rel, 2, eps, pivots=pivots, l2_engine=1)
+    parts = [gpu_join(E, Rel, 2, eps, pivots=pivots, rank=r, world=world, l2_engine=3)[0] for r in range(world)]
+    assert set().union(*[keyset(p) for p in parts]) == keyset(full_a)
+
+
+@pytest.mark.parametrize("d", [8, 200, 256])
+def test_tc2_dims(d):
+    """Kpad 8 (one K chunk), 200 (one A stage), 256 (largest)."""
+    E, Rel = generate(900, 3, d, seed=d)
+    eps = theta_for(E, Rel, 2, 1e-2)
+    res, _ = gpu_join(E, Rel, 2, eps, l2_engine=3)
+    check_parity(E, Rel, 2, eps, res)
+
+
+@pytest.mark.parametrize("cfg,hit,S", [("c3", 1e-5, 800), ("c4", 1e-5, 300)])
+def test_tc2_full_size_sampled(cfg, hit, S):
+    E, Rel = generate_config(cfg)
+    N, R = E.shape[0], Rel.shape[0]
+    rows = sample_rows(N, R, S, seed=9)
+    eps = theta_for(E, Rel, 2, hit, rows=rows)
+    res, st = gpu_join(E, Rel, 2, eps, l2_engine=3, pivots=8)
+    assert st["engine"] == 4
+    rep = check_parity(E, Rel, 2, eps, res, rows=rows)
+    assert rep["tight"] > 0
