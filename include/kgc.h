@@ -116,6 +116,8 @@ typedef struct {
     int32_t pivots_used;          /* 1, or K of the multi-pivot pruning                            */
     int32_t engine;               /* tile engine used: 1 tcgen05 TF32, 2 FP32 SIMT, 3 FP16x2 SIMT,   */
                                   /* 4 tcgen05 TF32 on CTA pairs                                      */
+    float ms_split;               /* device time of the rank-local split estimate (world > 1)       */
+    float ms_host;                /* host wall time of the whole kgc_join call                      */
 } kgc_stats_t;
 
 /* Fill *opt with defaults: device -1, rank 0, world 1, prune 1, pivot 0,

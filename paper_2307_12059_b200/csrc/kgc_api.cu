@@ -9,6 +9,7 @@
 //   a5/a6 K4 (L2, tcgen05) or K5 (L1 / L2 SIMT) over the work items
 //   a7/a8 K6+K7 FP64 re-check and compaction                    -> sync #2
 // Device buffers grow monotonically and are reused across joins.
+#include <chrono>
 #include <algorithm>
 #include <climits>
 #include <cmath>
@@ -49,6 +50,7 @@ struct kgc_ctx {
     long long n_results = -1;
     kgc_stats_t st{};
     cudaEvent_t ev[EV_COUNT] = {};
+    cudaEvent_t ev_split[2] = {};
     int launches = 0;
     // geometry of the last join (for kgc_inspect)
     long long N = 0, R = 0;
@@ -219,6 +221,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
         ctx->stream = ctx->own_stream;
     }
     for (auto& e : ctx->ev) cudaEventCreate(&e);
+    for (auto& e : ctx->ev_split) cudaEventCreate(&e);
     cudaSetDevice(prev);
     *out = ctx;
     return KGC_OK;
@@ -240,6 +243,8 @@ void kgc_destroy(kgc_ctx* ctx) {
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto e : ctx->ev_split)
         if (e) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     cudaSetDevice(prev);
@@ -597,7 +602,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         }
         {
             const char* e = getenv("KGC_T2_PREFETCH");
-            tp.t2pf = e ? atoi(e) : 1;
+            tp.t2pf = e ? atoi(e) : (tc2 ? 1 : 0);  // measured: helps the pair kernel, not the 1-CTA one
         }
         tp.Kpad = Kpad;
         tp.bq = bq;
@@ -691,14 +696,20 @@ static int split_range(kgc_ctx* ctx, const float* E_in, const float* Rel_in, lon
     *Rel_dev = Rel;
     CK(ensure(ctx->kt, (size_t)N * 4));
     CK(ensure(ctx->mm_t, 2 * 4));
-    CK(ensure(ctx->est_hist, 4096 * 4));
+    CK(ensure(ctx->est_hist, 2 * 4097 * 4));  // histogram + its cumulative form
     CK(ensure(ctx->est_cost, (size_t)R * 8));
+    CK(cudaEventRecord(ctx->ev_split[0], s));
     launch_split_estimate(E, Rel, N, R, d, norm, eps, P<float>(ctx->kt), P<unsigned>(ctx->mm_t),
-                          P<unsigned>(ctx->est_hist), P<double>(ctx->est_cost), s);
+                          P<unsigned>(ctx->est_hist), P<unsigned long long>(ctx->est_cost), s);
     LAUNCHED(5);
-    std::vector<double> cost((size_t)R);
-    CK(cudaMemcpyAsync(cost.data(), ctx->est_cost.p, (size_t)R * 8, cudaMemcpyDeviceToHost, s));
+    std::vector<unsigned long long> cnt((size_t)R);
+    CK(cudaMemcpyAsync(cnt.data(), ctx->est_cost.p, (size_t)R * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(ctx->ev_split[1], s));
     CK(cudaStreamSynchronize(s));
+    // estimated surviving work per relation: sampled in-range tail counts scaled to N queries
+    // (+1: never a zero-cost relation); integer inputs, so identical on every rank
+    std::vector<double> cost((size_t)R);
+    for (long long r = 0; r < R; ++r) cost[(size_t)r] = (double)cnt[(size_t)r] * (double)N / EST_SAMPLES + 1.0;
     double total = 0.0;
     for (double c : cost) total += c;
     const int W = ctx->opt.world, k = ctx->opt.rank;
@@ -756,11 +767,14 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
         set_err(ctx, "kgc_join: NULL E or Rel");
         return KGC_EINVAL;
     }
+    const auto host_t0 = std::chrono::steady_clock::now();
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(ctx->device);
     int rc = KGC_OK;
+    bool did_split = false;
     if (ctx->opt.world > 1 && ctx->opt.split == 0) {
+        did_split = true;
         // Rank-local split: query-tile ranges balanced by an estimated per-relation cost
         // (launch_split_estimate); each rank then preprocesses only the relations its range touches.
         const long long bq = plan_bq(ctx, norm, d, N);
@@ -788,6 +802,10 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
     if (rc != KGC_OK) {
         cudaStreamSynchronize(ctx->stream);
         cudaGetLastError();
+    } else {
+        ctx->st.ms_split = 0.f;
+        if (did_split) cudaEventElapsedTime(&ctx->st.ms_split, ctx->ev_split[0], ctx->ev_split[1]);
+        ctx->st.ms_host = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
     }
     cudaSetDevice(prev);
     return rc;

@@ -9,6 +9,7 @@ namespace kgc {
 constexpr int BM = 128;          // query rows per tile (= TMEM lanes = UMMA M)
 constexpr int BN_TC = 256;       // tail rows per tile, tensor-core engine (UMMA N)
 constexpr int BN_HALF = 128;     // tile rows (query and tail), FP16x2 L1 engine
+constexpr int EST_SAMPLES = 256;  // sampled queries per relation, rank-local split estimate
 constexpr int SIMT_T = 64;       // tile rows (query and tail), FP32 SIMT engines
 constexpr int SORT_IPB = 2048;   // radix-sort items per block (256 threads x 8)
 constexpr int TC_MAX_KPAD = 256; // tensor-core engine supports d <= 256
@@ -99,7 +100,7 @@ void launch_stage_half(const float* E, const float* Rel, const int* perm, long l
                        int QT, int tile0, int ntiles, float theta, float gam, void* out, float4* qs, float* rt,
                        cudaStream_t s);
 void launch_split_estimate(const float* E, const float* Rel, long long N, long long R, int d, int norm, float theta,
-                           float* kt, unsigned int* mm, unsigned int* hist, double* cost, cudaStream_t s);
+                           float* kt, unsigned int* mm, unsigned int* hist, unsigned long long* cnt, cudaStream_t s);
 void launch_absmax(const float* E, long long nE, const float* Rel, long long nR, unsigned int* out, cudaStream_t s);
 
 // ---- multi-pivot pruning (pivots.cu) ----

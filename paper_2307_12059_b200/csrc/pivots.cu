@@ -109,11 +109,11 @@ __global__ void __launch_bounds__(1024) pick_pivots_kernel(const float* __restri
 }
 
 // ----------------------------------------------------------------- keys
-// QUERY: a block walks MK_CH chunks of 32 entities against 16 relations (warp
-// w: relations w, w + 8; lane = entity); tails: 128 threads, MK_CH chunks of
+// QUERY: a block walks `nch` chunks of 32 entities against 16 relations (warp
+// w: relations w, w + 8; lane = entity); tails: 128 threads, `nch` chunks of
 // 128 entities (warp w: entities w*32 + lane).  Key min/max per (segment,
 // pivot) are kept per warp across chunks: one atomic pair per warp at the end.
-constexpr int MK_CH = 8;
+// nch is chosen so the grid still fills the GPU (~8 blocks per SM).
 // Row stride (floats) of the entity tile: a multiple of 4 whose quarter is odd,
 // so the per-lane float4 row reads of a quarter-warp hit distinct bank groups.
 __host__ __device__ inline int mk_stride(int d) {
@@ -123,7 +123,7 @@ __host__ __device__ inline int mk_stride(int d) {
 }
 template <int NORM, bool QUERY, int K>
 __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
-                                                      long long N, long long nseg, int d, int /*Kr*/,
+                                                      long long N, long long nseg, int d, int nch,
                                                       const float* __restrict__ P, float* __restrict__ keys,
                                                       unsigned int* minmax, unsigned int* nonfinite) {
     extern __shared__ __align__(16) float mk_smem[];
@@ -154,8 +154,8 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
     for (int u = 0; u < NU; ++u)
 #pragma unroll
         for (int k = 0; k < K; ++k) { mn[u][k] = FLT_MAX; mx[u][k] = 0.f; }
-    for (int ch = 0; ch < MK_CH; ++ch) {
-        const long long h0 = ((long long)blockIdx.x * MK_CH + ch) * ENT;
+    for (int ch = 0; ch < nch; ++ch) {
+        const long long h0 = ((long long)blockIdx.x * nch + ch) * ENT;
         if (h0 >= N) break;
         __syncthreads();
         for (int x = threadIdx.x; x < ENT * S; x += blockDim.x) {
@@ -393,11 +393,17 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
     const int S = mk_stride(d), D4 = (d + 3) / 4 * 4;
     const int ent = query ? 32 : 128;
     const size_t smem = (size_t)(ent * S + K * D4 + (query ? 16 * D4 : 0)) * sizeof(float);
-    dim3 grid((unsigned)((N + (long long)ent * MK_CH - 1) / ((long long)ent * MK_CH)),
-              query ? (unsigned)((nseg + 15) / 16) : 1u);
+    const long long gy = query ? (nseg + 15) / 16 : 1;
+    const long long chunks = (N + ent - 1) / ent;
+    long long gx_target = (148LL * 8 + gy - 1) / gy;
+    if (gx_target < 1) gx_target = 1;
+    long long nch = (chunks + gx_target - 1) / gx_target;
+    if (nch < 1) nch = 1;
+    if (nch > 8) nch = 8;
+    dim3 grid((unsigned)((chunks + nch - 1) / nch), (unsigned)gy);
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, query ? 256 : 128, smem, s>>>(E, Rel, N, nseg, d, K, P, keys, minmax, nonfinite);
+        kern<<<grid, query ? 256 : 128, smem, s>>>(E, Rel, N, nseg, d, (int)nch, P, keys, minmax, nonfinite);
     };
     auto byK = [&](auto n_, auto q_) {
         constexpr int NN = decltype(n_)::value;

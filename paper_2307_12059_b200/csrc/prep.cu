@@ -78,58 +78,70 @@ __global__ void tail_keys_kernel(const float* __restrict__ E, long long N, int d
     }
 }
 
-// d(h + r, p) for every (h, r): a block walks QK_CH chunks of 32 entity rows
-// (in shared memory) against 16 relation rows; warp w handles relations w and
-// w + 8, lane = entity.  Per-relation key min/max are kept per warp across the
-// chunks, so each warp issues one atomic pair per relation (not per chunk).
-constexpr int QK_ENT = 32, QK_REL = 16, QK_CH = 8;
+// d(h + r, p) for every (h, r): a block walks `nch` chunks of 32 entity rows
+// (in shared memory, fp32) against 32 relation rows (shared memory, FP64:
+// converted once per block); warp w handles relations w, w + 8, w + 16,
+// w + 24 with lane = entity, so each entity value is converted to FP64 once
+// per 4 relations.  Per-relation key min/max are kept per warp across the
+// chunks (one atomic pair per relation per warp).
+constexpr int QK_ENT = 32, QK_RPW = 4;  // relations per block: 8 * rpw, rpw <= QK_RPW (shared memory for large d)
 template <int NORM, bool PIV>
 __global__ void __launch_bounds__(256) query_keys_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
-                                                         long long N, long long R, int d,
+                                                         long long N, long long R, int d, int nch, int rpw,
                                                          const double* __restrict__ pivot, float* __restrict__ kq,
                                                          unsigned int* minmax, unsigned int* nonfinite) {
-    extern __shared__ float qk_smem[];
-    const int S = (d & 1) ? d : d + 1;  // odd row stride: conflict-free column reads
-    float* Es = qk_smem;                 // [QK_ENT][S]
-    float* Rs = qk_smem + QK_ENT * S;    // [QK_REL][d]
+    extern __shared__ double qk_smem_d[];
+    const int QK_REL = 8 * rpw;
+    double* Rs = qk_smem_d;                                 // [QK_REL][d] relation rows (FP64, exact)
+    double* Ps = Rs + (size_t)QK_REL * d;                   // [d] pivot (PIV)
+    const int S = (d & 1) ? d : d + 1;                      // odd row stride: conflict-free column reads
+    float* Es = reinterpret_cast<float*>(Ps + (PIV ? d : 0));  // [QK_ENT][S]
     const long long r0 = (long long)blockIdx.y * QK_REL;
     bool bad = false;
     for (int x = threadIdx.x; x < QK_REL * d; x += blockDim.x) {
-        int i = x / d, k = x % d;
-        float v = (r0 + i < R) ? Rel[(r0 + i) * d + k] : 0.f;
+        const int i = x / d, k = x % d;
+        const float v = (r0 + i < R) ? Rel[(r0 + i) * d + k] : 0.f;
         bad |= !isfinite(v);
-        Rs[i * d + k] = v;
+        Rs[x] = (double)v;
     }
+    if (PIV)
+        for (int k = threadIdx.x; k < d; k += blockDim.x) Ps[k] = pivot[k];
     if (blockIdx.x == 0 && __syncthreads_or(bad)) {
         if (threadIdx.x == 0) atomicOr(nonfinite, 1u);
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    float mn[2] = {FLT_MAX, FLT_MAX}, mx[2] = {0.f, 0.f};
-    for (int ch = 0; ch < QK_CH; ++ch) {
-        const long long h0 = ((long long)blockIdx.x * QK_CH + ch) * QK_ENT;
+    float mn[QK_RPW], mx[QK_RPW];
+#pragma unroll
+    for (int u = 0; u < QK_RPW; ++u) { mn[u] = FLT_MAX; mx[u] = 0.f; }
+    for (int ch = 0; ch < nch; ++ch) {
+        const long long h0 = ((long long)blockIdx.x * nch + ch) * QK_ENT;
         if (h0 >= N) break;
-        __syncthreads();  // previous chunk fully consumed
+        __syncthreads();  // previous chunk fully consumed (and Rs / Ps written)
         for (int x = threadIdx.x; x < QK_ENT * d; x += blockDim.x) {
-            int i = x / d, k = x % d;
+            const int i = x / d, k = x % d;
             Es[i * S + k] = (h0 + i < N) ? E[(h0 + i) * d + k] : 0.f;
         }
         __syncthreads();
         const long long h = h0 + lane;
+        const float* es = Es + lane * S;
+        double s[QK_RPW];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int rl = w + 8 * u;
-            const long long r = r0 + rl;
-            if (r >= R) break;
-            double s = 0.0;
-            const float* es = Es + lane * S;
-            const float* rs = Rs + rl * d;
-            for (int k = 0; k < d; ++k) {
-                double x = (double)es[k] + (double)rs[k];  // connector_1(h, r) = h + r
-                if (PIV) x -= pivot[k];
-                s += NORM == 1 ? fabs(x) : x * x;
+        for (int u = 0; u < QK_RPW; ++u) s[u] = 0.0;
+        for (int k = 0; k < d; ++k) {
+            const double e = (double)es[k];
+#pragma unroll
+            for (int u = 0; u < QK_RPW; ++u) {
+                if (u >= rpw) break;
+                double x = e + Rs[(w + 8 * u) * d + k];  // connector_1(h, r) = h + r
+                if (PIV) x -= Ps[k];
+                s[u] += NORM == 1 ? fabs(x) : x * x;
             }
-            float key = __double2float_rn(NORM == 2 ? sqrt(s) : s);
-            if (h < N) {
+        }
+#pragma unroll
+        for (int u = 0; u < QK_RPW; ++u) {
+            const long long r = r0 + w + 8 * u;
+            const float key = __double2float_rn(NORM == 2 ? sqrt(s[u]) : s[u]);
+            if (u < rpw && h < N && r < R) {
                 kq[r * N + h] = key;
                 mn[u] = fminf(mn[u], key);
                 mx[u] = fmaxf(mx[u], key);
@@ -137,9 +149,9 @@ __global__ void __launch_bounds__(256) query_keys_kernel(const float* __restrict
         }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < QK_RPW; ++u) {
         const long long r = r0 + w + 8 * u;
-        if (r >= R) break;
+        if (u >= rpw || r >= R) break;
         const float a = warp_min_f(mn[u]), z = warp_max_f(mx[u]);
         if (lane == 0) {
             atomicMin(&minmax[2 * r], __float_as_uint(a));
@@ -185,11 +197,21 @@ void launch_query_keys(const float* E, const float* Rel, long long N, long long 
                        cudaStream_t s) {
     init_minmax_kernel<<<grid_for(R, 256), 256, 0, s>>>(minmax, R);
     const int S = (d & 1) ? d : d + 1;
-    size_t smem = (size_t)(QK_ENT * S + QK_REL * d) * sizeof(float);
-    dim3 grid((unsigned)((N + QK_ENT * QK_CH - 1) / (QK_ENT * QK_CH)), (unsigned)((R + QK_REL - 1) / QK_REL));
+    int rpw = QK_RPW;
+    auto smem_for = [&](int rp) {
+        return (size_t)(8 * rp * d + (pivot ? d : 0)) * sizeof(double) + (size_t)QK_ENT * S * sizeof(float);
+    };
+    while (rpw > 1 && smem_for(rpw) > 200 * 1024) rpw >>= 1;
+    const size_t smem = smem_for(rpw);
+    // chunks per block: enough blocks to fill the GPU (~8 per SM), at most 8 chunks
+    const long long gy = (R + 8 * rpw - 1) / (8 * rpw), chunks = (N + QK_ENT - 1) / QK_ENT;
+    long long gx_target = (148LL * 8 + gy - 1) / gy;
+    long long nch = (chunks + gx_target - 1) / gx_target;
+    nch = nch < 1 ? 1 : (nch > 8 ? 8 : nch);
+    dim3 grid((unsigned)((chunks + nch - 1) / nch), (unsigned)gy);
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, 256, smem, s>>>(E, Rel, N, R, d, pivot, kq, minmax, nonfinite);
+        kern<<<grid, 256, smem, s>>>(E, Rel, N, R, d, (int)nch, rpw, pivot, kq, minmax, nonfinite);
     };
     if (norm == 1) {
         if (pivot) go(query_keys_kernel<1, true>); else go(query_keys_kernel<1, false>);
@@ -643,7 +665,7 @@ __device__ __forceinline__ size_t stage_off(int i, int k, int ROWS) {
 
 // grid: one block per tile; 256 threads.  `rel` == nullptr for tails.
 template <bool TC>
-__global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
+__global__ void __launch_bounds__(1024) stage_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
                                                     const int* __restrict__ perm, long long N, int d, int Kpad,
                                                     int ROWS, int QT, int tile0, int norm, float theta,
                                                     float* __restrict__ out, float4* __restrict__ qs,
@@ -657,14 +679,14 @@ __global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ E,
     const int* pr = perm + (Rel ? r * N : 0);
     const float* rel = Rel ? Rel + r * d : nullptr;
     float* dst = out + (size_t)blockIdx.x * ROWS * Kpad;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    __shared__ float sTn[8], sTd[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    __shared__ float sTn[32], sTd[32];
     float tn_max = 0.f, td_max = 0.f;
 
     // rows handled by warp w; TC: lanes over k (4 consecutive k per lane),
     // SIMT: lanes over rows.
     if (TC) {
-        for (int i = w; i < ROWS; i += 8) {
+        for (int i = w; i < ROWS; i += NW) {
             long long p = t_in_rel * ROWS + i;
             bool valid = p < N;
             long long h = valid ? pr[p] : 0;
@@ -712,7 +734,7 @@ __global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ E,
             }
         }
     } else {
-        for (int g = w; g < ROWS / 32; g += 8) {
+        for (int g = w; g < ROWS / 32; g += NW) {
             int i = g * 32 + lane;
             long long p = t_in_rel * ROWS + i;
             bool valid = p < N;
@@ -751,7 +773,7 @@ __global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ E,
         __syncthreads();
         if (threadIdx.x == 0) {
             float a = 0.f, b = 0.f;
-            for (int x = 0; x < 8; ++x) {
+            for (int x = 0; x < NW; ++x) {
                 a = fmaxf(a, sTn[x]);
                 b = fmaxf(b, sTd[x]);
             }
@@ -767,25 +789,28 @@ __global__ void __launch_bounds__(256) stage_kernel(const float* __restrict__ E,
 // (N / S) * sum over samples of #tails with |key(q) - key(t)| <= theta (bin
 // resolution).  Integer histogram + fixed-order per-relation sums: identical
 // on every rank.  Only steers load balance; never what is computed.
-constexpr int ESTB = 4096, EST_S = 256;
+constexpr int ESTB = 4096, EST_S = EST_SAMPLES;
 
+// warp per tail row (lanes over k, coalesced)
 __global__ void est_tail_keys_kernel(const float* __restrict__ E, long long N, int d, int norm, float* kt,
                                      unsigned int* mm) {
+    const int lane = threadIdx.x & 31;
+    const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     float mn = FLT_MAX, mx = 0.f;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
-        float s = 0.f;
-        for (int k = 0; k < d; ++k) {
+    for (long long i = w0; i < N; i += nw) {
+        float acc = 0.f;
+        for (int k = lane; k < d; k += 32) {
             const float v = E[i * d + k];
-            s = norm == 1 ? s + fabsf(v) : fmaf(v, v, s);
+            acc = norm == 1 ? acc + fabsf(v) : fmaf(v, v, acc);
         }
-        const float key = norm == 2 ? sqrtf(s) : s;
-        kt[i] = key;
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        const float key = norm == 2 ? sqrtf(acc) : acc;
+        if (lane == 0) kt[i] = key;
         mn = fminf(mn, key);
         mx = fmaxf(mx, key);
     }
-    mn = warp_min_f(mn);
-    mx = warp_max_f(mx);
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         atomicMin(&mm[0], __float_as_uint(mn));
         atomicMax(&mm[1], __float_as_uint(mx));
     }
@@ -801,52 +826,84 @@ __global__ void est_hist_kernel(const float* __restrict__ kt, long long N, const
     }
 }
 
-// one block per relation; thread s < EST_S takes head h = s N / EST_S
-__global__ void est_relation_cost_kernel(const float* __restrict__ E, const float* __restrict__ Rel, long long N,
-                                         int d, int norm, float theta, const unsigned int* mm,
-                                         const unsigned int* __restrict__ hist, double* cost) {
-    __shared__ unsigned int cum[ESTB + 1];
-    __shared__ double part[EST_S];
+// exclusive-to-inclusive prefix of the histogram: cum[0] = 0, cum[b + 1] = sum of hist[0..b]
+// (one block of 1024 threads, 4 bins per thread; integer sums, identical on every rank)
+__global__ void __launch_bounds__(1024) est_cum_kernel(const unsigned int* __restrict__ hist, unsigned int* cum) {
+    __shared__ unsigned int ws[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    unsigned int v[4], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { v[i] = hist[t * 4 + i]; sum += v[i]; }
+    unsigned int inc = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int x = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += x;
+    }
+    if (lane == 31) ws[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        unsigned int x = ws[lane], y = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int z = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += z;
+        }
+        ws[lane] = y - x;  // exclusive warp offsets
+    }
+    __syncthreads();
+    unsigned int run = ws[w] + inc - sum;
+    if (t == 0) cum[0] = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { run += v[i]; cum[t * 4 + i + 1] = run; }
+}
+
+// grid (R, EST_S / 32): block y of relation r takes samples y*32 .. y*32+31, 4 per warp with the
+// loads of all 4 in flight; sample s is head h = s N / EST_S, q = h + r (lanes over k); the count
+// of tails within theta comes from the cumulative histogram.  Integer atomics: the per-relation
+// totals are exact and order-independent, so every rank derives the same split.
+__global__ void __launch_bounds__(256) est_relation_cost_kernel(const float* __restrict__ E,
+                                                                const float* __restrict__ Rel, long long N, int d,
+                                                                int norm, float theta, const unsigned int* mm,
+                                                                const unsigned int* __restrict__ cum,
+                                                                unsigned long long* cnt) {
     const long long r = blockIdx.x;
     const float lo = __uint_as_float(mm[0]), hi = __uint_as_float(mm[1]);
     const float sc = hi > lo ? (float)ESTB / (hi - lo) : 0.f;
-    if (threadIdx.x == 0) {  // inclusive prefix, fixed order
-        unsigned int c = 0;
-        cum[0] = 0;
-        for (int b = 0; b < ESTB; ++b) { c += hist[b]; cum[b + 1] = c; }
-    }
-    __syncthreads();
-    const int s = threadIdx.x;
-    double cnt = 0.0;
-    if (s < EST_S && N > 0) {
-        const long long h = (long long)s * N / EST_S;
-        float acc = 0.f;
-        for (int k = 0; k < d; ++k) {
-            const float v = E[h * d + k] + Rel[r * d + k];
-            acc = norm == 1 ? acc + fabsf(v) : fmaf(v, v, acc);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int s0 = blockIdx.y * 32 + w * 4;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = lane; k < d; k += 32) {
+        const float rk = Rel[r * d + k];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long h = (long long)(s0 + u) * N / EST_S;
+            const float v = E[h * d + k] + rk;
+            acc[u] = norm == 1 ? acc[u] + fabsf(v) : fmaf(v, v, acc[u]);
         }
-        const float key = norm == 2 ? sqrtf(acc) : acc;
+    }
+    unsigned long long c = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        float a = acc[u];
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        const float key = norm == 2 ? sqrtf(a) : a;
         int b0 = (int)floorf((key - theta - lo) * sc), b1 = (int)floorf((key + theta - lo) * sc);
         b0 = b0 < 0 ? 0 : (b0 > ESTB ? ESTB : b0);
         b1 = b1 < -1 ? -1 : (b1 >= ESTB ? ESTB - 1 : b1);
-        cnt = b1 >= b0 ? (double)(cum[b1 + 1] - cum[b0]) : 0.0;
+        c += b1 >= b0 ? (unsigned long long)(cum[b1 + 1] - cum[b0]) : 0ull;
     }
-    if (s < EST_S) part[s] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int i = 0; i < EST_S; ++i) t += part[i];
-        cost[r] = t * (double)N / EST_S + 1.0;  // +1: never a zero-cost relation
-    }
+    if (lane == 0) atomicAdd(&cnt[r], c);
 }
 
 void launch_split_estimate(const float* E, const float* Rel, long long N, long long R, int d, int norm, float theta,
-                           float* kt, unsigned int* mm, unsigned int* hist, double* cost, cudaStream_t s) {
+                           float* kt, unsigned int* mm, unsigned int* hist, unsigned long long* cnt, cudaStream_t s) {
     init_minmax_kernel<<<1, 32, 0, s>>>(mm, 1);
-    cudaMemsetAsync(hist, 0, ESTB * sizeof(unsigned int), s);
-    est_tail_keys_kernel<<<grid_for(N, 256), 256, 0, s>>>(E, N, d, norm, kt, mm);
+    cudaMemsetAsync(hist, 0, 2 * (ESTB + 1) * sizeof(unsigned int), s);
+    cudaMemsetAsync(cnt, 0, (size_t)R * sizeof(unsigned long long), s);
+    est_tail_keys_kernel<<<grid_for(N * 32, 256, 148 * 8), 256, 0, s>>>(E, N, d, norm, kt, mm);
     est_hist_kernel<<<grid_for(N, 256), 256, 0, s>>>(kt, N, mm, hist);
-    est_relation_cost_kernel<<<(unsigned)R, EST_S, 0, s>>>(E, Rel, N, d, norm, theta, mm, hist, cost);
+    unsigned int* cum = hist + (ESTB + 1);
+    est_cum_kernel<<<1, 1024, 0, s>>>(hist, cum);
+    est_relation_cost_kernel<<<dim3((unsigned)R, EST_S / 32), 256, 0, s>>>(E, Rel, N, d, norm, theta, mm, cum, cnt);
 }
 
 // ------------------------------------------------------------ FP16x2 staging
@@ -921,7 +978,7 @@ void launch_stage_tails(const float* E, const int* tperm, long long N, int d, in
                         float* Tp, float* T2, float2* tstile, cudaStream_t s) {
     if (TT <= 0) return;
     if (tc_layout)
-        stage_kernel<true><<<TT, 256, 0, s>>>(E, nullptr, tperm, N, d, Kpad, BN, 1, 0, 2, 0.f, Tp, nullptr, T2, tstile,
+        stage_kernel<true><<<TT, 1024, 0, s>>>(E, nullptr, tperm, N, d, Kpad, BN, 1, 0, 2, 0.f, Tp, nullptr, T2, tstile,
                                               tc_layout == 2 ? BN / 2 : BN);
     else
         stage_kernel<false><<<TT, 256, 0, s>>>(E, nullptr, tperm, N, d, Kpad, BN, 1, 0, 2, 0.f, Tp, nullptr, T2, tstile,

@@ -49,7 +49,7 @@ class kgc_stats_t(ctypes.Structure):
                 ("ms_total", ctypes.c_float), ("ms_h2d", ctypes.c_float), ("ms_keys", ctypes.c_float),
                 ("ms_sort", ctypes.c_float), ("ms_ranges", ctypes.c_float), ("ms_stage", ctypes.c_float),
                 ("ms_tiles", ctypes.c_float), ("ms_recheck", ctypes.c_float), ("pivots_used", ctypes.c_int32),
-                ("engine", ctypes.c_int32)]
+                ("engine", ctypes.c_int32), ("ms_split", ctypes.c_float), ("ms_host", ctypes.c_float)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -216,6 +216,48 @@ def kgc_shard_range(cum, total: int, rank: int, world: int):
     if cost < 0:
         raise KgcError(int(cost), "kgc_shard_range: invalid argument")
     return int(b.value), int(e.value), int(cost)
+
+
+# ----------------------------------------------------------- multi-GPU finish
+
+def gather_results(res, root: int = 0, group=None):
+    """Multi-GPU finish: all-gather of the per-rank result
+    counts, then the sharded (h, r, t, dist) lists gathered to `root` by
+    point-to-point transfers over the process group (NCCL for device tensors,
+    gloo for host arrays).  Plumbing only: no arithmetic of the method.
+
+    `res`: this rank's results, a TRIPLET_DTYPE numpy array or an (n, 4)
+    int32 torch tensor holding the same 16-byte records (host or device).
+    Returns (counts, gathered): the per-rank counts (every rank) and, on
+    `root`, the concatenation in rank order as a TRIPLET_DTYPE array (None
+    elsewhere)."""
+    import torch
+    import torch.distributed as dist
+    if isinstance(res, np.ndarray):
+        t = torch.from_numpy(np.ascontiguousarray(res).view(np.int32).reshape(-1, 4))
+    else:
+        t = res.reshape(-1, 4).contiguous()
+    if dist.get_backend(group) == "nccl" and t.device.type != "cuda":
+        t = t.cuda()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+    cnt = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(cnt, n, group=group)
+    counts = [int(c.item()) for c in cnt]
+    if rank != root:
+        if counts[rank]:
+            dist.send(t, dist.get_global_rank(group, root) if group is not None else root, group=group)
+        return counts, None
+    parts = []
+    for src in range(world):
+        if src == root:
+            parts.append(t)
+        elif counts[src]:
+            buf = torch.empty((counts[src], 4), dtype=torch.int32, device=t.device)
+            dist.recv(buf, dist.get_global_rank(group, src) if group is not None else src, group=group)
+            parts.append(buf)
+    allr = torch.cat(parts) if parts else torch.empty((0, 4), dtype=torch.int32)
+    return counts, allr.cpu().numpy().reshape(-1).view(TRIPLET_DTYPE)
 
 
 # ----------------------------------------------------------- convenience

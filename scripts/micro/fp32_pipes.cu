@@ -80,12 +80,28 @@ __global__ void k_l2(const float* in, float* out){
   }
   float s=0; for(int i=0;i<16;++i) s+=acc[i]; out[blockIdx.x*blockDim.x+threadIdx.x]=s;
 }
+// mode 5: packed |q - t|: d2 = q2 - t2 (FADD2), clear both sign bits (LOP3 on the 64-bit pair), acc2 += (FADD2)
+__device__ __forceinline__ unsigned long long abs2(unsigned long long a){ return a & 0x7fffffff7fffffffULL; }
+__global__ void k_abs2(const float* in, float* out){
+  unsigned long long q[4], t[2], acc[8];
+  for(int i=0;i<4;++i){ float x=in[threadIdx.x+i]; q[i]=pk(x,x); }
+  for(int i=0;i<2;++i){ t[i]=pk(in[threadIdx.x+64+2*i], in[threadIdx.x+65+2*i]); }
+  for(int i=0;i<8;++i) acc[i]=0;
+  for(int it=0; it<ITERS; ++it){
+    #pragma unroll
+    for(int a=0;a<4;++a)
+    #pragma unroll
+      for(int b=0;b<2;++b){ unsigned long long d=sub2(q[a],t[b]); acc[a*2+b]=add2(acc[a*2+b], abs2(d)); }
+    q[0]=add2(q[0], 1);
+  }
+  float s=0; for(int i=0;i<8;++i){ float x,y; upk(acc[i],x,y); s+=x+y;} out[blockIdx.x*blockDim.x+threadIdx.x]=s;
+}
 int main(){
   float *in,*out; cudaMalloc(&in, 4096*4); cudaMalloc(&out, 148*16*256*4); cudaMemset(in,0,4096*4);
   int sms=148, clk_khz=0; cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
-  const char* names[]={"abs: FADD+FADD|.| per elem","max2: 2xFMNMX+FADD2 per 2 elem","max1: FMNMX+FADD per elem","l2pk: FADD2+FFMA2 per 2 elem","l2: FADD+FFMA per elem"};
-  void (*ks[])(const float*,float*)={k_abs,k_max2,k_max1,k_l2pk,k_l2};
-  for(int blocks_per_sm : {4, 8}) for(int m=0;m<5;++m){
+  const char* names[]={"abs: FADD+FADD|.| per elem","max2: 2xFMNMX+FADD2 per 2 elem","max1: FMNMX+FADD per elem","l2pk: FADD2+FFMA2 per 2 elem","l2: FADD+FFMA per elem","abs2: FADD2+LOP3x2+FADD2 per 2 elem"};
+  void (*ks[])(const float*,float*)={k_abs,k_max2,k_max1,k_l2pk,k_l2,k_abs2};
+  for(int blocks_per_sm : {4, 8}) for(int m=0;m<6;++m){
     cudaEvent_t a,b; cudaEventCreate(&a); cudaEventCreate(&b);
     ks[m]<<<sms*blocks_per_sm,256>>>(in,out); cudaDeviceSynchronize();
     cudaEventRecord(a); ks[m]<<<sms*blocks_per_sm,256>>>(in,out); cudaEventRecord(b); cudaEventSynchronize(b);

@@ -65,8 +65,15 @@ def _worker(rank, world, port, E, Rel, norm, eps, q):
         dist.all_reduce(counts)                      # as bench.py does after every step
         gathered = [None] * world
         dist.all_gather_object(gathered, (b, e, [tuple(x) for x in zip(res["h"], res["r"], res["t"])]))
+        # the library's multi-GPU finish: count all-gather + results gathered to rank 0
+        res16 = np.zeros(res.size, kgc.TRIPLET_DTYPE)
+        for f in ("h", "r", "t"):
+            res16[f] = res[f]
+        res16["dist"] = res["dist"].astype(np.float32)
+        cnts, allres = kgc.gather_results(res16, root=0)
+        assert sum(cnts) == int(counts[0]) and cnts[rank] == res.size
         if rank == 0:
-            q.put((int(counts[0]), int(counts[1]), total, gathered))
+            q.put((int(counts[0]), int(counts[1]), total, gathered, allres))
     finally:
         dist.destroy_process_group()
 
@@ -90,7 +97,7 @@ def test_two_rank_shards_union_equals_full_join(norm):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, E, Rel, norm, eps, q)) for r in range(2)]
     for p in procs:
         p.start()
-    n_all, cost_all, total, gathered = q.get(timeout=300)
+    n_all, cost_all, total, gathered, allres = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -100,6 +107,9 @@ def test_two_rank_shards_union_equals_full_join(norm):
     assert not (shards[0] & shards[1])
     assert shards[0] | shards[1] == full_set
     assert n_all == len(full_set)
+    # gather_results: rank 0 holds every shard's records, in rank order, nothing lost or duplicated
+    assert allres.size == n_all
+    assert set(zip(allres["h"].tolist(), allres["r"].tolist(), allres["t"].tolist())) == full_set
     assert cost_all == total
     (b0, e0, _), (b1, e1, _) = gathered
     assert b0 == 0 and e0 == b1          # contiguous split of the query tiles
