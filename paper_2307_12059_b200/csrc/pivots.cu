@@ -54,10 +54,22 @@ __global__ void __launch_bounds__(1024) pick_pivots_kernel(const float* __restri
     __shared__ float bv[32];
     __shared__ int bi[32];
     __shared__ int chosen;
-    for (int x = threadIdx.x; x < S * d; x += blockDim.x) {
-        const int sidx = x / d, k = x % d;
-        const long long row = (long long)sidx * N / S;
-        X[sidx * st + k] = E[row * d + k];
+    {   // warp per sample row (lanes over k, coalesced), 4 rows' loads in flight per lane
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int s0 = w * 4; s0 < S; s0 += nw * 4) {
+            for (int k0 = 0; k0 < d; k0 += 32) {
+                const int k = k0 + lane;
+                float v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int sidx = s0 + u;
+                    v[u] = (sidx < S && k < d) ? __ldg(E + ((long long)sidx * N / S) * d + k) : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (s0 + u < S && k < d) X[(s0 + u) * st + k] = v[u];
+            }
+        }
     }
     for (int k = threadIdx.x; k < d; k += blockDim.x) {
         const float v = p0 ? (float)p0[k] : 0.f;
@@ -67,15 +79,23 @@ __global__ void __launch_bounds__(1024) pick_pivots_kernel(const float* __restri
     __syncthreads();
     const int sidx = threadIdx.x;
     auto dist_to_piv = [&]() {
-        float sum = 0.f;
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains
         if (sidx < S) {
             const float* xr = X + sidx * st;
-            for (int k = 0; k < d; ++k) {
+            int k = 0;
+            for (; k + 4 <= d; k += 4) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float x = xr[k + u] - piv[k + u];
+                    s4[u] = NORM == 1 ? s4[u] + fabsf(x) : fmaf(x, x, s4[u]);
+                }
+            }
+            for (; k < d; ++k) {
                 const float x = xr[k] - piv[k];
-                sum = NORM == 1 ? sum + fabsf(x) : fmaf(x, x, sum);
+                s4[0] = NORM == 1 ? s4[0] + fabsf(x) : fmaf(x, x, s4[0]);
             }
         }
-        return sum;  // squared for L2 (monotone: fine for argmax)
+        return (s4[0] + s4[1]) + (s4[2] + s4[3]);  // squared for L2 (monotone: fine for argmax)
     };
     float mind = sidx < S ? dist_to_piv() : -1.f;
     for (int kk = 1; kk < K; ++kk) {
