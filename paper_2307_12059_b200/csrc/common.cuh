@@ -268,6 +268,50 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
+// Tensor-core epilogue: max over 32 accumulator columns of (acc_j - th_j), th = ||t||^2 / 2 --
+// packed subtraction (FADD2) and 3-input max (FMNMX3), both sm_100 forms: half the instructions
+// of FFMA + FMNMX per column.  fl(acc - t/2) = fl(2 acc - t) / 2 exactly, so the test
+// max >= c / 2 is the same decision as max(2 acc - t) >= c.
+__device__ __forceinline__ void sub2_f32(uint32_t a0, uint32_t a1, float t0, float t1, float& d0, float& d1) {
+    unsigned long long A, T, D;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "r"(a0), "r"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(T) : "f"(t0), "f"(t1));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(D) : "l"(A), "l"(T));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(D));
+}
+__device__ __forceinline__ float max3_f32(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float epi_max32(const uint32_t (&r)[32], const float4* __restrict__ th) {
+    float m[4] = {-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f};
+#pragma unroll
+    for (int u4 = 0; u4 < 8; ++u4) {
+        const float4 tt = __ldg(th + u4);
+        float a0, a1, a2, a3;
+        sub2_f32(r[4 * u4 + 0], r[4 * u4 + 1], tt.x, tt.y, a0, a1);
+        sub2_f32(r[4 * u4 + 2], r[4 * u4 + 3], tt.z, tt.w, a2, a3);
+        const int c = (u4 & 1) * 2;
+        m[c] = max3_f32(m[c], a0, a1);
+        m[c + 1] = max3_f32(m[c + 1], a2, a3);
+    }
+    return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+}
+// bit j set iff acc_j - th_j >= ch (the rare path after epi_max32 found a candidate)
+__device__ __forceinline__ uint32_t epi_hits32(const uint32_t (&r)[32], const float4* __restrict__ th, float ch) {
+    uint32_t hit = 0;
+#pragma unroll
+    for (int u4 = 0; u4 < 8; ++u4) {
+        const float4 tt = __ldg(th + u4);
+        hit |= (uint32_t)(__fsub_rn(__uint_as_float(r[4 * u4 + 0]), tt.x) >= ch) << (4 * u4 + 0);
+        hit |= (uint32_t)(__fsub_rn(__uint_as_float(r[4 * u4 + 1]), tt.y) >= ch) << (4 * u4 + 1);
+        hit |= (uint32_t)(__fsub_rn(__uint_as_float(r[4 * u4 + 2]), tt.z) >= ch) << (4 * u4 + 2);
+        hit |= (uint32_t)(__fsub_rn(__uint_as_float(r[4 * u4 + 3]), tt.w) >= ch) << (4 * u4 + 3);
+    }
+    return hit;
+}
+
 // float -> float rounded towards +inf from a double
 __device__ __forceinline__ float f2up(double x) { return __double2float_ru(x); }
 

@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
                 const float eb = Qd * Tm + Qn * Tdm + Qd * Tdm + p.eta * (Qn + Qd) * (Tm + Tdm);
                 const float sl = 4.76837158203125e-07f * (Qn + Tm) * (Qn + Tm);  // 8u (Qn + Tm)^2, fp32 evaluation
                 const float R = thf * thf + 2.0f * eb + sl;
-                // candidate iff 2 acc - ||t||^2 >= c
+                // candidate iff 2 acc - ||t||^2 >= c, tested as acc - ||t||^2/2 >= c/2 (T2 holds ||t||^2/2)
                 // Q2 is an FP32 sum: |Q2 - ||q||^2| <= (Kpad + 4) 2^-23 Q2 (builder)
                 const float c = Q2 - R - (float)(p.Kpad + 4) * 1.1920928955078125e-07f * Q2 - 9.5367431640625e-07f * (Q2 + R);
                 // ||t||^2 of this tile's and the next tile's columns into L1 ahead of use
@@ -216,28 +216,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
                 tc_fence_after();
                 const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_TC + col0);
                 uint32_t ra[32], rb[32];
+                const float ch2 = 0.5f * c;  // T2 holds ||t||^2 / 2 (stage kernel)
                 auto process = [&](const uint32_t (&r)[32], int ch) {
                     const float4* t2 = reinterpret_cast<const float4*>(t2row + ch * 32);
-                    float m0 = -3.0e38f, m1 = -3.0e38f, m2 = -3.0e38f, m3 = -3.0e38f;
-#pragma unroll
-                    for (int u4 = 0; u4 < 8; ++u4) {
-                        const float4 tt = __ldg(t2 + u4);
-                        m0 = fmaxf(m0, fmaf(2.0f, __uint_as_float(r[4 * u4 + 0]), -tt.x));
-                        m1 = fmaxf(m1, fmaf(2.0f, __uint_as_float(r[4 * u4 + 1]), -tt.y));
-                        m2 = fmaxf(m2, fmaf(2.0f, __uint_as_float(r[4 * u4 + 2]), -tt.z));
-                        m3 = fmaxf(m3, fmaf(2.0f, __uint_as_float(r[4 * u4 + 3]), -tt.w));
-                    }
-                    const float m = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-                    if (__any_sync(0xffffffffu, m >= c)) {
-                        uint32_t hit = 0;
-#pragma unroll
-                        for (int u4 = 0; u4 < 8; ++u4) {
-                            const float4 tt = __ldg(t2 + u4);
-                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 0]), -tt.x) >= c) << (4 * u4 + 0);
-                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 1]), -tt.y) >= c) << (4 * u4 + 1);
-                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 2]), -tt.z) >= c) << (4 * u4 + 2);
-                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 3]), -tt.w) >= c) << (4 * u4 + 3);
-                        }
+                    const float m = epi_max32(r, t2);
+                    if (__any_sync(0xffffffffu, m >= ch2)) {
+                        uint32_t hit = epi_hits32(r, t2, ch2);
                         unsigned long long slot = warp_reserve(__popc(hit), p.cand_count);
                         const int colb = j * BN_TC + col0 + ch * 32;
                         while (hit) {

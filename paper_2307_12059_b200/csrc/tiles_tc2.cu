@@ -236,28 +236,12 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
                 tc_fence_after();
                 const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_TC + col0);
                 uint32_t ra[32], rb[32];
+                const float ch2 = 0.5f * c;  // T2 holds ||t||^2 / 2 (stage kernel)
                 auto process = [&](const uint32_t (&r)[32], int ch) {
                     const float4* t2 = reinterpret_cast<const float4*>(t2row + ch * 32);
-                    float m0 = -3.0e38f, m1 = -3.0e38f, m2 = -3.0e38f, m3 = -3.0e38f;
-#pragma unroll
-                    for (int u4 = 0; u4 < 8; ++u4) {
-                        const float4 tt = __ldg(t2 + u4);
-                        m0 = fmaxf(m0, fmaf(2.0f, __uint_as_float(r[4 * u4 + 0]), -tt.x));
-                        m1 = fmaxf(m1, fmaf(2.0f, __uint_as_float(r[4 * u4 + 1]), -tt.y));
-                        m2 = fmaxf(m2, fmaf(2.0f, __uint_as_float(r[4 * u4 + 2]), -tt.z));
-                        m3 = fmaxf(m3, fmaf(2.0f, __uint_as_float(r[4 * u4 + 3]), -tt.w));
-                    }
-                    const float m = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-                    if (__any_sync(0xffffffffu, m >= c)) {
-                        uint32_t hit = 0;
-#pragma unroll
-                        for (int u4 = 0; u4 < 8; ++u4) {
-                            const float4 tt = __ldg(t2 + u4);
-                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 0]), -tt.x) >= c) << (4 * u4 + 0);
-                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 1]), -tt.y) >= c) << (4 * u4 + 1);
-                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 2]), -tt.z) >= c) << (4 * u4 + 2);
-                            hit |= (uint32_t)(fmaf(2.0f, __uint_as_float(r[4 * u4 + 3]), -tt.w) >= c) << (4 * u4 + 3);
-                        }
+                    const float m = epi_max32(r, t2);
+                    if (__any_sync(0xffffffffu, m >= ch2)) {
+                        uint32_t hit = epi_hits32(r, t2, ch2);
                         unsigned long long slot = warp_reserve(__popc(hit), p.cand_count);
                         const int colb = j * BN_TC + col0 + ch * 32;
                         while (hit) {
