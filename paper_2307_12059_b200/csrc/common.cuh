@@ -267,6 +267,9 @@ __device__ __forceinline__ long long balanced_begin(const long long* __restrict_
 __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 // Tensor-core epilogue: max over 32 accumulator columns of (acc_j - th_j), th = ||t||^2 / 2 --
 // packed subtraction (FADD2) and 3-input max (FMNMX3), both sm_100 forms: half the instructions

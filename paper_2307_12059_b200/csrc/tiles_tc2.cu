@@ -25,6 +25,7 @@
 //   b_empty, a_empty, acc_full: tcgen05.commit multicast to both CTAs.
 //   acc_empty (even CTA: 16 arrivals) the 8 epilogue warps of each CTA.
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -55,6 +56,9 @@ int tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
     const int budget = 227 * 1024 - 512 - 2 * BM * 16;
     const int A = BM * Kpad * 4;
     // prefer two A stages when the B ring still buffers >= 64 K-values
+    // (experiment knob KGC_TC2_MINK: the minimum ring depth in K-values for two A stages)
+    const char* e = getenv("KGC_TC2_MINK");
+    const int mink = e ? atoi(e) : 64;
     for (int as = 2; as >= 1; --as) {
         for (int KC : {32, 16, 8}) {
             const int B = HALF * KC * 4;
@@ -62,7 +66,7 @@ int tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
             if (rem <= 0) continue;
             int bs = rem / B;
             if (bs > 6) bs = 6;
-            if (bs >= 2 && (bs * KC >= 64 || as == 1)) {
+            if (bs >= 2 && (bs * KC >= mink || as == 1)) {
                 *a_stages = as;
                 *b_stages = bs;
                 *kc = KC;
@@ -334,6 +338,17 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
             mbar_arrive(&a_full[ai]);
             if (!leader) mbar_arrive_cluster(&a_full[ai], 0);
             if (++ai == a_stages) { ai = 0; aph ^= 1; }
+            if (a_stages == 1 && p.t2pf && it + it_step < it_end) {
+                // one query-tile buffer: the next build waits for every MMA of this item, so pull
+                // the next item's entity rows into L2 now (prefetch.global.L2, one per 128-B line)
+                const int4 wn = p.items[it + it_step];
+                const int rn = wn.x / p.QT;
+                const long long posn = (long long)(wn.x - rn * p.QT) * (2 * BM) + crank * BM + i;
+                if (posn < p.N) {
+                    const char* rowp = reinterpret_cast<const char*>(p.E + (long long)p.qperm[(long long)rn * p.N + posn] * p.d);
+                    for (int b = 0; b < p.d * 4; b += 128) prefetch_l2(rowp + b);
+                }
+            }
         }
         for (int k = 0; k < a_stages; ++k) {  // drain: the last a_empty commits have landed
             mbar_wait(&a_empty[ai], aph ^ 1);
