@@ -117,6 +117,27 @@ def join(E, Rel, norm: int, eps: float, rows=None, threads: int = 0) -> np.ndarr
     return out
 
 
+def topk(E, Rel, norm: int, k: int, exclude_self: bool = False, threads: int = 0) -> np.ndarray:
+    """The k smallest dist3 over all N*R*N triplets (ties broken by (h, r, t)), as a
+    TRIPLET_DTYPE array in ascending order -- the paper's minimum-distance statistic
+    "min_{i,j,k} ||h_i + r_j - t_k||" (reading R16), with or without self edges
+    h = t (P:128 reports both).  Brute force: every distance from ``dist_rows`` (FP64,
+    index-order sums), one stable sort.  Small inputs only (N*R*N values in memory)."""
+    E, Rel = _f32(E), _f32(Rel)
+    N, R = E.shape[0], Rel.shape[0]
+    D = dist_rows(E, Rel, norm, threads=threads)            # (N*R, N), row = h*R + r
+    h = np.repeat(np.arange(N), R * N)
+    r = np.tile(np.repeat(np.arange(R), N), N)
+    t = np.tile(np.arange(N), N * R)
+    dist = D.ravel()
+    keep = h != t if exclude_self else np.ones(dist.size, bool)
+    h, r, t, dist = h[keep], r[keep], t[keep], dist[keep]
+    order = np.lexsort((t, r, h, dist))[:k]                 # primary key: dist
+    out = np.zeros(order.size, dtype=TRIPLET_DTYPE)
+    out["h"], out["r"], out["t"], out["dist"] = h[order], r[order], t[order], dist[order]
+    return out
+
+
 def threads_used() -> int:
     return int(lib().kgco_threads_used())
 

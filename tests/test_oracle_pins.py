@@ -186,3 +186,56 @@ def test_sampled_rows_match_full_join(orc):
     rowset = set(rows.tolist())
     expect = {k for k in _keyset(full) if k[0] * 5 + k[1] in rowset}
     assert _keyset(sub) == expect
+
+
+# ------------------------------------------------- top-k (P:128 minimum-distance statistic)
+def _topk_python(E, Rel, norm, k, exclude_self):
+    """Independent brute force: pure Python loops and math.fsum (not oracle.dist_rows)."""
+    import math
+    items = []
+    for h in range(E.shape[0]):
+        for r in range(Rel.shape[0]):
+            for t in range(E.shape[0]):
+                if exclude_self and h == t:
+                    continue
+                x = [float(E[h, j]) + float(Rel[r, j]) - float(E[t, j]) for j in range(E.shape[1])]
+                d = math.fsum(abs(v) for v in x) if norm == 1 else math.sqrt(math.fsum(v * v for v in x))
+                items.append((d, h, r, t))
+    items.sort()
+    return items[:k]
+
+
+@pytest.mark.parametrize("norm", [1, 2])
+@pytest.mark.parametrize("exclude_self", [False, True])
+def test_topk_matches_python_brute_force(orc, norm, exclude_self):
+    rng = np.random.default_rng(11 + norm)
+    E = rng.standard_normal((9, 4)).astype(np.float32)
+    Rel = (0.3 * rng.standard_normal((3, 4))).astype(np.float32)
+    got = orc.topk(E, Rel, norm, 25, exclude_self=exclude_self)
+    ref = _topk_python(E, Rel, norm, 25, exclude_self)
+    assert [(int(a), int(b), int(c)) for a, b, c in zip(got["h"], got["r"], got["t"])] == [x[1:] for x in ref]
+    np.testing.assert_allclose(got["dist"], [x[0] for x in ref], rtol=1e-12, atol=1e-12)
+
+
+def test_topk_planted_translation_and_self_edges(orc):
+    """r = 0 makes every self edge a 0-distance hit; a planted exact translation t = h + r
+    (dyadic values) is the unique 0 once self edges are excluded."""
+    E = np.array([[0, 0], [1, 1], [3, 0], [0.5, 2]], np.float32)
+    Rel = np.array([[0, 0], [2, -1]], np.float32)      # E[1] + Rel[1] == E[2] exactly
+    top = orc.topk(E, Rel, 2, 6)
+    zero = {(int(h), int(r), int(t)) for h, r, t, d in zip(top["h"], top["r"], top["t"], top["dist"]) if d == 0}
+    assert zero == {(0, 0, 0), (1, 0, 1), (2, 0, 2), (3, 0, 3), (1, 1, 2)} and top["dist"][5] > 0
+    top1 = orc.topk(E, Rel, 2, 1, exclude_self=True)
+    assert (int(top1["h"][0]), int(top1["r"][0]), int(top1["t"][0])) == (1, 1, 2) and top1["dist"][0] == 0
+
+
+def test_topk_prefix_and_join_consistency(orc):
+    """top-k is a prefix of top-(k+m); the k-th distance theta_k gives join(theta_k) >= k rows."""
+    rng = np.random.default_rng(5)
+    E = rng.standard_normal((30, 6)).astype(np.float32)
+    Rel = (0.2 * rng.standard_normal((4, 6))).astype(np.float32)
+    a, b = orc.topk(E, Rel, 2, 10), orc.topk(E, Rel, 2, 40)
+    assert np.array_equal(a, b[:10])
+    assert np.all(np.diff(b["dist"]) >= 0)
+    j = orc.join(E, Rel, 2, float(b["dist"][-1]) * (1 + 1e-12))
+    assert j.size >= 40 and np.all(np.sort(j["dist"])[:40] == b["dist"])
