@@ -193,6 +193,22 @@ int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes);
 int64_t kgc_shard_range(const int64_t* cum, int64_t n, int64_t total, int32_t rank, int32_t world,
                         int64_t* begin, int64_t* end);
 
+/* The k smallest distances over all N*R*N triplets, ascending, ties ordered by
+ * (h, r, t): the paper's minimum-distance statistic min_{i,j,k} ||h_i + r_j - t_k||
+ * (PAPER.md:128 [§2, Table 1], with and without self edges h = t), SURVEY §8(f)
+ * row 4.  E, Rel, N, R, d, norm as for kgc_join; k >= 0; exclude_self 0 or 1
+ * (1 drops every triplet with h == t).  `out` (host or device memory, k records)
+ * receives min(k, available) records; the return value is that count, or a
+ * negative kgc_status.  Method: FP64 distances of up to 256 sampled (h, r) rows
+ * against every tail give an upper bound theta of the k-th smallest distance (k
+ * actual triplets lie within it); the epsilon-join at theta (every §8(a) step)
+ * returns a superset; the k-th smallest returned distance is found by bisection
+ * on the device.  Distances are K6's (FP64, rounded to float).  Afterwards
+ * kgc_results returns the epsilon-join at theta.  Needs world == 1
+ * (KGC_EINVAL otherwise). */
+int64_t kgc_topk(kgc_ctx* ctx, const float* E, const float* Rel, int64_t N, int64_t R, int32_t d, int32_t norm,
+                 int64_t k, int32_t exclude_self, kgc_triplet* out);
+
 /* ABI version compiled into the library (== KGC_ABI_VERSION). */
 int kgc_abi_version(void);
 

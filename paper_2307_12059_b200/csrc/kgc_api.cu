@@ -9,6 +9,7 @@
 //   a5/a6 K4 (L2, tcgen05) or K5 (L1 / L2 SIMT) over the work items
 //   a7/a8 K6+K7 FP64 re-check and compaction                    -> sync #2
 // Device buffers grow monotonically and are reused across joins.
+#include <cfloat>
 #include <chrono>
 #include <algorithm>
 #include <climits>
@@ -45,7 +46,8 @@ struct kgc_ctx {
     std::string err;
     DevBuf E, Rel, pivot, kt, kq, mm_t, mm_q, sk0, sv0, sk1, sv1, counts, scan_tmp, qperm, qskey, tperm, tskey, tmin,
         tmax, cmax, cmin, ranges, cost, cum, nitem, item_off, items, item_tiles, item_cum, Qp, qs, Tp, T2, tstile, cand,
-        res, ctr, est_hist, est_cost, mpP, mpkt, mpkq, mpmm_t, mpmm_q, mpc0, mpc1, tbmin, tbmax, qbmin, qbmax, tile_list;
+        res, ctr, est_hist, est_cost, mpP, mpkt, mpkq, mpmm_t, mpmm_q, mpc0, mpc1, tbmin, tbmax, qbmin, qbmax, tile_list,
+        tk_sample, tk_sel, tk_cnt;
     long long cand_cap = 0, res_cap = 0;
     long long n_results = -1;
     kgc_stats_t st{};
@@ -239,7 +241,8 @@ void kgc_destroy(kgc_ctx* ctx) {
                       &ctx->cmin,  &ctx->ranges, &ctx->cost,   &ctx->cum,   &ctx->nitem,  &ctx->item_off,
                       &ctx->items, &ctx->item_tiles, &ctx->item_cum, &ctx->Qp,     &ctx->qs,     &ctx->Tp,    &ctx->T2,     &ctx->tstile, &ctx->cand,
                       &ctx->res,   &ctx->ctr,  &ctx->est_hist, &ctx->est_cost, &ctx->mpP,   &ctx->mpkt,  &ctx->mpkq,  &ctx->mpmm_t, &ctx->mpmm_q,
-                      &ctx->mpc0,  &ctx->mpc1, &ctx->tbmin, &ctx->tbmax, &ctx->qbmin, &ctx->qbmax, &ctx->tile_list};
+                      &ctx->mpc0,  &ctx->mpc1, &ctx->tbmin, &ctx->tbmax, &ctx->qbmin, &ctx->qbmax, &ctx->tile_list,
+                      &ctx->tk_sample, &ctx->tk_sel, &ctx->tk_cnt};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& e : ctx->ev)
@@ -809,6 +812,145 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
     }
     cudaSetDevice(prev);
     return rc;
+}
+
+// ------------------------------------------------------------------ top-k
+// The k smallest dist3 over all triplets (PAPER.md:128's statistic).
+// See topk.cu for the three steps; everything but the final order of the <= k + ties
+// selected records runs on the device.
+namespace {
+// smallest float theta >= 0 with count(theta) >= k (count monotone in theta); +inf if none
+template <typename F>
+int bisect_theta(F count, long long k, float* theta) {
+    unsigned lo = 0u, hi = 0x7f7fffffu;  // float bit patterns of 0 and FLT_MAX (non-negative floats are ordered)
+    long long c = 0;
+    int rc = count(__uint_as_float_host(hi), &c);
+    if (rc != KGC_OK) return rc;
+    if (c < k) {
+        *theta = FLT_MAX;
+        return KGC_OK;
+    }
+    while (lo < hi) {
+        const unsigned mid = lo + (hi - lo) / 2;
+        rc = count(__uint_as_float_host(mid), &c);
+        if (rc != KGC_OK) return rc;
+        if (c >= k) hi = mid; else lo = mid + 1;
+    }
+    *theta = __uint_as_float_host(lo);
+    return KGC_OK;
+}
+}  // namespace
+
+extern "C" int64_t kgc_topk(kgc_ctx* ctx, const float* E, const float* Rel, int64_t N, int64_t R, int32_t d,
+                            int32_t norm, int64_t k, int32_t exclude_self, kgc_triplet* out) {
+    if (!ctx) return KGC_EINVAL;
+    ctx->n_results = -1;
+    if (k < 0 || N < 0 || R < 0 || d < 1 || d > KGC_MAX_DIM || (norm != 1 && norm != 2) ||
+        (exclude_self != 0 && exclude_self != 1) || (k > 0 && !out)) {
+        set_err(ctx, "kgc_topk: invalid arguments (k=%lld N=%lld R=%lld d=%d norm=%d)", (long long)k, (long long)N,
+                (long long)R, d, norm);
+        return KGC_EINVAL;
+    }
+    if (ctx->opt.world != 1) {
+        set_err(ctx, "kgc_topk: needs a single-shard context (world = 1)");
+        return KGC_EINVAL;
+    }
+    if (k == 0 || N == 0 || R == 0) {
+        ctx->n_results = 0;
+        return 0;
+    }
+    if (!E || !Rel) {
+        set_err(ctx, "kgc_topk: NULL E or Rel");
+        return KGC_EINVAL;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    long long result = 0;
+    auto run = [&]() -> int {
+        const float* Ed = E;
+        const float* Rd = Rel;
+        if (!is_device_ptr(E, ctx->device)) {
+            CK(ensure(ctx->E, (size_t)N * d * 4));
+            CK(cudaMemcpyAsync(ctx->E.p, E, (size_t)N * d * 4, cudaMemcpyDefault, s));
+            Ed = P<float>(ctx->E);
+        }
+        if (!is_device_ptr(Rel, ctx->device)) {
+            CK(ensure(ctx->Rel, (size_t)R * d * 4));
+            CK(cudaMemcpyAsync(ctx->Rel.p, Rel, (size_t)R * d * 4, cudaMemcpyDefault, s));
+            Rd = P<float>(ctx->Rel);
+        }
+        CK(ensure(ctx->tk_cnt, 8));
+        unsigned long long* dcnt = P<unsigned long long>(ctx->tk_cnt);
+        // 1. sampled rows against every tail -> an upper bound of the k-th smallest distance
+        const long long NR = N * R;
+        long long S = std::min<long long>(NR, 256);
+        CK(ensure(ctx->tk_sample, (size_t)S * N * 4));
+        launch_sample_dist(Ed, Rd, N, R, d, norm, (int)S, exclude_self, P<float>(ctx->tk_sample), s);
+        auto count_sample = [&](float th, long long* c) -> int {
+            unsigned long long h = 0;
+            launch_count_le(P<float>(ctx->tk_sample), S * N, th, dcnt, s);
+            CK(cudaMemcpyAsync(&h, dcnt, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            *c = (long long)h;
+            return KGC_OK;
+        };
+        float theta = 0.f;
+        int rc = bisect_theta(count_sample, k, &theta);
+        if (rc != KGC_OK) return rc;
+        // 2. the epsilon-join at theta (>= k triplets, or every triplet when theta = FLT_MAX)
+        rc = join_impl(ctx, Ed, Rd, N, R, d, norm, theta, 0, -1, -1, R);
+        if (rc != KGC_OK) return rc;
+        const long long n = ctx->n_results;
+        const KgcTripletDev* res = reinterpret_cast<const KgcTripletDev*>(ctx->res.p);
+        // 3. the k-th smallest returned distance, then the records within it, ordered on the host
+        auto count_res = [&](float th, long long* c) -> int {
+            unsigned long long h = 0;
+            launch_count_res_le(res, n, th, exclude_self, dcnt, s);
+            CK(cudaMemcpyAsync(&h, dcnt, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            *c = (long long)h;
+            return KGC_OK;
+        };
+        long long avail = 0;
+        rc = count_res(FLT_MAX, &avail);
+        if (rc != KGC_OK) return rc;
+        const long long kk = std::min<long long>(k, avail);
+        if (kk == 0) {
+            result = 0;
+            return KGC_OK;
+        }
+        float thk = 0.f;
+        rc = bisect_theta(count_res, kk, &thk);
+        if (rc != KGC_OK) return rc;
+        long long m = 0;
+        rc = count_res(thk, &m);
+        if (rc != KGC_OK) return rc;
+        CK(ensure(ctx->tk_sel, (size_t)m * 16));
+        launch_compact_res_le(res, n, thk, exclude_self, reinterpret_cast<KgcTripletDev*>(ctx->tk_sel.p), dcnt, m, s);
+        std::vector<kgc_triplet> sel((size_t)m);
+        CK(cudaMemcpyAsync(sel.data(), ctx->tk_sel.p, (size_t)m * 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::sort(sel.begin(), sel.end(), [](const kgc_triplet& a, const kgc_triplet& b) {
+            if (a.dist != b.dist) return a.dist < b.dist;
+            if (a.h != b.h) return a.h < b.h;
+            if (a.r != b.r) return a.r < b.r;
+            return a.t < b.t;
+        });
+        CK(cudaMemcpyAsync(out, sel.data(), (size_t)kk * 16, cudaMemcpyDefault, s));
+        CK(cudaStreamSynchronize(s));
+        if (!is_device_ptr(out, ctx->device)) ctx->st.d2h_bytes += kk * 16;
+        result = kk;
+        return KGC_OK;
+    };
+    const int rc = run();
+    if (rc != KGC_OK) {
+        cudaStreamSynchronize(s);
+        cudaGetLastError();
+    }
+    cudaSetDevice(prev);
+    return rc != KGC_OK ? rc : result;
 }
 
 extern "C" int64_t kgc_results(kgc_ctx* ctx, kgc_triplet* out, int64_t capacity) {

@@ -137,6 +137,14 @@ constexpr int HALF_FLUSH_PAIRS = 8;  // FP16x2 engine: flush to FP32 every 16 di
 
 // ---- verification (verify.cu) ----
 struct KgcTripletDev { int h, r, t; float dist; };
+// top-k (topk.cu)
+void launch_sample_dist(const float* E, const float* Rel, long long N, long long R, int d, int norm, int S,
+                        int exclude_self, float* out, cudaStream_t s);
+void launch_count_le(const float* a, long long n, float theta, unsigned long long* cnt, cudaStream_t s);
+void launch_count_res_le(const KgcTripletDev* res, long long n, float theta, int exclude_self,
+                         unsigned long long* cnt, cudaStream_t s);
+void launch_compact_res_le(const KgcTripletDev* res, long long n, float theta, int exclude_self, KgcTripletDev* out,
+                           unsigned long long* cnt, long long cap, cudaStream_t s);
 void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap,
                    const int* qperm, const int* tperm, const float* E, const float* Rel, long long N, int QT,
                    int bq, int d, int norm, float theta, KgcTripletDev* out, unsigned long long* res_count,

@@ -7,7 +7,7 @@ the library raises.
 
 Same names as the C ABI: kgc_default_options, kgc_create, kgc_join,
 kgc_results, kgc_stats, kgc_last_error, kgc_set_stream, kgc_destroy,
-kgc_inspect, kgc_shard_range, kgc_abi_version.  ``Join`` is a small
+kgc_inspect, kgc_shard_range, kgc_topk, kgc_abi_version.  ``Join`` is a small
 convenience wrapper around one context.
 """
 from __future__ import annotations
@@ -56,7 +56,7 @@ class kgc_stats_t(ctypes.Structure):
 
 
 EXPORTS = ["kgc_abi_version", "kgc_default_options", "kgc_create", "kgc_join", "kgc_results", "kgc_stats",
-           "kgc_last_error", "kgc_set_stream", "kgc_destroy", "kgc_inspect", "kgc_shard_range"]
+           "kgc_last_error", "kgc_set_stream", "kgc_destroy", "kgc_inspect", "kgc_shard_range", "kgc_topk"]
 
 _lib = None
 
@@ -92,6 +92,8 @@ def load_library(path: str | Path | None = None):
     L.kgc_inspect.restype = i64
     L.kgc_shard_range.argtypes = [vp, i64, i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.kgc_shard_range.restype = i64
+    L.kgc_topk.argtypes = [vp, vp, vp, i64, i64, i32, i32, i64, i32, vp]
+    L.kgc_topk.restype = i64
     if path is None:
         _lib = L
     return L
@@ -218,6 +220,19 @@ def kgc_shard_range(cum, total: int, rank: int, world: int):
     return int(b.value), int(e.value), int(cost)
 
 
+def kgc_topk(ctx, E, Rel, N: int, R: int, d: int, norm: int, k: int, exclude_self: bool = False, out=None):
+    """The k smallest distances over all triplets (see include/kgc.h); returns a
+    TRIPLET_DTYPE array (or fills `out`, host array or device tensor, and returns the count)."""
+    _check_f32(E, "E")
+    _check_f32(Rel, "Rel")
+    buf = out if out is not None else np.empty(max(int(k), 1), dtype=TRIPLET_DTYPE)
+    n = load_library().kgc_topk(ctx, _ptr(E), _ptr(Rel), int(N), int(R), int(d), int(norm), int(k),
+                                int(bool(exclude_self)), _ptr(buf))
+    if n < 0:
+        raise KgcError(int(n), kgc_last_error(ctx))
+    return int(n) if out is not None else buf[:n]
+
+
 # ----------------------------------------------------------- multi-GPU finish
 
 def gather_results(res, root: int = 0, group=None):
@@ -289,6 +304,10 @@ class Join:
 
     def stats(self) -> dict:
         return kgc_stats(self.ctx)
+
+    def topk(self, E, Rel, norm: int, k: int, exclude_self: bool = False):
+        N, d = int(E.shape[0]), int(E.shape[1])
+        return kgc_topk(self.ctx, E, Rel, N, int(Rel.shape[0]), d, norm, k, exclude_self)
 
     def inspect(self, what: str) -> np.ndarray:
         return kgc_inspect(self.ctx, what)
