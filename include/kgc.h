@@ -201,9 +201,9 @@ int64_t kgc_shard_range(const int64_t* cum, int64_t n, int64_t total, int32_t ra
  * receives min(k, available) records; the return value is that count, or a
  * negative kgc_status.  Method: FP64 distances of up to 256 sampled (h, r) rows
  * against every tail give an upper bound theta of the k-th smallest distance (k
- * actual triplets lie within it); the epsilon-join at theta (every §8(a) step)
- * returns a superset; the k-th smallest returned distance is found by bisection
- * on the device.  Distances are K6's (FP64, rounded to float).  Afterwards
+ * actual triplets lie within it); epsilon-joins (every §8(a) step) at theta *
+ * 0.9^j, j = 2, 1, 0, until one returns >= k triplets (j = 0 always does); the
+ * k-th smallest returned distance is found by bisection on the device.  Distances are K6's (FP64, rounded to float).  Afterwards
  * kgc_results returns the epsilon-join at theta.  Needs world == 1
  * (KGC_EINVAL otherwise). */
 int64_t kgc_topk(kgc_ctx* ctx, const float* E, const float* Rel, int64_t N, int64_t R, int32_t d, int32_t norm,

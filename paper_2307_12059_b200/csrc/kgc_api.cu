@@ -899,12 +899,13 @@ extern "C" int64_t kgc_topk(kgc_ctx* ctx, const float* E, const float* Rel, int6
         float theta = 0.f;
         int rc = bisect_theta(count_sample, k, &theta);
         if (rc != KGC_OK) return rc;
-        // 2. the epsilon-join at theta (>= k triplets, or every triplet when theta = FLT_MAX)
-        rc = join_impl(ctx, Ed, Rd, N, R, d, norm, theta, 0, -1, -1, R);
-        if (rc != KGC_OK) return rc;
-        const long long n = ctx->n_results;
-        const KgcTripletDev* res = reinterpret_cast<const KgcTripletDev*>(ctx->res.p);
-        // 3. the k-th smallest returned distance, then the records within it, ordered on the host
+        // 2. the epsilon-join at theta (>= k triplets, or every triplet when theta = FLT_MAX).
+        // The sample bound can be loose by orders of magnitude in result count (the closest
+        // triplets come from rare rows), so first try theta * 0.9^j, j = 2, 1 (joins at a
+        // smaller theta are cheap: fewer results, more pruning) and stop at the first with
+        // >= k usable triplets; theta itself always suffices.
+        const KgcTripletDev* res = nullptr;
+        long long n = 0;
         auto count_res = [&](float th, long long* c) -> int {
             unsigned long long h = 0;
             launch_count_res_le(res, n, th, exclude_self, dcnt, s);
@@ -913,6 +914,19 @@ extern "C" int64_t kgc_topk(kgc_ctx* ctx, const float* E, const float* Rel, int6
             *c = (long long)h;
             return KGC_OK;
         };
+        for (int j = (theta < FLT_MAX ? 2 : 0); j >= 0; --j) {
+            const float th = j ? theta * powf(0.9f, (float)j) : theta;
+            rc = join_impl(ctx, Ed, Rd, N, R, d, norm, th, 0, -1, -1, R);
+            if (rc != KGC_OK) return rc;
+            n = ctx->n_results;
+            res = reinterpret_cast<const KgcTripletDev*>(ctx->res.p);
+            if (j == 0) break;
+            long long have = 0;
+            rc = count_res(FLT_MAX, &have);
+            if (rc != KGC_OK) return rc;
+            if (have >= k) break;
+        }
+        // 3. the k-th smallest returned distance, then the records within it, ordered on the host
         long long avail = 0;
         rc = count_res(FLT_MAX, &avail);
         if (rc != KGC_OK) return rc;
