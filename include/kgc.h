@@ -193,6 +193,19 @@ int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes);
 int64_t kgc_shard_range(const int64_t* cum, int64_t n, int64_t total, int32_t rank, int32_t world,
                         int64_t* begin, int64_t* end);
 
+/* Structured Embedding (SE, PAPER.md:193 [§4.3]): every (h, r, t) with
+ * dist3 = || W_r^lhs h - W_r^rhs t ||_1 <= eps, i.e. the same join with
+ * connector_1(h, r) = W_r^lhs h, connector_2(t, r) = W_r^rhs t, dist = L1 ("SE is
+ * also transformable to a metric space").  E: N x d row-major fp32; Wl, Wr: R x d x d
+ * row-major fp32 (W_r[k][j] multiplies h_j into component k), host or device.
+ * Per relation the connectors are formed in FP64 (the re-check uses them) and
+ * rounded once to fp32 for the filters, whose threshold is widened by
+ * 2^-24 (max_h ||a_h||_1 + max_t ||b_t||_1) so the filtering stays lossless.
+ * Results (h, r, t, dist) via kgc_results, stats via kgc_stats (summed over
+ * relations).  Needs world == 1.  Errors as kgc_join. */
+int kgc_join_se(kgc_ctx* ctx, const float* E, const float* Wl, const float* Wr, int64_t N, int64_t R, int32_t d,
+                float eps);
+
 /* The k smallest distances over all N*R*N triplets, ascending, ties ordered by
  * (h, r, t): the paper's minimum-distance statistic min_{i,j,k} ||h_i + r_j - t_k||
  * (PAPER.md:128 [§2, Table 1], with and without self edges h = t), SURVEY §8(f)

@@ -138,6 +138,34 @@ def topk(E, Rel, norm: int, k: int, exclude_self: bool = False, threads: int = 0
     return out
 
 
+def se_connectors(E, Wl, Wr):
+    """SE connectors: a_{r,h} = W_r^lhs h and b_{r,t} = W_r^rhs t in FP64,
+    shape (R, N, d) each (numpy matmul of the float32 inputs promoted to float64)."""
+    E64 = np.asarray(E, np.float64)
+    A = np.einsum("rkj,nj->rnk", np.asarray(Wl, np.float64), E64)
+    B = np.einsum("rkj,nj->rnk", np.asarray(Wr, np.float64), E64)
+    return A, B
+
+
+def se_join(E, Wl, Wr, eps: float) -> np.ndarray:
+    """All (h, r, t) with ||W_r^lhs h - W_r^rhs t||_1 <= eps (SE, Definition 1
+    P:92-94), FP64, as TRIPLET_DTYPE ordered by (h, r, t).  Brute force, small inputs."""
+    A, B = se_connectors(E, Wl, Wr)
+    R, N, _ = A.shape
+    rows = []
+    for r in range(R):
+        D = np.abs(A[r][:, None, :] - B[r][None, :, :]).sum(axis=2)   # (h, t)
+        h, t = np.nonzero(D <= eps)
+        for hh, tt in zip(h, t):
+            rows.append((hh, r, tt, D[hh, tt]))
+    rows.sort()
+    out = np.zeros(len(rows), dtype=TRIPLET_DTYPE)
+    if rows:
+        arr = np.array(rows, dtype=np.float64)
+        out["h"], out["r"], out["t"], out["dist"] = arr[:, 0], arr[:, 1], arr[:, 2], arr[:, 3]
+    return out
+
+
 def threads_used() -> int:
     return int(lib().kgco_threads_used())
 

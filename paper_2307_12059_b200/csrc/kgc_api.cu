@@ -47,7 +47,7 @@ struct kgc_ctx {
     DevBuf E, Rel, pivot, kt, kq, mm_t, mm_q, sk0, sv0, sk1, sv1, counts, scan_tmp, qperm, qskey, tperm, tskey, tmin,
         tmax, cmax, cmin, ranges, cost, cum, nitem, item_off, items, item_tiles, item_cum, Qp, qs, Tp, T2, tstile, cand,
         res, ctr, est_hist, est_cost, mpP, mpkt, mpkq, mpmm_t, mpmm_q, mpc0, mpc1, tbmin, tbmax, qbmin, qbmax, tile_list,
-        tk_sample, tk_sel, tk_cnt;
+        tk_sample, tk_sel, tk_cnt, se_w, se_a64, se_b64, se_af, se_bf, se_zero, se_res, se_max;
     long long cand_cap = 0, res_cap = 0;
     long long n_results = -1;
     kgc_stats_t st{};
@@ -242,7 +242,8 @@ void kgc_destroy(kgc_ctx* ctx) {
                       &ctx->items, &ctx->item_tiles, &ctx->item_cum, &ctx->Qp,     &ctx->qs,     &ctx->Tp,    &ctx->T2,     &ctx->tstile, &ctx->cand,
                       &ctx->res,   &ctx->ctr,  &ctx->est_hist, &ctx->est_cost, &ctx->mpP,   &ctx->mpkt,  &ctx->mpkq,  &ctx->mpmm_t, &ctx->mpmm_q,
                       &ctx->mpc0,  &ctx->mpc1, &ctx->tbmin, &ctx->tbmax, &ctx->qbmin, &ctx->qbmax, &ctx->tile_list,
-                      &ctx->tk_sample, &ctx->tk_sel, &ctx->tk_cnt};
+                      &ctx->tk_sample, &ctx->tk_sel, &ctx->tk_cnt, &ctx->se_w, &ctx->se_a64, &ctx->se_b64,
+                      &ctx->se_af, &ctx->se_bf, &ctx->se_zero, &ctx->se_res, &ctx->se_max};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (auto& e : ctx->ev)
@@ -300,8 +301,18 @@ int64_t kgc_shard_range(const int64_t* cum, int64_t n, int64_t total, int32_t ra
 // sub-range starting at global relation r_off); [force_lo, force_hi): the
 // query tiles (in local numbering) this rank joins, or -1 for the
 // cost-balanced rule over all of them.
+// Optional parts of a join beyond TransE (SE, se.cu): a separate tail matrix, a wider
+// filter threshold (operands rounded on both sides), and FP64 connectors for the re-check.
+struct JoinExtra {
+    const float* Et = nullptr;    // tails (default: E)
+    float filt_eps = -1.f;        // threshold of every filter and pruning test (default: eps)
+    const double* A64 = nullptr;  // exact connectors for verify_se (default: TransE verify)
+    const double* B64 = nullptr;
+};
+
 static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long long N, long long R, int d, int norm,
-                     float eps, int r_off, long long force_lo, long long force_hi, long long R_global) {
+                     float eps, int r_off, long long force_lo, long long force_hi, long long R_global,
+                     const JoinExtra& ex = JoinExtra()) {
     cudaStream_t s = ctx->stream;
     ctx->launches = 0;
     kgc_stats_t& st = ctx->st;
@@ -363,6 +374,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         st.h2d_bytes += (int64_t)R * d * 4;
     }
     CK(cudaEventRecord(ctx->ev[EV_H2D], s));
+    const float* Et = ex.Et ? ex.Et : E;                   // tails
+    const float feps = ex.filt_eps >= 0.f ? ex.filt_eps : eps;  // filters and pruning
 
     // ---- allocations for the preprocessing
     const size_t NR = (size_t)N * R;
@@ -414,7 +427,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     st.pivots_used = K;
     if (K == 1) {
         // ---- a2: K1 keys (one pivot, FP64 -> float)
-        launch_tail_keys(E, N, d, norm, pivot, P<float>(ctx->kt), P<unsigned>(ctx->mm_t), &dctr->nonfinite, s);
+        launch_tail_keys(Et, N, d, norm, pivot, P<float>(ctx->kt), P<unsigned>(ctx->mm_t), &dctr->nonfinite, s);
         LAUNCHED(2);
         launch_query_keys(E, Rel, N, R, d, norm, pivot, P<float>(ctx->kq), P<unsigned>(ctx->mm_q), &dctr->nonfinite,
                           s);
@@ -436,7 +449,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         launch_tail_tile_bounds(P<float>(ctx->tskey), N, BN, TT, P<float>(ctx->tmin), P<float>(ctx->tmax),
                                 P<float>(ctx->cmax), P<float>(ctx->cmin), s, &ctx->launches);
         LAUNCHED(0);
-        launch_query_ranges(P<float>(ctx->qskey), N, R, QT, TT, bq, P<float>(ctx->cmax), P<float>(ctx->cmin), eps,
+        launch_query_ranges(P<float>(ctx->qskey), N, R, QT, TT, bq, P<float>(ctx->cmax), P<float>(ctx->cmin), feps,
                             ctx->opt.prune, P<int2>(ctx->ranges), P<long long>(ctx->cost), s);
         LAUNCHED(1);
     } else {
@@ -452,9 +465,9 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(ensure(ctx->tbmax, (size_t)TT * K * 4));
         CK(ensure(ctx->qbmin, (size_t)nq * K * 4));
         CK(ensure(ctx->qbmax, (size_t)nq * K * 4));
-        launch_pick_pivots(E, N, d, norm, K, pivot, P<float>(ctx->mpP), s);
+        launch_pick_pivots(Et, N, d, norm, K, pivot, P<float>(ctx->mpP), s);
         LAUNCHED(1);
-        launch_mp_keys(E, nullptr, N, 1, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkt), P<unsigned>(ctx->mpmm_t),
+        launch_mp_keys(Et, nullptr, N, 1, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkt), P<unsigned>(ctx->mpmm_t),
                        &dctr->nonfinite, s);
         LAUNCHED(2);
         launch_mp_keys(E, Rel, N, R, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q),
@@ -488,7 +501,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                         P<float>(ctx->qbmax), s);
         LAUNCHED(2);
         launch_mp_count(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tbmin), P<float>(ctx->tbmax), nq, TT,
-                        K, eps, mp_relm(d), 1, P<int2>(ctx->ranges), P<long long>(ctx->cost), s);
+                        K, feps, mp_relm(d), 1, P<int2>(ctx->ranges), P<long long>(ctx->cost), s);
         LAUNCHED(1);
     }
     scan_exclusive_i64(P<long long>(ctx->cost), P<long long>(ctx->cum), (size_t)nq, &dctr->total_cost,
@@ -522,7 +535,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         ctx->list_len = h1.c.my_cost;
         CK(ensure(ctx->tile_list, (size_t)h1.c.my_cost * 4 + 4));
         launch_mp_emit(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tbmin), P<float>(ctx->tbmax),
-                       P<long long>(ctx->cum), dctr, nq, TT, K, eps, mp_relm(d), 1, P<int>(ctx->tile_list), s);
+                       P<long long>(ctx->cum), dctr, nq, TT, K, feps, mp_relm(d), 1, P<int>(ctx->tile_list), s);
         LAUNCHED(1);
     }
     if (n_items > 0) {
@@ -559,19 +572,19 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         if (half) {
             CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * bq * Kpad * 2));
             CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * bq * 16));
-            launch_stage_half(E, nullptr, P<int>(ctx->tperm), N, d, Kpad, BN, 1, 0, TT, eps, gam, ctx->Tp.p, nullptr,
+            launch_stage_half(Et, nullptr, P<int>(ctx->tperm), N, d, Kpad, BN, 1, 0, TT, feps, gam, ctx->Tp.p, nullptr,
                               P<float>(ctx->T2), s);
-            launch_stage_half(E, Rel, P<int>(ctx->qperm), N, d, Kpad, bq, QT, tq0, tq1 - tq0, eps, gam, ctx->Qp.p,
+            launch_stage_half(E, Rel, P<int>(ctx->qperm), N, d, Kpad, bq, QT, tq0, tq1 - tq0, feps, gam, ctx->Qp.p,
                               P<float4>(ctx->qs), nullptr, s);
             LAUNCHED(2);
         } else {
-            launch_stage_tails(E, P<int>(ctx->tperm), N, d, Kpad, BN, TT, tc2 ? 2 : (tc ? 1 : 0), P<float>(ctx->Tp),
+            launch_stage_tails(Et, P<int>(ctx->tperm), N, d, Kpad, BN, TT, tc2 ? 2 : (tc ? 1 : 0), P<float>(ctx->Tp),
                                P<float>(ctx->T2), P<float2>(ctx->tstile), s);
             LAUNCHED(1);
             if (!tc) {  // the tensor-core engine forms its query tiles on the fly
                 CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * bq * Kpad * 4));
                 CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * bq * 16));
-                launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, bq, tq0, tq1, 0, norm, eps,
+                launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, bq, tq0, tq1, 0, norm, feps,
                                      P<float>(ctx->Qp), P<float4>(ctx->qs), s);
                 LAUNCHED(1);
             }
@@ -612,7 +625,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.bn = BN;
         tp.tq0 = tq0;
         tp.N = (int)N;
-        tp.theta = eps;
+        tp.theta = feps;
         tp.gam = gam;
         tp.Rt = P<float>(ctx->T2);
         tp.eta = (float)((Kpad / 8) * 3.814697265625e-06);  // Ksteps * 2^-18
@@ -633,9 +646,15 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         }
         CK(cudaEventRecord(ctx->ev[EV_TILES], s));
         if (n_items > 0) {
-            launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, P<int>(ctx->qperm), P<int>(ctx->tperm), E,
-                          Rel, N, QT, bq, d, norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p), &dctr->res,
-                          ctx->res_cap, ctx->num_sms, s, r_off);
+            if (ex.A64)
+                launch_verify_se(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, P<int>(ctx->qperm),
+                                 P<int>(ctx->tperm), ex.A64, ex.B64, N, (long long)QT * bq, d, eps,
+                                 reinterpret_cast<KgcTripletDev*>(ctx->res.p), &dctr->res, ctx->res_cap,
+                                 ctx->num_sms, s, r_off);
+            else
+                launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, P<int>(ctx->qperm), P<int>(ctx->tperm),
+                              E, Rel, N, QT, bq, d, norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p),
+                              &dctr->res, ctx->res_cap, ctx->num_sms, s, r_off);
             LAUNCHED(1);
         }
         CK(cudaEventRecord(ctx->ev[EV_VERIFY], s));
@@ -808,6 +827,166 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
     } else {
         ctx->st.ms_split = 0.f;
         if (did_split) cudaEventElapsedTime(&ctx->st.ms_split, ctx->ev_split[0], ctx->ev_split[1]);
+        ctx->st.ms_host = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+    }
+    cudaSetDevice(prev);
+    return rc;
+}
+
+// ------------------------------------------------------------------ SE
+// Structured Embedding: per relation, the FP64 connectors (se.cu), then the
+// L1 join of fl32(W_lhs h) against fl32(W_rhs t) with the filters widened by the rounding of
+// both sides, re-checked from the FP64 connectors; results appended across relations.
+extern "C" int kgc_join_se(kgc_ctx* ctx, const float* E, const float* Wl, const float* Wr, int64_t N, int64_t R,
+                           int32_t d, float eps) {
+    if (!ctx) return KGC_EINVAL;
+    ctx->n_results = -1;
+    ctx->have_join = false;
+    if (N < 0 || R < 0 || d < 1 || d > KGC_MAX_DIM || !(eps >= 0.f) || !std::isfinite(eps)) {
+        set_err(ctx, "kgc_join_se: invalid argument (N=%lld R=%lld d=%d eps=%g)", (long long)N, (long long)R, d,
+                (double)eps);
+        return KGC_EINVAL;
+    }
+    if (ctx->opt.world != 1) {
+        set_err(ctx, "kgc_join_se: needs a single-shard context (world = 1)");
+        return KGC_EINVAL;
+    }
+    if (N == 0 || R == 0) {
+        memset(&ctx->st, 0, sizeof ctx->st);
+        ctx->st.N = N;
+        ctx->st.R = R;
+        ctx->st.d = d;
+        ctx->st.norm = 1;
+        ctx->st.eps = eps;
+        ctx->st.world = 1;
+        ctx->n_results = 0;
+        ctx->have_join = true;
+        return KGC_OK;
+    }
+    if (!E || !Wl || !Wr) {
+        set_err(ctx, "kgc_join_se: NULL E, W_lhs or W_rhs");
+        return KGC_EINVAL;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const auto host_t0 = std::chrono::steady_clock::now();
+    long long total = 0;
+    int64_t h2d = 0;
+    auto run = [&]() -> int {
+        const float* Ed = E;
+        if (!is_device_ptr(E, ctx->device)) {
+            CK(ensure(ctx->E, (size_t)N * d * 4));
+            CK(cudaMemcpyAsync(ctx->E.p, E, (size_t)N * d * 4, cudaMemcpyDefault, s));
+            Ed = P<float>(ctx->E);
+            h2d += N * d * 4;
+        }
+        const size_t wsz = (size_t)R * d * d;
+        const float* Wld = Wl;
+        const float* Wrd = Wr;
+        if (!is_device_ptr(Wl, ctx->device) || !is_device_ptr(Wr, ctx->device)) {
+            CK(ensure(ctx->se_w, wsz * 2 * 4));
+            CK(cudaMemcpyAsync(ctx->se_w.p, Wl, wsz * 4, cudaMemcpyDefault, s));
+            CK(cudaMemcpyAsync(P<float>(ctx->se_w) + wsz, Wr, wsz * 4, cudaMemcpyDefault, s));
+            Wld = P<float>(ctx->se_w);
+            Wrd = P<float>(ctx->se_w) + wsz;
+            h2d += (int64_t)wsz * 8;
+        }
+        CK(ensure(ctx->se_a64, (size_t)N * d * 8));
+        CK(ensure(ctx->se_b64, (size_t)N * d * 8));
+        CK(ensure(ctx->se_af, (size_t)N * d * 4));
+        CK(ensure(ctx->se_bf, (size_t)N * d * 4));
+        CK(ensure(ctx->se_zero, (size_t)d * 4));
+        CK(ensure(ctx->se_max, 8));
+        CK(cudaMemsetAsync(ctx->se_zero.p, 0, (size_t)d * 4, s));
+        size_t se_cap = 0;
+        kgc_stats_t acc{};
+        for (long long r = 0; r < R; ++r) {
+            unsigned int mx[2] = {0, 0};
+            launch_se_connectors(Ed, Wld + (size_t)r * d * d, Wrd + (size_t)r * d * d, N, d, P<double>(ctx->se_a64),
+                                 P<double>(ctx->se_b64), P<float>(ctx->se_af), P<float>(ctx->se_bf),
+                                 P<unsigned>(ctx->se_max), P<unsigned>(ctx->se_max) + 1, s);
+            CK(cudaMemcpyAsync(mx, ctx->se_max.p, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            // |dist(fl a, fl b) - dist(a, b)| <= ||fl a - a||_1 + ||fl b - b||_1 <= 2^-24 (max||a||_1 + max||b||_1)
+            const double widen = 5.9604644775390625e-08 * ((double)__uint_as_float_host(mx[0]) +
+                                                           (double)__uint_as_float_host(mx[1])) * (1.0 + 1e-6);
+            const float feps = nextafterf((float)((double)eps + widen), FLT_MAX);
+            if (!std::isfinite(feps)) {
+                set_err(ctx, "kgc_join_se: connector values overflow float");
+                return KGC_EDATA;
+            }
+            JoinExtra ex;
+            ex.Et = P<float>(ctx->se_bf);
+            ex.filt_eps = feps;
+            ex.A64 = P<double>(ctx->se_a64);
+            ex.B64 = P<double>(ctx->se_b64);
+            const int rc = join_impl(ctx, P<float>(ctx->se_af), P<float>(ctx->se_zero), N, 1, d, 1, eps, (int)r, -1, -1,
+                                     1, ex);
+            if (rc != KGC_OK) return rc;
+            const long long n = ctx->n_results;
+            if (n > 0) {
+                if ((size_t)(total + n) > se_cap) {
+                    const size_t ncap = std::max<size_t>((size_t)(total + n) * 3 / 2, 1 << 16);
+                    DevBuf nb;
+                    CK(ensure(nb, ncap * 16));
+                    if (total) CK(cudaMemcpyAsync(nb.p, ctx->se_res.p, (size_t)total * 16, cudaMemcpyDeviceToDevice, s));
+                    CK(cudaStreamSynchronize(s));
+                    if (ctx->se_res.p) cudaFree(ctx->se_res.p);
+                    ctx->se_res = nb;
+                    se_cap = ncap;
+                }
+                CK(cudaMemcpyAsync(P<char>(ctx->se_res) + (size_t)total * 16, ctx->res.p, (size_t)n * 16,
+                                   cudaMemcpyDeviceToDevice, s));
+            }
+            total += n;
+            const kgc_stats_t& st = ctx->st;
+            acc.tile_pairs_total += st.tile_pairs_total;
+            acc.tile_pairs_surviving += st.tile_pairs_surviving;
+            acc.tile_pairs_mine += st.tile_pairs_mine;
+            acc.work_items_mine += st.work_items_mine;
+            acc.candidates += st.candidates;
+            acc.launches += st.launches + 5;
+            acc.reruns += st.reruns;
+            acc.ms_keys += st.ms_keys;
+            acc.ms_sort += st.ms_sort;
+            acc.ms_ranges += st.ms_ranges;
+            acc.ms_stage += st.ms_stage;
+            acc.ms_tiles += st.ms_tiles;
+            acc.ms_recheck += st.ms_recheck;
+            acc.ms_total += st.ms_total;
+            acc.query_tile_rows = st.query_tile_rows;
+            acc.tail_tile_rows = st.tail_tile_rows;
+            acc.query_tiles = st.query_tiles * R;
+            acc.tail_tiles = st.tail_tiles * R;
+            acc.pivots_used = st.pivots_used;
+            acc.engine = st.engine;
+        }
+        CK(cudaStreamSynchronize(s));
+        std::swap(ctx->res, ctx->se_res);  // the accumulated results become the context's results
+        ctx->res_cap = (long long)(ctx->res.n / 16);
+        acc.N = N;
+        acc.R = R;
+        acc.d = d;
+        acc.norm = 1;
+        acc.eps = eps;
+        acc.rank = 0;
+        acc.world = 1;
+        acc.triplets = (double)N * (double)N * (double)R;
+        acc.results = total;
+        acc.h2d_bytes = h2d;
+        ctx->st = acc;
+        return KGC_OK;
+    };
+    const int rc = run();
+    if (rc != KGC_OK) {
+        cudaStreamSynchronize(s);
+        cudaGetLastError();
+        ctx->n_results = -1;
+    } else {
+        ctx->n_results = total;
+        ctx->have_join = true;
         ctx->st.ms_host = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
     }
     cudaSetDevice(prev);

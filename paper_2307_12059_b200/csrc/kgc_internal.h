@@ -137,6 +137,13 @@ constexpr int HALF_FLUSH_PAIRS = 8;  // FP16x2 engine: flush to FP32 every 16 di
 
 // ---- verification (verify.cu) ----
 struct KgcTripletDev { int h, r, t; float dist; };
+// SE (se.cu)
+void launch_se_connectors(const float* E, const float* Wl, const float* Wr, long long N, int d, double* A64,
+                          double* B64, float* Af, float* Bf, unsigned int* maxa, unsigned int* maxb, cudaStream_t s);
+void launch_verify_se(const int2* cand, const unsigned long long* cand_count, long long cand_cap, const int* qperm,
+                      const int* tperm, const double* A64, const double* B64, long long N, long long rows, int d,
+                      float theta, KgcTripletDev* out, unsigned long long* res_count, long long res_cap, int num_sms,
+                      cudaStream_t s, int r);
 // top-k (topk.cu)
 void launch_sample_dist(const float* E, const float* Rel, long long N, long long R, int d, int norm, int S,
                         int exclude_self, float* out, cudaStream_t s);

@@ -7,7 +7,7 @@ the library raises.
 
 Same names as the C ABI: kgc_default_options, kgc_create, kgc_join,
 kgc_results, kgc_stats, kgc_last_error, kgc_set_stream, kgc_destroy,
-kgc_inspect, kgc_shard_range, kgc_topk, kgc_abi_version.  ``Join`` is a small
+kgc_inspect, kgc_shard_range, kgc_topk, kgc_join_se, kgc_abi_version.  ``Join`` is a small
 convenience wrapper around one context.
 """
 from __future__ import annotations
@@ -56,7 +56,8 @@ class kgc_stats_t(ctypes.Structure):
 
 
 EXPORTS = ["kgc_abi_version", "kgc_default_options", "kgc_create", "kgc_join", "kgc_results", "kgc_stats",
-           "kgc_last_error", "kgc_set_stream", "kgc_destroy", "kgc_inspect", "kgc_shard_range", "kgc_topk"]
+           "kgc_last_error", "kgc_set_stream", "kgc_destroy", "kgc_inspect", "kgc_shard_range", "kgc_topk",
+           "kgc_join_se"]
 
 _lib = None
 
@@ -94,6 +95,8 @@ def load_library(path: str | Path | None = None):
     L.kgc_shard_range.restype = i64
     L.kgc_topk.argtypes = [vp, vp, vp, i64, i64, i32, i32, i64, i32, vp]
     L.kgc_topk.restype = i64
+    L.kgc_join_se.argtypes = [vp, vp, vp, vp, i64, i64, i32, ctypes.c_float]
+    L.kgc_join_se.restype = ctypes.c_int
     if path is None:
         _lib = L
     return L
@@ -233,6 +236,15 @@ def kgc_topk(ctx, E, Rel, N: int, R: int, d: int, norm: int, k: int, exclude_sel
     return int(n) if out is not None else buf[:n]
 
 
+def kgc_join_se(ctx, E, Wl, Wr, N: int, R: int, d: int, eps: float) -> None:
+    """Structured Embedding join (see include/kgc.h); results via kgc_results."""
+    for x, n in ((E, "E"), (Wl, "Wl"), (Wr, "Wr")):
+        _check_f32(x, n)
+    rc = load_library().kgc_join_se(ctx, _ptr(E), _ptr(Wl), _ptr(Wr), int(N), int(R), int(d), float(eps))
+    if rc != KGC_OK:
+        raise KgcError(rc, kgc_last_error(ctx))
+
+
 # ----------------------------------------------------------- multi-GPU finish
 
 def gather_results(res, root: int = 0, group=None):
@@ -304,6 +316,11 @@ class Join:
 
     def stats(self) -> dict:
         return kgc_stats(self.ctx)
+
+    def run_se(self, E, Wl, Wr, eps: float) -> int:
+        N, d = int(E.shape[0]), int(E.shape[1])
+        kgc_join_se(self.ctx, E, Wl, Wr, N, int(Wl.shape[0]), d, eps)
+        return kgc_results(self.ctx)
 
     def topk(self, E, Rel, norm: int, k: int, exclude_self: bool = False):
         N, d = int(E.shape[0]), int(E.shape[1])

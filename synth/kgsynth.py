@@ -77,6 +77,18 @@ def generate(N: int, R: int, d: int, seed: int, dist: str = "cluster"):
             np.ascontiguousarray(Rel, dtype=np.float32))
 
 
+def generate_se(N: int, R: int, d: int, seed: int, dist: str = "cluster"):
+    """SE-shaped inputs (PAPER.md:193, Structured Embedding): entities as ``generate``;
+    per relation two d x d matrices W = I + 0.1 / sqrt(d) * N(0, 1) (lhs, rhs), so
+    W_lhs h and W_rhs t stay close for nearby entities.  Random draws only."""
+    E, _ = generate(N, R, d, seed, dist)
+    rng = np.random.default_rng(seed + 7919)
+    eye = np.eye(d)
+    Wl = (eye + 0.1 / math.sqrt(d) * rng.standard_normal((R, d, d))).astype(np.float32)
+    Wr = (eye + 0.1 / math.sqrt(d) * rng.standard_normal((R, d, d))).astype(np.float32)
+    return E, Wl, Wr
+
+
 def generate_config(name: str, dist: str | None = None):
     c = CONFIGS[name]
     return generate(c.N, c.R, c.d, c.seed, dist or c.dist)

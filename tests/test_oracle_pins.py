@@ -239,3 +239,47 @@ def test_topk_prefix_and_join_consistency(orc):
     assert np.all(np.diff(b["dist"]) >= 0)
     j = orc.join(E, Rel, 2, float(b["dist"][-1]) * (1 + 1e-12))
     assert j.size >= 40 and np.all(np.sort(j["dist"])[:40] == b["dist"])
+
+
+# ------------------------------------------------- SE (Structured Embedding)
+def test_se_identity_matrices_reduce_to_entity_l1(orc):
+    """W_lhs = W_rhs = I: dist3 = ||h - t||_1 (scipy cityblock, an independent library)."""
+    from scipy.spatial.distance import cdist
+    rng = np.random.default_rng(2)
+    E = rng.standard_normal((40, 7)).astype(np.float32)
+    W = np.stack([np.eye(7, dtype=np.float32)] * 2)
+    D = cdist(E.astype(np.float64), E.astype(np.float64), "cityblock")
+    eps = float(np.sort(D.ravel())[300])
+    got = orc.se_join(E, W, W, eps)
+    h, t = np.nonzero(D <= eps)
+    assert got.size == 2 * h.size
+    assert set(zip(got["h"].tolist(), got["t"].tolist())) == set(zip(h.tolist(), t.tolist()))
+    np.testing.assert_allclose(got["dist"], D[got["h"], got["t"]], rtol=1e-12, atol=1e-12)
+
+
+def test_se_matches_python_brute_force(orc):
+    import math
+    rng = np.random.default_rng(4)
+    E = rng.standard_normal((8, 3)).astype(np.float32)
+    Wl = rng.standard_normal((2, 3, 3)).astype(np.float32)
+    Wr = rng.standard_normal((2, 3, 3)).astype(np.float32)
+    ref = []
+    for h in range(8):
+        for r in range(2):
+            a = [math.fsum(float(Wl[r, k, j]) * float(E[h, j]) for j in range(3)) for k in range(3)]
+            for t in range(8):
+                b = [math.fsum(float(Wr[r, k, j]) * float(E[t, j]) for j in range(3)) for k in range(3)]
+                ref.append((math.fsum(abs(x - y) for x, y in zip(a, b)), h, r, t))
+    eps = sorted(x[0] for x in ref)[40]
+    got = orc.se_join(E, Wl, Wr, eps)
+    want = sorted((h, r, t) for d, h, r, t in ref if d <= eps)
+    assert [(int(a), int(b), int(c)) for a, b, c in zip(got["h"], got["r"], got["t"])] == want
+
+
+def test_se_planted_exact_match(orc):
+    """W_lhs = 2I, W_rhs = I and E_t = 2 E_h exactly (dyadic) -> distance 0."""
+    E = np.array([[0.5, 1.0], [1.0, 2.0], [3.0, -1.0]], np.float32)
+    Wl = np.array([2 * np.eye(2)], np.float32)
+    Wr = np.array([np.eye(2)], np.float32)
+    got = orc.se_join(E, Wl, Wr, 0.0)
+    assert {(int(h), int(t)) for h, t in zip(got["h"], got["t"])} == {(0, 1)} and got["dist"][0] == 0
