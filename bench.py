@@ -278,6 +278,8 @@ def run_ours(args, cfg, thresholds):
         st = stats_last[n]
         t_tiles = statistics.mean(phase[n]["ms_tiles"]) / 1e3
         pairs = st["tile_pairs_mine"] * st["query_tile_rows"] * st["tail_tile_rows"]
+        if st["engine"] == 5:   # gathered tails: the pairs left after the per-tail pivot test (padding excluded)
+            pairs = st["gathered_pairs"]
         flops = 2.0 * d * pairs
         if n == 2:
             tc = st["tail_tile_rows"] == 256
@@ -292,15 +294,18 @@ def run_ours(args, cfg, thresholds):
                                           "1.1/2.25") if tc else "148 SM x 128 FP32 lanes x FFMA(2 flop) x clock"})
         else:
             peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-            kernels.append({"kernel": "tiles_simt_kernel<1> (L1)", "bound": "alu", "ms": t_tiles * 1e3,
+            kname = "tiles_gather_kernel<1> (L1, gathered tails)" if st["engine"] == 5 else "tiles_simt_kernel<1> (L1)"
+            kernels.append({"kernel": kname, "bound": "alu", "ms": t_tiles * 1e3,
                             "achieved": flops / t_tiles / 1e12, "peak": peak, "unit": "TFLOP/s",
                             "peak_note": "148 SM x 128 FP32 lanes x 1 FADD/clk x sm_max_mhz (|q-t| = 2 FADD = 2 flop)"})
         if n == 1:
             # the L1 path's HBM use (BASELINE north_star asks for it): ncu dram bytes of the tile kernel /
             # its event time; operand bytes the bulk copies move (L2 -> SM) per the same time
             k1 = kernels[-1]
-            dram = ncu_traffic("tiles_simt_kernel<1>", args.config)
-            opb = st["tile_pairs_mine"] * (st["query_tile_rows"] + st["tail_tile_rows"]) * ((d + 7) // 8 * 8) * 4
+            dram = ncu_traffic(k1["kernel"].split()[0], args.config)
+            # operand bytes per computed pair: (query rows + tail rows) x Kpad x 4 per 64 x 64 block
+            opb = pairs * (st["query_tile_rows"] + st["tail_tile_rows"]) * ((d + 7) // 8 * 8) * 4 / \
+                (st["query_tile_rows"] * st["tail_tile_rows"])
             k1["hbm_gbs"] = dram / t_tiles / 1e9 if dram else None
             k1["hbm_frac"] = (dram / t_tiles / 1e9) / peaks["hbm_gbs"] if dram else None
             k1["operand_gbs_l2_to_sm"] = opb / t_tiles / 1e9
@@ -400,7 +405,7 @@ def run_ours(args, cfg, thresholds):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32",
             "dtype_detail": "L2 filter tcgen05 kind::tf32 (FP32 accumulate) + rigorous guard band; L1 filter FP32 "
-                            "SIMT; every emitted triplet re-checked in FP64",
+                            "SIMT on gathered tails; every emitted triplet re-checked in FP64",
             "data": "synthetic",
             "config": {"workload": wl, "N": N, "R": R, "d": d, "norms": args.norms, "eps": eps, "hit_rate": args.hit,
                        "parallelism": f"query-tile shards x{world}, tails replicated",
@@ -415,6 +420,8 @@ def run_ours(args, cfg, thresholds):
             "surviving_pair_fraction_tiles": {f"L{n}": stats_last[n]["tile_pairs_surviving"] *
                                               stats_last[n]["query_tile_rows"] * stats_last[n]["tail_tile_rows"] /
                                               max(1.0, float(N) * N * R) for n in args.norms},
+            "surviving_pair_fraction_gathered": {f"L{n}": stats_last[n]["gathered_pairs"] / max(1.0, float(N) * N * R)
+                                                 for n in args.norms if stats_last[n]["engine"] == 5},
             "surviving_pair_fraction_elements_sampled": elem,
             "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "wall_s_timed_region": wall,

@@ -83,8 +83,12 @@ typedef struct {
                               /* prune = 1; otherwise one pivot is used)                           */
     int64_t result_capacity;  /* initial result-buffer capacity in triplets; 0 = auto (grows)       */
     void*   stream;           /* cudaStream_t to run on; NULL = a stream the context creates       */
-    int32_t l1_engine;        /* 0 = auto (= 2); 1 = FP16x2 SIMT filter with rigorous band (used   */
-                              /* only when every |E|, |Rel| value <= 1000, else 2); 2 = FP32 SIMT   */
+    int32_t l1_engine;        /* 0 = auto (3 with multi-pivot pruning, else 2); 1 = FP16x2 SIMT    */
+                              /* filter with rigorous band (only when every |E|, |Rel| <= 1000);    */
+                              /* 2 = FP32 SIMT on 64 x 64 tiles; 3 = FP32 SIMT on gathered tails:   */
+                              /* inside each surviving tile pair only the tails whose own K pivot   */
+                              /* keys pass the test against the query tile's box (needs pivots >= 2; */
+                              /* also used for the L2 SIMT engine when set explicitly)              */
     int32_t split;            /* world > 1: 0 = rank-local (default: rank k takes query tiles       */
                               /* [k nq/W, (k+1) nq/W) and preprocesses only the relations they      */
                               /* touch; tails are replicated); 1 = global cost-balanced split (every */
@@ -115,9 +119,11 @@ typedef struct {
     float ms_total, ms_h2d, ms_keys, ms_sort, ms_ranges, ms_stage, ms_tiles, ms_recheck;
     int32_t pivots_used;          /* 1, or K of the multi-pivot pruning                            */
     int32_t engine;               /* tile engine used: 1 tcgen05 TF32, 2 FP32 SIMT, 3 FP16x2 SIMT,   */
-                                  /* 4 tcgen05 TF32 on CTA pairs                                      */
+                                  /* 4 tcgen05 TF32 on CTA pairs, 5 FP32 SIMT on gathered tails       */
     float ms_split;               /* device time of the rank-local split estimate (world > 1)       */
     float ms_host;                /* host wall time of the whole kgc_join call                      */
+    int64_t gathered_pairs;       /* engine 5: (query row, tail) pairs left after the per-tail K-pivot */
+                                  /* test inside surviving tiles (sentinel padding excluded)          */
 } kgc_stats_t;
 
 /* Fill *opt with defaults: device -1, rank 0, world 1, prune 1, pivot 0,
@@ -170,6 +176,11 @@ void kgc_destroy(kgc_ctx* ctx);
  *   KGC_INSPECT_QUERY_COST  int64[R*QT]  exclusive prefix of surviving tiles per query tile (K3)
  *   KGC_INSPECT_TILE_LIST   int32[mine]  multi-pivot: this shard's surviving tail tiles, query tile by
  *                                        query tile (offset of tile q = cost prefix[q] - prefix[first])
+ *   KGC_INSPECT_GATHER_LIST int32[64*mine] engine 5: per query tile q of this shard, its surviving sorted
+ *                                        tail positions in ascending order, padded with N to whole blocks
+ *                                        of 64, at offset 64 * (cost prefix[q] - prefix[first]) (the
+ *                                        tile list's offsets; entries past q's blocks are unused)
+ *   KGC_INSPECT_GATHER_COST int64[R*QT]  engine 5: 64-tail blocks per query tile (0 outside this shard)
  * With multi-pivot pruning (pivots_used = K > 1) the key arrays hold K floats
  * per row: TAIL_KEYS float[N][K], QUERY_KEYS float[R][N][K]. */
 enum {
@@ -179,7 +190,9 @@ enum {
     KGC_INSPECT_QUERY_PERM = 4,
     KGC_INSPECT_TILE_RANGES = 5,
     KGC_INSPECT_QUERY_COST = 6,
-    KGC_INSPECT_TILE_LIST = 7
+    KGC_INSPECT_TILE_LIST = 7,
+    KGC_INSPECT_GATHER_LIST = 8,
+    KGC_INSPECT_GATHER_COST = 9
 };
 int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes);
 

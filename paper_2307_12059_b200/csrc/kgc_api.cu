@@ -47,7 +47,7 @@ struct kgc_ctx {
     DevBuf E, Rel, pivot, kt, kq, mm_t, mm_q, sk0, sv0, sk1, sv1, counts, scan_tmp, qperm, qskey, tperm, tskey, tmin,
         tmax, cmax, cmin, ranges, cost, cum, nitem, item_off, items, item_tiles, item_cum, Qp, qs, Tp, T2, tstile, cand,
         res, ctr, est_hist, est_cost, mpP, mpkt, mpkq, mpmm_t, mpmm_q, mpc0, mpc1, tbmin, tbmax, qbmin, qbmax, tile_list,
-        tk_sample, tk_sel, tk_cnt, se_w, se_a64, se_b64, se_af, se_bf, se_zero, se_res, se_max;
+        tk_sample, tk_sel, tk_cnt, Ts, tks, gblk, granges, glist, se_w, se_a64, se_b64, se_af, se_bf, se_zero, se_res, se_max;
     long long cand_cap = 0, res_cap = 0;
     long long n_results = -1;
     kgc_stats_t st{};
@@ -59,6 +59,7 @@ struct kgc_ctx {
     int QT = 0, TT = 0, BN = 0;
     int K = 1;                  // pivots used by the last join
     long long list_len = 0;     // multi-pivot tile-list length of this shard
+    long long glist_len = 0;    // gathered-tail list length of this shard (entries)
     bool have_join = false;
 };
 
@@ -130,6 +131,14 @@ static int simt_t() {
     const char* e = getenv("KGC_SIMT_T");
     return (e && atoi(e) == 32) ? 32 : SIMT_T;
 }
+// Gathered-tail SIMT engine (l1_engine 3; auto for L1 with multi-pivot pruning):
+// element-level tail pruning inside surviving tiles (pivots.cu, tiles_simt.cu).
+static bool use_gather(const kgc_ctx* ctx, int norm) {
+    const char* e = getenv("KGC_GATHER");  // experiment knob: 0 = off, 1 = on for both norms
+    if (e) return atoi(e) != 0;
+    if (ctx->opt.l1_engine == 3) return true;
+    return norm == 1 && ctx->opt.l1_engine == 0;
+}
 static int plan_bq(const kgc_ctx* ctx, int norm, int d, long long N) {
     if (use_tc2(ctx, norm, d, N)) return 2 * BM;
     if (use_tc(ctx, norm, d)) return BM;
@@ -182,7 +191,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 3 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 2 || o.split < 0 || o.split > 1) {
+        o.l2_engine > 3 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 1) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -531,6 +540,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const int tq0 = h1.c.tq_begin == INT_MAX ? 0 : h1.c.tq_begin;
     const int tq1 = h1.c.tq_begin == INT_MAX ? 0 : h1.c.tq_end;
     ctx->list_len = 0;
+    ctx->glist_len = 0;
     if (n_items > 0 && K > 1) {
         ctx->list_len = h1.c.my_cost;
         CK(ensure(ctx->tile_list, (size_t)h1.c.my_cost * 4 + 4));
@@ -538,7 +548,43 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                        P<long long>(ctx->cum), dctr, nq, TT, K, feps, mp_relm(d), 1, P<int>(ctx->tile_list), s);
         LAUNCHED(1);
     }
-    if (n_items > 0) {
+    // Gathered tails: per query tile, the tails of its surviving tiles that pass the K-pivot
+    // test on their own keys, in blocks of GT_ROWS; work items reference blocks.
+    const bool gather = n_items > 0 && K > 1 && !tc && !half_req && simt_t() == GT_ROWS && use_gather(ctx, norm);
+    long long g_max_items = 0;
+    if (gather) {
+        g_max_items = h1.c.my_cost;  // blocks (and items) <= surviving tiles of this shard
+        CK(ensure(ctx->Ts, (size_t)(N + 1) * Kpad * 4));
+        CK(ensure(ctx->tks, (size_t)N * MP_MAX * 4));
+        CK(ensure(ctx->gblk, (size_t)nq * 8));
+        CK(ensure(ctx->granges, (size_t)nq * 8));
+        CK(ensure(ctx->glist, (size_t)g_max_items * GT_ROWS * 4 + 4));
+        CK(ensure(ctx->items, (size_t)g_max_items * 16));
+        CK(ensure(ctx->item_tiles, (size_t)g_max_items * 8));
+        CK(ensure(ctx->item_cum, (size_t)g_max_items * 8));
+        CK(ensure(ctx->scan_tmp, scan_tmp_bytes((size_t)std::max<long long>(g_max_items, nq))));
+        launch_stage_rows(Et, P<int>(ctx->tperm), P<float>(ctx->mpkt), N, d, Kpad, K, P<float>(ctx->Ts),
+                          P<float>(ctx->tks), s);
+        CK(cudaMemsetAsync(ctx->gblk.p, 0, (size_t)nq * 8, s));
+        CK(cudaMemsetAsync(ctx->nitem.p, 0, (size_t)nq * 4, s));
+        CK(cudaMemsetAsync(ctx->item_tiles.p, 0, (size_t)g_max_items * 8, s));
+        launch_gather_tails(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tks), P<int>(ctx->tile_list),
+                            P<long long>(ctx->cum), P<int2>(ctx->ranges), dctr, N, K, feps, mp_relm(d), chunk, nq,
+                            P<long long>(ctx->gblk), P<int2>(ctx->granges), P<int>(ctx->nitem), P<int>(ctx->glist), s);
+        LAUNCHED(2);
+        scan_exclusive_i32(P<int>(ctx->nitem), P<int>(ctx->item_off), (size_t)nq, ctx->scan_tmp.p, s,
+                           &ctx->launches);
+        LAUNCHED(0);
+        // items {q, b0, b1, tile-list offset of q}: block b of q is glist[GT_ROWS * (offset + b) ...]
+        launch_shard_items(P<int2>(ctx->granges), nullptr, P<long long>(ctx->cum), nq, ctx->opt.rank,
+                           ctx->opt.world, chunk, dctr, P<int>(ctx->nitem), P<int>(ctx->item_off),
+                           P<int4>(ctx->items), P<long long>(ctx->item_tiles), ctx->scan_tmp.p, s, &ctx->launches, 1,
+                           1, force_lo, force_hi);
+        LAUNCHED(0);
+        scan_exclusive_i64(P<long long>(ctx->item_tiles), P<long long>(ctx->item_cum), (size_t)g_max_items, nullptr,
+                           ctx->scan_tmp.p, s, &ctx->launches);
+        LAUNCHED(0);
+    } else if (n_items > 0) {
         CK(ensure(ctx->items, (size_t)n_items * 16));
         CK(ensure(ctx->item_tiles, (size_t)n_items * 8));
         CK(ensure(ctx->item_cum, (size_t)n_items * 8));
@@ -563,7 +609,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         set_err(ctx, "l1_engine=1 (FP16x2) needs every |E|, |Rel| value <= 1000; use l1_engine 0 or 2");
         return KGC_EINVAL;
     }
-    st.engine = tc2 ? 4 : (tc ? 1 : (half ? 3 : 2));
+    st.engine = tc2 ? 4 : (tc ? 1 : (half ? 3 : (gather ? 5 : 2)));
     const float gam = 1.0f + 10.0f * 4.8828125e-04f + (float)(d / 8 + 4) * 1.1920928955078125e-07f;
     if (n_items > 0) {
         CK(ensure(ctx->Tp, (size_t)TT * BN * Kpad * 4));
@@ -577,6 +623,12 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             launch_stage_half(E, Rel, P<int>(ctx->qperm), N, d, Kpad, bq, QT, tq0, tq1 - tq0, feps, gam, ctx->Qp.p,
                               P<float4>(ctx->qs), nullptr, s);
             LAUNCHED(2);
+        } else if (gather) {
+            CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * bq * Kpad * 4));
+            CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * bq * 16));
+            launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, bq, tq0, tq1, 0, norm, feps,
+                                 P<float>(ctx->Qp), P<float4>(ctx->qs), s);
+            LAUNCHED(1);
         } else {
             launch_stage_tails(Et, P<int>(ctx->tperm), N, d, Kpad, BN, TT, tc2 ? 2 : (tc ? 1 : 0), P<float>(ctx->Tp),
                                P<float>(ctx->T2), P<float2>(ctx->tstile), s);
@@ -637,8 +689,13 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.qperm = P<int>(ctx->qperm);
         tp.d = d;
         tp.QT = QT;
+        tp.Ts = P<float>(ctx->Ts);
+        tp.glist = P<int>(ctx->glist);
+        tp.dn_items = &dctr->n_items;
+        tp.dtotal = &dctr->gblocks;
         if (n_items > 0) {
-            if (tc2) launch_tiles_tc2(tp, ctx->num_sms, s);
+            if (gather) launch_tiles_gather(tp, norm, ctx->num_sms, g_max_items, s);
+            else if (tc2) launch_tiles_tc2(tp, ctx->num_sms, s);
             else if (tc) launch_tiles_tc(tp, ctx->num_sms, s);
             else if (half) launch_tiles_half_l1(tp, ctx->num_sms, s);
             else launch_tiles_simt(tp, norm, ctx->num_sms, s);
@@ -658,11 +715,14 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             LAUNCHED(1);
         }
         CK(cudaEventRecord(ctx->ev[EV_VERIFY], s));
-        unsigned long long hcnt[2];
+        unsigned long long hcnt[2], hg[2] = {0, 0};  // cand, res; gathered blocks, pairs
         CK(cudaMemcpyAsync(hcnt, &dctr->cand, 16, cudaMemcpyDeviceToHost, s));
+        if (gather) CK(cudaMemcpyAsync(hg, &dctr->gblocks, 16, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         cand_n = (long long)hcnt[0];
         res_n = (long long)hcnt[1];
+        st.gathered_pairs = (int64_t)hg[1] * bq;
+        ctx->glist_len = gather ? ctx->list_len * GT_ROWS : 0;
         if (cand_n > ctx->cand_cap) {
             ctx->cand_cap = cand_n + cand_n / 4 + 1024;
             st.reruns++;
@@ -1185,13 +1245,15 @@ extern "C" int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t by
         case KGC_INSPECT_TAIL_KEYS: src = ctx->K > 1 ? ctx->mpkt.p : ctx->kt.p; n = ctx->N * 4 * ctx->K; break;
         case KGC_INSPECT_QUERY_KEYS: src = ctx->K > 1 ? ctx->mpkq.p : ctx->kq.p; n = ctx->N * ctx->R * 4 * ctx->K; break;
         case KGC_INSPECT_TILE_LIST: src = ctx->tile_list.p; n = ctx->list_len * 4; break;
+        case KGC_INSPECT_GATHER_LIST: src = ctx->glist.p; n = ctx->glist_len * 4; break;
+        case KGC_INSPECT_GATHER_COST: src = ctx->glist_len ? ctx->gblk.p : nullptr; n = src ? ctx->R * (int64_t)ctx->QT * 8 : 0; break;
         case KGC_INSPECT_TAIL_PERM: src = ctx->tperm.p; n = ctx->N * 4; break;
         case KGC_INSPECT_QUERY_PERM: src = ctx->qperm.p; n = ctx->N * ctx->R * 4; break;
         case KGC_INSPECT_TILE_RANGES: src = ctx->ranges.p; n = ctx->R * (int64_t)ctx->QT * 8; break;
         case KGC_INSPECT_QUERY_COST: src = ctx->cum.p; n = ctx->R * (int64_t)ctx->QT * 8; break;
         default: return KGC_EINVAL;
     }
-    if (out && bytes > 0) {
+    if (out && bytes > 0 && n > 0) {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(ctx->device);

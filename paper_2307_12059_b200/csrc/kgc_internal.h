@@ -30,6 +30,8 @@ struct DevCounters {
     long long n_items;            // work items of this shard
     unsigned int absmax_bits;     // max |value| over E and Rel (float bits), for the FP16 engine
     unsigned int pad1;
+    long long gblocks;            // gathered-tail engine: GT_ROWS-tail blocks of this shard
+    unsigned long long gpairs;    // gathered-tail engine: surviving tails summed over query tiles
 };
 
 struct TileParams {
@@ -62,6 +64,12 @@ struct TileParams {
     const int* qperm;
     int d;
     int QT;
+    // gathered-tail SIMT engine (GT_ROWS tails per block, see tiles_simt.cu)
+    const float* Ts;              // sorted tails, row-major [N + 1][Kpad] (row N: sentinel)
+    const int* glist;             // per query tile (at GT_ROWS x its tile-list offset): surviving sorted
+                                  // tail positions, padded with N to whole blocks
+    const long long* dn_items;    // device: work items of this shard
+    const long long* dtotal;      // device: blocks of this shard (balanced CTA ranges)
 };
 
 // ---- launchers (prep.cu) ----
@@ -121,6 +129,15 @@ void launch_mp_emit(const float* qbmin, const float* qbmax, const float* tbmin, 
                     const long long* cum, const DevCounters* ctr, long long nq, int TT, int K, float theta, float relm,
                     int prune, int* list, cudaStream_t s);
 
+// ---- gathered-tail SIMT engine (pivots.cu): element-level tail pruning against query-tile boxes
+constexpr int GT_ROWS = 64;  // tails per gathered block (= SIMT_T)
+void launch_stage_rows(const float* E, const int* tperm, const float* keys, long long N, int d, int Kpad, int K,
+                       float* Ts, float* tks, cudaStream_t s);
+void launch_gather_tails(const float* qbmin, const float* qbmax, const float* tks, const int* list,
+                         const long long* cum, const int2* ranges, DevCounters* ctr, long long N, int K, float theta,
+                         float relm, int chunk, long long nq, long long* gblocks, int2* granges, int* nitem,
+                         int* glist, cudaStream_t s);
+
 // Tail tile of position j of item w (contiguous range or multi-pivot list).
 __device__ __forceinline__ int item_tile(const int4& w, int j, const int* __restrict__ list) {
     return w.w < 0 ? j : __ldg(list + w.w + j);
@@ -132,6 +149,7 @@ void launch_tiles_tc(const TileParams& p, int num_sms, cudaStream_t s);
 int  tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);
 void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s);
 void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t s);
+void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long max_items, cudaStream_t s);
 void launch_tiles_half_l1(const TileParams& p, int num_sms, cudaStream_t s);
 constexpr int HALF_FLUSH_PAIRS = 8;  // FP16x2 engine: flush to FP32 every 16 dims
 

@@ -13,6 +13,8 @@
 // candidate; the FP64 re-check (verify.cu) decides.
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace kgc {
@@ -389,6 +391,212 @@ void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t 
     }
     if (norm == 1) launch_simt_variant<1, 8, 8, 32, 2>(p, num_sms, s);
     else launch_simt_variant<2, 8, 8, 32, 2>(p, num_sms, s);
+}
+
+
+// ------------------------------------------------------------------------
+// Gathered-tail variant (l1_engine 3): the 64 tails of a block are not a
+// contiguous tile but the next 64 entries of the query tile's list of
+// surviving tails (pivots.cu, gather_tails_kernel), so the arithmetic skips
+// every tail that fails the K-pivot test against the query tile's box.  Tail
+// rows are gathered row-major into shared memory by per-row bulk copies
+// (klen * 4 bytes each, 16-B aligned), issued by the 32 lanes of the warp
+// that refills a stage; row stride GT_LD = KC + 4 floats keeps the float4 row
+// reads of the 8 tail rows a thread touches conflict-free (thread tx owns rows
+// tx, tx + 8, ..., tx + 56).  Queries stream k-major exactly as above.
+template <int NORM, int KC, int NSTAGE>
+__global__ void __launch_bounds__(64) tiles_gather_kernel(TileParams p) {
+    constexpr int T = SIMT_T, TM = 8, TN = 8, NT = 64, GX = T / TN;
+    constexpr int LD = KC + 4;  // tail row stride in shared memory (floats)
+    static_assert(T == GT_ROWS, "gathered block = tile");
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int Kpad = p.Kpad;
+    const int nkc = (Kpad + KC - 1) / KC;
+    // stage s: query chunk [KC][T] followed by tail rows [T][LD]
+    constexpr int STAGE = KC * T + T * LD;
+    float* St = reinterpret_cast<float*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(St + NSTAGE * STAGE);
+    int* released = reinterpret_cast<int*>(full + NSTAGE);
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int ty = tid / GX, tx = tid % GX;
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) {
+            mbar_init(&full[s], 1);
+            released[s] = 0;
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const long long n_items = *p.dn_items, total = *p.dtotal;
+
+    struct It {
+        long long it, end;
+        int4 w;
+        int j, c;
+    };
+    auto valid = [&](const It& ci) { return ci.it < ci.end; };
+    auto next = [&](It& ci) {
+        if (++ci.c < nkc) return;
+        ci.c = 0;
+        if (++ci.j <= ci.w.z) return;
+        if (++ci.it < ci.end) {
+            ci.w = p.items[ci.it];
+            ci.j = ci.w.y;
+        }
+    };
+    // Called by all 32 lanes of one warp once stage (g % NSTAGE) is free.
+    auto issue = [&](const It& ci, long long g) {
+        const int s = (int)(g % NSTAGE);
+        const int klen = Kpad - ci.c * KC < KC ? Kpad - ci.c * KC : KC;
+        const uint32_t qbytes = (uint32_t)klen * T * 4, rbytes = (uint32_t)klen * 4;
+        float* dst = St + (size_t)s * STAGE;
+        const int* seg = p.glist + ((long long)ci.w.w + ci.j) * T;
+        const int r0 = __ldg(seg + lane), r1 = __ldg(seg + lane + 32);
+        if (lane == 0) {
+            mbar_arrive_expect_tx(&full[s], qbytes + T * rbytes);
+            bulk_g2s(dst, p.Qp + (size_t)(ci.w.x - p.tq0) * T * Kpad + (size_t)ci.c * KC * T, qbytes, &full[s]);
+        }
+        float* tdst = dst + KC * T;
+        bulk_g2s(tdst + lane * LD, p.Ts + (size_t)r0 * Kpad + ci.c * KC, rbytes, &full[s]);
+        bulk_g2s(tdst + (lane + 32) * LD, p.Ts + (size_t)r1 * Kpad + ci.c * KC, rbytes, &full[s]);
+    };
+
+    It cs;  // the chunk sequence every thread consumes: this CTA's cost-balanced block of items
+    cs.it = balanced_begin(p.item_cum, n_items, total, blockIdx.x, gridDim.x);
+    cs.end = balanced_begin(p.item_cum, n_items, total, blockIdx.x + 1, gridDim.x);
+    cs.c = 0;
+    if (cs.it < cs.end) {
+        cs.w = p.items[cs.it];
+        cs.j = cs.w.y;
+    }
+    if (tid < 32) {  // prologue: warp 0 fills every stage
+        It pr = cs;
+        for (long long gp = 0; gp < NSTAGE && valid(pr); ++gp) {
+            issue(pr, gp);
+            next(pr);
+        }
+    }
+
+    float thr[TM];
+    float acc[TM][TN];
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b) acc[a][b] = 0.f;
+    long long cur_item = -1;
+
+    for (long long g = 0; valid(cs); ++g) {
+        if (cs.it != cur_item) {
+            cur_item = cs.it;
+#pragma unroll
+            for (int a = 0; a < TM; ++a) thr[a] = p.qs[(size_t)(cs.w.x - p.tq0) * T + ty * TM + a].w;
+        }
+        const int s = (int)(g % NSTAGE);
+        mbar_wait(&full[s], (uint32_t)(g / NSTAGE) & 1u);
+        const int klen = Kpad - cs.c * KC < KC ? Kpad - cs.c * KC : KC;
+        const float* qk = St + (size_t)s * STAGE + ty * TM;
+        const float* tk = St + (size_t)s * STAGE + KC * T + tx * LD;
+#pragma unroll 1
+        for (int k4 = 0; k4 < klen; k4 += 4) {
+            float4 tv[TN];
+#pragma unroll
+            for (int b = 0; b < TN; ++b) tv[b] = *reinterpret_cast<const float4*>(tk + b * GX * LD + k4);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                float qv[TM];
+#pragma unroll
+                for (int a = 0; a < TM; a += 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(qk + (k4 + kk) * T + a);
+                    qv[a] = v.x; qv[a + 1] = v.y; qv[a + 2] = v.z; qv[a + 3] = v.w;
+                }
+#pragma unroll
+                for (int a = 0; a < TM; ++a)
+#pragma unroll
+                    for (int b = 0; b < TN; ++b) {
+                        const float t = kk == 0 ? tv[b].x : kk == 1 ? tv[b].y : kk == 2 ? tv[b].z : tv[b].w;
+                        const float df = qv[a] - t;
+                        if (NORM == 1) acc[a][b] += fabsf(df);
+                        else acc[a][b] = fmaf(df, df, acc[a][b]);
+                    }
+            }
+        }
+        // The last warp to finish reading stage s refills it with chunk g + NSTAGE.
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+            __threadfence_block();
+            last = atomicAdd(&released[s], 1) == NT / 32 - 1;
+            if (last) released[s] = 0;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+            It nx = cs;
+#pragma unroll 1
+            for (int x = 0; x < NSTAGE && valid(nx); ++x) next(nx);
+            if (valid(nx)) {
+                fence_proxy_async_smem();
+                issue(nx, g + NSTAGE);
+            }
+        }
+        if (cs.c == nkc - 1) {
+            unsigned long long hit = 0;
+#pragma unroll
+            for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TN; ++b) hit |= (unsigned long long)(acc[a][b] <= thr[a]) << (a * TN + b);
+            if (__any_sync(0xffffffffu, hit != 0)) {
+                const int* seg = p.glist + ((long long)cs.w.w + cs.j) * T + tx;
+#pragma unroll
+                for (int b = 0; b < TN; ++b) {
+                    const unsigned long long colm = 0x0101010101010101ull << b;  // column b of the micro-tile
+                    if ((hit & colm) && __ldg(seg + b * GX) >= p.N) hit &= ~colm;  // sentinel padding
+                }
+                unsigned long long slot = warp_reserve(__popcll(hit), p.cand_count);
+                while (hit) {
+                    const int ab = __ffsll(hit) - 1;
+                    if (slot < (unsigned long long)p.cand_cap)
+                        p.cand[slot] = make_int2(cs.w.x * T + ty * TM + ab / TN, __ldg(seg + (ab % TN) * GX));
+                    ++slot;
+                    hit &= hit - 1;
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TN; ++b) acc[a][b] = 0.f;
+        }
+        next(cs);
+    }
+}
+
+template <int NORM, int KC, int NS>
+static void launch_gather_variant(const TileParams& p, int num_sms, long long max_items, cudaStream_t s) {
+    constexpr int T = SIMT_T;
+    const size_t smem = (size_t)NS * (KC * T + T * (KC + 4)) * 4 + 128;
+    auto kern = tiles_gather_kernel<NORM, KC, NS>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 64, smem);
+    if (per_sm < 1) per_sm = 1;
+    long long g = (long long)num_sms * per_sm;
+    if (g > max_items) g = max_items;
+    if (g < 1) g = 1;
+    kern<<<(unsigned)g, 64, smem, s>>>(p);
+}
+
+void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long max_items, cudaStream_t s) {
+    if (max_items <= 0) return;
+    const char* e = getenv("KGC_GT_VAR");  // experiment knob: K-chunk / stage variants
+    const int v = e ? atoi(e) : 0;
+    if (norm == 1) {
+        if (v == 1) launch_gather_variant<1, 24, 2>(p, num_sms, max_items, s);
+        else if (v == 2) launch_gather_variant<1, 16, 3>(p, num_sms, max_items, s);
+        else if (v == 3) launch_gather_variant<1, 32, 3>(p, num_sms, max_items, s);
+        else launch_gather_variant<1, 32, 2>(p, num_sms, max_items, s);
+    } else {
+        launch_gather_variant<2, 32, 2>(p, num_sms, max_items, s);
+    }
 }
 
 }  // namespace kgc

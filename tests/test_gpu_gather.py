@@ -1,0 +1,155 @@
+"""GPU parity of the gathered-tail SIMT engine (engine 5, l1_engine 3): inside
+every surviving tile pair only the tails whose own K pivot keys pass Lemma 1's
+L_inf test against the query tile's key box are computed (pivots.cu,
+tiles_simt.cu).  Lemma 1 makes the dropped tails provably
+farther than theta from every query of the tile, so the set must not change."""
+import numpy as np
+import pytest
+
+from synth import generate, generate_config, sample_rows
+from tests.gpu_util import check_parity, gpu_join, keyset, theta_for
+
+pytestmark = pytest.mark.gpu
+
+L1_GATHER = dict(pivots=8, l1_engine=3)
+L1_TILES = dict(pivots=8, l1_engine=2)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2307_12059_b200 import _build
+    _build.build()
+
+
+@pytest.mark.parametrize("norm", [1, 2])
+@pytest.mark.parametrize("K", [2, 8])
+def test_gather_c1_full(norm, K):
+    E, Rel = generate_config("c1")
+    eps = theta_for(E, Rel, norm, 1e-3)
+    opts = dict(pivots=K, l1_engine=3, l2_engine=2)
+    res, st = gpu_join(E, Rel, norm, eps, **opts)
+    assert st["engine"] == 5 and st["pivots_used"] == K
+    rep = check_parity(E, Rel, norm, eps, res)
+    assert rep["tight"] > 1000
+    assert 0 < st["gathered_pairs"] < st["tile_pairs_surviving"] * 64 * 64
+
+
+def test_gather_is_l1_default_with_pivots():
+    E, Rel = generate_config("c1")
+    eps = theta_for(E, Rel, 1, 1e-3)
+    _, st = gpu_join(E, Rel, 1, eps, pivots=8)
+    assert st["engine"] == 5
+    _, st1 = gpu_join(E, Rel, 1, eps)           # one pivot: contiguous tiles
+    assert st1["engine"] == 2
+
+
+@pytest.mark.parametrize("N,R,d", [(1, 1, 1), (7, 3, 5), (65, 2, 8), (129, 2, 9), (300, 5, 100), (1000, 4, 200),
+                                   (513, 2, 256), (700, 3, 50), (2049, 3, 33)])
+@pytest.mark.parametrize("norm", [1, 2])
+@pytest.mark.parametrize("dist", ["cluster", "uniform"])
+def test_gather_ragged(N, R, d, norm, dist):
+    E, Rel = generate(N, R, d, seed=3 * N + d, dist=dist)
+    eps = theta_for(E, Rel, norm, 0.01 if N > 10 else 0.3)
+    res, st = gpu_join(E, Rel, norm, eps, pivots=8, l1_engine=3, l2_engine=2)
+    assert st["engine"] == (5 if st["work_items_mine"] > 0 else 2)
+    check_parity(E, Rel, norm, eps, res)
+
+
+@pytest.mark.parametrize("norm", [1, 2])
+def test_gather_equals_contiguous_tiles(norm):
+    E, Rel = generate(8000, 5, 64, seed=51)
+    eps = theta_for(E, Rel, norm, 1e-3)
+    a, sa = gpu_join(E, Rel, norm, eps, pivots=8, l1_engine=2, l2_engine=2)
+    b, sb = gpu_join(E, Rel, norm, eps, pivots=8, l1_engine=3, l2_engine=2)
+    assert sa["engine"] == 2 and sb["engine"] == 5
+    assert keyset(a) == keyset(b)
+    assert sa["tile_pairs_surviving"] == sb["tile_pairs_surviving"]
+    assert sb["gathered_pairs"] < sb["tile_pairs_surviving"] * 64 * 64
+    # same candidates up to tails dropped by the per-tail test (all provably misses)
+    assert sb["candidates"] <= sa["candidates"]
+
+
+def test_gather_lists_complete_and_sound():
+    """Every (query tile, tail) with some query row passing the K-pivot L_inf
+    test (|d(p_k,q) - d(p_k,t)| <= eps for all k) is in the query tile's
+    gathered list; lists are ascending, padded with N to blocks of 64, and hold
+    only tails of the query tile's surviving tiles."""
+    from paper_2307_12059_b200 import kgc
+    N, R, K, d = 3000, 3, 8, 32
+    E, Rel = generate(N, R, d, seed=52)
+    eps = theta_for(E, Rel, 1, 1e-3)
+    with kgc.Join(pivots=K, l1_engine=3) as j:
+        j.run(E, Rel, 1, eps)
+        kt = j.inspect("tail_keys").reshape(N, K)
+        kq = j.inspect("query_keys").reshape(R, N, K)
+        tperm = j.inspect("tail_perm")
+        qperm = j.inspect("query_perm").reshape(R, N)
+        cum = j.inspect("query_cost")
+        lst = j.inspect("tile_list")
+        gcum = j.inspect("gather_cost")
+        glist = j.inspect("gather_list")
+        st = j.stats()
+    assert st["engine"] == 5
+    BM, BN, QT = st["query_tile_rows"], st["tail_tile_rows"], st["query_tiles"]
+    skt = kt[tperm]
+    nq = R * QT
+    assert gcum.shape == (nq,) and len(glist) == 64 * len(lst)
+    for r in range(R):
+        skq = kq[r][qperm[r]]
+        for qt in range(QT):
+            tq = r * QT + qt
+            ntl = (cum[tq + 1] if tq + 1 < nq else len(lst) + cum[0]) - cum[tq]
+            g0 = 64 * (cum[tq] - cum[0])
+            seg = glist[g0:g0 + 64 * gcum[tq]]
+            assert gcum[tq] <= ntl
+            real = seg[seg < N]
+            assert len(seg) == 64 * ((len(real) + 63) // 64)      # whole blocks
+            assert np.all(seg[len(real):] == N)                  # padding at the end only
+            assert np.all(np.diff(real) > 0)                      # ascending, unique
+            tiles = set(lst[cum[tq] - cum[0]: cum[tq] - cum[0] + ntl].tolist())
+            assert set((real // BN).tolist()) <= tiles
+            rows = skq[qt * BM:(qt + 1) * BM]
+            ok = np.ones((rows.shape[0], N), bool)
+            for k in range(K):
+                ok &= np.abs(rows[:, None, k] - skt[None, :, k]) <= eps
+            need = set(np.nonzero(ok.any(axis=0))[0].tolist())
+            assert need <= set(real.tolist())
+    assert st["gathered_pairs"] == BM * int(np.sum([np.sum(glist[64 * (cum[q] - cum[0]):][:64 * gcum[q]] < N)
+                                                     for q in range(nq)]))
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_gather_sharding_invariance(world):
+    E, Rel = generate(4000, 7, 48, seed=53)
+    eps = theta_for(E, Rel, 1, 1e-3)
+    full, _ = gpu_join(E, Rel, 1, eps, **L1_GATHER)
+    for split in (0, 1):
+        parts = [gpu_join(E, Rel, 1, eps, rank=r, world=world, split=split, **L1_GATHER)[0] for r in range(world)]
+        sets = [keyset(p) for p in parts]
+        assert sum(len(s) for s in sets) == len(set().union(*sets))
+        assert set().union(*sets) == keyset(full)
+
+
+def test_gather_host_inputs_and_capacity_rerun():
+    E, Rel = generate(3000, 4, 40, seed=54)
+    eps = theta_for(E, Rel, 1, 3e-3)
+    a, sa = gpu_join(E, Rel, 1, eps, device_inputs=False, result_capacity=16, **L1_GATHER)
+    b, _ = gpu_join(E, Rel, 1, eps, **L1_GATHER)
+    assert sa["reruns"] >= 1
+    assert keyset(a) == keyset(b)
+    check_parity(E, Rel, 1, eps, a)
+
+
+@pytest.mark.parametrize("hit", [1e-5, 1e-4])
+def test_gather_c2_l1_full_size_sampled(hit):
+    E, Rel = generate_config("c2")
+    N, R = E.shape[0], Rel.shape[0]
+    rows = sample_rows(N, R, 1200, seed=9)
+    eps = theta_for(E, Rel, 1, hit, rows=rows)
+    res, st = gpu_join(E, Rel, 1, eps, **L1_GATHER)
+    assert st["engine"] == 5
+    rep = check_parity(E, Rel, 1, eps, res, rows=rows)
+    assert rep["tight"] > 0
