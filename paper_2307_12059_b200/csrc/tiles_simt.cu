@@ -401,13 +401,16 @@ void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t 
 // every tail that fails the K-pivot test against the query tile's box.  Tail
 // rows are gathered row-major into shared memory by per-row bulk copies
 // (klen * 4 bytes each, 16-B aligned), issued by the 32 lanes of the warp
-// that refills a stage; row stride GT_LD = KC + 4 floats keeps the float4 row
-// reads of the 8 tail rows a thread touches conflict-free (thread tx owns rows
-// tx, tx + 8, ..., tx + 56).  Queries stream k-major exactly as above.
-template <int NORM, int KC, int NSTAGE>
-__global__ void __launch_bounds__(64) tiles_gather_kernel(TileParams p) {
+// that refills a stage.  Thread tx owns tail rows tx, tx + 8, ..., tx + 56; its
+// float4 row reads are conflict-free either with a padded row stride KC + 4
+// (SWZ = 0) or with 16-byte piece p of row i stored at piece p ^ (i & 7) of an
+// unpadded 32-float row (SWZ = 1, KC = 32: 16 KB per stage, 7 CTAs per SM).
+// Queries stream k-major exactly as above.
+template <int NORM, int KC, int NSTAGE, int SWZ>
+__global__ void __launch_bounds__(64, 8) tiles_gather_kernel(TileParams p) {
     constexpr int T = SIMT_T, TM = 8, TN = 8, NT = 64, GX = T / TN;
-    constexpr int LD = KC + 4;  // tail row stride in shared memory (floats)
+    static_assert(!SWZ || KC == 32, "swizzle over the 8 pieces of a 32-float row");
+    constexpr int LD = SWZ ? KC : KC + 4;  // tail row stride in shared memory (floats)
     static_assert(T == GT_ROWS, "gathered block = tile");
     extern __shared__ __align__(128) uint8_t smem[];
     const int Kpad = p.Kpad;
@@ -417,12 +420,13 @@ __global__ void __launch_bounds__(64) tiles_gather_kernel(TileParams p) {
     float* St = reinterpret_cast<float*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(St + NSTAGE * STAGE);
     int* released = reinterpret_cast<int*>(full + NSTAGE);
+    int* ridx = released + NSTAGE;  // [T] row indices of the block being issued
 
     const int tid = threadIdx.x, lane = tid & 31;
     const int ty = tid / GX, tx = tid % GX;
     if (tid == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], 1 + 32);  // the bulk copy's expect_tx arrival + 32 lanes' cp.async arrivals
             released[s] = 0;
         }
         fence_mbar_init();
@@ -445,21 +449,63 @@ __global__ void __launch_bounds__(64) tiles_gather_kernel(TileParams p) {
             ci.j = ci.w.y;
         }
     };
-    // Called by all 32 lanes of one warp once stage (g % NSTAGE) is free.
+    // Called by all 32 lanes of one warp once stage (g % NSTAGE) is free: the query
+    // chunk by one bulk copy (transaction bytes), the 64 gathered tail rows by 16-byte
+    // cp.async pieces (8 consecutive lanes per 128-byte row chunk), each lane's pieces
+    // arriving on the stage barrier through cp.async.mbarrier.arrive.noinc (barrier
+    // count 1 + 32).  Row indices: lane l loads those of rows l and l + 32 once, the
+    // pieces take them by shuffle.
     auto issue = [&](const It& ci, long long g) {
         const int s = (int)(g % NSTAGE);
         const int klen = Kpad - ci.c * KC < KC ? Kpad - ci.c * KC : KC;
-        const uint32_t qbytes = (uint32_t)klen * T * 4, rbytes = (uint32_t)klen * 4;
+        const uint32_t qbytes = (uint32_t)klen * T * 4;
         float* dst = St + (size_t)s * STAGE;
-        const int* seg = p.glist + ((long long)ci.w.w + ci.j) * T;
-        const int r0 = __ldg(seg + lane), r1 = __ldg(seg + lane + 32);
+        // the block's row indices: from global memory at its first chunk (kept in shared
+        // memory for the others -- issues are serialised, see the release protocol below)
+        int r0, r1;
+        if (ci.c == 0) {
+            const int* seg = p.glist + ((long long)ci.w.w + ci.j) * T;
+            r0 = __ldg(seg + lane);
+            r1 = __ldg(seg + lane + 32);
+            if (lane < 2) prefetch_l1(seg + T + lane * 32);  // the next block's indices
+            if (nkc > 1) {
+                ridx[lane] = r0;
+                ridx[lane + 32] = r1;
+            }
+        } else {
+            r0 = ridx[lane];
+            r1 = ridx[lane + 32];
+        }
         if (lane == 0) {
-            mbar_arrive_expect_tx(&full[s], qbytes + T * rbytes);
+            mbar_arrive_expect_tx(&full[s], qbytes);
             bulk_g2s(dst, p.Qp + (size_t)(ci.w.x - p.tq0) * T * Kpad + (size_t)ci.c * KC * T, qbytes, &full[s]);
         }
-        float* tdst = dst + KC * T;
-        bulk_g2s(tdst + lane * LD, p.Ts + (size_t)r0 * Kpad + ci.c * KC, rbytes, &full[s]);
-        bulk_g2s(tdst + (lane + 32) * LD, p.Ts + (size_t)r1 * Kpad + ci.c * KC, rbytes, &full[s]);
+        const uint32_t tdst = smem_u32(dst + KC * T);
+        const float* src0 = p.Ts + (size_t)ci.c * KC;
+        auto piece = [&](int row, int pseg, int ridx) {
+            const int slot = SWZ ? (pseg ^ (row & 7)) : pseg;
+            cp_async16(tdst + (uint32_t)(row * LD + slot * 4) * 4u, src0 + (size_t)ridx * Kpad + pseg * 4);
+        };
+        if (klen == KC && 32 % (KC / 4) == 0) {
+            // full chunk, compile-time pieces per row dividing 32: every pass covers rows of one half
+            constexpr int PR = KC / 4, RPP = 32 / PR;
+            const int prow = lane / PR, pseg = lane % PR;
+#pragma unroll 2
+            for (int m = 0; m < T / RPP; ++m) {
+                const int row = m * RPP + prow;
+                piece(row, pseg, __shfl_sync(0xffffffffu, m * RPP < 32 ? r0 : r1, row & 31));
+            }
+        } else {
+            const int per_row = klen / 4;  // 16-byte pieces per row chunk (klen % 8 == 0)
+            // warp-uniform trip count (the shuffles need every lane)
+#pragma unroll 1
+            for (int pc = lane; pc < ((T * per_row + 31) & ~31); pc += 32) {
+                const int row = pc / per_row, pseg = pc - row * per_row;
+                const int a0 = __shfl_sync(0xffffffffu, r0, row & 31), a1 = __shfl_sync(0xffffffffu, r1, row & 31);
+                if (row < T) piece(row, pseg, row < 32 ? a0 : a1);
+            }
+        }
+        cp_async_mbar_arrive_noinc(&full[s]);
     };
 
     It cs;  // the chunk sequence every thread consumes: this CTA's cost-balanced block of items
@@ -501,7 +547,8 @@ __global__ void __launch_bounds__(64) tiles_gather_kernel(TileParams p) {
         for (int k4 = 0; k4 < klen; k4 += 4) {
             float4 tv[TN];
 #pragma unroll
-            for (int b = 0; b < TN; ++b) tv[b] = *reinterpret_cast<const float4*>(tk + b * GX * LD + k4);
+            for (int b = 0; b < TN; ++b)
+                tv[b] = *reinterpret_cast<const float4*>(tk + b * GX * LD + (SWZ ? (((k4 >> 2) ^ tx) << 2) : k4));
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
                 float qv[TM];
@@ -570,11 +617,11 @@ __global__ void __launch_bounds__(64) tiles_gather_kernel(TileParams p) {
     }
 }
 
-template <int NORM, int KC, int NS>
+template <int NORM, int KC, int NS, int SWZ = 0>
 static void launch_gather_variant(const TileParams& p, int num_sms, long long max_items, cudaStream_t s) {
     constexpr int T = SIMT_T;
-    const size_t smem = (size_t)NS * (KC * T + T * (KC + 4)) * 4 + 128;
-    auto kern = tiles_gather_kernel<NORM, KC, NS>;
+    const size_t smem = (size_t)NS * (KC * T + T * (SWZ ? KC : KC + 4)) * 4 + 128 + T * 4;
+    auto kern = tiles_gather_kernel<NORM, KC, NS, SWZ>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 64, smem);
@@ -590,9 +637,12 @@ void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long m
     const char* e = getenv("KGC_GT_VAR");  // experiment knob: K-chunk / stage variants
     const int v = e ? atoi(e) : 0;
     if (norm == 1) {
+        // measured on c2 L1 (gathered-tail tiles ms): 32/2 padded 4.85, 32/2 swizzled 4.90,
+        // 24/2 5.20, 16/3 5.47, 32/3 swizzled 5.54
         if (v == 1) launch_gather_variant<1, 24, 2>(p, num_sms, max_items, s);
         else if (v == 2) launch_gather_variant<1, 16, 3>(p, num_sms, max_items, s);
-        else if (v == 3) launch_gather_variant<1, 32, 3>(p, num_sms, max_items, s);
+        else if (v == 3) launch_gather_variant<1, 32, 2, 1>(p, num_sms, max_items, s);
+        else if (v == 4) launch_gather_variant<1, 32, 3, 1>(p, num_sms, max_items, s);
         else launch_gather_variant<1, 32, 2>(p, num_sms, max_items, s);
     } else {
         launch_gather_variant<2, 32, 2>(p, num_sms, max_items, s);

@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_gt.log 2>&1 || exit 1
 for V in ${VARS:-0 1 2 3}; do
-  KGC_GT_VAR=$V timeout 300 python bench.py --norms 1 --no-cpu --no-e2e > gpurun_out/gt_v$V.json 2>/dev/null
+  KGC_GT_VAR=$V timeout 120 python bench.py --norms 1 --no-cpu --no-e2e > gpurun_out/gt_v$V.json 2>/dev/null
   python -c "
 import json,sys; d=json.loads(open('gpurun_out/gt_v$V.json').read())
 k=[k for k in d['kernels'] if 'achieved' in k][0]
