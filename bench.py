@@ -19,6 +19,7 @@ flushed (512 MiB write) before every timed step, outside the events.
 from __future__ import annotations
 
 import argparse
+from concurrent.futures import ThreadPoolExecutor
 import json
 import os
 import statistics
@@ -219,14 +220,36 @@ def run_ours(args, cfg, thresholds):
         E_h, Rel_h = Et.cpu().numpy(), Rt.cpu().numpy()
     torch.cuda.synchronize()
 
-    joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, stream=stream.cuda_stream)
+    # the joins of one step (one per norm) run concurrently: one context, stream and host thread
+    # each (a context is single-threaded; kgc_join blocks its thread at its two host syncs, so
+    # the other join fills those gaps); --sequential runs them one after the other on one stream
+    conc = len(args.norms) > 1 and not args.sequential
+    jstream = {n: (torch.cuda.Stream(dev) if conc else stream) for n in args.norms}
+    pool = ThreadPoolExecutor(len(args.norms)) if conc else None
+
+    def run_joins(fn):
+        """fn(n) for every norm, concurrently on the norms' streams, ordered after / before `stream`."""
+        if not conc:
+            return [fn(n) for n in args.norms]
+        ev0 = torch.cuda.Event()
+        ev0.record(stream)
+        for n in args.norms:
+            jstream[n].wait_event(ev0)
+        out = [f.result() for f in [pool.submit(fn, n) for n in args.norms]]
+        for n in args.norms:
+            ev = torch.cuda.Event()
+            ev.record(jstream[n])
+            stream.wait_event(ev)
+        return out
+
+    joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, stream=jstream[n].cuda_stream)
              for n in args.norms}
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     counts = torch.zeros(len(args.norms), dtype=torch.int64, device=dev)
 
     def step():
-        for i, n in enumerate(args.norms):
-            c = joins[n].run(Et, Rt, n, eps[n])
+        cs = run_joins(lambda n: joins[n].run(Et, Rt, n, eps[n]))
+        for i, c in enumerate(cs):
             counts[i] = c
         if world > 1:
             dist.all_reduce(counts)
@@ -336,18 +359,21 @@ def run_ours(args, cfg, thresholds):
         out_pin = {n: torch.empty((max(1, stats_last[n]["results"]) * 2, 4), dtype=torch.int32).pin_memory()
                    for n in args.norms}
         e2e_joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots,
-                                 stream=stream.cuda_stream) for n in args.norms}
+                                 stream=jstream[n].cuda_stream) for n in args.norms}
         h2d = d2h = 0
+
+        def e2e_one(n):
+            j = e2e_joins[n]
+            kgc.kgc_join(j.ctx, E_pin, R_pin, N, R, d, n, eps[n])
+            cnt = kgc.kgc_results(j.ctx)
+            if cnt > out_pin[n].shape[0]:
+                out_pin[n] = torch.empty((cnt * 2, 4), dtype=torch.int32).pin_memory()
+            kgc.kgc_results(j.ctx, out_pin[n], cnt)
+            return cnt
 
         def e2e_step():
             nonlocal h2d, d2h
-            for n in args.norms:
-                j = e2e_joins[n]
-                kgc.kgc_join(j.ctx, E_pin, R_pin, N, R, d, n, eps[n])
-                cnt = kgc.kgc_results(j.ctx)
-                if cnt > out_pin[n].shape[0]:
-                    out_pin[n] = torch.empty((cnt * 2, 4), dtype=torch.int32).pin_memory()
-                kgc.kgc_results(j.ctx, out_pin[n], cnt)
+            for cnt in run_joins(e2e_one):
                 h2d += E_pin.numel() * 4 + R_pin.numel() * 4
                 d2h += cnt * 16
         e2e_step()
@@ -409,6 +435,8 @@ def run_ours(args, cfg, thresholds):
             "data": "synthetic",
             "config": {"workload": wl, "N": N, "R": R, "d": d, "norms": args.norms, "eps": eps, "hit_rate": args.hit,
                        "parallelism": f"query-tile shards x{world}, tails replicated",
+                       "joins": ("concurrent: one context, stream and host thread per norm" if conc else
+                                 "sequential on one stream"),
                        "pivots": args.pivots,
                        "l2_cache": "flushed (512 MiB write) before every timed step, outside the timed events"},
             "result_triplets_per_step": results_total,
@@ -489,6 +517,7 @@ def main():
     ap.add_argument("--hit", type=float, default=1e-4)
     ap.add_argument("--norms", default="2,1", help="norms joined per step, e.g. '2,1' or '2'")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sequential", action="store_true", help="run the step's joins one after the other")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=256, help="(h,r) rows per reference step")

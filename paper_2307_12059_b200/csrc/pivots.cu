@@ -427,8 +427,7 @@ __global__ void stage_rows_kernel(const float* __restrict__ E, const int* __rest
 }
 
 // One pass, warp per query tile of this shard: the tails of its surviving tiles
-// (two 32-tail halves per 64-row tile, both halves' keys loaded before either
-// test) that pass the per-tail test, written in ascending sorted position at
+// (two 32-tail halves per 64-row tile) that pass the per-tail test, written in ascending sorted position at
 // list offset GT_ROWS * (tile prefix[q] - prefix[first]) -- the tile list's own
 // offsets, an upper bound -- and padded with N to a multiple of GT_ROWS.
 __global__ void gather_tails_kernel(const float* __restrict__ qbmin, const float* __restrict__ qbmax,
@@ -453,26 +452,35 @@ __global__ void gather_tails_kernel(const float* __restrict__ qbmin, const float
         const int* L = list + (cum[q] - base);
         int* out = glist + (cum[q] - base) * GT_ROWS;
         long long c = 0;
-        int jn = ntl > 0 ? __ldg(L) : 0;
-        for (int u = 0; u < ntl; ++u) {
-            const long long i0 = (long long)jn * 64 + lane, i1 = i0 + 32;
-            if (u + 1 < ntl) jn = __ldg(L + u + 1);
-            float t0[MP_MAX], t1[MP_MAX];
-            {
-                const float4 a = i0 < N ? __ldg(tks + 2 * i0) : make_float4(0, 0, 0, 0);
-                const float4 b = i0 < N ? __ldg(tks + 2 * i0 + 1) : make_float4(0, 0, 0, 0);
-                const float4 e = i1 < N ? __ldg(tks + 2 * i1) : make_float4(0, 0, 0, 0);
-                const float4 f = i1 < N ? __ldg(tks + 2 * i1 + 1) : make_float4(0, 0, 0, 0);
-                t0[0] = a.x; t0[1] = a.y; t0[2] = a.z; t0[3] = a.w; t0[4] = b.x; t0[5] = b.y; t0[6] = b.z; t0[7] = b.w;
-                t1[0] = e.x; t1[1] = e.y; t1[2] = e.z; t1[3] = e.w; t1[4] = f.x; t1[5] = f.y; t1[6] = f.z; t1[7] = f.w;
+        // UN tiles per step: all their key loads issued before the first test (the loop is
+        // latency-bound and list lengths are heavy-tailed)
+        constexpr int UN = 4;
+        for (int u0 = 0; u0 < ntl; u0 += UN) {
+            float4 kv[UN][2][2];
+            long long ib[UN];
+#pragma unroll
+            for (int x = 0; x < UN; ++x) {
+                ib[x] = u0 + x < ntl ? (long long)__ldg(L + u0 + x) * 64 + lane : N;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const long long i = ib[x] + 32 * h;
+                    kv[x][h][0] = i < N ? __ldg(tks + 2 * i) : make_float4(0, 0, 0, 0);
+                    kv[x][h][1] = i < N ? __ldg(tks + 2 * i + 1) : make_float4(0, 0, 0, 0);
+                }
             }
-            const bool ok0 = i0 < N && mp_survives(qmn, qmx, t0, t0, K, theta, relm);
-            const bool ok1 = i1 < N && mp_survives(qmn, qmx, t1, t1, K, theta, relm);
-            const unsigned m0 = __ballot_sync(0xffffffffu, ok0), m1 = __ballot_sync(0xffffffffu, ok1);
-            if (ok0) out[c + __popc(m0 & lanemask_lt())] = (int)i0;  // ascending positions
-            c += __popc(m0);
-            if (ok1) out[c + __popc(m1 & lanemask_lt())] = (int)i1;
-            c += __popc(m1);
+#pragma unroll
+            for (int x = 0; x < UN; ++x) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const long long i = ib[x] + 32 * h;
+                    const float4 a = kv[x][h][0], b = kv[x][h][1];
+                    const float tk[MP_MAX] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                    const bool ok = i < N && mp_survives(qmn, qmx, tk, tk, K, theta, relm);
+                    const unsigned m = __ballot_sync(0xffffffffu, ok);
+                    if (ok) out[c + __popc(m & lanemask_lt())] = (int)i;  // ascending positions
+                    c += __popc(m);
+                }
+            }
         }
         const long long nb = (c + GT_ROWS - 1) / GT_ROWS;
         for (long long o = c + lane; o < nb * GT_ROWS; o += 32) out[o] = (int)N;  // sentinel padding
