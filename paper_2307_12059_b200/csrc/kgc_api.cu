@@ -694,7 +694,26 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.dn_items = &dctr->n_items;
         tp.dtotal = &dctr->gblocks;
         if (n_items > 0) {
-            if (gather) launch_tiles_gather(tp, norm, ctx->num_sms, g_max_items, s);
+            if (gather) {
+                const char* pe = getenv("KGC_GT_PROF");  // experiment: wait-cycle instrumentation
+                unsigned long long* prof = nullptr;
+                if (pe && atoi(pe)) {
+                    CK(cudaMalloc(&prof, 16 * 8));
+                    CK(cudaMemsetAsync(prof, 0, 128, s));
+                }
+                tp.prof = prof;
+                launch_tiles_gather(tp, norm, ctx->num_sms, g_max_items, s);
+                if (prof) {
+                    unsigned long long h[16];
+                    CK(cudaMemcpyAsync(h, prof, 128, cudaMemcpyDeviceToHost, s));
+                    CK(cudaStreamSynchronize(s));
+                    cudaFree(prof);
+                    fprintf(stderr, "gt_prof warps %llu avg cycles %.0f | wait/warp: item-start %.0f (%llu) "
+                            "block-start %.0f (%llu) other %.0f (%llu) | waited: issue->ready %.0f cycles (%llu)\n", h[7],
+                            (double)h[6] / h[7], (double)h[0] / h[7], h[1], (double)h[2] / h[7], h[3],
+                            (double)h[4] / h[7], h[5], h[9] ? (double)h[8] / h[9] : 0.0, h[9]);
+                }
+            }
             else if (tc2) launch_tiles_tc2(tp, ctx->num_sms, s);
             else if (tc) launch_tiles_tc(tp, ctx->num_sms, s);
             else if (half) launch_tiles_half_l1(tp, ctx->num_sms, s);

@@ -70,6 +70,7 @@ struct TileParams {
                                   // tail positions, padded with N to whole blocks
     const long long* dn_items;    // device: work items of this shard
     const long long* dtotal;      // device: blocks of this shard (balanced CTA ranges)
+    unsigned long long* prof;     // experiment: wait-cycle counters (KGC_GT_PROF), else nullptr
 };
 
 // ---- launchers (prep.cu) ----

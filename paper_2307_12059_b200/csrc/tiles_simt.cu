@@ -398,16 +398,19 @@ void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t 
 // Gathered-tail variant (l1_engine 3): the 64 tails of a block are not a
 // contiguous tile but the next 64 entries of the query tile's list of
 // surviving tails (pivots.cu, gather_tails_kernel), so the arithmetic skips
-// every tail that fails the K-pivot test against the query tile's box.  Tail
-// rows are gathered row-major into shared memory by per-row bulk copies
-// (klen * 4 bytes each, 16-B aligned), issued by the 32 lanes of the warp
-// that refills a stage.  Thread tx owns tail rows tx, tx + 8, ..., tx + 56; its
-// float4 row reads are conflict-free either with a padded row stride KC + 4
-// (SWZ = 0) or with 16-byte piece p of row i stored at piece p ^ (i & 7) of an
-// unpadded 32-float row (SWZ = 1, KC = 32: 16 KB per stage, 7 CTAs per SM).
-// Queries stream k-major exactly as above.
-template <int NORM, int KC, int NSTAGE, int SWZ>
-__global__ void __launch_bounds__(64, 8) tiles_gather_kernel(TileParams p) {
+// every tail that fails the K-pivot test against the query tile's box.
+// Per stage: the query K-chunk by one bulk copy (as above), the 64 tail rows'
+// K-chunk gathered row-major by 16-byte cp.async pieces that arrive on the
+// stage's mbarrier (cp.async.mbarrier.arrive.noinc), issued by the 32 lanes of
+// the refilling warp.  K-chunks are balanced (a short last chunk left the next
+// block's first refill exposed).  Refill duty alternates between the two warps
+// by chunk parity, gated by an "empty" mbarrier the other warp arrives on.
+// Thread tx owns tail rows tx, tx + 8, ..., tx + 56; its float4 row reads are
+// conflict-free with a padded row stride KC + 4 (SWZ = 0) or with 16-byte
+// piece p of row i stored at piece p ^ (i & 7) of a 32-float row (SWZ = 1).
+// PROF = 1: clock64 wait instrumentation (KGC_GT_PROF=1, experiment only).
+template <int NORM, int KC, int NSTAGE, int SWZ, int PROF = 0, int DUTY = 1, int MINB = 8, int KUN = 1>
+__global__ void __launch_bounds__(64, MINB) tiles_gather_kernel(TileParams p) {
     constexpr int T = SIMT_T, TM = 8, TN = 8, NT = 64, GX = T / TN;
     static_assert(!SWZ || KC == 32, "swizzle over the 8 pieces of a 32-float row");
     constexpr int LD = SWZ ? KC : KC + 4;  // tail row stride in shared memory (floats)
@@ -415,18 +418,26 @@ __global__ void __launch_bounds__(64, 8) tiles_gather_kernel(TileParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int Kpad = p.Kpad;
     const int nkc = (Kpad + KC - 1) / KC;
+    // balanced K-chunks (multiples of 4 floats, sizes differ by at most 4): a short last
+    // chunk would leave too little compute to hide the next block's first refill
+    const int cu = (Kpad / 4) / nkc, cr = (Kpad / 4) % nkc;
+    auto chunk_k0 = [&](int c) { return 4 * (c * cu + (c < cr ? c : cr)); };
+    auto chunk_len = [&](int c) { return 4 * (cu + (c < cr ? 1 : 0)); };
     // stage s: query chunk [KC][T] followed by tail rows [T][LD]
     constexpr int STAGE = KC * T + T * LD;
     float* St = reinterpret_cast<float*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(St + NSTAGE * STAGE);
-    int* released = reinterpret_cast<int*>(full + NSTAGE);
+    uint64_t* empty = full + NSTAGE;  // the non-duty warp has finished reading the stage
+    int* released = reinterpret_cast<int*>(empty + NSTAGE);
     int* ridx = released + NSTAGE;  // [T] row indices of the block being issued
+    __shared__ long long issued_at[PROF ? NSTAGE : 1];
 
     const int tid = threadIdx.x, lane = tid & 31;
     const int ty = tid / GX, tx = tid % GX;
     if (tid == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full[s], 1 + 32);  // the bulk copy's expect_tx arrival + 32 lanes' cp.async arrivals
+            mbar_init(&empty[s], 1);
             released[s] = 0;
         }
         fence_mbar_init();
@@ -457,7 +468,7 @@ __global__ void __launch_bounds__(64, 8) tiles_gather_kernel(TileParams p) {
     // pieces take them by shuffle.
     auto issue = [&](const It& ci, long long g) {
         const int s = (int)(g % NSTAGE);
-        const int klen = Kpad - ci.c * KC < KC ? Kpad - ci.c * KC : KC;
+        const int klen = chunk_len(ci.c), k0 = chunk_k0(ci.c);
         const uint32_t qbytes = (uint32_t)klen * T * 4;
         float* dst = St + (size_t)s * STAGE;
         // the block's row indices: from global memory at its first chunk (kept in shared
@@ -478,34 +489,28 @@ __global__ void __launch_bounds__(64, 8) tiles_gather_kernel(TileParams p) {
         }
         if (lane == 0) {
             mbar_arrive_expect_tx(&full[s], qbytes);
-            bulk_g2s(dst, p.Qp + (size_t)(ci.w.x - p.tq0) * T * Kpad + (size_t)ci.c * KC * T, qbytes, &full[s]);
+            bulk_g2s(dst, p.Qp + (size_t)(ci.w.x - p.tq0) * T * Kpad + (size_t)k0 * T, qbytes, &full[s]);
         }
         const uint32_t tdst = smem_u32(dst + KC * T);
-        const float* src0 = p.Ts + (size_t)ci.c * KC;
+        const float* src0 = p.Ts + k0;
         auto piece = [&](int row, int pseg, int ridx) {
             const int slot = SWZ ? (pseg ^ (row & 7)) : pseg;
             cp_async16(tdst + (uint32_t)(row * LD + slot * 4) * 4u, src0 + (size_t)ridx * Kpad + pseg * 4);
         };
-        if (klen == KC && 32 % (KC / 4) == 0) {
-            // full chunk, compile-time pieces per row dividing 32: every pass covers rows of one half
-            constexpr int PR = KC / 4, RPP = 32 / PR;
-            const int prow = lane / PR, pseg = lane % PR;
+        {
+            // rpp rows per pass over rpp * per_row lanes (two divisions per issue)
+            const int per_row = klen / 4, rpp = 32 / per_row;
+            const int prow = lane / per_row, pseg = lane - prow * per_row;
+            const bool act = lane < rpp * per_row;
 #pragma unroll 2
-            for (int m = 0; m < T / RPP; ++m) {
-                const int row = m * RPP + prow;
-                piece(row, pseg, __shfl_sync(0xffffffffu, m * RPP < 32 ? r0 : r1, row & 31));
-            }
-        } else {
-            const int per_row = klen / 4;  // 16-byte pieces per row chunk (klen % 8 == 0)
-            // warp-uniform trip count (the shuffles need every lane)
-#pragma unroll 1
-            for (int pc = lane; pc < ((T * per_row + 31) & ~31); pc += 32) {
-                const int row = pc / per_row, pseg = pc - row * per_row;
+            for (int row0 = 0; row0 < T; row0 += rpp) {
+                const int row = row0 + prow;
                 const int a0 = __shfl_sync(0xffffffffu, r0, row & 31), a1 = __shfl_sync(0xffffffffu, r1, row & 31);
-                if (row < T) piece(row, pseg, row < 32 ? a0 : a1);
+                if (act && row < T) piece(row, pseg, row < 32 ? a0 : a1);
             }
         }
         cp_async_mbar_arrive_noinc(&full[s]);
+        if (PROF && lane == 0) issued_at[s] = clock64();
     };
 
     It cs;  // the chunk sequence every thread consumes: this CTA's cost-balanced block of items
@@ -531,6 +536,7 @@ __global__ void __launch_bounds__(64, 8) tiles_gather_kernel(TileParams p) {
 #pragma unroll
         for (int b = 0; b < TN; ++b) acc[a][b] = 0.f;
     long long cur_item = -1;
+    const long long tstart = PROF ? clock64() : 0;
 
     for (long long g = 0; valid(cs); ++g) {
         if (cs.it != cur_item) {
@@ -539,11 +545,26 @@ __global__ void __launch_bounds__(64, 8) tiles_gather_kernel(TileParams p) {
             for (int a = 0; a < TM; ++a) thr[a] = p.qs[(size_t)(cs.w.x - p.tq0) * T + ty * TM + a].w;
         }
         const int s = (int)(g % NSTAGE);
-        mbar_wait(&full[s], (uint32_t)(g / NSTAGE) & 1u);
-        const int klen = Kpad - cs.c * KC < KC ? Kpad - cs.c * KC : KC;
+        if (PROF) {  // wait-time instrumentation (KGC_GT_PROF=1): by chunk kind
+            const long long t0 = clock64();
+            mbar_wait(&full[s], (uint32_t)(g / NSTAGE) & 1u);
+            const long long t1 = clock64(), dt = t1 - t0;
+            const int kind = cs.c != 0 ? 2 : (cs.j == cs.w.y ? 0 : 1);  // item start / block start / other
+            if (lane == 0) {
+                atomicAdd(p.prof + 2 * kind, (unsigned long long)dt);
+                atomicAdd(p.prof + 2 * kind + 1, 1ull);
+                if (g >= NSTAGE && dt > 200) {  // waited: issue -> ready latency
+                    atomicAdd(p.prof + 8, (unsigned long long)(t1 - issued_at[s]));
+                    atomicAdd(p.prof + 9, 1ull);
+                }
+            }
+        } else {
+            mbar_wait(&full[s], (uint32_t)(g / NSTAGE) & 1u);
+        }
+        const int klen = chunk_len(cs.c);
         const float* qk = St + (size_t)s * STAGE + ty * TM;
         const float* tk = St + (size_t)s * STAGE + KC * T + tx * LD;
-#pragma unroll 1
+#pragma unroll KUN
         for (int k4 = 0; k4 < klen; k4 += 4) {
             float4 tv[TN];
 #pragma unroll
@@ -568,15 +589,28 @@ __global__ void __launch_bounds__(64, 8) tiles_gather_kernel(TileParams p) {
                     }
             }
         }
-        // The last warp to finish reading stage s refills it with chunk g + NSTAGE.
+        // Refill duty alternates with the chunk: warp (g & 1) refills stage s with chunk
+        // g + NSTAGE once the other warp has released it (empty[s]); the other warp just
+        // releases.  (A fixed "last releaser refills" rule made the refilling warp the
+        // slower one for good, and its partner then waited on every chunk.)
         __syncwarp();
         int last = 0;
-        if (lane == 0) {
-            __threadfence_block();
-            last = atomicAdd(&released[s], 1) == NT / 32 - 1;
-            if (last) released[s] = 0;
+        if (DUTY) {
+            const int warp = tid >> 5;
+            if (warp == (int)(g & 1)) {
+                mbar_wait(&empty[s], (uint32_t)(g / NSTAGE) & 1u);
+                last = 1;
+            } else if (lane == 0) {
+                mbar_arrive(&empty[s]);
+            }
+        } else {
+            if (lane == 0) {
+                __threadfence_block();
+                last = atomicAdd(&released[s], 1) == NT / 32 - 1;
+                if (last) released[s] = 0;
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
         }
-        last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
             It nx = cs;
 #pragma unroll 1
@@ -615,13 +649,19 @@ __global__ void __launch_bounds__(64, 8) tiles_gather_kernel(TileParams p) {
         }
         next(cs);
     }
+    if (PROF && lane == 0) {
+        atomicAdd(p.prof + 6, (unsigned long long)(clock64() - tstart));
+        atomicAdd(p.prof + 7, 1ull);
+    }
 }
 
-template <int NORM, int KC, int NS, int SWZ = 0>
+template <int NORM, int KC, int NS, int SWZ = 0, int DUTY = 1, int MINB = 8, int KUN = 1>
 static void launch_gather_variant(const TileParams& p, int num_sms, long long max_items, cudaStream_t s) {
     constexpr int T = SIMT_T;
     const size_t smem = (size_t)NS * (KC * T + T * (SWZ ? KC : KC + 4)) * 4 + 128 + T * 4;
-    auto kern = tiles_gather_kernel<NORM, KC, NS, SWZ>;
+    static_assert(NS * 20 <= 128, "barriers and counters fit the 128-byte tail");
+    auto kern = p.prof ? tiles_gather_kernel<NORM, KC, NS, SWZ, 1, DUTY, MINB, KUN>
+                       : tiles_gather_kernel<NORM, KC, NS, SWZ, 0, DUTY, MINB, KUN>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 64, smem);
@@ -634,18 +674,19 @@ static void launch_gather_variant(const TileParams& p, int num_sms, long long ma
 
 void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long max_items, cudaStream_t s) {
     if (max_items <= 0) return;
-    const char* e = getenv("KGC_GT_VAR");  // experiment knob: K-chunk / stage variants
+    const char* e = getenv("KGC_GT_VAR");  // experiment knob: chunk / stage / refill-protocol variants
     const int v = e ? atoi(e) : 0;
+    // measured on c2 L1 (tile-kernel ms, same session): KC 24 / 2 stages / alternating refill duty
+    // 4.83; KC 32 4.93-5.07; KC 16 4.95; KC 24 with "last releaser refills" 4.93; KC 32 swizzled
+    // 4.90; 3 stages 4.98-5.54; k-loop unrolled x2 at 6 CTAs/SM 4.99
     if (norm == 1) {
-        // measured on c2 L1 (gathered-tail tiles ms): 32/2 padded 4.85, 32/2 swizzled 4.90,
-        // 24/2 5.20, 16/3 5.47, 32/3 swizzled 5.54
-        if (v == 1) launch_gather_variant<1, 24, 2>(p, num_sms, max_items, s);
-        else if (v == 2) launch_gather_variant<1, 16, 3>(p, num_sms, max_items, s);
+        if (v == 1) launch_gather_variant<1, 32, 2>(p, num_sms, max_items, s);
+        else if (v == 2) launch_gather_variant<1, 16, 2>(p, num_sms, max_items, s);
         else if (v == 3) launch_gather_variant<1, 32, 2, 1>(p, num_sms, max_items, s);
-        else if (v == 4) launch_gather_variant<1, 32, 3, 1>(p, num_sms, max_items, s);
-        else launch_gather_variant<1, 32, 2>(p, num_sms, max_items, s);
+        else if (v == 4) launch_gather_variant<1, 24, 2, 0, 0>(p, num_sms, max_items, s);
+        else launch_gather_variant<1, 24, 2>(p, num_sms, max_items, s);
     } else {
-        launch_gather_variant<2, 32, 2>(p, num_sms, max_items, s);
+        launch_gather_variant<2, 24, 2>(p, num_sms, max_items, s);
     }
 }
 
