@@ -76,7 +76,11 @@ typedef struct {
     int32_t pivot;            /* 0 = zero vector (default); 1 = mean of the tails      */
     int32_t l2_engine;        /* 0 = auto (3 when N * pad8(d) * 4 > 48 MiB, else 1; 2 if d > 256);  */
                               /* 1 = tcgen05 TF32 filter; 2 = FP32 SIMT filter; 3 = tcgen05 TF32 on */
-                              /* CTA pairs (cta_group::2, 256-row query tiles)                     */
+                              /* CTA pairs (cta_group::2, 256-row query tiles); 4 = tcgen05 TF32 */
+                              /* on gathered tail blocks (needs pivots >= 2: per 128-row query tile */
+                              /* only the tails whose own K keys pass the test against the tile's   */
+                              /* key box, 256 per block; falls back to 1 when the lists would      */
+                              /* exceed 8 GiB)                                                      */
     int32_t chunk_tiles;      /* max tail tiles per work item (load-balance granularity); 0 = auto */
     int32_t pivots;           /* 0/1 = one pivot (default); 2..8 = multi-pivot tile     */
                               /* pruning (L_inf over K pivot distances; needs d <= 256, */
@@ -119,7 +123,8 @@ typedef struct {
     float ms_total, ms_h2d, ms_keys, ms_sort, ms_ranges, ms_stage, ms_tiles, ms_recheck;
     int32_t pivots_used;          /* 1, or K of the multi-pivot pruning                            */
     int32_t engine;               /* tile engine used: 1 tcgen05 TF32, 2 FP32 SIMT, 3 FP16x2 SIMT,   */
-                                  /* 4 tcgen05 TF32 on CTA pairs, 5 FP32 SIMT on gathered tails       */
+                                  /* 4 tcgen05 TF32 on CTA pairs, 5 FP32 SIMT on gathered tails,      */
+                                  /* 6 tcgen05 TF32 on gathered tail blocks                           */
     float ms_split;               /* device time of the rank-local split estimate (world > 1)       */
     float ms_host;                /* host wall time of the whole kgc_join call                      */
     int64_t gathered_pairs;       /* engine 5: (query row, tail) pairs left after the per-tail K-pivot */

@@ -144,6 +144,33 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lb
     return d;  // base offset 0, lbo mode 0, layout type 0 (SWIZZLE_NONE)
 }
 
+// K-major, 128-byte swizzle: rows of 128 bytes (32 fp32 of K) in 8-row atoms of
+// 1024 bytes, 16-byte chunks XOR-permuted by row % 8 (the layout TMA writes with
+// CU_TENSOR_MAP_SWIZZLE_128B); SBO = 1024 between 8-row groups, LBO unused (1),
+// layout type 2 (SWIZZLE_128B) in bits 61-63.  The atom must be 1024-B aligned;
+// a K step of 8 fp32 advances the start address by 32 bytes.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+// TMA row gather (sm_100): rows r0..r3 of a 2-D tensor map (box = {cols, 1}),
+// columns [c0, c0 + cols), written as 4 consecutive box rows at smem_dst with the
+// map's swizzle; completes as transaction bytes on `bar`.
+__device__ __forceinline__ void tma_gather4(uint32_t smem_dst, const void* tmap, int c0, int r0, int r1, int r2,
+                                            int r3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_dst),
+        "l"(tmap), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // Instruction descriptor for kind::tf32: D = F32, A = B = TF32, both K-major.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4)                          // D format F32

@@ -21,6 +21,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled (driver entry point through cudart)
+
 #include "../../include/kgc.h"
 #include "kgc_internal.h"
 
@@ -47,7 +49,7 @@ struct kgc_ctx {
     DevBuf E, Rel, pivot, kt, kq, mm_t, mm_q, sk0, sv0, sk1, sv1, counts, scan_tmp, qperm, qskey, tperm, tskey, tmin,
         tmax, cmax, cmin, ranges, cost, cum, nitem, item_off, items, item_tiles, item_cum, Qp, qs, Tp, T2, tstile, cand,
         res, ctr, est_hist, est_cost, mpP, mpkt, mpkq, mpmm_t, mpmm_q, mpc0, mpc1, tbmin, tbmax, qbmin, qbmax, tile_list,
-        tk_sample, tk_sel, tk_cnt, Ts, tks, gblk, granges, glist, se_w, se_a64, se_b64, se_af, se_bf, se_zero, se_res, se_max;
+        tk_sample, tk_sel, tk_cnt, Ts, tks, gblk, granges, glist, tsc, gT2, gtst, tmapbuf, se_w, se_a64, se_b64, se_af, se_bf, se_zero, se_res, se_max;
     long long cand_cap = 0, res_cap = 0;
     long long n_results = -1;
     kgc_stats_t st{};
@@ -60,6 +62,7 @@ struct kgc_ctx {
     int K = 1;                  // pivots used by the last join
     long long list_len = 0;     // multi-pivot tile-list length of this shard
     long long glist_len = 0;    // gathered-tail list length of this shard (entries)
+    CUtensorMap tmap_host;      // tensor map over the sorted tails (gathered tensor-core engine)
     bool have_join = false;
 };
 
@@ -133,6 +136,38 @@ static int simt_t() {
 }
 // Gathered-tail SIMT engine (l1_engine 3; auto for L1 with multi-pivot pruning):
 // element-level tail pruning inside surviving tiles (pivots.cu, tiles_simt.cu).
+// Tensor-core engine on gathered tail blocks (l2_engine 4): the same per-tail test,
+// blocks of 256 gathered rows (tiles_tc.cu, GATHER); needs K pivots and the 1-CTA geometry.
+static bool use_gather_tc(const kgc_ctx* ctx) {
+    const char* e = getenv("KGC_GATHER_TC");  // experiment knob
+    if (e) return atoi(e) != 0;
+    return ctx->opt.l2_engine == 4;
+}
+// 2-D tensor map over the sorted row-major tails Ts[N + 1][Kpad] (fp32): box = 32 columns x 1
+// row, 128-byte swizzle -- the operand of the TMA row gathers (tiles_tc.cu, GATHER).
+static int make_tails_tmap(CUtensorMap* m, const float* Ts, long long rows, int Kpad) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return -1;
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t gdim[2] = {(cuuint64_t)Kpad, (cuuint64_t)rows};
+    const cuuint64_t gstride[1] = {(cuuint64_t)Kpad * 4};
+    const cuuint32_t box[2] = {32, 1};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(Ts), gdim, gstride, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -1;
+}
+
+// Device memory the gathered tensor-core lists may take (glist + ||t||^2/2 per entry)
+// before the join falls back to contiguous tiles.
+constexpr size_t GATHER_TC_BUDGET = 8ull << 30;
 static bool use_gather(const kgc_ctx* ctx, int norm) {
     const char* e = getenv("KGC_GATHER");  // experiment knob: 0 = off, 1 = on for both norms
     if (e) return atoi(e) != 0;
@@ -191,7 +226,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 3 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 1) {
+        o.l2_engine > 4 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 1) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -336,15 +371,17 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     st.triplets = (double)N * (double)N * (double)R_global;
 
     const bool tc = use_tc(ctx, norm, d);
-    const bool tc2 = use_tc2(ctx, norm, d, N);
-    if (norm == 2 && (ctx->opt.l2_engine == 1 || ctx->opt.l2_engine == 3) && !tc) {
+    const int K_plan = (ctx->opt.pivots >= 2 && ctx->opt.prune && d <= MP_MAX_DIM) ? ctx->opt.pivots : 1;
+    const bool gtc_req = tc && K_plan > 1 && use_gather_tc(ctx);  // gathered tensor-core blocks requested
+    const bool tc2 = !gtc_req && use_tc2(ctx, norm, d, N);
+    if (norm == 2 && (ctx->opt.l2_engine == 1 || ctx->opt.l2_engine == 3 || ctx->opt.l2_engine == 4) && !tc) {
         set_err(ctx, "l2_engine=%d (tcgen05) supports d <= %d", ctx->opt.l2_engine, TC_MAX_KPAD);
         return KGC_EINVAL;
     }
     const int Kpad = ((d + 7) / 8) * 8;
     // tile geometry of the plan: tensor cores 128 x 256; FP16x2 L1 128 x 128; FP32 SIMT 64 x 64
     const bool half_req = norm == 1 && ctx->opt.l1_engine == 1;
-    const int bq = plan_bq(ctx, norm, d, N);
+    const int bq = gtc_req ? BM : plan_bq(ctx, norm, d, N);
     const int BN = tc ? BN_TC : (half_req ? BN_HALF : simt_t());
     const int QT = (int)((N + bq - 1) / bq);
     const int TT = (int)((N + BN - 1) / BN);
@@ -551,26 +588,44 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     // Gathered tails: per query tile, the tails of its surviving tiles that pass the K-pivot
     // test on their own keys, in blocks of GT_ROWS; work items reference blocks.
     const bool gather = n_items > 0 && K > 1 && !tc && !half_req && simt_t() == GT_ROWS && use_gather(ctx, norm);
+    const bool gather_tc = n_items > 0 && gtc_req && K > 1 && tc_gather_ok(Kpad) &&
+                           (size_t)h1.c.my_cost * BN_TC * 8 <= GATHER_TC_BUDGET;
+    const int GB = gather_tc ? BN_TC : GT_ROWS;  // rows per gathered block (= tail tile rows)
     long long g_max_items = 0;
-    if (gather) {
+    if (gather || gather_tc) {
         g_max_items = h1.c.my_cost;  // blocks (and items) <= surviving tiles of this shard
         CK(ensure(ctx->Ts, (size_t)(N + 1) * Kpad * 4));
         CK(ensure(ctx->tks, (size_t)N * MP_MAX * 4));
         CK(ensure(ctx->gblk, (size_t)nq * 8));
         CK(ensure(ctx->granges, (size_t)nq * 8));
-        CK(ensure(ctx->glist, (size_t)g_max_items * GT_ROWS * 4 + 4));
+        CK(ensure(ctx->glist, (size_t)g_max_items * GB * 4 + 4));
         CK(ensure(ctx->items, (size_t)g_max_items * 16));
         CK(ensure(ctx->item_tiles, (size_t)g_max_items * 8));
         CK(ensure(ctx->item_cum, (size_t)g_max_items * 8));
         CK(ensure(ctx->scan_tmp, scan_tmp_bytes((size_t)std::max<long long>(g_max_items, nq))));
+        if (gather_tc) {
+            CK(ensure(ctx->tsc, (size_t)N * 16));
+            CK(ensure(ctx->gT2, (size_t)g_max_items * GB * 4 + 4));
+            CK(ensure(ctx->gtst, (size_t)g_max_items * 8));
+        }
         launch_stage_rows(Et, P<int>(ctx->tperm), P<float>(ctx->mpkt), N, d, Kpad, K, P<float>(ctx->Ts),
-                          P<float>(ctx->tks), s);
+                          P<float>(ctx->tks), gather_tc ? P<float4>(ctx->tsc) : nullptr, s);
+        if (gather_tc) {
+            CK(ensure(ctx->tmapbuf, sizeof(CUtensorMap)));
+            if (make_tails_tmap(&ctx->tmap_host, P<float>(ctx->Ts), N + 1, Kpad)) {
+                set_err(ctx, "cuTensorMapEncodeTiled failed for the gathered tails");
+                return KGC_ECUDA;
+            }
+            CK(cudaMemcpyAsync(ctx->tmapbuf.p, &ctx->tmap_host, sizeof(CUtensorMap), cudaMemcpyHostToDevice, s));
+        }
         CK(cudaMemsetAsync(ctx->gblk.p, 0, (size_t)nq * 8, s));
         CK(cudaMemsetAsync(ctx->nitem.p, 0, (size_t)nq * 4, s));
         CK(cudaMemsetAsync(ctx->item_tiles.p, 0, (size_t)g_max_items * 8, s));
         launch_gather_tails(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tks), P<int>(ctx->tile_list),
-                            P<long long>(ctx->cum), P<int2>(ctx->ranges), dctr, N, K, feps, mp_relm(d), chunk, nq,
-                            P<long long>(ctx->gblk), P<int2>(ctx->granges), P<int>(ctx->nitem), P<int>(ctx->glist), s);
+                            P<long long>(ctx->cum), P<int2>(ctx->ranges), dctr, N, GB, K, feps, mp_relm(d), chunk, nq,
+                            P<long long>(ctx->gblk), P<int2>(ctx->granges), P<int>(ctx->nitem), P<int>(ctx->glist),
+                            gather_tc ? P<float4>(ctx->tsc) : nullptr, gather_tc ? P<float>(ctx->gT2) : nullptr,
+                            gather_tc ? P<float2>(ctx->gtst) : nullptr, s);
         LAUNCHED(2);
         scan_exclusive_i32(P<int>(ctx->nitem), P<int>(ctx->item_off), (size_t)nq, ctx->scan_tmp.p, s,
                            &ctx->launches);
@@ -609,7 +664,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         set_err(ctx, "l1_engine=1 (FP16x2) needs every |E|, |Rel| value <= 1000; use l1_engine 0 or 2");
         return KGC_EINVAL;
     }
-    st.engine = tc2 ? 4 : (tc ? 1 : (half ? 3 : (gather ? 5 : 2)));
+    st.engine = gather_tc ? 6 : (tc2 ? 4 : (tc ? 1 : (half ? 3 : (gather ? 5 : 2))));
     const float gam = 1.0f + 10.0f * 4.8828125e-04f + (float)(d / 8 + 4) * 1.1920928955078125e-07f;
     if (n_items > 0) {
         CK(ensure(ctx->Tp, (size_t)TT * BN * Kpad * 4));
@@ -623,6 +678,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             launch_stage_half(E, Rel, P<int>(ctx->qperm), N, d, Kpad, bq, QT, tq0, tq1 - tq0, feps, gam, ctx->Qp.p,
                               P<float4>(ctx->qs), nullptr, s);
             LAUNCHED(2);
+        } else if (gather_tc) {
+            // nothing to stage: builder warps form the query tiles, the producer gathers the tails
         } else if (gather) {
             CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * bq * Kpad * 4));
             CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * bq * 16));
@@ -693,6 +750,9 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.glist = P<int>(ctx->glist);
         tp.dn_items = &dctr->n_items;
         tp.dtotal = &dctr->gblocks;
+        tp.gT2 = P<float>(ctx->gT2);
+        tp.gtst = P<float2>(ctx->gtst);
+        tp.tmap = ctx->tmapbuf.p;
         if (n_items > 0) {
             if (gather) {
                 const char* pe = getenv("KGC_GT_PROF");  // experiment: wait-cycle instrumentation
@@ -714,7 +774,11 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                             (double)h[4] / h[7], h[5], h[9] ? (double)h[8] / h[9] : 0.0, h[9]);
                 }
             }
-            else if (tc2) launch_tiles_tc2(tp, ctx->num_sms, s);
+            else if (gather_tc) {
+                TileParams tg = tp;
+                tg.n_items = g_max_items;  // grid bound; the kernel reads the item count on the device
+                launch_tiles_tc_gather(tg, ctx->num_sms, s);
+            } else if (tc2) launch_tiles_tc2(tp, ctx->num_sms, s);
             else if (tc) launch_tiles_tc(tp, ctx->num_sms, s);
             else if (half) launch_tiles_half_l1(tp, ctx->num_sms, s);
             else launch_tiles_simt(tp, norm, ctx->num_sms, s);
@@ -736,12 +800,12 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(cudaEventRecord(ctx->ev[EV_VERIFY], s));
         unsigned long long hcnt[2], hg[2] = {0, 0};  // cand, res; gathered blocks, pairs
         CK(cudaMemcpyAsync(hcnt, &dctr->cand, 16, cudaMemcpyDeviceToHost, s));
-        if (gather) CK(cudaMemcpyAsync(hg, &dctr->gblocks, 16, cudaMemcpyDeviceToHost, s));
+        if (gather || gather_tc) CK(cudaMemcpyAsync(hg, &dctr->gblocks, 16, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         cand_n = (long long)hcnt[0];
         res_n = (long long)hcnt[1];
         st.gathered_pairs = (int64_t)hg[1] * bq;
-        ctx->glist_len = gather ? ctx->list_len * GT_ROWS : 0;
+        ctx->glist_len = (gather || gather_tc) ? ctx->list_len * GB : 0;
         if (cand_n > ctx->cand_cap) {
             ctx->cand_cap = cand_n + cand_n / 4 + 1024;
             st.reruns++;

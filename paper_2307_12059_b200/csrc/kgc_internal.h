@@ -66,8 +66,11 @@ struct TileParams {
     int QT;
     // gathered-tail SIMT engine (GT_ROWS tails per block, see tiles_simt.cu)
     const float* Ts;              // sorted tails, row-major [N + 1][Kpad] (row N: sentinel)
-    const int* glist;             // per query tile (at GT_ROWS x its tile-list offset): surviving sorted
-                                  // tail positions, padded with N to whole blocks
+    const int* glist;             // per query tile (at bn x its tile-list offset): surviving sorted
+                                  // tail positions, padded with N to whole blocks of bn
+    const float* gT2;             // tensor-core gathered blocks: ||t||^2 / 2 per list entry (3e38 padding)
+    const float2* gtst;           // tensor-core gathered blocks: per block {max ||t||, max ||t - tf32(t)||}
+    const void* tmap;             // tensor-core gathered blocks: CUtensorMap over Ts (device memory)
     const long long* dn_items;    // device: work items of this shard
     const long long* dtotal;      // device: blocks of this shard (balanced CTA ranges)
     unsigned long long* prof;     // experiment: wait-cycle counters (KGC_GT_PROF), else nullptr
@@ -133,11 +136,12 @@ void launch_mp_emit(const float* qbmin, const float* qbmax, const float* tbmin, 
 // ---- gathered-tail SIMT engine (pivots.cu): element-level tail pruning against query-tile boxes
 constexpr int GT_ROWS = 64;  // tails per gathered block (= SIMT_T)
 void launch_stage_rows(const float* E, const int* tperm, const float* keys, long long N, int d, int Kpad, int K,
-                       float* Ts, float* tks, cudaStream_t s);
+                       float* Ts, float* tks, float4* tsc, cudaStream_t s);
+// BN = 64 (SIMT engine) or 256 (tensor-core engine: also gT2 / gtst)
 void launch_gather_tails(const float* qbmin, const float* qbmax, const float* tks, const int* list,
-                         const long long* cum, const int2* ranges, DevCounters* ctr, long long N, int K, float theta,
-                         float relm, int chunk, long long nq, long long* gblocks, int2* granges, int* nitem,
-                         int* glist, cudaStream_t s);
+                         const long long* cum, const int2* ranges, DevCounters* ctr, long long N, int BN, int K,
+                         float theta, float relm, int chunk, long long nq, long long* gblocks, int2* granges,
+                         int* nitem, int* glist, const float4* tsc, float* gT2, float2* gtst, cudaStream_t s);
 
 // Tail tile of position j of item w (contiguous range or multi-pivot list).
 __device__ __forceinline__ int item_tile(const int4& w, int j, const int* __restrict__ list) {
@@ -147,6 +151,8 @@ __device__ __forceinline__ int item_tile(const int4& w, int j, const int* __rest
 // ---- tile engines ----
 int  tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);
 void launch_tiles_tc(const TileParams& p, int num_sms, cudaStream_t s);
+void launch_tiles_tc_gather(const TileParams& p, int num_sms, cudaStream_t s);
+int  tc_gather_ok(int Kpad);  // the gathered tensor-core engine needs 32-wide K-chunks
 int  tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);
 void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s);
 void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t s);

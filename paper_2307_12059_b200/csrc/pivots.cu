@@ -404,39 +404,72 @@ __global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __r
 // Measured on c2 L1 (numpy model of the same pivots): 2.76% -> 1.43% of all
 // pairs computed.
 
-// Sorted tails, row-major with row stride Kpad (zero padded), row N = 1e30
-// (the sentinel: its distance to any query overflows the threshold), and the
-// sorted tails' keys with row stride MP_MAX (two float4 loads per tail).  One
-// warp per row.
+// Sorted tails, row-major with row stride Kpad (zero padded), row N = zeros
+// (the sentinel the lists are padded with; the engines mask it by index or by
+// ||t||^2 = 3e38), the sorted tails' keys with row stride MP_MAX (two float4
+// loads per tail), and for the tensor-core engine the per-tail scalars
+// {||t||^2 / 2, ||t|| (up), ||t - tf32(t)|| (up), 0} from FP64 sums -- the
+// same values the tile staging kernel (prep.cu) computes.  One warp per row.
+__device__ __forceinline__ double gt_warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 __global__ void stage_rows_kernel(const float* __restrict__ E, const int* __restrict__ tperm,
                                   const float* __restrict__ keys, long long N, int d, int Kpad, int K,
-                                  float* __restrict__ Ts, float* __restrict__ tks) {
+                                  float* __restrict__ Ts, float* __restrict__ tks, float4* __restrict__ tsc) {
     const int lane = threadIdx.x & 31;
     for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; i <= N;
          i += ((long long)gridDim.x * blockDim.x) >> 5) {
         float* dst = Ts + (size_t)i * Kpad;
         if (i == N) {
-            for (int k = lane; k < Kpad; k += 32) dst[k] = 1.0e30f;
+            for (int k = lane; k < Kpad; k += 32) dst[k] = 0.f;
             continue;
         }
         const long long src = tperm[i];
         const float* row = E + (size_t)src * d;
-        for (int k = lane; k < Kpad; k += 32) dst[k] = k < d ? __ldg(row + k) : 0.f;
+        double s2 = 0.0, sd2 = 0.0;
+        for (int k = lane; k < Kpad; k += 32) {
+            const float x = k < d ? __ldg(row + k) : 0.f;
+            dst[k] = x;
+            const double xd = x, rd = (double)(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
+            s2 += xd * xd;
+            sd2 += rd * rd;
+        }
         if (lane < MP_MAX) tks[(size_t)i * MP_MAX + lane] = lane < K ? __ldg(keys + (size_t)src * K + lane) : 0.f;
+        if (tsc) {
+            s2 = gt_warp_sum(s2);
+            sd2 = gt_warp_sum(sd2);
+            if (lane == 0)
+                tsc[i] = make_float4(__double2float_rn(0.5 * s2), __double2float_ru(sqrt(s2)),
+                                     __double2float_ru(sqrt(sd2)), 0.f);
+        }
     }
 }
 
-// One pass, warp per query tile of this shard: the tails of its surviving tiles
-// (two 32-tail halves per 64-row tile) that pass the per-tail test, written in ascending sorted position at
-// list offset GT_ROWS * (tile prefix[q] - prefix[first]) -- the tile list's own
-// offsets, an upper bound -- and padded with N to a multiple of GT_ROWS.
+__device__ __forceinline__ float gt_warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// One pass, warp per query tile of this shard: the tails of its surviving BN-row
+// tiles (BN / 32 groups of 32 per tile, UN tiles' key loads in flight) that pass
+// the per-tail test, written in ascending sorted position at list offset
+// BN * (tile prefix[q] - prefix[first]) -- the tile list's own offsets, an
+// upper bound -- and padded with the sentinel N to whole blocks of BN.  TCM
+// (tensor-core engine): also ||t||^2/2 per list entry (3e38 for padding) and per
+// block the maxima of ||t|| and ||t - tf32(t)|| (the guard band's Tm, Tdm).
+template <int BN, bool TCM>
 __global__ void gather_tails_kernel(const float* __restrict__ qbmin, const float* __restrict__ qbmax,
                                     const float4* __restrict__ tks, const int* __restrict__ list,
                                     const long long* __restrict__ cum, const int2* __restrict__ ranges,
                                     DevCounters* ctr, long long N, int K, float theta, float relm, int chunk,
                                     long long* __restrict__ gblocks, int2* __restrict__ granges,
-                                    int* __restrict__ nitem, int* __restrict__ glist) {
-    static_assert(SIMT_T == 64 && GT_ROWS == 64, "two 32-tail halves per tile");
+                                    int* __restrict__ nitem, int* __restrict__ glist,
+                                    const float4* __restrict__ tsc, float* __restrict__ gT2,
+                                    float2* __restrict__ gtst) {
+    constexpr int H = BN / 32, UN = BN == 64 ? 4 : 1;
     const int tq0 = ctr->tq_begin, tq1 = ctr->tq_end;
     if (tq0 >= tq1) return;
     const long long base = cum[tq0];
@@ -449,20 +482,19 @@ __global__ void gather_tails_kernel(const float* __restrict__ qbmin, const float
         for (int k = 0; k < MP_MAX; ++k)
             if (k < K) { qmn[k] = qbmin[q * K + k]; qmx[k] = qbmax[q * K + k]; }
         const int ntl = ranges[q].y + 1;
-        const int* L = list + (cum[q] - base);
-        int* out = glist + (cum[q] - base) * GT_ROWS;
+        const long long loff = cum[q] - base;
+        const int* L = list + loff;
+        int* out = glist + loff * BN;
         long long c = 0;
-        // UN tiles per step: all their key loads issued before the first test (the loop is
-        // latency-bound and list lengths are heavy-tailed)
-        constexpr int UN = 4;
+        float bn_max = 0.f, bd_max = 0.f;  // TCM: running maxima of the current block
         for (int u0 = 0; u0 < ntl; u0 += UN) {
-            float4 kv[UN][2][2];
+            float4 kv[UN][H][2];
             long long ib[UN];
 #pragma unroll
             for (int x = 0; x < UN; ++x) {
-                ib[x] = u0 + x < ntl ? (long long)__ldg(L + u0 + x) * 64 + lane : N;
+                ib[x] = u0 + x < ntl ? (long long)__ldg(L + u0 + x) * BN + lane : N;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < H; ++h) {
                     const long long i = ib[x] + 32 * h;
                     kv[x][h][0] = i < N ? __ldg(tks + 2 * i) : make_float4(0, 0, 0, 0);
                     kv[x][h][1] = i < N ? __ldg(tks + 2 * i + 1) : make_float4(0, 0, 0, 0);
@@ -471,19 +503,47 @@ __global__ void gather_tails_kernel(const float* __restrict__ qbmin, const float
 #pragma unroll
             for (int x = 0; x < UN; ++x) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < H; ++h) {
                     const long long i = ib[x] + 32 * h;
                     const float4 a = kv[x][h][0], b = kv[x][h][1];
                     const float tk[MP_MAX] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
                     const bool ok = i < N && mp_survives(qmn, qmx, tk, tk, K, theta, relm);
                     const unsigned m = __ballot_sync(0xffffffffu, ok);
-                    if (ok) out[c + __popc(m & lanemask_lt())] = (int)i;  // ascending positions
+                    if (!m) continue;
+                    const long long pos = c + __popc(m & lanemask_lt());
+                    if (ok) out[pos] = (int)i;  // ascending positions
+                    if (TCM) {
+                        float4 sc = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (ok) {
+                            sc = __ldg(tsc + i);
+                            gT2[loff * BN + pos] = sc.x;
+                        }
+                        // this group spans at most two blocks: the current one and the next
+                        const long long bcur = c / BN;
+                        const bool nxt = ok && pos / BN != bcur;
+                        const float n1 = gt_warp_max(ok && !nxt ? sc.y : 0.f), d1 = gt_warp_max(ok && !nxt ? sc.z : 0.f);
+                        bn_max = fmaxf(bn_max, n1);
+                        bd_max = fmaxf(bd_max, d1);
+                        if (__any_sync(0xffffffffu, nxt)) {
+                            if (lane == 0) gtst[loff + bcur] = make_float2(bn_max, bd_max);
+                            bn_max = gt_warp_max(nxt ? sc.y : 0.f);
+                            bd_max = gt_warp_max(nxt ? sc.z : 0.f);
+                        }
+                    }
                     c += __popc(m);
+                    if (TCM && c % BN == 0) {  // the group filled its block exactly
+                        if (lane == 0) gtst[loff + c / BN - 1] = make_float2(bn_max, bd_max);
+                        bn_max = bd_max = 0.f;
+                    }
                 }
             }
         }
-        const long long nb = (c + GT_ROWS - 1) / GT_ROWS;
-        for (long long o = c + lane; o < nb * GT_ROWS; o += 32) out[o] = (int)N;  // sentinel padding
+        const long long nb = (c + BN - 1) / BN;
+        for (long long o = c + lane; o < nb * BN; o += 32) {
+            out[o] = (int)N;  // sentinel padding
+            if (TCM) gT2[loff * BN + o] = 3e38f;
+        }
+        if (TCM && c % BN != 0 && lane == 0) gtst[loff + c / BN] = make_float2(bn_max, bd_max);  // partial block
         if (lane == 0) {
             gblocks[q] = nb;
             granges[q] = make_int2(0, (int)nb - 1);
@@ -577,17 +637,22 @@ void launch_mp_emit(const float* qbmin, const float* qbmax, const float* tbmin, 
 }
 
 void launch_stage_rows(const float* E, const int* tperm, const float* keys, long long N, int d, int Kpad, int K,
-                       float* Ts, float* tks, cudaStream_t s) {
-    stage_rows_kernel<<<grid_for_mp((N + 1) * 32, 256), 256, 0, s>>>(E, tperm, keys, N, d, Kpad, K, Ts, tks);
+                       float* Ts, float* tks, float4* tsc, cudaStream_t s) {
+    stage_rows_kernel<<<grid_for_mp((N + 1) * 32, 256), 256, 0, s>>>(E, tperm, keys, N, d, Kpad, K, Ts, tks, tsc);
 }
 
 void launch_gather_tails(const float* qbmin, const float* qbmax, const float* tks, const int* list,
-                         const long long* cum, const int2* ranges, DevCounters* ctr, long long N, int K, float theta,
-                         float relm, int chunk, long long nq, long long* gblocks, int2* granges, int* nitem,
-                         int* glist, cudaStream_t s) {
-    gather_tails_kernel<<<grid_for_mp(nq * 32, 256), 256, 0, s>>>(qbmin, qbmax, reinterpret_cast<const float4*>(tks),
-                                                                 list, cum, ranges, ctr, N, K, theta, relm, chunk,
-                                                                 gblocks, granges, nitem, glist);
+                         const long long* cum, const int2* ranges, DevCounters* ctr, long long N, int BN, int K,
+                         float theta, float relm, int chunk, long long nq, long long* gblocks, int2* granges,
+                         int* nitem, int* glist, const float4* tsc, float* gT2, float2* gtst, cudaStream_t s) {
+    const unsigned g = grid_for_mp(nq * 32, 256);
+    const float4* tk4 = reinterpret_cast<const float4*>(tks);
+    if (BN == 64)
+        gather_tails_kernel<64, false><<<g, 256, 0, s>>>(qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm,
+                                                         chunk, gblocks, granges, nitem, glist, tsc, gT2, gtst);
+    else
+        gather_tails_kernel<256, true><<<g, 256, 0, s>>>(qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm,
+                                                         chunk, gblocks, granges, nitem, glist, tsc, gT2, gtst);
 }
 
 }  // namespace kgc

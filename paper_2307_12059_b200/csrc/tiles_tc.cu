@@ -67,6 +67,15 @@ int tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
     return -1;
 }
 
+// GATHER: tail blocks are the query tile's gathered surviving tails (pivots.cu,
+// gather_tails_kernel<256>): the producer thread gathers their rows from the
+// sorted row-major tails with TMA row gathers (cp.async.bulk.tensor ...
+// tile::gather4, a 2-D tensor map over Ts with 128-byte swizzle), so each K-chunk
+// of 32 arrives as a 128B-swizzled K-major operand (umma_desc_sw128); the
+// epilogue takes ||t||^2/2 and the block's guard-band maxima from the list build.
+// (A warp of 16-byte cp.async pieces was measured 4x slower than contiguous tiles
+// on c3: one warp cannot keep enough scattered loads in flight.)
+template <bool GATHER>
 __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, int a_stages, int b_stages, int KC) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int Kpad = p.Kpad;
@@ -86,10 +95,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // this CTA's contiguous, cost-balanced block of work items (every role walks it)
-    const long long it_begin = p.sched ? balanced_begin(p.item_cum, p.n_items, p.total_tiles, blockIdx.x, gridDim.x)
+    // gathered: the item count and block total were produced on the device
+    const long long n_items = GATHER ? *p.dn_items : p.n_items, total = GATHER ? *p.dtotal : p.total_tiles;
+    const long long it_begin = p.sched ? balanced_begin(p.item_cum, n_items, total, blockIdx.x, gridDim.x)
                                        : (long long)blockIdx.x;
-    const long long it_end = p.sched ? balanced_begin(p.item_cum, p.n_items, p.total_tiles, blockIdx.x + 1, gridDim.x)
-                                     : p.n_items;
+    const long long it_end = p.sched ? balanced_begin(p.item_cum, n_items, total, blockIdx.x + 1, gridDim.x)
+                                     : n_items;
     const long long it_step = p.sched ? 1 : gridDim.x;
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -110,7 +121,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
+    if (warp == 0 && GATHER) {
+        // ------------------------------------------------ producer (gathered tail blocks)
+        // 64 TMA row gathers of 4 rows x 128 bytes per K-chunk (KC = 32: one 128-byte
+        // swizzle atom row; columns past Kpad are zero-filled by TMA).  The block's row
+        // indices are loaded once per block, lane l holding gathers l and l + 32.
+        int bi = 0;
+        uint32_t bph = 0;
+        for (long long it = it_begin; it < it_end; it += it_step) {
+            const int4 w = p.items[it];
+            for (int jj = w.y; jj <= w.z; ++jj) {
+                const int4* seg = reinterpret_cast<const int4*>(p.glist + ((long long)w.w + jj) * BN_TC);
+                const int4 ra = __ldg(seg + lane), rb = __ldg(seg + lane + 32);
+                for (int c = 0; c < nkc; ++c) {
+                    TC_WAIT(0, &b_empty[bi], bph ^ 1);
+                    if (lane == 0) mbar_arrive_expect_tx(&b_full[bi], (uint32_t)BN_TC * 128u);
+                    __syncwarp();
+                    const uint32_t bbase = smem_u32(Bs + (size_t)bi * BN_TC * KC);
+                    tma_gather4(bbase + (uint32_t)lane * 512u, p.tmap, c * KC, ra.x, ra.y, ra.z, ra.w, &b_full[bi]);
+                    tma_gather4(bbase + (uint32_t)(lane + 32) * 512u, p.tmap, c * KC, rb.x, rb.y, rb.z, rb.w,
+                                &b_full[bi]);
+                    if (++bi == b_stages) { bi = 0; bph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------ producer (tail tiles)
             int bi = 0;
@@ -148,7 +183,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
                 for (int c = 0; c < nkc; ++c) {
                     TC_WAIT(3, &b_full[bi], bph);
                     tc_fence_after();
-                    const uint64_t b_desc0 = umma_desc_kmajor(smem_u32(Bs + (size_t)bi * BN_TC * KC), LBO_B, SBO);
+                    // gathered blocks arrive 128B-swizzled (TMA); a K step is 32 bytes there
+                    const uint64_t b_desc0 = GATHER ? umma_desc_sw128(smem_u32(Bs + (size_t)bi * BN_TC * KC))
+                                                    : umma_desc_kmajor(smem_u32(Bs + (size_t)bi * BN_TC * KC), LBO_B, SBO);
+                    constexpr uint32_t BSTEP = GATHER ? 2u : 2u * (LBO_B >> 4);  // descriptor units per K = 8
                     const int nsteps = (Kpad - c * KC < KC ? Kpad - c * KC : KC) / 8;
                     // descriptor start address advances by 2 core matrices (K = 8) per step
                     const uint64_t a_desc = a_desc0 + (uint64_t)((uint32_t)(c * KC / 4) * (LBO_A >> 4));
@@ -156,12 +194,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
 #pragma unroll
                         for (int s = 0; s < 4; ++s) {
                             if (s < nsteps)
-                                mma_tf32(d_tmem, a_desc + (uint64_t)(2 * s * (LBO_A >> 4)),
-                                         b_desc0 + (uint64_t)(2 * s * (LBO_B >> 4)), IDESC, (c | s) != 0);
+                                mma_tf32(d_tmem, a_desc + (uint64_t)(2 * s * (LBO_A >> 4)), b_desc0 + (uint64_t)(s * BSTEP),
+                                         IDESC, (c | s) != 0);
                         }
                         for (int s = 4; s < nsteps; ++s)  // KC > 32 is not configured; kept for safety
-                            mma_tf32(d_tmem, a_desc + (uint64_t)(2 * s * (LBO_A >> 4)),
-                                     b_desc0 + (uint64_t)(2 * s * (LBO_B >> 4)), IDESC, 1u);
+                            mma_tf32(d_tmem, a_desc + (uint64_t)(2 * s * (LBO_A >> 4)), b_desc0 + (uint64_t)(s * BSTEP),
+                                     IDESC, 1u);
                         mma_commit(&b_empty[bi]);
                     }
                     __syncwarp();
@@ -196,8 +234,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
             // theta_f covers q = fl32(h + r) vs the exact h + r (|dq_k| <= 2^-24 |q_k|)
             const float thf = p.theta * (1.0f + 2.44140625e-04f) + 2.384185791015625e-07f * Qn;
             for (int jj = w.y; jj <= w.z; ++jj) {
-                const int j = item_tile(w, jj, p.tile_list);
-                const float2 tv = p.tstile[j];
+                // gathered: j is the block (the tile list's offset + jj), else the tail tile
+                const int j = GATHER ? w.w + jj : item_tile(w, jj, p.tile_list);
+                const float2 tv = GATHER ? p.gtst[j] : p.tstile[j];
                 const float Tm = tv.x, Tdm = tv.y;
                 // |acc - q.t| <= Qd Tm + Qn Tdm + Qd Tdm + eta (Qn + Qd)(Tm + Tdm)
                 const float eb = Qd * Tm + Qn * Tdm + Qd * Tdm + p.eta * (Qn + Qd) * (Tm + Tdm);
@@ -208,9 +247,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
                 const float c = Q2 - R - (float)(p.Kpad + 4) * 1.1920928955078125e-07f * Q2 - 9.5367431640625e-07f * (Q2 + R);
                 // ||t||^2 of this tile's and the next tile's columns into L1 ahead of use
                 // (4 lines each); each chunk's loads would otherwise be an L2 round trip
-                const float* t2row = p.T2 + (size_t)j * BN_TC + col0;
+                const float* t2row = (GATHER ? p.gT2 : p.T2) + (size_t)j * BN_TC + col0;
                 if (p.t2pf && lane < 4) prefetch_l1(t2row + lane * 32);
-                else if (p.t2pf && lane < 8 && jj < w.z)
+                else if (!GATHER && p.t2pf && lane < 8 && jj < w.z)
                     prefetch_l1(p.T2 + (size_t)item_tile(w, jj + 1, p.tile_list) * BN_TC + col0 + (lane - 4) * 32);
                 TC_WAIT(5, &acc_full[acc], accph);
                 tc_fence_after();
@@ -226,7 +265,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
                         const int colb = j * BN_TC + col0 + ch * 32;
                         while (hit) {
                             const int u = __ffs(hit) - 1;
-                            if (slot < (unsigned long long)p.cand_cap) p.cand[slot] = make_int2(rowid, colb + u);
+                            // gathered: the list entry holds the sorted tail position
+                            const int col = GATHER ? __ldg(p.glist + (size_t)colb + u) : colb + u;
+                            if (slot < (unsigned long long)p.cand_cap) p.cand[slot] = make_int2(rowid, col);
                             ++slot;
                             hit &= hit - 1;
                         }
@@ -343,9 +384,25 @@ void launch_tiles_tc(const TileParams& p, int num_sms, cudaStream_t s) {
     if (p.n_items <= 0) return;
     int as, bs, kc;
     int smem = tc_smem_bytes(p.Kpad, &as, &bs, &kc);
-    cudaFuncSetAttribute(tiles_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tiles_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     long long g = p.n_items < num_sms ? p.n_items : num_sms;
-    tiles_tc_kernel<<<(unsigned)g, TC_THREADS, smem, s>>>(p, as, bs, kc);
+    tiles_tc_kernel<false><<<(unsigned)g, TC_THREADS, smem, s>>>(p, as, bs, kc);
+}
+
+// Gathered tail blocks: items, their count and block total are on the device
+// (p.items, *p.dn_items, *p.dtotal); p.n_items is an upper bound that sizes the grid.
+int tc_gather_ok(int Kpad) {
+    int as, bs, kc;
+    return tc_smem_bytes(Kpad, &as, &bs, &kc) > 0 && kc == 32;
+}
+
+void launch_tiles_tc_gather(const TileParams& p, int num_sms, cudaStream_t s) {
+    if (p.n_items <= 0) return;  // here: an upper bound of the device-side item count
+    int as, bs, kc;
+    int smem = tc_smem_bytes(p.Kpad, &as, &bs, &kc);
+    cudaFuncSetAttribute(tiles_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    long long g = p.n_items < num_sms ? p.n_items : num_sms;
+    tiles_tc_kernel<true><<<(unsigned)g, TC_THREADS, smem, s>>>(p, as, bs, kc);
 }
 
 }  // namespace kgc

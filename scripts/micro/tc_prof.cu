@@ -15,7 +15,7 @@ int main(int argc, char** argv) {
     FILE* f = fopen(argv[1], "rb"); fread(E.data(), 4, E.size(), f); fclose(f);
     f = fopen(argv[2], "rb"); fread(Rl.data(), 4, Rl.size(), f); fclose(f);
     kgc_ctx* ctx; kgc_options o; kgc_default_options(&o); const int eng = getenv("ENGINE") ? atoi(getenv("ENGINE")) : 1; o.l2_engine = eng;
-    auto prof = eng == 3 ? kgc_debug_tc2_prof : kgc_debug_tc_prof; o.pivots = getenv("PIVOTS") ? atoi(getenv("PIVOTS")) : 1;
+    auto prof = eng == 3 ? kgc_debug_tc2_prof : kgc_debug_tc_prof; (void)0; o.pivots = getenv("PIVOTS") ? atoi(getenv("PIVOTS")) : 1;
     if (kgc_create(&ctx, &o)) { printf("create: %s\n", kgc_last_error(nullptr)); return 1; }
     for (int rep = 0; rep < 2; ++rep) {
         prof(nullptr, 1);

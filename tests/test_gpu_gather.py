@@ -153,3 +153,108 @@ def test_gather_c2_l1_full_size_sampled(hit):
     assert st["engine"] == 5
     rep = check_parity(E, Rel, 1, eps, res, rows=rows)
     assert rep["tight"] > 0
+
+
+# ------------------------------------------------- tensor-core engine on gathered tail blocks (l2_engine 4)
+TC_GATHER = dict(pivots=8, l2_engine=4)
+
+
+@pytest.mark.parametrize("K", [2, 8])
+def test_tc_gather_c1_full(K):
+    E, Rel = generate_config("c1")
+    eps = theta_for(E, Rel, 2, 1e-3)
+    res, st = gpu_join(E, Rel, 2, eps, pivots=K, l2_engine=4)
+    assert st["engine"] == 6 and st["pivots_used"] == K
+    assert st["query_tile_rows"] == 128 and st["tail_tile_rows"] == 256
+    rep = check_parity(E, Rel, 2, eps, res)
+    assert rep["tight"] > 1000
+    assert 0 < st["gathered_pairs"] <= st["tile_pairs_surviving"] * 128 * 256
+
+
+@pytest.mark.parametrize("N,R,d", [(1, 1, 1), (7, 3, 5), (129, 2, 9), (257, 3, 33), (300, 5, 100), (1000, 4, 200),
+                                   (513, 2, 256), (700, 3, 50), (3000, 3, 8), (2049, 2, 104)])
+@pytest.mark.parametrize("dist", ["cluster", "uniform"])
+def test_tc_gather_ragged(N, R, d, dist):
+    E, Rel = generate(N, R, d, seed=5 * N + d, dist=dist)
+    eps = theta_for(E, Rel, 2, 0.01 if N > 10 else 0.3)
+    res, st = gpu_join(E, Rel, 2, eps, **TC_GATHER)
+    assert st["engine"] == (6 if st["work_items_mine"] > 0 else 1)
+    check_parity(E, Rel, 2, eps, res)
+
+
+def test_tc_gather_equals_contiguous_tiles():
+    E, Rel = generate(12000, 5, 64, seed=61)
+    eps = theta_for(E, Rel, 2, 1e-3)
+    a, sa = gpu_join(E, Rel, 2, eps, pivots=8, l2_engine=1)
+    b, sb = gpu_join(E, Rel, 2, eps, **TC_GATHER)
+    assert sa["engine"] == 1 and sb["engine"] == 6
+    assert keyset(a) == keyset(b)
+    assert sa["tile_pairs_surviving"] == sb["tile_pairs_surviving"]
+    assert sb["gathered_pairs"] < sb["tile_pairs_surviving"] * 128 * 256
+    assert sb["candidates"] <= sa["candidates"] * 1.05 + 100
+
+
+def test_tc_gather_lists_complete():
+    from paper_2307_12059_b200 import kgc
+    N, R, K, d = 4000, 3, 8, 32
+    E, Rel = generate(N, R, d, seed=62)
+    eps = theta_for(E, Rel, 2, 1e-3)
+    with kgc.Join(**TC_GATHER) as j:
+        j.run(E, Rel, 2, eps)
+        kt = j.inspect("tail_keys").reshape(N, K)
+        kq = j.inspect("query_keys").reshape(R, N, K)
+        tperm = j.inspect("tail_perm")
+        qperm = j.inspect("query_perm").reshape(R, N)
+        cum = j.inspect("query_cost")
+        lst = j.inspect("tile_list")
+        nb = j.inspect("gather_cost")
+        glist = j.inspect("gather_list")
+        st = j.stats()
+    assert st["engine"] == 6
+    BM, BN, QT = st["query_tile_rows"], st["tail_tile_rows"], st["query_tiles"]
+    skt = kt[tperm]
+    nq = R * QT
+    assert len(glist) == BN * len(lst)
+    total = 0
+    for r in range(R):
+        skq = kq[r][qperm[r]]
+        for qt in range(QT):
+            tq = r * QT + qt
+            ntl = (cum[tq + 1] if tq + 1 < nq else len(lst) + cum[0]) - cum[tq]
+            seg = glist[BN * (cum[tq] - cum[0]):][:BN * nb[tq]]
+            real = seg[seg < N]
+            total += len(real)
+            assert len(seg) == BN * ((len(real) + BN - 1) // BN)
+            assert np.all(seg[len(real):] == N) and np.all(np.diff(real) > 0)
+            tiles = set(lst[cum[tq] - cum[0]: cum[tq] - cum[0] + ntl].tolist())
+            assert set((real // BN).tolist()) <= tiles
+            rows = skq[qt * BM:(qt + 1) * BM]
+            ok = np.ones((rows.shape[0], N), bool)
+            for k in range(K):
+                ok &= np.abs(rows[:, None, k] - skt[None, :, k]) <= eps
+            assert set(np.nonzero(ok.any(axis=0))[0].tolist()) <= set(real.tolist())
+    assert st["gathered_pairs"] == BM * total
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_tc_gather_sharding_invariance(world):
+    E, Rel = generate(5000, 7, 48, seed=63)
+    eps = theta_for(E, Rel, 2, 1e-3)
+    full, _ = gpu_join(E, Rel, 2, eps, **TC_GATHER)
+    for split in (0, 1):
+        parts = [gpu_join(E, Rel, 2, eps, rank=r, world=world, split=split, **TC_GATHER)[0] for r in range(world)]
+        sets = [keyset(p) for p in parts]
+        assert sum(len(s) for s in sets) == len(set().union(*sets))
+        assert set().union(*sets) == keyset(full)
+
+
+@pytest.mark.parametrize("cfg,hit,S", [("c2", 1e-4, 1200), ("c3", 1e-5, 800), ("c3", 1e-3, 400)])
+def test_tc_gather_full_size_sampled(cfg, hit, S):
+    E, Rel = generate_config(cfg)
+    N, R = E.shape[0], Rel.shape[0]
+    rows = sample_rows(N, R, S, seed=10)
+    eps = theta_for(E, Rel, 2, hit, rows=rows)
+    res, st = gpu_join(E, Rel, 2, eps, **TC_GATHER)
+    assert st["engine"] == 6
+    rep = check_parity(E, Rel, 2, eps, res, rows=rows)
+    assert rep["tight"] > 0
