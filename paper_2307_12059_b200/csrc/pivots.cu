@@ -558,6 +558,92 @@ __global__ void gather_tails_kernel(const float* __restrict__ qbmin, const float
     }
 }
 
+// The SIMT engine's list build with one 256-thread block per query tile: tile
+// lists are heavy-tailed (c2 L1: median 3 surviving tiles per query tile, p99
+// 137, max 496), so a warp per query tile left a long serial chain.  Warp w takes
+// a contiguous eighth of the list; pass 1 counts, a shared-memory prefix orders
+// the eighths, pass 2 writes (keys reloaded from L1/L2) -- the same ascending
+// output as gather_tails_kernel<64, false>.
+__global__ void __launch_bounds__(256) gather_tails_block_kernel(
+    const float* __restrict__ qbmin, const float* __restrict__ qbmax, const float4* __restrict__ tks,
+    const int* __restrict__ list, const long long* __restrict__ cum, const int2* __restrict__ ranges,
+    DevCounters* ctr, long long N, int K, float theta, float relm, int chunk, long long* __restrict__ gblocks,
+    int2* __restrict__ granges, int* __restrict__ nitem, int* __restrict__ glist) {
+    constexpr int BN = 64, NW = 8, UN = 2;
+    __shared__ long long wcnt[NW + 1];
+    const int tq0 = ctr->tq_begin, tq1 = ctr->tq_end;
+    if (tq0 >= tq1) return;
+    const long long base = cum[tq0];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned long long pairs = 0, blocks = 0;
+    for (long long q = tq0 + blockIdx.x; q < tq1; q += gridDim.x) {
+        float qmn[MP_MAX], qmx[MP_MAX];
+#pragma unroll
+        for (int k = 0; k < MP_MAX; ++k)
+            if (k < K) { qmn[k] = qbmin[q * K + k]; qmx[k] = qbmax[q * K + k]; }
+        const int ntl = ranges[q].y + 1;
+        const long long loff = cum[q] - base;
+        const int* L = list + loff;
+        int* out = glist + loff * BN;
+        const int u_lo = (int)((long long)ntl * w / NW), u_hi = (int)((long long)ntl * (w + 1) / NW);
+        long long c = 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            if (pass == 1) c = wcnt[w];
+            for (int u0 = u_lo; u0 < u_hi; u0 += UN) {
+                float4 kv[UN][2][2];
+                long long ib[UN];
+#pragma unroll
+                for (int x = 0; x < UN; ++x) {
+                    ib[x] = u0 + x < u_hi ? (long long)__ldg(L + u0 + x) * BN + lane : N;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const long long i = ib[x] + 32 * h;
+                        kv[x][h][0] = i < N ? __ldg(tks + 2 * i) : make_float4(0, 0, 0, 0);
+                        kv[x][h][1] = i < N ? __ldg(tks + 2 * i + 1) : make_float4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int x = 0; x < UN; ++x) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const long long i = ib[x] + 32 * h;
+                        const float4 a = kv[x][h][0], b = kv[x][h][1];
+                        const float tk[MP_MAX] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                        const bool ok = i < N && mp_survives(qmn, qmx, tk, tk, K, theta, relm);
+                        const unsigned m = __ballot_sync(0xffffffffu, ok);
+                        if (pass == 1 && ok) out[c + __popc(m & lanemask_lt())] = (int)i;
+                        c += __popc(m);
+                    }
+                }
+            }
+            if (pass == 0) {
+                if (lane == 0) wcnt[w + 1] = c;
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    wcnt[0] = 0;
+                    for (int x = 1; x <= NW; ++x) wcnt[x] += wcnt[x - 1];
+                }
+                __syncthreads();
+            }
+        }
+        const long long tot = wcnt[NW];
+        const long long nb = (tot + BN - 1) / BN;
+        for (long long o = tot + threadIdx.x; o < nb * BN; o += blockDim.x) out[o] = (int)N;  // sentinel padding
+        if (threadIdx.x == 0) {
+            gblocks[q] = nb;
+            granges[q] = make_int2(0, (int)nb - 1);
+            nitem[q] = (int)((nb + chunk - 1) / chunk);
+            pairs += (unsigned long long)tot;
+            blocks += (unsigned long long)nb;
+        }
+        __syncthreads();  // wcnt is reused by the next query tile
+    }
+    if (threadIdx.x == 0 && blocks) {
+        atomicAdd(&ctr->gpairs, pairs);
+        atomicAdd((unsigned long long*)&ctr->gblocks, blocks);
+    }
+}
+
 // ------------------------------------------------------------ launchers
 void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, const double* p0, float* P,
                         cudaStream_t s) {
@@ -648,8 +734,8 @@ void launch_gather_tails(const float* qbmin, const float* qbmax, const float* tk
     const unsigned g = grid_for_mp(nq * 32, 256);
     const float4* tk4 = reinterpret_cast<const float4*>(tks);
     if (BN == 64)
-        gather_tails_kernel<64, false><<<g, 256, 0, s>>>(qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm,
-                                                         chunk, gblocks, granges, nitem, glist, tsc, gT2, gtst);
+        gather_tails_block_kernel<<<grid_for_mp(nq, 1, 148LL * 16), 256, 0, s>>>(
+            qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm, chunk, gblocks, granges, nitem, glist);
     else
         gather_tails_kernel<256, true><<<g, 256, 0, s>>>(qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm,
                                                          chunk, gblocks, granges, nitem, glist, tsc, gT2, gtst);
