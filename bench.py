@@ -242,7 +242,7 @@ def run_ours(args, cfg, thresholds):
             stream.wait_event(ev)
         return out
 
-    joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, stream=jstream[n].cuda_stream)
+    joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, split=args.split, stream=jstream[n].cuda_stream)
              for n in args.norms}
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     counts = torch.zeros(len(args.norms), dtype=torch.int64, device=dev)
@@ -358,7 +358,7 @@ def run_ours(args, cfg, thresholds):
         R_pin = torch.from_numpy(Rel_h).pin_memory()
         out_pin = {n: torch.empty((max(1, stats_last[n]["results"]) * 2, 4), dtype=torch.int32).pin_memory()
                    for n in args.norms}
-        e2e_joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots,
+        e2e_joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, split=args.split,
                                  stream=jstream[n].cuda_stream) for n in args.norms}
         h2d = d2h = 0
 
@@ -477,7 +477,7 @@ def run_emulated_ranks(args, cfg, thresholds):
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     out = {"emulated_ranks": W, "config": args.config, "pivots": args.pivots, "shard_ms": []}
     for rank in range(W):
-        joins = {n: kgc.Join(device=0, rank=rank, world=W, pivots=args.pivots, stream=stream.cuda_stream)
+        joins = {n: kgc.Join(device=0, rank=rank, world=W, pivots=args.pivots, split=args.split, stream=stream.cuda_stream)
                  for n in args.norms}
         for _ in range(max(1, args.warmup)):
             for n in args.norms:
@@ -493,11 +493,13 @@ def run_emulated_ranks(args, cfg, thresholds):
             torch.cuda.synchronize()
             times.append(a.elapsed_time(b))
         out["shard_ms"].append(statistics.mean(times))
+        ph = {f"L{n}": {k: round(v, 3) for k, v in joins[n].stats().items()
+                        if k.startswith("ms_") or k in ("launches", "work_items_mine", "tile_pairs_mine",
+                                                         "gathered_pairs", "candidates")}
+              for n in args.norms}
         if rank == 0:
-            out["rank0_phases"] = {f"L{n}": {k: round(v, 3) for k, v in joins[n].stats().items()
-                                             if k.startswith("ms_") or k in ("launches", "work_items_mine",
-                                                                             "tile_pairs_mine")}
-                                   for n in args.norms}
+            out["rank0_phases"] = ph
+        out.setdefault("phases", []).append(ph)
         for j in joins.values():
             j.close()
     ms = max(out["shard_ms"])
@@ -518,6 +520,7 @@ def main():
     ap.add_argument("--norms", default="2,1", help="norms joined per step, e.g. '2,1' or '2'")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sequential", action="store_true", help="run the step's joins one after the other")
+    ap.add_argument("--split", type=int, default=0, help="world > 1: 0 = rank-local split, 1 = global cost-balanced")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=256, help="(h,r) rows per reference step")
