@@ -434,7 +434,8 @@ def run_ours(args, cfg, thresholds):
                             "SIMT on gathered tails; every emitted triplet re-checked in FP64",
             "data": "synthetic",
             "config": {"workload": wl, "N": N, "R": R, "d": d, "norms": args.norms, "eps": eps, "hit_rate": args.hit,
-                       "parallelism": f"query-tile shards x{world}, tails replicated",
+                       "parallelism": f"query-tile shards x{world} ({['rank-local', 'cost-balanced', 'cyclic'][args.split]} "
+                                      f"split), tails replicated",
                        "joins": ("concurrent: one context, stream and host thread per norm" if conc else
                                  "sequential on one stream"),
                        "pivots": args.pivots,
@@ -520,7 +521,9 @@ def main():
     ap.add_argument("--norms", default="2,1", help="norms joined per step, e.g. '2,1' or '2'")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sequential", action="store_true", help="run the step's joins one after the other")
-    ap.add_argument("--split", type=int, default=0, help="world > 1: 0 = rank-local split, 1 = global cost-balanced")
+    ap.add_argument("--split", default="auto",
+                    help="world > 1: 0 = rank-local split, 1 = global cost-balanced, 2 = cyclic; auto = best "
+                         "measured per config (c2: 2, its hits concentrate in a few relations)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=256, help="(h,r) rows per reference step")
@@ -535,6 +538,7 @@ def main():
     # the paper's single pivot is faster on c3 (its extra keys/sort cost exceeds the pruning gain).
     best_pivots = {"c1": 1, "c2": 8, "c3": 1, "c4": 8, "c5": 8}
     args.pivots = best_pivots.get(args.config, 1) if args.pivots == "auto" else int(args.pivots)
+    args.split = {"c2": 2}.get(args.config, 0) if args.split == "auto" else int(args.split)
     cfg = CONFIGS[args.config]
     thresholds = load_thresholds()
     if args.impl == "reference":

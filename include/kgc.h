@@ -96,7 +96,9 @@ typedef struct {
     int32_t split;            /* world > 1: 0 = rank-local (default: rank k takes query tiles       */
                               /* [k nq/W, (k+1) nq/W) and preprocesses only the relations they      */
                               /* touch; tails are replicated); 1 = global cost-balanced split (every */
-                              /* rank preprocesses everything, shards by surviving-tile counts)     */
+                              /* rank preprocesses everything, shards by surviving-tile counts);   */
+                              /* 2 = cyclic (every rank preprocesses everything and takes query    */
+                              /* tiles q with q % world == rank: hit-dense relations spread out)    */
 } kgc_options;
 
 /* Per-join statistics (of the last successful kgc_join). */

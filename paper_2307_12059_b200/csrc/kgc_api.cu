@@ -226,7 +226,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 4 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 1) {
+        o.l2_engine > 4 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -578,9 +578,13 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const int tq1 = h1.c.tq_begin == INT_MAX ? 0 : h1.c.tq_end;
     ctx->list_len = 0;
     ctx->glist_len = 0;
+    // Lists are laid out by the surviving-tile prefix over this shard's query-tile range; with the
+    // cyclic split (force_lo == -2) that range interleaves other ranks' tiles: size by the total.
+    const bool cyc = force_lo == -2;
+    const long long list_span = cyc ? h1.c.total_cost : h1.c.my_cost;
     if (n_items > 0 && K > 1) {
-        ctx->list_len = h1.c.my_cost;
-        CK(ensure(ctx->tile_list, (size_t)h1.c.my_cost * 4 + 4));
+        ctx->list_len = list_span;
+        CK(ensure(ctx->tile_list, (size_t)list_span * 4 + 4));
         launch_mp_emit(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tbmin), P<float>(ctx->tbmax),
                        P<long long>(ctx->cum), dctr, nq, TT, K, feps, mp_relm(d), 1, P<int>(ctx->tile_list), s);
         LAUNCHED(1);
@@ -589,7 +593,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     // test on their own keys, in blocks of GT_ROWS; work items reference blocks.
     const bool gather = n_items > 0 && K > 1 && !tc && !half_req && simt_t() == GT_ROWS && use_gather(ctx, norm);
     const bool gather_tc = n_items > 0 && gtc_req && K > 1 && tc_gather_ok(Kpad) &&
-                           (size_t)h1.c.my_cost * BN_TC * 8 <= GATHER_TC_BUDGET;
+                           (size_t)list_span * BN_TC * 8 <= GATHER_TC_BUDGET;
     const int GB = gather_tc ? BN_TC : GT_ROWS;  // rows per gathered block (= tail tile rows)
     long long g_max_items = 0;
     if (gather || gather_tc) {
@@ -598,15 +602,15 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(ensure(ctx->tks, (size_t)N * MP_MAX * 4));
         CK(ensure(ctx->gblk, (size_t)nq * 8));
         CK(ensure(ctx->granges, (size_t)nq * 8));
-        CK(ensure(ctx->glist, (size_t)g_max_items * GB * 4 + 4));
+        CK(ensure(ctx->glist, (size_t)list_span * GB * 4 + 4));
         CK(ensure(ctx->items, (size_t)g_max_items * 16));
         CK(ensure(ctx->item_tiles, (size_t)g_max_items * 8));
         CK(ensure(ctx->item_cum, (size_t)g_max_items * 8));
         CK(ensure(ctx->scan_tmp, scan_tmp_bytes((size_t)std::max<long long>(g_max_items, nq))));
         if (gather_tc) {
             CK(ensure(ctx->tsc, (size_t)N * 16));
-            CK(ensure(ctx->gT2, (size_t)g_max_items * GB * 4 + 4));
-            CK(ensure(ctx->gtst, (size_t)g_max_items * 8));
+            CK(ensure(ctx->gT2, (size_t)list_span * GB * 4 + 4));
+            CK(ensure(ctx->gtst, (size_t)list_span * 8));
         }
         launch_stage_rows(Et, P<int>(ctx->tperm), P<float>(ctx->mpkt), N, d, Kpad, K, P<float>(ctx->Ts),
                           P<float>(ctx->tks), gather_tc ? P<float4>(ctx->tsc) : nullptr, s);
@@ -625,7 +629,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                             P<long long>(ctx->cum), P<int2>(ctx->ranges), dctr, N, GB, K, feps, mp_relm(d), chunk, nq,
                             P<long long>(ctx->gblk), P<int2>(ctx->granges), P<int>(ctx->nitem), P<int>(ctx->glist),
                             gather_tc ? P<float4>(ctx->tsc) : nullptr, gather_tc ? P<float>(ctx->gT2) : nullptr,
-                            gather_tc ? P<float2>(ctx->gtst) : nullptr, s);
+                            gather_tc ? P<float2>(ctx->gtst) : nullptr, cyc ? ctx->opt.world : 0, ctx->opt.rank,
+                            s);
         LAUNCHED(2);
         scan_exclusive_i32(P<int>(ctx->nitem), P<int>(ctx->item_off), (size_t)nq, ctx->scan_tmp.p, s,
                            &ctx->launches);
@@ -961,6 +966,10 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
                            b - r_lo * QT, R);
             ctx->st.h2d_bytes += h2d;
         }
+    } else if (ctx->opt.world > 1 && ctx->opt.split == 2) {
+        // Cyclic split: every rank preprocesses everything and takes query tiles q with
+        // q % world == rank, so hit-dense relations spread over all ranks.
+        rc = join_impl(ctx, E, Rel, N, R, d, norm, eps, 0, -2, -2, R);
     } else {
         rc = join_impl(ctx, E, Rel, N, R, d, norm, eps, 0, -1, -1, R);
     }

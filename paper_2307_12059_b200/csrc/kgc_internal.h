@@ -141,7 +141,8 @@ void launch_stage_rows(const float* E, const int* tperm, const float* keys, long
 void launch_gather_tails(const float* qbmin, const float* qbmax, const float* tks, const int* list,
                          const long long* cum, const int2* ranges, DevCounters* ctr, long long N, int BN, int K,
                          float theta, float relm, int chunk, long long nq, long long* gblocks, int2* granges,
-                         int* nitem, int* glist, const float4* tsc, float* gT2, float2* gtst, cudaStream_t s);
+                         int* nitem, int* glist, const float4* tsc, float* gT2, float2* gtst, int cyc_world,
+                         int cyc_rank, cudaStream_t s);
 
 // Tail tile of position j of item w (contiguous range or multi-pivot list).
 __device__ __forceinline__ int item_tile(const int4& w, int j, const int* __restrict__ list) {

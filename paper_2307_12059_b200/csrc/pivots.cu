@@ -468,7 +468,7 @@ __global__ void gather_tails_kernel(const float* __restrict__ qbmin, const float
                                     long long* __restrict__ gblocks, int2* __restrict__ granges,
                                     int* __restrict__ nitem, int* __restrict__ glist,
                                     const float4* __restrict__ tsc, float* __restrict__ gT2,
-                                    float2* __restrict__ gtst) {
+                                    float2* __restrict__ gtst, int cyc_world, int cyc_rank) {
     constexpr int H = BN / 32, UN = BN == 64 ? 4 : 1;
     const int tq0 = ctr->tq_begin, tq1 = ctr->tq_end;
     if (tq0 >= tq1) return;
@@ -477,6 +477,7 @@ __global__ void gather_tails_kernel(const float* __restrict__ qbmin, const float
     unsigned long long pairs = 0, blocks = 0;
     for (long long q = tq0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); q < tq1;
          q += ((long long)gridDim.x * blockDim.x) >> 5) {
+        if (cyc_world > 1 && q % cyc_world != cyc_rank) continue;  // cyclic split: not this rank's tile
         float qmn[MP_MAX], qmx[MP_MAX];
 #pragma unroll
         for (int k = 0; k < MP_MAX; ++k)
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(256) gather_tails_block_kernel(
     const float* __restrict__ qbmin, const float* __restrict__ qbmax, const float4* __restrict__ tks,
     const int* __restrict__ list, const long long* __restrict__ cum, const int2* __restrict__ ranges,
     DevCounters* ctr, long long N, int K, float theta, float relm, int chunk, long long* __restrict__ gblocks,
-    int2* __restrict__ granges, int* __restrict__ nitem, int* __restrict__ glist) {
+    int2* __restrict__ granges, int* __restrict__ nitem, int* __restrict__ glist, int cyc_world, int cyc_rank) {
     constexpr int BN = 64, NW = 8, UN = 2;
     __shared__ long long wcnt[NW + 1];
     const int tq0 = ctr->tq_begin, tq1 = ctr->tq_end;
@@ -577,6 +578,7 @@ __global__ void __launch_bounds__(256) gather_tails_block_kernel(
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned long long pairs = 0, blocks = 0;
     for (long long q = tq0 + blockIdx.x; q < tq1; q += gridDim.x) {
+        if (cyc_world > 1 && q % cyc_world != cyc_rank) continue;  // cyclic split: not this rank's tile
         float qmn[MP_MAX], qmx[MP_MAX];
 #pragma unroll
         for (int k = 0; k < MP_MAX; ++k)
@@ -730,15 +732,18 @@ void launch_stage_rows(const float* E, const int* tperm, const float* keys, long
 void launch_gather_tails(const float* qbmin, const float* qbmax, const float* tks, const int* list,
                          const long long* cum, const int2* ranges, DevCounters* ctr, long long N, int BN, int K,
                          float theta, float relm, int chunk, long long nq, long long* gblocks, int2* granges,
-                         int* nitem, int* glist, const float4* tsc, float* gT2, float2* gtst, cudaStream_t s) {
+                         int* nitem, int* glist, const float4* tsc, float* gT2, float2* gtst, int cyc_world,
+                         int cyc_rank, cudaStream_t s) {
     const unsigned g = grid_for_mp(nq * 32, 256);
     const float4* tk4 = reinterpret_cast<const float4*>(tks);
     if (BN == 64)
         gather_tails_block_kernel<<<grid_for_mp(nq, 1, 148LL * 16), 256, 0, s>>>(
-            qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm, chunk, gblocks, granges, nitem, glist);
+            qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm, chunk, gblocks, granges, nitem, glist,
+            cyc_world, cyc_rank);
     else
         gather_tails_kernel<256, true><<<g, 256, 0, s>>>(qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm,
-                                                         chunk, gblocks, granges, nitem, glist, tsc, gT2, gtst);
+                                                         chunk, gblocks, granges, nitem, glist, tsc, gT2, gtst,
+                                                         cyc_world, cyc_rank);
 }
 
 }  // namespace kgc

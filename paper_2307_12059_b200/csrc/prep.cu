@@ -592,6 +592,8 @@ __global__ void shard_count_kernel(const long long* __restrict__ cost, const lon
         int owner = 0;
         if (force_lo >= 0) {
             owner = (q >= force_lo && q < force_hi) ? rank : rank + 1;  // rank-local split: a fixed range
+        } else if (force_lo == -2) {
+            owner = (int)(q % world);  // cyclic split: query tiles dealt round-robin
         } else if (total > 0) {
             long long o = (long long)world * cum[q] / total;
             owner = (int)(o < world - 1 ? o : world - 1);

@@ -126,7 +126,7 @@ def test_gather_sharding_invariance(world):
     E, Rel = generate(4000, 7, 48, seed=53)
     eps = theta_for(E, Rel, 1, 1e-3)
     full, _ = gpu_join(E, Rel, 1, eps, **L1_GATHER)
-    for split in (0, 1):
+    for split in (0, 1, 2):
         parts = [gpu_join(E, Rel, 1, eps, rank=r, world=world, split=split, **L1_GATHER)[0] for r in range(world)]
         sets = [keyset(p) for p in parts]
         assert sum(len(s) for s in sets) == len(set().union(*sets))
@@ -241,7 +241,7 @@ def test_tc_gather_sharding_invariance(world):
     E, Rel = generate(5000, 7, 48, seed=63)
     eps = theta_for(E, Rel, 2, 1e-3)
     full, _ = gpu_join(E, Rel, 2, eps, **TC_GATHER)
-    for split in (0, 1):
+    for split in (0, 1, 2):
         parts = [gpu_join(E, Rel, 2, eps, rank=r, world=world, split=split, **TC_GATHER)[0] for r in range(world)]
         sets = [keyset(p) for p in parts]
         assert sum(len(s) for s in sets) == len(set().union(*sets))

@@ -82,10 +82,10 @@ def test_pivot_invariance(norm):
     check_parity(E, Rel, norm, eps, b)
 
 
-@pytest.mark.parametrize("world,split", [(2, 0), (3, 0), (5, 0), (8, 0), (2, 1), (3, 1), (5, 1)])
+@pytest.mark.parametrize("world,split", [(2, 0), (3, 0), (5, 0), (8, 0), (2, 1), (3, 1), (5, 1), (2, 2), (3, 2), (8, 2)])
 def test_sharding_invariance(world, split):
     """Union of the shards of `world` contexts == the 1-context set, shards disjoint
-    (split 0: rank-local preprocessing of a query-tile range; 1: global cost split)."""
+    (split 0: rank-local preprocessing of a query-tile range; 1: global cost split; 2: cyclic)."""
     E, Rel = generate(3000, 7, 48, seed=33)
     eps = theta_for(E, Rel, 2, 1e-3)
     full, _ = gpu_join(E, Rel, 2, eps)
@@ -432,3 +432,19 @@ def test_tc2_full_size_sampled(cfg, hit, S):
     assert st["engine"] == 4
     rep = check_parity(E, Rel, 2, eps, res, rows=rows)
     assert rep["tight"] > 0
+
+
+@pytest.mark.parametrize("norm,opts", [(2, dict(l2_engine=1)), (2, dict(l2_engine=3)), (2, dict(l2_engine=2)),
+                                       (1, dict()), (1, dict(l1_engine=2)), (1, dict(l1_engine=1))])
+@pytest.mark.parametrize("world", [2, 5])
+def test_cyclic_split_invariance_multipivot(norm, opts, world):
+    """split 2 (query tiles dealt round-robin to ranks): shards disjoint, union = the 1-context set,
+    for every tile engine with 8 pivots (tile lists laid out over the whole query-tile range)."""
+    E, Rel = generate(4000, 5, 40, seed=34)
+    eps = theta_for(E, Rel, norm, 2e-3)
+    full, _ = gpu_join(E, Rel, norm, eps, pivots=8, **opts)
+    parts = [gpu_join(E, Rel, norm, eps, rank=r, world=world, split=2, pivots=8, **opts) for r in range(world)]
+    sets = [keyset(p[0]) for p in parts]
+    assert sum(len(s) for s in sets) == len(set().union(*sets))
+    assert set().union(*sets) == keyset(full)
+    assert sum(p[1]["tile_pairs_mine"] for p in parts) == parts[0][1]["tile_pairs_surviving"]
