@@ -689,7 +689,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * bq * Kpad * 4));
             CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * bq * 16));
             launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, bq, tq0, tq1, 0, norm, feps,
-                                 P<float>(ctx->Qp), P<float4>(ctx->qs), s);
+                                 P<float>(ctx->Qp), P<float4>(ctx->qs), s, cyc ? ctx->opt.world : 0, ctx->opt.rank);
             LAUNCHED(1);
         } else {
             launch_stage_tails(Et, P<int>(ctx->tperm), N, d, Kpad, BN, TT, tc2 ? 2 : (tc ? 1 : 0), P<float>(ctx->Tp),
@@ -699,7 +699,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                 CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * bq * Kpad * 4));
                 CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * bq * 16));
                 launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, bq, tq0, tq1, 0, norm, feps,
-                                     P<float>(ctx->Qp), P<float4>(ctx->qs), s);
+                                     P<float>(ctx->Qp), P<float4>(ctx->qs), s, cyc ? ctx->opt.world : 0,
+                                     ctx->opt.rank);
                 LAUNCHED(1);
             }
         }

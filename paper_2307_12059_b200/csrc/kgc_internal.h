@@ -105,7 +105,7 @@ void launch_stage_tails(const float* E, const int* tperm, long long N, int d, in
                         int tc_layout, float* Tp, float* T2, float2* tstile, cudaStream_t s);
 void launch_stage_queries(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad,
                           int QT, int bq, int tq0, int tq1, int tc_layout, int norm, float theta, float* Qp,
-                          float4* qs, cudaStream_t s);
+                          float4* qs, cudaStream_t s, int cyc_world = 0, int cyc_rank = 0);
 // FP16x2 L1 engine staging: tiles of half2 words, element (i, k-pair p) at p * ROWS + i;
 // per row the exact residual R = sum_k |v_k - fp16(v_k)| (rounded up)
 void launch_stage_half(const float* E, const float* Rel, const int* perm, long long N, int d, int Kpad, int ROWS,

@@ -671,8 +671,10 @@ __global__ void __launch_bounds__(1024) stage_kernel(const float* __restrict__ E
                                                     const int* __restrict__ perm, long long N, int d, int Kpad,
                                                     int ROWS, int QT, int tile0, int norm, float theta,
                                                     float* __restrict__ out, float4* __restrict__ qs,
-                                                    float* __restrict__ T2, float2* __restrict__ tstile, int split) {
+                                                    float* __restrict__ T2, float2* __restrict__ tstile, int split,
+                                                    int cyc_world = 0, int cyc_rank = 0) {
     const int tile = tile0 + blockIdx.x;
+    if (cyc_world > 1 && tile % cyc_world != cyc_rank) return;  // cyclic split: another rank's query tile
     long long r = 0, t_in_rel = tile;
     if (Rel) {
         r = tile / QT;
@@ -990,14 +992,14 @@ void launch_stage_tails(const float* E, const int* tperm, long long N, int d, in
 
 void launch_stage_queries(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad, int QT,
                           int bq, int tq0, int tq1, int tc_layout, int norm, float theta, float* Qp, float4* qs,
-                          cudaStream_t s) {
+                          cudaStream_t s, int cyc_world, int cyc_rank) {
     if (tq1 <= tq0) return;
     if (tc_layout)
         stage_kernel<true><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, bq, QT, tq0, norm, theta, Qp, qs,
-                                                     nullptr, nullptr, bq);
+                                                     nullptr, nullptr, bq, cyc_world, cyc_rank);
     else
         stage_kernel<false><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, bq, QT, tq0, norm, theta, Qp, qs,
-                                                      nullptr, nullptr, bq);
+                                                      nullptr, nullptr, bq, cyc_world, cyc_rank);
 }
 
 }  // namespace kgc
