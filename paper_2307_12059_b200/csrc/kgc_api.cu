@@ -594,15 +594,17 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const bool gather = n_items > 0 && K > 1 && !tc && !half_req && simt_t() == GT_ROWS && use_gather(ctx, norm);
     const bool gather_tc = n_items > 0 && gtc_req && K > 1 && tc_gather_ok(Kpad) &&
                            (size_t)list_span * BN_TC * 8 <= GATHER_TC_BUDGET;
-    const int GB = gather_tc ? BN_TC : GT_ROWS;  // rows per gathered block (= tail tile rows)
+    // rows per gathered block: tensor cores 256 (= tail tile rows); SIMT 64 or 32 (KGC_GT_TB experiment knob)
+    const char* gtb = getenv("KGC_GT_TB");
+    const int GB = gather_tc ? BN_TC : ((gtb && atoi(gtb) == 32) ? 32 : GT_ROWS);
     long long g_max_items = 0;
     if (gather || gather_tc) {
-        g_max_items = h1.c.my_cost;  // blocks (and items) <= surviving tiles of this shard
+        g_max_items = h1.c.my_cost * (BN / GB > 1 ? BN / GB : 1);  // blocks (and items) <= tiles x rows per block
         CK(ensure(ctx->Ts, (size_t)(N + 1) * Kpad * 4));
         CK(ensure(ctx->tks, (size_t)N * MP_MAX * 4));
         CK(ensure(ctx->gblk, (size_t)nq * 8));
         CK(ensure(ctx->granges, (size_t)nq * 8));
-        CK(ensure(ctx->glist, (size_t)list_span * GB * 4 + 4));
+        CK(ensure(ctx->glist, (size_t)list_span * BN * 4 + 4));  // laid out at BN x the tile-list offsets
         CK(ensure(ctx->items, (size_t)g_max_items * 16));
         CK(ensure(ctx->item_tiles, (size_t)g_max_items * 8));
         CK(ensure(ctx->item_cum, (size_t)g_max_items * 8));
@@ -626,11 +628,11 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(cudaMemsetAsync(ctx->nitem.p, 0, (size_t)nq * 4, s));
         CK(cudaMemsetAsync(ctx->item_tiles.p, 0, (size_t)g_max_items * 8, s));
         launch_gather_tails(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tks), P<int>(ctx->tile_list),
-                            P<long long>(ctx->cum), P<int2>(ctx->ranges), dctr, N, GB, K, feps, mp_relm(d), chunk, nq,
+                            P<long long>(ctx->cum), P<int2>(ctx->ranges), dctr, N, BN, K, feps, mp_relm(d), chunk, nq,
                             P<long long>(ctx->gblk), P<int2>(ctx->granges), P<int>(ctx->nitem), P<int>(ctx->glist),
                             gather_tc ? P<float4>(ctx->tsc) : nullptr, gather_tc ? P<float>(ctx->gT2) : nullptr,
                             gather_tc ? P<float2>(ctx->gtst) : nullptr, cyc ? ctx->opt.world : 0, ctx->opt.rank,
-                            s);
+                            s, GB);
         LAUNCHED(2);
         scan_exclusive_i32(P<int>(ctx->nitem), P<int>(ctx->item_off), (size_t)nq, ctx->scan_tmp.p, s,
                            &ctx->launches);
@@ -759,6 +761,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.gT2 = P<float>(ctx->gT2);
         tp.gtst = P<float2>(ctx->gtst);
         tp.tmap = ctx->tmapbuf.p;
+        tp.gb = GB;
         if (n_items > 0) {
             if (gather) {
                 const char* pe = getenv("KGC_GT_PROF");  // experiment: wait-cycle instrumentation
@@ -811,7 +814,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         cand_n = (long long)hcnt[0];
         res_n = (long long)hcnt[1];
         st.gathered_pairs = (int64_t)hg[1] * bq;
-        ctx->glist_len = (gather || gather_tc) ? ctx->list_len * GB : 0;
+        ctx->glist_len = (gather || gather_tc) ? ctx->list_len * BN : 0;
         if (cand_n > ctx->cand_cap) {
             ctx->cand_cap = cand_n + cand_n / 4 + 1024;
             st.reruns++;

@@ -71,6 +71,7 @@ struct TileParams {
     const float* gT2;             // tensor-core gathered blocks: ||t||^2 / 2 per list entry (3e38 padding)
     const float2* gtst;           // tensor-core gathered blocks: per block {max ||t||, max ||t - tf32(t)||}
     const void* tmap;             // tensor-core gathered blocks: CUtensorMap over Ts (device memory)
+    int gb;                       // SIMT gathered blocks: tails per block (32 or 64)
     const long long* dn_items;    // device: work items of this shard
     const long long* dtotal;      // device: blocks of this shard (balanced CTA ranges)
     unsigned long long* prof;     // experiment: wait-cycle counters (KGC_GT_PROF), else nullptr
@@ -142,7 +143,7 @@ void launch_gather_tails(const float* qbmin, const float* qbmax, const float* tk
                          const long long* cum, const int2* ranges, DevCounters* ctr, long long N, int BN, int K,
                          float theta, float relm, int chunk, long long nq, long long* gblocks, int2* granges,
                          int* nitem, int* glist, const float4* tsc, float* gT2, float2* gtst, int cyc_world,
-                         int cyc_rank, cudaStream_t s);
+                         int cyc_rank, cudaStream_t s, int gb = 64);
 
 // Tail tile of position j of item w (contiguous range or multi-pivot list).
 __device__ __forceinline__ int item_tile(const int4& w, int j, const int* __restrict__ list) {

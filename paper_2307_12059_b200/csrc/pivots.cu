@@ -569,8 +569,9 @@ __global__ void __launch_bounds__(256) gather_tails_block_kernel(
     const float* __restrict__ qbmin, const float* __restrict__ qbmax, const float4* __restrict__ tks,
     const int* __restrict__ list, const long long* __restrict__ cum, const int2* __restrict__ ranges,
     DevCounters* ctr, long long N, int K, float theta, float relm, int chunk, long long* __restrict__ gblocks,
-    int2* __restrict__ granges, int* __restrict__ nitem, int* __restrict__ glist, int cyc_world, int cyc_rank) {
-    constexpr int BN = 64, NW = 8, UN = 2;
+    int2* __restrict__ granges, int* __restrict__ nitem, int* __restrict__ glist, int cyc_world, int cyc_rank,
+    int GB) {
+    constexpr int BN = 64, NW = 8, UN = 2;  // BN: tail-tile rows (list offsets); GB: rows per gathered block
     __shared__ long long wcnt[NW + 1];
     const int tq0 = ctr->tq_begin, tq1 = ctr->tq_end;
     if (tq0 >= tq1) return;
@@ -629,8 +630,8 @@ __global__ void __launch_bounds__(256) gather_tails_block_kernel(
             }
         }
         const long long tot = wcnt[NW];
-        const long long nb = (tot + BN - 1) / BN;
-        for (long long o = tot + threadIdx.x; o < nb * BN; o += blockDim.x) out[o] = (int)N;  // sentinel padding
+        const long long nb = (tot + GB - 1) / GB;
+        for (long long o = tot + threadIdx.x; o < nb * GB; o += blockDim.x) out[o] = (int)N;  // sentinel padding
         if (threadIdx.x == 0) {
             gblocks[q] = nb;
             granges[q] = make_int2(0, (int)nb - 1);
@@ -733,13 +734,13 @@ void launch_gather_tails(const float* qbmin, const float* qbmax, const float* tk
                          const long long* cum, const int2* ranges, DevCounters* ctr, long long N, int BN, int K,
                          float theta, float relm, int chunk, long long nq, long long* gblocks, int2* granges,
                          int* nitem, int* glist, const float4* tsc, float* gT2, float2* gtst, int cyc_world,
-                         int cyc_rank, cudaStream_t s) {
+                         int cyc_rank, cudaStream_t s, int gb) {
     const unsigned g = grid_for_mp(nq * 32, 256);
     const float4* tk4 = reinterpret_cast<const float4*>(tks);
     if (BN == 64)
         gather_tails_block_kernel<<<grid_for_mp(nq, 1, 148LL * 16), 256, 0, s>>>(
             qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm, chunk, gblocks, granges, nitem, glist,
-            cyc_world, cyc_rank);
+            cyc_world, cyc_rank, gb);
     else
         gather_tails_kernel<256, true><<<g, 256, 0, s>>>(qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm,
                                                          chunk, gblocks, granges, nitem, glist, tsc, gT2, gtst,

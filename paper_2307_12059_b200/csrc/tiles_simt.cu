@@ -409,12 +409,15 @@ void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t 
 // conflict-free with a padded row stride KC + 4 (SWZ = 0) or with 16-byte
 // piece p of row i stored at piece p ^ (i & 7) of a 32-float row (SWZ = 1).
 // PROF = 1: clock64 wait instrumentation (KGC_GT_PROF=1, experiment only).
-template <int NORM, int KC, int NSTAGE, int SWZ, int PROF = 0, int DUTY = 1, int MINB = 8, int KUN = 1>
-__global__ void __launch_bounds__(64, MINB) tiles_gather_kernel(TileParams p) {
-    constexpr int T = SIMT_T, TM = 8, TN = 8, NT = 64, GX = T / TN;
+// TB = tails per block: 64 (two warps sharing the stages) or 32 (one warp per CTA:
+// no lock-step between warps, half the padding; the query chunk is shared by 32 tails).
+template <int NORM, int KC, int NSTAGE, int SWZ, int PROF = 0, int DUTY = 1, int MINB = 8, int KUN = 1, int TB = 64>
+__global__ void __launch_bounds__(TB, MINB) tiles_gather_kernel(TileParams p) {
+    constexpr int T = SIMT_T, TM = 8, TN = 8, NT = TB, GX = TB / TN, NWARP = TB / 32;
     static_assert(!SWZ || KC == 32, "swizzle over the 8 pieces of a 32-float row");
+    static_assert(TB == 32 || TB == 64, "one or two warps");
     constexpr int LD = SWZ ? KC : KC + 4;  // tail row stride in shared memory (floats)
-    static_assert(T == GT_ROWS, "gathered block = tile");
+    constexpr int BPT = SIMT_T / TB;       // blocks per tile-list slot (list offsets are in 64-tail tiles)
     extern __shared__ __align__(128) uint8_t smem[];
     const int Kpad = p.Kpad;
     const int nkc = (Kpad + KC - 1) / KC;
@@ -423,13 +426,13 @@ __global__ void __launch_bounds__(64, MINB) tiles_gather_kernel(TileParams p) {
     const int cu = (Kpad / 4) / nkc, cr = (Kpad / 4) % nkc;
     auto chunk_k0 = [&](int c) { return 4 * (c * cu + (c < cr ? c : cr)); };
     auto chunk_len = [&](int c) { return 4 * (cu + (c < cr ? 1 : 0)); };
-    // stage s: query chunk [KC][T] followed by tail rows [T][LD]
-    constexpr int STAGE = KC * T + T * LD;
+    // stage s: query chunk [KC][T] followed by tail rows [TB][LD]
+    constexpr int STAGE = KC * T + TB * LD;
     float* St = reinterpret_cast<float*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(St + NSTAGE * STAGE);
     uint64_t* empty = full + NSTAGE;  // the non-duty warp has finished reading the stage
     int* released = reinterpret_cast<int*>(empty + NSTAGE);
-    int* ridx = released + NSTAGE;  // [T] row indices of the block being issued
+    int* ridx = released + NSTAGE;  // [TB] row indices of the block being issued
     __shared__ long long issued_at[PROF ? NSTAGE : 1];
 
     const int tid = threadIdx.x, lane = tid & 31;
@@ -473,19 +476,19 @@ __global__ void __launch_bounds__(64, MINB) tiles_gather_kernel(TileParams p) {
         float* dst = St + (size_t)s * STAGE;
         // the block's row indices: from global memory at its first chunk (kept in shared
         // memory for the others -- issues are serialised, see the release protocol below)
-        int r0, r1;
+        int r0, r1 = 0;
         if (ci.c == 0) {
-            const int* seg = p.glist + ((long long)ci.w.w + ci.j) * T;
+            const int* seg = p.glist + ((long long)ci.w.w * BPT + ci.j) * TB;
             r0 = __ldg(seg + lane);
-            r1 = __ldg(seg + lane + 32);
-            if (lane < 2) prefetch_l1(seg + T + lane * 32);  // the next block's indices
+            if (TB == 64) r1 = __ldg(seg + lane + 32);
+            if (lane < TB / 32) prefetch_l1(seg + TB + lane * 32);  // the next block's indices
             if (nkc > 1) {
                 ridx[lane] = r0;
-                ridx[lane + 32] = r1;
+                if (TB == 64) ridx[lane + 32] = r1;
             }
         } else {
             r0 = ridx[lane];
-            r1 = ridx[lane + 32];
+            if (TB == 64) r1 = ridx[lane + 32];
         }
         if (lane == 0) {
             mbar_arrive_expect_tx(&full[s], qbytes);
@@ -503,10 +506,11 @@ __global__ void __launch_bounds__(64, MINB) tiles_gather_kernel(TileParams p) {
             const int prow = lane / per_row, pseg = lane - prow * per_row;
             const bool act = lane < rpp * per_row;
 #pragma unroll 2
-            for (int row0 = 0; row0 < T; row0 += rpp) {
+            for (int row0 = 0; row0 < TB; row0 += rpp) {
                 const int row = row0 + prow;
-                const int a0 = __shfl_sync(0xffffffffu, r0, row & 31), a1 = __shfl_sync(0xffffffffu, r1, row & 31);
-                if (act && row < T) piece(row, pseg, row < 32 ? a0 : a1);
+                const int a0 = __shfl_sync(0xffffffffu, r0, row & 31);
+                const int a1 = TB == 64 ? __shfl_sync(0xffffffffu, r1, row & 31) : 0;
+                if (act && row < TB) piece(row, pseg, row < 32 ? a0 : a1);
             }
         }
         cp_async_mbar_arrive_noinc(&full[s]);
@@ -595,7 +599,9 @@ __global__ void __launch_bounds__(64, MINB) tiles_gather_kernel(TileParams p) {
         // slower one for good, and its partner then waited on every chunk.)
         __syncwarp();
         int last = 0;
-        if (DUTY) {
+        if (NWARP == 1) {
+            last = 1;  // the only reader refills its own stage
+        } else if (DUTY) {
             const int warp = tid >> 5;
             if (warp == (int)(g & 1)) {
                 mbar_wait(&empty[s], (uint32_t)(g / NSTAGE) & 1u);
@@ -627,7 +633,7 @@ __global__ void __launch_bounds__(64, MINB) tiles_gather_kernel(TileParams p) {
 #pragma unroll
                 for (int b = 0; b < TN; ++b) hit |= (unsigned long long)(acc[a][b] <= thr[a]) << (a * TN + b);
             if (__any_sync(0xffffffffu, hit != 0)) {
-                const int* seg = p.glist + ((long long)cs.w.w + cs.j) * T + tx;
+                const int* seg = p.glist + ((long long)cs.w.w * BPT + cs.j) * TB + tx;
 #pragma unroll
                 for (int b = 0; b < TN; ++b) {
                     const unsigned long long colm = 0x0101010101010101ull << b;  // column b of the micro-tile
@@ -655,21 +661,21 @@ __global__ void __launch_bounds__(64, MINB) tiles_gather_kernel(TileParams p) {
     }
 }
 
-template <int NORM, int KC, int NS, int SWZ = 0, int DUTY = 1, int MINB = 8, int KUN = 1>
+template <int NORM, int KC, int NS, int SWZ = 0, int DUTY = 1, int MINB = 8, int KUN = 1, int TB = 64>
 static void launch_gather_variant(const TileParams& p, int num_sms, long long max_items, cudaStream_t s) {
     constexpr int T = SIMT_T;
-    const size_t smem = (size_t)NS * (KC * T + T * (SWZ ? KC : KC + 4)) * 4 + 128 + T * 4;
+    const size_t smem = (size_t)NS * (KC * T + TB * (SWZ ? KC : KC + 4)) * 4 + 128 + TB * 4;
     static_assert(NS * 20 <= 128, "barriers and counters fit the 128-byte tail");
-    auto kern = p.prof ? tiles_gather_kernel<NORM, KC, NS, SWZ, 1, DUTY, MINB, KUN>
-                       : tiles_gather_kernel<NORM, KC, NS, SWZ, 0, DUTY, MINB, KUN>;
+    auto kern = p.prof ? tiles_gather_kernel<NORM, KC, NS, SWZ, 1, DUTY, MINB, KUN, TB>
+                       : tiles_gather_kernel<NORM, KC, NS, SWZ, 0, DUTY, MINB, KUN, TB>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 64, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TB, smem);
     if (per_sm < 1) per_sm = 1;
     long long g = (long long)num_sms * per_sm;
     if (g > max_items) g = max_items;
     if (g < 1) g = 1;
-    kern<<<(unsigned)g, 64, smem, s>>>(p);
+    kern<<<(unsigned)g, TB, smem, s>>>(p);
 }
 
 void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long max_items, cudaStream_t s) {
@@ -679,6 +685,16 @@ void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long m
     // measured on c2 L1 (tile-kernel ms, same session): KC 24 / 2 stages / alternating refill duty
     // 4.83; KC 32 4.93-5.07; KC 16 4.95; KC 24 with "last releaser refills" 4.93; KC 32 swizzled
     // 4.90; 3 stages 4.98-5.54; k-loop unrolled x2 at 6 CTAs/SM 4.99
+    if (p.gb == 32) {  // one warp per CTA, 32-tail blocks
+        if (norm == 1) {
+            if (v == 1) launch_gather_variant<1, 32, 2, 0, 1, 8, 1, 32>(p, num_sms, max_items, s);
+            else if (v == 2) launch_gather_variant<1, 24, 3, 0, 1, 8, 1, 32>(p, num_sms, max_items, s);
+            else launch_gather_variant<1, 24, 2, 0, 1, 8, 1, 32>(p, num_sms, max_items, s);
+        } else {
+            launch_gather_variant<2, 24, 2, 0, 1, 8, 1, 32>(p, num_sms, max_items, s);
+        }
+        return;
+    }
     if (norm == 1) {
         if (v == 1) launch_gather_variant<1, 32, 2>(p, num_sms, max_items, s);
         else if (v == 2) launch_gather_variant<1, 16, 2>(p, num_sms, max_items, s);
