@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(256) radix_scatter_kernel(const KeyT* __restri
     __shared__ int wcnt[8][257];
     const long long s = blockIdx.y;
     const int b = blockIdx.x;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int w = threadIdx.x >> 5;
     run[threadIdx.x] = 0;
     const long long base = (long long)b * SORT_IPB;
     const int boff = offs[(s * 256 + threadIdx.x) * B + b];
