@@ -242,7 +242,7 @@ def run_ours(args, cfg, thresholds):
             stream.wait_event(ev)
         return out
 
-    joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, split=args.split, stream=jstream[n].cuda_stream)
+    joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, split=args.split, tail_shard=args.tail_shard, stream=jstream[n].cuda_stream)
              for n in args.norms}
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     counts = torch.zeros(len(args.norms), dtype=torch.int64, device=dev)
@@ -358,7 +358,7 @@ def run_ours(args, cfg, thresholds):
         R_pin = torch.from_numpy(Rel_h).pin_memory()
         out_pin = {n: torch.empty((max(1, stats_last[n]["results"]) * 2, 4), dtype=torch.int32).pin_memory()
                    for n in args.norms}
-        e2e_joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, split=args.split,
+        e2e_joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, split=args.split, tail_shard=args.tail_shard,
                                  stream=jstream[n].cuda_stream) for n in args.norms}
         h2d = d2h = 0
 
@@ -434,8 +434,9 @@ def run_ours(args, cfg, thresholds):
                             "SIMT on gathered tails; every emitted triplet re-checked in FP64",
             "data": "synthetic",
             "config": {"workload": wl, "N": N, "R": R, "d": d, "norms": args.norms, "eps": eps, "hit_rate": args.hit,
-                       "parallelism": f"query-tile shards x{world} ({['rank-local', 'cost-balanced', 'cyclic'][args.split]} "
-                                      f"split), tails replicated",
+                       "parallelism": (f"tail partitions x{world}, every query on every rank" if args.tail_shard else
+                                       f"query-tile shards x{world} ({['rank-local', 'cost-balanced', 'cyclic'][args.split]} "
+                                       f"split), tails replicated"),
                        "joins": ("concurrent: one context, stream and host thread per norm" if conc else
                                  "sequential on one stream"),
                        "pivots": args.pivots,
@@ -478,7 +479,7 @@ def run_emulated_ranks(args, cfg, thresholds):
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     out = {"emulated_ranks": W, "config": args.config, "pivots": args.pivots, "shard_ms": []}
     for rank in range(W):
-        joins = {n: kgc.Join(device=0, rank=rank, world=W, pivots=args.pivots, split=args.split, stream=stream.cuda_stream)
+        joins = {n: kgc.Join(device=0, rank=rank, world=W, pivots=args.pivots, split=args.split, tail_shard=args.tail_shard, stream=stream.cuda_stream)
                  for n in args.norms}
         for _ in range(max(1, args.warmup)):
             for n in args.norms:
@@ -521,6 +522,8 @@ def main():
     ap.add_argument("--norms", default="2,1", help="norms joined per step, e.g. '2,1' or '2'")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sequential", action="store_true", help="run the step's joins one after the other")
+    ap.add_argument("--tail-shard", type=int, default=0,
+                    help="world > 1: 1 = partition-based join (rank k holds tails [kN/W, (k+1)N/W), every query)")
     ap.add_argument("--split", default="auto",
                     help="world > 1: 0 = rank-local split, 1 = global cost-balanced, 2 = cyclic; auto = best "
                          "measured per config (c2: 2, its hits concentrate in a few relations)")

@@ -42,7 +42,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define KGC_ABI_VERSION 1
+#define KGC_ABI_VERSION 2  /* 2: kgc_options.tail_shard, kgc_stats_t.gathered_pairs */
 
 /* Opaque context: owns device buffers, the stream, per-join statistics. */
 typedef struct kgc_ctx kgc_ctx;
@@ -99,6 +99,9 @@ typedef struct {
                               /* rank preprocesses everything, shards by surviving-tile counts);   */
                               /* 2 = cyclic (every rank preprocesses everything and takes query    */
                               /* tiles q with q % world == rank: hit-dense relations spread out)    */
+    int32_t tail_shard;       /* world > 1: 1 = partition-based join (§4.7): rank */
+                              /* k holds only tails [k N/W, (k+1) N/W) and joins every query       */
+                              /* against them (split is ignored); 0 = tails replicated (default)   */
 } kgc_options;
 
 /* Per-join statistics (of the last successful kgc_join). */
@@ -135,7 +138,7 @@ typedef struct {
 
 /* Fill *opt with defaults: device -1, rank 0, world 1, prune 1, pivot 0,
  * l2_engine 0, chunk_tiles 0, pivots 1, result_capacity 0, stream NULL,
- * l1_engine 0, split 0. */
+ * l1_engine 0, split 0, tail_shard 0. */
 void kgc_default_options(kgc_options* opt);
 
 /* Create a context.  opt == NULL means defaults.  Returns KGC_ENODEV when no

@@ -216,6 +216,7 @@ void kgc_default_options(kgc_options* o) {
     o->pivots = 1;
     o->l1_engine = 0;
     o->split = 0;
+    o->tail_shard = 0;
     o->result_capacity = 0;
     o->stream = nullptr;
 }
@@ -226,7 +227,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 4 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2) {
+        o.l2_engine > 4 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2 || o.tail_shard < 0 || o.tail_shard > 1) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -348,7 +349,9 @@ int64_t kgc_shard_range(const int64_t* cum, int64_t n, int64_t total, int32_t ra
 // Optional parts of a join beyond TransE (SE, se.cu): a separate tail matrix, a wider
 // filter threshold (operands rounded on both sides), and FP64 connectors for the re-check.
 struct JoinExtra {
-    const float* Et = nullptr;    // tails (default: E)
+    const float* Et = nullptr;    // tails (default: E, or rows [t_off, t_off + Nt) of the device copy of E)
+    long long Nt = -1;            // tail rows (default: N); tail partitions (kgc_options.tail_shard)
+    long long t_off = 0;          // first tail row of the partition (added to emitted t)
     float filt_eps = -1.f;        // threshold of every filter and pruning test (default: eps)
     const double* A64 = nullptr;  // exact connectors for verify_se (default: TransE verify)
     const double* B64 = nullptr;
@@ -373,7 +376,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const bool tc = use_tc(ctx, norm, d);
     const int K_plan = (ctx->opt.pivots >= 2 && ctx->opt.prune && d <= MP_MAX_DIM) ? ctx->opt.pivots : 1;
     const bool gtc_req = tc && K_plan > 1 && use_gather_tc(ctx);  // gathered tensor-core blocks requested
-    const bool tc2 = !gtc_req && use_tc2(ctx, norm, d, N);
+    const long long NT = ex.Nt >= 0 ? ex.Nt : N;  // tail rows (a tail partition, or all N)
+    const bool tc2 = !gtc_req && use_tc2(ctx, norm, d, NT);
     if (norm == 2 && (ctx->opt.l2_engine == 1 || ctx->opt.l2_engine == 3 || ctx->opt.l2_engine == 4) && !tc) {
         set_err(ctx, "l2_engine=%d (tcgen05) supports d <= %d", ctx->opt.l2_engine, TC_MAX_KPAD);
         return KGC_EINVAL;
@@ -384,7 +388,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const int bq = gtc_req ? BM : plan_bq(ctx, norm, d, N);
     const int BN = tc ? BN_TC : (half_req ? BN_HALF : simt_t());
     const int QT = (int)((N + bq - 1) / bq);
-    const int TT = (int)((N + BN - 1) / BN);
+    const int TT = (int)((NT + BN - 1) / BN);
     const long long nq = R * (long long)QT;
     int chunk = ctx->opt.chunk_tiles > 0 ? ctx->opt.chunk_tiles : (tc ? 16 : 8);
     if (tc && ctx->opt.chunk_tiles == 0) {
@@ -420,14 +424,14 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         st.h2d_bytes += (int64_t)R * d * 4;
     }
     CK(cudaEventRecord(ctx->ev[EV_H2D], s));
-    const float* Et = ex.Et ? ex.Et : E;                   // tails
+    const float* Et = ex.Et ? ex.Et : E + ex.t_off * d;   // tails (device)
     const float feps = ex.filt_eps >= 0.f ? ex.filt_eps : eps;  // filters and pruning
 
     // ---- allocations for the preprocessing
     const size_t NR = (size_t)N * R;
-    const size_t nsort = std::max(NR, (size_t)N);
+    const size_t nsort = std::max(NR, (size_t)NT);
     CK(ensure(ctx->ctr, sizeof(DevCounters)));
-    CK(ensure(ctx->kt, (size_t)N * 4));
+    CK(ensure(ctx->kt, (size_t)NT * 4));
     CK(ensure(ctx->kq, NR * 4));
     CK(ensure(ctx->mm_t, 2 * 4));
     CK(ensure(ctx->mm_q, (size_t)R * 2 * 4));
@@ -435,13 +439,13 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     CK(ensure(ctx->sv0, nsort * 4));
     CK(ensure(ctx->sk1, nsort * 4));
     CK(ensure(ctx->sv1, nsort * 4));
-    CK(ensure(ctx->counts, std::max(radix_counts_len(R, N), radix_counts_len(1, N)) * 4));
+    CK(ensure(ctx->counts, std::max(radix_counts_len(R, N), radix_counts_len(1, NT)) * 4));
     const size_t scan_n = std::max({radix_counts_len(R, N), (size_t)nq, (size_t)1});
     CK(ensure(ctx->scan_tmp, scan_tmp_bytes(scan_n)));
     CK(ensure(ctx->qperm, NR * 4));
     CK(ensure(ctx->qskey, NR * 4));
-    CK(ensure(ctx->tperm, (size_t)N * 4));
-    CK(ensure(ctx->tskey, (size_t)N * 4));
+    CK(ensure(ctx->tperm, (size_t)NT * 4 + 4));
+    CK(ensure(ctx->tskey, (size_t)NT * 4 + 4));
     CK(ensure(ctx->tmin, (size_t)TT * 4));
     CK(ensure(ctx->tmax, (size_t)TT * 4));
     CK(ensure(ctx->cmax, (size_t)TT * 4));
@@ -460,7 +464,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const double* pivot = nullptr;
     if (ctx->opt.pivot == 1) {
         CK(ensure(ctx->pivot, (size_t)d * 8));
-        launch_pivot_mean(E, N, d, P<double>(ctx->pivot), s);
+        launch_pivot_mean(Et, NT, d, P<double>(ctx->pivot), s);
         LAUNCHED(1);
         pivot = P<double>(ctx->pivot);
     }
@@ -473,14 +477,14 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     st.pivots_used = K;
     if (K == 1) {
         // ---- a2: K1 keys (one pivot, FP64 -> float)
-        launch_tail_keys(Et, N, d, norm, pivot, P<float>(ctx->kt), P<unsigned>(ctx->mm_t), &dctr->nonfinite, s);
+        launch_tail_keys(Et, NT, d, norm, pivot, P<float>(ctx->kt), P<unsigned>(ctx->mm_t), &dctr->nonfinite, s);
         LAUNCHED(2);
         launch_query_keys(E, Rel, N, R, d, norm, pivot, P<float>(ctx->kq), P<unsigned>(ctx->mm_q), &dctr->nonfinite,
                           s);
         LAUNCHED(2);
         CK(cudaEventRecord(ctx->ev[EV_KEYS], s));
         // ---- a3: K2 sorts (tails once, queries per relation)
-        radix_sort_segments(P<float>(ctx->kt), P<unsigned>(ctx->mm_t), 1, N, P<unsigned>(ctx->sk0),
+        radix_sort_segments(P<float>(ctx->kt), P<unsigned>(ctx->mm_t), 1, NT, P<unsigned>(ctx->sk0),
                             P<unsigned>(ctx->sv0), P<unsigned>(ctx->sk1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
                             P<int>(ctx->tperm), P<float>(ctx->tskey), ctx->scan_tmp.p, ctx->scan_tmp.n, s,
                             &ctx->launches);
@@ -492,7 +496,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         LAUNCHED(0);
         CK(cudaEventRecord(ctx->ev[EV_SORT], s));
         // ---- a4: K3 tile ranges (Lemma 1 + 2 at tile granularity)
-        launch_tail_tile_bounds(P<float>(ctx->tskey), N, BN, TT, P<float>(ctx->tmin), P<float>(ctx->tmax),
+        launch_tail_tile_bounds(P<float>(ctx->tskey), NT, BN, TT, P<float>(ctx->tmin), P<float>(ctx->tmax),
                                 P<float>(ctx->cmax), P<float>(ctx->cmin), s, &ctx->launches);
         LAUNCHED(0);
         launch_query_ranges(P<float>(ctx->qskey), N, R, QT, TT, bq, P<float>(ctx->cmax), P<float>(ctx->cmin), feps,
@@ -501,7 +505,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     } else {
         // ---- a2: K pivot distances per row (FP32)
         CK(ensure(ctx->mpP, (size_t)K * d * 4));
-        CK(ensure(ctx->mpkt, (size_t)N * K * 4));
+        CK(ensure(ctx->mpkt, (size_t)NT * K * 4 + 4));
         CK(ensure(ctx->mpkq, NR * K * 4));
         CK(ensure(ctx->mpmm_t, (size_t)K * 8));
         CK(ensure(ctx->mpmm_q, (size_t)R * K * 8));
@@ -511,9 +515,9 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(ensure(ctx->tbmax, (size_t)TT * K * 4));
         CK(ensure(ctx->qbmin, (size_t)nq * K * 4));
         CK(ensure(ctx->qbmax, (size_t)nq * K * 4));
-        launch_pick_pivots(Et, N, d, norm, K, pivot, P<float>(ctx->mpP), s);
+        launch_pick_pivots(Et, NT, d, norm, K, pivot, P<float>(ctx->mpP), s);
         LAUNCHED(1);
-        launch_mp_keys(Et, nullptr, N, 1, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkt), P<unsigned>(ctx->mpmm_t),
+        launch_mp_keys(Et, nullptr, NT, 1, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkt), P<unsigned>(ctx->mpmm_t),
                        &dctr->nonfinite, s);
         LAUNCHED(2);
         launch_mp_keys(E, Rel, N, R, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q),
@@ -522,15 +526,15 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(cudaEventRecord(ctx->ev[EV_KEYS], s));
         // ---- a3: Morton-order sorts (tiles compact in pivot space)
         const int bits = 8;  // per pivot, over the first min(K, MP_SORT_PIVOTS) pivots
-        launch_mp_morton(P<float>(ctx->mpkt), P<unsigned>(ctx->mpmm_t), 1, N, K, bits,
+        launch_mp_morton(P<float>(ctx->mpkt), P<unsigned>(ctx->mpmm_t), 1, NT, K, bits,
                          P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
         LAUNCHED(1);
         const int code_bits = bits * (K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS);
-        radix_sort_u64_segments(1, N, code_bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
+        radix_sort_u64_segments(1, NT, code_bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
                                 P<unsigned long long>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
                                 ctx->scan_tmp.p, s, &ctx->launches);
         LAUNCHED(0);
-        CK(cudaMemcpyAsync(ctx->tperm.p, ctx->sv0.p, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(ctx->tperm.p, ctx->sv0.p, (size_t)NT * 4, cudaMemcpyDeviceToDevice, s));
         launch_mp_morton(P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q), R, N, K, bits,
                          P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
         LAUNCHED(1);
@@ -541,7 +545,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(cudaMemcpyAsync(ctx->qperm.p, ctx->sv0.p, NR * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaEventRecord(ctx->ev[EV_SORT], s));
         // ---- a4: K-dim tile boxes and the L_inf test of every tile pair
-        launch_mp_boxes(P<float>(ctx->mpkt), P<unsigned>(ctx->tperm), 1, N, BN, TT, K, P<float>(ctx->tbmin),
+        launch_mp_boxes(P<float>(ctx->mpkt), P<unsigned>(ctx->tperm), 1, NT, BN, TT, K, P<float>(ctx->tbmin),
                         P<float>(ctx->tbmax), s);
         launch_mp_boxes(P<float>(ctx->mpkq), P<unsigned>(ctx->qperm), R, N, bq, QT, K, P<float>(ctx->qbmin),
                         P<float>(ctx->qbmax), s);
@@ -600,8 +604,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     long long g_max_items = 0;
     if (gather || gather_tc) {
         g_max_items = h1.c.my_cost * (BN / GB > 1 ? BN / GB : 1);  // blocks (and items) <= tiles x rows per block
-        CK(ensure(ctx->Ts, (size_t)(N + 1) * Kpad * 4));
-        CK(ensure(ctx->tks, (size_t)N * MP_MAX * 4));
+        CK(ensure(ctx->Ts, (size_t)(NT + 1) * Kpad * 4));
+        CK(ensure(ctx->tks, (size_t)NT * MP_MAX * 4 + 4));
         CK(ensure(ctx->gblk, (size_t)nq * 8));
         CK(ensure(ctx->granges, (size_t)nq * 8));
         CK(ensure(ctx->glist, (size_t)list_span * BN * 4 + 4));  // laid out at BN x the tile-list offsets
@@ -610,15 +614,15 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(ensure(ctx->item_cum, (size_t)g_max_items * 8));
         CK(ensure(ctx->scan_tmp, scan_tmp_bytes((size_t)std::max<long long>(g_max_items, nq))));
         if (gather_tc) {
-            CK(ensure(ctx->tsc, (size_t)N * 16));
+            CK(ensure(ctx->tsc, (size_t)NT * 16 + 16));
             CK(ensure(ctx->gT2, (size_t)list_span * GB * 4 + 4));
             CK(ensure(ctx->gtst, (size_t)list_span * 8));
         }
-        launch_stage_rows(Et, P<int>(ctx->tperm), P<float>(ctx->mpkt), N, d, Kpad, K, P<float>(ctx->Ts),
+        launch_stage_rows(Et, P<int>(ctx->tperm), P<float>(ctx->mpkt), NT, d, Kpad, K, P<float>(ctx->Ts),
                           P<float>(ctx->tks), gather_tc ? P<float4>(ctx->tsc) : nullptr, s);
         if (gather_tc) {
             CK(ensure(ctx->tmapbuf, sizeof(CUtensorMap)));
-            if (make_tails_tmap(&ctx->tmap_host, P<float>(ctx->Ts), N + 1, Kpad)) {
+            if (make_tails_tmap(&ctx->tmap_host, P<float>(ctx->Ts), NT + 1, Kpad)) {
                 set_err(ctx, "cuTensorMapEncodeTiled failed for the gathered tails");
                 return KGC_ECUDA;
             }
@@ -628,7 +632,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(cudaMemsetAsync(ctx->nitem.p, 0, (size_t)nq * 4, s));
         CK(cudaMemsetAsync(ctx->item_tiles.p, 0, (size_t)g_max_items * 8, s));
         launch_gather_tails(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tks), P<int>(ctx->tile_list),
-                            P<long long>(ctx->cum), P<int2>(ctx->ranges), dctr, N, BN, K, feps, mp_relm(d), chunk, nq,
+                            P<long long>(ctx->cum), P<int2>(ctx->ranges), dctr, NT, BN, K, feps, mp_relm(d), chunk, nq,
                             P<long long>(ctx->gblk), P<int2>(ctx->granges), P<int>(ctx->nitem), P<int>(ctx->glist),
                             gather_tc ? P<float4>(ctx->tsc) : nullptr, gather_tc ? P<float>(ctx->gT2) : nullptr,
                             gather_tc ? P<float2>(ctx->gtst) : nullptr, cyc ? ctx->opt.world : 0, ctx->opt.rank,
@@ -680,7 +684,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         if (half) {
             CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * bq * Kpad * 2));
             CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * bq * 16));
-            launch_stage_half(Et, nullptr, P<int>(ctx->tperm), N, d, Kpad, BN, 1, 0, TT, feps, gam, ctx->Tp.p, nullptr,
+            launch_stage_half(Et, nullptr, P<int>(ctx->tperm), NT, d, Kpad, BN, 1, 0, TT, feps, gam, ctx->Tp.p, nullptr,
                               P<float>(ctx->T2), s);
             launch_stage_half(E, Rel, P<int>(ctx->qperm), N, d, Kpad, bq, QT, tq0, tq1 - tq0, feps, gam, ctx->Qp.p,
                               P<float4>(ctx->qs), nullptr, s);
@@ -694,7 +698,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                                  P<float>(ctx->Qp), P<float4>(ctx->qs), s, cyc ? ctx->opt.world : 0, ctx->opt.rank);
             LAUNCHED(1);
         } else {
-            launch_stage_tails(Et, P<int>(ctx->tperm), N, d, Kpad, BN, TT, tc2 ? 2 : (tc ? 1 : 0), P<float>(ctx->Tp),
+            launch_stage_tails(Et, P<int>(ctx->tperm), NT, d, Kpad, BN, TT, tc2 ? 2 : (tc ? 1 : 0), P<float>(ctx->Tp),
                                P<float>(ctx->T2), P<float2>(ctx->tstile), s);
             LAUNCHED(1);
             if (!tc) {  // the tensor-core engine forms its query tiles on the fly
@@ -742,6 +746,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.bn = BN;
         tp.tq0 = tq0;
         tp.N = (int)N;
+        tp.Nt = (int)NT;
         tp.theta = feps;
         tp.gam = gam;
         tp.Rt = P<float>(ctx->T2);
@@ -803,7 +808,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             else
                 launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, P<int>(ctx->qperm), P<int>(ctx->tperm),
                               E, Rel, N, QT, bq, d, norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p),
-                              &dctr->res, ctx->res_cap, ctx->num_sms, s, r_off);
+                              &dctr->res, ctx->res_cap, ctx->num_sms, s, r_off, NT, ex.t_off);
             LAUNCHED(1);
         }
         CK(cudaEventRecord(ctx->ev[EV_VERIFY], s));
@@ -947,7 +952,24 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
     cudaSetDevice(ctx->device);
     int rc = KGC_OK;
     bool did_split = false;
-    if (ctx->opt.world > 1 && ctx->opt.split == 0) {
+    if (ctx->opt.world > 1 && ctx->opt.tail_shard) {
+        // Partition-based join (§4.7): this rank's tail partition against every
+        // query (all query tiles owned: the fixed range [0, inf)); results carry global tail ids.
+        const long long t0 = N * ctx->opt.rank / ctx->opt.world, t1 = N * (ctx->opt.rank + 1) / ctx->opt.world;
+        if (t1 <= t0) {
+            memset(&ctx->st, 0, sizeof ctx->st);
+            ctx->st.N = N; ctx->st.R = R; ctx->st.d = d; ctx->st.norm = norm; ctx->st.eps = eps;
+            ctx->st.rank = ctx->opt.rank; ctx->st.world = ctx->opt.world;
+            ctx->st.triplets = (double)N * (double)N * (double)R;
+            ctx->n_results = 0;
+            ctx->have_join = true;
+        } else {
+            JoinExtra ex;
+            ex.Nt = t1 - t0;
+            ex.t_off = t0;
+            rc = join_impl(ctx, E, Rel, N, R, d, norm, eps, 0, 0, LLONG_MAX, R, ex);
+        }
+    } else if (ctx->opt.world > 1 && ctx->opt.split == 0) {
         did_split = true;
         // Rank-local split: query-tile ranges balanced by an estimated per-relation cost
         // (launch_split_estimate); each rank then preprocesses only the relations its range touches.

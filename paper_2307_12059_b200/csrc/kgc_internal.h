@@ -50,7 +50,8 @@ struct TileParams {
     int Kpad;
     int bq, bn;             // query / tail tile rows of the plan
     int tq0;                // first staged query tile
-    int N;                  // tails (valid columns are < N)
+    int N;                  // entities (query rows per relation)
+    int Nt;                 // tails (valid sorted tail positions are < Nt; a partition of E, or N)
     float theta;
     float eta;              // tensor-core accumulation error coefficient
     float gam;              // FP16 engine: relative error factor (1 + gamma)
@@ -182,6 +183,6 @@ void launch_compact_res_le(const KgcTripletDev* res, long long n, float theta, i
 void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap,
                    const int* qperm, const int* tperm, const float* E, const float* Rel, long long N, int QT,
                    int bq, int d, int norm, float theta, KgcTripletDev* out, unsigned long long* res_count,
-                   long long res_cap, int num_sms, cudaStream_t s, int r_off);
+                   long long res_cap, int num_sms, cudaStream_t s, int r_off, long long Nt = -1, long long t_off = 0);
 
 }  // namespace kgc

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__((TBM / TM) * (TBN / TN)) tiles_simt_kernel(Til
                 const int colb = j * TBN + tx * TN;
 #pragma unroll
                 for (int b = 0; b < TN; ++b)
-                    if (colb + b >= p.N)
+                    if (colb + b >= p.Nt)
 #pragma unroll
                         for (int a = 0; a < TM; ++a) hit &= ~(1ull << (a * TN + b));
                 unsigned long long slot = warp_reserve(__popcll(hit), p.cand_count);
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(256, 1) tiles_half_l1_kernel(TileParams p) {
             if (__any_sync(0xffffffffu, hit != 0)) {
 #pragma unroll
                 for (int b = 0; b < 8; ++b)
-                    if (colb + b >= p.N) hit &= ~(0x0101010101010101ull << b);
+                    if (colb + b >= p.Nt) hit &= ~(0x0101010101010101ull << b);
                 unsigned long long slot = warp_reserve(__popcll(hit), p.cand_count);
                 while (hit) {
                     const int ab = __ffsll(hit) - 1;
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(TB, MINB) tiles_gather_kernel(TileParams p) {
 #pragma unroll
                 for (int b = 0; b < TN; ++b) {
                     const unsigned long long colm = 0x0101010101010101ull << b;  // column b of the micro-tile
-                    if ((hit & colm) && __ldg(seg + b * GX) >= p.N) hit &= ~colm;  // sentinel padding
+                    if ((hit & colm) && __ldg(seg + b * GX) >= p.Nt) hit &= ~colm;  // sentinel padding
                 }
                 unsigned long long slot = warp_reserve(__popcll(hit), p.cand_count);
                 while (hit) {

@@ -29,7 +29,8 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
                                                         const int* __restrict__ tperm, const float* __restrict__ E,
                                                         const float* __restrict__ Rel, long long N, int QT, int bq,
                                                         int d, double theta, KgcTripletDev* __restrict__ out,
-                                                        unsigned long long* res_count, long long res_cap, int r_off) {
+                                                        unsigned long long* res_count, long long res_cap, int r_off,
+                                                        long long Nt, long long t_off) {
     long long nc = (long long)*cand_count;
     if (nc > cand_cap) nc = cand_cap;
     const int lane = threadIdx.x & 31, g = lane >> 3, s = lane & 7;
@@ -45,11 +46,11 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
             const int2 cv = cand[idx];
             const long long rr = cv.x / rows_per_rel;
             const long long pos = cv.x - rr * rows_per_rel;
-            valid = pos < N && cv.y < N;
+            valid = pos < N && cv.y < Nt;
             if (valid) {
                 r = (int)rr;
                 h = qperm[rr * N + pos];
-                t = tperm[cv.y];
+                t = (int)(tperm[cv.y] + t_off);  // tail partition: rows [t_off, t_off + Nt) of E
             }
         }
         // ---- stage 2: distances, 8 lanes per candidate
@@ -106,12 +107,12 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
 void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap, const int* qperm,
                    const int* tperm, const float* E, const float* Rel, long long N, int QT, int bq, int d, int norm,
                    float theta, KgcTripletDev* out, unsigned long long* res_count, long long res_cap, int num_sms,
-                   cudaStream_t s, int r_off) {
+                   cudaStream_t s, int r_off, long long Nt, long long t_off) {
     const bool vec4 = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(E) | reinterpret_cast<uintptr_t>(Rel)) % 16 == 0);
     auto kern = norm == 1 ? (vec4 ? verify_kernel<1, true> : verify_kernel<1, false>)
                           : (vec4 ? verify_kernel<2, true> : verify_kernel<2, false>);
     kern<<<num_sms * 8, 256, 0, s>>>(cand, cand_count, cand_cap, qperm, tperm, E, Rel, N, QT, bq, d, (double)theta, out,
-                                     res_count, res_cap, r_off);
+                                     res_count, res_cap, r_off, Nt < 0 ? N : Nt, t_off);
 }
 
 }  // namespace kgc

@@ -34,7 +34,7 @@ class kgc_options(ctypes.Structure):
                 ("prune", ctypes.c_int32), ("pivot", ctypes.c_int32), ("l2_engine", ctypes.c_int32),
                 ("chunk_tiles", ctypes.c_int32), ("pivots", ctypes.c_int32),
                 ("result_capacity", ctypes.c_int64), ("stream", ctypes.c_void_p), ("l1_engine", ctypes.c_int32),
-                ("split", ctypes.c_int32)]
+                ("split", ctypes.c_int32), ("tail_shard", ctypes.c_int32)]
 
 
 class kgc_stats_t(ctypes.Structure):

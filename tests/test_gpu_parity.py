@@ -448,3 +448,36 @@ def test_cyclic_split_invariance_multipivot(norm, opts, world):
     assert sum(len(s) for s in sets) == len(set().union(*sets))
     assert set().union(*sets) == keyset(full)
     assert sum(p[1]["tile_pairs_mine"] for p in parts) == parts[0][1]["tile_pairs_surviving"]
+
+
+# ------------------------------------------------- partition-based join (§4.7)
+@pytest.mark.parametrize("norm,opts", [(2, dict()), (2, dict(l2_engine=3)), (2, dict(l2_engine=2)),
+                                       (2, dict(pivots=8)), (2, dict(pivots=8, l2_engine=4)), (1, dict()),
+                                       (1, dict(pivots=8)), (1, dict(l1_engine=1))])
+@pytest.mark.parametrize("world", [2, 3])
+def test_tail_partition_join(norm, opts, world):
+    """tail_shard = 1: rank k joins every query against tails [kN/W, (k+1)N/W) only (PAPER.md:419-422);
+    each shard's tails lie in its partition, shards are disjoint, their union is the full set and
+    matches the oracle."""
+    N = 3000
+    E, Rel = generate(N, 5, 40, seed=35)
+    eps = theta_for(E, Rel, norm, 2e-3)
+    full, _ = gpu_join(E, Rel, norm, eps, **opts)
+    parts = [gpu_join(E, Rel, norm, eps, rank=r, world=world, tail_shard=1, device_inputs=(r != 1), **opts)
+             for r in range(world)]
+    for r, (res, st) in enumerate(parts):
+        t0, t1 = N * r // world, N * (r + 1) // world
+        assert np.all((res["t"] >= t0) & (res["t"] < t1)), r
+        assert st["results"] == res.size
+    sets = [keyset(p[0]) for p in parts]
+    assert sum(len(s) for s in sets) == len(set().union(*sets))
+    assert set().union(*sets) == keyset(full)
+    check_parity(E, Rel, norm, eps, np.concatenate([p[0] for p in parts]))
+
+
+def test_tail_partition_more_ranks_than_tails():
+    E, Rel = generate(2, 3, 4, seed=36)
+    eps = theta_for(E, Rel, 2, 0.3)
+    full, _ = gpu_join(E, Rel, 2, eps)
+    parts = [gpu_join(E, Rel, 2, eps, rank=r, world=5, tail_shard=1)[0] for r in range(5)]
+    assert set().union(*[keyset(p) for p in parts]) == keyset(full)
