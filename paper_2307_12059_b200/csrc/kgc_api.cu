@@ -49,7 +49,7 @@ struct kgc_ctx {
     DevBuf E, Rel, pivot, kt, kq, mm_t, mm_q, sk0, sv0, sk1, sv1, counts, scan_tmp, qperm, qskey, tperm, tskey, tmin,
         tmax, cmax, cmin, ranges, cost, cum, nitem, item_off, items, item_tiles, item_cum, Qp, qs, Tp, T2, tstile, cand,
         res, ctr, est_hist, est_cost, mpP, mpkt, mpkq, mpmm_t, mpmm_q, mpc0, mpc1, tbmin, tbmax, qbmin, qbmax, tile_list,
-        tk_sample, tk_sel, tk_cnt, Ts, tks, gblk, granges, glist, tsc, gT2, gtst, tmapbuf, se_w, se_a64, se_b64, se_af, se_bf, se_zero, se_res, se_max;
+        tk_sample, tk_sel, tk_cnt, Ts, tks, gblk, granges, glist, tsc, gT2, gtst, tmapbuf, fz, frt, frn, fzero, se_w, se_a64, se_b64, se_af, se_bf, se_zero, se_res, se_max;
     long long cand_cap = 0, res_cap = 0;
     long long n_results = -1;
     kgc_stats_t st{};
@@ -63,6 +63,7 @@ struct kgc_ctx {
     long long list_len = 0;     // multi-pivot tile-list length of this shard
     long long glist_len = 0;    // gathered-tail list length of this shard (entries)
     CUtensorMap tmap_host;      // tensor map over the sorted tails (gathered tensor-core engine)
+    std::vector<int4> fitems;   // relation-factored engine: work items built on the host
     bool have_join = false;
 };
 
@@ -227,7 +228,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 4 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2 || o.tail_shard < 0 || o.tail_shard > 1) {
+        o.l2_engine > 5 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2 || o.tail_shard < 0 || o.tail_shard > 1) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -378,7 +379,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const bool gtc_req = tc && K_plan > 1 && use_gather_tc(ctx);  // gathered tensor-core blocks requested
     const long long NT = ex.Nt >= 0 ? ex.Nt : N;  // tail rows (a tail partition, or all N)
     const bool tc2 = !gtc_req && use_tc2(ctx, norm, d, NT);
-    if (norm == 2 && (ctx->opt.l2_engine == 1 || ctx->opt.l2_engine == 3 || ctx->opt.l2_engine == 4) && !tc) {
+    if (norm == 2 && (ctx->opt.l2_engine == 1 || ctx->opt.l2_engine == 3 || ctx->opt.l2_engine >= 4) && !tc) {
         set_err(ctx, "l2_engine=%d (tcgen05) supports d <= %d", ctx->opt.l2_engine, TC_MAX_KPAD);
         return KGC_EINVAL;
     }
@@ -460,6 +461,135 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     hc.tq_end = 0;
     CK(cudaMemcpyAsync(ctx->ctr.p, &hc, sizeof hc, cudaMemcpyHostToDevice, s));
     DevCounters* dctr = P<DevCounters>(ctx->ctr);
+
+    // ---- relation-factored L2 (l2_engine 5): one G = H T^T tile serves every
+    // relation; no pivots, sorts or pruning (it is the engine for data where tiles do not prune)
+    if (norm == 2 && ctx->opt.l2_engine == 5 && tc && ex.Nt < 0 && !ex.A64 && !ex.Et) {
+        const long long ntpad = (long long)TT * BN_TC;
+        CK(ensure(ctx->tperm, (size_t)ntpad * 4));
+        CK(ensure(ctx->qperm, (size_t)N * 4));
+        launch_iota(P<int>(ctx->tperm), N, s);  // natural order on both sides
+        launch_iota(P<int>(ctx->qperm), N, s);
+        CK(ensure(ctx->fz, (size_t)R * N * 4));
+        CK(ensure(ctx->frt, (size_t)R * ntpad * 4));
+        CK(ensure(ctx->frn, (size_t)R * 4));
+        CK(ensure(ctx->fzero, (size_t)d * 4));
+        CK(cudaMemsetAsync(ctx->fzero.p, 0, (size_t)d * 4, s));
+        launch_factored_tables(E, Rel, P<int>(ctx->tperm), N, R, d, feps, ntpad, P<float>(ctx->fz),
+                               P<float>(ctx->frt), P<float>(ctx->frn), &dctr->nonfinite, s);
+        LAUNCHED(3);
+        CK(cudaEventRecord(ctx->ev[EV_KEYS], s));
+        CK(cudaEventRecord(ctx->ev[EV_SORT], s));
+        // this rank's head tiles (uniform dense work: a contiguous split), every tail tile
+        const long long ha = (long long)QT * ctx->opt.rank / ctx->opt.world;
+        const long long hb = (long long)QT * (ctx->opt.rank + 1) / ctx->opt.world;
+        ctx->fitems.clear();
+        for (long long q = ha; q < hb; ++q)
+            for (int j0 = 0; j0 < TT; j0 += chunk)
+                ctx->fitems.push_back(make_int4((int)q, j0, std::min(TT - 1, j0 + chunk - 1), -1));
+        const long long n_items = (long long)ctx->fitems.size();
+        st.tile_pairs_total = (long long)QT * TT;
+        st.tile_pairs_surviving = st.tile_pairs_total;
+        st.tile_pairs_mine = (hb - ha) * TT;
+        st.work_items_mine = n_items;
+        st.engine = 7;
+        if (n_items > 0) {
+            CK(ensure(ctx->items, (size_t)n_items * 16));
+            CK(cudaMemcpyAsync(ctx->items.p, ctx->fitems.data(), (size_t)n_items * 16, cudaMemcpyHostToDevice, s));
+        }
+        CK(cudaEventRecord(ctx->ev[EV_RANGES], s));
+        CK(ensure(ctx->Tp, (size_t)TT * BN * Kpad * 4));
+        CK(ensure(ctx->T2, (size_t)TT * BN * 4));
+        CK(ensure(ctx->tstile, (size_t)TT * 8));
+        launch_stage_tails(E, P<int>(ctx->tperm), N, d, Kpad, BN, TT, 1, P<float>(ctx->Tp), P<float>(ctx->T2),
+                           P<float2>(ctx->tstile), s);
+        LAUNCHED(1);
+        CK(cudaEventRecord(ctx->ev[EV_STAGE], s));
+        if (ctx->cand_cap == 0) ctx->cand_cap = 1 << 20;
+        if (ctx->res_cap == 0) ctx->res_cap = ctx->opt.result_capacity > 0 ? ctx->opt.result_capacity : (1 << 20);
+        long long cand_n = 0, res_n = 0;
+        for (;;) {
+            CK(ensure(ctx->cand, (size_t)ctx->cand_cap * 8));
+            CK(ensure(ctx->res, (size_t)ctx->res_cap * 16));
+            CK(cudaMemsetAsync(&dctr->cand, 0, 16, s));
+            TileParams tp{};
+            tp.Tp = P<float>(ctx->Tp);
+            tp.T2 = P<float>(ctx->T2);
+            tp.tstile = P<float2>(ctx->tstile);
+            tp.items = P<int4>(ctx->items);
+            tp.n_items = n_items;
+            tp.total_tiles = st.tile_pairs_mine;
+            tp.Kpad = Kpad;
+            tp.bq = bq;
+            tp.bn = BN;
+            tp.N = (int)N;
+            tp.Nt = (int)N;
+            tp.theta = feps;
+            tp.eta = (float)((Kpad / 8) * 3.814697265625e-06);
+            tp.cand = P<int2>(ctx->cand);
+            tp.cand_count = &dctr->cand;
+            tp.cand_cap = ctx->cand_cap;
+            tp.E = E;
+            tp.Rel = P<float>(ctx->fzero);  // builders form fl32(h + 0) = h
+            tp.qperm = P<int>(ctx->qperm);
+            tp.d = d;
+            tp.QT = QT;
+            tp.fz = P<float>(ctx->fz);
+            tp.frt = P<float>(ctx->frt);
+            tp.frn = P<float>(ctx->frn);
+            tp.R = (int)R;
+            tp.ntpad = ntpad;
+            if (n_items > 0) {
+                launch_tiles_tc_factored(tp, ctx->num_sms, s);
+                LAUNCHED(1);
+            }
+            CK(cudaEventRecord(ctx->ev[EV_TILES], s));
+            if (n_items > 0) {
+                launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, nullptr, nullptr, E, Rel, N, QT, bq, d,
+                              norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p), &dctr->res, ctx->res_cap,
+                              ctx->num_sms, s, r_off);
+                LAUNCHED(1);
+            }
+            CK(cudaEventRecord(ctx->ev[EV_VERIFY], s));
+            unsigned long long hcnt[2];
+            unsigned int nf = 0;
+            CK(cudaMemcpyAsync(hcnt, &dctr->cand, 16, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(&nf, &dctr->nonfinite, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (nf) {
+                set_err(ctx, "non-finite value in E or Rel");
+                return KGC_EDATA;
+            }
+            cand_n = (long long)hcnt[0];
+            res_n = (long long)hcnt[1];
+            if (cand_n > ctx->cand_cap) {
+                ctx->cand_cap = cand_n + cand_n / 4 + 1024;
+                st.reruns++;
+                continue;
+            }
+            if (res_n > ctx->res_cap) {
+                ctx->res_cap = res_n + res_n / 4 + 1024;
+                st.reruns++;
+                continue;
+            }
+            break;
+        }
+        st.candidates = cand_n;
+        st.results = res_n;
+        st.launches = ctx->launches;
+        float ms[EV_COUNT] = {};
+        for (int k = 1; k < EV_COUNT; ++k) cudaEventElapsedTime(&ms[k], ctx->ev[k - 1], ctx->ev[k]);
+        st.ms_h2d = ms[EV_H2D];
+        st.ms_keys = ms[EV_KEYS];
+        st.ms_ranges = ms[EV_RANGES];
+        st.ms_stage = ms[EV_STAGE];
+        st.ms_tiles = ms[EV_TILES];
+        st.ms_recheck = ms[EV_VERIFY];
+        cudaEventElapsedTime(&st.ms_total, ctx->ev[EV_START], ctx->ev[EV_VERIFY]);
+        ctx->n_results = res_n;
+        ctx->have_join = true;
+        return KGC_OK;
+    }
 
     const double* pivot = nullptr;
     if (ctx->opt.pivot == 1) {
@@ -969,7 +1099,7 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
             ex.t_off = t0;
             rc = join_impl(ctx, E, Rel, N, R, d, norm, eps, 0, 0, LLONG_MAX, R, ex);
         }
-    } else if (ctx->opt.world > 1 && ctx->opt.split == 0) {
+    } else if (ctx->opt.world > 1 && ctx->opt.split == 0 && !(norm == 2 && ctx->opt.l2_engine == 5)) {
         did_split = true;
         // Rank-local split: query-tile ranges balanced by an estimated per-relation cost
         // (launch_split_estimate); each rank then preprocesses only the relations its range touches.

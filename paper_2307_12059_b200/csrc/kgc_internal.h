@@ -73,6 +73,12 @@ struct TileParams {
     const float2* gtst;           // tensor-core gathered blocks: per block {max ||t||, max ||t - tf32(t)||}
     const void* tmap;             // tensor-core gathered blocks: CUtensorMap over Ts (device memory)
     int gb;                       // SIMT gathered blocks: tails per block (32 or 64)
+    // relation-factored tensor-core engine (tiles_tc.cu, MODE 2)
+    const float* fz;              // [R][N] (||h + r||^2 - theta^2) / 2 rounded down
+    const float* frt;             // [R][ntpad] r.t (sorted tail positions; 0 past N)
+    const float* frn;             // [R] ||r|| rounded up
+    int R;
+    long long ntpad;
     const long long* dn_items;    // device: work items of this shard
     const long long* dtotal;      // device: blocks of this shard (balanced CTA ranges)
     unsigned long long* prof;     // experiment: wait-cycle counters (KGC_GT_PROF), else nullptr
@@ -155,6 +161,11 @@ __device__ __forceinline__ int item_tile(const int4& w, int j, const int* __rest
 int  tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);
 void launch_tiles_tc(const TileParams& p, int num_sms, cudaStream_t s);
 void launch_tiles_tc_gather(const TileParams& p, int num_sms, cudaStream_t s);
+void launch_tiles_tc_factored(const TileParams& p, int num_sms, cudaStream_t s);
+void launch_factored_tables(const float* E, const float* Rel, const int* tperm, long long N, long long R, int d,
+                            float theta, long long ntpad, float* fz, float* frt, float* frn, unsigned int* nonfinite,
+                            cudaStream_t s);
+void launch_iota(int* out, long long n, cudaStream_t s);
 int  tc_gather_ok(int Kpad);  // the gathered tensor-core engine needs 32-wide K-chunks
 int  tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);
 void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s);

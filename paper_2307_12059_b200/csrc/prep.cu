@@ -1002,4 +1002,57 @@ void launch_stage_queries(const float* E, const float* Rel, const int* qperm, lo
                                                       nullptr, nullptr, bq, cyc_world, cyc_rank);
 }
 
+// ------------------------------------------------ relation-factored L2 tables
+// (tiles_tc.cu MODE 2).  One warp per (relation, row), lanes
+// over k, FP64 sums of the fp32 inputs:
+//   fz[r][h]  = (||E_h + Rel_r||^2 - theta^2) / 2, rounded down (h + r formed in FP64)
+//   frt[r][j] = Rel_r . E_t for the sorted tail t = tperm[j], rounded to nearest (0 for j >= N)
+//   frn[r]    = ||Rel_r||, rounded up
+__global__ void factored_tables_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
+                                       const int* __restrict__ tperm, long long N, long long R, int d, double theta,
+                                       long long ntpad, float* __restrict__ fz, float* __restrict__ frt,
+                                       float* __restrict__ frn, unsigned int* __restrict__ nonfinite) {
+    const int lane = threadIdx.x & 31;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long total = R * ntpad;
+    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < total; w += nw) {
+        const long long r = w / ntpad, j = w - r * ntpad;
+        const float* rel = Rel + r * d;
+        double z = 0.0, rt = 0.0, rr = 0.0;
+        if (j < N) {
+            const float* eh = E + j * d;                    // fz: natural head order
+            const float* et = E + (long long)tperm[j] * d;  // frt: sorted tail order
+            for (int k = lane; k < d; k += 32) {
+                const double a = (double)eh[k] + (double)rel[k];
+                z += a * a;
+                rt += (double)rel[k] * (double)et[k];
+                if (j == 0) rr += (double)rel[k] * (double)rel[k];
+            }
+        }
+        z = warp_sum_d(z);
+        rt = warp_sum_d(rt);
+        rr = warp_sum_d(rr);
+        if (lane == 0) {
+            if (j < N && !(isfinite(z) && isfinite(rt))) atomicOr(nonfinite, 1u);  // any non-finite E or Rel
+            if (j < N) fz[r * N + j] = __double2float_rd(0.5 * (z - theta * theta));
+            frt[r * ntpad + j] = j < N ? __double2float_rn(rt) : 0.f;
+            if (j == 0) frn[r] = __double2float_ru(sqrt(rr));
+        }
+    }
+}
+
+__global__ void iota_kernel(int* out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = (int)i;
+}
+
+void launch_factored_tables(const float* E, const float* Rel, const int* tperm, long long N, long long R, int d,
+                            float theta, long long ntpad, float* fz, float* frt, float* frn, unsigned int* nonfinite,
+                            cudaStream_t s) {
+    factored_tables_kernel<<<grid_for(R * ntpad * 32, 256), 256, 0, s>>>(E, Rel, tperm, N, R, d, (double)theta, ntpad,
+                                                                       fz, frt, frn, nonfinite);
+}
+
+void launch_iota(int* out, long long n, cudaStream_t s) { iota_kernel<<<grid_for(n, 256), 256, 0, s>>>(out, n); }
+
 }  // namespace kgc

@@ -75,8 +75,15 @@ int tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
 // epilogue takes ||t||^2/2 and the block's guard-band maxima from the list build.
 // (A warp of 16-byte cp.async pieces was measured 4x slower than contiguous tiles
 // on c3: one warp cannot keep enough scattered loads in flight.)
-template <bool GATHER>
+// MODE 2 (FACTORED): the relation-factored L2 join for low-pruning
+// data.  D^2(h, r, t) = ||h + r||^2 + ||t||^2 - 2 h.t - 2 r.t (TransE), so a
+// 128 x 256 tile of G = H T^T (heads in natural order, every tail tile, no relation)
+// serves all R relations: per relation the epilogue adds r.t (table) and tests against
+// (||h + r||^2 - theta^2) / 2 (table), widened by the TF32 band of G and the FP32
+// rounding of the two additions.
+template <int MODE>
 __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, int a_stages, int b_stages, int KC) {
+    constexpr bool GATHER = MODE == 1, FACT = MODE == 2;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int Kpad = p.Kpad;
     const uint32_t A_FLOATS = BM * Kpad;
@@ -233,7 +240,79 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
             const int rowid = w.x * BM + i;
             // theta_f covers q = fl32(h + r) vs the exact h + r (|dq_k| <= 2^-24 |q_k|)
             const float thf = p.theta * (1.0f + 2.44140625e-04f) + 2.384185791015625e-07f * Qn;
-            for (int jj = w.y; jj <= w.z; ++jj) {
+            if (FACT) {
+                const long long h = (long long)w.x * BM + i;
+                const bool hv = h < p.N;
+                const long long rows_per_rel = (long long)p.QT * BM;
+                for (int j = w.y; j <= w.z; ++j) {
+                    const float2 tv = p.tstile[j];
+                    const float Tm = tv.x, Tdm = tv.y;
+                    const float eb = Qd * Tm + Qn * Tdm + Qd * Tdm + p.eta * (Qn + Qd) * (Tm + Tdm);
+                    const float* t2row = p.T2 + (size_t)j * BN_TC + col0;
+                    TC_WAIT(5, &acc_full[acc], accph);
+                    tc_fence_after();
+                    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_TC + col0);
+                    for (int ch = 0; ch < 4; ++ch) {
+                        uint32_t ra[32];
+                        tmem_ld32_nowait(tbase + 32 * ch, ra);
+                        tmem_wait_ld();
+                        if (ch == 3) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+                        }
+                        float v[32];  // acc - ||t||^2 / 2 (padding columns: -3e38)
+                        const float4* t2 = reinterpret_cast<const float4*>(t2row + ch * 32);
+#pragma unroll
+                        for (int u4 = 0; u4 < 8; ++u4) {
+                            const float4 tt = __ldg(t2 + u4);
+                            v[4 * u4 + 0] = __uint_as_float(ra[4 * u4 + 0]) - tt.x;
+                            v[4 * u4 + 1] = __uint_as_float(ra[4 * u4 + 1]) - tt.y;
+                            v[4 * u4 + 2] = __uint_as_float(ra[4 * u4 + 2]) - tt.z;
+                            v[4 * u4 + 3] = __uint_as_float(ra[4 * u4 + 3]) - tt.w;
+                        }
+                        const long long colb = (long long)j * BN_TC + col0 + ch * 32;
+                        for (int rel = 0; rel < p.R; ++rel) {
+                            // S' = fl(fl(acc - T2) + fl(r.t)) is within eb + 2^-21 (Hn + Rn + Tm)^2 of
+                            // h.t + r.t - ||t||^2/2; a hit has S >= Z = (||h + r||^2 - theta^2)/2 >= zd
+                            const float zd = hv ? __ldg(p.fz + (size_t)rel * p.N + h) : 3e38f;
+                            const float rn = __ldg(p.frn + rel);
+                            const float e2 = Qn + rn + Tm;
+                            const float err = eb + 4.76837158203125e-07f * e2 * e2;
+                            const float c = zd - err * 1.0000010f - 2.384185791015625e-07f * fabsf(zd);
+                            const float4* rt4 = reinterpret_cast<const float4*>(p.frt + (size_t)rel * p.ntpad + colb);
+                            float m0 = -3e38f, m1 = -3e38f;
+#pragma unroll
+                            for (int u4 = 0; u4 < 8; ++u4) {
+                                const float4 rt = __ldg(rt4 + u4);
+                                m0 = max3_f32(m0, v[4 * u4 + 0] + rt.x, v[4 * u4 + 1] + rt.y);
+                                m1 = max3_f32(m1, v[4 * u4 + 2] + rt.z, v[4 * u4 + 3] + rt.w);
+                            }
+                            if (__any_sync(0xffffffffu, fmaxf(m0, m1) >= c)) {
+                                uint32_t hit = 0;
+#pragma unroll
+                                for (int u4 = 0; u4 < 8; ++u4) {
+                                    const float4 rt = __ldg(rt4 + u4);
+                                    hit |= (uint32_t)(v[4 * u4 + 0] + rt.x >= c) << (4 * u4 + 0);
+                                    hit |= (uint32_t)(v[4 * u4 + 1] + rt.y >= c) << (4 * u4 + 1);
+                                    hit |= (uint32_t)(v[4 * u4 + 2] + rt.z >= c) << (4 * u4 + 2);
+                                    hit |= (uint32_t)(v[4 * u4 + 3] + rt.w >= c) << (4 * u4 + 3);
+                                }
+                                unsigned long long slot = warp_reserve(__popc(hit), p.cand_count);
+                                while (hit) {
+                                    const int u = __ffs(hit) - 1;
+                                    if (slot < (unsigned long long)p.cand_cap)
+                                        p.cand[slot] = make_int2((int)(rel * rows_per_rel + h), (int)(colb + u));
+                                    ++slot;
+                                    hit &= hit - 1;
+                                }
+                            }
+                        }
+                    }
+                    if (++acc == 2) { acc = 0; accph ^= 1; }
+                }
+            }
+            if (!FACT) for (int jj = w.y; jj <= w.z; ++jj) {
                 // gathered: j is the block (the tile list's offset + jj), else the tail tile
                 const int j = GATHER ? w.w + jj : item_tile(w, jj, p.tile_list);
                 const float2 tv = GATHER ? p.gtst[j] : p.tstile[j];
@@ -384,9 +463,19 @@ void launch_tiles_tc(const TileParams& p, int num_sms, cudaStream_t s) {
     if (p.n_items <= 0) return;
     int as, bs, kc;
     int smem = tc_smem_bytes(p.Kpad, &as, &bs, &kc);
-    cudaFuncSetAttribute(tiles_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tiles_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     long long g = p.n_items < num_sms ? p.n_items : num_sms;
-    tiles_tc_kernel<false><<<(unsigned)g, TC_THREADS, smem, s>>>(p, as, bs, kc);
+    tiles_tc_kernel<0><<<(unsigned)g, TC_THREADS, smem, s>>>(p, as, bs, kc);
+}
+
+// Relation-factored L2 (MODE 2): items are (head tile, tail-tile range); p.R relations per tile.
+void launch_tiles_tc_factored(const TileParams& p, int num_sms, cudaStream_t s) {
+    if (p.n_items <= 0) return;
+    int as, bs, kc;
+    int smem = tc_smem_bytes(p.Kpad, &as, &bs, &kc);
+    cudaFuncSetAttribute(tiles_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    long long g = p.n_items < num_sms ? p.n_items : num_sms;
+    tiles_tc_kernel<2><<<(unsigned)g, TC_THREADS, smem, s>>>(p, as, bs, kc);
 }
 
 // Gathered tail blocks: items, their count and block total are on the device
@@ -400,9 +489,9 @@ void launch_tiles_tc_gather(const TileParams& p, int num_sms, cudaStream_t s) {
     if (p.n_items <= 0) return;  // here: an upper bound of the device-side item count
     int as, bs, kc;
     int smem = tc_smem_bytes(p.Kpad, &as, &bs, &kc);
-    cudaFuncSetAttribute(tiles_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tiles_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     long long g = p.n_items < num_sms ? p.n_items : num_sms;
-    tiles_tc_kernel<true><<<(unsigned)g, TC_THREADS, smem, s>>>(p, as, bs, kc);
+    tiles_tc_kernel<1><<<(unsigned)g, TC_THREADS, smem, s>>>(p, as, bs, kc);
 }
 
 }  // namespace kgc

@@ -49,8 +49,8 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
             valid = pos < N && cv.y < Nt;
             if (valid) {
                 r = (int)rr;
-                h = qperm[rr * N + pos];
-                t = (int)(tperm[cv.y] + t_off);  // tail partition: rows [t_off, t_off + Nt) of E
+                h = qperm ? qperm[rr * N + pos] : (int)pos;                        // null: natural order
+                t = (int)((tperm ? tperm[cv.y] : cv.y) + t_off);  // tail partition: rows [t_off, t_off + Nt) of E
             }
         }
         // ---- stage 2: distances, 8 lanes per candidate
