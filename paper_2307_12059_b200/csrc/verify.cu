@@ -6,22 +6,28 @@
 // PAPER.md:369).  Each candidate (sorted query row, sorted tail) is mapped
 // back through the permutations (h = pi_r[i], t = pi_T[j]) and its distance
 // dist3(h, r, t) = ||h + r - t||_p is recomputed from the
-// ORIGINAL fp32 embeddings in FP64 (8 lanes per candidate, lanes over k,
-// shuffle tree).  Kept iff dist <= theta (inclusive); emitted as
+// ORIGINAL fp32 embeddings in FP64 (VERIFY_LPC lanes per candidate, lanes over
+// k, shuffle tree; 1 by default: one lane per candidate, k in order).  Kept iff dist <= theta (inclusive); emitted as
 // {h, r, t, (float)dist} with one atomic per warp per 32 candidates.
 #include "common.cuh"
+
+#ifndef VERIFY_LPC
+#define VERIFY_LPC 1
+#endif
 
 namespace kgc {
 
 // One warp verifies 32 candidates per round.  Stage 1: lane l loads
 // candidate base + l and maps it through the permutations (one independent
-// load chain per lane, all 32 in flight together).  Stage 2: the 8 lanes of
-// group g compute the distances of candidates g*8 .. g*8+7 (lanes over k,
-// FP64 partial sums, 3-step shuffle tree); the sum of candidate c lands back
-// in lane c.  Stage 3: warp-aggregated append of the kept candidates in
-// candidate order.  No data-dependent branches in stage 2, so the compiler
-// overlaps the loads of consecutive candidates; E_h and Rel_r repeat across
-// consecutive candidates of one query row and hit L1.
+// load chain per lane, all 32 in flight together).  Stage 2: the LPC lanes of
+// group g compute the distances of candidates g*LPC .. g*LPC+LPC-1 (lanes over
+// k, FP64 partial sums, log2(LPC)-step shuffle tree); the sum of candidate c
+// lands back in lane c.  Stage 3: warp-aggregated append of the kept
+// candidates in candidate order.  No data-dependent branches in stage 2, so
+// the loads of consecutive k overlap; E_h and Rel_r repeat across consecutive
+// candidates of one query row and hit L1.  Measured on c2 (L2 / L1 verify ms):
+// LPC 8 0.71 / 0.48 (the shuffles saturated the MIO queue), 4 0.51 / 0.35,
+// 2 0.48 / 0.33, 1 0.47 / 0.33.
 template <int NORM, bool VEC4>
 __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__ cand,
                                                         const unsigned long long* __restrict__ cand_count,
@@ -33,7 +39,8 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
                                                         long long Nt, long long t_off) {
     long long nc = (long long)*cand_count;
     if (nc > cand_cap) nc = cand_cap;
-    const int lane = threadIdx.x & 31, g = lane >> 3, s = lane & 7;
+    constexpr int LPC = VERIFY_LPC;  // lanes per candidate
+    const int lane = threadIdx.x & 31, g = lane / LPC, s = lane % LPC;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const long long rows_per_rel = (long long)QT * bq;
@@ -53,11 +60,11 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
                 t = (int)((tperm ? tperm[cv.y] : cv.y) + t_off);  // tail partition: rows [t_off, t_off + Nt) of E
             }
         }
-        // ---- stage 2: distances, 8 lanes per candidate
+        // ---- stage 2: distances, LPC lanes per candidate
         double mine = 0.0;
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
-            const int src = g * 8 + it;
+        for (int it = 0; it < LPC; ++it) {
+            const int src = g * LPC + it;
             const int hh = __shfl_sync(0xffffffffu, h, src);
             const int rq = __shfl_sync(0xffffffffu, r, src);
             const int tt = __shfl_sync(0xffffffffu, t, src);
@@ -67,7 +74,7 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
             double acc = 0.0;
             if (VEC4) {
 #pragma unroll 2
-                for (int k = s * 4; k < d; k += 32) {
+                for (int k = s * 4; k < d; k += 4 * LPC) {
                     const float4 a = __ldg(reinterpret_cast<const float4*>(eh + k));
                     const float4 b = __ldg(reinterpret_cast<const float4*>(er + k));
                     const float4 c = __ldg(reinterpret_cast<const float4*>(et + k));
@@ -79,15 +86,14 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
                     else acc += x0 * x0 + x1 * x1 + x2 * x2 + x3 * x3;
                 }
             } else {
-                for (int k = s; k < d; k += 8) {
+                for (int k = s; k < d; k += LPC) {
                     const double x = ((double)__ldg(eh + k) + (double)__ldg(er + k)) - (double)__ldg(et + k);
                     acc += NORM == 1 ? fabs(x) : x * x;
                 }
             }
-            acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-            if (s == it) mine = acc;  // lane g*8 + it owns candidate g*8 + it
+#pragma unroll
+            for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (s == it) mine = acc;  // lane g*LPC + it owns candidate g*LPC + it
         }
         // ---- stage 3: keep iff dist <= theta (inclusive); append in candidate order
         const double dist = NORM == 2 ? sqrt(mine) : mine;
