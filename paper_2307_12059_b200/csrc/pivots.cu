@@ -12,11 +12,12 @@
 //                 decides how much is pruned, never what is returned)
 //   mp_keys       d(p_k, x) for every query q = fl32(h + r) and tail, FP32
 //                 (relative error <= (d + 4) 2^-24, covered by the test margin)
-//   mp_morton     64-bit Morton code of the K quantised keys, so that the
-//                 radix-sorted tiles are compact in pivot space
+//   mp_morton     32-bit Hilbert (default) or Morton code of the first 4 quantised
+//                 keys, so that the radix-sorted tiles are compact in pivot space
 //   mp_boxes      per tile and pivot: [min, max] of its rows' keys
 //   mp_count / mp_emit  per query tile: count, then list, the surviving tail tiles
 #include <cfloat>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -256,7 +257,7 @@ __global__ void mp_init_minmax_kernel(unsigned int* mm, long long n) {
 // -------------------------------------------------------------- Morton
 __global__ void mp_morton_kernel(const float* __restrict__ keys, const unsigned int* __restrict__ minmax, long long nseg,
                                  long long L, int K, int bits, unsigned long long* __restrict__ code,
-                                 unsigned int* __restrict__ idx) {
+                                 unsigned int* __restrict__ idx, int hilbert) {
     const long long n = nseg * L;
     const float scale_max = (float)((1u << bits) - 1);
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
@@ -277,6 +278,35 @@ __global__ void mp_morton_kernel(const float* __restrict__ keys, const unsigned 
             }
         }
         const int Ks = K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS;  // order by the first pivots only
+        if (hilbert && Ks > 1) {
+            // Hilbert instead of Morton order: Skilling's axes-to-transpose on the quantised
+            // coordinates (Gray code + rotations), then the same bit interleave gives the Hilbert
+            // index -- consecutive codes are adjacent cells, so tiles are more compact
+            const unsigned M = 1u << (bits - 1);
+            for (unsigned Q = M; Q > 1; Q >>= 1) {
+                const unsigned P = Q - 1;
+#pragma unroll
+                for (int k = 0; k < MP_SORT_PIVOTS; ++k) {
+                    if (k >= Ks) continue;
+                    if (q[k] & Q) {
+                        q[0] ^= P;
+                    } else {
+                        const unsigned tt = (q[0] ^ q[k]) & P;
+                        q[0] ^= tt;
+                        q[k] ^= tt;
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 1; k < MP_SORT_PIVOTS; ++k)
+                if (k < Ks) q[k] ^= q[k - 1];
+            unsigned tt = 0;
+            for (unsigned Q = M; Q > 1; Q >>= 1)
+                if (q[Ks - 1] & Q) tt ^= Q - 1;
+#pragma unroll
+            for (int k = 0; k < MP_SORT_PIVOTS; ++k)
+                if (k < Ks) q[k] ^= tt;
+        }
         unsigned long long c = 0;
         for (int b = bits - 1; b >= 0; --b)
 #pragma unroll
@@ -703,7 +733,11 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
 
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
                       unsigned long long* code, unsigned int* idx, cudaStream_t s) {
-    mp_morton_kernel<<<grid_for_mp(nseg * L, 256), 256, 0, s>>>(keys, minmax, nseg, L, K, bits, code, idx);
+    // Hilbert order by default (c2: gathered L1 pairs 1.72% -> 1.69%, tile kernel -4%);
+    // KGC_HILBERT=0 restores the Morton (Z) order
+    const char* e = getenv("KGC_HILBERT");
+    const int hilbert = e ? atoi(e) : 1;
+    mp_morton_kernel<<<grid_for_mp(nseg * L, 256), 256, 0, s>>>(keys, minmax, nseg, L, K, bits, code, idx, hilbert);
 }
 
 void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg, long long L, int ROWS, int ntile,
