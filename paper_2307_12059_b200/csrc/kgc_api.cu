@@ -665,6 +665,9 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                                 ctx->scan_tmp.p, s, &ctx->launches);
         LAUNCHED(0);
         CK(cudaMemcpyAsync(ctx->tperm.p, ctx->sv0.p, (size_t)NT * 4, cudaMemcpyDeviceToDevice, s));
+        const char* kde = getenv("KGC_KD");  // local kd refinement of both orders (experiment knob)
+        const bool kd = kde ? atoi(kde) != 0 : false;
+        if (kd) launch_kd_refine(P<float>(ctx->mpkt), P<int>(ctx->tperm), 1, NT, K, s);
         launch_mp_morton(P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q), R, N, K, bits,
                          P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
         LAUNCHED(1);
@@ -673,6 +676,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                                 ctx->scan_tmp.p, s, &ctx->launches);
         LAUNCHED(0);
         CK(cudaMemcpyAsync(ctx->qperm.p, ctx->sv0.p, NR * 4, cudaMemcpyDeviceToDevice, s));
+        if (kd) launch_kd_refine(P<float>(ctx->mpkq), P<int>(ctx->qperm), R, N, K, s);
         CK(cudaEventRecord(ctx->ev[EV_SORT], s));
         // ---- a4: K-dim tile boxes and the L_inf test of every tile pair
         launch_mp_boxes(P<float>(ctx->mpkt), P<unsigned>(ctx->tperm), 1, NT, BN, TT, K, P<float>(ctx->tbmin),

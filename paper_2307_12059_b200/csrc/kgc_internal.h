@@ -133,6 +133,7 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
                     const float* P, float* keys, unsigned int* minmax, unsigned int* nonfinite, cudaStream_t s);
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
                       unsigned long long* code, unsigned int* idx, cudaStream_t s);
+void launch_kd_refine(const float* keys, int* perm, long long nseg, long long L, int K, cudaStream_t s);
 void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg, long long L, int ROWS, int ntile,
                      int K, float* bmin, float* bmax, cudaStream_t s);
 void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,

@@ -677,6 +677,115 @@ __global__ void __launch_bounds__(256) gather_tails_block_kernel(
     }
 }
 
+// ------------------------------------------- local kd refinement of the order
+// The space-filling-curve order keeps tiles compact only as far as the curve is;
+// a kd-tree keeps query boxes tighter (numpy, c2 L1: 13% fewer gathered tails).  A
+// cheap local form: every aligned chunk of KD_CH consecutive sorted rows of a
+// segment is split three times along its widest pivot-key dimension (512 -> 256
+// -> 128 -> 64-row leaves = the SIMT tiles; pairs of leaves form the 128-row
+// tensor-core tiles): one block per chunk, bitonic sorts in shared memory
+// (numpy: 7% fewer gathered tails than Hilbert alone).  Only the order changes.
+constexpr int KD_CH = 512, KD_LEVELS = 3;
+__global__ void __launch_bounds__(KD_CH) kd_refine_kernel(const float* __restrict__ keys, int* __restrict__ perm,
+                                                         long long L, int K) {
+    __shared__ float kk[KD_CH][MP_MAX + 1];  // padded: row reads are conflict-free
+    __shared__ int idx[KD_CH];
+    __shared__ float sk[KD_CH];
+    __shared__ int sl[KD_CH];
+    __shared__ int ndim[1 << (KD_LEVELS - 1)];
+    const long long seg = blockIdx.y;
+    const long long c0 = (long long)blockIdx.x * KD_CH;
+    if (c0 >= L) return;
+    const int n = (int)(L - c0 < KD_CH ? L - c0 : KD_CH);
+    const int i = threadIdx.x, lane = i & 31, w = i >> 5;
+    int* pr = perm + seg * L + c0;
+    const int my = i < n ? pr[i] : -1;
+    idx[i] = my;
+    if (K == MP_MAX) {  // two 16-byte loads per row
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (my >= 0) {
+            const float4* r4 = reinterpret_cast<const float4*>(keys + ((size_t)seg * L + my) * MP_MAX);
+            a = __ldg(r4);
+            b = __ldg(r4 + 1);
+        }
+        kk[i][0] = a.x; kk[i][1] = a.y; kk[i][2] = a.z; kk[i][3] = a.w;
+        kk[i][4] = b.x; kk[i][5] = b.y; kk[i][6] = b.z; kk[i][7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < MP_MAX; ++k)
+            kk[i][k] = (my >= 0 && k < K) ? keys[((size_t)seg * L + my) * K + k] : 0.f;
+    }
+    __syncthreads();
+    for (int lev = 0; lev < KD_LEVELS; ++lev) {
+        const int S = KD_CH >> lev, nodes = 1 << lev;
+        if (w < nodes) {  // widest key dimension of node w over its real rows
+            float mn[MP_MAX], mx[MP_MAX];
+#pragma unroll
+            for (int k = 0; k < MP_MAX; ++k) { mn[k] = 3e38f; mx[k] = -3e38f; }
+            for (int j = w * S + lane; j < (w + 1) * S; j += 32)
+                if (idx[j] >= 0)
+#pragma unroll
+                    for (int k = 0; k < MP_MAX; ++k) { mn[k] = fminf(mn[k], kk[j][k]); mx[k] = fmaxf(mx[k], kk[j][k]); }
+            int best = 0;
+            float bw = -1.f;
+#pragma unroll
+            for (int k = 0; k < MP_MAX; ++k) {
+                float a = mn[k], z = mx[k];
+                for (int o = 16; o > 0; o >>= 1) {
+                    a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+                    z = fmaxf(z, __shfl_xor_sync(0xffffffffu, z, o));
+                }
+                if (k < K && z - a > bw) { bw = z - a; best = k; }
+            }
+            if (lane == 0) ndim[w] = best;
+        }
+        __syncthreads();
+        sk[i] = idx[i] >= 0 ? kk[i][ndim[i / S]] : 3e38f;  // padding rows sort to the end
+        sl[i] = i;
+        __syncthreads();
+        for (int size = 2; size <= S; size <<= 1) {  // bitonic sort of every S-row node
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const float a = sk[i], b = sk[j];
+                    if ((a > b) == up && a != b) {
+                        sk[i] = b; sk[j] = a;
+                        const int t = sl[i]; sl[i] = sl[j]; sl[j] = t;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // apply the node permutations
+        const int src = sl[i];
+        const int nidx = idx[src];
+        float nk[MP_MAX];
+#pragma unroll
+        for (int k = 0; k < MP_MAX; ++k) nk[k] = kk[src][k];
+        __syncthreads();
+        idx[i] = nidx;
+#pragma unroll
+        for (int k = 0; k < MP_MAX; ++k) kk[i][k] = nk[k];
+        __syncthreads();
+    }
+    // padding rows are at the end of every node that holds any; compact the real rows
+    // (the partial last chunk: real rows first, in node order)
+    if (n == KD_CH) {
+        pr[i] = idx[i];
+    } else if (i == 0) {
+        int o = 0;
+        for (int j = 0; j < KD_CH; ++j)
+            if (idx[j] >= 0) pr[o++] = idx[j];
+    }
+}
+
+void launch_kd_refine(const float* keys, int* perm, long long nseg, long long L, int K, cudaStream_t s) {
+    if (L < 2 * SIMT_T) return;
+    dim3 grid((unsigned)((L + KD_CH - 1) / KD_CH), (unsigned)nseg);
+    kd_refine_kernel<<<grid, KD_CH, 0, s>>>(keys, perm, L, K);
+}
+
 // ------------------------------------------------------------ launchers
 void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, const double* p0, float* P,
                         cudaStream_t s) {
