@@ -693,6 +693,7 @@ __global__ void __launch_bounds__(KD_CH) kd_refine_kernel(const float* __restric
     __shared__ float sk[KD_CH];
     __shared__ int sl[KD_CH];
     __shared__ int ndim[1 << (KD_LEVELS - 1)];
+    __shared__ float wmn[KD_CH / 32][MP_MAX], wmx[KD_CH / 32][MP_MAX];
     const long long seg = blockIdx.y;
     const long long c0 = (long long)blockIdx.x * KD_CH;
     if (c0 >= L) return;
@@ -718,45 +719,61 @@ __global__ void __launch_bounds__(KD_CH) kd_refine_kernel(const float* __restric
     __syncthreads();
     for (int lev = 0; lev < KD_LEVELS; ++lev) {
         const int S = KD_CH >> lev, nodes = 1 << lev;
-        if (w < nodes) {  // widest key dimension of node w over its real rows
-            float mn[MP_MAX], mx[MP_MAX];
-#pragma unroll
-            for (int k = 0; k < MP_MAX; ++k) { mn[k] = 3e38f; mx[k] = -3e38f; }
-            for (int j = w * S + lane; j < (w + 1) * S; j += 32)
-                if (idx[j] >= 0)
-#pragma unroll
-                    for (int k = 0; k < MP_MAX; ++k) { mn[k] = fminf(mn[k], kk[j][k]); mx[k] = fmaxf(mx[k], kk[j][k]); }
-            int best = 0;
-            float bw = -1.f;
+        {   // widest key dimension of every node over its real rows: warp partials, then one
+            // thread per node combines its warps
+            const bool real = idx[i] >= 0;
 #pragma unroll
             for (int k = 0; k < MP_MAX; ++k) {
-                float a = mn[k], z = mx[k];
+                float a = real ? kk[i][k] : 3e38f, z = real ? kk[i][k] : -3e38f;
                 for (int o = 16; o > 0; o >>= 1) {
                     a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
                     z = fmaxf(z, __shfl_xor_sync(0xffffffffu, z, o));
                 }
-                if (k < K && z - a > bw) { bw = z - a; best = k; }
+                if (lane == 0) { wmn[w][k] = a; wmx[w][k] = z; }
             }
-            if (lane == 0) ndim[w] = best;
-        }
-        __syncthreads();
-        sk[i] = idx[i] >= 0 ? kk[i][ndim[i / S]] : 3e38f;  // padding rows sort to the end
-        sl[i] = i;
-        __syncthreads();
-        for (int size = 2; size <= S; size <<= 1) {  // bitonic sort of every S-row node
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                const int j = i ^ stride;
-                if (j > i) {
-                    const bool up = (i & size) == 0;
-                    const float a = sk[i], b = sk[j];
-                    if ((a > b) == up && a != b) {
-                        sk[i] = b; sk[j] = a;
-                        const int t = sl[i]; sl[i] = sl[j]; sl[j] = t;
-                    }
+            __syncthreads();
+            if (i < nodes) {
+                const int wpn = (KD_CH / 32) / nodes;  // warps per node
+                int best = 0;
+                float bw = -1.f;
+                for (int k = 0; k < K; ++k) {
+                    float a = 3e38f, z = -3e38f;
+                    for (int x = i * wpn; x < (i + 1) * wpn; ++x) { a = fminf(a, wmn[x][k]); z = fmaxf(z, wmx[x][k]); }
+                    if (z - a > bw) { bw = z - a; best = k; }
                 }
-                __syncthreads();
+                ndim[i] = best;
             }
         }
+        __syncthreads();
+        // bitonic sort of every S-row node on (key, slot): strides < 32 by warp shuffles,
+        // larger strides through shared memory (19 barriers over the three levels, not 109)
+        float kv = idx[i] >= 0 ? kk[i][ndim[i / S]] : 3e38f;  // padding rows sort to the end
+        int sv = i;
+        for (int size = 2; size <= S; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                float pk;
+                int ps;
+                if (stride >= 32) {
+                    sk[i] = kv;
+                    sl[i] = sv;
+                    __syncthreads();
+                    pk = sk[i ^ stride];
+                    ps = sl[i ^ stride];
+                    __syncthreads();
+                } else {
+                    pk = __shfl_xor_sync(0xffffffffu, kv, stride);
+                    ps = __shfl_xor_sync(0xffffffffu, sv, stride);
+                }
+                const bool up = (i & size) == 0, lower = (i & stride) == 0;
+                const bool p_less = pk < kv || (pk == kv && ps < sv);
+                if (lower == up ? p_less : !p_less) {  // keep the min (ascending lower half) or the max
+                    kv = pk;
+                    sv = ps;
+                }
+            }
+        }
+        sl[i] = sv;
+        __syncthreads();
         // apply the node permutations
         const int src = sl[i];
         const int nidx = idx[src];
