@@ -1,20 +1,28 @@
 """bench.py -- throughput of the B200 TransE completion join (arXiv 2307.12059).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2] [--hit 1e-4]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4] [--hit 1e-5]
 
 One *step* is one pass of the whole hot path (every SURVEY §8(a) row) over the
-synthetic workload: kgc_join with L2 (tcgen05 engine) followed by kgc_join
-with L1 (SIMT engine) on the same inputs, each = K1 keys, K2 sorts, K3 tile
-ranges + shard split, staging, tile engine, FP64 verify + compaction.
+synthetic workload: kgc_join per norm of the workload on the same inputs, each =
+(N > 1: E/Rel broadcast from rank 0) K1 keys, K2 sorts, K3 tile ranges + shard
+split, staging, tile engine, FP64 verify + compaction (and the count all-reduce).
 
-metric = candidate triplets / s = (N * N * R per join, summed over the two
-joins) / device time of the step; whole-job value over all ranks (query tiles
-are sharded across ranks, tails replicated: strong scaling on a fixed config).
+Default workload: c4 (YAGO3-10-shaped, N=123182, R=37, d=200, TransE L2, theta at
+hit rate 1e-5), the largest BASELINE.json config that fits one GPU's
+single-GPU line (c5 is the 8-GPU config).  The same JSON line also carries
+`extra_workloads`: the c2 L2+L1 step (WN18-shaped, both norms) and the c3
+theta sweep (FB15k-shaped, hit rates 1e-6..1e-3; the analogue of the paper's
+epsilon sweep), each timed the same way.
 
-For N > 1 launch with torchrun (one process per GPU, NCCL); the timed region
-ends with an NCCL all-reduce of the result counts; times are the max over
-ranks.  Inputs are resident in HBM when the timed region starts; L2 is
-flushed (512 MiB write) before every timed step, outside the events.
+metric = candidate triplets / s = (N * N * R per join, summed over the joins)
+/ device time of the step; whole-job value over all ranks (query tiles are
+sharded across ranks, tails replicated: strong scaling on a fixed config).
+
+--gpus N > 1 without a launcher re-executes itself under torch.distributed.run
+(one process per GPU, NCCL, 127.0.0.1); under torchrun WORLD_SIZE must equal
+--gpus.  Times are the max over ranks.  Inputs are resident in HBM (on rank 0)
+when the timed region starts; L2 is flushed (512 MiB write) before every timed
+step, outside the events.
 """
 from __future__ import annotations
 
@@ -171,7 +179,8 @@ def run_reference(args, cfg, thresholds):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args, cfg), "sample": f"{rows_per_step} seeded (h,r) rows x all {N} "
                    f"tails per step, norms {args.norms}"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.threads_used(), "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.threads_used(), "cpu_model": cpu_model(),
+                         "kind": "oracle",
                          "sample": f"{rows_per_step} (h,r) rows x {N} tails x norms {args.norms} per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -182,6 +191,180 @@ def run_reference(args, cfg, thresholds):
 def workload_name(args, cfg):
     return (f"{cfg.name} ({cfg.note}): N={cfg.N} R={cfg.R} d={cfg.d}, TransE norms {args.norms}, "
             f"theta at hit rate {args.hit:g}, {cfg.dist} embeddings ({GENERATOR_VERSION}, seed {cfg.seed})")
+
+
+# Best measured settings per workload: multi-pivot pruning pays on c2 / c4 / c5,
+# the paper's single pivot is faster on c3 (its extra keys / sort cost exceed the pruning gain);
+# the cyclic split spreads c2's hit-dense relations over the ranks.
+BEST_PIVOTS = {"c1": 1, "c2": 8, "c3": 1, "c4": 8, "c5": 8}
+BEST_SPLIT = {"c2": 2}
+DEFAULT_HIT = {"c1": 1e-3, "c2": 1e-4, "c3": 1e-5, "c4": 1e-5, "c5": 1e-6}
+DEFAULT_NORMS = {"c1": "2,1", "c2": "2,1", "c3": "2", "c4": "2", "c5": "2"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+class StepRunner:
+    """The joins of one step: one libkgc context per norm.  With two norms they run
+    concurrently, each on its own stream and host thread (a context is single-threaded
+    and kgc_join blocks its thread at two host syncs, so the other join fills those gaps);
+    `sequential` runs them one after the other on `stream`."""
+
+    def __init__(self, torch, kgc, dev, stream, norms, eps, rank, world, pivots, split, tail_shard, sequential):
+        self.torch, self.stream, self.norms, self.eps = torch, stream, norms, eps
+        self.conc = len(norms) > 1 and not sequential
+        self.jstream = {n: (torch.cuda.Stream(dev) if self.conc else stream) for n in norms}
+        self.pool = ThreadPoolExecutor(len(norms)) if self.conc else None
+        self.opts = dict(device=dev.index, rank=rank, world=world, pivots=pivots, split=split, tail_shard=tail_shard)
+        self.kgc = kgc
+        self.joins = {n: kgc.Join(stream=self.jstream[n].cuda_stream, **self.opts) for n in norms}
+
+    def new_joins(self):
+        return {n: self.kgc.Join(stream=self.jstream[n].cuda_stream, **self.opts) for n in self.norms}
+
+    def run_joins(self, fn):
+        """fn(n) for every norm, concurrently on the norms' streams, ordered after / before `stream`."""
+        torch = self.torch
+        if not self.conc:
+            return [fn(n) for n in self.norms]
+        ev0 = torch.cuda.Event()
+        ev0.record(self.stream)
+        for n in self.norms:
+            self.jstream[n].wait_event(ev0)
+        out = [f.result() for f in [self.pool.submit(fn, n) for n in self.norms]]
+        for n in self.norms:
+            ev = torch.cuda.Event()
+            ev.record(self.jstream[n])
+            self.stream.wait_event(ev)
+        return out
+
+    def close(self):
+        for j in self.joins.values():
+            j.close()
+        if self.pool:
+            self.pool.shutdown()
+
+
+PHASES = ("ms_total", "ms_h2d", "ms_keys", "ms_sort", "ms_ranges", "ms_stage", "ms_tiles", "ms_recheck")
+
+
+def timed_steps(torch, stream, step, steps, flush, barrier=None):
+    """`steps` timed steps (CUDA events on `stream`, L2 flushed before each outside the events);
+    returns (total ms, per-step per-norm stats list)."""
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    stats = []
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    for k in range(steps):
+        flush.zero_()                      # L2 flush (> 126 MB), outside the events
+        starts[k].record(stream)
+        stats.append(step())
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    return sum(s.elapsed_time(e) for s, e in zip(starts, ends)), stats
+
+
+def kernel_table(stats_steps, norms, d, peaks, peak_src, config, N, R):
+    """Per-kernel device times (libkgc's per-phase CUDA events on the launching stream) and the
+    roofline of each tile kernel: algorithmic work per unit x units per launch / mean duration."""
+    last = stats_steps[-1]
+    kernels = []
+    for n in norms:
+        st = last[n]
+        mean = {k: statistics.mean(s[n][k] for s in stats_steps) for k in PHASES}
+        t_tiles = mean["ms_tiles"] / 1e3
+        pairs = st["tile_pairs_mine"] * st["query_tile_rows"] * st["tail_tile_rows"]
+        if st["engine"] == 5:   # gathered tails: the pairs left after the per-tail pivot test (padding excluded)
+            pairs = st["gathered_pairs"]
+        flops = 2.0 * d * pairs
+        alu = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        if n == 2:
+            tc = st["tail_tile_rows"] == 256
+            peak = peaks["bf16_tflops"] * (1.1 / 2.25) if tc else 2 * alu
+            kname = ("tiles_tc2_kernel (L2, tcgen05.mma.cta_group::2 kind::tf32)" if st["engine"] == 4 else
+                     "tiles_tc_kernel (L2, tcgen05 kind::tf32)") if tc else "tiles_simt_kernel<2>"
+            ent = {"kernel": kname, "bound": "tensor" if tc else "alu", "ms": t_tiles * 1e3,
+                   "achieved": flops / t_tiles / 1e12 if t_tiles > 0 else 0.0, "peak": peak, "unit": "TFLOP/s",
+                   "work": f"2*d flops x {pairs:.4g} (query, tail) pairs in surviving {st['query_tile_rows']}x"
+                           f"{st['tail_tile_rows']} tiles",
+                   "peak_note": (f"{peak_src} bf16 burst {peaks['bf16_tflops']} x nominal tf32/bf16 1.1/2.25")
+                   if tc else "148 SM x 128 FP32 lanes x FFMA(2 flop) x clock"}
+        else:
+            kname = "tiles_gather_kernel<1> (L1, gathered tails)" if st["engine"] == 5 else "tiles_simt_kernel<1> (L1)"
+            ent = {"kernel": kname, "bound": "alu", "ms": t_tiles * 1e3,
+                   "achieved": flops / t_tiles / 1e12 if t_tiles > 0 else 0.0, "peak": alu, "unit": "TFLOP/s",
+                   "work": f"2*d FP32 ops x {pairs:.4g} computed (query, tail) pairs",
+                   "peak_note": "148 SM x 128 FP32 lanes x 1 FADD/clk x sm_max_mhz (|q-t| = 2 FADD = 2 flop)"}
+            # the L1 path's HBM use (BASELINE north_star asks for it): ncu dram bytes of the tile kernel /
+            # its event time; operand bytes the copies move (L2 -> SM) per the same time
+            dram = ncu_traffic(kname.split()[0], config)
+            opb = pairs * (st["query_tile_rows"] + st["tail_tile_rows"]) * ((d + 7) // 8 * 8) * 4 / \
+                (st["query_tile_rows"] * st["tail_tile_rows"])
+            ent["hbm_gbs"] = dram / t_tiles / 1e9 if dram and t_tiles > 0 else None
+            ent["hbm_frac"] = ent["hbm_gbs"] / peaks["hbm_gbs"] if ent["hbm_gbs"] else None
+            ent["operand_gbs_l2_to_sm"] = opb / t_tiles / 1e9 if t_tiles > 0 else None
+        ent["frac"] = ent["achieved"] / ent["peak"]
+        kernels.append(ent)
+        for key, name in (("ms_keys", "K1 keys"), ("ms_sort", "K2 sort"), ("ms_ranges", "K3 ranges"),
+                          ("ms_stage", "stage"), ("ms_recheck", "K6 verify")):
+            e = {"kernel": f"{name} (L{n})", "ms": mean[key]}
+            if key == "ms_keys" and mean[key] > 0:
+                # algorithmic HBM bytes of the precompute: read E and Rel, write N*R + N keys x K pivots
+                Kp = st["pivots_used"]
+                byts = (N * d + R * d) * 4 + (N * R + N) * Kp * 4
+                e.update({"bound": "hbm", "achieved_gbs": byts / (mean[key] / 1e3) / 1e9, "peak_gbs": peaks["hbm_gbs"],
+                          "frac": byts / (mean[key] / 1e3) / 1e9 / peaks["hbm_gbs"],
+                          "note": "phase time incl. pivot choice and both key kernels; E is L2-resident"})
+            if key == "ms_recheck":
+                e["candidates"] = st["candidates"]
+            kernels.append(e)
+    return kernels
+
+
+def measure_workload(torch, kgc, dev, stream, name, norms, hit, steps, warmup, thresholds, flush, sequential=False):
+    """One extra workload on this GPU (world 1), timed like the headline: {value, ms_per_step, ...}."""
+    cfg = CONFIGS[name]
+    E_h, Rel_h = generate_config(name)
+    Et, Rt = torch.from_numpy(E_h).to(dev), torch.from_numpy(Rel_h).to(dev)
+    eps = {n: float(thresholds[name][f"L{n}@{hit:g}"]["theta"]) for n in norms}
+    runner = StepRunner(torch, kgc, dev, stream, norms, eps, 0, 1, BEST_PIVOTS.get(name, 1), 0, 0, sequential)
+
+    def step():
+        runner.run_joins(lambda n: runner.joins[n].run(Et, Rt, n, eps[n]))
+        return {n: runner.joins[n].stats() for n in norms}
+
+    for _ in range(warmup):
+        step()
+    ms, stats = timed_steps(torch, stream, step, steps, flush)
+    runner.close()
+    ms_step = ms / steps
+    trip = float(cfg.N) * cfg.N * cfg.R * len(norms)
+    peaks, peak_src = load_peaks()
+    kern = kernel_table(stats, norms, cfg.d, peaks, peak_src, name, cfg.N, cfg.R)
+    tiles = [k for k in kern if "achieved" in k]
+    dom = max(tiles, key=lambda k: k["ms"])
+    res = sum(stats[-1][n]["results"] for n in norms)
+    return {"workload": f"{name}: N={cfg.N} R={cfg.R} d={cfg.d}, norms {norms}, hit rate {hit:g}",
+            "value": trip / (ms_step / 1e3), "unit": UNIT, "ms_per_step": ms_step, "steps": steps,
+            "eps": eps, "result_triplets_per_step": res,
+            "pruned_tile_fraction": {f"L{n}": 1 - stats[-1][n]["tile_pairs_surviving"] /
+                                     max(1, stats[-1][n]["tile_pairs_total"]) for n in norms},
+            "dominant_kernel": {"kernel": dom["kernel"], "ms": dom["ms"], "frac": dom["frac"], "bound": dom["bound"]},
+            "phases_ms": {k["kernel"]: round(k["ms"], 4) for k in kern}}
 
 
 # ------------------------------------------------------------------ our arm
@@ -195,16 +378,19 @@ def run_ours(args, cfg, thresholds):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream()
+    barrier = (lambda: dist.barrier()) if world > 1 else None
 
     N, R, d = cfg.N, cfg.R, cfg.d
     eps = {n: float(thresholds[args.config][f"L{n}@{args.hit:g}"]["theta"]) for n in args.norms}
-    # inputs: rank 0 generates, NCCL broadcast to the other ranks (outside the timed region)
+    # inputs: resident on rank 0; every step starts with their NCCL broadcast to the other ranks
+    # (inside the timed region)
     if rank == 0:
         E_h, Rel_h = generate_config(args.config)
         Et = torch.from_numpy(E_h).to(dev)
@@ -213,77 +399,36 @@ def run_ours(args, cfg, thresholds):
         E_h = Rel_h = None
         Et = torch.empty((N, d), dtype=torch.float32, device=dev)
         Rt = torch.empty((R, d), dtype=torch.float32, device=dev)
-    if world > 1:
-        dist.broadcast(Et, 0)
-        dist.broadcast(Rt, 0)
-    if E_h is None:
-        E_h, Rel_h = Et.cpu().numpy(), Rt.cpu().numpy()
     torch.cuda.synchronize()
 
-    # the joins of one step (one per norm) run concurrently: one context, stream and host thread
-    # each (a context is single-threaded; kgc_join blocks its thread at its two host syncs, so
-    # the other join fills those gaps); --sequential runs them one after the other on one stream
-    conc = len(args.norms) > 1 and not args.sequential
-    jstream = {n: (torch.cuda.Stream(dev) if conc else stream) for n in args.norms}
-    pool = ThreadPoolExecutor(len(args.norms)) if conc else None
-
-    def run_joins(fn):
-        """fn(n) for every norm, concurrently on the norms' streams, ordered after / before `stream`."""
-        if not conc:
-            return [fn(n) for n in args.norms]
-        ev0 = torch.cuda.Event()
-        ev0.record(stream)
-        for n in args.norms:
-            jstream[n].wait_event(ev0)
-        out = [f.result() for f in [pool.submit(fn, n) for n in args.norms]]
-        for n in args.norms:
-            ev = torch.cuda.Event()
-            ev.record(jstream[n])
-            stream.wait_event(ev)
-        return out
-
-    joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, split=args.split, tail_shard=args.tail_shard, stream=jstream[n].cuda_stream)
-             for n in args.norms}
+    runner = StepRunner(torch, kgc, dev, stream, args.norms, eps, rank, world, args.pivots, args.split,
+                        args.tail_shard, args.sequential)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     counts = torch.zeros(len(args.norms), dtype=torch.int64, device=dev)
 
     def step():
-        cs = run_joins(lambda n: joins[n].run(Et, Rt, n, eps[n]))
+        if world > 1:
+            dist.broadcast(Et, 0)
+            dist.broadcast(Rt, 0)
+        cs = runner.run_joins(lambda n: runner.joins[n].run(Et, Rt, n, eps[n]))
         for i, c in enumerate(cs):
             counts[i] = c
         if world > 1:
             dist.all_reduce(counts)
+        return {n: runner.joins[n].stats() for n in args.norms}
 
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
+    if E_h is None:
+        E_h, Rel_h = Et.cpu().numpy(), Rt.cpu().numpy()
 
-    # ---- timed region (device time, CUDA events on the launching stream)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    phase = {n: {} for n in args.norms}
-    launches = 0
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    # ---- timed region (device time, CUDA events on the launching stream, max over ranks)
     wall0 = time.perf_counter()
     with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush.zero_()                      # L2 flush (> 126 MB), outside the events
-            starts[k].record(stream)
-            step()
-            ends[k].record(stream)
-            for n in args.norms:
-                st = joins[n].stats()
-                launches += st["launches"]
-                for key in ("ms_total", "ms_h2d", "ms_keys", "ms_sort", "ms_ranges", "ms_stage", "ms_tiles",
-                            "ms_recheck"):
-                    phase[n].setdefault(key, []).append(st[key])
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+        ms, stats_steps = timed_steps(torch, stream, step, args.steps, flush, barrier)
     wall = time.perf_counter() - wall0
-    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    launches = sum(s[n]["launches"] for s in stats_steps for n in args.norms)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -292,64 +437,18 @@ def run_ours(args, cfg, thresholds):
     trip_per_step = float(N) * N * R * len(args.norms)
     value = trip_per_step / (ms_per_step / 1e3)
     results_total = int(counts.sum().item())
-    stats_last = {n: joins[n].stats() for n in args.norms}
+    stats_last = stats_steps[-1]
 
-    # ---- roofline of the dominant kernel (per-phase CUDA events inside libkgc)
     peaks, peak_src = load_peaks()
-    kernels = []
-    for n in args.norms:
-        st = stats_last[n]
-        t_tiles = statistics.mean(phase[n]["ms_tiles"]) / 1e3
-        pairs = st["tile_pairs_mine"] * st["query_tile_rows"] * st["tail_tile_rows"]
-        if st["engine"] == 5:   # gathered tails: the pairs left after the per-tail pivot test (padding excluded)
-            pairs = st["gathered_pairs"]
-        flops = 2.0 * d * pairs
-        if n == 2:
-            tc = st["tail_tile_rows"] == 256
-            peak = peaks["bf16_tflops"] * (1.1 / 2.25) if tc else \
-                148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12 * 2
-            kname = ("tiles_tc2_kernel (L2, tcgen05.mma.cta_group::2 kind::tf32)" if st["engine"] == 4 else
-                     "tiles_tc_kernel (L2, tcgen05 kind::tf32)") if tc else "tiles_simt_kernel<2>"
-            kernels.append({"kernel": kname,
-                            "bound": "tensor" if tc else "alu", "ms": t_tiles * 1e3,
-                            "achieved": flops / t_tiles / 1e12, "peak": peak, "unit": "TFLOP/s",
-                            "peak_note": (f"{peak_src} bf16 burst {peaks['bf16_tflops']} x nominal tf32/bf16 "
-                                          "1.1/2.25") if tc else "148 SM x 128 FP32 lanes x FFMA(2 flop) x clock"})
-        else:
-            peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-            kname = "tiles_gather_kernel<1> (L1, gathered tails)" if st["engine"] == 5 else "tiles_simt_kernel<1> (L1)"
-            kernels.append({"kernel": kname, "bound": "alu", "ms": t_tiles * 1e3,
-                            "achieved": flops / t_tiles / 1e12, "peak": peak, "unit": "TFLOP/s",
-                            "peak_note": "148 SM x 128 FP32 lanes x 1 FADD/clk x sm_max_mhz (|q-t| = 2 FADD = 2 flop)"})
-        if n == 1:
-            # the L1 path's HBM use (BASELINE north_star asks for it): ncu dram bytes of the tile kernel /
-            # its event time; operand bytes the bulk copies move (L2 -> SM) per the same time
-            k1 = kernels[-1]
-            dram = ncu_traffic(k1["kernel"].split()[0], args.config)
-            # operand bytes per computed pair: (query rows + tail rows) x Kpad x 4 per 64 x 64 block
-            opb = pairs * (st["query_tile_rows"] + st["tail_tile_rows"]) * ((d + 7) // 8 * 8) * 4 / \
-                (st["query_tile_rows"] * st["tail_tile_rows"])
-            k1["hbm_gbs"] = dram / t_tiles / 1e9 if dram else None
-            k1["hbm_frac"] = (dram / t_tiles / 1e9) / peaks["hbm_gbs"] if dram else None
-            k1["operand_gbs_l2_to_sm"] = opb / t_tiles / 1e9
-        for key, name in (("ms_keys", "K1 keys"), ("ms_sort", "K2 sort"), ("ms_ranges", "K3 ranges"),
-                          ("ms_stage", "stage"), ("ms_recheck", "K6 verify")):
-            ent = {"kernel": f"{name} (L{n})", "ms": statistics.mean(phase[n][key])}
-            if key == "ms_keys":
-                # algorithmic HBM bytes of the precompute: read E and Rel, write N*R + N keys x K pivots
-                Kp = st["pivots_used"]
-                byts = (N * d + R * d) * 4 + (N * R + N) * Kp * 4
-                ent.update({"bound": "hbm", "achieved_gbs": byts / (ent["ms"] / 1e3) / 1e9,
-                            "peak_gbs": peaks["hbm_gbs"],
-                            "frac": byts / (ent["ms"] / 1e3) / 1e9 / peaks["hbm_gbs"],
-                            "note": "phase time incl. pivot choice and both key kernels; E is L2-resident"})
-            kernels.append(ent)
+    kernels = kernel_table(stats_steps, args.norms, d, peaks, peak_src, args.config, N, R)
     dom = max((k for k in kernels if "achieved" in k), key=lambda k: k["ms"])
     wl = workload_name(args, cfg)
     traffic = ncu_traffic(dom["kernel"].split()[0], args.config)
     roofline = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
                 "frac": dom["achieved"] / dom["peak"], "traffic": traffic, "kernel": dom["kernel"],
-                "peak_source": dom["peak_note"]}
+                "work": dom["work"], "peak_source": dom["peak_note"],
+                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu "
+                                "--set full capture (profiles/ncu_traffic.json)"}
 
     # ---- end to end through the public C ABI with HOST buffers
     e2e = None
@@ -358,8 +457,7 @@ def run_ours(args, cfg, thresholds):
         R_pin = torch.from_numpy(Rel_h).pin_memory()
         out_pin = {n: torch.empty((max(1, stats_last[n]["results"]) * 2, 4), dtype=torch.int32).pin_memory()
                    for n in args.norms}
-        e2e_joins = {n: kgc.Join(device=local, rank=rank, world=world, pivots=args.pivots, split=args.split, tail_shard=args.tail_shard,
-                                 stream=jstream[n].cuda_stream) for n in args.norms}
+        e2e_joins = runner.new_joins()
         h2d = d2h = 0
 
         def e2e_one(n):
@@ -373,7 +471,7 @@ def run_ours(args, cfg, thresholds):
 
         def e2e_step():
             nonlocal h2d, d2h
-            for cnt in run_joins(e2e_one):
+            for cnt in runner.run_joins(e2e_one):
                 h2d += E_pin.numel() * 4 + R_pin.numel() * 4
                 d2h += cnt * 16
         e2e_step()
@@ -394,7 +492,7 @@ def run_ours(args, cfg, thresholds):
         e2e_ms = float(te.item()) / args.steps
         e2e = {"value": trip_per_step / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-               "path": "kgc_join(host pinned E, Rel) + kgc_results(host pinned) per norm"}
+               "path": "kgc_join(host pinned E, Rel) + kgc_results(host pinned) per norm, every rank"}
         for j in e2e_joins.values():
             j.close()
 
@@ -414,16 +512,26 @@ def run_ours(args, cfg, thresholds):
             oracle.join(E_h, Rel_h, n, eps[n], rows=rows)
         tcpu = time.perf_counter() - t0
         cpu = {"value": S * N * len(args.norms) / tcpu, "unit": UNIT, "cores": oracle.threads_used(),
-               "kind": "oracle", "seconds": tcpu,
+               "cpu_model": cpu_model(), "kind": "oracle", "seconds": tcpu,
                "sample": f"{S} seeded (h,r) rows x all {N} tails, norms {args.norms} (FP64 brute force, C + OpenMP)"}
 
     elem = None
-    if rank == 0 and world == 1:
-        rows = sample_rows(N, R, 256, seed=5)
-        elem = {f"L{n}": element_fraction(joins[n], N, R, stats_last[n]["pivots_used"], eps[n], rows)
+    if rank == 0 and world == 1 and not args.no_extras:
+        rows = sample_rows(N, R, 128 if N > 50000 else 256, seed=5)
+        elem = {f"L{n}": element_fraction(runner.joins[n], N, R, stats_last[n]["pivots_used"], eps[n], rows)
                 for n in args.norms}
-    for j in joins.values():
-        j.close()
+    runner.close()
+
+    # ---- extra workloads (same GPU, same timing rules): c2 both norms, c3 theta sweep
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras = []
+        plan = [("c2", [2, 1], 1e-4)] + [("c3", [2], h) for h in (1e-6, 1e-5, 1e-4, 1e-3)]
+        for name, norms, hit in plan:
+            if name == args.config and norms == args.norms and hit == args.hit:
+                continue
+            extras.append(measure_workload(torch, kgc, dev, stream, name, norms, hit, args.extra_steps, 3,
+                                           thresholds, flush))
     clocks = clk.summary()
     if rank == 0:
         line = {
@@ -436,9 +544,9 @@ def run_ours(args, cfg, thresholds):
             "config": {"workload": wl, "N": N, "R": R, "d": d, "norms": args.norms, "eps": eps, "hit_rate": args.hit,
                        "parallelism": (f"tail partitions x{world}, every query on every rank" if args.tail_shard else
                                        f"query-tile shards x{world} ({['rank-local', 'cost-balanced', 'cyclic'][args.split]} "
-                                       f"split), tails replicated"),
-                       "joins": ("concurrent: one context, stream and host thread per norm" if conc else
-                                 "sequential on one stream"),
+                                       f"split), tails replicated; E/Rel NCCL-broadcast from rank 0 every step"),
+                       "joins": ("concurrent: one context, stream and host thread per norm" if runner.conc else
+                                 "one context per norm on one stream"),
                        "pivots": args.pivots,
                        "l2_cache": "flushed (512 MiB write) before every timed step, outside the timed events"},
             "result_triplets_per_step": results_total,
@@ -455,6 +563,7 @@ def run_ours(args, cfg, thresholds):
             "surviving_pair_fraction_elements_sampled": elem,
             "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "wall_s_timed_region": wall,
+            "extra_workloads": extras,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -511,16 +620,31 @@ def run_emulated_ranks(args, cfg, thresholds):
     return 0
 
 
-def main():
+def relaunch_distributed(args_argv, n):
+    """--gpus N without a launcher: re-execute this script under torch.distributed.run
+    (one process per GPU on this node, rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *args_argv]
+    return subprocess.call(cmd)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--hit", type=float, default=1e-4)
-    ap.add_argument("--norms", default="2,1", help="norms joined per step, e.g. '2,1' or '2'")
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--hit", type=float, default=None, help="target hit rate of theta (default: per config)")
+    ap.add_argument("--norms", default=None, help="norms joined per step, e.g. '2,1' or '2' (default: per config)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the c2 step / c3 sweep extra workloads")
+    ap.add_argument("--extra-steps", type=int, default=5)
     ap.add_argument("--sequential", action="store_true", help="run the step's joins one after the other")
     ap.add_argument("--tail-shard", type=int, default=0,
                     help="world > 1: 1 = partition-based join (rank k holds tails [kN/W, (k+1)N/W), every query)")
@@ -529,19 +653,21 @@ def main():
                          "measured per config (c2: 2, its hits concentrate in a few relations)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-rows", type=int, default=256, help="(h,r) rows per reference step")
+    ap.add_argument("--ref-rows", type=int, default=None, help="(h,r) rows per reference step")
     ap.add_argument("--emulate-ranks", type=int, default=0,
                     help="diagnostic: on ONE GPU run each of W shards in turn and print the per-shard device times "
                          "(projects the N=W device time; not the official line)")
     ap.add_argument("--pivots", default="auto",
                     help="1 = the paper's single pivot; 2..8 = multi-pivot pruning; auto = best measured per config")
-    args = ap.parse_args()
-    args.norms = [int(x) for x in args.norms.split(",")]
-    # Best measured pivot count per workload: multi-pivot pruning pays on c2 / c4,
-    # the paper's single pivot is faster on c3 (its extra keys/sort cost exceeds the pruning gain).
-    best_pivots = {"c1": 1, "c2": 8, "c3": 1, "c4": 8, "c5": 8}
-    args.pivots = best_pivots.get(args.config, 1) if args.pivots == "auto" else int(args.pivots)
-    args.split = {"c2": 2}.get(args.config, 0) if args.split == "auto" else int(args.split)
+    args = ap.parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not args.emulate_ranks:
+        return relaunch_distributed(argv, args.gpus)
+    args.norms = [int(x) for x in (args.norms or DEFAULT_NORMS[args.config]).split(",")]
+    args.hit = DEFAULT_HIT[args.config] if args.hit is None else args.hit
+    args.pivots = BEST_PIVOTS.get(args.config, 1) if args.pivots == "auto" else int(args.pivots)
+    args.split = BEST_SPLIT.get(args.config, 0) if args.split == "auto" else int(args.split)
+    if args.ref_rows is None:
+        args.ref_rows = 64 if CONFIGS[args.config].N > 100000 else 256
     cfg = CONFIGS[args.config]
     thresholds = load_thresholds()
     if args.impl == "reference":

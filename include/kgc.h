@@ -42,7 +42,8 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define KGC_ABI_VERSION 2  /* 2: kgc_options.tail_shard, kgc_stats_t.gathered_pairs */
+#define KGC_ABI_VERSION 3  /* 2: kgc_options.tail_shard, kgc_stats_t.gathered_pairs; 3: kgc_options.relation_batch,
+                              kgc_join_block */
 
 /* Opaque context: owns device buffers, the stream, per-join statistics. */
 typedef struct kgc_ctx kgc_ctx;
@@ -104,6 +105,11 @@ typedef struct {
     int32_t tail_shard;       /* world > 1: 1 = partition-based join (§4.7): rank */
                               /* k holds only tails [k N/W, (k+1) N/W) and joins every query       */
                               /* against them (split is ignored); 0 = tails replicated (default)   */
+    int32_t relation_batch;   /* relations per internal join pass; 0 = auto (as many as keep N x     */
+                              /* batch <= 2^28 query rows).  A join over more relations runs as    */
+                              /* consecutive batches whose results are appended (each batch is a   */
+                              /* complete join of its relations, so the union is R(eps)); this is   */
+                              /* what lifts N x R beyond 32-bit row ids (10^6 x 1000) */
 } kgc_options;
 
 /* Per-join statistics (of the last successful kgc_join). */
@@ -140,7 +146,7 @@ typedef struct {
 
 /* Fill *opt with defaults: device -1, rank 0, world 1, prune 1, pivot 0,
  * l2_engine 0, chunk_tiles 0, pivots 1, result_capacity 0, stream NULL,
- * l1_engine 0, split 0, tail_shard 0. */
+ * l1_engine 0, split 0, tail_shard 0, relation_batch 0. */
 void kgc_default_options(kgc_options* opt);
 
 /* Create a context.  opt == NULL means defaults.  Returns KGC_ENODEV when no
@@ -152,6 +158,13 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt);
  *   Rel : R x d float32, row-major, contiguous (relation embeddings)
  *   norm: 1 or 2; eps: distance threshold >= 0, finite.
  * N == 0 or R == 0 is valid and yields 0 results (E / Rel may then be NULL).
+ * Limits: N < 2^29 and R < 2^31 (int32 ids in kgc_triplet); larger N x R than
+ * 2^28 query rows runs in relation batches (kgc_options.relation_batch), bounded
+ * only by device memory.  Otherwise KGC_EINVAL.
+ * Stream order: every device operation runs on the context's stream (opt.stream /
+ * kgc_set_stream, else a non-blocking stream of the context).  Device-memory E /
+ * Rel must therefore be complete before the call, or be produced on the stream the
+ * context runs on (pass the producer's stream with kgc_set_stream).
  * Blocks until the result count is known.  On error the previous results are
  * dropped and the context stays usable. */
 int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t N, int64_t R, int32_t d,
@@ -206,6 +219,7 @@ enum {
     KGC_INSPECT_GATHER_LIST = 8,
     KGC_INSPECT_GATHER_COST = 9
 };
+/* After a join that ran in relation batches the arrays are those of the last batch. */
 int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes);
 
 /* Pure host function (no device needed), used by split = 1: the shard of
@@ -217,6 +231,19 @@ int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes);
  * same rule. */
 int64_t kgc_shard_range(const int64_t* cum, int64_t n, int64_t total, int32_t rank, int32_t world,
                         int64_t* begin, int64_t* end);
+
+/* One block of the partition-based join (PAPER.md:419-422 [§4.7]: "divide both
+ * datasets into several partitions ... join each pair of partitions"): every
+ * (h, r, t) with h in [h_off, h_off + Nh), t in [t_off, t_off + Nt), r in [0, R) and
+ * || Eh[h - h_off] + Rel_r - Et[t - t_off] ||_norm <= eps; records carry the global
+ * ids h, r, t.  Eh: Nh x d, Et: Nt x d, Rel: R x d, row-major fp32, host or device.
+ * The per-GPU step of kgc.partition_join, which keeps one entity block per GPU
+ * and passes the tail blocks around a ring of ranks, so that no GPU holds all of
+ * E.  Needs world == 1 and tail_shard == 0 (the caller orders the blocks);
+ * kgc_stats().triplets = Nh * Nt * R.  Errors as kgc_join (h_off + Nh and
+ * t_off + Nt must fit int32). */
+int kgc_join_block(kgc_ctx* ctx, const float* Eh, int64_t Nh, int64_t h_off, const float* Et, int64_t Nt,
+                   int64_t t_off, const float* Rel, int64_t R, int32_t d, int32_t norm, float eps);
 
 /* Structured Embedding (SE, PAPER.md:193 [§4.3]): every (h, r, t) with
  * dist3 = || W_r^lhs h - W_r^rhs t ||_1 <= eps, i.e. the same join with
@@ -242,8 +269,10 @@ int kgc_join_se(kgc_ctx* ctx, const float* E, const float* Wl, const float* Wr, 
  * actual triplets lie within it); epsilon-joins (every §8(a) step) at theta *
  * 0.9^j, j = 2, 1, 0, until one returns >= k triplets (j = 0 always does); the
  * k-th smallest returned distance is found by bisection on the device.  Distances are K6's (FP64, rounded to float).  Afterwards
- * kgc_results returns the epsilon-join at theta.  Needs world == 1
- * (KGC_EINVAL otherwise). */
+ * kgc_results / kgc_stats return the epsilon-join that was kept, i.e. the one at
+ * theta * 0.9^j for the first j (2, 1, 0) that returned >= k triplets; its
+ * threshold is kgc_stats().eps.  k == 0, N == 0 or R == 0 returns 0 with empty
+ * statistics.  Needs world == 1 (KGC_EINVAL otherwise). */
 int64_t kgc_topk(kgc_ctx* ctx, const float* E, const float* Rel, int64_t N, int64_t R, int32_t d, int32_t norm,
                  int64_t k, int32_t exclude_self, kgc_triplet* out);
 

@@ -39,6 +39,16 @@ enum Phase { EV_START, EV_H2D, EV_KEYS, EV_SORT, EV_RANGES, EV_STAGE, EV_TILES, 
 
 }  // namespace
 
+// Every device buffer of a context, in one list: the context declares them and
+// kgc_destroy frees them from the same list, so no buffer can be left out.
+#define KGC_DEVBUFS(X) X(E) X(Rel) X(pivot) X(kt) X(kq) X(mm_t) X(mm_q) X(sk0) X(sv0) X(sk1) X(sv1) X(counts) \
+    X(scan_tmp) X(qperm) X(qskey) X(tperm) X(tskey) X(tmin) X(tmax) X(cmax) X(cmin) X(ranges) X(cost) X(cum) \
+    X(nitem) X(item_off) X(items) X(item_tiles) X(item_cum) X(Qp) X(qs) X(Tp) X(T2) X(tstile) X(cand) X(res) X(ctr) \
+    X(est_hist) X(est_cost) X(mpP) X(mpkt) X(mpkq) X(mpmm_t) X(mpmm_q) X(mpc0) X(mpc1) X(tbmin) X(tbmax) X(qbmin) \
+    X(qbmax) X(tile_list) X(tk_sample) X(tk_sel) X(tk_cnt) X(Ts) X(tks) X(gblk) X(granges) X(glist) X(tsc) X(gT2) \
+    X(gtst) X(tmapbuf) X(fz) X(frt) X(frn) X(fzero) X(se_w) X(se_a64) X(se_b64) X(se_af) X(se_bf) X(se_zero) \
+    X(acc) X(Eb) X(se_max) X(mpqn)
+
 struct kgc_ctx {
     kgc_options opt{};
     int device = 0;
@@ -46,10 +56,9 @@ struct kgc_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
     std::string err;
-    DevBuf E, Rel, pivot, kt, kq, mm_t, mm_q, sk0, sv0, sk1, sv1, counts, scan_tmp, qperm, qskey, tperm, tskey, tmin,
-        tmax, cmax, cmin, ranges, cost, cum, nitem, item_off, items, item_tiles, item_cum, Qp, qs, Tp, T2, tstile, cand,
-        res, ctr, est_hist, est_cost, mpP, mpkt, mpkq, mpmm_t, mpmm_q, mpc0, mpc1, tbmin, tbmax, qbmin, qbmax, tile_list,
-        tk_sample, tk_sel, tk_cnt, Ts, tks, gblk, granges, glist, tsc, gT2, gtst, tmapbuf, fz, frt, frn, fzero, se_w, se_a64, se_b64, se_af, se_bf, se_zero, se_res, se_max;
+#define KGC_DECLARE_BUF(n) DevBuf n;
+    KGC_DEVBUFS(KGC_DECLARE_BUF)
+#undef KGC_DECLARE_BUF
     long long cand_cap = 0, res_cap = 0;
     long long n_results = -1;
     kgc_stats_t st{};
@@ -218,6 +227,7 @@ void kgc_default_options(kgc_options* o) {
     o->l1_engine = 0;
     o->split = 0;
     o->tail_shard = 0;
+    o->relation_batch = 0;
     o->result_capacity = 0;
     o->stream = nullptr;
 }
@@ -228,7 +238,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 5 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2 || o.tail_shard < 0 || o.tail_shard > 1) {
+        o.l2_engine > 5 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2 || o.tail_shard < 0 || o.tail_shard > 1 || o.relation_batch < 0) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -281,17 +291,9 @@ void kgc_destroy(kgc_ctx* ctx) {
     cudaGetDevice(&prev);
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    DevBuf* bufs[] = {&ctx->E,     &ctx->Rel,    &ctx->pivot,  &ctx->kt,    &ctx->kq,     &ctx->mm_t,   &ctx->mm_q,
-                      &ctx->sk0,   &ctx->sv0,    &ctx->sk1,    &ctx->sv1,   &ctx->counts, &ctx->scan_tmp,
-                      &ctx->qperm, &ctx->qskey,  &ctx->tperm,  &ctx->tskey, &ctx->tmin,   &ctx->tmax,   &ctx->cmax,
-                      &ctx->cmin,  &ctx->ranges, &ctx->cost,   &ctx->cum,   &ctx->nitem,  &ctx->item_off,
-                      &ctx->items, &ctx->item_tiles, &ctx->item_cum, &ctx->Qp,     &ctx->qs,     &ctx->Tp,    &ctx->T2,     &ctx->tstile, &ctx->cand,
-                      &ctx->res,   &ctx->ctr,  &ctx->est_hist, &ctx->est_cost, &ctx->mpP,   &ctx->mpkt,  &ctx->mpkq,  &ctx->mpmm_t, &ctx->mpmm_q,
-                      &ctx->mpc0,  &ctx->mpc1, &ctx->tbmin, &ctx->tbmax, &ctx->qbmin, &ctx->qbmax, &ctx->tile_list,
-                      &ctx->tk_sample, &ctx->tk_sel, &ctx->tk_cnt, &ctx->se_w, &ctx->se_a64, &ctx->se_b64,
-                      &ctx->se_af, &ctx->se_bf, &ctx->se_zero, &ctx->se_res, &ctx->se_max};
-    for (DevBuf* b : bufs)
-        if (b->p) cudaFree(b->p);
+#define KGC_FREE_BUF(n) if (ctx->n.p) cudaFree(ctx->n.p);
+    KGC_DEVBUFS(KGC_FREE_BUF)
+#undef KGC_FREE_BUF
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_split)
@@ -353,6 +355,7 @@ struct JoinExtra {
     const float* Et = nullptr;    // tails (default: E, or rows [t_off, t_off + Nt) of the device copy of E)
     long long Nt = -1;            // tail rows (default: N); tail partitions (kgc_options.tail_shard)
     long long t_off = 0;          // first tail row of the partition (added to emitted t)
+    long long h_off = 0;          // first head row of a head block (added to emitted h; kgc_join_block)
     float filt_eps = -1.f;        // threshold of every filter and pruning test (default: eps)
     const double* A64 = nullptr;  // exact connectors for verify_se (default: TransE verify)
     const double* B64 = nullptr;
@@ -386,7 +389,9 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const int Kpad = ((d + 7) / 8) * 8;
     // tile geometry of the plan: tensor cores 128 x 256; FP16x2 L1 128 x 128; FP32 SIMT 64 x 64
     const bool half_req = norm == 1 && ctx->opt.l1_engine == 1;
-    const int bq = gtc_req ? BM : plan_bq(ctx, norm, d, N);
+    // query-tile rows: the engine's (the pair engine's choice follows the tail rows, so a tail
+    // partition may use the 1-CTA engine where the whole tail set would not)
+    const int bq = gtc_req ? BM : (tc2 ? 2 * BM : (tc ? BM : (half_req ? BN_HALF : simt_t())));
     const int BN = tc ? BN_TC : (half_req ? BN_HALF : simt_t());
     const int QT = (int)((N + bq - 1) / bq);
     const int TT = (int)((NT + BN - 1) / BN);
@@ -545,7 +550,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             }
             CK(cudaEventRecord(ctx->ev[EV_TILES], s));
             if (n_items > 0) {
-                launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, nullptr, nullptr, E, Rel, N, QT, bq, d,
+                launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, nullptr, nullptr, E, Rel, E, N, QT, bq, d,
                               norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p), &dctr->res, ctx->res_cap,
                               ctx->num_sms, s, r_off);
                 LAUNCHED(1);
@@ -639,6 +644,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(ensure(ctx->mpkq, NR * K * 4));
         CK(ensure(ctx->mpmm_t, (size_t)K * 8));
         CK(ensure(ctx->mpmm_q, (size_t)R * K * 8));
+        CK(ensure(ctx->mpqn, (size_t)R * 4));
         CK(ensure(ctx->mpc0, nsort * 8));
         CK(ensure(ctx->mpc1, nsort * 8));
         CK(ensure(ctx->tbmin, (size_t)TT * K * 4));
@@ -648,10 +654,10 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         launch_pick_pivots(Et, NT, d, norm, K, pivot, P<float>(ctx->mpP), s);
         LAUNCHED(1);
         launch_mp_keys(Et, nullptr, NT, 1, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkt), P<unsigned>(ctx->mpmm_t),
-                       &dctr->nonfinite, s);
+                       nullptr, &dctr->nonfinite, s);
         LAUNCHED(2);
         launch_mp_keys(E, Rel, N, R, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q),
-                       &dctr->nonfinite, s);
+                       P<unsigned>(ctx->mpqn), &dctr->nonfinite, s);
         LAUNCHED(2);
         CK(cudaEventRecord(ctx->ev[EV_KEYS], s));
         // ---- a3: Morton-order sorts (tiles compact in pivot space)
@@ -680,9 +686,9 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(cudaEventRecord(ctx->ev[EV_SORT], s));
         // ---- a4: K-dim tile boxes and the L_inf test of every tile pair
         launch_mp_boxes(P<float>(ctx->mpkt), P<unsigned>(ctx->tperm), 1, NT, BN, TT, K, P<float>(ctx->tbmin),
-                        P<float>(ctx->tbmax), s);
+                        P<float>(ctx->tbmax), nullptr, s);
         launch_mp_boxes(P<float>(ctx->mpkq), P<unsigned>(ctx->qperm), R, N, bq, QT, K, P<float>(ctx->qbmin),
-                        P<float>(ctx->qbmax), s);
+                        P<float>(ctx->qbmax), P<unsigned>(ctx->mpqn), s);
         LAUNCHED(2);
         launch_mp_count(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tbmin), P<float>(ctx->tbmax), nq, TT,
                         K, feps, mp_relm(d), 1, P<int2>(ctx->ranges), P<long long>(ctx->cost), s);
@@ -941,8 +947,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                                  ctx->num_sms, s, r_off);
             else
                 launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, P<int>(ctx->qperm), P<int>(ctx->tperm),
-                              E, Rel, N, QT, bq, d, norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p),
-                              &dctr->res, ctx->res_cap, ctx->num_sms, s, r_off, NT, ex.t_off);
+                              E, Rel, Et, N, QT, bq, d, norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p),
+                              &dctr->res, ctx->res_cap, ctx->num_sms, s, r_off, NT, ex.t_off, ex.h_off);
             LAUNCHED(1);
         }
         CK(cudaEventRecord(ctx->ev[EV_VERIFY], s));
@@ -1047,6 +1053,143 @@ static int split_range(kgc_ctx* ctx, const float* E_in, const float* Rel_in, lon
     return KGC_OK;
 }
 
+// ------------------------------------------------------------ relation batches
+// Results of several join_impl calls (relation batches, SE relations) are appended to
+// ctx->acc; acc_finish makes the accumulated list the context's results.
+static int acc_append(kgc_ctx* ctx, long long* total) {
+    const long long n = ctx->n_results;
+    if (n <= 0) return KGC_OK;
+    cudaStream_t s = ctx->stream;
+    const size_t need = (size_t)(*total + n) * 16;
+    if (need > ctx->acc.n) {
+        DevBuf nb;
+        CK(ensure(nb, std::max<size_t>(need + need / 2, (size_t)1 << 20)));
+        if (*total) CK(cudaMemcpyAsync(nb.p, ctx->acc.p, (size_t)*total * 16, cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        if (ctx->acc.p) cudaFree(ctx->acc.p);
+        ctx->acc = nb;
+    }
+    CK(cudaMemcpyAsync(P<char>(ctx->acc) + (size_t)*total * 16, ctx->res.p, (size_t)n * 16, cudaMemcpyDeviceToDevice,
+                       s));
+    *total += n;
+    return KGC_OK;
+}
+static int acc_finish(kgc_ctx* ctx, long long total) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::swap(ctx->res, ctx->acc);  // the accumulated results become the context's results
+    ctx->res_cap = (long long)(ctx->res.n / 16);
+    ctx->n_results = total;
+    return KGC_OK;
+}
+// Sum of the per-call statistics of a multi-call join (geometry from the last call).
+static void acc_stats(kgc_stats_t& a, const kgc_stats_t& st) {
+    a.tile_pairs_total += st.tile_pairs_total;
+    a.tile_pairs_surviving += st.tile_pairs_surviving;
+    a.tile_pairs_mine += st.tile_pairs_mine;
+    a.work_items_mine += st.work_items_mine;
+    a.candidates += st.candidates;
+    a.results += st.results;
+    a.h2d_bytes += st.h2d_bytes;
+    a.launches += st.launches;
+    a.reruns += st.reruns;
+    a.gathered_pairs += st.gathered_pairs;
+    a.ms_h2d += st.ms_h2d;
+    a.ms_keys += st.ms_keys;
+    a.ms_sort += st.ms_sort;
+    a.ms_ranges += st.ms_ranges;
+    a.ms_stage += st.ms_stage;
+    a.ms_tiles += st.ms_tiles;
+    a.ms_recheck += st.ms_recheck;
+    a.ms_total += st.ms_total;
+    a.query_tile_rows = st.query_tile_rows;
+    a.tail_tile_rows = st.tail_tile_rows;
+    a.query_tiles = st.query_tiles;
+    a.tail_tiles = st.tail_tiles;
+    a.pivots_used = st.pivots_used;
+    a.engine = st.engine;
+}
+
+// Relations per join_impl call.  Row ids (relation x sorted query position) are 32-bit in
+// the candidate records and several kernels, and the per-call buffers grow with N x R
+// (keys, sort scratch, permutations), so a join over more than 2^28 query rows (the
+// paper's motivating 10^6 entities x 1000 relations, is 10^9) runs as
+// consecutive relation batches of at most 2^28 rows each; results are appended.  Every
+// batch is a complete join of its relations (Definition 1 is per triplet), so the union is
+// the join.  kgc_options.relation_batch overrides the size (tests).
+static long long relation_batch(const kgc_ctx* ctx, long long N) {
+    if (ctx->opt.relation_batch > 0) return ctx->opt.relation_batch;
+    const long long rb = (1LL << 28) / std::max<long long>(N, 1);
+    return std::max<long long>(rb, 1);
+}
+
+// The join of relations [r_lo, r_hi).  Query tiles [a, b) in the global numbering r * QT + q
+// (a >= 0), or the modes of join_impl: a = b = -1 (cost-balanced shard of everything), -2
+// (cyclic), or a = 0, b = LLONG_MAX (every query tile: tail partitions).
+static int join_relations(kgc_ctx* ctx, const float* E, const float* Rel, long long N, long long R, int d, int norm,
+                          float eps, long long r_lo, long long r_hi, long long a, long long b, long long QT,
+                          const JoinExtra& ex) {
+    const long long rb = relation_batch(ctx, N);
+    auto local = [&](long long r1, long long r2, long long* la, long long* lb) {
+        if (a < 0 || b == LLONG_MAX) {
+            *la = a;
+            *lb = b;
+            return true;
+        }
+        *la = std::max(a, r1 * QT) - r1 * QT;
+        *lb = std::min(b, r2 * QT) - r1 * QT;
+        return *la < *lb;
+    };
+    if (r_hi - r_lo <= rb) {
+        long long la = 0, lb = 0;
+        local(r_lo, r_hi, &la, &lb);
+        return join_impl(ctx, E, Rel + r_lo * d, N, r_hi - r_lo, d, norm, eps, (int)r_lo, la, lb, R, ex);
+    }
+    cudaStream_t s = ctx->stream;
+    // stage host inputs once (join_impl would copy them per batch)
+    const float* Ed = E;
+    const float* Rd = Rel;
+    int64_t h2d = 0;
+    if (!is_device_ptr(E, ctx->device)) {
+        CK(ensure(ctx->E, (size_t)N * d * 4));
+        CK(cudaMemcpyAsync(ctx->E.p, E, (size_t)N * d * 4, cudaMemcpyDefault, s));
+        Ed = P<float>(ctx->E);
+        h2d += (int64_t)N * d * 4;
+    }
+    if (!is_device_ptr(Rel, ctx->device)) {
+        CK(ensure(ctx->Rel, (size_t)R * d * 4));
+        CK(cudaMemcpyAsync(ctx->Rel.p, Rel, (size_t)R * d * 4, cudaMemcpyDefault, s));
+        Rd = P<float>(ctx->Rel);
+        h2d += (int64_t)R * d * 4;
+    }
+    kgc_stats_t acc{};
+    long long total = 0;
+    for (long long r1 = r_lo; r1 < r_hi; r1 += rb) {
+        const long long r2 = std::min(r_hi, r1 + rb);
+        long long la = 0, lb = 0;
+        if (!local(r1, r2, &la, &lb)) continue;
+        const int rc = join_impl(ctx, Ed, Rd + r1 * d, N, r2 - r1, d, norm, eps, (int)r1, la, lb, R, ex);
+        if (rc != KGC_OK) return rc;
+        acc_stats(acc, ctx->st);
+        const int rc2 = acc_append(ctx, &total);
+        if (rc2 != KGC_OK) return rc2;
+    }
+    const int rc = acc_finish(ctx, total);
+    if (rc != KGC_OK) return rc;
+    acc.N = N;
+    acc.R = R;
+    acc.d = d;
+    acc.norm = norm;
+    acc.eps = eps;
+    acc.rank = ctx->opt.rank;
+    acc.world = ctx->opt.world;
+    acc.triplets = (double)N * (double)N * (double)R;
+    acc.h2d_bytes += h2d;
+    acc.results = total;
+    ctx->st = acc;
+    ctx->have_join = true;
+    return KGC_OK;
+}
+
 extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t N, int64_t R, int32_t d, int32_t norm,
                         float eps) {
     if (!ctx) return KGC_EINVAL;
@@ -1059,8 +1202,8 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
                 norm, (double)eps);
         return KGC_EINVAL;
     }
-    if (N > INT_MAX / 2 || (double)R * (double)((N + SIMT_T - 1) / SIMT_T + 1) * BM > 2.0e9) {  // rowid fits int32
-        set_err(ctx, "kgc_join: N*R too large for 32-bit row ids");
+    if (N > INT_MAX / 4 || R > INT_MAX) {  // entity / relation ids are int32 in the records
+        set_err(ctx, "kgc_join: N > 2^29 or R > 2^31 - 1 (32-bit entity / relation ids)");
         return KGC_EINVAL;
     }
     if (N == 0 || R == 0) {
@@ -1101,7 +1244,7 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
             JoinExtra ex;
             ex.Nt = t1 - t0;
             ex.t_off = t0;
-            rc = join_impl(ctx, E, Rel, N, R, d, norm, eps, 0, 0, LLONG_MAX, R, ex);
+            rc = join_relations(ctx, E, Rel, N, R, d, norm, eps, 0, R, 0, LLONG_MAX, 0, ex);
         }
     } else if (ctx->opt.world > 1 && ctx->opt.split == 0 && !(norm == 2 && ctx->opt.l2_engine == 5)) {
         did_split = true;
@@ -1122,16 +1265,15 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
         } else if (rc == KGC_OK) {
             (void)nq;
             const long long r_lo = a / QT, r_hi = (b - 1) / QT + 1;
-            rc = join_impl(ctx, Ed, Rd + r_lo * d, N, r_hi - r_lo, d, norm, eps, (int)r_lo, a - r_lo * QT,
-                           b - r_lo * QT, R);
+            rc = join_relations(ctx, Ed, Rd, N, R, d, norm, eps, r_lo, r_hi, a, b, QT, JoinExtra());
             ctx->st.h2d_bytes += h2d;
         }
     } else if (ctx->opt.world > 1 && ctx->opt.split == 2) {
         // Cyclic split: every rank preprocesses everything and takes query tiles q with
         // q % world == rank, so hit-dense relations spread over all ranks.
-        rc = join_impl(ctx, E, Rel, N, R, d, norm, eps, 0, -2, -2, R);
+        rc = join_relations(ctx, E, Rel, N, R, d, norm, eps, 0, R, -2, -2, 0, JoinExtra());
     } else {
-        rc = join_impl(ctx, E, Rel, N, R, d, norm, eps, 0, -1, -1, R);
+        rc = join_relations(ctx, E, Rel, N, R, d, norm, eps, 0, R, -1, -1, 0, JoinExtra());
     }
     if (rc != KGC_OK) {
         cudaStreamSynchronize(ctx->stream);
@@ -1139,6 +1281,80 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
     } else {
         ctx->st.ms_split = 0.f;
         if (did_split) cudaEventElapsedTime(&ctx->st.ms_split, ctx->ev_split[0], ctx->ev_split[1]);
+        ctx->st.ms_host = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+    }
+    cudaSetDevice(prev);
+    return rc;
+}
+
+// ------------------------------------------------------------------ head block x tail block
+// One block of the partition-based join (§4.7): the queries of a head
+// block against one tail block, ids offset to the global numbering.  The ring that walks
+// every tail block past every head block runs over the caller's process group
+// (kgc.partition_join); this call is the per-GPU step of it.
+extern "C" int kgc_join_block(kgc_ctx* ctx, const float* Eh, int64_t Nh, int64_t h_off, const float* Et, int64_t Nt,
+                              int64_t t_off, const float* Rel, int64_t R, int32_t d, int32_t norm, float eps) {
+    if (!ctx) return KGC_EINVAL;
+    ctx->err.clear();
+    ctx->n_results = -1;
+    ctx->have_join = false;
+    if (Nh < 0 || Nt < 0 || h_off < 0 || t_off < 0 || R < 0 || d < 1 || d > KGC_MAX_DIM || (norm != 1 && norm != 2) ||
+        !(eps >= 0.f) || !std::isfinite(eps) || h_off + Nh > INT_MAX || t_off + Nt > INT_MAX || Nh > INT_MAX / 4 ||
+        Nt > INT_MAX / 4 || R > INT_MAX) {
+        set_err(ctx, "kgc_join_block: invalid argument (Nh=%lld h_off=%lld Nt=%lld t_off=%lld R=%lld d=%d norm=%d "
+                "eps=%g)", (long long)Nh, (long long)h_off, (long long)Nt, (long long)t_off, (long long)R, d, norm,
+                (double)eps);
+        return KGC_EINVAL;
+    }
+    if (ctx->opt.world != 1 || ctx->opt.tail_shard) {
+        set_err(ctx, "kgc_join_block: needs a single-shard context (world = 1); the caller orders the blocks");
+        return KGC_EINVAL;
+    }
+    if (Nh == 0 || Nt == 0 || R == 0) {
+        memset(&ctx->st, 0, sizeof ctx->st);
+        ctx->st.N = Nh;
+        ctx->st.R = R;
+        ctx->st.d = d;
+        ctx->st.norm = norm;
+        ctx->st.eps = eps;
+        ctx->st.world = 1;
+        ctx->n_results = 0;
+        ctx->have_join = true;
+        return KGC_OK;
+    }
+    if (!Eh || !Et || !Rel) {
+        set_err(ctx, "kgc_join_block: NULL Eh, Et or Rel");
+        return KGC_EINVAL;
+    }
+    const auto host_t0 = std::chrono::steady_clock::now();
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->device);
+    auto run = [&]() -> int {
+        JoinExtra ex;
+        ex.Et = Et;
+        ex.Nt = Nt;
+        ex.t_off = t_off;
+        ex.h_off = h_off;
+        int64_t h2d = 0;
+        if (!is_device_ptr(Et, ctx->device)) {
+            CK(ensure(ctx->Eb, (size_t)Nt * d * 4));
+            CK(cudaMemcpyAsync(ctx->Eb.p, Et, (size_t)Nt * d * 4, cudaMemcpyDefault, ctx->stream));
+            ex.Et = P<float>(ctx->Eb);
+            h2d = Nt * d * 4;
+        }
+        const int rc = join_relations(ctx, Eh, Rel, Nh, R, d, norm, eps, 0, R, -1, -1, 0, ex);
+        ctx->st.h2d_bytes += h2d;
+        return rc;
+    };
+    const int rc = run();
+    if (rc != KGC_OK) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaGetLastError();
+        ctx->n_results = -1;
+        ctx->have_join = false;
+    } else {
+        ctx->st.triplets = (double)Nh * (double)Nt * (double)R;
         ctx->st.ms_host = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
     }
     cudaSetDevice(prev);
@@ -1212,7 +1428,6 @@ extern "C" int kgc_join_se(kgc_ctx* ctx, const float* E, const float* Wl, const 
         CK(ensure(ctx->se_zero, (size_t)d * 4));
         CK(ensure(ctx->se_max, 8));
         CK(cudaMemsetAsync(ctx->se_zero.p, 0, (size_t)d * 4, s));
-        size_t se_cap = 0;
         kgc_stats_t acc{};
         for (long long r = 0; r < R; ++r) {
             unsigned int mx[2] = {0, 0};
@@ -1226,7 +1441,7 @@ extern "C" int kgc_join_se(kgc_ctx* ctx, const float* E, const float* Wl, const 
                                                            (double)__uint_as_float_host(mx[1])) * (1.0 + 1e-6);
             const float feps = nextafterf((float)((double)eps + widen), FLT_MAX);
             if (!std::isfinite(feps)) {
-                set_err(ctx, "kgc_join_se: connector values overflow float");
+                set_err(ctx, "kgc_join_se: non-finite value in E, W_lhs or W_rhs (or connector values overflow float)");
                 return KGC_EDATA;
             }
             JoinExtra ex;
@@ -1237,47 +1452,15 @@ extern "C" int kgc_join_se(kgc_ctx* ctx, const float* E, const float* Wl, const 
             const int rc = join_impl(ctx, P<float>(ctx->se_af), P<float>(ctx->se_zero), N, 1, d, 1, eps, (int)r, -1, -1,
                                      1, ex);
             if (rc != KGC_OK) return rc;
-            const long long n = ctx->n_results;
-            if (n > 0) {
-                if ((size_t)(total + n) > se_cap) {
-                    const size_t ncap = std::max<size_t>((size_t)(total + n) * 3 / 2, 1 << 16);
-                    DevBuf nb;
-                    CK(ensure(nb, ncap * 16));
-                    if (total) CK(cudaMemcpyAsync(nb.p, ctx->se_res.p, (size_t)total * 16, cudaMemcpyDeviceToDevice, s));
-                    CK(cudaStreamSynchronize(s));
-                    if (ctx->se_res.p) cudaFree(ctx->se_res.p);
-                    ctx->se_res = nb;
-                    se_cap = ncap;
-                }
-                CK(cudaMemcpyAsync(P<char>(ctx->se_res) + (size_t)total * 16, ctx->res.p, (size_t)n * 16,
-                                   cudaMemcpyDeviceToDevice, s));
-            }
-            total += n;
-            const kgc_stats_t& st = ctx->st;
-            acc.tile_pairs_total += st.tile_pairs_total;
-            acc.tile_pairs_surviving += st.tile_pairs_surviving;
-            acc.tile_pairs_mine += st.tile_pairs_mine;
-            acc.work_items_mine += st.work_items_mine;
-            acc.candidates += st.candidates;
-            acc.launches += st.launches + 5;
-            acc.reruns += st.reruns;
-            acc.ms_keys += st.ms_keys;
-            acc.ms_sort += st.ms_sort;
-            acc.ms_ranges += st.ms_ranges;
-            acc.ms_stage += st.ms_stage;
-            acc.ms_tiles += st.ms_tiles;
-            acc.ms_recheck += st.ms_recheck;
-            acc.ms_total += st.ms_total;
-            acc.query_tile_rows = st.query_tile_rows;
-            acc.tail_tile_rows = st.tail_tile_rows;
-            acc.query_tiles = st.query_tiles * R;
-            acc.tail_tiles = st.tail_tiles * R;
-            acc.pivots_used = st.pivots_used;
-            acc.engine = st.engine;
+            acc_stats(acc, ctx->st);
+            acc.launches += 5;
+            const int rc2 = acc_append(ctx, &total);
+            if (rc2 != KGC_OK) return rc2;
         }
-        CK(cudaStreamSynchronize(s));
-        std::swap(ctx->res, ctx->se_res);  // the accumulated results become the context's results
-        ctx->res_cap = (long long)(ctx->res.n / 16);
+        const int rc = acc_finish(ctx, total);
+        if (rc != KGC_OK) return rc;
+        acc.query_tiles *= R;
+        acc.tail_tiles *= R;
         acc.N = N;
         acc.R = R;
         acc.d = d;
@@ -1347,7 +1530,14 @@ extern "C" int64_t kgc_topk(kgc_ctx* ctx, const float* E, const float* Rel, int6
         return KGC_EINVAL;
     }
     if (k == 0 || N == 0 || R == 0) {
+        memset(&ctx->st, 0, sizeof ctx->st);  // no join ran: empty statistics, not the previous join's
+        ctx->st.N = N;
+        ctx->st.R = R;
+        ctx->st.d = d;
+        ctx->st.norm = norm;
+        ctx->st.world = 1;
         ctx->n_results = 0;
+        ctx->have_join = true;
         return 0;
     }
     if (!E || !Rel) {

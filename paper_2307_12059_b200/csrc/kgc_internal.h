@@ -130,12 +130,13 @@ void radix_sort_u64_segments(long long S, long long L, int bits, unsigned long l
 void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, const double* p0, float* P,
                         cudaStream_t s);
 void launch_mp_keys(const float* E, const float* Rel, long long N, long long nseg, int d, int norm, int K,
-                    const float* P, float* keys, unsigned int* minmax, unsigned int* nonfinite, cudaStream_t s);
+                    const float* P, float* keys, unsigned int* minmax, unsigned int* qnmax, unsigned int* nonfinite,
+                    cudaStream_t s);
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
                       unsigned long long* code, unsigned int* idx, cudaStream_t s);
 void launch_kd_refine(const float* keys, int* perm, long long nseg, long long L, int K, cudaStream_t s);
 void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg, long long L, int ROWS, int ntile,
-                     int K, float* bmin, float* bmax, cudaStream_t s);
+                     int K, float* bmin, float* bmax, const unsigned int* qnmax, cudaStream_t s);
 void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,
                      int TT, int K, float theta, float relm, int prune, int2* ranges, long long* cost, cudaStream_t s);
 void launch_mp_emit(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax,
@@ -192,9 +193,12 @@ void launch_count_res_le(const KgcTripletDev* res, long long n, float theta, int
                          unsigned long long* cnt, cudaStream_t s);
 void launch_compact_res_le(const KgcTripletDev* res, long long n, float theta, int exclude_self, KgcTripletDev* out,
                            unsigned long long* cnt, long long cap, cudaStream_t s);
+// E: heads (row h of the query side), Et: tails (row t of the tail side, e.g. E + t_off d for a
+// tail partition); records carry h + h_off, r + r_off, t + t_off.
 void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap,
-                   const int* qperm, const int* tperm, const float* E, const float* Rel, long long N, int QT,
-                   int bq, int d, int norm, float theta, KgcTripletDev* out, unsigned long long* res_count,
-                   long long res_cap, int num_sms, cudaStream_t s, int r_off, long long Nt = -1, long long t_off = 0);
+                   const int* qperm, const int* tperm, const float* E, const float* Rel, const float* Et, long long N,
+                   int QT, int bq, int d, int norm, float theta, KgcTripletDev* out, unsigned long long* res_count,
+                   long long res_cap, int num_sms, cudaStream_t s, int r_off, long long Nt = -1, long long t_off = 0,
+                   long long h_off = 0);
 
 }  // namespace kgc

@@ -16,6 +16,7 @@
 //                 keys, so that the radix-sorted tiles are compact in pivot space
 //   mp_boxes      per tile and pivot: [min, max] of its rows' keys
 //   mp_count / mp_emit  per query tile: count, then list, the surviving tail tiles
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 #include <type_traits>
@@ -146,7 +147,8 @@ template <int NORM, bool QUERY, int K>
 __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
                                                       long long N, long long nseg, int d, int nch,
                                                       const float* __restrict__ P, float* __restrict__ keys,
-                                                      unsigned int* minmax, unsigned int* nonfinite) {
+                                                      unsigned int* minmax, unsigned int* qnmax,
+                                                      unsigned int* nonfinite) {
     extern __shared__ __align__(16) float mk_smem[];
     const int S = mk_stride(d);                            // entity row stride (zero padded)
     const int D4 = (d + 3) / 4 * 4;                        // pivot / relation row stride (zero padded)
@@ -170,11 +172,13 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
         }
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    float mn[NU][K], mx[NU][K];
+    float mn[NU][K], mx[NU][K], qn[NU];
 #pragma unroll
-    for (int u = 0; u < NU; ++u)
+    for (int u = 0; u < NU; ++u) {
+        qn[u] = 0.f;
 #pragma unroll
         for (int k = 0; k < K; ++k) { mn[u][k] = FLT_MAX; mx[u][k] = 0.f; }
+    }
     for (int ch = 0; ch < nch; ++ch) {
         const long long h0 = ((long long)blockIdx.x * nch + ch) * ENT;
         if (h0 >= N) break;
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
         for (int x = threadIdx.x; x < ENT * S; x += blockDim.x) {
             const int i = x / S, k = x % S;
             const float v = (h0 + i < N && k < d) ? E[(h0 + i) * d + k] : 0.f;
-            if (!QUERY) bad |= !isfinite(v);
+            bad |= !isfinite(v);
             Es[x] = v;
         }
         __syncthreads();
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
             const long long h = h0 + eloc;
             const float* es = Es + eloc * S;
             const float* rs = QUERY ? Rs + rl * D4 : nullptr;
-            float acc[K];
+            float acc[K], an = 0.f;  // an: ||fl32(h + r)||_p (squared for L2), queries only
 #pragma unroll
             for (int k = 0; k < K; ++k) acc[k] = 0.f;
             // 4 dims per step: float4 loads of the entity row, relation row (broadcast)
@@ -207,6 +211,8 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
                     const float4 r4 = *reinterpret_cast<const float4*>(rs + dd);
                     q4 = make_float4(__fadd_rn(e4.x, r4.x), __fadd_rn(e4.y, r4.y), __fadd_rn(e4.z, r4.z),
                                      __fadd_rn(e4.w, r4.w));  // connector_1(h, r) = h + r
+                    if (NORM == 1) an = an + fabsf(q4.x) + fabsf(q4.y) + fabsf(q4.z) + fabsf(q4.w);
+                    else an = fmaf(q4.w, q4.w, fmaf(q4.z, q4.z, fmaf(q4.y, q4.y, fmaf(q4.x, q4.x, an))));
                 }
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
@@ -217,6 +223,7 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
                 }
             }
             if (h < N) {
+                if (QUERY) qn[u] = fmaxf(qn[u], NORM == 2 ? sqrtf(an) : an);
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const float key = NORM == 2 ? sqrtf(acc[k]) : acc[k];
@@ -244,14 +251,161 @@ __global__ void __launch_bounds__(256) mp_keys_kernel(const float* __restrict__ 
                 atomicMax(&minmax[((size_t)r * K + k) * 2 + 1], __float_as_uint(z));
             }
         }
+        if (QUERY) {
+            float z = qn[u];
+            for (int o = 16; o > 0; o >>= 1) z = fmaxf(z, __shfl_xor_sync(0xffffffffu, z, o));
+            if (lane == 0) atomicMax(&qnmax[r], __float_as_uint(z));
+        }
     }
 }
 
-__global__ void mp_init_minmax_kernel(unsigned int* mm, long long n) {
+// Query keys d(p_k, fl32(h + r)) for every (h, r): the K1 kernel with the most work
+// (N R K d distances, c4: 7.3e9 per join).  Lane = entity (32 per chunk, rows staged in
+// shared memory), warp w = NU consecutive relations, so each staged entity element and
+// each (negated) pivot element loaded from shared memory serves NU x K distance terms:
+// with NU = 4, K = 8 a 4-dim step is 13 shared loads against 72 packed FP32 ops
+// (FADD2 / FFMA2: two dims per instruction), where one relation per lane was bound by
+// the shared-memory loads.  Per (relation, pivot) key min / max: REDUX per chunk, the
+// running value held by lane u K + k.  Same FP32 values up to summation order (the key
+// margin covers any order); ||fl32(h + r)||_p per relation for the box widening.
+template <int NORM, int K, int NU>
+__global__ void __launch_bounds__(256) mp_qkeys_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
+                                                       long long N, long long R, int d, int nch,
+                                                       const float* __restrict__ P, float* __restrict__ keys,
+                                                       unsigned int* minmax, unsigned int* qnmax,
+                                                       unsigned int* nonfinite) {
+    static_assert(NU * K <= 32, "one lane per (relation, pivot) min/max");
+    extern __shared__ __align__(16) float mq_smem[];
+    const int S = mk_stride(d);
+    const int D4 = (d + 3) / 4 * 4;
+    constexpr int RB = 8 * NU;                            // relations per block
+    float* Es = mq_smem;                                  // [32][S] entity rows
+    float* Ps = Es + 32 * S;                              // [K][D4] negated pivots
+    float* Rs = Ps + K * D4;                              // [RB][D4] relation rows
+    const long long r0 = (long long)blockIdx.y * RB;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    bool bad = false;
+    for (int x = threadIdx.x; x < K * D4; x += blockDim.x) {
+        const int i = x / D4, k = x % D4;
+        Ps[x] = k < d ? -P[i * d + k] : 0.f;
+    }
+    for (int x = threadIdx.x; x < RB * D4; x += blockDim.x) {
+        const int i = x / D4, k = x % D4;
+        const float v = (r0 + i < R && k < d) ? Rel[(r0 + i) * d + k] : 0.f;
+        bad |= !isfinite(v);
+        Rs[x] = v;
+    }
+    const long long rw = r0 + (long long)w * NU;          // this warp's first relation
+    const int nu = rw >= R ? 0 : (int)min((long long)NU, R - rw);
+    float run_mn = FLT_MAX, run_mx = 0.f, run_qn = 0.f;  // lane u K + k: (relation rw + u, pivot k)
+    for (int ch = 0; ch < nch; ++ch) {
+        const long long h0 = ((long long)blockIdx.x * nch + ch) * 32;
+        if (h0 >= N) break;
+        __syncthreads();
+        for (int x = threadIdx.x; x < 32 * S; x += blockDim.x) {
+            const int i = x / S, k = x % S;
+            const float v = (h0 + i < N && k < d) ? E[(h0 + i) * d + k] : 0.f;
+            bad |= !isfinite(v);
+            Es[x] = v;
+        }
+        __syncthreads();
+        if (nu == 0) continue;
+        const long long h = h0 + lane;
+        const float* es = Es + lane * S;
+        float2 acc[NU][K], an[NU];
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+            an[u] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[u][k] = make_float2(0.f, 0.f);
+        }
+        for (int dd = 0; dd < D4; dd += 4) {
+            const float4 e4 = *reinterpret_cast<const float4*>(es + dd);
+            float2 qa[NU], qb[NU];
+#pragma unroll
+            for (int u = 0; u < NU; ++u) {
+                const float4 r4 = *reinterpret_cast<const float4*>(Rs + (w * NU + u) * D4 + dd);
+                qa[u] = __fadd2_rn(make_float2(e4.x, e4.y), make_float2(r4.x, r4.y));  // connector_1 = h + r
+                qb[u] = __fadd2_rn(make_float2(e4.z, e4.w), make_float2(r4.z, r4.w));
+                if (NORM == 2) {
+                    an[u] = __ffma2_rn(qa[u], qa[u], an[u]);
+                    an[u] = __ffma2_rn(qb[u], qb[u], an[u]);
+                } else {
+                    an[u].x += fabsf(qa[u].x) + fabsf(qb[u].x);
+                    an[u].y += fabsf(qa[u].y) + fabsf(qb[u].y);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const float4 p4 = *reinterpret_cast<const float4*>(Ps + k * D4 + dd);
+                const float2 pa = make_float2(p4.x, p4.y), pb = make_float2(p4.z, p4.w);
+#pragma unroll
+                for (int u = 0; u < NU; ++u) {
+                    const float2 xa = __fadd2_rn(qa[u], pa), xb = __fadd2_rn(qb[u], pb);
+                    if (NORM == 2) {
+                        acc[u][k] = __ffma2_rn(xa, xa, acc[u][k]);
+                        acc[u][k] = __ffma2_rn(xb, xb, acc[u][k]);
+                    } else {
+                        acc[u][k].x += fabsf(xa.x) + fabsf(xb.x);
+                        acc[u][k].y += fabsf(xa.y) + fabsf(xb.y);
+                    }
+                }
+            }
+        }
+        const bool hv = h < N;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+            if (u >= nu) break;
+            const long long r = rw + u;
+            float kv[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const float s2 = acc[u][k].x + acc[u][k].y;
+                kv[k] = NORM == 2 ? sqrtf(s2) : s2;
+            }
+            if (hv) {
+                float* dst = keys + ((size_t)r * N + h) * K;
+                if (K == 8) {
+                    reinterpret_cast<float4*>(dst)[0] = make_float4(kv[0], kv[1], kv[2], kv[3]);
+                    reinterpret_cast<float4*>(dst)[1] = make_float4(kv[4], kv[5], kv[6], kv[7]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) dst[k] = kv[k];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const unsigned bits = __float_as_uint(kv[k]);
+                const unsigned m = __reduce_min_sync(0xffffffffu, hv ? bits : 0x7f7fffffu);
+                const unsigned z = __reduce_max_sync(0xffffffffu, hv ? bits : 0u);
+                if (lane == u * K + k) {
+                    run_mn = fminf(run_mn, __uint_as_float(m));
+                    run_mx = fmaxf(run_mx, __uint_as_float(z));
+                }
+            }
+            const float qn = NORM == 2 ? sqrtf(an[u].x + an[u].y) : an[u].x + an[u].y;
+            const unsigned zq = __reduce_max_sync(0xffffffffu, hv ? __float_as_uint(qn) : 0u);
+            if (lane == u) run_qn = fmaxf(run_qn, __uint_as_float(zq));
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
+    if (lane < nu * K) {
+        const long long r = rw + lane / K;
+        const int k = lane % K;
+        atomicMin(&minmax[((size_t)r * K + k) * 2], __float_as_uint(run_mn));
+        atomicMax(&minmax[((size_t)r * K + k) * 2 + 1], __float_as_uint(run_mx));
+    }
+    if (lane < nu) atomicMax(&qnmax[rw + lane], __float_as_uint(run_qn));
+}
+
+__global__ void mp_init_minmax_kernel(unsigned int* mm, long long n, unsigned int* qnmax, long long nseg) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         mm[2 * i] = __float_as_uint(FLT_MAX);
         mm[2 * i + 1] = 0u;
     }
+    if (qnmax)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nseg; i += (long long)gridDim.x * blockDim.x)
+            qnmax[i] = 0u;
 }
 
 // -------------------------------------------------------------- Morton
@@ -319,9 +473,16 @@ __global__ void mp_morton_kernel(const float* __restrict__ keys, const unsigned 
 
 // --------------------------------------------------------------- boxes
 // One warp per tile: [min, max] per pivot of the keys of its (sorted) rows.
+// Query keys are distances from q^ = fl32(h + r), not from h + r: by the triangle
+// inequality |d(p, q^) - d(p, h + r)| <= ||q^ - (h + r)||_p <= 2^-24 ||h + r||_p, a term that
+// does not scale with the key (embeddings with a common offset far larger than their
+// spread make keys small and ||h + r|| large).  So every query box is widened by
+// 2^-23 max_h ||q^||_p of its relation (qnmax; the factor 2 covers the FP32 norm and
+// the 2^-24 -> ||q^|| vs ||h + r|| conversion), rounded outward: the boxes then bound
+// the keys of the exact h + r, and every test built on them stays lossless.
 __global__ void mp_boxes_kernel(const float* __restrict__ keys, const unsigned int* __restrict__ perm, long long nseg,
                                 long long L, int ROWS, int ntile, int K, float* __restrict__ bmin,
-                                float* __restrict__ bmax) {
+                                float* __restrict__ bmax, const unsigned int* __restrict__ qnmax) {
     const int lane = threadIdx.x & 31;
     const long long nt = nseg * ntile;
     for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < nt;
@@ -344,6 +505,11 @@ __global__ void mp_boxes_kernel(const float* __restrict__ keys, const unsigned i
                 for (int o = 16; o > 0; o >>= 1) {
                     a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
                     z = fmaxf(z, __shfl_xor_sync(0xffffffffu, z, o));
+                }
+                if (qnmax) {
+                    const float m = __fmul_ru(__uint_as_float(qnmax[s]), 1.1920928955078125e-07f);  // 2^-23
+                    a = __fsub_rd(a, m);
+                    z = __fadd_ru(z, m);
                 }
                 if (lane == 0) { bmin[w * K + k] = a; bmax[w * K + k] = z; }
             }
@@ -817,10 +983,57 @@ void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, con
     kern<<<1, 1024, smem, s>>>(E, N, d, K, (int)S, p0, P);
 }
 
+static void launch_mp_qkeys(const float* E, const float* Rel, long long N, long long R, int d, int norm, int K,
+                            const float* P, float* keys, unsigned int* minmax, unsigned int* qnmax,
+                            unsigned int* nonfinite, cudaStream_t s) {
+    // relations per warp: up to 4 (32 per block), fewer when R is small so warps are not idle
+    const int NU = (int)std::min<long long>(4, std::max<long long>(1, (R + 7) / 8));
+    const int S = mk_stride(d), D4 = (d + 3) / 4 * 4;
+    const size_t smem = (size_t)(32 * S + K * D4 + 8 * NU * D4) * sizeof(float);
+    const long long gy = (R + 8 * NU - 1) / (8 * NU);
+    const long long chunks = (N + 31) / 32;
+    long long gx_target = (148LL * 6 + gy - 1) / gy;
+    if (gx_target < 1) gx_target = 1;
+    long long nch = (chunks + gx_target - 1) / gx_target;
+    nch = std::max<long long>(1, std::min<long long>(nch, 16));
+    dim3 grid((unsigned)((chunks + nch - 1) / nch), (unsigned)gy);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, 256, smem, s>>>(E, Rel, N, R, d, (int)nch, P, keys, minmax, qnmax, nonfinite);
+    };
+    auto byNU = [&](auto n_, auto k_) {
+        constexpr int NN = decltype(n_)::value, KK = decltype(k_)::value;
+        switch (NU) {
+            case 1: go(mp_qkeys_kernel<NN, KK, 1>); break;
+            case 2: go(mp_qkeys_kernel<NN, KK, 2>); break;
+            case 3: go(mp_qkeys_kernel<NN, KK, 3>); break;
+            default: go(mp_qkeys_kernel<NN, KK, 4>); break;
+        }
+    };
+    auto byK = [&](auto n_) {
+        switch (K) {
+            case 2: byNU(n_, std::integral_constant<int, 2>{}); break;
+            case 3: byNU(n_, std::integral_constant<int, 3>{}); break;
+            case 4: byNU(n_, std::integral_constant<int, 4>{}); break;
+            case 5: byNU(n_, std::integral_constant<int, 5>{}); break;
+            case 6: byNU(n_, std::integral_constant<int, 6>{}); break;
+            case 7: byNU(n_, std::integral_constant<int, 7>{}); break;
+            default: byNU(n_, std::integral_constant<int, 8>{}); break;
+        }
+    };
+    if (norm == 1) byK(std::integral_constant<int, 1>{});
+    else byK(std::integral_constant<int, 2>{});
+}
+
 void launch_mp_keys(const float* E, const float* Rel, long long N, long long nseg, int d, int norm, int K,
-                    const float* P, float* keys, unsigned int* minmax, unsigned int* nonfinite, cudaStream_t s) {
+                    const float* P, float* keys, unsigned int* minmax, unsigned int* qnmax, unsigned int* nonfinite,
+                    cudaStream_t s) {
     const bool query = Rel != nullptr;
-    mp_init_minmax_kernel<<<grid_for_mp(nseg * K, 256), 256, 0, s>>>(minmax, nseg * K);
+    mp_init_minmax_kernel<<<grid_for_mp(nseg * K, 256), 256, 0, s>>>(minmax, nseg * K, query ? qnmax : nullptr, nseg);
+    if (query) {
+        launch_mp_qkeys(E, Rel, N, nseg, d, norm, K, P, keys, minmax, qnmax, nonfinite, s);
+        return;
+    }
     const int S = mk_stride(d), D4 = (d + 3) / 4 * 4;
     const int ent = query ? 32 : 128;
     const size_t smem = (size_t)(ent * S + K * D4 + (query ? 16 * D4 : 0)) * sizeof(float);
@@ -834,7 +1047,7 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
     dim3 grid((unsigned)((chunks + nch - 1) / nch), (unsigned)gy);
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, query ? 256 : 128, smem, s>>>(E, Rel, N, nseg, d, (int)nch, P, keys, minmax, nonfinite);
+        kern<<<grid, query ? 256 : 128, smem, s>>>(E, Rel, N, nseg, d, (int)nch, P, keys, minmax, qnmax, nonfinite);
     };
     auto byK = [&](auto n_, auto q_) {
         constexpr int NN = decltype(n_)::value;
@@ -867,9 +1080,9 @@ void launch_mp_morton(const float* keys, const unsigned int* minmax, long long n
 }
 
 void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg, long long L, int ROWS, int ntile,
-                     int K, float* bmin, float* bmax, cudaStream_t s) {
+                     int K, float* bmin, float* bmax, const unsigned int* qnmax, cudaStream_t s) {
     mp_boxes_kernel<<<grid_for_mp(nseg * ntile * 32, 256), 256, 0, s>>>(keys, perm, nseg, L, ROWS, ntile, K, bmin,
-                                                                         bmax);
+                                                                         bmax, qnmax);
 }
 
 void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,

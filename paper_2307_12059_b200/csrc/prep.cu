@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(256) query_keys_kernel(const float* __restrict
     if (blockIdx.x == 0 && __syncthreads_or(bad)) {
         if (threadIdx.x == 0) atomicOr(nonfinite, 1u);
     }
+    bad = false;  // from here: the entity rows (a tail partition does not cover every head)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     float mn[QK_RPW], mx[QK_RPW];
 #pragma unroll
@@ -119,7 +120,9 @@ __global__ void __launch_bounds__(256) query_keys_kernel(const float* __restrict
         __syncthreads();  // previous chunk fully consumed (and Rs / Ps written)
         for (int x = threadIdx.x; x < QK_ENT * d; x += blockDim.x) {
             const int i = x / d, k = x % d;
-            Es[i * S + k] = (h0 + i < N) ? E[(h0 + i) * d + k] : 0.f;
+            const float v = (h0 + i < N) ? E[(h0 + i) * d + k] : 0.f;
+            bad |= !isfinite(v);
+            Es[i * S + k] = v;
         }
         __syncthreads();
         const long long h = h0 + lane;
@@ -148,6 +151,7 @@ __global__ void __launch_bounds__(256) query_keys_kernel(const float* __restrict
             }
         }
     }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
 #pragma unroll
     for (int u = 0; u < QK_RPW; ++u) {
         const long long r = r0 + w + 8 * u;

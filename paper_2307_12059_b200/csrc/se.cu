@@ -56,7 +56,9 @@ __global__ void __launch_bounds__(1024) se_connector_kernel(const float* __restr
     }
 }
 
-// max over rows of ||x_h||_1 (FP64 sums, rounded up), as float bits (values >= 0)
+// max over rows of ||x_h||_1 (FP64 sums, rounded up), as float bits (values >= 0); a
+// non-finite connector (NaN or inf in E, W_lhs or W_rhs) gives +inf, which the host
+// reports as KGC_EDATA
 __global__ void row_l1_max_kernel(const double* __restrict__ X, long long N, int d, unsigned int* out) {
     const int lane = threadIdx.x & 31;
     float m = 0.f;
@@ -65,7 +67,7 @@ __global__ void row_l1_max_kernel(const double* __restrict__ X, long long N, int
         double s = 0.0;
         for (int k = lane; k < d; k += 32) s += fabs(X[h * d + k]);
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        m = fmaxf(m, f2up(s));
+        m = isfinite(s) ? fmaxf(m, f2up(s)) : __int_as_float(0x7f800000);  // NaN / inf -> +inf: KGC_EDATA
     }
     if (lane == 0) atomicMax(out, __float_as_uint(m));
 }

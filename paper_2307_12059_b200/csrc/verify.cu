@@ -33,10 +33,11 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
                                                         const unsigned long long* __restrict__ cand_count,
                                                         long long cand_cap, const int* __restrict__ qperm,
                                                         const int* __restrict__ tperm, const float* __restrict__ E,
-                                                        const float* __restrict__ Rel, long long N, int QT, int bq,
+                                                        const float* __restrict__ Rel, const float* __restrict__ Et,
+                                                        long long N, int QT, int bq,
                                                         int d, double theta, KgcTripletDev* __restrict__ out,
                                                         unsigned long long* res_count, long long res_cap, int r_off,
-                                                        long long Nt, long long t_off) {
+                                                        long long Nt, long long t_off, long long h_off) {
     long long nc = (long long)*cand_count;
     if (nc > cand_cap) nc = cand_cap;
     constexpr int LPC = VERIFY_LPC;  // lanes per candidate
@@ -48,7 +49,7 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
         // ---- stage 1: this lane's candidate
         const long long idx = base + lane;
         bool valid = idx < nc;
-        int h = 0, r = 0, t = 0;
+        int h = 0, r = 0, t = 0;  // h: row of E, t: row of Et
         if (valid) {
             const int2 cv = cand[idx];
             const long long rr = cv.x / rows_per_rel;
@@ -56,8 +57,8 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
             valid = pos < N && cv.y < Nt;
             if (valid) {
                 r = (int)rr;
-                h = qperm ? qperm[rr * N + pos] : (int)pos;                        // null: natural order
-                t = (int)((tperm ? tperm[cv.y] : cv.y) + t_off);  // tail partition: rows [t_off, t_off + Nt) of E
+                h = qperm ? qperm[rr * N + pos] : (int)pos;  // null: natural order
+                t = tperm ? tperm[cv.y] : cv.y;
             }
         }
         // ---- stage 2: distances, LPC lanes per candidate
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
             const int tt = __shfl_sync(0xffffffffu, t, src);
             const float* eh = E + (long long)hh * d;
             const float* er = Rel + (long long)rq * d;
-            const float* et = E + (long long)tt * d;
+            const float* et = Et + (long long)tt * d;
             double acc = 0.0;
             if (VEC4) {
 #pragma unroll 2
@@ -101,9 +102,9 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
         const unsigned long long slot = warp_append(keep, res_count);
         if (keep && slot < (unsigned long long)res_cap) {
             KgcTripletDev o;
-            o.h = h;
-            o.r = r + r_off;  // relation index in the caller's Rel
-            o.t = t;
+            o.h = (int)(h + h_off);  // global ids: head block / tail partition offsets,
+            o.r = r + r_off;         // relation index in the caller's Rel
+            o.t = (int)(t + t_off);
             o.dist = (float)dist;
             out[slot] = o;
         }
@@ -111,14 +112,15 @@ __global__ void __launch_bounds__(256, 3) verify_kernel(const int2* __restrict__
 }
 
 void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap, const int* qperm,
-                   const int* tperm, const float* E, const float* Rel, long long N, int QT, int bq, int d, int norm,
-                   float theta, KgcTripletDev* out, unsigned long long* res_count, long long res_cap, int num_sms,
-                   cudaStream_t s, int r_off, long long Nt, long long t_off) {
-    const bool vec4 = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(E) | reinterpret_cast<uintptr_t>(Rel)) % 16 == 0);
+                   const int* tperm, const float* E, const float* Rel, const float* Et, long long N, int QT, int bq,
+                   int d, int norm, float theta, KgcTripletDev* out, unsigned long long* res_count, long long res_cap,
+                   int num_sms, cudaStream_t s, int r_off, long long Nt, long long t_off, long long h_off) {
+    const bool vec4 = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(E) | reinterpret_cast<uintptr_t>(Rel) |
+                                        reinterpret_cast<uintptr_t>(Et)) % 16 == 0);
     auto kern = norm == 1 ? (vec4 ? verify_kernel<1, true> : verify_kernel<1, false>)
                           : (vec4 ? verify_kernel<2, true> : verify_kernel<2, false>);
-    kern<<<num_sms * 8, 256, 0, s>>>(cand, cand_count, cand_cap, qperm, tperm, E, Rel, N, QT, bq, d, (double)theta, out,
-                                     res_count, res_cap, r_off, Nt < 0 ? N : Nt, t_off);
+    kern<<<num_sms * 8, 256, 0, s>>>(cand, cand_count, cand_cap, qperm, tperm, E, Rel, Et, N, QT, bq, d,
+                                     (double)theta, out, res_count, res_cap, r_off, Nt < 0 ? N : Nt, t_off, h_off);
 }
 
 }  // namespace kgc

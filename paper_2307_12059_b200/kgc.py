@@ -34,7 +34,7 @@ class kgc_options(ctypes.Structure):
                 ("prune", ctypes.c_int32), ("pivot", ctypes.c_int32), ("l2_engine", ctypes.c_int32),
                 ("chunk_tiles", ctypes.c_int32), ("pivots", ctypes.c_int32),
                 ("result_capacity", ctypes.c_int64), ("stream", ctypes.c_void_p), ("l1_engine", ctypes.c_int32),
-                ("split", ctypes.c_int32), ("tail_shard", ctypes.c_int32)]
+                ("split", ctypes.c_int32), ("tail_shard", ctypes.c_int32), ("relation_batch", ctypes.c_int32)]
 
 
 class kgc_stats_t(ctypes.Structure):
@@ -58,7 +58,7 @@ class kgc_stats_t(ctypes.Structure):
 
 EXPORTS = ["kgc_abi_version", "kgc_default_options", "kgc_create", "kgc_join", "kgc_results", "kgc_stats",
            "kgc_last_error", "kgc_set_stream", "kgc_destroy", "kgc_inspect", "kgc_shard_range", "kgc_topk",
-           "kgc_join_se"]
+           "kgc_join_se", "kgc_join_block"]
 
 _lib = None
 
@@ -98,6 +98,8 @@ def load_library(path: str | Path | None = None):
     L.kgc_topk.restype = i64
     L.kgc_join_se.argtypes = [vp, vp, vp, vp, i64, i64, i32, ctypes.c_float]
     L.kgc_join_se.restype = ctypes.c_int
+    L.kgc_join_block.argtypes = [vp, vp, i64, i64, vp, i64, i64, vp, i64, i32, i32, ctypes.c_float]
+    L.kgc_join_block.restype = ctypes.c_int
     if path is None:
         _lib = L
     return L
@@ -247,6 +249,17 @@ def kgc_join_se(ctx, E, Wl, Wr, N: int, R: int, d: int, eps: float) -> None:
         raise KgcError(rc, kgc_last_error(ctx))
 
 
+def kgc_join_block(ctx, Eh, Nh: int, h_off: int, Et, Nt: int, t_off: int, Rel, R: int, d: int, norm: int,
+                   eps: float) -> None:
+    """One head block x tail block of the partition-based join (see include/kgc.h)."""
+    for x, n in ((Eh, "Eh"), (Et, "Et"), (Rel, "Rel")):
+        _check_f32(x, n)
+    rc = load_library().kgc_join_block(ctx, _ptr(Eh), int(Nh), int(h_off), _ptr(Et), int(Nt), int(t_off), _ptr(Rel),
+                                       int(R), int(d), int(norm), float(eps))
+    if rc != KGC_OK:
+        raise KgcError(rc, kgc_last_error(ctx))
+
+
 # ----------------------------------------------------------- multi-GPU finish
 
 def gather_results(res, root: int = 0, group=None):
@@ -298,14 +311,24 @@ class Join:
     def __init__(self, **options):
         stream = options.pop("stream", None)
         self.ctx = kgc_create(**options)
+        self._own_order = stream is None
         if stream is not None:
             kgc_set_stream(self.ctx, stream)
+
+    def _follow_torch_stream(self, x):
+        """Without an explicit stream, a join on CUDA tensors runs on torch's current
+        stream of their device, so it is ordered after the kernels that produced them
+        (include/kgc.h, "Stream order")."""
+        if self._own_order and getattr(x, "is_cuda", False):
+            import torch
+            kgc_set_stream(self.ctx, torch.cuda.current_stream(x.device).cuda_stream)
 
     def run(self, E, Rel, norm: int, eps: float) -> int:
         N, d = (int(E.shape[0]), int(E.shape[1])) if E is not None and len(E.shape) == 2 else (0, 1)
         R = int(Rel.shape[0]) if Rel is not None else 0
         if Rel is not None and len(Rel.shape) == 2 and R and int(Rel.shape[1]) != d:
             raise ValueError("E and Rel dimensions differ")
+        self._follow_torch_stream(E)
         kgc_join(self.ctx, E, Rel, N, R, d, norm, eps)
         return kgc_results(self.ctx)
 
@@ -321,11 +344,13 @@ class Join:
 
     def run_se(self, E, Wl, Wr, eps: float) -> int:
         N, d = int(E.shape[0]), int(E.shape[1])
+        self._follow_torch_stream(E)
         kgc_join_se(self.ctx, E, Wl, Wr, N, int(Wl.shape[0]), d, eps)
         return kgc_results(self.ctx)
 
     def topk(self, E, Rel, norm: int, k: int, exclude_self: bool = False):
         N, d = int(E.shape[0]), int(E.shape[1])
+        self._follow_torch_stream(E)
         return kgc_topk(self.ctx, E, Rel, N, int(Rel.shape[0]), d, norm, k, exclude_self)
 
     def inspect(self, what: str) -> np.ndarray:

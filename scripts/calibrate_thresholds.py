@@ -31,8 +31,10 @@ def main(names):
     out_path = ROOT / "configs" / "thresholds.json"
     data = json.loads(out_path.read_text()) if out_path.exists() else {}
     data["_about"] = ("theta (distance threshold, float32-exact) per config / norm / target hit rate, calibrated by "
-                      "scripts/calibrate_thresholds.py from FP64 oracle distances of a seeded row sample, moved to "
-                      "the middle of a >= 4e-4*theta gap free of sampled distances and self-edge distances ||r_j||.")
+                      "scripts/calibrate_thresholds.py with oracle.calibrate_theta: the midpoint of the k-th and "
+                      "(k+1)-th smallest FP64 dist3 over a seeded row sample (k = hit rate x sample size), moved "
+                      "below any self-edge distance ||r_j||_p within 2e-4*theta (DESIGN.md reading R14), rounded to "
+                      "float32.")
     data["generator"] = GENERATOR_VERSION
     for name in names:
         c = CONFIGS[name]
