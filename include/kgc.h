@@ -84,6 +84,9 @@ typedef struct {
                               /* exceed 8 GiB); 5 = relation-factored tcgen05 TF32 (no pruning: one */
                               /* G = H T^T tile per (head tile, tail tile) serves all R relations   */
                               /* in the epilogue; for data where tiles do not prune)                */
+                              /* 6 = CTA pairs (as 3) on gathered tail blocks when pivots >= 2:    */
+                              /* per 256-row query tile the tails passing the per-tail K-pivot     */
+                              /* test, 256 per block, each CTA gathering its 128 rows with cp.async */
     int32_t chunk_tiles;      /* max tail tiles per work item (load-balance granularity); 0 = auto */
     int32_t pivots;           /* 0/1 = one pivot (default); 2..8 = multi-pivot tile     */
                               /* pruning (L_inf over K pivot distances; needs d <= 256, */
@@ -137,7 +140,8 @@ typedef struct {
     int32_t pivots_used;          /* 1, or K of the multi-pivot pruning                            */
     int32_t engine;               /* tile engine used: 1 tcgen05 TF32, 2 FP32 SIMT, 3 FP16x2 SIMT,   */
                                   /* 4 tcgen05 TF32 on CTA pairs, 5 FP32 SIMT on gathered tails,      */
-                                  /* 6 tcgen05 TF32 on gathered tail blocks, 7 relation-factored      */
+                                  /* 6 tcgen05 TF32 on gathered tail blocks, 7 relation-factored,     */
+                                  /* 8 tcgen05 TF32 on CTA pairs over gathered tail blocks            */
     float ms_split;               /* device time of the rank-local split estimate (world > 1)       */
     float ms_host;                /* host wall time of the whole kgc_join call                      */
     int64_t gathered_pairs;       /* engine 5: (query row, tail) pairs left after the per-tail K-pivot */

@@ -133,25 +133,27 @@ static bool use_tc(const kgc_ctx* ctx, int norm, int d) {
 // pair kernel is 8% slower).
 static bool use_tc2(const kgc_ctx* ctx, int norm, int d, long long N) {
     if (!use_tc(ctx, norm, d)) return false;
-    if (ctx->opt.l2_engine == 3) return true;
+    if (ctx->opt.l2_engine == 3 || ctx->opt.l2_engine == 6) return true;  // 6: gathered when K > 1
     if (ctx->opt.l2_engine != 0) return false;
-    const char* e = getenv("KGC_TC2");  // experiment knob: force the automatic choice
+    const char* e = kgc_knob("KGC_TC2");  // experiment knob: force the automatic choice
     if (e) return atoi(e) != 0;
     return (double)N * (double)(((d + 7) / 8) * 8) * 4.0 > 48.0 * 1048576.0;
 }
 // FP32 SIMT tile edge (experiment knob KGC_SIMT_T = 32 | 64)
 static int simt_t() {
-    const char* e = getenv("KGC_SIMT_T");
+    const char* e = kgc_knob("KGC_SIMT_T");
     return (e && atoi(e) == 32) ? 32 : SIMT_T;
 }
 // Gathered-tail SIMT engine (l1_engine 3; auto for L1 with multi-pivot pruning):
 // element-level tail pruning inside surviving tiles (pivots.cu, tiles_simt.cu).
 // Tensor-core engine on gathered tail blocks (l2_engine 4): the same per-tail test,
 // blocks of 256 gathered rows (tiles_tc.cu, GATHER); needs K pivots and the 1-CTA geometry.
+// l2_engine 6: the same on CTA pairs (256-row query tiles, each CTA gathers half of every
+// block with cp.async pieces; tiles_tc2.cu, GATHER).
 static bool use_gather_tc(const kgc_ctx* ctx) {
-    const char* e = getenv("KGC_GATHER_TC");  // experiment knob
+    const char* e = kgc_knob("KGC_GATHER_TC");  // experiment knob
     if (e) return atoi(e) != 0;
-    return ctx->opt.l2_engine == 4;
+    return ctx->opt.l2_engine == 4 || ctx->opt.l2_engine == 6;
 }
 // 2-D tensor map over the sorted row-major tails Ts[N + 1][Kpad] (fp32): box = 32 columns x 1
 // row, 128-byte swizzle -- the operand of the TMA row gathers (tiles_tc.cu, GATHER).
@@ -179,7 +181,7 @@ static int make_tails_tmap(CUtensorMap* m, const float* Ts, long long rows, int 
 // before the join falls back to contiguous tiles.
 constexpr size_t GATHER_TC_BUDGET = 8ull << 30;
 static bool use_gather(const kgc_ctx* ctx, int norm) {
-    const char* e = getenv("KGC_GATHER");  // experiment knob: 0 = off, 1 = on for both norms
+    const char* e = kgc_knob("KGC_GATHER");  // experiment knob: 0 = off, 1 = on for both norms
     if (e) return atoi(e) != 0;
     if (ctx->opt.l1_engine == 3) return true;
     return norm == 1 && ctx->opt.l1_engine == 0;
@@ -238,7 +240,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 5 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2 || o.tail_shard < 0 || o.tail_shard > 1 || o.relation_batch < 0) {
+        o.l2_engine > 6 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2 || o.tail_shard < 0 || o.tail_shard > 1 || o.relation_batch < 0) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -391,7 +393,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const bool half_req = norm == 1 && ctx->opt.l1_engine == 1;
     // query-tile rows: the engine's (the pair engine's choice follows the tail rows, so a tail
     // partition may use the 1-CTA engine where the whole tail set would not)
-    const int bq = gtc_req ? BM : (tc2 ? 2 * BM : (tc ? BM : (half_req ? BN_HALF : simt_t())));
+    const bool gtc_pair = gtc_req && ctx->opt.l2_engine == 6;       // gathered blocks on CTA pairs
+    const int bq = gtc_req ? (gtc_pair ? 2 * BM : BM) : (tc2 ? 2 * BM : (tc ? BM : (half_req ? BN_HALF : simt_t())));
     const int BN = tc ? BN_TC : (half_req ? BN_HALF : simt_t());
     const int QT = (int)((N + bq - 1) / bq);
     const int TT = (int)((NT + BN - 1) / BN);
@@ -399,7 +402,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     int chunk = ctx->opt.chunk_tiles > 0 ? ctx->opt.chunk_tiles : (tc ? 16 : 8);
     if (tc && ctx->opt.chunk_tiles == 0) {
         int as = 0, bs = 0, kc = 0;
-        const int sb = tc2 ? tc2_smem_bytes(Kpad, &as, &bs, &kc) : tc_smem_bytes(Kpad, &as, &bs, &kc);
+        const int sb = (tc2 || gtc_pair) ? tc2_smem_bytes(Kpad, &as, &bs, &kc) : tc_smem_bytes(Kpad, &as, &bs, &kc);
         if (sb > 0 && as == 1) chunk = 64;  // amortise A rebuilds
     }
     ctx->N = N;
@@ -671,7 +674,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                                 ctx->scan_tmp.p, s, &ctx->launches);
         LAUNCHED(0);
         CK(cudaMemcpyAsync(ctx->tperm.p, ctx->sv0.p, (size_t)NT * 4, cudaMemcpyDeviceToDevice, s));
-        const char* kde = getenv("KGC_KD");  // local kd refinement of both orders (experiment knob)
+        const char* kde = kgc_knob("KGC_KD");  // local kd refinement of both orders (experiment knob)
         const bool kd = kde ? atoi(kde) != 0 : false;
         if (kd) launch_kd_refine(P<float>(ctx->mpkt), P<int>(ctx->tperm), 1, NT, K, s);
         launch_mp_morton(P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q), R, N, K, bits,
@@ -736,10 +739,10 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     // Gathered tails: per query tile, the tails of its surviving tiles that pass the K-pivot
     // test on their own keys, in blocks of GT_ROWS; work items reference blocks.
     const bool gather = n_items > 0 && K > 1 && !tc && !half_req && simt_t() == GT_ROWS && use_gather(ctx, norm);
-    const bool gather_tc = n_items > 0 && gtc_req && K > 1 && tc_gather_ok(Kpad) &&
+    const bool gather_tc = n_items > 0 && gtc_req && K > 1 && (gtc_pair ? tc2_gather_ok(Kpad) : tc_gather_ok(Kpad)) &&
                            (size_t)list_span * BN_TC * 8 <= GATHER_TC_BUDGET;
     // rows per gathered block: tensor cores 256 (= tail tile rows); SIMT 64 or 32 (KGC_GT_TB experiment knob)
-    const char* gtb = getenv("KGC_GT_TB");
+    const char* gtb = kgc_knob("KGC_GT_TB");
     const int GB = gather_tc ? BN_TC : ((gtb && atoi(gtb) == 32) ? 32 : GT_ROWS);
     long long g_max_items = 0;
     if (gather || gather_tc) {
@@ -760,7 +763,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         }
         launch_stage_rows(Et, P<int>(ctx->tperm), P<float>(ctx->mpkt), NT, d, Kpad, K, P<float>(ctx->Ts),
                           P<float>(ctx->tks), gather_tc ? P<float4>(ctx->tsc) : nullptr, s);
-        if (gather_tc) {
+        if (gather_tc && !gtc_pair) {  // the 1-CTA engine gathers with TMA row gathers
             CK(ensure(ctx->tmapbuf, sizeof(CUtensorMap)));
             if (make_tails_tmap(&ctx->tmap_host, P<float>(ctx->Ts), NT + 1, Kpad)) {
                 set_err(ctx, "cuTensorMapEncodeTiled failed for the gathered tails");
@@ -815,7 +818,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         set_err(ctx, "l1_engine=1 (FP16x2) needs every |E|, |Rel| value <= 1000; use l1_engine 0 or 2");
         return KGC_EINVAL;
     }
-    st.engine = gather_tc ? 6 : (tc2 ? 4 : (tc ? 1 : (half ? 3 : (gather ? 5 : 2))));
+    st.engine = gather_tc ? (gtc_pair ? 8 : 6) : ((tc2 || gtc_pair) ? 4 : (tc ? 1 : (half ? 3 : (gather ? 5 : 2))));
     const float gam = 1.0f + 10.0f * 4.8828125e-04f + (float)(d / 8 + 4) * 1.1920928955078125e-07f;
     if (n_items > 0) {
         CK(ensure(ctx->Tp, (size_t)TT * BN * Kpad * 4));
@@ -838,7 +841,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                                  P<float>(ctx->Qp), P<float4>(ctx->qs), s, cyc ? ctx->opt.world : 0, ctx->opt.rank);
             LAUNCHED(1);
         } else {
-            launch_stage_tails(Et, P<int>(ctx->tperm), NT, d, Kpad, BN, TT, tc2 ? 2 : (tc ? 1 : 0), P<float>(ctx->Tp),
+            launch_stage_tails(Et, P<int>(ctx->tperm), NT, d, Kpad, BN, TT, (tc2 || gtc_pair) ? 2 : (tc ? 1 : 0), P<float>(ctx->Tp),
                                P<float>(ctx->T2), P<float2>(ctx->tstile), s);
             LAUNCHED(1);
             if (!tc) {  // the tensor-core engine forms its query tiles on the fly
@@ -874,12 +877,12 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.item_cum = P<long long>(ctx->item_cum);
         tp.total_tiles = h1.c.my_cost;
         {   // tuning knob for experiments: KGC_SCHED_TC / KGC_SCHED_SIMT = 0 (round-robin) | 1 (balanced blocks)
-            const char* e = getenv(tc ? "KGC_SCHED_TC" : "KGC_SCHED_SIMT");
+            const char* e = kgc_knob(tc ? "KGC_SCHED_TC" : "KGC_SCHED_SIMT");
             tp.sched = e ? atoi(e) : (tc ? 0 : 1);
         }
         {
-            const char* e = getenv("KGC_T2_PREFETCH");
-            tp.t2pf = e ? atoi(e) : (tc2 ? 1 : 0);  // measured: helps the pair kernel, not the 1-CTA one
+            const char* e = kgc_knob("KGC_T2_PREFETCH");
+            tp.t2pf = e ? atoi(e) : ((tc2 || gtc_pair) ? 1 : 0);  // measured: helps the pair kernel, not the 1-CTA one
         }
         tp.Kpad = Kpad;
         tp.bq = bq;
@@ -909,7 +912,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         tp.gb = GB;
         if (n_items > 0) {
             if (gather) {
-                const char* pe = getenv("KGC_GT_PROF");  // experiment: wait-cycle instrumentation
+                const char* pe = kgc_knob("KGC_GT_PROF");  // experiment: wait-cycle instrumentation
                 unsigned long long* prof = nullptr;
                 if (pe && atoi(pe)) {
                     CK(cudaMalloc(&prof, 16 * 8));
@@ -931,8 +934,9 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             else if (gather_tc) {
                 TileParams tg = tp;
                 tg.n_items = g_max_items;  // grid bound; the kernel reads the item count on the device
-                launch_tiles_tc_gather(tg, ctx->num_sms, s);
-            } else if (tc2) launch_tiles_tc2(tp, ctx->num_sms, s);
+                if (gtc_pair) launch_tiles_tc2_gather(tg, ctx->num_sms, s);
+                else launch_tiles_tc_gather(tg, ctx->num_sms, s);
+            } else if (tc2 || gtc_pair) launch_tiles_tc2(tp, ctx->num_sms, s);  // gtc_pair: list fallback
             else if (tc) launch_tiles_tc(tp, ctx->num_sms, s);
             else if (half) launch_tiles_half_l1(tp, ctx->num_sms, s);
             else launch_tiles_simt(tp, norm, ctx->num_sms, s);

@@ -2,9 +2,22 @@
 // translation units: tile geometry, kernel launchers, parameter blocks.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 namespace kgc {
+
+// Experiment knobs (environment variables such as KGC_KD, KGC_GT_TB, KGC_SCHED_TC) are read
+// only by a debug build (nvcc -DKGC_EXPERIMENTS): in the product build every choice is fixed by
+// kgc_options and the size rules, so the environment cannot change what or how a join computes.
+inline const char* kgc_knob(const char* name) {
+#ifdef KGC_EXPERIMENTS
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
 
 constexpr int BM = 128;          // query rows per tile (= TMEM lanes = UMMA M)
 constexpr int BN_TC = 256;       // tail rows per tile, tensor-core engine (UMMA N)
@@ -171,6 +184,8 @@ void launch_iota(int* out, long long n, cudaStream_t s);
 int  tc_gather_ok(int Kpad);  // the gathered tensor-core engine needs 32-wide K-chunks
 int  tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);
 void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s);
+int  tc2_gather_ok(int Kpad);  // the gathered CTA-pair engine needs 32-wide K-chunks
+void launch_tiles_tc2_gather(const TileParams& p, int num_sms, cudaStream_t s);  // p.n_items: a bound
 void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t s);
 void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long max_items, cudaStream_t s);
 void launch_tiles_half_l1(const TileParams& p, int num_sms, cudaStream_t s);

@@ -1074,7 +1074,7 @@ void launch_mp_morton(const float* keys, const unsigned int* minmax, long long n
                       unsigned long long* code, unsigned int* idx, cudaStream_t s) {
     // Hilbert order by default (c2: gathered L1 pairs 1.72% -> 1.69%, tile kernel -4%);
     // KGC_HILBERT=0 restores the Morton (Z) order
-    const char* e = getenv("KGC_HILBERT");
+    const char* e = kgc_knob("KGC_HILBERT");
     const int hilbert = e ? atoi(e) : 1;
     mp_morton_kernel<<<grid_for_mp(nseg * L, 256), 256, 0, s>>>(keys, minmax, nseg, L, K, bits, code, idx, hilbert);
 }

@@ -680,7 +680,7 @@ static void launch_gather_variant(const TileParams& p, int num_sms, long long ma
 
 void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long max_items, cudaStream_t s) {
     if (max_items <= 0) return;
-    const char* e = getenv("KGC_GT_VAR");  // experiment knob: chunk / stage / refill-protocol variants
+    const char* e = kgc_knob("KGC_GT_VAR");  // experiment knob: chunk / stage / refill-protocol variants
     const int v = e ? atoi(e) : 0;
     // measured on c2 L1 (tile-kernel ms, same session): KC 24 / 2 stages / alternating refill duty
     // 4.83; KC 32 4.93-5.07; KC 16 4.95; KC 24 with "last releaser refills" 4.93; KC 32 swizzled

@@ -24,6 +24,19 @@
 //            only on a barrier of the destination CTA).
 //   b_empty, a_empty, acc_full: tcgen05.commit multicast to both CTAs.
 //   acc_empty (even CTA: 16 arrivals) the 8 epilogue warps of each CTA.
+//
+// GATHER (l2_engine 6): the tail operand is not a contiguous tail tile but a block
+// of 256 gathered tails -- the tails of the query tile's surviving tiles whose own
+// K pivot keys pass the L_inf test against the query tile's key box (Lemma 1 per
+// tail, pivots.cu gather_tails_kernel<256>), at 3-4x fewer pairs than whole tiles.
+// The producer WARP of each CTA gathers its 128 rows of the block with 16-byte
+// cp.async pieces straight into the same no-swizzle K-major layout (8 lanes per
+// 128-byte row chunk: 4 rows per instruction, the block's row indices in
+// registers), keeps up to 3 chunks in flight, and signals a chunk after
+// cp.async.wait_group + fence.proxy.async (generic-proxy writes made visible to
+// tcgen05.mma).  The epilogue takes ||t||^2 / 2 per list entry and the block's
+// guard-band maxima from the list build, and emits the list entry (sorted tail
+// position) as the candidate column.
 #include <cstdio>
 #include <cstdlib>
 
@@ -57,7 +70,7 @@ int tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
     const int A = BM * Kpad * 4;
     // prefer two A stages when the B ring still buffers >= 64 K-values
     // (experiment knob KGC_TC2_MINK: the minimum ring depth in K-values for two A stages)
-    const char* e = getenv("KGC_TC2_MINK");
+    const char* e = kgc_knob("KGC_TC2_MINK");
     const int mink = e ? atoi(e) : 64;
     for (int as = 2; as >= 1; --as) {
         for (int KC : {32, 16, 8}) {
@@ -78,6 +91,7 @@ int tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
     return -1;
 }
 
+template <bool GATHER>
 __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p, int a_stages, int b_stages, int KC) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int Kpad = p.Kpad;
@@ -99,9 +113,12 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
     const uint32_t crank = cluster_ctarank();
     const bool leader = crank == 0;
     const long long cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-    const long long it_begin = p.sched ? balanced_begin(p.item_cum, p.n_items, p.total_tiles, cid, ncl) : cid;
-    const long long it_end = p.sched ? balanced_begin(p.item_cum, p.n_items, p.total_tiles, cid + 1, ncl) : p.n_items;
-    const long long it_step = p.sched ? 1 : ncl;
+    // gathered: the item count was produced on the device (round-robin items)
+    const long long n_items = GATHER ? *p.dn_items : p.n_items;
+    const bool sched = !GATHER && p.sched;
+    const long long it_begin = sched ? balanced_begin(p.item_cum, n_items, p.total_tiles, cid, ncl) : cid;
+    const long long it_end = sched ? balanced_begin(p.item_cum, n_items, p.total_tiles, cid + 1, ncl) : n_items;
+    const long long it_step = sched ? 1 : ncl;
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&a_full[i], leader ? 2 * BM : BM);
@@ -110,7 +127,9 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
             mbar_init(&acc_empty[i], 16);
         }
         for (int i = 0; i < b_stages; ++i) {
-            mbar_init(&b_full[i], leader ? 2 : 1);
+            // producer: one expect_tx arrival (bulk copy) or 32 lane arrivals (gathered); + the relay
+            const uint32_t prod = GATHER ? 32u : 1u;
+            mbar_init(&b_full[i], leader ? prod + 1 : prod);
             mbar_init(&b_empty[i], 1);
         }
         fence_mbar_init();
@@ -121,7 +140,61 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
+    if (warp == 0 && GATHER) {
+        // ------------------------------------------------ producer (gathered blocks): this CTA's 128 rows
+        int bi = 0, npend = 0;
+        uint32_t bph = 0;
+        const int lag = b_stages - 1 < 3 ? b_stages - 1 : 3;  // chunks in flight beyond the newest
+        const int p8 = lane & 7, rsub = lane >> 3;            // 16-byte piece of a 128-byte row chunk; row in a quad
+        auto signal_oldest = [&](int keep) {
+            cp_async_wait_n(keep);
+            fence_proxy_async_smem();  // generic-proxy smem writes -> visible to tcgen05.mma
+            int s0 = bi - npend;
+            if (s0 < 0) s0 += b_stages;
+            mbar_arrive(&b_full[s0]);
+            --npend;
+        };
+        for (long long it = it_begin; it < it_end; it += it_step) {
+            const int4 w = p.items[it];
+            for (int jj = w.y; jj <= w.z; ++jj) {
+                // the block's 128 row indices of this CTA: lane l loads rows 4l..4l+3, then lane
+                // l keeps the index of row 4u + rsub for every instruction u
+                const int4 rv = __ldg(reinterpret_cast<const int4*>(p.glist + ((long long)w.w + jj) * BN_TC +
+                                                                    crank * HALF) + lane);
+                int idx[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) {
+                    const int a = __shfl_sync(0xffffffffu, rv.x, u), b = __shfl_sync(0xffffffffu, rv.y, u);
+                    const int c2 = __shfl_sync(0xffffffffu, rv.z, u), d2 = __shfl_sync(0xffffffffu, rv.w, u);
+                    idx[u] = rsub == 0 ? a : (rsub == 1 ? b : (rsub == 2 ? c2 : d2));
+                }
+                for (int c = 0; c < nkc; ++c) {
+                    TC2_WAIT(0, &b_empty[bi], bph ^ 1);
+                    const int klen = Kpad - c * KC < KC ? Kpad - c * KC : KC;
+                    if (4 * p8 < klen) {
+                        const uint32_t sbase = smem_u32(Bs + (size_t)bi * HALF * KC);
+                        const float* src0 = p.Ts + (size_t)c * KC + 4 * p8;
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) {
+                            const int i = 4 * u + rsub;
+                            // UMMA K-major, no swizzle: 8-row x 16-byte core matrices, K-quad p8
+                            const uint32_t off = (uint32_t)(((p8 * (HALF / 8) + (i >> 3)) * 32 + (i & 7) * 4) * 4);
+                            cp_async16(sbase + off, src0 + (size_t)idx[u] * Kpad);
+                        }
+                    }
+                    cp_async_commit();
+                    ++npend;
+                    if (++bi == b_stages) { bi = 0; bph ^= 1; }
+                    if (npend > lag) signal_oldest(lag);
+                }
+            }
+        }
+        while (npend > 0) signal_oldest(0);
+        for (int k = 0; k < b_stages; ++k) {  // drain: the last commits have landed
+            mbar_wait(&b_empty[bi], bph ^ 1);
+            if (++bi == b_stages) { bi = 0; bph ^= 1; }
+        }
+    } else if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------ producer: this CTA's half of each tail tile
             int bi = 0;
@@ -222,8 +295,9 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
             const int rowid = w.x * (2 * BM) + (int)crank * BM + i;
             const float thf = p.theta * (1.0f + 2.44140625e-04f) + 2.384185791015625e-07f * Qn;
             for (int jj = w.y; jj <= w.z; ++jj) {
-                const int j = item_tile(w, jj, p.tile_list);
-                const float2 tv = p.tstile[j];
+                // gathered: j is the block (the tile list's offset + jj), else the tail tile
+                const int j = GATHER ? w.w + jj : item_tile(w, jj, p.tile_list);
+                const float2 tv = GATHER ? p.gtst[j] : p.tstile[j];
                 const float Tm = tv.x, Tdm = tv.y;
                 // guard band exactly as tiles_tc.cu
                 const float eb = Qd * Tm + Qn * Tdm + Qd * Tdm + p.eta * (Qn + Qd) * (Tm + Tdm);
@@ -232,10 +306,12 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
                 const float c = Q2 - R - (float)(p.Kpad + 4) * 1.1920928955078125e-07f * Q2 - 9.5367431640625e-07f * (Q2 + R);
                 // ||t||^2 of this tile's and the next tile's columns into L1 ahead of use
                 // (4 lines each); each chunk's loads would otherwise be an L2 round trip
-                const float* t2row = p.T2 + (size_t)j * BN_TC + col0;
+                const float* t2base = GATHER ? p.gT2 : p.T2;
+                const float* t2row = t2base + (size_t)j * BN_TC + col0;
                 if (p.t2pf && lane < 4) prefetch_l1(t2row + lane * 32);
                 else if (p.t2pf && lane < 8 && jj < w.z)
-                    prefetch_l1(p.T2 + (size_t)item_tile(w, jj + 1, p.tile_list) * BN_TC + col0 + (lane - 4) * 32);
+                    prefetch_l1(t2base + (size_t)(GATHER ? j + 1 : item_tile(w, jj + 1, p.tile_list)) * BN_TC + col0 +
+                                (lane - 4) * 32);
                 TC2_WAIT(5, &acc_full[acc], accph);
                 tc_fence_after();
                 const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_TC + col0);
@@ -250,7 +326,9 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
                         const int colb = j * BN_TC + col0 + ch * 32;
                         while (hit) {
                             const int u = __ffs(hit) - 1;
-                            if (slot < (unsigned long long)p.cand_cap) p.cand[slot] = make_int2(rowid, colb + u);
+                            // gathered: the list entry holds the sorted tail position
+                            const int col = GATHER ? __ldg(p.glist + (size_t)colb + u) : colb + u;
+                            if (slot < (unsigned long long)p.cand_cap) p.cand[slot] = make_int2(rowid, col);
                             ++slot;
                             hit &= hit - 1;
                         }
@@ -375,11 +453,13 @@ extern "C" __attribute__((visibility("default"))) void kgc_debug_tc2_prof(unsign
 namespace kgc {
 #endif
 
-void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s) {
+template <bool GATHER>
+static void launch_tc2(const TileParams& p, int num_sms, cudaStream_t s) {
     if (p.n_items <= 0) return;
     int as, bs, kc;
     const int smem = tc2_smem_bytes(p.Kpad, &as, &bs, &kc);
-    cudaFuncSetAttribute(tiles_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    auto kern = tiles_tc2_kernel<GATHER>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -393,13 +473,22 @@ void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s) {
     cfg.numAttrs = 1;
     cfg.gridDim = dim3(num_sms & ~1);
     int max_clusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, tiles_tc2_kernel, &cfg) != cudaSuccess || max_clusters <= 0) {
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters <= 0) {
         cudaGetLastError();
         max_clusters = num_sms / 2;
     }
-    long long g = p.n_items < max_clusters ? p.n_items : max_clusters;
+    long long g = p.n_items < max_clusters ? p.n_items : max_clusters;  // gathered: n_items is a bound
     cfg.gridDim = dim3((unsigned)(2 * g));
-    cudaLaunchKernelEx(&cfg, tiles_tc2_kernel, p, as, bs, kc);
+    cudaLaunchKernelEx(&cfg, kern, p, as, bs, kc);
 }
+
+void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s) { launch_tc2<false>(p, num_sms, s); }
+
+// gathered tail blocks need 32-wide K-chunks (8 pieces of 16 bytes per row chunk)
+int tc2_gather_ok(int Kpad) {
+    int as, bs, kc;
+    return tc2_smem_bytes(Kpad, &as, &bs, &kc) > 0 && kc == 32 && bs >= 2;
+}
+void launch_tiles_tc2_gather(const TileParams& p, int num_sms, cudaStream_t s) { launch_tc2<true>(p, num_sms, s); }
 
 }  // namespace kgc

@@ -7,8 +7,10 @@ the library raises.
 
 Same names as the C ABI: kgc_default_options, kgc_create, kgc_join,
 kgc_results, kgc_stats, kgc_last_error, kgc_set_stream, kgc_destroy,
-kgc_inspect, kgc_shard_range, kgc_topk, kgc_join_se, kgc_abi_version.  ``Join`` is a small
-convenience wrapper around one context.
+kgc_inspect, kgc_shard_range, kgc_topk, kgc_join_se, kgc_join_block,
+kgc_abi_version.  ``Join`` is a small convenience wrapper around one context;
+``gather_results`` and ``partition_join`` are the multi-GPU plumbing over a
+torch process group (bytes only: every step of the method runs in libkgc).
 """
 from __future__ import annotations
 
@@ -302,6 +304,70 @@ def gather_results(res, root: int = 0, group=None):
     return counts, allr.cpu().numpy().reshape(-1).view(TRIPLET_DTYPE)
 
 
+def partition_join(E_local, h_off: int, Rel, norm: int, eps: float, group=None, join=None, **options):
+    """Partition-based join over a process group (§4.7).
+
+    Rank k holds only entity block k: E_local = rows [h_off, h_off + n_k) of E (blocks may
+    differ in size).  The tail blocks travel around a ring of ranks: at step s rank k holds
+    block (k - s) mod W, joins its own heads against it with kgc_join_block (every tcgen05 /
+    SIMT step of the hot path runs in libkgc) while the block is forwarded to rank k + 1 and
+    the next one received from rank k - 1 (NCCL send/recv of device tensors, overlapped with
+    the join; gloo with host tensors), so after W steps every (head block, tail block) pair
+    has been joined exactly once and the union over ranks is R(eps).  Per-GPU resident
+    inputs: the own block plus two tail buffers -- 3 N d / W floats instead of N d.
+
+    Returns this rank's records (h, r, t global) as an (n, 4) int32 tensor on the join's
+    device (TRIPLET_DTYPE records; kgc.gather_results collects them).  `join`: an existing
+    kgc.Join to use (world 1), else one is created with **options.  Plumbing only: the ring
+    moves bytes, libkgc computes."""
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = E_local.device if hasattr(E_local, "device") else torch.device("cpu")
+    comm_dev = dev if nccl else torch.device("cpu")
+    Eh = E_local if hasattr(E_local, "data_ptr") else torch.from_numpy(np.ascontiguousarray(E_local))
+    n, d = int(Eh.shape[0]), int(Eh.shape[1])
+    R = int(Rel.shape[0])
+    meta = torch.tensor([n, int(h_off)], dtype=torch.int64, device=comm_dev)
+    allm = [torch.zeros_like(meta) for _ in range(world)]
+    dist.all_gather(allm, meta, group=group)
+    sizes = [int(m[0]) for m in allm]
+    offs = [int(m[1]) for m in allm]
+    cap = max(sizes) if sizes else 0
+    gr = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    bufs = [torch.empty((max(cap, 1), d), dtype=torch.float32, device=comm_dev) for _ in range(2)]
+    bufs[0][:n].copy_(Eh.to(comm_dev))
+    own = join is None
+    j = join if join is not None else Join(**options)
+    out = []
+    try:
+        cur = 0
+        for step in range(world):
+            src = (rank - step) % world  # owner of the tail block held now
+            works = []
+            if step + 1 < world:
+                ops = [dist.P2POp(dist.isend, bufs[cur], gr((rank + 1) % world), group),
+                       dist.P2POp(dist.irecv, bufs[1 - cur], gr((rank - 1) % world), group)]
+                works = dist.batch_isend_irecv(ops)
+            tails = bufs[cur][:sizes[src]]
+            if sizes[src] and n and R:
+                j._follow_torch_stream(tails)
+                kgc_join_block(j.ctx, Eh, n, int(h_off), tails, sizes[src], offs[src], Rel, R, d, norm, eps)
+                cnt = kgc_results(j.ctx)
+                part = torch.empty((cnt, 4), dtype=torch.int32, device=dev)
+                if cnt:
+                    kgc_results(j.ctx, part, cnt)
+                out.append(part)
+            for w in works:
+                w.wait()
+            cur = 1 - cur
+    finally:
+        if own:
+            j.close()
+    return torch.cat(out) if out else torch.empty((0, 4), dtype=torch.int32, device=dev)
+
+
 # ----------------------------------------------------------- convenience
 
 class Join:
@@ -346,6 +412,14 @@ class Join:
         N, d = int(E.shape[0]), int(E.shape[1])
         self._follow_torch_stream(E)
         kgc_join_se(self.ctx, E, Wl, Wr, N, int(Wl.shape[0]), d, eps)
+        return kgc_results(self.ctx)
+
+    def run_block(self, Eh, h_off: int, Et, t_off: int, Rel, norm: int, eps: float) -> int:
+        """kgc_join_block: heads Eh (global rows h_off..) against tails Et (global rows t_off..)."""
+        d = int(Eh.shape[1])
+        self._follow_torch_stream(Eh)
+        kgc_join_block(self.ctx, Eh, int(Eh.shape[0]), h_off, Et, int(Et.shape[0]), t_off, Rel, int(Rel.shape[0]), d,
+                       norm, eps)
         return kgc_results(self.ctx)
 
     def topk(self, E, Rel, norm: int, k: int, exclude_self: bool = False):

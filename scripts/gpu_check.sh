@@ -22,4 +22,11 @@ if [ "${NCU:-1}" == "1" ]; then
   echo "ncu_launches_rc=$?"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${NCU_KERNELS:-tiles_|verify}" -s ${NCU_SKIP:-3} -c ${NCU_COUNT:-3} -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu ${BENCH_ARGS} > gpurun_out/ncu_$TAG.log 2>&1
   echo "ncu_full_rc=$?"
+  # export the raw metrics page here (gpurun copies back at most 64 MiB); keep the report only if small
+  ncu -i gpurun_out/prof_$TAG.ncu-rep --page raw --csv > gpurun_out/prof_${TAG}_raw.csv 2>/dev/null
+  if [ -n "${SRC_KERNEL}" ]; then
+    ncu -i gpurun_out/prof_$TAG.ncu-rep --page source --csv --kernel-name regex:"${SRC_KERNEL}" --launch-count 1 > gpurun_out/prof_${TAG}_src.csv 2>/dev/null
+  fi
+  sz=$(stat -c %s gpurun_out/prof_$TAG.ncu-rep 2>/dev/null || echo 0)
+  if [ "$sz" -gt 25000000 ]; then rm -f gpurun_out/prof_$TAG.ncu-rep; fi
 fi

@@ -73,7 +73,11 @@ def launches(tag):
 
 def full(tag, workload):
     rep = OUT / f"prof_{tag}.ncu-rep"
-    raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw_csv = OUT / f"prof_{tag}_raw.csv"   # exported on the GPU box when the report is too large to copy
+    if raw_csv.exists():
+        raw = raw_csv.read_text()
+    else:
+        raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     col = {h: i for i, h in enumerate(hdr)}
@@ -128,6 +132,6 @@ if __name__ == "__main__":
     PROF.mkdir(exist_ok=True)
     if (OUT / f"launches_{tag}.csv").exists():
         launches(tag)
-    if (OUT / f"prof_{tag}.ncu-rep").exists():
+    if (OUT / f"prof_{tag}.ncu-rep").exists() or (OUT / f"prof_{tag}_raw.csv").exists():
         full(tag, workload)
     print("wrote", sorted(p.name for p in PROF.glob(f"{tag}*")))

@@ -113,3 +113,87 @@ def test_two_rank_shards_union_equals_full_join(norm):
     assert cost_all == total
     (b0, e0, _), (b1, e1, _) = gathered
     assert b0 == 0 and e0 == b1          # contiguous split of the query tiles
+
+
+# ------------------------------------------------ partition-based ring join (host logic)
+def _ring_worker(rank, world, port, E, Rel, norm, eps, bounds, q):
+    """kgc.partition_join over gloo with libkgc's block join replaced, in this test process
+    only, by an oracle block join: exercises the ring (block sizes / offsets exchange, send /
+    recv order, which block each step holds) without a GPU."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle
+        from paper_2307_12059_b200 import kgc
+        state = {}
+
+        class _Ctx:
+            def _follow_torch_stream(self, x):
+                pass
+
+            def close(self):
+                pass
+
+            ctx = None
+
+        def block(ctx, Eh, Nh, h_off, Et, Nt, t_off, Rel_, R, d, norm_, eps_):
+            Eh, Et = np.asarray(Eh), np.asarray(Et)
+            Ecat = np.vstack([Eh, Et])
+            rows = (np.arange(Nh)[:, None] * R + np.arange(R)[None, :]).ravel()
+            res = oracle.join(Ecat, np.asarray(Rel_), norm_, eps_, rows=rows)
+            res = res[res["t"] >= Nh]
+            out = np.zeros(res.size, kgc.TRIPLET_DTYPE)
+            out["h"], out["r"], out["t"] = res["h"] + h_off, res["r"], res["t"] - Nh + t_off
+            out["dist"] = res["dist"]
+            state["res"] = out
+            state.setdefault("blocks", []).append((h_off, t_off, Nt))
+
+        def results(ctx, out=None, capacity=None):
+            r = state["res"]
+            if out is not None:
+                out.numpy().reshape(-1).view(kgc.TRIPLET_DTYPE)[:r.size] = r
+            return r.size
+
+        kgc.kgc_join_block = block
+        kgc.kgc_results = results
+        a, b = bounds[rank]
+        mine = kgc.partition_join(torch.from_numpy(E[a:b].copy()), a, Rel, norm, eps, join=_Ctx())
+        recs = mine.numpy().reshape(-1).view(kgc.TRIPLET_DTYPE)
+        q.put((rank, [tuple(x) for x in zip(recs["h"].tolist(), recs["r"].tolist(), recs["t"].tolist())],
+               state.get("blocks", [])))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partition_ring_covers_every_block_pair_once(world):
+    from oracle import oracle
+    from synth import generate
+    E, Rel = generate(301, 3, 12, seed=51)
+    norm = 2
+    D = np.sort(oracle.dist_rows(E, Rel, norm).ravel())
+    eps = float(np.float32(0.5 * (D[900] + D[901])))
+    cuts = [0, 90, 200, 301][:world] + [301] if world == 3 else [0, 130, 301]
+    bounds = [(cuts[i], cuts[i + 1]) for i in range(world)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ring_worker, args=(r, world, port, E, Rel, norm, eps, bounds, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = oracle.join(E, Rel, norm, eps)
+    full_set = set(zip(full["h"].tolist(), full["r"].tolist(), full["t"].tolist()))
+    sets = {r: set(s) for r, s, _ in got}
+    assert sum(len(s) for s in sets.values()) == len(set().union(*sets.values()))   # disjoint
+    assert set().union(*sets.values()) == full_set
+    for r, _, blocks in got:
+        a, b = bounds[r]
+        assert all(h_off == a for h_off, _, _ in blocks)
+        assert sorted(t for _, t, _ in blocks) == sorted(x[0] for x in bounds)     # every tail block once
+        for res_h in sets[r]:
+            assert a <= res_h[0] < b

@@ -258,3 +258,81 @@ def test_tc_gather_full_size_sampled(cfg, hit, S):
     assert st["engine"] == 6
     rep = check_parity(E, Rel, 2, eps, res, rows=rows)
     assert rep["tight"] > 0
+
+
+# ------------------------------------------------- CTA-pair tensor-core engine on gathered blocks (l2_engine 6)
+TC2_GATHER = dict(pivots=8, l2_engine=6)
+
+
+@pytest.mark.parametrize("K", [2, 8])
+def test_tc2_gather_c1_full(K):
+    E, Rel = generate_config("c1")
+    eps = theta_for(E, Rel, 2, 1e-3)
+    res, st = gpu_join(E, Rel, 2, eps, pivots=K, l2_engine=6)
+    assert st["engine"] == 8 and st["pivots_used"] == K
+    assert st["query_tile_rows"] == 256 and st["tail_tile_rows"] == 256
+    rep = check_parity(E, Rel, 2, eps, res)
+    assert rep["tight"] > 1000
+    assert 0 < st["gathered_pairs"] <= st["tile_pairs_surviving"] * 256 * 256
+
+
+def test_tc2_gather_one_pivot_is_contiguous_pair_engine():
+    E, Rel = generate_config("c1")
+    eps = theta_for(E, Rel, 2, 1e-3)
+    res, st = gpu_join(E, Rel, 2, eps, pivots=1, l2_engine=6)
+    assert st["engine"] == 4
+    check_parity(E, Rel, 2, eps, res)
+
+
+@pytest.mark.parametrize("N,R,d", [(1, 1, 1), (7, 3, 5), (129, 2, 9), (257, 3, 33), (300, 5, 100), (1000, 4, 200),
+                                   (513, 2, 256), (700, 3, 50), (3000, 3, 8), (2049, 2, 104), (5000, 2, 36)])
+@pytest.mark.parametrize("dist", ["cluster", "uniform"])
+def test_tc2_gather_ragged(N, R, d, dist):
+    E, Rel = generate(N, R, d, seed=7 * N + d, dist=dist)
+    eps = theta_for(E, Rel, 2, 0.01 if N > 10 else 0.3)
+    res, st = gpu_join(E, Rel, 2, eps, **TC2_GATHER)
+    assert st["engine"] in (8, 4)
+    check_parity(E, Rel, 2, eps, res)
+
+
+def test_tc2_gather_equals_contiguous_pair_tiles():
+    E, Rel = generate(12000, 5, 64, seed=61)
+    eps = theta_for(E, Rel, 2, 1e-3)
+    a, sa = gpu_join(E, Rel, 2, eps, pivots=8, l2_engine=3)
+    b, sb = gpu_join(E, Rel, 2, eps, **TC2_GATHER)
+    assert sa["engine"] == 4 and sb["engine"] == 8
+    assert keyset(a) == keyset(b)
+    assert sa["tile_pairs_surviving"] == sb["tile_pairs_surviving"]
+    assert sb["gathered_pairs"] < sb["tile_pairs_surviving"] * 256 * 256
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_tc2_gather_sharding_invariance(world):
+    E, Rel = generate(5000, 7, 48, seed=64)
+    eps = theta_for(E, Rel, 2, 1e-3)
+    full, _ = gpu_join(E, Rel, 2, eps, **TC2_GATHER)
+    for split in (0, 1, 2):
+        parts = [gpu_join(E, Rel, 2, eps, rank=r, world=world, split=split, **TC2_GATHER)[0] for r in range(world)]
+        sets = [keyset(p) for p in parts]
+        assert sum(len(s) for s in sets) == len(set().union(*sets))
+        assert set().union(*sets) == keyset(full)
+
+
+def test_tc2_gather_host_inputs_and_capacity_rerun():
+    E, Rel = generate(6000, 4, 40, seed=65)
+    eps = theta_for(E, Rel, 2, 2e-3)
+    a, sa = gpu_join(E, Rel, 2, eps, device_inputs=False, result_capacity=16, **TC2_GATHER)
+    assert sa["reruns"] >= 1 and sa["engine"] == 8
+    check_parity(E, Rel, 2, eps, a)
+
+
+@pytest.mark.parametrize("cfg,hit,S", [("c2", 1e-4, 1200), ("c3", 1e-5, 800), ("c4", 1e-5, 300), ("c3", 1e-3, 300)])
+def test_tc2_gather_full_size_sampled(cfg, hit, S):
+    E, Rel = generate_config(cfg)
+    N, R = E.shape[0], Rel.shape[0]
+    rows = sample_rows(N, R, S, seed=11)
+    eps = theta_for(E, Rel, 2, hit, rows=rows)
+    res, st = gpu_join(E, Rel, 2, eps, **TC2_GATHER)
+    assert st["engine"] == 8
+    rep = check_parity(E, Rel, 2, eps, res, rows=rows)
+    assert rep["tight"] > 0
