@@ -36,10 +36,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     BUILD.mkdir(exist_ok=True)
     cc = nvcc()
+    # KGC_BUILD_EXPERIMENTS=1: a debug build whose kernels read the experiment knobs
+    # (kgc_internal.h, kgc_knob) -- for A/B measurements only, never the product build
+    flags = FLAGS + (["-DKGC_EXPERIMENTS"] if os.environ.get("KGC_BUILD_EXPERIMENTS") == "1" else [])
 
     def compile_one(src: str) -> Path:
         obj = BUILD / (Path(src).stem + ".o")
-        cmd = [cc, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [cc, *ARCH, *flags, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)

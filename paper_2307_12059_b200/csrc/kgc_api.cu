@@ -949,10 +949,17 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                                  P<int>(ctx->tperm), ex.A64, ex.B64, N, (long long)QT * bq, d, eps,
                                  reinterpret_cast<KgcTripletDev*>(ctx->res.p), &dctr->res, ctx->res_cap,
                                  ctx->num_sms, s, r_off);
-            else
+            else {
+                // E back into L2 for the row gathers (the tile kernel streamed the staged tails through it)
+                if ((size_t)N * d * 4 > (32u << 20)) {
+                    launch_l2_prefetch(E, (size_t)N * d * 4, ctx->num_sms, s);
+                    if (Et != E) launch_l2_prefetch(Et, (size_t)NT * d * 4, ctx->num_sms, s);
+                    LAUNCHED(Et != E ? 2 : 1);
+                }
                 launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, P<int>(ctx->qperm), P<int>(ctx->tperm),
                               E, Rel, Et, N, QT, bq, d, norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p),
                               &dctr->res, ctx->res_cap, ctx->num_sms, s, r_off, NT, ex.t_off, ex.h_off);
+            }
             LAUNCHED(1);
         }
         CK(cudaEventRecord(ctx->ev[EV_VERIFY], s));

@@ -208,6 +208,7 @@ void launch_count_res_le(const KgcTripletDev* res, long long n, float theta, int
                          unsigned long long* cnt, cudaStream_t s);
 void launch_compact_res_le(const KgcTripletDev* res, long long n, float theta, int exclude_self, KgcTripletDev* out,
                            unsigned long long* cnt, long long cap, cudaStream_t s);
+void launch_l2_prefetch(const void* p, size_t bytes, int num_sms, cudaStream_t s);
 // E: heads (row h of the query side), Et: tails (row t of the tail side, e.g. E + t_off d for a
 // tail partition); records carry h + h_off, r + r_off, t + t_off.
 void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap,

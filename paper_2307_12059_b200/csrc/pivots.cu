@@ -279,8 +279,8 @@ __global__ void __launch_bounds__(256) mp_qkeys_kernel(const float* __restrict__
     const int S = mk_stride(d);
     const int D4 = (d + 3) / 4 * 4;
     constexpr int RB = 8 * NU;                            // relations per block
-    float* Es = mq_smem;                                  // [32][S] entity rows
-    float* Ps = Es + 32 * S;                              // [K][D4] negated pivots
+    float* Eb = mq_smem;                                  // [2][32][S] entity rows, double-buffered
+    float* Ps = Eb + 2 * 32 * S;                          // [K][D4] negated pivots
     float* Rs = Ps + K * D4;                              // [RB][D4] relation rows
     const long long r0 = (long long)blockIdx.y * RB;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -298,17 +298,50 @@ __global__ void __launch_bounds__(256) mp_qkeys_kernel(const float* __restrict__
     const long long rw = r0 + (long long)w * NU;          // this warp's first relation
     const int nu = rw >= R ? 0 : (int)min((long long)NU, R - rw);
     float run_mn = FLT_MAX, run_mx = 0.f, run_qn = 0.f;  // lane u K + k: (relation rw + u, pivot k)
-    for (int ch = 0; ch < nch; ++ch) {
+    // entity rows of chunk `ch` into buffer b: 16-byte cp.async pieces (zero-filled past N) when
+    // rows are 16-byte aligned, else plain loads; the next chunk's copies overlap this chunk's math
+    const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(E) & 15) == 0;
+    const int q4 = D4 / 4;
+    auto stage = [&](int ch, int b) {
         const long long h0 = ((long long)blockIdx.x * nch + ch) * 32;
-        if (h0 >= N) break;
-        __syncthreads();
-        for (int x = threadIdx.x; x < 32 * S; x += blockDim.x) {
-            const int i = x / S, k = x % S;
-            const float v = (h0 + i < N && k < d) ? E[(h0 + i) * d + k] : 0.f;
-            bad |= !isfinite(v);
-            Es[x] = v;
+        float* Es = Eb + b * 32 * S;
+        if (vec) {
+            for (int x = threadIdx.x; x < 32 * q4; x += blockDim.x) {
+                const int i = x / q4, c = x % q4;
+                const bool ok = h0 + i < N;
+                const float* src = E + (ok ? (h0 + i) * d + 4 * c : 0);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(Es + i * S + 4 * c)),
+                             "l"(src), "r"(ok ? 16 : 0) : "memory");
+            }
+        } else {
+            for (int x = threadIdx.x; x < 32 * S; x += blockDim.x) {
+                const int i = x / S, k = x % S;
+                Es[x] = (h0 + i < N && k < d) ? E[(h0 + i) * d + k] : 0.f;
+            }
         }
-        __syncthreads();
+        cp_async_commit();
+    };
+    int nch_here = 0;  // chunks of this block that exist
+    while (nch_here < nch && ((long long)blockIdx.x * nch + nch_here) * 32 < N) ++nch_here;
+    if (nch_here > 0) stage(0, 0);
+    for (int ch = 0; ch < nch_here; ++ch) {
+        const long long h0 = ((long long)blockIdx.x * nch + ch) * 32;
+        const float* Es = Eb + (ch & 1) * 32 * S;
+        __syncthreads();  // every warp is done with the buffer the next chunk goes into
+        if (ch + 1 < nch_here) {
+            stage(ch + 1, (ch + 1) & 1);
+            cp_async_wait_n(1);
+        } else {
+            cp_async_wait_n(0);
+        }
+        __syncthreads();  // this chunk's rows have landed (every thread's copies)
+        if (vec)  // non-finite check of the pieces this thread copied
+            for (int x = threadIdx.x; x < 32 * q4; x += blockDim.x) {
+                const float4 v = *reinterpret_cast<const float4*>(Es + (x / q4) * S + 4 * (x % q4));
+                bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+            }
+        else
+            for (int x = threadIdx.x; x < 32 * S; x += blockDim.x) bad |= !isfinite(Es[x]);
         if (nu == 0) continue;
         const long long h = h0 + lane;
         const float* es = Es + lane * S;
@@ -761,13 +794,15 @@ __global__ void gather_tails_kernel(const float* __restrict__ qbmin, const float
 // a contiguous eighth of the list; pass 1 counts, a shared-memory prefix orders
 // the eighths, pass 2 writes (keys reloaded from L1/L2) -- the same ascending
 // output as gather_tails_kernel<64, false>.
+template <int BN>
 __global__ void __launch_bounds__(256) gather_tails_block_kernel(
     const float* __restrict__ qbmin, const float* __restrict__ qbmax, const float4* __restrict__ tks,
     const int* __restrict__ list, const long long* __restrict__ cum, const int2* __restrict__ ranges,
     DevCounters* ctr, long long N, int K, float theta, float relm, int chunk, long long* __restrict__ gblocks,
     int2* __restrict__ granges, int* __restrict__ nitem, int* __restrict__ glist, int cyc_world, int cyc_rank,
     int GB) {
-    constexpr int BN = 64, NW = 8, UN = 2;  // BN: tail-tile rows (list offsets); GB: rows per gathered block
+    // BN: tail-tile rows (list offsets; 64 SIMT, 256 tensor cores); GB: rows per gathered block
+    constexpr int NW = 8, H = BN / 32, UN = BN == 64 ? 2 : 1;
     __shared__ long long wcnt[NW + 1];
     const int tq0 = ctr->tq_begin, tq1 = ctr->tq_end;
     if (tq0 >= tq1) return;
@@ -789,13 +824,13 @@ __global__ void __launch_bounds__(256) gather_tails_block_kernel(
         for (int pass = 0; pass < 2; ++pass) {
             if (pass == 1) c = wcnt[w];
             for (int u0 = u_lo; u0 < u_hi; u0 += UN) {
-                float4 kv[UN][2][2];
+                float4 kv[UN][H][2];
                 long long ib[UN];
 #pragma unroll
                 for (int x = 0; x < UN; ++x) {
                     ib[x] = u0 + x < u_hi ? (long long)__ldg(L + u0 + x) * BN + lane : N;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                    for (int h = 0; h < H; ++h) {
                         const long long i = ib[x] + 32 * h;
                         kv[x][h][0] = i < N ? __ldg(tks + 2 * i) : make_float4(0, 0, 0, 0);
                         kv[x][h][1] = i < N ? __ldg(tks + 2 * i + 1) : make_float4(0, 0, 0, 0);
@@ -804,7 +839,7 @@ __global__ void __launch_bounds__(256) gather_tails_block_kernel(
 #pragma unroll
                 for (int x = 0; x < UN; ++x) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                    for (int h = 0; h < H; ++h) {
                         const long long i = ib[x] + 32 * h;
                         const float4 a = kv[x][h][0], b = kv[x][h][1];
                         const float tk[MP_MAX] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
@@ -986,10 +1021,17 @@ void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, con
 static void launch_mp_qkeys(const float* E, const float* Rel, long long N, long long R, int d, int norm, int K,
                             const float* P, float* keys, unsigned int* minmax, unsigned int* qnmax,
                             unsigned int* nonfinite, cudaStream_t s) {
-    // relations per warp: up to 4 (32 per block), fewer when R is small so warps are not idle
-    const int NU = (int)std::min<long long>(4, std::max<long long>(1, (R + 7) / 8));
+    // relations per warp NU (8 NU per block): per 4-dim step a warp issues ~K + 1 + NU shared loads
+    // and NU (2K + 2) packed FP32 ops, and ceil(R / 8 NU) blocks cover the relations -- pick the NU
+    // with the least issue per entity chunk (c4, R = 37: 3; c2, R = 18: 3; c5, R = 100: 4)
+    int NU = 1;
+    double best = 1e300;
+    for (int nu = 1; nu <= 4 && nu * K <= 32; ++nu) {
+        const double c = (double)((R + 8 * nu - 1) / (8 * nu)) * (K + 1 + nu + nu * (2.0 * K + 2));
+        if (c < best - 1e-9) { best = c; NU = nu; }
+    }
     const int S = mk_stride(d), D4 = (d + 3) / 4 * 4;
-    const size_t smem = (size_t)(32 * S + K * D4 + 8 * NU * D4) * sizeof(float);
+    const size_t smem = (size_t)(2 * 32 * S + K * D4 + 8 * NU * D4) * sizeof(float);
     const long long gy = (R + 8 * NU - 1) / (8 * NU);
     const long long chunks = (N + 31) / 32;
     long long gx_target = (148LL * 6 + gy - 1) / gy;
@@ -1103,6 +1145,41 @@ void launch_stage_rows(const float* E, const int* tperm, const float* keys, long
     stage_rows_kernel<<<grid_for_mp((N + 1) * 32, 256), 256, 0, s>>>(E, tperm, keys, N, d, Kpad, K, Ts, tks, tsc);
 }
 
+// Tensor-core gathered blocks: per list entry ||t||^2 / 2 (3e38 for the sentinel padding)
+// and per block of BN entries the maxima of ||t|| and ||t - tf32(t)|| (the guard band's Tm,
+// Tdm) -- from the written lists, one warp per block (8 entries per lane).
+template <int BN>
+__global__ void gather_scalars_kernel(const long long* __restrict__ cum, const long long* __restrict__ gblocks,
+                                      const DevCounters* ctr, const int* __restrict__ glist,
+                                      const float4* __restrict__ tsc, long long N, float* __restrict__ gT2,
+                                      float2* __restrict__ gtst) {
+    const int tq0 = ctr->tq_begin, tq1 = ctr->tq_end;
+    if (tq0 >= tq1) return;
+    const long long base = cum[tq0];
+    const int lane = threadIdx.x & 31;
+    const long long nwarp = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long q = tq0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); q < tq1; q += nwarp) {
+        const long long loff = cum[q] - base, nb = gblocks[q];
+        for (long long b = 0; b < nb; ++b) {
+            const long long e0 = (loff + b) * BN;
+            float mn = 0.f, md = 0.f;
+#pragma unroll
+            for (int u = 0; u < BN / 32; ++u) {
+                const long long e = e0 + u * 32 + lane;
+                const int i = __ldg(glist + e);
+                float4 sc = make_float4(3e38f, 0.f, 0.f, 0.f);
+                if (i < N) sc = __ldg(tsc + i);
+                gT2[e] = sc.x;
+                mn = fmaxf(mn, sc.y);
+                md = fmaxf(md, sc.z);
+            }
+            mn = gt_warp_max(mn);
+            md = gt_warp_max(md);
+            if (lane == 0) gtst[loff + b] = make_float2(mn, md);
+        }
+    }
+}
+
 void launch_gather_tails(const float* qbmin, const float* qbmax, const float* tks, const int* list,
                          const long long* cum, const int2* ranges, DevCounters* ctr, long long N, int BN, int K,
                          float theta, float relm, int chunk, long long nq, long long* gblocks, int2* granges,
@@ -1110,14 +1187,20 @@ void launch_gather_tails(const float* qbmin, const float* qbmax, const float* tk
                          int cyc_rank, cudaStream_t s, int gb) {
     const unsigned g = grid_for_mp(nq * 32, 256);
     const float4* tk4 = reinterpret_cast<const float4*>(tks);
-    if (BN == 64)
-        gather_tails_block_kernel<<<grid_for_mp(nq, 1, 148LL * 16), 256, 0, s>>>(
+    (void)g;
+    if (BN == 64) {
+        gather_tails_block_kernel<64><<<grid_for_mp(nq, 1, 148LL * 16), 256, 0, s>>>(
             qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm, chunk, gblocks, granges, nitem, glist,
             cyc_world, cyc_rank, gb);
-    else
-        gather_tails_kernel<256, true><<<g, 256, 0, s>>>(qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm,
-                                                         chunk, gblocks, granges, nitem, glist, tsc, gT2, gtst,
-                                                         cyc_world, cyc_rank);
+    } else {
+        // tensor cores: the same block-per-query-tile list build (a warp per query tile left long serial
+        // chains on heavy-tailed tile lists: c4 3.2 ms), then the per-entry / per-block scalars
+        gather_tails_block_kernel<256><<<grid_for_mp(nq, 1, 148LL * 16), 256, 0, s>>>(
+            qbmin, qbmax, tk4, list, cum, ranges, ctr, N, K, theta, relm, chunk, gblocks, granges, nitem, glist,
+            cyc_world, cyc_rank, 256);
+        gather_scalars_kernel<256><<<grid_for_mp(nq * 32, 256), 256, 0, s>>>(cum, gblocks, ctr, glist, tsc, N, gT2,
+                                                                              gtst);
+    }
 }
 
 }  // namespace kgc

@@ -30,9 +30,9 @@
 // K pivot keys pass the L_inf test against the query tile's key box (Lemma 1 per
 // tail, pivots.cu gather_tails_kernel<256>), at 3-4x fewer pairs than whole tiles.
 // The producer WARP of each CTA gathers its 128 rows of the block with 16-byte
-// cp.async pieces straight into the same no-swizzle K-major layout (8 lanes per
-// 128-byte row chunk: 4 rows per instruction, the block's row indices in
-// registers), keeps up to 3 chunks in flight, and signals a chunk after
+// cp.async pieces straight into a 128-byte-swizzled K-major operand (8 lanes per
+// 128-byte row chunk: 4 rows = 512 contiguous bytes per instruction, the block's
+// row indices in registers), keeps up to 3 chunks in flight, and signals a chunk after
 // cp.async.wait_group + fence.proxy.async (generic-proxy writes made visible to
 // tcgen05.mma).  The epilogue takes ||t||^2 / 2 per list entry and the block's
 // guard-band maxima from the list build, and emits the list entry (sorted tail
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
         // ------------------------------------------------ producer (gathered blocks): this CTA's 128 rows
         int bi = 0, npend = 0;
         uint32_t bph = 0;
-        const int lag = b_stages - 1 < 3 ? b_stages - 1 : 3;  // chunks in flight beyond the newest
+        const int lag = b_stages - 1 < 3 ? b_stages - 1 : 3;  // chunks in flight (measured: 5 slower than 3)
         const int p8 = lane & 7, rsub = lane >> 3;            // 16-byte piece of a 128-byte row chunk; row in a quad
         auto signal_oldest = [&](int keep) {
             cp_async_wait_n(keep);
@@ -177,8 +177,11 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
 #pragma unroll
                         for (int u = 0; u < 32; ++u) {
                             const int i = 4 * u + rsub;
-                            // UMMA K-major, no swizzle: 8-row x 16-byte core matrices, K-quad p8
-                            const uint32_t off = (uint32_t)(((p8 * (HALF / 8) + (i >> 3)) * 32 + (i & 7) * 4) * 4);
+                            // K-major, 128-byte swizzle: row i's 128-byte K-chunk at i * 128, its 16-byte
+                            // piece p at (p ^ (i % 8)) * 16 -- the 4 rows of one instruction fill 512
+                            // contiguous bytes (no bank conflicts; the no-swizzle layout put the 8 pieces of
+                            // a row 2 KB apart: 8-way conflicts)
+                            const uint32_t off = (uint32_t)(i * 128 + ((p8 ^ (i & 7)) << 4));
                             cp_async16(sbase + off, src0 + (size_t)idx[u] * Kpad);
                         }
                     }
@@ -235,7 +238,10 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
                     for (int c = 0; c < nkc; ++c) {
                         TC2_WAIT(3, &b_full[bi], bph);
                         tc_fence_after();
-                        const uint64_t b_desc0 = umma_desc_kmajor(smem_u32(Bs + (size_t)bi * HALF * KC), LBO_B2, SBO2);
+                        const uint64_t b_desc0 = GATHER ? umma_desc_sw128(smem_u32(Bs + (size_t)bi * HALF * KC))
+                                                        : umma_desc_kmajor(smem_u32(Bs + (size_t)bi * HALF * KC), LBO_B2, SBO2);
+                        // descriptor units (16 B) per K = 8 step: 32 bytes in the swizzled rows, 2 core matrices otherwise
+                        const uint32_t bstep = GATHER ? 2u : 2u * (LBO_B2 >> 4);
                         const int nsteps = (Kpad - c * KC < KC ? Kpad - c * KC : KC) / 8;
                         const uint64_t a_desc = a_desc0 + (uint64_t)((uint32_t)(c * KC / 4) * (LBO_A2 >> 4));
                         if (elect_one()) {
@@ -243,7 +249,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
                             for (int s = 0; s < 4; ++s) {
                                 if (s < nsteps)
                                     mma_tf32_pair(d_tmem, a_desc + (uint64_t)(2 * s * (LBO_A2 >> 4)),
-                                                  b_desc0 + (uint64_t)(2 * s * (LBO_B2 >> 4)), IDESC2, (c | s) != 0);
+                                                  b_desc0 + (uint64_t)(s * bstep), IDESC2, (c | s) != 0);
                             }
                             mma_commit_pair(&b_empty[bi], 3);
                         }
