@@ -41,6 +41,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tc_build.cuh"
 
 namespace kgc {
 
@@ -363,61 +364,18 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
         }
     }
     if (warp >= TC2_BUILDER_WARP0) {
-        // ---------------------------------------------------- builders: this CTA's 128 query rows
-        const int i = (warp - TC2_BUILDER_WARP0) * 32 + lane;
+        // ---------------------------------------------------- builders (tc_build.cuh)
+        const int wb = warp - TC2_BUILDER_WARP0;
         const bool vec4 = (p.d % 4 == 0) && ((reinterpret_cast<uintptr_t>(p.E) | reinterpret_cast<uintptr_t>(p.Rel)) % 16 == 0);
+        const int i = wb * 32 + lane;  // the row whose next-item entity row this lane prefetches
         int ai = 0;
         uint32_t aph = 0;
         for (long long it = it_begin; it < it_end; it += it_step) {
             const int4 w = p.items[it];
             const int r = w.x / p.QT;
-            const long long pos = (long long)(w.x - r * p.QT) * (2 * BM) + crank * BM + i;
-            const bool valid = pos < p.N;
-            const long long h = valid ? p.qperm[(long long)r * p.N + pos] : 0;
-            const float* e = p.E + h * p.d;
-            const float* rr = p.Rel + (long long)r * p.d;
             TC2_WAIT(6, &a_empty[ai], aph ^ 1);
-            float* A = As + (size_t)ai * A_FLOATS;
-            float s2 = 0.f, sd2 = 0.f;
-            const int nq = Kpad >> 2;
-            for (int kq0 = 0; kq0 < nq; kq0 += 8) {
-                float4 v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int kq = kq0 + u, k = kq * 4;
-                    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (valid && kq < nq) {
-                        if (vec4 && k < p.d) {
-                            const float4 a = __ldg(reinterpret_cast<const float4*>(e + k));
-                            const float4 b = __ldg(reinterpret_cast<const float4*>(rr + k));
-                            v[u] = make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
-                                               __fadd_rn(a.w, b.w));
-                        } else {
-                            float* vv = reinterpret_cast<float*>(&v[u]);
-#pragma unroll
-                            for (int c = 0; c < 4; ++c)
-                                if (k + c < p.d) vv[c] = __fadd_rn(__ldg(e + k + c), __ldg(rr + k + c));
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int kq = kq0 + u;
-                    if (kq < nq) {
-                        const float* vv = reinterpret_cast<const float*>(&v[u]);
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const float rd = vv[c] - __uint_as_float(__float_as_uint(vv[c]) & 0xFFFFE000u);  // exact
-                            s2 = fmaf(vv[c], vv[c], s2);
-                            sd2 = fmaf(rd, rd, sd2);
-                        }
-                        *reinterpret_cast<float4*>(A + ((size_t)kq * (BM / 8) + (i >> 3)) * 32 + (i & 7) * 4) = v[u];
-                    }
-                }
-            }
-            const float gam = 1.0f + (float)(Kpad + 4) * 1.1920928955078125e-07f;
-            qrow[ai * BM + i] = valid ? make_float4(s2, __fsqrt_ru(__fmul_ru(s2, gam)), __fsqrt_ru(__fmul_ru(sd2, gam)), 0.f)
-                                      : make_float4(3e38f, 0.f, 0.f, 0.f);
+            build_query_rows(As + (size_t)ai * A_FLOATS, qrow + ai * BM, p.E, p.Rel, p.qperm, p.N, p.d, Kpad, r,
+                             (long long)(w.x - r * p.QT) * (2 * BM) + crank * BM, wb, lane, vec4);
             fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the pair's tcgen05.mma
             mbar_arrive(&a_full[ai]);
             if (!leader) mbar_arrive_cluster(&a_full[ai], 0);

@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/b.log 2>&1 || { tail gpurun_out/b.log; exit 1; }
+timeout 300 python scripts/engine_ab.py c4 2 1e-5 'pivots=8' 2>&1 | tail -1 | cut -c1-300
+timeout 300 python scripts/engine_ab.py c3 2 1e-5 'pivots=1' 2>&1 | tail -1 | cut -c1-300
+timeout 300 python scripts/engine_ab.py c2 2 1e-4 'pivots=8' 2>&1 | tail -1 | cut -c1-300
+bash scripts/micro/build_prof.sh > gpurun_out/prof_build.log 2>&1; ENGINE=3 PIVOTS=8 bash scripts/micro/run_tc_prof.sh c4 1e-05 2>&1 | tail -9
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_gather.py tests/test_gpu_factored.py tests/test_gpu_stress.py -q -p no:cacheprovider -x > gpurun_out/par_r02r.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/par_r02r.log
