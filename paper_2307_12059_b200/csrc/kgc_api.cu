@@ -884,6 +884,10 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             const char* e = kgc_knob("KGC_T2_PREFETCH");
             tp.t2pf = e ? atoi(e) : ((tc2 || gtc_pair) ? 1 : 0);  // measured: helps the pair kernel, not the 1-CTA one
         }
+        {
+            const char* e = kgc_knob("KGC_L2HINT");
+            tp.l2hint = e ? atoi(e) : 1;
+        }
         tp.Kpad = Kpad;
         tp.bq = bq;
         tp.bn = BN;

@@ -59,6 +59,7 @@ struct TileParams {
     const long long* item_cum;  // exclusive prefix of item tile counts (cost-balanced CTA ranges)
     long long total_tiles;
     int t2pf;                   // tensor-core epilogues: prefetch ||t||^2 lines into L1 (experiment knob)
+    int l2hint;                 // pair engine: L2 evict-last on the staged tails, evict-first on entity rows
     int sched;                  // 0 = round-robin items, 1 = contiguous cost-balanced blocks
     int Kpad;
     int bq, bn;             // query / tail tile rows of the plan

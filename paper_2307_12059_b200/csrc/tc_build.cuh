@@ -21,7 +21,7 @@ namespace kgc {
 __device__ __forceinline__ void build_query_rows(float* __restrict__ A, float4* __restrict__ qrow,
                                                  const float* __restrict__ E, const float* __restrict__ Rel,
                                                  const int* __restrict__ qperm, long long N, int d, int Kpad, int r,
-                                                 long long pos0, int wb, int lane, bool vec4) {
+                                                 long long pos0, int wb, int lane, bool vec4, int l2hint = 0) {
     const int i = 32 * wb + lane;
     const long long pos = pos0 + i;
     const bool valid = pos < N;
@@ -42,10 +42,17 @@ __device__ __forceinline__ void build_query_rows(float* __restrict__ A, float4* 
     };
     if (vec4) {
         const int dq = d >> 2;
+        // l2hint: the entity rows are read once per item -- evict them first, so the staged
+        // tail tiles (re-read for every query tile) keep the L2
+        const uint64_t pol = l2hint ? l2_policy_evict_first() : 0;
         for (int kq = 0; kq < nq; ++kq) {
             float* dst = Ai + (size_t)kq * (BM / 8) * 32;
-            if (valid && kq < dq) cp_async16(smem_u32(dst), e + 4 * kq);
-            else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid && kq < dq) {
+                if (l2hint) cp_async16_hint(smem_u32(dst), e + 4 * kq, pol);
+                else cp_async16(smem_u32(dst), e + 4 * kq);
+            } else {
+                *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
         cp_async_commit();
         cp_async_wait_n(0);

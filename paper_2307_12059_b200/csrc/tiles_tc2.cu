@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
             // ------------------------------------------------ producer: this CTA's half of each tail tile
             int bi = 0;
             uint32_t bph = 0;
+            const uint64_t pol_keep = l2_policy_evict_last();
             for (long long it = it_begin; it < it_end; it += it_step) {
                 const int4 w = p.items[it];
                 for (int j = w.y; j <= w.z; ++j) {
@@ -212,7 +213,11 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
                         const uint32_t bytes = (uint32_t)klen * HALF * 4;
                         TC2_WAIT(0, &b_empty[bi], bph ^ 1);
                         mbar_arrive_expect_tx(&b_full[bi], bytes);
-                        bulk_g2s(Bs + (size_t)bi * HALF * KC, tsrc + (size_t)c * KC * HALF, bytes, &b_full[bi]);
+                        if (p.l2hint)  // the staged tails are re-read for every query tile: keep them in L2
+                            bulk_g2s_hint(Bs + (size_t)bi * HALF * KC, tsrc + (size_t)c * KC * HALF, bytes, &b_full[bi],
+                                          pol_keep);
+                        else
+                            bulk_g2s(Bs + (size_t)bi * HALF * KC, tsrc + (size_t)c * KC * HALF, bytes, &b_full[bi]);
                         if (++bi == b_stages) { bi = 0; bph ^= 1; }
                     }
                 }
@@ -375,7 +380,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
             const int r = w.x / p.QT;
             TC2_WAIT(6, &a_empty[ai], aph ^ 1);
             build_query_rows(As + (size_t)ai * A_FLOATS, qrow + ai * BM, p.E, p.Rel, p.qperm, p.N, p.d, Kpad, r,
-                             (long long)(w.x - r * p.QT) * (2 * BM) + crank * BM, wb, lane, vec4);
+                             (long long)(w.x - r * p.QT) * (2 * BM) + crank * BM, wb, lane, vec4, p.l2hint);
             fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the pair's tcgen05.mma
             mbar_arrive(&a_full[ai]);
             if (!leader) mbar_arrive_cluster(&a_full[ai], 0);
