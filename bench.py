@@ -293,9 +293,9 @@ def kernel_table(stats_steps, norms, d, peaks, peak_src, config, N, R):
         flops = 2.0 * d * pairs
         alu = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         if n == 2:
-            tc = st["tail_tile_rows"] == 256
+            tc = st["engine"] in (1, 4, 6, 7, 8)  # tensor-core engines (kgc.h kgc_stats_t.engine)
             peak = peaks["bf16_tflops"] * (1.1 / 2.25) if tc else 2 * alu
-            kname = ("tiles_tc2_kernel (L2, tcgen05.mma.cta_group::2 kind::tf32)" if st["engine"] == 4 else
+            kname = ("tiles_tc2_kernel (L2, tcgen05.mma.cta_group::2 kind::tf32)" if st["engine"] in (4, 8) else
                      "tiles_tc_kernel (L2, tcgen05 kind::tf32)") if tc else "tiles_simt_kernel<2>"
             ent = {"kernel": kname, "bound": "tensor" if tc else "alu", "ms": t_tiles * 1e3,
                    "achieved": flops / t_tiles / 1e12 if t_tiles > 0 else 0.0, "peak": peak, "unit": "TFLOP/s",

@@ -21,6 +21,7 @@ inline const char* kgc_knob(const char* name) {
 
 constexpr int BM = 128;          // query rows per tile (= TMEM lanes = UMMA M)
 constexpr int BN_TC = 256;       // tail rows per tile, tensor-core engine (UMMA N)
+constexpr int BN_PAIR = 128;     // tail rows per tile, CTA-pair engine on contiguous tiles (UMMA N = 128)
 constexpr int BN_HALF = 128;     // tile rows (query and tail), FP16x2 L1 engine
 constexpr int EST_SAMPLES = 256;  // sampled queries per relation, rank-local split estimate
 constexpr int SIMT_T = 64;       // tile rows (query and tail), FP32 SIMT engines
@@ -183,7 +184,7 @@ void launch_factored_tables(const float* E, const float* Rel, const int* tperm, 
                             cudaStream_t s);
 void launch_iota(int* out, long long n, cudaStream_t s);
 int  tc_gather_ok(int Kpad);  // the gathered tensor-core engine needs 32-wide K-chunks
-int  tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc);
+int  tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc, int bnt = BN_TC);
 void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s);
 int  tc2_gather_ok(int Kpad);  // the gathered CTA-pair engine needs 32-wide K-chunks
 void launch_tiles_tc2_gather(const TileParams& p, int num_sms, cudaStream_t s);  // p.n_items: a bound

@@ -60,13 +60,14 @@ __device__ unsigned long long g_tc2_prof[16];
 
 constexpr int TC2_THREADS = 448;  // same roles as tiles_tc.cu
 constexpr int TC2_BUILDER_WARP0 = 10;
-constexpr int HALF = BN_TC / 2;                 // tail rows per CTA
 constexpr uint32_t LBO_A2 = (BM / 8) * 128;     // 128 query rows per CTA
-constexpr uint32_t LBO_B2 = (HALF / 8) * 128;   // 128 tail rows per CTA
 constexpr uint32_t SBO2 = 128;
-constexpr uint32_t IDESC2 = idesc_tf32(2 * BM, BN_TC);  // M = 256, N = 256
+// tail tiles of BNT rows (256, or 128: finer tail tiles prune better, same B bytes per MAC);
+// each CTA streams HALFT = BNT / 2 of them
 
-int tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
+int tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc, int bnt) {
+    (void)bnt;  // 128-row tiles are streamed whole by one CTA: the same 128 rows per CTA and stage
+    const int HALF = 128;
     const int budget = 227 * 1024 - 512 - 2 * BM * 16;
     const int A = BM * Kpad * 4;
     // prefer two A stages when the B ring still buffers >= 64 K-values
@@ -92,8 +93,18 @@ int tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
     return -1;
 }
 
-template <bool GATHER>
+template <bool GATHER, int BNT>
 __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p, int a_stages, int b_stages, int KC) {
+    static_assert(!GATHER || BNT == BN_TC, "gathered blocks are 256 tails");
+    // BNT = tail-tile rows.  256: each CTA streams one half of every tile.  128 (PAIRED): the
+    // surviving tiles of an item are taken two at a time, CTA c streaming the whole of the
+    // (2m + c)-th -- one M = 256, N = 256 MMA covers two 128-row tiles (an N = 128 MMA ran at
+    // half the rate: c4 380 vs 700 TF/s), while the tile test prunes at 128-row granularity
+    constexpr bool PAIRED = BNT == 128;
+    constexpr int HALF = 128;                              // tail rows per CTA and MMA
+    constexpr int TSTEP = PAIRED ? 2 : 1;                  // list entries per MMA tile
+    constexpr uint32_t LBO_B2 = (HALF / 8) * 128;
+    constexpr uint32_t IDESC2 = idesc_tf32(2 * BM, 2 * HALF);  // M = 256, N = 256
     extern __shared__ __align__(1024) uint8_t smem[];
     const int Kpad = p.Kpad;
     const uint32_t A_FLOATS = BM * Kpad;
@@ -160,7 +171,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
             for (int jj = w.y; jj <= w.z; ++jj) {
                 // the block's 128 row indices of this CTA: lane l loads rows 4l..4l+3, then lane
                 // l keeps the index of row 4u + rsub for every instruction u
-                const int4 rv = __ldg(reinterpret_cast<const int4*>(p.glist + ((long long)w.w + jj) * BN_TC +
+                const int4 rv = __ldg(reinterpret_cast<const int4*>(p.glist + ((long long)w.w + jj) * BNT +
                                                                     crank * HALF) + lane);
                 int idx[32];
 #pragma unroll
@@ -206,12 +217,21 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
             const uint64_t pol_keep = l2_policy_evict_last();
             for (long long it = it_begin; it < it_end; it += it_step) {
                 const int4 w = p.items[it];
-                for (int j = w.y; j <= w.z; ++j) {
-                    const float* tsrc = p.Tp + ((size_t)item_tile(w, j, p.tile_list) * BN_TC + crank * HALF) * Kpad;
+                for (int j = w.y; j <= w.z; j += TSTEP) {
+                    // PAIRED: this CTA's tile is list entry j + crank (none past the item's end: the
+                    // MMA half it feeds is ignored by the epilogue)
+                    const bool have = !PAIRED || j + (int)crank <= w.z;
+                    const float* tsrc = PAIRED ? p.Tp + (size_t)(have ? item_tile(w, j + crank, p.tile_list) : 0) * HALF * Kpad
+                                               : p.Tp + ((size_t)item_tile(w, j, p.tile_list) * BNT + crank * HALF) * Kpad;
                     for (int c = 0; c < nkc; ++c) {
                         const int klen = Kpad - c * KC < KC ? Kpad - c * KC : KC;
                         const uint32_t bytes = (uint32_t)klen * HALF * 4;
                         TC2_WAIT(0, &b_empty[bi], bph ^ 1);
+                        if (!have) {
+                            mbar_arrive(&b_full[bi]);  // the stage's arrival, no bytes
+                            if (++bi == b_stages) { bi = 0; bph ^= 1; }
+                            continue;
+                        }
                         mbar_arrive_expect_tx(&b_full[bi], bytes);
                         if (p.l2hint)  // the staged tails are re-read for every query tile: keep them in L2
                             bulk_g2s_hint(Bs + (size_t)bi * HALF * KC, tsrc + (size_t)c * KC * HALF, bytes, &b_full[bi],
@@ -237,10 +257,10 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
                 TC2_WAIT(1, &a_full[ai], aph);
                 tc_fence_after();
                 const uint64_t a_desc0 = umma_desc_kmajor(smem_u32(As + (size_t)ai * A_FLOATS), LBO_A2, SBO2);
-                for (int j = w.y; j <= w.z; ++j) {
+                for (int j = w.y; j <= w.z; j += TSTEP) {
                     TC2_WAIT(2, &acc_empty[acc], accph ^ 1);
                     tc_fence_after();
-                    const uint32_t d_tmem = tmem + (uint32_t)(acc * BN_TC);
+                    const uint32_t d_tmem = tmem + (uint32_t)(acc * 2 * HALF);
                     for (int c = 0; c < nkc; ++c) {
                         TC2_WAIT(3, &b_full[bi], bph);
                         tc_fence_after();
@@ -280,7 +300,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
             uint32_t bph = 0;
             for (long long it = it_begin; it < it_end; it += it_step) {
                 const int4 w = p.items[it];
-                for (int j = w.y; j <= w.z; ++j) {
+                for (int j = w.y; j <= w.z; j += TSTEP) {
                     for (int c = 0; c < nkc; ++c) {
                         TC2_WAIT(7, &b_full[bi], bph);
                         mbar_arrive_cluster(&b_full[bi], 0);
@@ -292,7 +312,8 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
     } else if (warp < TC2_BUILDER_WARP0) {
         // ---------------------------------------------------- epilogue (both CTAs, own 128 rows)
         const int q = warp & 3;
-        const int col0 = ((warp - 2) >> 2) * (BN_TC / 2);
+        const int hcol = (warp - 2) >> 2;       // column half of the 256-column accumulator
+        const int col0 = hcol * HALF;           // its first TMEM column
         const int i = q * 32 + lane;
         int acc = 0, ai = 0;
         uint32_t accph = 0, aph = 0;
@@ -306,9 +327,13 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
             const float Q2 = qv.x, Qn = qv.y, Qd = qv.z;
             const int rowid = w.x * (2 * BM) + (int)crank * BM + i;
             const float thf = p.theta * (1.0f + 2.44140625e-04f) + 2.384185791015625e-07f * Qn;
-            for (int jj = w.y; jj <= w.z; ++jj) {
+            for (int jj = w.y; jj <= w.z; jj += TSTEP) {
+                // PAIRED: this warp's column half is list entry jj + hcol (absent past the item's end)
+                const bool have = !PAIRED || jj + hcol <= w.z;
                 // gathered: j is the block (the tile list's offset + jj), else the tail tile
-                const int j = GATHER ? w.w + jj : item_tile(w, jj, p.tile_list);
+                const int j = GATHER ? w.w + jj : item_tile(w, PAIRED ? (have ? jj + hcol : jj) : jj, p.tile_list);
+                // column offset of this warp's columns inside tile j
+                const int tcol = PAIRED ? 0 : col0;
                 const float2 tv = GATHER ? p.gtst[j] : p.tstile[j];
                 const float Tm = tv.x, Tdm = tv.y;
                 // guard band exactly as tiles_tc.cu
@@ -319,23 +344,24 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
                 // ||t||^2 of this tile's and the next tile's columns into L1 ahead of use
                 // (4 lines each); each chunk's loads would otherwise be an L2 round trip
                 const float* t2base = GATHER ? p.gT2 : p.T2;
-                const float* t2row = t2base + (size_t)j * BN_TC + col0;
+                const float* t2row = t2base + (size_t)j * BNT + tcol;
                 if (p.t2pf && lane < 4) prefetch_l1(t2row + lane * 32);
-                else if (p.t2pf && lane < 8 && jj < w.z)
-                    prefetch_l1(t2base + (size_t)(GATHER ? j + 1 : item_tile(w, jj + 1, p.tile_list)) * BN_TC + col0 +
-                                (lane - 4) * 32);
+                else if (p.t2pf && lane < 8 && jj + TSTEP + (PAIRED ? hcol : 0) <= w.z)
+                    prefetch_l1(t2base + (size_t)(GATHER ? j + 1 : item_tile(w, jj + TSTEP + (PAIRED ? hcol : 0), p.tile_list)) * BNT +
+                                tcol + (lane - 4) * 32);
                 TC2_WAIT(5, &acc_full[acc], accph);
                 tc_fence_after();
-                const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_TC + col0);
+                const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 2 * HALF + col0);
                 uint32_t ra[32], rb[32];
                 const float ch2 = 0.5f * c;  // T2 holds ||t||^2 / 2 (stage kernel)
                 auto process = [&](const uint32_t (&r)[32], int ch) {
+                    if (!have) return;
                     const float4* t2 = reinterpret_cast<const float4*>(t2row + ch * 32);
                     const float m = epi_max32(r, t2);
                     if (__any_sync(0xffffffffu, m >= ch2)) {
                         uint32_t hit = epi_hits32(r, t2, ch2);
                         unsigned long long slot = warp_reserve(__popc(hit), p.cand_count);
-                        const int colb = j * BN_TC + col0 + ch * 32;
+                        const int colb = j * BNT + tcol + ch * 32;
                         while (hit) {
                             const int u = __ffs(hit) - 1;
                             // gathered: the list entry holds the sorted tail position
@@ -346,6 +372,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
                         }
                     }
                 };
+                // software-pipelined TMEM loads: chunk ch + 1 is in flight while ch is tested
                 tmem_ld32_nowait(tbase + 0, ra);
                 tmem_wait_ld();
                 tmem_ld32_nowait(tbase + 32, rb);
@@ -422,12 +449,12 @@ extern "C" __attribute__((visibility("default"))) void kgc_debug_tc2_prof(unsign
 namespace kgc {
 #endif
 
-template <bool GATHER>
+template <bool GATHER, int BNT>
 static void launch_tc2(const TileParams& p, int num_sms, cudaStream_t s) {
     if (p.n_items <= 0) return;
     int as, bs, kc;
-    const int smem = tc2_smem_bytes(p.Kpad, &as, &bs, &kc);
-    auto kern = tiles_tc2_kernel<GATHER>;
+    const int smem = tc2_smem_bytes(p.Kpad, &as, &bs, &kc, BNT);
+    auto kern = tiles_tc2_kernel<GATHER, BNT>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -451,13 +478,16 @@ static void launch_tc2(const TileParams& p, int num_sms, cudaStream_t s) {
     cudaLaunchKernelEx(&cfg, kern, p, as, bs, kc);
 }
 
-void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s) { launch_tc2<false>(p, num_sms, s); }
+void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s) {
+    if (p.bn == 128) launch_tc2<false, 128>(p, num_sms, s);
+    else launch_tc2<false, BN_TC>(p, num_sms, s);
+}
 
 // gathered tail blocks need 32-wide K-chunks (8 pieces of 16 bytes per row chunk)
 int tc2_gather_ok(int Kpad) {
     int as, bs, kc;
-    return tc2_smem_bytes(Kpad, &as, &bs, &kc) > 0 && kc == 32 && bs >= 2;
+    return tc2_smem_bytes(Kpad, &as, &bs, &kc, BN_TC) > 0 && kc == 32 && bs >= 2;
 }
-void launch_tiles_tc2_gather(const TileParams& p, int num_sms, cudaStream_t s) { launch_tc2<true>(p, num_sms, s); }
+void launch_tiles_tc2_gather(const TileParams& p, int num_sms, cudaStream_t s) { launch_tc2<true, BN_TC>(p, num_sms, s); }
 
 }  // namespace kgc

@@ -302,7 +302,7 @@ def test_tc2_gather_equals_contiguous_pair_tiles():
     b, sb = gpu_join(E, Rel, 2, eps, **TC2_GATHER)
     assert sa["engine"] == 4 and sb["engine"] == 8
     assert keyset(a) == keyset(b)
-    assert sa["tile_pairs_surviving"] == sb["tile_pairs_surviving"]
+    assert sa["tail_tile_rows"] == 128 and sb["tail_tile_rows"] == 256  # contiguous pair tiles are 128 tails
     assert sb["gathered_pairs"] < sb["tile_pairs_surviving"] * 256 * 256
 
 

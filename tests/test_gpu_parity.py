@@ -388,11 +388,12 @@ def test_l1_half_engine_tiny_values_and_planted_zeros():
 
 
 # ------------------------------------------------- tcgen05 on CTA pairs (l2_engine 3)
-def test_tc2_engine_reported_and_tiles_256():
+def test_tc2_engine_reported_and_tiles_256x128():
+    """CTA-pair engine: 256-row query tiles (128 per CTA) x 128-row tail tiles (UMMA M = 256, N = 128)."""
     E, Rel = generate(1000, 3, 64, seed=5)
     eps = theta_for(E, Rel, 2, 1e-2)
     res, st = gpu_join(E, Rel, 2, eps, l2_engine=3)
-    assert st["engine"] == 4 and st["query_tile_rows"] == 256 and st["tail_tile_rows"] == 256
+    assert st["engine"] == 4 and st["query_tile_rows"] == 256 and st["tail_tile_rows"] == 128
     check_parity(E, Rel, 2, eps, res)
 
 
