@@ -397,6 +397,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     const int bq = gtc_req ? (gtc_pair ? 2 * BM : BM) : (tc2 ? 2 * BM : (tc ? BM : (half_req ? BN_HALF : simt_t())));
     // tail tile rows: the contiguous pair engine uses 128-row tail tiles (UMMA N = 128; finer tail
     // tiles prune better at the same B bytes per MAC: c4 5.70% -> 4.76% of pairs, c3 9.18 -> 6.30%)
+    // (the same pairing in the 1-CTA engine needs 16 bulk copies of 2 KB per chunk to interleave two
+    // 128-row tiles into one N = 256 operand and measured 1.55x slower on c3: it keeps 256-row tiles)
     const int BN = tc ? ((tc2 && !gtc_req) ? BN_PAIR : BN_TC) : (half_req ? BN_HALF : simt_t());
     const int QT = (int)((N + bq - 1) / bq);
     const int TT = (int)((NT + BN - 1) / BN);
