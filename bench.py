@@ -126,10 +126,10 @@ def ncu_traffic(kernel: str, workload: str):
         w = d.get(workload, {})
         if kernel in w:
             return w[kernel].get("dram_bytes_per_launch")
-        # template arguments beyond the first (tile shapes) may differ between captures: newest matching tag
-        base = kernel.rstrip(">").split(",")[0]
-        hits = [v for k, v in w.items() if k.split(",")[0].rstrip(">") == base]
-        return max(hits, key=lambda v: v.get("tag", ""))["dram_bytes_per_launch"] if hits else None
+        # template arguments (tile shapes) differ between captures: the newest capture of the same kernel
+        base = kernel.split("<")[0]
+        hits = [v for k, v in w.items() if k.split("<")[0] == base]
+        return hits[-1]["dram_bytes_per_launch"] if hits else None  # the last capture written
     except (ValueError, AttributeError, KeyError):
         return None
 
