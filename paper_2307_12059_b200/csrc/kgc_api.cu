@@ -47,7 +47,7 @@ enum Phase { EV_START, EV_H2D, EV_KEYS, EV_SORT, EV_RANGES, EV_STAGE, EV_TILES, 
     X(est_hist) X(est_cost) X(mpP) X(mpkt) X(mpkq) X(mpmm_t) X(mpmm_q) X(mpc0) X(mpc1) X(tbmin) X(tbmax) X(qbmin) \
     X(qbmax) X(tile_list) X(tk_sample) X(tk_sel) X(tk_cnt) X(Ts) X(tks) X(gblk) X(granges) X(glist) X(tsc) X(gT2) \
     X(gtst) X(tmapbuf) X(fz) X(frt) X(frn) X(fzero) X(se_w) X(se_a64) X(se_b64) X(se_af) X(se_bf) X(se_zero) \
-    X(acc) X(Eb) X(se_max) X(mpqn)
+    X(acc) X(Eb) X(mpbits) X(se_max) X(mpqn)
 
 struct kgc_ctx {
     kgc_options opt{};
@@ -74,6 +74,7 @@ struct kgc_ctx {
     CUtensorMap tmap_host;      // tensor map over the sorted tails (gathered tensor-core engine)
     std::vector<int4> fitems;   // relation-factored engine: work items built on the host
     bool have_join = false;
+    unsigned int* mp_bits = nullptr;  // this join's K-pivot survival masks (or nullptr)
 };
 
 static std::string g_create_err;
@@ -697,8 +698,16 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         launch_mp_boxes(P<float>(ctx->mpkq), P<unsigned>(ctx->qperm), R, N, bq, QT, K, P<float>(ctx->qbmin),
                         P<float>(ctx->qbmax), P<unsigned>(ctx->mpqn), s);
         LAUNCHED(2);
+        // survival masks kept for mp_emit when they fit (c4: 2.2 MB; c5: 380 MB -> recompute)
+        const size_t bits_bytes = (size_t)nq * ((TT + 31) / 32) * 4;
+        unsigned int* sbits = nullptr;
+        if (bits_bytes <= (64u << 20)) {
+            CK(ensure(ctx->mpbits, bits_bytes + 4));
+            sbits = P<unsigned int>(ctx->mpbits);
+        }
+        ctx->mp_bits = sbits;
         launch_mp_count(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tbmin), P<float>(ctx->tbmax), nq, TT,
-                        K, feps, mp_relm(d), 1, P<int2>(ctx->ranges), P<long long>(ctx->cost), s);
+                        K, feps, mp_relm(d), 1, P<int2>(ctx->ranges), P<long long>(ctx->cost), sbits, s);
         LAUNCHED(1);
     }
     scan_exclusive_i64(P<long long>(ctx->cost), P<long long>(ctx->cum), (size_t)nq, &dctr->total_cost,
@@ -737,7 +746,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         ctx->list_len = list_span;
         CK(ensure(ctx->tile_list, (size_t)list_span * 4 + 4));
         launch_mp_emit(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tbmin), P<float>(ctx->tbmax),
-                       P<long long>(ctx->cum), dctr, nq, TT, K, feps, mp_relm(d), 1, P<int>(ctx->tile_list), s);
+                       P<long long>(ctx->cum), dctr, nq, TT, K, feps, mp_relm(d), 1, P<int>(ctx->tile_list), ctx->mp_bits,
+                       s);
         LAUNCHED(1);
     }
     // Gathered tails: per query tile, the tails of its surviving tiles that pass the K-pivot

@@ -152,11 +152,14 @@ void launch_mp_morton(const float* keys, const unsigned int* minmax, long long n
 void launch_kd_refine(const float* keys, int* perm, long long nseg, long long L, int K, cudaStream_t s);
 void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg, long long L, int ROWS, int ntile,
                      int K, float* bmin, float* bmax, const unsigned int* qnmax, cudaStream_t s);
+// bits (optional, nq x ceil(TT / 32) words): mp_count stores each query tile's survival masks
+// there and mp_emit expands them instead of repeating the box tests
 void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,
-                     int TT, int K, float theta, float relm, int prune, int2* ranges, long long* cost, cudaStream_t s);
+                     int TT, int K, float theta, float relm, int prune, int2* ranges, long long* cost, unsigned int* bits,
+                     cudaStream_t s);
 void launch_mp_emit(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax,
                     const long long* cum, const DevCounters* ctr, long long nq, int TT, int K, float theta, float relm,
-                    int prune, int* list, cudaStream_t s);
+                    int prune, int* list, const unsigned int* bits, cudaStream_t s);
 
 // ---- gathered-tail SIMT engine (pivots.cu): element-level tail pruning against query-tile boxes
 constexpr int GT_ROWS = 64;  // tails per gathered block (= SIMT_T)

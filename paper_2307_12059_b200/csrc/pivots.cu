@@ -570,7 +570,8 @@ __device__ __forceinline__ bool mp_survives(const float* qmn, const float* qmx, 
 // One warp per query tile, lanes over tail tiles.
 __global__ void mp_count_kernel(const float* __restrict__ qbmin, const float* __restrict__ qbmax,
                                 const float* __restrict__ tbmin, const float* __restrict__ tbmax, long long nq, int TT,
-                                int K, float theta, float relm, int prune, int2* ranges, long long* cost) {
+                                int K, float theta, float relm, int prune, int2* ranges, long long* cost,
+                                unsigned int* __restrict__ bits) {
     const int lane = threadIdx.x & 31;
     for (long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; q < nq;
          q += ((long long)gridDim.x * blockDim.x) >> 5) {
@@ -583,7 +584,9 @@ __global__ void mp_count_kernel(const float* __restrict__ qbmin, const float* __
             for (int j0 = 0; j0 < TT; j0 += 32) {
                 const int j = j0 + lane;
                 const bool ok = j < TT && mp_survives(qmn, qmx, tbmin + (size_t)j * K, tbmax + (size_t)j * K, K, theta, relm);
-                c += __popc(__ballot_sync(0xffffffffu, ok));
+                const unsigned m = __ballot_sync(0xffffffffu, ok);
+                c += __popc(m);
+                if (bits && lane == 0) bits[q * ((TT + 31) >> 5) + (j0 >> 5)] = m;  // mp_emit expands these
             }
         } else {
             c = TT;
@@ -598,11 +601,38 @@ __global__ void mp_count_kernel(const float* __restrict__ qbmin, const float* __
 __global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __restrict__ qbmax,
                                const float* __restrict__ tbmin, const float* __restrict__ tbmax,
                                const long long* __restrict__ cum, const DevCounters* ctr, int TT, int K, float theta,
-                               float relm, int prune, int* __restrict__ list) {
+                               float relm, int prune, int* __restrict__ list, const unsigned int* __restrict__ bits) {
     const int tq0 = ctr->tq_begin, tq1 = ctr->tq_end;
     if (tq0 >= tq1) return;
     const long long base = cum[tq0];
     const int lane = threadIdx.x & 31;
+    if (bits) {  // the survival masks mp_count wrote: expand, no second pass over the boxes
+        const int TW = (TT + 31) >> 5;
+        for (long long q = tq0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); q < tq1;
+             q += ((long long)gridDim.x * blockDim.x) >> 5) {
+            long long o = cum[q] - base;
+            for (int w0 = 0; w0 < TW; w0 += 32) {
+                const int wi = w0 + lane;
+                const unsigned m = wi < TW ? __ldg(bits + q * TW + wi) : 0u;
+                const int n = __popc(m);
+                int incl = n;  // exclusive prefix of the words' counts across lanes (ascending j)
+#pragma unroll
+                for (int x = 1; x < 32; x <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, x);
+                    if (lane >= x) incl += y;
+                }
+                long long pos = o + incl - n;
+                unsigned mm = m;
+                while (mm) {
+                    const int b = __ffs(mm) - 1;
+                    list[pos++] = (wi << 5) + b;
+                    mm &= mm - 1;
+                }
+                o += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        return;
+    }
     for (long long q = tq0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); q < tq1;
          q += ((long long)gridDim.x * blockDim.x) >> 5) {
         float qmn[MP_MAX], qmx[MP_MAX];
@@ -1128,16 +1158,17 @@ void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg
 }
 
 void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,
-                     int TT, int K, float theta, float relm, int prune, int2* ranges, long long* cost, cudaStream_t s) {
+                     int TT, int K, float theta, float relm, int prune, int2* ranges, long long* cost, unsigned int* bits,
+                     cudaStream_t s) {
     mp_count_kernel<<<grid_for_mp(nq * 32, 256), 256, 0, s>>>(qbmin, qbmax, tbmin, tbmax, nq, TT, K, theta, relm, prune,
-                                                          ranges, cost);
+                                                          ranges, cost, prune ? bits : nullptr);
 }
 
 void launch_mp_emit(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax,
                     const long long* cum, const DevCounters* ctr, long long nq, int TT, int K, float theta, float relm,
-                    int prune, int* list, cudaStream_t s) {
+                    int prune, int* list, const unsigned int* bits, cudaStream_t s) {
     mp_emit_kernel<<<grid_for_mp(nq * 32, 256), 256, 0, s>>>(qbmin, qbmax, tbmin, tbmax, cum, ctr, TT, K, theta, relm, prune,
-                                                         list);
+                                                         list, prune ? bits : nullptr);
 }
 
 void launch_stage_rows(const float* E, const int* tperm, const float* keys, long long N, int d, int Kpad, int K,
