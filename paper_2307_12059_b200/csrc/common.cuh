@@ -378,6 +378,33 @@ __device__ __forceinline__ float epi_max32(const uint32_t (&r)[32], const float4
     }
     return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
 }
+// the same with the thresholds in shared memory (plain loads)
+__device__ __forceinline__ float epi_max32_s(const uint32_t (&r)[32], const float4* th) {
+    float m[4] = {-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f};
+#pragma unroll
+    for (int u4 = 0; u4 < 8; ++u4) {
+        const float4 tt = th[u4];
+        float a0, a1, a2, a3;
+        sub2_f32(r[4 * u4 + 0], r[4 * u4 + 1], tt.x, tt.y, a0, a1);
+        sub2_f32(r[4 * u4 + 2], r[4 * u4 + 3], tt.z, tt.w, a2, a3);
+        const int c = (u4 & 1) * 2;
+        m[c] = max3_f32(m[c], a0, a1);
+        m[c + 1] = max3_f32(m[c + 1], a2, a3);
+    }
+    return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+}
+__device__ __forceinline__ uint32_t epi_hits32_s(const uint32_t (&r)[32], const float4* th, float ch) {
+    uint32_t hit = 0;
+#pragma unroll
+    for (int u4 = 0; u4 < 8; ++u4) {
+        const float4 tt = th[u4];
+        hit |= (uint32_t)(__fsub_rn(__uint_as_float(r[4 * u4 + 0]), tt.x) >= ch) << (4 * u4 + 0);
+        hit |= (uint32_t)(__fsub_rn(__uint_as_float(r[4 * u4 + 1]), tt.y) >= ch) << (4 * u4 + 1);
+        hit |= (uint32_t)(__fsub_rn(__uint_as_float(r[4 * u4 + 2]), tt.z) >= ch) << (4 * u4 + 2);
+        hit |= (uint32_t)(__fsub_rn(__uint_as_float(r[4 * u4 + 3]), tt.w) >= ch) << (4 * u4 + 3);
+    }
+    return hit;
+}
 // bit j set iff acc_j - th_j >= ch (the rare path after epi_max32 found a candidate)
 __device__ __forceinline__ uint32_t epi_hits32(const uint32_t (&r)[32], const float4* __restrict__ th, float ch) {
     uint32_t hit = 0;

@@ -43,9 +43,10 @@ constexpr uint32_t LBO_A = (BM / 8) * 128;     // bytes between K-adjacent core 
 constexpr uint32_t LBO_B = (BN_TC / 8) * 128;  // same, tail tile
 constexpr uint32_t SBO = 128;                  // bytes between M/N-adjacent core matrices
 constexpr uint32_t IDESC = idesc_tf32(BM, BN_TC);
+constexpr int TC_T2S_BYTES = 8 * 128 * 4;       // per epilogue warp: ||t||^2 / 2 of its 128 columns
 
 int tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
-    const int budget = 227 * 1024 - 512 - 2 * BM * 16;
+    const int budget = 227 * 1024 - 512 - 2 * BM * 16 - TC_T2S_BYTES;
     const int A = BM * Kpad * 4;
     for (int KC : {32, 16, 8}) {
         const int B = BN_TC * KC * 4;
@@ -58,7 +59,7 @@ int tc_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc) {
                 *a_stages = as;
                 *b_stages = bs;
                 *kc = KC;
-                int bytes = as * A + bs * B + 256 + as * BM * 16;
+                int bytes = as * A + bs * B + 256 + as * BM * 16 + TC_T2S_BYTES;
                 // >= 117 KB keeps one CTA per SM, so the 512-column TMEM
                 // allocation never waits on a co-resident CTA.
                 return bytes < 117 * 1024 ? 117 * 1024 : bytes;
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
     uint64_t* acc_empty = acc_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
     float4* qrow = reinterpret_cast<float4*>(bars + 32);  // [a_stages][BM] {||q||^2, ||q||, ||q - tf32(q)||, 0}
+    float* t2smem = reinterpret_cast<float*>(qrow + a_stages * BM);  // [8 epilogue warps][128]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // this CTA's contiguous, cost-balanced block of work items (every role walks it)
@@ -230,6 +232,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
         const int i = q * 32 + lane;
         int acc = 0, ai = 0;
         uint32_t accph = 0, aph = 0;
+        float* t2s = t2smem + (warp - 2) * 128;
+        float4 nt2 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float2 ntv = make_float2(0.f, 0.f);
+        auto load_ahead = [&](const int4& w, int jj) {
+            const int j = GATHER ? w.w + jj : item_tile(w, jj, p.tile_list);
+            nt2 = __ldg(reinterpret_cast<const float4*>((GATHER ? p.gT2 : p.T2) + (size_t)j * BN_TC + col0) + lane);
+            ntv = GATHER ? p.gtst[j] : p.tstile[j];
+        };
+        if (!FACT && it_begin < it_end) {
+            const int4 w0 = p.items[it_begin];
+            load_ahead(w0, w0.y);
+        }
         for (long long it = it_begin; it < it_end; it += it_step) {
             const int4 w = p.items[it];
             TC_WAIT(4, &a_full[ai], aph);
@@ -336,7 +350,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
             if (!FACT) for (int jj = w.y; jj <= w.z; ++jj) {
                 // gathered: j is the block (the tile list's offset + jj), else the tail tile
                 const int j = GATHER ? w.w + jj : item_tile(w, jj, p.tile_list);
-                const float2 tv = GATHER ? p.gtst[j] : p.tstile[j];
+                // this tile's ||t||^2 / 2 slice and band maxima (loaded a tile ago: tiles_tc2.cu) into
+                // shared memory, then the next tile's loads
+                __syncwarp();
+                reinterpret_cast<float4*>(t2s)[lane] = nt2;
+                const float2 tv = ntv;
+                __syncwarp();
+                if (jj < w.z) {
+                    load_ahead(w, jj + 1);
+                } else if (it + it_step < it_end) {
+                    const int4 wn = p.items[it + it_step];
+                    load_ahead(wn, wn.y);
+                }
                 const float Tm = tv.x, Tdm = tv.y;
                 // |acc - q.t| <= Qd Tm + Qn Tdm + Qd Tdm + eta (Qn + Qd)(Tm + Tdm)
                 const float eb = Qd * Tm + Qn * Tdm + Qd * Tdm + p.eta * (Qn + Qd) * (Tm + Tdm);
@@ -345,22 +370,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tiles_tc_kernel(TileParams p, i
                 // candidate iff 2 acc - ||t||^2 >= c, tested as acc - ||t||^2/2 >= c/2 (T2 holds ||t||^2/2)
                 // Q2 is an FP32 sum: |Q2 - ||q||^2| <= (Kpad + 4) 2^-23 Q2 (builder)
                 const float c = Q2 - R - (float)(p.Kpad + 4) * 1.1920928955078125e-07f * Q2 - 9.5367431640625e-07f * (Q2 + R);
-                // ||t||^2 of this tile's and the next tile's columns into L1 ahead of use
-                // (4 lines each); each chunk's loads would otherwise be an L2 round trip
-                const float* t2row = (GATHER ? p.gT2 : p.T2) + (size_t)j * BN_TC + col0;
-                if (p.t2pf && lane < 4) prefetch_l1(t2row + lane * 32);
-                else if (!GATHER && p.t2pf && lane < 8 && jj < w.z)
-                    prefetch_l1(p.T2 + (size_t)item_tile(w, jj + 1, p.tile_list) * BN_TC + col0 + (lane - 4) * 32);
                 TC_WAIT(5, &acc_full[acc], accph);
                 tc_fence_after();
                 const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN_TC + col0);
                 uint32_t ra[32], rb[32];
                 const float ch2 = 0.5f * c;  // T2 holds ||t||^2 / 2 (stage kernel)
                 auto process = [&](const uint32_t (&r)[32], int ch) {
-                    const float4* t2 = reinterpret_cast<const float4*>(t2row + ch * 32);
-                    const float m = epi_max32(r, t2);
+                    const float4* t2 = reinterpret_cast<const float4*>(t2s + ch * 32);
+                    const float m = epi_max32_s(r, t2);
                     if (__any_sync(0xffffffffu, m >= ch2)) {
-                        uint32_t hit = epi_hits32(r, t2, ch2);
+                        uint32_t hit = epi_hits32_s(r, t2, ch2);
                         unsigned long long slot = warp_reserve(__popc(hit), p.cand_count);
                         const int colb = j * BN_TC + col0 + ch * 32;
                         while (hit) {

@@ -61,6 +61,7 @@ __device__ unsigned long long g_tc2_prof[16];
 constexpr int TC2_THREADS = 448;  // same roles as tiles_tc.cu
 constexpr int TC2_BUILDER_WARP0 = 10;
 constexpr uint32_t LBO_A2 = (BM / 8) * 128;     // 128 query rows per CTA
+constexpr int TC2_T2S_BYTES = 8 * 128 * 4;      // per epilogue warp: ||t||^2 / 2 of its 128 columns
 constexpr uint32_t SBO2 = 128;
 // tail tiles of BNT rows (256, or 128: finer tail tiles prune better, same B bytes per MAC);
 // each CTA streams HALFT = BNT / 2 of them
@@ -68,7 +69,7 @@ constexpr uint32_t SBO2 = 128;
 int tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc, int bnt) {
     (void)bnt;  // 128-row tiles are streamed whole by one CTA: the same 128 rows per CTA and stage
     const int HALF = 128;
-    const int budget = 227 * 1024 - 512 - 2 * BM * 16;
+    const int budget = 227 * 1024 - 512 - 2 * BM * 16 - TC2_T2S_BYTES;
     const int A = BM * Kpad * 4;
     // prefer two A stages when the B ring still buffers >= 64 K-values
     // (experiment knob KGC_TC2_MINK: the minimum ring depth in K-values for two A stages)
@@ -85,7 +86,7 @@ int tc2_smem_bytes(int Kpad, int* a_stages, int* b_stages, int* kc, int bnt) {
                 *a_stages = as;
                 *b_stages = bs;
                 *kc = KC;
-                const int bytes = as * A + bs * B + 512 + as * BM * 16;
+                const int bytes = as * A + bs * B + 512 + as * BM * 16 + TC2_T2S_BYTES;
                 return bytes < 117 * 1024 ? 117 * 1024 : bytes;  // one CTA per SM
             }
         }
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
     uint64_t* b_empty = b_full + b_stages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 40);
     float4* qrow = reinterpret_cast<float4*>(bars + 64);  // [a_stages][BM] {||q||^2, ||q||, ||q - tf32(q)||, 0}
+    float* t2smem = reinterpret_cast<float*>(qrow + a_stages * BM);  // [8 epilogue warps][128]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = cluster_ctarank();
@@ -311,10 +313,36 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
         }
     } else if (warp < TC2_BUILDER_WARP0) {
         // ---------------------------------------------------- epilogue (both CTAs, own 128 rows)
+        // Each warp's ||t||^2 / 2 slice (128 floats) and band maxima of the NEXT tile are loaded one
+        // tile ahead (one float4 per lane) and parked in shared memory: read at use they were a
+        // global-load latency per 32-column chunk, and on d = 128 (c5) the MMA waited on the
+        // accumulator 38% of the time (ncu: the first FADD2 of each chunk stalled on them).
         const int q = warp & 3;
         const int hcol = (warp - 2) >> 2;       // column half of the 256-column accumulator
         const int col0 = hcol * HALF;           // its first TMEM column
+        const int tcol = PAIRED ? 0 : col0;     // this warp's first column inside its tile
         const int i = q * 32 + lane;
+        float* t2s = t2smem + (warp - 2) * 128;
+        const float* t2base = GATHER ? p.gT2 : p.T2;
+        auto tile_of = [&](const int4& w, int jj, int& j, bool& have) {
+            // PAIRED: this warp's column half is list entry jj + hcol (absent past the item's end)
+            have = !PAIRED || jj + hcol <= w.z;
+            // gathered: j is the block (the tile list's offset + jj), else the tail tile
+            j = GATHER ? w.w + jj : item_tile(w, PAIRED ? (have ? jj + hcol : jj) : jj, p.tile_list);
+        };
+        float4 nt2 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float2 ntv = make_float2(0.f, 0.f);
+        auto load_ahead = [&](const int4& w, int jj) {
+            int j;
+            bool hv;
+            tile_of(w, jj, j, hv);
+            nt2 = __ldg(reinterpret_cast<const float4*>(t2base + (size_t)j * BNT + tcol) + lane);
+            ntv = GATHER ? p.gtst[j] : p.tstile[j];
+        };
+        if (it_begin < it_end) {
+            const int4 w0 = p.items[it_begin];
+            load_ahead(w0, w0.y);
+        }
         int acc = 0, ai = 0;
         uint32_t accph = 0, aph = 0;
         for (long long it = it_begin; it < it_end; it += it_step) {
@@ -328,27 +356,26 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
             const int rowid = w.x * (2 * BM) + (int)crank * BM + i;
             const float thf = p.theta * (1.0f + 2.44140625e-04f) + 2.384185791015625e-07f * Qn;
             for (int jj = w.y; jj <= w.z; jj += TSTEP) {
-                // PAIRED: this warp's column half is list entry jj + hcol (absent past the item's end)
-                const bool have = !PAIRED || jj + hcol <= w.z;
-                // gathered: j is the block (the tile list's offset + jj), else the tail tile
-                const int j = GATHER ? w.w + jj : item_tile(w, PAIRED ? (have ? jj + hcol : jj) : jj, p.tile_list);
-                // column offset of this warp's columns inside tile j
-                const int tcol = PAIRED ? 0 : col0;
-                const float2 tv = GATHER ? p.gtst[j] : p.tstile[j];
+                int j;
+                bool have;
+                tile_of(w, jj, j, have);
+                // this tile's slice (loaded a tile ago) into shared memory, then the next tile's loads
+                __syncwarp();
+                reinterpret_cast<float4*>(t2s)[lane] = nt2;
+                const float2 tv = ntv;
+                __syncwarp();
+                if (jj + TSTEP <= w.z) {
+                    load_ahead(w, jj + TSTEP);
+                } else if (it + it_step < it_end) {
+                    const int4 wn = p.items[it + it_step];
+                    load_ahead(wn, wn.y);
+                }
                 const float Tm = tv.x, Tdm = tv.y;
                 // guard band exactly as tiles_tc.cu
                 const float eb = Qd * Tm + Qn * Tdm + Qd * Tdm + p.eta * (Qn + Qd) * (Tm + Tdm);
                 const float sl = 4.76837158203125e-07f * (Qn + Tm) * (Qn + Tm);
                 const float R = thf * thf + 2.0f * eb + sl;
                 const float c = Q2 - R - (float)(p.Kpad + 4) * 1.1920928955078125e-07f * Q2 - 9.5367431640625e-07f * (Q2 + R);
-                // ||t||^2 of this tile's and the next tile's columns into L1 ahead of use
-                // (4 lines each); each chunk's loads would otherwise be an L2 round trip
-                const float* t2base = GATHER ? p.gT2 : p.T2;
-                const float* t2row = t2base + (size_t)j * BNT + tcol;
-                if (p.t2pf && lane < 4) prefetch_l1(t2row + lane * 32);
-                else if (p.t2pf && lane < 8 && jj + TSTEP + (PAIRED ? hcol : 0) <= w.z)
-                    prefetch_l1(t2base + (size_t)(GATHER ? j + 1 : item_tile(w, jj + TSTEP + (PAIRED ? hcol : 0), p.tile_list)) * BNT +
-                                tcol + (lane - 4) * 32);
                 TC2_WAIT(5, &acc_full[acc], accph);
                 tc_fence_after();
                 const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 2 * HALF + col0);
@@ -356,10 +383,10 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) tiles_tc2_kernel(TileParams p,
                 const float ch2 = 0.5f * c;  // T2 holds ||t||^2 / 2 (stage kernel)
                 auto process = [&](const uint32_t (&r)[32], int ch) {
                     if (!have) return;
-                    const float4* t2 = reinterpret_cast<const float4*>(t2row + ch * 32);
-                    const float m = epi_max32(r, t2);
+                    const float4* t2 = reinterpret_cast<const float4*>(t2s + ch * 32);
+                    const float m = epi_max32_s(r, t2);
                     if (__any_sync(0xffffffffu, m >= ch2)) {
-                        uint32_t hit = epi_hits32(r, t2, ch2);
+                        uint32_t hit = epi_hits32_s(r, t2, ch2);
                         unsigned long long slot = warp_reserve(__popc(hit), p.cand_count);
                         const int colb = j * BNT + tcol + ch * 32;
                         while (hit) {
