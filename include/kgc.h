@@ -210,6 +210,7 @@ void kgc_destroy(kgc_ctx* ctx);
  *                                        of 64, at offset 64 * (cost prefix[q] - prefix[first]) (the
  *                                        tile list's offsets; entries past q's blocks are unused)
  *   KGC_INSPECT_GATHER_COST int64[R*QT]  engine 5: 64-tail blocks per query tile (0 outside this shard)
+ *   KGC_INSPECT_PIVOTS      float[K*d]   multi-pivot: the K pivots p_k, row-major (0 bytes with one pivot)
  * With multi-pivot pruning (pivots_used = K > 1) the key arrays hold K floats
  * per row: TAIL_KEYS float[N][K], QUERY_KEYS float[R][N][K]. */
 enum {
@@ -221,7 +222,8 @@ enum {
     KGC_INSPECT_QUERY_COST = 6,
     KGC_INSPECT_TILE_LIST = 7,
     KGC_INSPECT_GATHER_LIST = 8,
-    KGC_INSPECT_GATHER_COST = 9
+    KGC_INSPECT_GATHER_COST = 9,
+    KGC_INSPECT_PIVOTS = 10
 };
 /* After a join that ran in relation batches the arrays are those of the last batch. */
 int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes);

@@ -431,6 +431,250 @@ __global__ void __launch_bounds__(256) mp_qkeys_kernel(const float* __restrict__
     if (lane < nu) atomicMax(&qnmax[rw + lane], __float_as_uint(run_qn));
 }
 
+// ------------------------------------------- factorised L2 keys (FP64)
+// For L2 the K query keys of (h, r) need not cost K d operations each:
+//   ||h + r - p_k||^2 = ||h - p_k||^2 + 2 h.r - 2 r.p_k + ||r||^2
+//                     =   A[h][k]     + 2 B[h][r] - 2 C[r][k] + rr[r]
+// (TransE's connector_1 = h + r; the same expansion as the relation-factored
+// engine).  A is N x K (computed once per join, and for the tails it IS the tail key
+// squared), C and rr are R x K and R, and only B = h.r costs d per (h, r): one dot
+// product instead of K distances (c4: 7.3e9 -> 9.1e8 terms).  Everything is FP64
+// from the fp32 inputs, so the keys are those of the EXACT h + r (not of fl32(h + r)).
+// Error (u = 2^-53; products of two floats are exact in FP64; a d-term sum of
+// magnitudes M errs by <= (d - 1) u M; A <= (||h|| + ||p||)^2):
+//   |D~^2 - D^2| <= (d + 6) u (||h|| + ||r|| + ||p_k||)^2,
+// and sqrt is 1/2-Hoelder (|sqrt a - sqrt b| <= sqrt|a - b|, the clamp at 0 only
+// shrinks it), so |D~ - D| <= sqrt((d + 6) u) (Hmax + ||r|| + Pmax) =: delta_r.  The
+// float key sqrtf(fl32(D~^2)) adds < 2^-23 relative, inside the test margin relm;
+// delta_r widens the query boxes of relation r (through qnmax, which mp_boxes scales
+// by 2^-23: qnmax[r] = delta_r 2^23 rounded up).  The fl32(h + r) widening of the FP32
+// keys is not needed: these keys bound the exact h + r directly.
+
+// Per entity row x (one warp per row, lanes over dimensions): A[x][k] = ||x - p_k||^2
+// (FP64; optional), the tail keys sqrtf(fl32(A)) (optional) with their per-pivot
+// min / max, max_x ||x|| rounded up (optional), and the non-finite check of x.
+template <int K>
+__global__ void __launch_bounds__(256) mp_ent_kernel(const float* __restrict__ X, long long n, int d,
+                                                     const float* __restrict__ P, double* __restrict__ A,
+                                                     float* __restrict__ keys, unsigned int* minmax,
+                                                     unsigned int* xmax, unsigned int* nonfinite) {
+    extern __shared__ __align__(16) double me_smem[];
+    double* Ps = me_smem;  // [K][d], converted once per block (F2F.F64.F32 issues at 1/8 of the FFMA rate)
+    for (int x = threadIdx.x; x < K * d; x += blockDim.x) Ps[x] = (double)P[x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    float mn[K], mx[K], run_x = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) { mn[k] = FLT_MAX; mx[k] = 0.f; }
+    bool bad = false;
+    for (long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; row < n;
+         row += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const float* xr = X + row * d;
+        double acc[K], xx = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = 0.0;
+        for (int i = lane; i < d; i += 32) {
+            const float v = __ldg(xr + i);
+            bad |= !isfinite(v);
+            const double dv = (double)v;
+            xx = fma(dv, dv, xx);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const double t = dv - Ps[k * d + i];
+                acc[k] = fma(t, t, acc[k]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            xx += __shfl_xor_sync(0xffffffffu, xx, o);
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+        }
+        if (A && lane < K) {
+            double a = acc[0];
+#pragma unroll
+            for (int k = 1; k < K; ++k) if (lane == k) a = acc[k];
+            A[row * K + lane] = a;
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const float key = __fsqrt_rn(__double2float_rn(acc[k]));
+            mn[k] = fminf(mn[k], key);
+            mx[k] = fmaxf(mx[k], key);
+            if (keys && lane == k) keys[row * K + k] = key;
+        }
+        run_x = fmaxf(run_x, __double2float_ru(sqrt(xx) * (1.0 + 0x1p-40)));
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
+    if (minmax && lane < K) {
+        float a = mn[0], z = mx[0];
+#pragma unroll
+        for (int k = 1; k < K; ++k) if (lane == k) { a = mn[k]; z = mx[k]; }
+        // every lane of a warp holds the same values (the reductions above are warp-wide)
+        atomicMin(&minmax[2 * lane], __float_as_uint(a));
+        atomicMax(&minmax[2 * lane + 1], __float_as_uint(z));
+    }
+    if (xmax && lane == 0) atomicMax(xmax, __float_as_uint(run_x));
+}
+
+// Query keys from the factorisation: lane = entity (32 per chunk, rows staged in shared
+// memory, double-buffered by cp.async), warp w = NU consecutive relations whose rows are
+// held in shared memory as FP64; per (h, r) one FP64 dot product B = h.r, then
+// D~^2_k = A[h][k] + 2B - 2C[r][k] + rr[r] for every pivot.
+template <int K, int NU>
+__global__ void __launch_bounds__(256) mp_qkeys_fact_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
+                                                            long long N, long long R, int d, int nch,
+                                                            const float* __restrict__ P, const double* __restrict__ A,
+                                                            const unsigned int* __restrict__ hmax,
+                                                            float* __restrict__ keys, unsigned int* minmax,
+                                                            unsigned int* qnmax, unsigned int* nonfinite) {
+    static_assert(NU * K <= 32, "one lane per (relation, pivot) min/max");
+    extern __shared__ __align__(16) double mf_smem[];
+    const int D2 = (d + 1) / 2 * 2;
+    constexpr int RB = 8 * NU;
+    double* Rs = mf_smem;                                  // [RB][D2] relation rows (FP64)
+    double* Cs = Rs + RB * D2;                             // [RB][K + 1]: 2 C[r][k], then rr[r]
+    const int SD = (D2 & 3) ? D2 : D2 + 2;                 // FP64 entity row stride: SD / 2 odd (conflict-free double2)
+    double* Ed = Cs + RB * (K + 1);                        // [32][SD] this chunk's entity rows in FP64
+    __shared__ double pmax_s;
+    const long long r0 = (long long)blockIdx.y * RB;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    bool bad = false;
+    for (int x = threadIdx.x; x < RB * D2; x += blockDim.x) {
+        const int i = x / D2, k = x % D2;
+        const float v = (r0 + i < R && k < d) ? Rel[(r0 + i) * d + k] : 0.f;
+        bad |= !isfinite(v);
+        Rs[x] = (double)v;
+    }
+    if (threadIdx.x == 0) pmax_s = 0.0;
+    __syncthreads();
+    // C and rr: one warp per (relation, pivot-or-norm) pair; max ||p_k|| by warp 0
+    for (int pr = w; pr < RB * (K + 1); pr += 8) {
+        const int i = pr / (K + 1), k = pr % (K + 1);
+        double s = 0.0;
+        for (int x = lane; x < d; x += 32)
+            s = fma(Rs[i * D2 + x], k < K ? (double)__ldg(P + k * d + x) : Rs[i * D2 + x], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) Cs[pr] = k < K ? 2.0 * s : s;
+    }
+    if (w == 0) {
+        double pm = 0.0;
+        for (int k = 0; k < K; ++k) {
+            double s = 0.0;
+            for (int x = lane; x < d; x += 32) {
+                const double v = (double)__ldg(P + k * d + x);
+                s = fma(v, v, s);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            pm = fmax(pm, s);
+        }
+        if (lane == 0) pmax_s = sqrt(pm);
+    }
+    const long long rw = r0 + (long long)w * NU;
+    const int nu = rw >= R ? 0 : (int)min((long long)NU, R - rw);
+    float run_mn = FLT_MAX, run_mx = 0.f;
+    // entity rows: the next chunk's 32 rows are loaded into registers (warp w: rows w, w + 8, ...,
+    // lanes over k: coalesced, no index division) while this chunk computes, then converted to FP64
+    // once per block into Ed (F2F.F64.F32 issues at 1/8 of the FFMA rate: once per warp was 8x that)
+    constexpr int PR = 4, PK = (MP_MAX_DIM + 31) / 32;  // rows per warp, k-steps per lane
+    float pre[PR][PK];
+    auto load = [&](int ch) {
+        const long long h0 = ((long long)blockIdx.x * nch + ch) * 32;
+#pragma unroll
+        for (int a = 0; a < PR; ++a) {
+            const long long h = h0 + w + 8 * a;
+#pragma unroll
+            for (int c = 0; c < PK; ++c) {
+                const int k = lane + 32 * c;
+                pre[a][c] = (h < N && k < d) ? __ldg(E + h * d + k) : 0.f;
+            }
+        }
+    };
+    int nch_here = 0;
+    while (nch_here < nch && ((long long)blockIdx.x * nch + nch_here) * 32 < N) ++nch_here;
+    if (nch_here > 0) load(0);
+    for (int ch = 0; ch < nch_here; ++ch) {
+        const long long h0 = ((long long)blockIdx.x * nch + ch) * 32;
+        __syncthreads();  // every warp is done with Ed (and, at ch = 0, with the Cs / pmax_s set-up)
+#pragma unroll
+        for (int a = 0; a < PR; ++a)
+#pragma unroll
+            for (int c = 0; c < PK; ++c) {
+                const int k = lane + 32 * c;
+                if (k < D2) Ed[(w + 8 * a) * SD + k] = (double)pre[a][c];
+            }
+        __syncthreads();
+        if (ch + 1 < nch_here) load(ch + 1);  // in flight during this chunk's arithmetic
+        if (nu == 0) continue;
+        const long long h = h0 + lane;
+        const bool hv = h < N;
+        const double* es = Ed + lane * SD;
+        double b[NU];
+#pragma unroll
+        for (int u = 0; u < NU; ++u) b[u] = 0.0;
+        const double* rs = Rs + (w * NU) * D2;
+        for (int x = 0; x < D2; x += 2) {
+            const double2 e2 = *reinterpret_cast<const double2*>(es + x);
+#pragma unroll
+            for (int u = 0; u < NU; ++u) {
+                const double2 r2 = *reinterpret_cast<const double2*>(rs + u * D2 + x);
+                b[u] = fma(e2.y, r2.y, fma(e2.x, r2.x, b[u]));
+            }
+        }
+        double a[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) a[k] = hv ? __ldg(A + h * K + k) : 0.0;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+            if (u >= nu) break;
+            const long long r = rw + u;
+            const double* cr = Cs + (w * NU + u) * (K + 1);
+            const double b2 = 2.0 * b[u] + cr[K];
+            float kv[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const double q2 = (a[k] + b2) - cr[k];
+                kv[k] = __fsqrt_rn(__double2float_rn(fmax(q2, 0.0)));
+            }
+            if (hv) {
+                float* dst = keys + ((size_t)r * N + h) * K;
+                if (K == 8) {
+                    reinterpret_cast<float4*>(dst)[0] = make_float4(kv[0], kv[1], kv[2], kv[3]);
+                    reinterpret_cast<float4*>(dst)[1] = make_float4(kv[4], kv[5], kv[6], kv[7]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) dst[k] = kv[k];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const unsigned bits = __float_as_uint(kv[k]);
+                const unsigned m = __reduce_min_sync(0xffffffffu, hv ? bits : 0x7f7fffffu);
+                const unsigned z = __reduce_max_sync(0xffffffffu, hv ? bits : 0u);
+                if (lane == u * K + k) {
+                    run_mn = fminf(run_mn, __uint_as_float(m));
+                    run_mx = fmaxf(run_mx, __uint_as_float(z));
+                }
+            }
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
+    if (nch_here > 0 && lane < nu * K) {
+        const long long r = rw + lane / K;
+        const int k = lane % K;
+        atomicMin(&minmax[((size_t)r * K + k) * 2], __float_as_uint(run_mn));
+        atomicMax(&minmax[((size_t)r * K + k) * 2 + 1], __float_as_uint(run_mx));
+    }
+    if (lane < nu) {  // box widening delta_r, in units of 2^-23 (see above)
+        const double rr = Cs[(w * NU + lane) * (K + 1) + K];
+        const double S1 = (double)__uint_as_float(*hmax) + sqrt(rr) * (1.0 + 0x1p-40) + pmax_s * (1.0 + 0x1p-40);
+        const double delta = sqrt((double)(d + 6) * 0x1p-53) * (1.0 + 0x1p-20) * S1;
+        atomicMax(&qnmax[rw + lane], __float_as_uint(__double2float_ru(delta * 0x1p23)));
+    }
+}
+
 __global__ void mp_init_minmax_kernel(unsigned int* mm, long long n, unsigned int* qnmax, long long nseg) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         mm[2 * i] = __float_as_uint(FLT_MAX);
@@ -1140,6 +1384,65 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
     using BF = std::integral_constant<bool, false>;
     if (norm == 1) { if (query) byK(I1{}, BT{}); else byK(I1{}, BF{}); }
     else { if (query) byK(I2{}, BT{}); else byK(I2{}, BF{}); }
+}
+
+// L2 keys by the factorisation (see mp_qkeys_fact_kernel): tails (Et, NT) and queries
+// (E + Rel, N x R), both FP64.  A (N x K doubles) and hmax (one word) are scratch.
+void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long R, const float* Et, long long NT,
+                        int d, int K, const float* P, float* tkeys, unsigned int* tminmax, float* qkeys,
+                        unsigned int* qminmax, unsigned int* qnmax, double* A, unsigned int* hmax,
+                        unsigned int* nonfinite, cudaStream_t s) {
+    mp_init_minmax_kernel<<<grid_for_mp(K, 256), 256, 0, s>>>(tminmax, K, nullptr, 0);
+    mp_init_minmax_kernel<<<grid_for_mp(R * K, 256), 256, 0, s>>>(qminmax, R * K, qnmax, R);
+    cudaMemsetAsync(hmax, 0, 4, s);
+    const size_t esm = (size_t)K * d * 8;
+    auto ent = [&](auto kern, const float* X, long long n, double* a, float* keys, unsigned int* mm, unsigned int* xm) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
+        kern<<<grid_for_mp(n * 32, 256, 148LL * 8), 256, esm, s>>>(X, n, d, P, a, keys, mm, xm, nonfinite);
+    };
+    auto fact = [&](auto kern, int NU) {
+        const int D2 = (d + 1) / 2 * 2, RB = 8 * NU;
+        const size_t smem = (size_t)RB * D2 * 8 + (size_t)RB * (K + 1) * 8 + (size_t)32 * (D2 + 2) * 8;
+        const long long gy = (R + RB - 1) / RB;
+        const long long chunks = (N + 31) / 32;
+        long long gx_target = (148LL * 4 + gy - 1) / gy;
+        if (gx_target < 1) gx_target = 1;
+        long long nch = (chunks + gx_target - 1) / gx_target;
+        nch = std::max<long long>(1, std::min<long long>(nch, 32));
+        dim3 grid((unsigned)((chunks + nch - 1) / nch), (unsigned)gy);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, 256, smem, s>>>(E, Rel, N, R, d, (int)nch, P, A, hmax, qkeys, qminmax, qnmax, nonfinite);
+    };
+    auto byK = [&](auto k_) {
+        constexpr int KK = decltype(k_)::value;
+        const bool same = Et == E && NT == N;
+        if (same) {
+            ent(mp_ent_kernel<KK>, E, N, A, tkeys, tminmax, hmax);
+        } else {
+            ent(mp_ent_kernel<KK>, Et, NT, nullptr, tkeys, tminmax, nullptr);
+            ent(mp_ent_kernel<KK>, E, N, A, nullptr, nullptr, hmax);
+        }
+        // NU relations per warp (NU K <= 32): fewest relation blocks of 8 NU for this R
+        constexpr int NUMAX = 32 / KK < 4 ? 32 / KK : 4;
+        int nu = 1;
+        for (int c = 2; c <= NUMAX; ++c)
+            if ((R + 8 * c - 1) / (8 * c) < (R + 8 * nu - 1) / (8 * nu)) nu = c;
+        switch (nu) {
+            case 1: fact(mp_qkeys_fact_kernel<KK, 1>, 1); break;
+            case 2: fact(mp_qkeys_fact_kernel<KK, (NUMAX >= 2 ? 2 : 1)>, NUMAX >= 2 ? 2 : 1); break;
+            case 3: fact(mp_qkeys_fact_kernel<KK, (NUMAX >= 3 ? 3 : 1)>, NUMAX >= 3 ? 3 : 1); break;
+            default: fact(mp_qkeys_fact_kernel<KK, NUMAX>, NUMAX); break;
+        }
+    };
+    switch (K) {
+        case 2: byK(std::integral_constant<int, 2>{}); break;
+        case 3: byK(std::integral_constant<int, 3>{}); break;
+        case 4: byK(std::integral_constant<int, 4>{}); break;
+        case 5: byK(std::integral_constant<int, 5>{}); break;
+        case 6: byK(std::integral_constant<int, 6>{}); break;
+        case 7: byK(std::integral_constant<int, 7>{}); break;
+        default: byK(std::integral_constant<int, 8>{}); break;
+    }
 }
 
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,

@@ -1077,12 +1077,132 @@ void launch_absmax(const float* E, long long nE, const float* Rel, long long nR,
     absmax_kernel<<<grid_for(nE + nR, 256, 148 * 4), 256, 0, s>>>(E, nE, Rel, nR, out);
 }
 
+// SIMT-layout staging of query tiles (and tail tiles for the contiguous SIMT engine),
+// coalesced: one block per tile, warp per row with lanes over k (row reads of E are
+// whole 128-byte lines), rows parked in shared memory (stride Kpad + 1: conflict-free
+// column reads), then written out column by column ([k][ROWS], consecutive threads on
+// consecutive rows).  Same staged values as stage_kernel<false>; the row sums are FP32 with
+// rigorous upper bounds (>= the exact sums), so thresholds stay upper bounds.  The old kernel gave every lane a
+// whole row and walked k: 32 rows per load instruction, two active warps per block
+// (c2 L1 queries 0.44 ms).
+template <int ROWS>
+__global__ void __launch_bounds__(256) stage_simt_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
+                                                         const int* __restrict__ perm, long long N, int d, int Kpad,
+                                                         int QT, int tile0, int norm, float theta,
+                                                         float* __restrict__ out, float4* __restrict__ qs,
+                                                         float* __restrict__ T2, int cyc_world, int cyc_rank,
+                                                         int cyc_shift = 0) {
+    extern __shared__ float ss_smem[];  // [ROWS][Kpad + 1]
+    const int tile = tile0 + blockIdx.x;
+    if (cyc_world > 1 && (tile >> cyc_shift) % cyc_world != cyc_rank) return;  // (half tiles: shift 1)
+    long long r = 0, t_in_rel = tile;
+    if (Rel) {
+        r = tile / QT;
+        t_in_rel = tile - r * QT;
+    }
+    const int* pr = perm + (Rel ? r * N : 0);
+    const float* rel = Rel ? Rel + r * d : nullptr;
+    const int LDS = Kpad + 1;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    for (int i = w; i < ROWS; i += NW) {
+        const long long p = t_in_rel * ROWS + i;
+        const bool valid = p < N;
+        const long long h = valid ? pr[p] : 0;
+        // FP32 sums (FP64 conversions issue at 1/8 of the FFMA rate), then rigorous upper bounds:
+        // any-order sums of d nonnegative terms err by <= (d - 1) 2^-24 relative, the squares by 2^-24 more
+        float f2 = 0.f, f1 = 0.f;
+        for (int k = lane; k < Kpad; k += 32) {
+            float x = 0.f;
+            if (valid && k < d) x = rel ? __fadd_rn(__ldg(E + h * d + k), __ldg(rel + k)) : __ldg(E + h * d + k);
+            ss_smem[i * LDS + k] = x;
+            f2 = fmaf(x, x, f2);
+            f1 += fabsf(x);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            f2 += __shfl_xor_sync(0xffffffffu, f2, o);
+            f1 += __shfl_xor_sync(0xffffffffu, f1, o);
+        }
+        const double s2 = (double)f2 * (1.0 + (d + 2) * 5.9604644775390625e-08);
+        const double s1 = (double)f1 * (1.0 + (d + 1) * 5.9604644775390625e-08);
+        if (lane == 0) {
+            if (rel) {
+                float thr;
+                if (norm == 1) {
+                    thr = f2up((theta + s1 * 2.384185791015625e-07) * (1.0 + (d + 2) * 1.1920928955078125e-07) *
+                               (1.0 + 9.5367431640625e-07));
+                } else {
+                    const double thf = (double)theta * (1.0 + 2.44140625e-04) + 2.384185791015625e-07 * sqrt(s2);
+                    thr = f2up(thf * thf * (1.0 + (d + 3) * 1.1920928955078125e-07) * (1.0 + 9.5367431640625e-07));
+                }
+                qs[(size_t)blockIdx.x * ROWS + i] =
+                    valid ? make_float4(__double2float_rn(s2), f2up(sqrt(s2)), 0.f, thr) : make_float4(3e38f, 0.f, 0.f, -1.f);
+            }
+        }
+    }
+    __syncthreads();
+    float* dst = out + (size_t)blockIdx.x * ROWS * Kpad;
+    static_assert(256 % ROWS == 0, "whole rows per pass");
+    const int i = threadIdx.x % ROWS;
+    for (int k = threadIdx.x / ROWS; k < Kpad; k += 256 / ROWS)
+        dst[k * ROWS + i] = ss_smem[i * LDS + k];  // SIMT layout: element (i, k) at k * ROWS + i
+}
+
+// Half-tile staging for the one-warp gathered engine (QR = 32): tile t of relation r is half
+// tiles 2t and 2t + 1 of a 32-row tiling of the same sorted order, so the row scalars land at the
+// same qs indices as with 64-row tiles and the SIMT layout is [k][32] per half tile.
+void launch_stage_queries_half(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad, int QT,
+                               int tq0, int tq1, int norm, float theta, float* Qp, float4* qs, cudaStream_t s,
+                               int cyc_world, int cyc_rank) {
+    if (tq1 <= tq0) return;
+    const size_t smem = (size_t)32 * (Kpad + 1) * 4;
+    cudaFuncSetAttribute(stage_simt_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    stage_simt_kernel<32><<<2 * (tq1 - tq0), 256, smem, s>>>(E, Rel, qperm, N, d, Kpad, 2 * QT, 2 * tq0, norm, theta,
+                                                            Qp, qs, nullptr, cyc_world, cyc_rank, 1);
+}
+
+__global__ void items_halves_kernel(const int4* __restrict__ items, const long long* __restrict__ tiles,
+                                    const DevCounters* ctr, int4* __restrict__ items2, long long* __restrict__ tiles2,
+                                    long long* hctr) {
+    const long long n = ctr->n_items;
+    if (blockIdx.x == 0 && threadIdx.x == 0) hctr[0] = 2 * n;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int4 w = items[i];
+        const long long t = tiles[i];
+        items2[2 * i] = make_int4(2 * w.x, w.y, w.z, w.w);
+        items2[2 * i + 1] = make_int4(2 * w.x + 1, w.y, w.z, w.w);
+        tiles2[2 * i] = t;
+        tiles2[2 * i + 1] = t;
+    }
+}
+
+void launch_items_halves(const int4* items, const long long* item_tiles, const DevCounters* ctr, long long max_items,
+                         int4* items2, long long* item_tiles2, long long* item_cum2, long long* hctr, void* scan_tmp,
+                         cudaStream_t s, int* launches) {
+    // entries past the device item count stay zero (tiles2 zeroed by the caller), so the
+    // prefix over 2 max_items gives the balanced split its block total
+    items_halves_kernel<<<grid_for(max_items, 256), 256, 0, s>>>(items, item_tiles, ctr, items2, item_tiles2, hctr);
+    scan_exclusive_i64(item_tiles2, item_cum2, (size_t)(2 * max_items), hctr + 1, scan_tmp, s, launches);
+    if (launches) *launches += 1;
+}
+
+// the coalesced SIMT staging parks a whole tile in shared memory (<= 100 KB)
+static bool stage_simt_ok(int rows, int Kpad) {
+    const size_t smem = (size_t)rows * (Kpad + 1) * 4;
+    if (rows != SIMT_T || smem > 100 * 1024) return false;
+    cudaFuncSetAttribute(stage_simt_kernel<SIMT_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return true;
+}
+
 void launch_stage_tails(const float* E, const int* tperm, long long N, int d, int Kpad, int BN, int TT, int tc_layout,
                         float* Tp, float* T2, float2* tstile, cudaStream_t s) {
     if (TT <= 0) return;
     if (tc_layout)
         stage_kernel<true><<<TT, 1024, 0, s>>>(E, nullptr, tperm, N, d, Kpad, BN, 1, 0, 2, 0.f, Tp, nullptr, T2, tstile,
                                               tc_layout == 2 ? BN / 2 : BN);
+    else if (stage_simt_ok(BN, Kpad))
+        stage_simt_kernel<SIMT_T><<<TT, 256, (size_t)BN * (Kpad + 1) * 4, s>>>(E, nullptr, tperm, N, d, Kpad, 1, 0, 2,
+                                                                              0.f, Tp, nullptr, T2, 0, 0);
     else
         stage_kernel<false><<<TT, 256, 0, s>>>(E, nullptr, tperm, N, d, Kpad, BN, 1, 0, 2, 0.f, Tp, nullptr, T2, tstile,
                                                BN);
@@ -1095,6 +1215,10 @@ void launch_stage_queries(const float* E, const float* Rel, const int* qperm, lo
     if (tc_layout)
         stage_kernel<true><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, bq, QT, tq0, norm, theta, Qp, qs,
                                                      nullptr, nullptr, bq, cyc_world, cyc_rank);
+    else if (stage_simt_ok(bq, Kpad))
+        stage_simt_kernel<SIMT_T><<<tq1 - tq0, 256, (size_t)bq * (Kpad + 1) * 4, s>>>(E, Rel, qperm, N, d, Kpad, QT,
+                                                                                     tq0, norm, theta, Qp, qs, nullptr,
+                                                                                     cyc_world, cyc_rank);
     else
         stage_kernel<false><<<tq1 - tq0, 256, 0, s>>>(E, Rel, qperm, N, d, Kpad, bq, QT, tq0, norm, theta, Qp, qs,
                                                       nullptr, nullptr, bq, cyc_world, cyc_rank);

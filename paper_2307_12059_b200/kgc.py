@@ -26,7 +26,7 @@ STATUS_NAMES = {0: "KGC_OK", -1: "KGC_EINVAL", -2: "KGC_EDATA", -3: "KGC_ENOMEM"
                 -5: "KGC_ENODEV", -6: "KGC_ESTATE"}
 KGC_MAX_DIM = 1024
 INSPECT = {"tail_keys": 1, "query_keys": 2, "tail_perm": 3, "query_perm": 4, "tile_ranges": 5, "query_cost": 6,
-           "tile_list": 7, "gather_list": 8, "gather_cost": 9}
+           "tile_list": 7, "gather_list": 8, "gather_cost": 9, "pivots": 10}
 
 TRIPLET_DTYPE = np.dtype([("h", np.int32), ("r", np.int32), ("t", np.int32), ("dist", np.float32)])
 
@@ -210,7 +210,7 @@ def kgc_inspect(ctx, what: str) -> np.ndarray:
         raise KgcError(int(n), kgc_last_error(ctx))
     dtype = {"tail_keys": np.float32, "query_keys": np.float32, "tail_perm": np.int32, "query_perm": np.int32,
              "tile_ranges": np.int32, "query_cost": np.int64, "tile_list": np.int32, "gather_list": np.int32,
-             "gather_cost": np.int64}[what]
+             "gather_cost": np.int64, "pivots": np.float32}[what]
     out = np.empty(n // np.dtype(dtype).itemsize, dtype=dtype)
     rc = load_library().kgc_inspect(ctx, code, out.ctypes.data, n)
     if rc < 0:

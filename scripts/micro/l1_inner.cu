@@ -69,7 +69,7 @@ int main(){
   float *g,*o; cudaMalloc(&g, 8*KLEN*128*4); cudaMalloc(&o, 148*16*256*4); cudaMemset(g,0,8*KLEN*128*4);
   int clk=0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const char* nm[]={"abs  (FADD+FADD|.|)","max2 (2 FMNMX+FADD2)"};
-  for(int v=0;v<2;++v){ for(int bps : {2,4}) {
+  for(int v=0;v<2;++v){ for(int bps : {1,2,4}) {
     auto kern = v==0 ? k<0> : k<1>;
     cudaEvent_t a,b; cudaEventCreate(&a); cudaEventCreate(&b);
     kern<<<148*bps,256>>>(g,o); cudaDeviceSynchronize();
