@@ -47,7 +47,7 @@ enum Phase { EV_START, EV_H2D, EV_KEYS, EV_SORT, EV_RANGES, EV_STAGE, EV_TILES, 
     X(est_hist) X(est_cost) X(mpP) X(mpkt) X(mpkq) X(mpmm_t) X(mpmm_q) X(mpc0) X(mpc1) X(tbmin) X(tbmax) X(qbmin) \
     X(qbmax) X(tile_list) X(tk_sample) X(tk_sel) X(tk_cnt) X(Ts) X(tks) X(gblk) X(granges) X(glist) X(tsc) X(gT2) \
     X(gtst) X(tmapbuf) X(fz) X(frt) X(frn) X(fzero) X(se_w) X(se_a64) X(se_b64) X(se_af) X(se_bf) X(se_zero) \
-    X(acc) X(Eb) X(mpbits) X(se_max) X(mpqn) X(mpA) X(mphx) X(items_h) X(itiles_h) X(icum_h) X(hctr)
+    X(acc) X(Eb) X(mpbits) X(se_max) X(mpqn) X(mpA) X(mphx)
 
 struct kgc_ctx {
     kgc_options opt{};
@@ -769,9 +769,6 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     // rows per gathered block: tensor cores 256 (= tail tile rows); SIMT 64 or 32 (KGC_GT_TB experiment knob)
     const char* gtb = kgc_knob("KGC_GT_TB");
     const int GB = gather_tc ? BN_TC : ((gtb && atoi(gtb) == 32) ? 32 : GT_ROWS);
-    // half-tile units (one warp per CTA, 32 query rows x 64 gathered tails): KGC_GT_HALF (experiment)
-    const char* ghe = kgc_knob("KGC_GT_HALF");
-    const bool ghalf = gather && GB == GT_ROWS && (ghe ? atoi(ghe) != 0 : false);
     long long g_max_items = 0;
     if (gather || gather_tc) {
         g_max_items = h1.c.my_cost * (BN / GB > 1 ? BN / GB : 1);  // blocks (and items) <= tiles x rows per block
@@ -821,18 +818,6 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         scan_exclusive_i64(P<long long>(ctx->item_tiles), P<long long>(ctx->item_cum), (size_t)g_max_items, nullptr,
                            ctx->scan_tmp.p, s, &ctx->launches);
         LAUNCHED(0);
-        if (ghalf) {
-            CK(ensure(ctx->items_h, (size_t)g_max_items * 32));
-            CK(ensure(ctx->itiles_h, (size_t)g_max_items * 16));
-            CK(ensure(ctx->icum_h, (size_t)g_max_items * 16));
-            CK(ensure(ctx->hctr, 16));
-            CK(ensure(ctx->scan_tmp, scan_tmp_bytes((size_t)(2 * g_max_items))));
-            CK(cudaMemsetAsync(ctx->itiles_h.p, 0, (size_t)g_max_items * 16, s));
-            launch_items_halves(P<int4>(ctx->items), P<long long>(ctx->item_tiles), dctr, g_max_items,
-                                P<int4>(ctx->items_h), P<long long>(ctx->itiles_h), P<long long>(ctx->icum_h),
-                                P<long long>(ctx->hctr), ctx->scan_tmp.p, s, &ctx->launches);
-            LAUNCHED(1);
-        }
     } else if (n_items > 0) {
         CK(ensure(ctx->items, (size_t)n_items * 16));
         CK(ensure(ctx->item_tiles, (size_t)n_items * 8));
@@ -877,13 +862,8 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         } else if (gather) {
             CK(ensure(ctx->Qp, (size_t)(tq1 - tq0) * bq * Kpad * 4));
             CK(ensure(ctx->qs, (size_t)(tq1 - tq0) * bq * 16));
-            if (ghalf)
-                launch_stage_queries_half(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, tq0, tq1, norm, feps,
-                                          P<float>(ctx->Qp), P<float4>(ctx->qs), s, cyc ? ctx->opt.world : 0,
-                                          ctx->opt.rank);
-            else
-                launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, bq, tq0, tq1, 0, norm, feps,
-                                     P<float>(ctx->Qp), P<float4>(ctx->qs), s, cyc ? ctx->opt.world : 0, ctx->opt.rank);
+            launch_stage_queries(E, Rel, P<int>(ctx->qperm), N, d, Kpad, QT, bq, tq0, tq1, 0, norm, feps,
+                                 P<float>(ctx->Qp), P<float4>(ctx->qs), s, cyc ? ctx->opt.world : 0, ctx->opt.rank);
             LAUNCHED(1);
         } else {
             // pair engine: 256-row tiles as two 128-row UMMA blocks (layout 2); 128-row tiles whole (layout 1)
@@ -969,19 +949,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                     CK(cudaMemsetAsync(prof, 0, 128, s));
                 }
                 tp.prof = prof;
-                tp.qr = SIMT_T;
-                if (ghalf) {  // half-tile units: items and staged queries by half tile
-                    TileParams th = tp;
-                    th.qr = 32;
-                    th.tq0 = 2 * tq0;
-                    th.items = P<int4>(ctx->items_h);
-                    th.item_cum = P<long long>(ctx->icum_h);
-                    th.dn_items = P<long long>(ctx->hctr);
-                    th.dtotal = P<long long>(ctx->hctr) + 1;
-                    launch_tiles_gather(th, norm, ctx->num_sms, 2 * g_max_items, s);
-                } else {
-                    launch_tiles_gather(tp, norm, ctx->num_sms, g_max_items, s);
-                }
+                launch_tiles_gather(tp, norm, ctx->num_sms, g_max_items, s);
                 if (prof) {
                     unsigned long long h[16];
                     CK(cudaMemcpyAsync(h, prof, 128, cudaMemcpyDeviceToHost, s));

@@ -88,7 +88,6 @@ struct TileParams {
     const float2* gtst;           // tensor-core gathered blocks: per block {max ||t||, max ||t - tf32(t)||}
     const void* tmap;             // tensor-core gathered blocks: CUtensorMap over Ts (device memory)
     int gb;                       // SIMT gathered blocks: tails per block (32 or 64)
-    int qr;                       // SIMT gathered engine: query rows per work unit (64 = tile, 32 = half tile)
     // relation-factored tensor-core engine (tiles_tc.cu, MODE 2)
     const float* fz;              // [R][N] (||h + r||^2 - theta^2) / 2 rounded down
     const float* frt;             // [R][ntpad] r.t (sorted tail positions; 0 past N)
@@ -199,14 +198,6 @@ void launch_tiles_tc2(const TileParams& p, int num_sms, cudaStream_t s);
 int  tc2_gather_ok(int Kpad);  // the gathered CTA-pair engine needs 32-wide K-chunks
 void launch_tiles_tc2_gather(const TileParams& p, int num_sms, cudaStream_t s);  // p.n_items: a bound
 void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t s);
-// half-tile units for the gathered SIMT engine: queries staged per 32-row half tile, every
-// item {tile, j0, j1, list_off} split into {2 tile, ...} and {2 tile + 1, ...} (prep.cu)
-void launch_stage_queries_half(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad, int QT,
-                               int tq0, int tq1, int norm, float theta, float* Qp, float4* qs, cudaStream_t s,
-                               int cyc_world, int cyc_rank);
-void launch_items_halves(const int4* items, const long long* item_tiles, const DevCounters* ctr, long long max_items,
-                         int4* items2, long long* item_tiles2, long long* item_cum2, long long* hctr, void* scan_tmp,
-                         cudaStream_t s, int* launches);
 void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long max_items, cudaStream_t s);
 void launch_tiles_half_l1(const TileParams& p, int num_sms, cudaStream_t s);
 constexpr int HALF_FLUSH_PAIRS = 8;  // FP16x2 engine: flush to FP32 every 16 dims

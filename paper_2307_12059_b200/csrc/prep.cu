@@ -1090,11 +1090,10 @@ __global__ void __launch_bounds__(256) stage_simt_kernel(const float* __restrict
                                                          const int* __restrict__ perm, long long N, int d, int Kpad,
                                                          int QT, int tile0, int norm, float theta,
                                                          float* __restrict__ out, float4* __restrict__ qs,
-                                                         float* __restrict__ T2, int cyc_world, int cyc_rank,
-                                                         int cyc_shift = 0) {
+                                                         float* __restrict__ T2, int cyc_world, int cyc_rank) {
     extern __shared__ float ss_smem[];  // [ROWS][Kpad + 1]
     const int tile = tile0 + blockIdx.x;
-    if (cyc_world > 1 && (tile >> cyc_shift) % cyc_world != cyc_rank) return;  // (half tiles: shift 1)
+    if (cyc_world > 1 && tile % cyc_world != cyc_rank) return;
     long long r = 0, t_in_rel = tile;
     if (Rel) {
         r = tile / QT;
@@ -1146,44 +1145,6 @@ __global__ void __launch_bounds__(256) stage_simt_kernel(const float* __restrict
     const int i = threadIdx.x % ROWS;
     for (int k = threadIdx.x / ROWS; k < Kpad; k += 256 / ROWS)
         dst[k * ROWS + i] = ss_smem[i * LDS + k];  // SIMT layout: element (i, k) at k * ROWS + i
-}
-
-// Half-tile staging for the one-warp gathered engine (QR = 32): tile t of relation r is half
-// tiles 2t and 2t + 1 of a 32-row tiling of the same sorted order, so the row scalars land at the
-// same qs indices as with 64-row tiles and the SIMT layout is [k][32] per half tile.
-void launch_stage_queries_half(const float* E, const float* Rel, const int* qperm, long long N, int d, int Kpad, int QT,
-                               int tq0, int tq1, int norm, float theta, float* Qp, float4* qs, cudaStream_t s,
-                               int cyc_world, int cyc_rank) {
-    if (tq1 <= tq0) return;
-    const size_t smem = (size_t)32 * (Kpad + 1) * 4;
-    cudaFuncSetAttribute(stage_simt_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    stage_simt_kernel<32><<<2 * (tq1 - tq0), 256, smem, s>>>(E, Rel, qperm, N, d, Kpad, 2 * QT, 2 * tq0, norm, theta,
-                                                            Qp, qs, nullptr, cyc_world, cyc_rank, 1);
-}
-
-__global__ void items_halves_kernel(const int4* __restrict__ items, const long long* __restrict__ tiles,
-                                    const DevCounters* ctr, int4* __restrict__ items2, long long* __restrict__ tiles2,
-                                    long long* hctr) {
-    const long long n = ctr->n_items;
-    if (blockIdx.x == 0 && threadIdx.x == 0) hctr[0] = 2 * n;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const int4 w = items[i];
-        const long long t = tiles[i];
-        items2[2 * i] = make_int4(2 * w.x, w.y, w.z, w.w);
-        items2[2 * i + 1] = make_int4(2 * w.x + 1, w.y, w.z, w.w);
-        tiles2[2 * i] = t;
-        tiles2[2 * i + 1] = t;
-    }
-}
-
-void launch_items_halves(const int4* items, const long long* item_tiles, const DevCounters* ctr, long long max_items,
-                         int4* items2, long long* item_tiles2, long long* item_cum2, long long* hctr, void* scan_tmp,
-                         cudaStream_t s, int* launches) {
-    // entries past the device item count stay zero (tiles2 zeroed by the caller), so the
-    // prefix over 2 max_items gives the balanced split its block total
-    items_halves_kernel<<<grid_for(max_items, 256), 256, 0, s>>>(items, item_tiles, ctr, items2, item_tiles2, hctr);
-    scan_exclusive_i64(item_tiles2, item_cum2, (size_t)(2 * max_items), hctr + 1, scan_tmp, s, launches);
-    if (launches) *launches += 1;
 }
 
 // the coalesced SIMT staging parks a whole tile in shared memory (<= 100 KB)

@@ -411,17 +411,9 @@ void launch_tiles_simt(const TileParams& p, int norm, int num_sms, cudaStream_t 
 // PROF = 1: clock64 wait instrumentation (KGC_GT_PROF=1, experiment only).
 // TB = tails per block: 64 (two warps sharing the stages) or 32 (one warp per CTA:
 // no lock-step between warps, half the padding; the query chunk is shared by 32 tails).
-// PRODW = 1: one more warp (the last) is a dedicated producer -- it issues every stage once
-// the compute warps have released it (empty barrier, one arrival per compute warp), so the
-// compute warps only wait, compute and release.
-// QR = query rows per work unit: 64 (a whole query tile, two warps sharing each stage) or 32
-// (half tiles: one warp per CTA with its own stages -- no lock-step between warps; the
-// queries are staged per 32-row half tile and the items name half tiles, see kgc_api.cu).
-template <int NORM, int KC, int NSTAGE, int SWZ, int PROF = 0, int DUTY = 1, int MINB = 8, int KUN = 1, int TB = 64,
-          int PRODW = 0, int QR = SIMT_T>
-__global__ void __launch_bounds__((QR / 8) * (TB / 8) + 32 * PRODW, MINB) tiles_gather_kernel(TileParams p) {
-    constexpr int T = QR, TM = 8, TN = 8, NT = (QR / TM) * (TB / TN), GX = TB / TN, NWARP = NT / 32;
-    static_assert(NT % 32 == 0, "whole warps");
+template <int NORM, int KC, int NSTAGE, int SWZ, int PROF = 0, int DUTY = 1, int MINB = 8, int KUN = 1, int TB = 64>
+__global__ void __launch_bounds__(TB, MINB) tiles_gather_kernel(TileParams p) {
+    constexpr int T = SIMT_T, TM = 8, TN = 8, NT = TB, GX = TB / TN, NWARP = TB / 32;
     static_assert(!SWZ || KC == 32, "swizzle over the 8 pieces of a 32-float row");
     static_assert(TB == 32 || TB == 64, "one or two warps");
     constexpr int LD = SWZ ? KC : KC + 4;  // tail row stride in shared memory (floats)
@@ -448,7 +440,7 @@ __global__ void __launch_bounds__((QR / 8) * (TB / 8) + 32 * PRODW, MINB) tiles_
     if (tid == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full[s], 1 + 32);  // the bulk copy's expect_tx arrival + 32 lanes' cp.async arrivals
-            mbar_init(&empty[s], PRODW ? NWARP : 1);
+            mbar_init(&empty[s], 1);
             released[s] = 0;
         }
         fence_mbar_init();
@@ -533,22 +525,7 @@ __global__ void __launch_bounds__((QR / 8) * (TB / 8) + 32 * PRODW, MINB) tiles_
         cs.w = p.items[cs.it];
         cs.j = cs.w.y;
     }
-    if (PRODW) {
-        if (tid >= NT) {  // the producer warp: every stage, once released
-            It pr = cs;
-            for (long long gp = 0; valid(pr); ++gp) {
-                const int s = (int)(gp % NSTAGE);
-                if (gp >= NSTAGE) {
-                    mbar_wait(&empty[s], (uint32_t)(gp / NSTAGE - 1) & 1u);
-                    fence_proxy_async_smem();  // the compute warps' reads before the bulk copy's writes
-                }
-                issue(pr, gp);
-                next(pr);
-            }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            return;
-        }
-    } else if (tid < 32) {  // prologue: warp 0 fills every stage
+    if (tid < 32) {  // prologue: warp 0 fills every stage
         It pr = cs;
         for (long long gp = 0; gp < NSTAGE && valid(pr); ++gp) {
             issue(pr, gp);
@@ -622,9 +599,7 @@ __global__ void __launch_bounds__((QR / 8) * (TB / 8) + 32 * PRODW, MINB) tiles_
         // slower one for good, and its partner then waited on every chunk.)
         __syncwarp();
         int last = 0;
-        if (PRODW) {
-            if (lane == 0) mbar_arrive(&empty[s]);
-        } else if (NWARP == 1) {
+        if (NWARP == 1) {
             last = 1;  // the only reader refills its own stage
         } else if (DUTY) {
             const int warp = tid >> 5;
@@ -686,22 +661,21 @@ __global__ void __launch_bounds__((QR / 8) * (TB / 8) + 32 * PRODW, MINB) tiles_
     }
 }
 
-template <int NORM, int KC, int NS, int SWZ = 0, int DUTY = 1, int MINB = 8, int KUN = 1, int TB = 64, int PRODW = 0,
-          int QR = SIMT_T>
+template <int NORM, int KC, int NS, int SWZ = 0, int DUTY = 1, int MINB = 8, int KUN = 1, int TB = 64>
 static void launch_gather_variant(const TileParams& p, int num_sms, long long max_items, cudaStream_t s) {
-    constexpr int T = QR, NT = (QR / 8) * (TB / 8) + 32 * PRODW;
+    constexpr int T = SIMT_T;
     const size_t smem = (size_t)NS * (KC * T + TB * (SWZ ? KC : KC + 4)) * 4 + 128 + TB * 4;
     static_assert(NS * 20 <= 128, "barriers and counters fit the 128-byte tail");
-    auto kern = p.prof ? tiles_gather_kernel<NORM, KC, NS, SWZ, 1, DUTY, MINB, KUN, TB, PRODW, QR>
-                       : tiles_gather_kernel<NORM, KC, NS, SWZ, 0, DUTY, MINB, KUN, TB, PRODW, QR>;
+    auto kern = p.prof ? tiles_gather_kernel<NORM, KC, NS, SWZ, 1, DUTY, MINB, KUN, TB>
+                       : tiles_gather_kernel<NORM, KC, NS, SWZ, 0, DUTY, MINB, KUN, TB>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TB, smem);
     if (per_sm < 1) per_sm = 1;
     long long g = (long long)num_sms * per_sm;
     if (g > max_items) g = max_items;
     if (g < 1) g = 1;
-    kern<<<(unsigned)g, NT, smem, s>>>(p);
+    kern<<<(unsigned)g, TB, smem, s>>>(p);
 }
 
 void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long max_items, cudaStream_t s) {
@@ -711,17 +685,6 @@ void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long m
     // measured on c2 L1 (tile-kernel ms, same session): KC 24 / 2 stages / alternating refill duty
     // 4.83; KC 32 4.93-5.07; KC 16 4.95; KC 24 with "last releaser refills" 4.93; KC 32 swizzled
     // 4.90; 3 stages 4.98-5.54; k-loop unrolled x2 at 6 CTAs/SM 4.99
-    if (p.qr == 32) {  // half-tile units: one warp per CTA, 32 queries x 64 gathered tails, own stages
-        if (norm == 1) {
-            if (v == 1) launch_gather_variant<1, 24, 2, 0, 1, 11, 1, 64, 0, 32>(p, num_sms, max_items, s);
-            else if (v == 2) launch_gather_variant<1, 16, 3, 0, 1, 10, 1, 64, 0, 32>(p, num_sms, max_items, s);
-            else if (v == 3) launch_gather_variant<1, 32, 2, 0, 1, 8, 1, 64, 0, 32>(p, num_sms, max_items, s);
-            else launch_gather_variant<1, 16, 2, 0, 1, 15, 1, 64, 0, 32>(p, num_sms, max_items, s);
-        } else {
-            launch_gather_variant<2, 16, 2, 0, 1, 15, 1, 64, 0, 32>(p, num_sms, max_items, s);
-        }
-        return;
-    }
     if (p.gb == 32) {  // one warp per CTA, 32-tail blocks
         if (norm == 1) {
             if (v == 1) launch_gather_variant<1, 32, 2, 0, 1, 8, 1, 32>(p, num_sms, max_items, s);
@@ -737,16 +700,6 @@ void launch_tiles_gather(const TileParams& p, int norm, int num_sms, long long m
         else if (v == 2) launch_gather_variant<1, 16, 2>(p, num_sms, max_items, s);
         else if (v == 3) launch_gather_variant<1, 32, 2, 1>(p, num_sms, max_items, s);
         else if (v == 4) launch_gather_variant<1, 24, 2, 0, 0>(p, num_sms, max_items, s);
-        // dedicated producer warp (3-warp CTAs; registers cap them at 5 per SM)
-        else if (v == 5) launch_gather_variant<1, 24, 2, 0, 1, 5, 1, 64, 1>(p, num_sms, max_items, s);
-        else if (v == 6) launch_gather_variant<1, 24, 3, 0, 1, 5, 1, 64, 1>(p, num_sms, max_items, s);
-        else if (v == 7) launch_gather_variant<1, 16, 3, 0, 1, 5, 1, 64, 1>(p, num_sms, max_items, s);
-        else if (v == 8) launch_gather_variant<1, 32, 2, 0, 1, 5, 1, 64, 1>(p, num_sms, max_items, s);
-        else if (v == 9) launch_gather_variant<1, 16, 4, 0, 1, 5, 1, 64, 1>(p, num_sms, max_items, s);
-        // no producer, last releaser refills, 3 stages (the leading warp may run a chunk ahead)
-        else if (v == 10) launch_gather_variant<1, 16, 3, 0, 0, 8>(p, num_sms, max_items, s);
-        else if (v == 11) launch_gather_variant<1, 24, 3, 0, 0, 5>(p, num_sms, max_items, s);
-        else if (v == 12) launch_gather_variant<1, 16, 4, 0, 0, 6>(p, num_sms, max_items, s);
         else launch_gather_variant<1, 24, 2>(p, num_sms, max_items, s);
     } else {
         launch_gather_variant<2, 24, 2>(p, num_sms, max_items, s);
