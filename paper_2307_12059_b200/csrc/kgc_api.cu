@@ -47,7 +47,7 @@ enum Phase { EV_START, EV_H2D, EV_KEYS, EV_SORT, EV_RANGES, EV_STAGE, EV_TILES, 
     X(est_hist) X(est_cost) X(mpP) X(mpkt) X(mpkq) X(mpmm_t) X(mpmm_q) X(mpc0) X(mpc1) X(tbmin) X(tbmax) X(qbmin) \
     X(qbmax) X(tile_list) X(tk_sample) X(tk_sel) X(tk_cnt) X(Ts) X(tks) X(gblk) X(granges) X(glist) X(tsc) X(gT2) \
     X(gtst) X(tmapbuf) X(fz) X(frt) X(frn) X(fzero) X(se_w) X(se_a64) X(se_b64) X(se_af) X(se_bf) X(se_zero) \
-    X(acc) X(Eb) X(mpbits) X(se_max) X(mpqn) X(mpA) X(mphx)
+    X(acc) X(Eb) X(mpbits) X(se_max) X(mpqn) X(mpA) X(mphx) X(mpB) X(mpC)
 
 struct kgc_ctx {
     kgc_options opt{};
@@ -242,7 +242,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 6 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2 || o.tail_shard < 0 || o.tail_shard > 1 || o.relation_batch < 0) {
+        o.l2_engine > 6 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || !mp_pivots_ok(o.pivots) || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2 || o.tail_shard < 0 || o.tail_shard > 1 || o.relation_batch < 0) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -665,11 +665,14 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         LAUNCHED(1);
         if (norm == 2) {  // FP64 factorisation: one h.r dot product per query row instead of K distances
             CK(ensure(ctx->mpA, (size_t)N * K * 8));
+            CK(ensure(ctx->mpB, (size_t)N * R * 8));
+            CK(ensure(ctx->mpC, (size_t)R * (K + 1) * 8));
             CK(ensure(ctx->mphx, 16));
             launch_mp_keys_l2f(E, Rel, N, R, Et, NT, d, K, P<float>(ctx->mpP), P<float>(ctx->mpkt),
                                P<unsigned>(ctx->mpmm_t), P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q),
-                               P<unsigned>(ctx->mpqn), P<double>(ctx->mpA), P<unsigned>(ctx->mphx), &dctr->nonfinite, s);
-            LAUNCHED((Et == E && NT == N) ? 4 : 5);
+                               P<unsigned>(ctx->mpqn), P<double>(ctx->mpA), P<double>(ctx->mpB), P<double>(ctx->mpC),
+                               P<unsigned>(ctx->mphx), &dctr->nonfinite, s);
+            LAUNCHED((Et == E && NT == N) ? 6 : 7);
         } else {
             launch_mp_keys(Et, nullptr, NT, 1, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkt),
                            P<unsigned>(ctx->mpmm_t), nullptr, &dctr->nonfinite, s);
@@ -705,14 +708,14 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(cudaEventRecord(ctx->ev[EV_SORT], s));
         // ---- a4: K-dim tile boxes and the L_inf test of every tile pair
         launch_mp_boxes(P<float>(ctx->mpkt), P<unsigned>(ctx->tperm), 1, NT, BN, TT, K, P<float>(ctx->tbmin),
-                        P<float>(ctx->tbmax), nullptr, s);
+                        P<float>(ctx->tbmax), nullptr, s, 1);  // tail boxes [k][TT]
         launch_mp_boxes(P<float>(ctx->mpkq), P<unsigned>(ctx->qperm), R, N, bq, QT, K, P<float>(ctx->qbmin),
                         P<float>(ctx->qbmax), P<unsigned>(ctx->mpqn), s);
         LAUNCHED(2);
-        // survival masks kept for mp_emit when they fit (c4: 2.2 MB; c5: 380 MB -> recompute)
+        // survival masks kept for mp_emit when they fit (c4: 2.2 MB; c5: 380 MB; beyond 2 GiB: recompute)
         const size_t bits_bytes = (size_t)nq * ((TT + 31) / 32) * 4;
         unsigned int* sbits = nullptr;
-        if (bits_bytes <= (64u << 20)) {
+        if (bits_bytes <= (2ull << 30)) {
             CK(ensure(ctx->mpbits, bits_bytes + 4));
             sbits = P<unsigned int>(ctx->mpbits);
         }
@@ -773,7 +776,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
     if (gather || gather_tc) {
         g_max_items = h1.c.my_cost * (BN / GB > 1 ? BN / GB : 1);  // blocks (and items) <= tiles x rows per block
         CK(ensure(ctx->Ts, (size_t)(NT + 1) * Kpad * 4));
-        CK(ensure(ctx->tks, (size_t)NT * MP_MAX * 4 + 4));
+        CK(ensure(ctx->tks, (size_t)NT * MP_G * 4 + 4));
         CK(ensure(ctx->gblk, (size_t)nq * 8));
         CK(ensure(ctx->granges, (size_t)nq * 8));
         CK(ensure(ctx->glist, (size_t)list_span * BN * 4 + 4));  // laid out at BN x the tile-list offsets

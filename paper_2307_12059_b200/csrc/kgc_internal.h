@@ -27,7 +27,9 @@ constexpr int EST_SAMPLES = 256;  // sampled queries per relation, rank-local sp
 constexpr int SIMT_T = 64;       // tile rows (query and tail), FP32 SIMT engines
 constexpr int SORT_IPB = 2048;   // radix-sort items per block (256 threads x 8)
 constexpr int TC_MAX_KPAD = 256; // tensor-core engine supports d <= 256
-constexpr int MP_MAX = 8;        // multi-pivot pruning: at most 8 pivots
+constexpr int MP_MAX = 32;       // multi-pivot pruning: at most 32 pivots (2..8, 12, 16, 24, 32)
+constexpr int MP_G = 8;          // pivots of the per-tail test of the gathered engines (the first 8)
+inline bool mp_pivots_ok(int k) { return k <= 8 || k == 12 || k == 16 || k == 24 || k == 32; }
 
 constexpr int MP_MAX_DIM = 256;  // multi-pivot pruning supports d <= 256
 constexpr int MP_SORT_PIVOTS = 4; // Morton order over the first 4 pivots (8 bits each: 32-bit code)
@@ -148,16 +150,17 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
                     const float* P, float* keys, unsigned int* minmax, unsigned int* qnmax, unsigned int* nonfinite,
                     cudaStream_t s);
 // L2 with K pivots: tail and query keys from the FP64 factorisation
-// ||h + r - p||^2 = ||h - p||^2 + 2 h.r - 2 r.p + ||r||^2 (pivots.cu); A: N x K doubles scratch
+// ||h + r - p||^2 = ||h - p||^2 + 2 h.r - 2 r.p + ||r||^2 (pivots.cu); scratch: A N x K, Bhr R x N,
+// Cg R x (K + 1) doubles
 void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long R, const float* Et, long long NT,
                         int d, int K, const float* P, float* tkeys, unsigned int* tminmax, float* qkeys,
-                        unsigned int* qminmax, unsigned int* qnmax, double* A, unsigned int* hmax,
-                        unsigned int* nonfinite, cudaStream_t s);
+                        unsigned int* qminmax, unsigned int* qnmax, double* A, double* Bhr, double* Cg,
+                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s);
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
                       unsigned long long* code, unsigned int* idx, cudaStream_t s);
 void launch_kd_refine(const float* keys, int* perm, long long nseg, long long L, int K, cudaStream_t s);
 void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg, long long L, int ROWS, int ntile,
-                     int K, float* bmin, float* bmax, const unsigned int* qnmax, cudaStream_t s);
+                     int K, float* bmin, float* bmax, const unsigned int* qnmax, cudaStream_t s, int transpose = 0);
 // bits (optional, nq x ceil(TT / 32) words): mp_count stores each query tile's survival masks
 // there and mp_emit expands them instead of repeating the box tests
 void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,

@@ -450,228 +450,279 @@ __global__ void __launch_bounds__(256) mp_qkeys_kernel(const float* __restrict__
 // by 2^-23: qnmax[r] = delta_r 2^23 rounded up).  The fl32(h + r) widening of the FP32
 // keys is not needed: these keys bound the exact h + r directly.
 
-// Per entity row x (one warp per row, lanes over dimensions): A[x][k] = ||x - p_k||^2
-// (FP64; optional), the tail keys sqrtf(fl32(A)) (optional) with their per-pivot
-// min / max, max_x ||x|| rounded up (optional), and the non-finite check of x.
+// Per entity row x (one thread per row, the pivots in shared memory as FP64, [d][K] so a
+// double2 load serves two pivots): A[x][k] = ||x - p_k||^2 in FP64 from the differences (no
+// cancellation: relative error <= (d + 3) 2^-53; optional), the tail keys sqrtf(fl32(A)) (optional)
+// with their per-pivot min / max, max_x ||x|| rounded up (optional), and the non-finite check of x.
 template <int K>
 __global__ void __launch_bounds__(256) mp_ent_kernel(const float* __restrict__ X, long long n, int d,
                                                      const float* __restrict__ P, double* __restrict__ A,
                                                      float* __restrict__ keys, unsigned int* minmax,
                                                      unsigned int* xmax, unsigned int* nonfinite) {
     extern __shared__ __align__(16) double me_smem[];
-    double* Ps = me_smem;  // [K][d], converted once per block (F2F.F64.F32 issues at 1/8 of the FFMA rate)
-    for (int x = threadIdx.x; x < K * d; x += blockDim.x) Ps[x] = (double)P[x];
+    constexpr int KP = (K + 1) / 2 * 2;
+    double* Ps = me_smem;  // [d][KP], converted once per block
+    for (int x = threadIdx.x; x < d * KP; x += blockDim.x) {
+        const int i = x / KP, k = x - i * KP;
+        Ps[x] = k < K ? (double)P[k * d + i] : 0.0;
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    float mn[K], mx[K], run_x = 0.f;
-#pragma unroll
-    for (int k = 0; k < K; ++k) { mn[k] = FLT_MAX; mx[k] = 0.f; }
+    const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+    float run_mn = FLT_MAX, run_mx = 0.f, run_x = 0.f;  // lane k: pivot k
     bool bad = false;
-    for (long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; row < n;
-         row += ((long long)gridDim.x * blockDim.x) >> 5) {
-        const float* xr = X + row * d;
-        double acc[K], xx = 0.0;
+    const long long nblk = (n + blockDim.x - 1) / blockDim.x;
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const long long row = blk * blockDim.x + threadIdx.x;
+        const bool rv = row < n;
+        const float* xr = X + (rv ? row : 0) * d;
+        double acc[KP], xx = 0.0;
 #pragma unroll
-        for (int k = 0; k < K; ++k) acc[k] = 0.0;
-        for (int i = lane; i < d; i += 32) {
-            const float v = __ldg(xr + i);
+        for (int k = 0; k < KP; ++k) acc[k] = 0.0;
+        auto step = [&](float v, int i) {
             bad |= !isfinite(v);
             const double dv = (double)v;
             xx = fma(dv, dv, xx);
+            const double2* pr = reinterpret_cast<const double2*>(Ps + i * KP);
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const double t = dv - Ps[k * d + i];
-                acc[k] = fma(t, t, acc[k]);
+            for (int k = 0; k < KP; k += 2) {
+                const double2 p2 = pr[k / 2];
+                const double t0 = dv - p2.x, t1 = dv - p2.y;
+                acc[k] = fma(t0, t0, acc[k]);
+                acc[k + 1] = fma(t1, t1, acc[k + 1]);
+            }
+        };
+        if (rv) {
+            if (vec) {
+                for (int i = 0; i < d; i += 4) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(xr + i));
+                    step(v.x, i); step(v.y, i + 1); step(v.z, i + 2); step(v.w, i + 3);
+                }
+            } else {
+                for (int i = 0; i < d; ++i) step(__ldg(xr + i), i);
             }
         }
+        if (rv && A) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            xx += __shfl_xor_sync(0xffffffffu, xx, o);
-#pragma unroll
-            for (int k = 0; k < K; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-        }
-        if (A && lane < K) {
-            double a = acc[0];
-#pragma unroll
-            for (int k = 1; k < K; ++k) if (lane == k) a = acc[k];
-            A[row * K + lane] = a;
+            for (int k = 0; k < K; ++k) A[row * K + k] = acc[k];
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const float key = __fsqrt_rn(__double2float_rn(acc[k]));
-            mn[k] = fminf(mn[k], key);
-            mx[k] = fmaxf(mx[k], key);
-            if (keys && lane == k) keys[row * K + k] = key;
+            if (rv && keys) keys[row * K + k] = key;
+            const unsigned bits = __float_as_uint(key);
+            const unsigned m = __reduce_min_sync(0xffffffffu, rv ? bits : 0x7f7fffffu);
+            const unsigned z = __reduce_max_sync(0xffffffffu, rv ? bits : 0u);
+            if (lane == k) {
+                run_mn = fminf(run_mn, __uint_as_float(m));
+                run_mx = fmaxf(run_mx, __uint_as_float(z));
+            }
         }
-        run_x = fmaxf(run_x, __double2float_ru(sqrt(xx) * (1.0 + 0x1p-40)));
+        if (rv) run_x = fmaxf(run_x, __double2float_ru(sqrt(xx) * (1.0 + 0x1p-40)));
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
     if (minmax && lane < K) {
-        float a = mn[0], z = mx[0];
-#pragma unroll
-        for (int k = 1; k < K; ++k) if (lane == k) { a = mn[k]; z = mx[k]; }
-        // every lane of a warp holds the same values (the reductions above are warp-wide)
-        atomicMin(&minmax[2 * lane], __float_as_uint(a));
-        atomicMax(&minmax[2 * lane + 1], __float_as_uint(z));
+        atomicMin(&minmax[2 * lane], __float_as_uint(run_mn));
+        atomicMax(&minmax[2 * lane + 1], __float_as_uint(run_mx));
     }
-    if (xmax && lane == 0) atomicMax(xmax, __float_as_uint(run_x));
+    if (xmax) {
+        const unsigned z = __reduce_max_sync(0xffffffffu, __float_as_uint(run_x));
+        if (lane == 0) atomicMax(xmax, z);
+    }
 }
 
-// Query keys from the factorisation: lane = entity (32 per chunk, rows staged in shared
-// memory, double-buffered by cp.async), warp w = NU consecutive relations whose rows are
-// held in shared memory as FP64; per (h, r) one FP64 dot product B = h.r, then
-// D~^2_k = A[h][k] + 2B - 2C[r][k] + rr[r] for every pivot.
-template <int K, int NU>
-__global__ void __launch_bounds__(256) mp_qkeys_fact_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
-                                                            long long N, long long R, int d, int nch,
-                                                            const float* __restrict__ P, const double* __restrict__ A,
-                                                            const unsigned int* __restrict__ hmax,
-                                                            float* __restrict__ keys, unsigned int* minmax,
-                                                            unsigned int* qnmax, unsigned int* nonfinite) {
-    static_assert(NU * K <= 32, "one lane per (relation, pivot) min/max");
-    extern __shared__ __align__(16) double mf_smem[];
-    const int D2 = (d + 1) / 2 * 2;
-    constexpr int RB = 8 * NU;
-    double* Rs = mf_smem;                                  // [RB][D2] relation rows (FP64)
-    double* Cs = Rs + RB * D2;                             // [RB][K + 1]: 2 C[r][k], then rr[r]
-    const int SD = (D2 & 3) ? D2 : D2 + 2;                 // FP64 entity row stride: SD / 2 odd (conflict-free double2)
-    double* Ed = Cs + RB * (K + 1);                        // [32][SD] this chunk's entity rows in FP64
-    __shared__ double pmax_s;
-    const long long r0 = (long long)blockIdx.y * RB;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    bool bad = false;
-    for (int x = threadIdx.x; x < RB * D2; x += blockDim.x) {
-        const int i = x / D2, k = x % D2;
-        const float v = (r0 + i < R && k < d) ? Rel[(r0 + i) * d + k] : 0.f;
-        bad |= !isfinite(v);
-        Rs[x] = (double)v;
+// B[r][h] = E_h . Rel_r for every (h, r) in FP64 (products of two floats are exact, FP64 sums):
+// the one d-term quantity per query row.  A register-blocked SIMT GEMM (FP64 tensor cores run at
+// the same ~60 FMA/clk/SM on B200): block = 4 warps, tile 128 entities x 32 relations, thread =
+// 4 entities x 8 relations (lane: entities 4 lane .. 4 lane + 3, warp w: relations 8 w ..), K-chunks
+// of 32 dims staged in shared memory as FP64 (converted once per block); per dim a warp issues
+// 32 DFMA against 12 shared-memory wavefronts.
+constexpr int HR_BM = 128, HR_BR = 32, HR_KC = 32;
+__global__ void __launch_bounds__(128) mp_hr_kernel(const float* __restrict__ E, const float* __restrict__ Rel,
+                                                    long long N, long long R, int d, double* __restrict__ B) {
+    __shared__ __align__(16) double Es[HR_KC][HR_BM];
+    __shared__ __align__(16) double Rs[HR_KC][HR_BR];
+    const long long h0 = (long long)blockIdx.x * HR_BM, r0 = (long long)blockIdx.y * HR_BR;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    double acc[4][8];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[a][c] = 0.0;
+    for (int k0 = 0; k0 < d; k0 += HR_KC) {
+        __syncthreads();
+        // entities: consecutive threads on consecutive rows (conflict-free stores; each row's
+        // 128-byte line is reused from L1 across the chunk's k)
+        for (int x = tid; x < HR_BM * HR_KC; x += 128) {
+            const int i = x % HR_BM, k = x / HR_BM;
+            const long long h = h0 + i;
+            Es[k][i] = (h < N && k0 + k < d) ? (double)__ldg(E + h * d + k0 + k) : 0.0;
+        }
+        for (int x = tid; x < HR_BR * HR_KC; x += 128) {
+            const int i = x % HR_BR, k = x / HR_BR;
+            const long long r = r0 + i;
+            Rs[k][i] = (r < R && k0 + k < d) ? (double)__ldg(Rel + r * d + k0 + k) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int k = 0; k < HR_KC; ++k) {
+            const double2 e01 = *reinterpret_cast<const double2*>(&Es[k][4 * lane]);
+            const double2 e23 = *reinterpret_cast<const double2*>(&Es[k][4 * lane + 2]);
+            const double ev[4] = {e01.x, e01.y, e23.x, e23.y};
+            double rv[8];
+#pragma unroll
+            for (int c = 0; c < 8; c += 2) {
+                const double2 r2 = *reinterpret_cast<const double2*>(&Rs[k][8 * w + c]);
+                rv[c] = r2.x;
+                rv[c + 1] = r2.y;
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[a][c] = fma(ev[a], rv[c], acc[a][c]);
+        }
     }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const long long r = r0 + 8 * w + c;
+        if (r >= R) break;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const long long h = h0 + 4 * lane + a;
+            if (h < N) B[r * N + h] = acc[a][c];
+        }
+    }
+}
+
+// Per relation: Cg[r][k] = 2 r.p_k (k < K), Cg[r][K] = ||r||^2 (FP64), the non-finite check of
+// Rel, and the box widening delta_r of the factorised keys (qnmax[r] = delta_r 2^23, rounded up;
+// needs max ||h|| from mp_ent_kernel).  One warp per (relation, term).
+__global__ void mp_rel_terms_kernel(const float* __restrict__ Rel, long long R, int d, int K,
+                                    const float* __restrict__ P, double* __restrict__ Cg,
+                                    const unsigned int* __restrict__ hmax, unsigned int* qnmax,
+                                    unsigned int* nonfinite) {
+    __shared__ double pmax_s;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
     if (threadIdx.x == 0) pmax_s = 0.0;
     __syncthreads();
-    // C and rr: one warp per (relation, pivot-or-norm) pair; max ||p_k|| by warp 0
-    for (int pr = w; pr < RB * (K + 1); pr += 8) {
-        const int i = pr / (K + 1), k = pr % (K + 1);
-        double s = 0.0;
-        for (int x = lane; x < d; x += 32)
-            s = fma(Rs[i * D2 + x], k < K ? (double)__ldg(P + k * d + x) : Rs[i * D2 + x], s);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) Cs[pr] = k < K ? 2.0 * s : s;
-    }
-    if (w == 0) {
-        double pm = 0.0;
-        for (int k = 0; k < K; ++k) {
-            double s = 0.0;
+    if (blockIdx.x == 0) {  // max ||p_k||
+        for (int k = w; k < K; k += NW) {
+            double sp = 0.0;
             for (int x = lane; x < d; x += 32) {
                 const double v = (double)__ldg(P + k * d + x);
-                s = fma(v, v, s);
+                sp = fma(v, v, sp);
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            pm = fmax(pm, s);
+            for (int o = 16; o > 0; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
+            if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&pmax_s), __double_as_longlong(sp));
         }
-        if (lane == 0) pmax_s = sqrt(pm);
     }
-    const long long rw = r0 + (long long)w * NU;
-    const int nu = rw >= R ? 0 : (int)min((long long)NU, R - rw);
-    float run_mn = FLT_MAX, run_mx = 0.f;
-    // entity rows: the next chunk's 32 rows are loaded into registers (warp w: rows w, w + 8, ...,
-    // lanes over k: coalesced, no index division) while this chunk computes, then converted to FP64
-    // once per block into Ed (F2F.F64.F32 issues at 1/8 of the FFMA rate: once per warp was 8x that)
-    constexpr int PR = 4, PK = (MP_MAX_DIM + 31) / 32;  // rows per warp, k-steps per lane
-    float pre[PR][PK];
-    auto load = [&](int ch) {
-        const long long h0 = ((long long)blockIdx.x * nch + ch) * 32;
-#pragma unroll
-        for (int a = 0; a < PR; ++a) {
-            const long long h = h0 + w + 8 * a;
-#pragma unroll
-            for (int c = 0; c < PK; ++c) {
-                const int k = lane + 32 * c;
-                pre[a][c] = (h < N && k < d) ? __ldg(E + h * d + k) : 0.f;
-            }
+    __syncthreads();
+    bool bad = false;
+    const long long nt = R * (K + 1);
+    for (long long t = (long long)blockIdx.x * NW + w; t < nt; t += (long long)gridDim.x * NW) {
+        const long long r = t / (K + 1);
+        const int k = (int)(t - r * (K + 1));
+        double sum = 0.0;
+        for (int x = lane; x < d; x += 32) {
+            const float rv = __ldg(Rel + r * d + x);
+            bad |= !isfinite(rv);
+            const double dr = (double)rv;
+            sum = fma(dr, k < K ? (double)__ldg(P + k * d + x) : dr, sum);
         }
-    };
-    int nch_here = 0;
-    while (nch_here < nch && ((long long)blockIdx.x * nch + nch_here) * 32 < N) ++nch_here;
-    if (nch_here > 0) load(0);
-    for (int ch = 0; ch < nch_here; ++ch) {
-        const long long h0 = ((long long)blockIdx.x * nch + ch) * 32;
-        __syncthreads();  // every warp is done with Ed (and, at ch = 0, with the Cs / pmax_s set-up)
 #pragma unroll
-        for (int a = 0; a < PR; ++a)
-#pragma unroll
-            for (int c = 0; c < PK; ++c) {
-                const int k = lane + 32 * c;
-                if (k < D2) Ed[(w + 8 * a) * SD + k] = (double)pre[a][c];
-            }
-        __syncthreads();
-        if (ch + 1 < nch_here) load(ch + 1);  // in flight during this chunk's arithmetic
-        if (nu == 0) continue;
-        const long long h = h0 + lane;
-        const bool hv = h < N;
-        const double* es = Ed + lane * SD;
-        double b[NU];
-#pragma unroll
-        for (int u = 0; u < NU; ++u) b[u] = 0.0;
-        const double* rs = Rs + (w * NU) * D2;
-        for (int x = 0; x < D2; x += 2) {
-            const double2 e2 = *reinterpret_cast<const double2*>(es + x);
-#pragma unroll
-            for (int u = 0; u < NU; ++u) {
-                const double2 r2 = *reinterpret_cast<const double2*>(rs + u * D2 + x);
-                b[u] = fma(e2.y, r2.y, fma(e2.x, r2.x, b[u]));
-            }
-        }
-        double a[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) a[k] = hv ? __ldg(A + h * K + k) : 0.0;
-#pragma unroll
-        for (int u = 0; u < NU; ++u) {
-            if (u >= nu) break;
-            const long long r = rw + u;
-            const double* cr = Cs + (w * NU + u) * (K + 1);
-            const double b2 = 2.0 * b[u] + cr[K];
-            float kv[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const double q2 = (a[k] + b2) - cr[k];
-                kv[k] = __fsqrt_rn(__double2float_rn(fmax(q2, 0.0)));
-            }
-            if (hv) {
-                float* dst = keys + ((size_t)r * N + h) * K;
-                if (K == 8) {
-                    reinterpret_cast<float4*>(dst)[0] = make_float4(kv[0], kv[1], kv[2], kv[3]);
-                    reinterpret_cast<float4*>(dst)[1] = make_float4(kv[4], kv[5], kv[6], kv[7]);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < K; ++k) dst[k] = kv[k];
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const unsigned bits = __float_as_uint(kv[k]);
-                const unsigned m = __reduce_min_sync(0xffffffffu, hv ? bits : 0x7f7fffffu);
-                const unsigned z = __reduce_max_sync(0xffffffffu, hv ? bits : 0u);
-                if (lane == u * K + k) {
-                    run_mn = fminf(run_mn, __uint_as_float(m));
-                    run_mx = fmaxf(run_mx, __uint_as_float(z));
-                }
-            }
-        }
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) Cg[t] = k < K ? 2.0 * sum : sum;
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
-    if (nch_here > 0 && lane < nu * K) {
-        const long long r = rw + lane / K;
-        const int k = lane % K;
-        atomicMin(&minmax[((size_t)r * K + k) * 2], __float_as_uint(run_mn));
-        atomicMax(&minmax[((size_t)r * K + k) * 2 + 1], __float_as_uint(run_mx));
+    if (blockIdx.x == 0) {
+        // delta_r needs max ||p|| of every pivot: block 0 only (it computed pmax_s), after the
+        // terms above are globally visible -- recompute ||r|| here instead of reading Cg
+        const double pm = sqrt(pmax_s) * (1.0 + 0x1p-40);
+        for (long long r = w; r < R; r += NW) {
+            double rr = 0.0;
+            for (int x = lane; x < d; x += 32) {
+                const double v = (double)__ldg(Rel + r * d + x);
+                rr = fma(v, v, rr);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
+            if (lane == 0) {
+                const double S1 = (double)__uint_as_float(*hmax) + sqrt(rr) * (1.0 + 0x1p-40) + pm;
+                const double delta = sqrt((double)(d + 6) * 0x1p-53) * (1.0 + 0x1p-20) * S1;
+                atomicMax(&qnmax[r], __float_as_uint(__double2float_ru(delta * 0x1p23)));
+            }
+        }
     }
-    if (lane < nu) {  // box widening delta_r, in units of 2^-23 (see above)
-        const double rr = Cs[(w * NU + lane) * (K + 1) + K];
-        const double S1 = (double)__uint_as_float(*hmax) + sqrt(rr) * (1.0 + 0x1p-40) + pmax_s * (1.0 + 0x1p-40);
-        const double delta = sqrt((double)(d + 6) * 0x1p-53) * (1.0 + 0x1p-20) * S1;
-        atomicMax(&qnmax[rw + lane], __float_as_uint(__double2float_ru(delta * 0x1p23)));
+}
+
+// Query keys from the factorisation: thread = entity h (its K values A[h][k] in registers),
+// loop over a chunk of relations: D~^2_k = (A[h][k] + (2 B[r][h] + ||r||^2)) - 2 r.p_k, key =
+// sqrtf(fl32(max(D~^2, 0))).  Writes are K contiguous floats per (r, h) row; per (relation,
+// pivot) min / max: warp REDUX, shared-memory atomics per block, one global atomic per block.
+constexpr int QK_RCH = 8;  // relations per block
+template <int K>
+__global__ void __launch_bounds__(256) mp_qkeys_fact_kernel(const double* __restrict__ B, const double* __restrict__ A,
+                                                            const double* __restrict__ Cg, long long N, long long R,
+                                                            float* __restrict__ keys, unsigned int* minmax) {
+    __shared__ unsigned int smn[QK_RCH][K], smx[QK_RCH][K];
+    __shared__ double cs[QK_RCH][K + 1];
+    const long long r0 = (long long)blockIdx.y * QK_RCH;
+    const int nr = (int)min((long long)QK_RCH, R - r0);
+    for (int x = threadIdx.x; x < QK_RCH * K; x += blockDim.x) {
+        smn[x / K][x % K] = 0x7f7fffffu;
+        smx[x / K][x % K] = 0u;
+    }
+    for (int x = threadIdx.x; x < nr * (K + 1); x += blockDim.x) cs[x / (K + 1)][x % (K + 1)] = Cg[r0 * (K + 1) + x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool hv = h < N;
+    double a[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) a[k] = hv ? __ldg(A + h * K + k) : 0.0;
+    for (int u = 0; u < nr; ++u) {
+        const long long r = r0 + u;
+        const double b2 = 2.0 * (hv ? __ldg(B + r * N + h) : 0.0) + cs[u][K];
+        float* dst = keys + ((size_t)r * N + h) * K;
+#pragma unroll
+        for (int k0 = 0; k0 < K; k0 += 4) {
+            float kv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = k0 + j;
+                kv[j] = k < K ? __fsqrt_rn(__double2float_rn(fmax((a[k < K ? k : 0] + b2) - cs[u][k < K ? k : 0], 0.0)))
+                              : 0.f;
+            }
+            if (hv) {
+                if (K % 4 == 0) {
+                    *reinterpret_cast<float4*>(dst + k0) = make_float4(kv[0], kv[1], kv[2], kv[3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (k0 + j < K) dst[k0 + j] = kv[j];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = k0 + j;
+                if (k < K) {
+                    const unsigned bits = __float_as_uint(kv[j]);
+                    const unsigned m = __reduce_min_sync(0xffffffffu, hv ? bits : 0x7f7fffffu);
+                    const unsigned z = __reduce_max_sync(0xffffffffu, hv ? bits : 0u);
+                    if (lane == 0) {
+                        atomicMin(&smn[u][k], m);
+                        atomicMax(&smx[u][k], z);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < nr * K; x += blockDim.x) {
+        const int u = x / K, k = x % K;
+        atomicMin(&minmax[((r0 + u) * K + k) * 2], smn[u][k]);
+        atomicMax(&minmax[((r0 + u) * K + k) * 2 + 1], smx[u][k]);
     }
 }
 
@@ -693,9 +744,9 @@ __global__ void mp_morton_kernel(const float* __restrict__ keys, const unsigned 
     const float scale_max = (float)((1u << bits) - 1);
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
         const long long s = t / L, i = t - s * L;
-        unsigned q[MP_MAX];
+        unsigned q[MP_SORT_PIVOTS];
 #pragma unroll
-        for (int k = 0; k < MP_MAX; ++k) {
+        for (int k = 0; k < MP_SORT_PIVOTS; ++k) {
             q[k] = 0;
             if (k < K) {
                 const float lo = __uint_as_float(minmax[(s * K + k) * 2]);
@@ -741,7 +792,7 @@ __global__ void mp_morton_kernel(const float* __restrict__ keys, const unsigned 
         unsigned long long c = 0;
         for (int b = bits - 1; b >= 0; --b)
 #pragma unroll
-            for (int k = 0; k < MP_MAX; ++k)
+            for (int k = 0; k < MP_SORT_PIVOTS; ++k)
                 if (k < Ks) c = (c << 1) | ((q[k] >> b) & 1u);
         code[t] = c;
         idx[t] = (unsigned)i;
@@ -757,9 +808,11 @@ __global__ void mp_morton_kernel(const float* __restrict__ keys, const unsigned 
 // 2^-23 max_h ||q^||_p of its relation (qnmax; the factor 2 covers the FP32 norm and
 // the 2^-24 -> ||q^|| vs ||h + r|| conversion), rounded outward: the boxes then bound
 // the keys of the exact h + r, and every test built on them stays lossless.
+// transpose = 1 (tail boxes): bmin[k * (nseg ntile) + tile], so the tile test's lanes (one tail
+// tile each) read consecutive words per pivot.
 __global__ void mp_boxes_kernel(const float* __restrict__ keys, const unsigned int* __restrict__ perm, long long nseg,
                                 long long L, int ROWS, int ntile, int K, float* __restrict__ bmin,
-                                float* __restrict__ bmax, const unsigned int* __restrict__ qnmax) {
+                                float* __restrict__ bmax, const unsigned int* __restrict__ qnmax, int transpose) {
     const int lane = threadIdx.x & 31;
     const long long nt = nseg * ntile;
     for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < nt;
@@ -771,9 +824,21 @@ __global__ void mp_boxes_kernel(const float* __restrict__ keys, const unsigned i
         for (int k = 0; k < MP_MAX; ++k) { mn[k] = FLT_MAX; mx[k] = -FLT_MAX; }
         for (long long i = b + lane; i < e; i += 32) {
             const float* kr = keys + ((size_t)s * L + perm[s * L + i]) * K;
+            if ((K & 3) == 0) {  // 16-byte rows: one float4 per 4 pivots
 #pragma unroll
-            for (int k = 0; k < MP_MAX; ++k)
-                if (k < K) { mn[k] = fminf(mn[k], kr[k]); mx[k] = fmaxf(mx[k], kr[k]); }
+                for (int k = 0; k < MP_MAX; k += 4)
+                    if (k < K) {
+                        const float4 v = __ldg(reinterpret_cast<const float4*>(kr + k));
+                        mn[k] = fminf(mn[k], v.x); mx[k] = fmaxf(mx[k], v.x);
+                        mn[k + 1] = fminf(mn[k + 1], v.y); mx[k + 1] = fmaxf(mx[k + 1], v.y);
+                        mn[k + 2] = fminf(mn[k + 2], v.z); mx[k + 2] = fmaxf(mx[k + 2], v.z);
+                        mn[k + 3] = fminf(mn[k + 3], v.w); mx[k + 3] = fmaxf(mx[k + 3], v.w);
+                    }
+            } else {
+#pragma unroll
+                for (int k = 0; k < MP_MAX; ++k)
+                    if (k < K) { mn[k] = fminf(mn[k], kr[k]); mx[k] = fmaxf(mx[k], kr[k]); }
+            }
         }
 #pragma unroll
         for (int k = 0; k < MP_MAX; ++k) {
@@ -788,7 +853,11 @@ __global__ void mp_boxes_kernel(const float* __restrict__ keys, const unsigned i
                     a = __fsub_rd(a, m);
                     z = __fadd_ru(z, m);
                 }
-                if (lane == 0) { bmin[w * K + k] = a; bmax[w * K + k] = z; }
+                if (lane == 0) {
+                    const long long o = transpose ? k * nt + w : w * K + k;
+                    bmin[o] = a;
+                    bmax[o] = z;
+                }
             }
         }
     }
@@ -798,14 +867,24 @@ __global__ void mp_boxes_kernel(const float* __restrict__ keys, const unsigned i
 // Tile pair survives iff for every pivot k the intervals are within th_k,
 // th_k = theta (1 + 2^-14) + relm (|qmax_k| + |tmax_k|), relm covering the
 // FP32 key error.
+// KM: register-array size (MP_MAX for the tile test, MP_G for the per-tail test).  Pivots are
+// tested 8 at a time; the lane stops at the first group that fails (most tile pairs fail on the
+// first pivots: with 32 pivots the loads of the later boxes are mostly skipped).
+template <int KM>
 __device__ __forceinline__ bool mp_survives(const float* qmn, const float* qmx, const float* __restrict__ tmn,
-                                            const float* __restrict__ tmx, int K, float theta, float relm) {
+                                            const float* __restrict__ tmx, int K, float theta, float relm,
+                                            int ts = 1) {
     bool ok = true;
 #pragma unroll
-    for (int k = 0; k < MP_MAX; ++k) {
-        if (k < K) {
-            const float th = theta * (1.0f + 6.103515625e-05f) + relm * (fabsf(qmx[k]) + fabsf(tmx[k]));
-            ok &= !(tmx[k] < qmn[k] - th || tmn[k] > qmx[k] + th);
+    for (int k0 = 0; k0 < KM; k0 += 8) {
+        if (k0 >= K || !ok) break;
+#pragma unroll
+        for (int k = k0; k < k0 + 8; ++k) {
+            if (k < K) {
+                const float tz = tmx[k * ts], ta = tmn[k * ts];  // ts: pivot stride of the tail box
+                const float th = theta * (1.0f + 6.103515625e-05f) + relm * (fabsf(qmx[k]) + fabsf(tz));
+                ok &= !(tz < qmn[k] - th || ta > qmx[k] + th);
+            }
         }
     }
     return ok;
@@ -827,7 +906,7 @@ __global__ void mp_count_kernel(const float* __restrict__ qbmin, const float* __
         if (prune) {
             for (int j0 = 0; j0 < TT; j0 += 32) {
                 const int j = j0 + lane;
-                const bool ok = j < TT && mp_survives(qmn, qmx, tbmin + (size_t)j * K, tbmax + (size_t)j * K, K, theta, relm);
+                const bool ok = j < TT && mp_survives<MP_MAX>(qmn, qmx, tbmin + j, tbmax + j, K, theta, relm, TT);
                 const unsigned m = __ballot_sync(0xffffffffu, ok);
                 c += __popc(m);
                 if (bits && lane == 0) bits[q * ((TT + 31) >> 5) + (j0 >> 5)] = m;  // mp_emit expands these
@@ -886,8 +965,8 @@ __global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __r
         long long o = cum[q] - base;
         for (int j0 = 0; j0 < TT; j0 += 32) {
             const int j = j0 + lane;
-            const bool ok = j < TT && (!prune || mp_survives(qmn, qmx, tbmin + (size_t)j * K, tbmax + (size_t)j * K,
-                                                             K, theta, relm));
+            const bool ok = j < TT && (!prune || mp_survives<MP_MAX>(qmn, qmx, tbmin + j, tbmax + j, K, theta,
+                                                                     relm, TT));
             const unsigned m = __ballot_sync(0xffffffffu, ok);
             if (ok) list[o + __popc(m & lanemask_lt())] = j;  // ascending j order
             o += __popc(m);
@@ -909,7 +988,7 @@ __global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __r
 
 // Sorted tails, row-major with row stride Kpad (zero padded), row N = zeros
 // (the sentinel the lists are padded with; the engines mask it by index or by
-// ||t||^2 = 3e38), the sorted tails' keys with row stride MP_MAX (two float4
+// ||t||^2 = 3e38), the sorted tails' first MP_G keys with row stride MP_G (two float4
 // loads per tail), and for the tensor-core engine the per-tail scalars
 // {||t||^2 / 2, ||t|| (up), ||t - tf32(t)|| (up), 0} from FP64 sums -- the
 // same values the tile staging kernel (prep.cu) computes.  One warp per row.
@@ -939,7 +1018,7 @@ __global__ void stage_rows_kernel(const float* __restrict__ E, const int* __rest
             s2 += xd * xd;
             sd2 += rd * rd;
         }
-        if (lane < MP_MAX) tks[(size_t)i * MP_MAX + lane] = lane < K ? __ldg(keys + (size_t)src * K + lane) : 0.f;
+        if (lane < MP_G) tks[(size_t)i * MP_G + lane] = lane < K ? __ldg(keys + (size_t)src * K + lane) : 0.f;
         if (tsc) {
             s2 = gt_warp_sum(s2);
             sd2 = gt_warp_sum(sd2);
@@ -981,10 +1060,12 @@ __global__ void gather_tails_kernel(const float* __restrict__ qbmin, const float
     for (long long q = tq0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); q < tq1;
          q += ((long long)gridDim.x * blockDim.x) >> 5) {
         if (cyc_world > 1 && q % cyc_world != cyc_rank) continue;  // cyclic split: not this rank's tile
-        float qmn[MP_MAX], qmx[MP_MAX];
+        // the per-tail test uses the first MP_G pivots (tks holds those; fewer pivots only prune less)
+        const int Kg = K < MP_G ? K : MP_G;
+        float qmn[MP_G], qmx[MP_G];
 #pragma unroll
-        for (int k = 0; k < MP_MAX; ++k)
-            if (k < K) { qmn[k] = qbmin[q * K + k]; qmx[k] = qbmax[q * K + k]; }
+        for (int k = 0; k < MP_G; ++k)
+            if (k < Kg) { qmn[k] = qbmin[q * K + k]; qmx[k] = qbmax[q * K + k]; }
         const int ntl = ranges[q].y + 1;
         const long long loff = cum[q] - base;
         const int* L = list + loff;
@@ -1010,8 +1091,8 @@ __global__ void gather_tails_kernel(const float* __restrict__ qbmin, const float
                 for (int h = 0; h < H; ++h) {
                     const long long i = ib[x] + 32 * h;
                     const float4 a = kv[x][h][0], b = kv[x][h][1];
-                    const float tk[MP_MAX] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-                    const bool ok = i < N && mp_survives(qmn, qmx, tk, tk, K, theta, relm);
+                    const float tk[MP_G] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                    const bool ok = i < N && mp_survives<MP_G>(qmn, qmx, tk, tk, Kg, theta, relm);
                     const unsigned m = __ballot_sync(0xffffffffu, ok);
                     if (!m) continue;
                     const long long pos = c + __popc(m & lanemask_lt());
@@ -1085,10 +1166,12 @@ __global__ void __launch_bounds__(256) gather_tails_block_kernel(
     unsigned long long pairs = 0, blocks = 0;
     for (long long q = tq0 + blockIdx.x; q < tq1; q += gridDim.x) {
         if (cyc_world > 1 && q % cyc_world != cyc_rank) continue;  // cyclic split: not this rank's tile
-        float qmn[MP_MAX], qmx[MP_MAX];
+        // the per-tail test uses the first MP_G pivots (tks holds those; fewer pivots only prune less)
+        const int Kg = K < MP_G ? K : MP_G;
+        float qmn[MP_G], qmx[MP_G];
 #pragma unroll
-        for (int k = 0; k < MP_MAX; ++k)
-            if (k < K) { qmn[k] = qbmin[q * K + k]; qmx[k] = qbmax[q * K + k]; }
+        for (int k = 0; k < MP_G; ++k)
+            if (k < Kg) { qmn[k] = qbmin[q * K + k]; qmx[k] = qbmax[q * K + k]; }
         const int ntl = ranges[q].y + 1;
         const long long loff = cum[q] - base;
         const int* L = list + loff;
@@ -1116,8 +1199,8 @@ __global__ void __launch_bounds__(256) gather_tails_block_kernel(
                     for (int h = 0; h < H; ++h) {
                         const long long i = ib[x] + 32 * h;
                         const float4 a = kv[x][h][0], b = kv[x][h][1];
-                        const float tk[MP_MAX] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-                        const bool ok = i < N && mp_survives(qmn, qmx, tk, tk, K, theta, relm);
+                        const float tk[MP_G] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                        const bool ok = i < N && mp_survives<MP_G>(qmn, qmx, tk, tk, Kg, theta, relm);
                         const unsigned m = __ballot_sync(0xffffffffu, ok);
                         if (pass == 1 && ok) out[c + __popc(m & lanemask_lt())] = (int)i;
                         c += __popc(m);
@@ -1163,12 +1246,12 @@ __global__ void __launch_bounds__(256) gather_tails_block_kernel(
 constexpr int KD_CH = 512, KD_LEVELS = 3;
 __global__ void __launch_bounds__(KD_CH) kd_refine_kernel(const float* __restrict__ keys, int* __restrict__ perm,
                                                          long long L, int K) {
-    __shared__ float kk[KD_CH][MP_MAX + 1];  // padded: row reads are conflict-free
+    __shared__ float kk[KD_CH][MP_G + 1];  // padded: row reads are conflict-free
     __shared__ int idx[KD_CH];
     __shared__ float sk[KD_CH];
     __shared__ int sl[KD_CH];
     __shared__ int ndim[1 << (KD_LEVELS - 1)];
-    __shared__ float wmn[KD_CH / 32][MP_MAX], wmx[KD_CH / 32][MP_MAX];
+    __shared__ float wmn[KD_CH / 32][MP_G], wmx[KD_CH / 32][MP_G];
     const long long seg = blockIdx.y;
     const long long c0 = (long long)blockIdx.x * KD_CH;
     if (c0 >= L) return;
@@ -1177,10 +1260,10 @@ __global__ void __launch_bounds__(KD_CH) kd_refine_kernel(const float* __restric
     int* pr = perm + seg * L + c0;
     const int my = i < n ? pr[i] : -1;
     idx[i] = my;
-    if (K == MP_MAX) {  // two 16-byte loads per row
+    if (K == MP_G) {  // two 16-byte loads per row
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
         if (my >= 0) {
-            const float4* r4 = reinterpret_cast<const float4*>(keys + ((size_t)seg * L + my) * MP_MAX);
+            const float4* r4 = reinterpret_cast<const float4*>(keys + ((size_t)seg * L + my) * MP_G);
             a = __ldg(r4);
             b = __ldg(r4 + 1);
         }
@@ -1188,7 +1271,7 @@ __global__ void __launch_bounds__(KD_CH) kd_refine_kernel(const float* __restric
         kk[i][4] = b.x; kk[i][5] = b.y; kk[i][6] = b.z; kk[i][7] = b.w;
     } else {
 #pragma unroll
-        for (int k = 0; k < MP_MAX; ++k)
+        for (int k = 0; k < MP_G; ++k)
             kk[i][k] = (my >= 0 && k < K) ? keys[((size_t)seg * L + my) * K + k] : 0.f;
     }
     __syncthreads();
@@ -1198,7 +1281,7 @@ __global__ void __launch_bounds__(KD_CH) kd_refine_kernel(const float* __restric
             // thread per node combines its warps
             const bool real = idx[i] >= 0;
 #pragma unroll
-            for (int k = 0; k < MP_MAX; ++k) {
+            for (int k = 0; k < MP_G; ++k) {
                 float a = real ? kk[i][k] : 3e38f, z = real ? kk[i][k] : -3e38f;
                 for (int o = 16; o > 0; o >>= 1) {
                     a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
@@ -1252,13 +1335,13 @@ __global__ void __launch_bounds__(KD_CH) kd_refine_kernel(const float* __restric
         // apply the node permutations
         const int src = sl[i];
         const int nidx = idx[src];
-        float nk[MP_MAX];
+        float nk[MP_G];
 #pragma unroll
-        for (int k = 0; k < MP_MAX; ++k) nk[k] = kk[src][k];
+        for (int k = 0; k < MP_G; ++k) nk[k] = kk[src][k];
         __syncthreads();
         idx[i] = nidx;
 #pragma unroll
-        for (int k = 0; k < MP_MAX; ++k) kk[i][k] = nk[k];
+        for (int k = 0; k < MP_G; ++k) kk[i][k] = nk[k];
         __syncthreads();
     }
     // padding rows are at the end of every node that holds any; compact the real rows
@@ -1273,7 +1356,7 @@ __global__ void __launch_bounds__(KD_CH) kd_refine_kernel(const float* __restric
 }
 
 void launch_kd_refine(const float* keys, int* perm, long long nseg, long long L, int K, cudaStream_t s) {
-    if (L < 2 * SIMT_T) return;
+    if (L < 2 * SIMT_T || K > MP_G) return;  // (experiment: up to MP_G pivots)
     dim3 grid((unsigned)((L + KD_CH - 1) / KD_CH), (unsigned)nseg);
     kd_refine_kernel<<<grid, KD_CH, 0, s>>>(keys, perm, L, K);
 }
@@ -1290,6 +1373,24 @@ void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, con
     auto kern = norm == 1 ? pick_pivots_kernel<1> : pick_pivots_kernel<2>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<1, 1024, smem, s>>>(E, N, d, K, (int)S, p0, P);
+}
+
+// K dispatch for the key kernels: 2..8, 12, 16, 24, 32 pivots (mp_pivots_ok)
+template <class F>
+static void for_pivots(int K, F&& f) {
+    switch (K) {
+        case 2: f(std::integral_constant<int, 2>{}); break;
+        case 3: f(std::integral_constant<int, 3>{}); break;
+        case 4: f(std::integral_constant<int, 4>{}); break;
+        case 5: f(std::integral_constant<int, 5>{}); break;
+        case 6: f(std::integral_constant<int, 6>{}); break;
+        case 7: f(std::integral_constant<int, 7>{}); break;
+        case 8: f(std::integral_constant<int, 8>{}); break;
+        case 12: f(std::integral_constant<int, 12>{}); break;
+        case 16: f(std::integral_constant<int, 16>{}); break;
+        case 24: f(std::integral_constant<int, 24>{}); break;
+        default: f(std::integral_constant<int, 32>{}); break;
+    }
 }
 
 static void launch_mp_qkeys(const float* E, const float* Rel, long long N, long long R, int d, int norm, int K,
@@ -1319,24 +1420,13 @@ static void launch_mp_qkeys(const float* E, const float* Rel, long long N, long 
     };
     auto byNU = [&](auto n_, auto k_) {
         constexpr int NN = decltype(n_)::value, KK = decltype(k_)::value;
-        switch (NU) {
-            case 1: go(mp_qkeys_kernel<NN, KK, 1>); break;
-            case 2: go(mp_qkeys_kernel<NN, KK, 2>); break;
-            case 3: go(mp_qkeys_kernel<NN, KK, 3>); break;
-            default: go(mp_qkeys_kernel<NN, KK, 4>); break;
-        }
+        // NU K <= 32 (one lane per (relation, pivot) min / max): larger NU only for small K
+        if (NU == 1) go(mp_qkeys_kernel<NN, KK, 1>);
+        if constexpr (2 * KK <= 32) if (NU == 2) go(mp_qkeys_kernel<NN, KK, 2>);
+        if constexpr (3 * KK <= 32) if (NU == 3) go(mp_qkeys_kernel<NN, KK, 3>);
+        if constexpr (4 * KK <= 32) if (NU == 4) go(mp_qkeys_kernel<NN, KK, 4>);
     };
-    auto byK = [&](auto n_) {
-        switch (K) {
-            case 2: byNU(n_, std::integral_constant<int, 2>{}); break;
-            case 3: byNU(n_, std::integral_constant<int, 3>{}); break;
-            case 4: byNU(n_, std::integral_constant<int, 4>{}); break;
-            case 5: byNU(n_, std::integral_constant<int, 5>{}); break;
-            case 6: byNU(n_, std::integral_constant<int, 6>{}); break;
-            case 7: byNU(n_, std::integral_constant<int, 7>{}); break;
-            default: byNU(n_, std::integral_constant<int, 8>{}); break;
-        }
-    };
+    auto byK = [&](auto n_) { for_pivots(K, [&](auto k_) { byNU(n_, k_); }); };
     if (norm == 1) byK(std::integral_constant<int, 1>{});
     else byK(std::integral_constant<int, 2>{});
 }
@@ -1368,15 +1458,7 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
     auto byK = [&](auto n_, auto q_) {
         constexpr int NN = decltype(n_)::value;
         constexpr bool QQ = decltype(q_)::value;
-        switch (K) {
-            case 2: go(mp_keys_kernel<NN, QQ, 2>); break;
-            case 3: go(mp_keys_kernel<NN, QQ, 3>); break;
-            case 4: go(mp_keys_kernel<NN, QQ, 4>); break;
-            case 5: go(mp_keys_kernel<NN, QQ, 5>); break;
-            case 6: go(mp_keys_kernel<NN, QQ, 6>); break;
-            case 7: go(mp_keys_kernel<NN, QQ, 7>); break;
-            default: go(mp_keys_kernel<NN, QQ, 8>); break;
-        }
+        if constexpr (!QQ) for_pivots(K, [&](auto k_) { go(mp_keys_kernel<NN, QQ, decltype(k_)::value>); });
     };
     using I1 = std::integral_constant<int, 1>;
     using I2 = std::integral_constant<int, 2>;
@@ -1390,28 +1472,15 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
 // (E + Rel, N x R), both FP64.  A (N x K doubles) and hmax (one word) are scratch.
 void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long R, const float* Et, long long NT,
                         int d, int K, const float* P, float* tkeys, unsigned int* tminmax, float* qkeys,
-                        unsigned int* qminmax, unsigned int* qnmax, double* A, unsigned int* hmax,
-                        unsigned int* nonfinite, cudaStream_t s) {
+                        unsigned int* qminmax, unsigned int* qnmax, double* A, double* Bhr, double* Cg,
+                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s) {
     mp_init_minmax_kernel<<<grid_for_mp(K, 256), 256, 0, s>>>(tminmax, K, nullptr, 0);
     mp_init_minmax_kernel<<<grid_for_mp(R * K, 256), 256, 0, s>>>(qminmax, R * K, qnmax, R);
     cudaMemsetAsync(hmax, 0, 4, s);
-    const size_t esm = (size_t)K * d * 8;
+    const size_t esm = (size_t)((K + 1) / 2 * 2) * d * 8;
     auto ent = [&](auto kern, const float* X, long long n, double* a, float* keys, unsigned int* mm, unsigned int* xm) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
-        kern<<<grid_for_mp(n * 32, 256, 148LL * 8), 256, esm, s>>>(X, n, d, P, a, keys, mm, xm, nonfinite);
-    };
-    auto fact = [&](auto kern, int NU) {
-        const int D2 = (d + 1) / 2 * 2, RB = 8 * NU;
-        const size_t smem = (size_t)RB * D2 * 8 + (size_t)RB * (K + 1) * 8 + (size_t)32 * (D2 + 2) * 8;
-        const long long gy = (R + RB - 1) / RB;
-        const long long chunks = (N + 31) / 32;
-        long long gx_target = (148LL * 4 + gy - 1) / gy;
-        if (gx_target < 1) gx_target = 1;
-        long long nch = (chunks + gx_target - 1) / gx_target;
-        nch = std::max<long long>(1, std::min<long long>(nch, 32));
-        dim3 grid((unsigned)((chunks + nch - 1) / nch), (unsigned)gy);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, 256, smem, s>>>(E, Rel, N, R, d, (int)nch, P, A, hmax, qkeys, qminmax, qnmax, nonfinite);
+        kern<<<grid_for_mp(n, 256, 148LL * 2), 256, esm, s>>>(X, n, d, P, a, keys, mm, xm, nonfinite);
     };
     auto byK = [&](auto k_) {
         constexpr int KK = decltype(k_)::value;
@@ -1422,27 +1491,14 @@ void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long
             ent(mp_ent_kernel<KK>, Et, NT, nullptr, tkeys, tminmax, nullptr);
             ent(mp_ent_kernel<KK>, E, N, A, nullptr, nullptr, hmax);
         }
-        // NU relations per warp (NU K <= 32): fewest relation blocks of 8 NU for this R
-        constexpr int NUMAX = 32 / KK < 4 ? 32 / KK : 4;
-        int nu = 1;
-        for (int c = 2; c <= NUMAX; ++c)
-            if ((R + 8 * c - 1) / (8 * c) < (R + 8 * nu - 1) / (8 * nu)) nu = c;
-        switch (nu) {
-            case 1: fact(mp_qkeys_fact_kernel<KK, 1>, 1); break;
-            case 2: fact(mp_qkeys_fact_kernel<KK, (NUMAX >= 2 ? 2 : 1)>, NUMAX >= 2 ? 2 : 1); break;
-            case 3: fact(mp_qkeys_fact_kernel<KK, (NUMAX >= 3 ? 3 : 1)>, NUMAX >= 3 ? 3 : 1); break;
-            default: fact(mp_qkeys_fact_kernel<KK, NUMAX>, NUMAX); break;
-        }
+        mp_rel_terms_kernel<<<(unsigned)std::min<long long>(148LL * 4, (R * (KK + 1) + 7) / 8), 256, 0, s>>>(
+            Rel, R, d, KK, P, Cg, hmax, qnmax, nonfinite);
+        dim3 ghr((unsigned)((N + HR_BM - 1) / HR_BM), (unsigned)((R + HR_BR - 1) / HR_BR));
+        mp_hr_kernel<<<ghr, 128, 0, s>>>(E, Rel, N, R, d, Bhr);
+        dim3 gk((unsigned)((N + 255) / 256), (unsigned)((R + QK_RCH - 1) / QK_RCH));
+        mp_qkeys_fact_kernel<KK><<<gk, 256, 0, s>>>(Bhr, A, Cg, N, R, qkeys, qminmax);
     };
-    switch (K) {
-        case 2: byK(std::integral_constant<int, 2>{}); break;
-        case 3: byK(std::integral_constant<int, 3>{}); break;
-        case 4: byK(std::integral_constant<int, 4>{}); break;
-        case 5: byK(std::integral_constant<int, 5>{}); break;
-        case 6: byK(std::integral_constant<int, 6>{}); break;
-        case 7: byK(std::integral_constant<int, 7>{}); break;
-        default: byK(std::integral_constant<int, 8>{}); break;
-    }
+    for_pivots(K, byK);
 }
 
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
@@ -1455,9 +1511,9 @@ void launch_mp_morton(const float* keys, const unsigned int* minmax, long long n
 }
 
 void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg, long long L, int ROWS, int ntile,
-                     int K, float* bmin, float* bmax, const unsigned int* qnmax, cudaStream_t s) {
+                     int K, float* bmin, float* bmax, const unsigned int* qnmax, cudaStream_t s, int transpose) {
     mp_boxes_kernel<<<grid_for_mp(nseg * ntile * 32, 256), 256, 0, s>>>(keys, perm, nseg, L, ROWS, ntile, K, bmin,
-                                                                         bmax, qnmax);
+                                                                         bmax, qnmax, transpose);
 }
 
 void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,
