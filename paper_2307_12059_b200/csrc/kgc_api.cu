@@ -64,6 +64,8 @@ struct kgc_ctx {
     kgc_stats_t st{};
     cudaEvent_t ev[EV_COUNT] = {};
     cudaEvent_t ev_split[2] = {};
+    cudaStream_t aux = nullptr;     // fork / join stream for pivot-independent work (the h.r GEMM)
+    cudaEvent_t ev_fork[2] = {};
     int launches = 0;
     // geometry of the last join (for kgc_inspect)
     long long N = 0, R = 0;
@@ -284,6 +286,8 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     }
     for (auto& e : ctx->ev) cudaEventCreate(&e);
     for (auto& e : ctx->ev_split) cudaEventCreate(&e);
+    cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
+    for (auto& e : ctx->ev_fork) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     cudaSetDevice(prev);
     *out = ctx;
     return KGC_OK;
@@ -302,6 +306,12 @@ void kgc_destroy(kgc_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_split)
         if (e) cudaEventDestroy(e);
+    for (auto e : ctx->ev_fork)
+        if (e) cudaEventDestroy(e);
+    if (ctx->aux) {
+        cudaStreamSynchronize(ctx->aux);
+        cudaStreamDestroy(ctx->aux);
+    }
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     cudaSetDevice(prev);
     delete ctx;
@@ -661,18 +671,25 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(ensure(ctx->tbmax, (size_t)TT * K * 4));
         CK(ensure(ctx->qbmin, (size_t)nq * K * 4));
         CK(ensure(ctx->qbmax, (size_t)nq * K * 4));
+        if (norm == 2) {  // the h.r GEMM needs no pivots: it runs on the aux stream beside the pivot choice
+            CK(ensure(ctx->mpB, (size_t)N * R * 8));
+            CK(cudaEventRecord(ctx->ev_fork[0], s));
+            CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork[0], 0));
+            launch_mp_hr(E, Rel, N, R, d, P<double>(ctx->mpB), ctx->aux);
+            CK(cudaEventRecord(ctx->ev_fork[1], ctx->aux));
+            LAUNCHED(1);
+        }
         launch_pick_pivots(Et, NT, d, norm, K, pivot, P<float>(ctx->mpP), s);
         LAUNCHED(1);
         if (norm == 2) {  // FP64 factorisation: one h.r dot product per query row instead of K distances
             CK(ensure(ctx->mpA, (size_t)N * K * 8));
-            CK(ensure(ctx->mpB, (size_t)N * R * 8));
             CK(ensure(ctx->mpC, (size_t)R * (K + 1) * 8));
             CK(ensure(ctx->mphx, 16));
             launch_mp_keys_l2f(E, Rel, N, R, Et, NT, d, K, P<float>(ctx->mpP), P<float>(ctx->mpkt),
                                P<unsigned>(ctx->mpmm_t), P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q),
                                P<unsigned>(ctx->mpqn), P<double>(ctx->mpA), P<double>(ctx->mpB), P<double>(ctx->mpC),
-                               P<unsigned>(ctx->mphx), &dctr->nonfinite, s);
-            LAUNCHED((Et == E && NT == N) ? 6 : 7);
+                               P<unsigned>(ctx->mphx), &dctr->nonfinite, s, ctx->aux, ctx->ev_fork);
+            LAUNCHED((Et == E && NT == N) ? 5 : 6);
         } else {
             launch_mp_keys(Et, nullptr, NT, 1, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkt),
                            P<unsigned>(ctx->mpmm_t), nullptr, &dctr->nonfinite, s);

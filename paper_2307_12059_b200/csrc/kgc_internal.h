@@ -155,7 +155,10 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
 void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long R, const float* Et, long long NT,
                         int d, int K, const float* P, float* tkeys, unsigned int* tminmax, float* qkeys,
                         unsigned int* qminmax, unsigned int* qnmax, double* A, double* Bhr, double* Cg,
-                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s);
+                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s, cudaStream_t aux,
+                        cudaEvent_t* ev_fork);
+// B[r][h] = E_h . Rel_r in FP64 (the pivot-independent part of the factorised keys)
+void launch_mp_hr(const float* E, const float* Rel, long long N, long long R, int d, double* B, cudaStream_t s);
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
                       unsigned long long* code, unsigned int* idx, cudaStream_t s);
 void launch_kd_refine(const float* keys, int* perm, long long nseg, long long L, int K, cudaStream_t s);

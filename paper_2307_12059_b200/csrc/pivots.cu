@@ -450,6 +450,17 @@ __global__ void __launch_bounds__(256) mp_qkeys_kernel(const float* __restrict__
 // by 2^-23: qnmax[r] = delta_r 2^23 rounded up).  The fl32(h + r) widening of the FP32
 // keys is not needed: these keys bound the exact h + r directly.
 
+// Key = sqrt of the FP64 squared distance rounded to float: the hardware approximation
+// (sqrt.approx.f32, MUFU; relative error < 2^-22) -- the IEEE sqrtf is a multi-instruction
+// sequence that made the 32-pivot key kernel issue-bound (c4: 1.5e8 keys per join).  With the
+// fl32 rounding of D^2 (2^-25 in the key) the key errs by < 2^-21 relative, well inside the tile
+// test's margin relm = (d + 8) 2^-23 (>= 9 2^-23) per key.
+__device__ __forceinline__ float key_sqrt(float x) {
+    float y;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Per entity row x (one thread per row, the pivots in shared memory as FP64, [d][K] so a
 // double2 load serves two pivots): A[x][k] = ||x - p_k||^2 in FP64 from the differences (no
 // cancellation: relative error <= (d + 3) 2^-53; optional), the tail keys sqrtf(fl32(A)) (optional)
@@ -508,7 +519,7 @@ __global__ void __launch_bounds__(256) mp_ent_kernel(const float* __restrict__ X
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const float key = __fsqrt_rn(__double2float_rn(acc[k]));
+            const float key = key_sqrt(__double2float_rn(acc[k]));
             if (rv && keys) keys[row * K + k] = key;
             const unsigned bits = __float_as_uint(key);
             const unsigned m = __reduce_min_sync(0xffffffffu, rv ? bits : 0x7f7fffffu);
@@ -691,7 +702,7 @@ __global__ void __launch_bounds__(256) mp_qkeys_fact_kernel(const double* __rest
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int k = k0 + j;
-                kv[j] = k < K ? __fsqrt_rn(__double2float_rn(fmax((a[k < K ? k : 0] + b2) - cs[u][k < K ? k : 0], 0.0)))
+                kv[j] = k < K ? key_sqrt(__double2float_rn(fmax((a[k < K ? k : 0] + b2) - cs[u][k < K ? k : 0], 0.0)))
                               : 0.f;
             }
             if (hv) {
@@ -703,16 +714,20 @@ __global__ void __launch_bounds__(256) mp_qkeys_fact_kernel(const double* __rest
                         if (k0 + j < K) dst[k0 + j] = kv[j];
                 }
             }
+            // per (relation, pivot) key range: only the first MP_SORT_PIVOTS pivots are quantised
+            // for the Hilbert order (mp_morton_kernel); nothing else reads the ranges
+            if (k0 < MP_SORT_PIVOTS) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int k = k0 + j;
-                if (k < K) {
-                    const unsigned bits = __float_as_uint(kv[j]);
-                    const unsigned m = __reduce_min_sync(0xffffffffu, hv ? bits : 0x7f7fffffu);
-                    const unsigned z = __reduce_max_sync(0xffffffffu, hv ? bits : 0u);
-                    if (lane == 0) {
-                        atomicMin(&smn[u][k], m);
-                        atomicMax(&smx[u][k], z);
+                for (int j = 0; j < 4; ++j) {
+                    const int k = k0 + j;
+                    if (k < K && k < MP_SORT_PIVOTS) {
+                        const unsigned bits = __float_as_uint(kv[j]);
+                        const unsigned m = __reduce_min_sync(0xffffffffu, hv ? bits : 0x7f7fffffu);
+                        const unsigned z = __reduce_max_sync(0xffffffffu, hv ? bits : 0u);
+                        if (lane == 0) {
+                            atomicMin(&smn[u][k], m);
+                            atomicMax(&smx[u][k], z);
+                        }
                     }
                 }
             }
@@ -890,31 +905,52 @@ __device__ __forceinline__ bool mp_survives(const float* qmn, const float* qmx, 
     return ok;
 }
 
-// One warp per query tile, lanes over tail tiles.
-__global__ void mp_count_kernel(const float* __restrict__ qbmin, const float* __restrict__ qbmax,
-                                const float* __restrict__ tbmin, const float* __restrict__ tbmax, long long nq, int TT,
-                                int K, float theta, float relm, int prune, int2* ranges, long long* cost,
-                                unsigned int* __restrict__ bits) {
-    const int lane = threadIdx.x & 31;
-    for (long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; q < nq;
-         q += ((long long)gridDim.x * blockDim.x) >> 5) {
+// One warp per query tile, lanes over tail tiles; the block's 16 query tiles share the tail
+// boxes, staged in shared memory in chunks of MC_CT tail tiles ([pivot][tile]: consecutive lanes
+// read consecutive words) -- the per-lane global loads of the boxes (a dependent L2 round trip
+// per 32 tail tiles) made the 32-pivot test latency-bound.
+constexpr int MC_CT = 128, MC_W = 16;
+__global__ void __launch_bounds__(32 * MC_W) mp_count_kernel(const float* __restrict__ qbmin,
+                                                             const float* __restrict__ qbmax,
+                                                             const float* __restrict__ tbmin,
+                                                             const float* __restrict__ tbmax, long long nq, int TT,
+                                                             int K, float theta, float relm, int prune, int2* ranges,
+                                                             long long* cost, unsigned int* __restrict__ bits) {
+    __shared__ float sbn[MP_MAX][MC_CT], sbx[MP_MAX][MC_CT];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int TW = (TT + 31) >> 5;
+    for (long long qb = (long long)blockIdx.x * MC_W; qb < nq; qb += (long long)gridDim.x * MC_W) {
+        const long long q = qb + w;
+        const bool qv = q < nq;
         float qmn[MP_MAX], qmx[MP_MAX];
 #pragma unroll
         for (int k = 0; k < MP_MAX; ++k)
-            if (k < K) { qmn[k] = qbmin[q * K + k]; qmx[k] = qbmax[q * K + k]; }
+            if (k < K) { qmn[k] = qv ? qbmin[q * K + k] : 0.f; qmx[k] = qv ? qbmax[q * K + k] : 0.f; }
         int c = 0;
         if (prune) {
-            for (int j0 = 0; j0 < TT; j0 += 32) {
-                const int j = j0 + lane;
-                const bool ok = j < TT && mp_survives<MP_MAX>(qmn, qmx, tbmin + j, tbmax + j, K, theta, relm, TT);
-                const unsigned m = __ballot_sync(0xffffffffu, ok);
-                c += __popc(m);
-                if (bits && lane == 0) bits[q * ((TT + 31) >> 5) + (j0 >> 5)] = m;  // mp_emit expands these
+            for (int j0 = 0; j0 < TT; j0 += MC_CT) {
+                __syncthreads();  // the previous chunk is consumed
+                for (int x = threadIdx.x; x < K * MC_CT; x += blockDim.x) {
+                    const int k = x / MC_CT, jj = x - k * MC_CT;
+                    const bool in = j0 + jj < TT;
+                    sbn[k][jj] = in ? tbmin[(size_t)k * TT + j0 + jj] : 0.f;
+                    sbx[k][jj] = in ? tbmax[(size_t)k * TT + j0 + jj] : 0.f;
+                }
+                __syncthreads();
+                if (!qv) continue;
+                for (int jj0 = 0; jj0 < MC_CT && j0 + jj0 < TT; jj0 += 32) {
+                    const int jj = jj0 + lane;
+                    const bool ok = j0 + jj < TT && mp_survives<MP_MAX>(qmn, qmx, &sbn[0][jj], &sbx[0][jj], K, theta,
+                                                                       relm, MC_CT);
+                    const unsigned m = __ballot_sync(0xffffffffu, ok);
+                    c += __popc(m);
+                    if (bits && lane == 0) bits[q * TW + ((j0 + jj0) >> 5)] = m;  // mp_emit expands these
+                }
             }
         } else {
             c = TT;
         }
-        if (lane == 0) {
+        if (qv && lane == 0) {
             ranges[q] = make_int2(0, c - 1);  // positions in this query tile's list
             cost[q] = c;
         }
@@ -1473,7 +1509,9 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
 void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long R, const float* Et, long long NT,
                         int d, int K, const float* P, float* tkeys, unsigned int* tminmax, float* qkeys,
                         unsigned int* qminmax, unsigned int* qnmax, double* A, double* Bhr, double* Cg,
-                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s) {
+                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s, cudaStream_t aux,
+                        cudaEvent_t* ev_fork) {
+    (void)aux;
     mp_init_minmax_kernel<<<grid_for_mp(K, 256), 256, 0, s>>>(tminmax, K, nullptr, 0);
     mp_init_minmax_kernel<<<grid_for_mp(R * K, 256), 256, 0, s>>>(qminmax, R * K, qnmax, R);
     cudaMemsetAsync(hmax, 0, 4, s);
@@ -1493,12 +1531,16 @@ void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long
         }
         mp_rel_terms_kernel<<<(unsigned)std::min<long long>(148LL * 4, (R * (KK + 1) + 7) / 8), 256, 0, s>>>(
             Rel, R, d, KK, P, Cg, hmax, qnmax, nonfinite);
-        dim3 ghr((unsigned)((N + HR_BM - 1) / HR_BM), (unsigned)((R + HR_BR - 1) / HR_BR));
-        mp_hr_kernel<<<ghr, 128, 0, s>>>(E, Rel, N, R, d, Bhr);
+        cudaStreamWaitEvent(s, ev_fork[1], 0);  // B from the aux stream (launch_mp_hr)
         dim3 gk((unsigned)((N + 255) / 256), (unsigned)((R + QK_RCH - 1) / QK_RCH));
         mp_qkeys_fact_kernel<KK><<<gk, 256, 0, s>>>(Bhr, A, Cg, N, R, qkeys, qminmax);
     };
     for_pivots(K, byK);
+}
+
+void launch_mp_hr(const float* E, const float* Rel, long long N, long long R, int d, double* B, cudaStream_t s) {
+    dim3 ghr((unsigned)((N + HR_BM - 1) / HR_BM), (unsigned)((R + HR_BR - 1) / HR_BR));
+    mp_hr_kernel<<<ghr, 128, 0, s>>>(E, Rel, N, R, d, B);
 }
 
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
@@ -1519,8 +1561,9 @@ void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg
 void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,
                      int TT, int K, float theta, float relm, int prune, int2* ranges, long long* cost, unsigned int* bits,
                      cudaStream_t s) {
-    mp_count_kernel<<<grid_for_mp(nq * 32, 256), 256, 0, s>>>(qbmin, qbmax, tbmin, tbmax, nq, TT, K, theta, relm, prune,
-                                                          ranges, cost, prune ? bits : nullptr);
+    mp_count_kernel<<<grid_for_mp(nq, MC_W, 148LL * 16), 32 * MC_W, 0, s>>>(qbmin, qbmax, tbmin, tbmax, nq, TT, K,
+                                                                          theta, relm, prune, ranges, cost,
+                                                                          prune ? bits : nullptr);
 }
 
 void launch_mp_emit(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax,
