@@ -47,7 +47,7 @@ enum Phase { EV_START, EV_H2D, EV_KEYS, EV_SORT, EV_RANGES, EV_STAGE, EV_TILES, 
     X(est_hist) X(est_cost) X(mpP) X(mpkt) X(mpkq) X(mpmm_t) X(mpmm_q) X(mpc0) X(mpc1) X(tbmin) X(tbmax) X(qbmin) \
     X(qbmax) X(tile_list) X(tk_sample) X(tk_sel) X(tk_cnt) X(Ts) X(tks) X(gblk) X(granges) X(glist) X(tsc) X(gT2) \
     X(gtst) X(tmapbuf) X(fz) X(frt) X(frn) X(fzero) X(se_w) X(se_a64) X(se_b64) X(se_af) X(se_bf) X(se_zero) \
-    X(acc) X(Eb) X(mpbits) X(se_max) X(mpqn) X(mpA) X(mphx) X(mpB) X(mpC)
+    X(acc) X(Eb) X(mpbits) X(se_max) X(mpqn) X(mpA) X(mphx) X(mpB) X(mpC) X(mpk4) X(mpmm4)
 
 struct kgc_ctx {
     kgc_options opt{};
@@ -72,6 +72,7 @@ struct kgc_ctx {
     int QT = 0, TT = 0, BN = 0;
     int K = 1;                  // pivots used by the last join
     int d = 0;                  // embedding dimension of the last join
+    bool l2f = false;           // the last join's K-pivot L2 keys came from the factorisation (not materialised)
     long long list_len = 0;     // multi-pivot tile-list length of this shard
     long long glist_len = 0;    // gathered-tail list length of this shard (entries)
     CUtensorMap tmap_host;      // tensor map over the sorted tails (gathered tensor-core engine)
@@ -661,7 +662,12 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         // ---- a2: K pivot distances per row (FP32)
         CK(ensure(ctx->mpP, (size_t)K * d * 4));
         CK(ensure(ctx->mpkt, (size_t)NT * K * 4 + 4));
-        CK(ensure(ctx->mpkq, NR * K * 4));
+        if (norm == 1) CK(ensure(ctx->mpkq, NR * K * 4));  // L1: materialised FP32 keys; L2: on the fly
+        if (norm == 1 && K > MP_MAX_L1) {
+            set_err(ctx, "pivots > %d need norm 2 (the L1 keys support at most %d pivots)", MP_MAX_L1, MP_MAX_L1);
+            return KGC_EINVAL;
+        }
+        ctx->l2f = norm == 2;
         CK(ensure(ctx->mpmm_t, (size_t)K * 8));
         CK(ensure(ctx->mpmm_q, (size_t)R * K * 8));
         CK(ensure(ctx->mpqn, (size_t)R * 4));
@@ -682,13 +688,16 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         launch_pick_pivots(Et, NT, d, norm, K, pivot, P<float>(ctx->mpP), s);
         LAUNCHED(1);
         if (norm == 2) {  // FP64 factorisation: one h.r dot product per query row instead of K distances
+            const int KO = K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS;
             CK(ensure(ctx->mpA, (size_t)N * K * 8));
             CK(ensure(ctx->mpC, (size_t)R * (K + 1) * 8));
+            CK(ensure(ctx->mpk4, NR * KO * 4));
+            CK(ensure(ctx->mpmm4, (size_t)R * KO * 8));
             CK(ensure(ctx->mphx, 16));
             launch_mp_keys_l2f(E, Rel, N, R, Et, NT, d, K, P<float>(ctx->mpP), P<float>(ctx->mpkt),
-                               P<unsigned>(ctx->mpmm_t), P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q),
+                               P<unsigned>(ctx->mpmm_t), P<float>(ctx->mpk4), P<unsigned>(ctx->mpmm4),
                                P<unsigned>(ctx->mpqn), P<double>(ctx->mpA), P<double>(ctx->mpB), P<double>(ctx->mpC),
-                               P<unsigned>(ctx->mphx), &dctr->nonfinite, s, ctx->aux, ctx->ev_fork);
+                               P<unsigned>(ctx->mphx), &dctr->nonfinite, s, ctx->ev_fork[1]);
             LAUNCHED((Et == E && NT == N) ? 5 : 6);
         } else {
             launch_mp_keys(Et, nullptr, NT, 1, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkt),
@@ -713,21 +722,29 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         const char* kde = kgc_knob("KGC_KD");  // local kd refinement of both orders (experiment knob)
         const bool kd = kde ? atoi(kde) != 0 : false;
         if (kd) launch_kd_refine(P<float>(ctx->mpkt), P<int>(ctx->tperm), 1, NT, K, s);
-        launch_mp_morton(P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q), R, N, K, bits,
-                         P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
+        if (norm == 2)  // the Hilbert pivots' keys (the rest are computed on the fly by the boxes)
+            launch_mp_morton(P<float>(ctx->mpk4), P<unsigned>(ctx->mpmm4), R, N, K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS,
+                             bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
+        else
+            launch_mp_morton(P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q), R, N, K, bits,
+                             P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
         LAUNCHED(1);
         radix_sort_u64_segments(R, N, code_bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
                                 P<unsigned long long>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
                                 ctx->scan_tmp.p, s, &ctx->launches);
         LAUNCHED(0);
         CK(cudaMemcpyAsync(ctx->qperm.p, ctx->sv0.p, NR * 4, cudaMemcpyDeviceToDevice, s));
-        if (kd) launch_kd_refine(P<float>(ctx->mpkq), P<int>(ctx->qperm), R, N, K, s);
+        if (kd && norm == 1) launch_kd_refine(P<float>(ctx->mpkq), P<int>(ctx->qperm), R, N, K, s);
         CK(cudaEventRecord(ctx->ev[EV_SORT], s));
         // ---- a4: K-dim tile boxes and the L_inf test of every tile pair
         launch_mp_boxes(P<float>(ctx->mpkt), P<unsigned>(ctx->tperm), 1, NT, BN, TT, K, P<float>(ctx->tbmin),
                         P<float>(ctx->tbmax), nullptr, s, 1);  // tail boxes [k][TT]
-        launch_mp_boxes(P<float>(ctx->mpkq), P<unsigned>(ctx->qperm), R, N, bq, QT, K, P<float>(ctx->qbmin),
-                        P<float>(ctx->qbmax), P<unsigned>(ctx->mpqn), s);
+        if (norm == 2)
+            launch_mp_qboxes_fact(P<unsigned>(ctx->qperm), P<double>(ctx->mpB), P<double>(ctx->mpA), P<double>(ctx->mpC),
+                                  N, R, K, bq, QT, P<unsigned>(ctx->mpqn), P<float>(ctx->qbmin), P<float>(ctx->qbmax), s);
+        else
+            launch_mp_boxes(P<float>(ctx->mpkq), P<unsigned>(ctx->qperm), R, N, bq, QT, K, P<float>(ctx->qbmin),
+                            P<float>(ctx->qbmax), P<unsigned>(ctx->mpqn), s);
         LAUNCHED(2);
         // survival masks kept for mp_emit when they fit (c4: 2.2 MB; c5: 380 MB; beyond 2 GiB: recompute)
         const size_t bits_bytes = (size_t)nq * ((TT + 31) / 32) * 4;
@@ -1742,11 +1759,24 @@ extern "C" int kgc_stats(const kgc_ctx* ctx, kgc_stats_t* out) {
 extern "C" int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes) {
     if (!ctx || bytes < 0) return KGC_EINVAL;
     if (!ctx->have_join || ctx->N == 0 || ctx->R == 0) return KGC_ESTATE;
+    struct DevGuard {
+        int prev = 0;
+        explicit DevGuard(int dev) { cudaGetDevice(&prev); cudaSetDevice(dev); }
+        ~DevGuard() { cudaSetDevice(prev); }
+    } guard(ctx->device);
     const void* src = nullptr;
     int64_t n = 0;
     switch (what) {
         case KGC_INSPECT_TAIL_KEYS: src = ctx->K > 1 ? ctx->mpkt.p : ctx->kt.p; n = ctx->N * 4 * ctx->K; break;
-        case KGC_INSPECT_QUERY_KEYS: src = ctx->K > 1 ? ctx->mpkq.p : ctx->kq.p; n = ctx->N * ctx->R * 4 * ctx->K; break;
+        case KGC_INSPECT_QUERY_KEYS:
+            if (ctx->K > 1 && ctx->l2f) {  // L2: materialise the keys the join computed on the fly
+                if (ensure(ctx->mpkq, (size_t)ctx->N * ctx->R * ctx->K * 4) != cudaSuccess) return KGC_ECUDA;
+                launch_mp_qkeys_all(P<double>(ctx->mpB), P<double>(ctx->mpA), P<double>(ctx->mpC), ctx->N, ctx->R,
+                                    ctx->K, P<float>(ctx->mpkq), ctx->stream);
+            }
+            src = ctx->K > 1 ? ctx->mpkq.p : ctx->kq.p;
+            n = ctx->N * ctx->R * 4 * ctx->K;
+            break;
         case KGC_INSPECT_TILE_LIST: src = ctx->tile_list.p; n = ctx->list_len * 4; break;
         case KGC_INSPECT_GATHER_LIST: src = ctx->glist.p; n = ctx->glist_len * 4; break;
         case KGC_INSPECT_GATHER_COST: src = ctx->glist_len ? ctx->gblk.p : nullptr; n = src ? ctx->R * (int64_t)ctx->QT * 8 : 0; break;

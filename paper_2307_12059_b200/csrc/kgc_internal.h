@@ -27,9 +27,10 @@ constexpr int EST_SAMPLES = 256;  // sampled queries per relation, rank-local sp
 constexpr int SIMT_T = 64;       // tile rows (query and tail), FP32 SIMT engines
 constexpr int SORT_IPB = 2048;   // radix-sort items per block (256 threads x 8)
 constexpr int TC_MAX_KPAD = 256; // tensor-core engine supports d <= 256
-constexpr int MP_MAX = 32;       // multi-pivot pruning: at most 32 pivots (2..8, 12, 16, 24, 32)
+constexpr int MP_MAX = 64;       // multi-pivot pruning: at most 64 pivots (2..8, 12, 16, 24, 32; 48, 64 with L2)
 constexpr int MP_G = 8;          // pivots of the per-tail test of the gathered engines (the first 8)
-inline bool mp_pivots_ok(int k) { return k <= 8 || k == 12 || k == 16 || k == 24 || k == 32; }
+inline bool mp_pivots_ok(int k) { return k <= 8 || k == 12 || k == 16 || k == 24 || k == 32 || k == 48 || k == 64; }
+constexpr int MP_MAX_L1 = 32;    // the L1 keys (FP32, materialised) support at most 32 pivots
 
 constexpr int MP_MAX_DIM = 256;  // multi-pivot pruning supports d <= 256
 constexpr int MP_SORT_PIVOTS = 4; // Morton order over the first 4 pivots (8 bits each: 32-bit code)
@@ -153,10 +154,14 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
 // ||h + r - p||^2 = ||h - p||^2 + 2 h.r - 2 r.p + ||r||^2 (pivots.cu); scratch: A N x K, Bhr R x N,
 // Cg R x (K + 1) doubles
 void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long R, const float* Et, long long NT,
-                        int d, int K, const float* P, float* tkeys, unsigned int* tminmax, float* qkeys,
-                        unsigned int* qminmax, unsigned int* qnmax, double* A, double* Bhr, double* Cg,
-                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s, cudaStream_t aux,
-                        cudaEvent_t* ev_fork);
+                        int d, int K, const float* P, float* tkeys, unsigned int* tminmax, float* qkeys4,
+                        unsigned int* qmm4, unsigned int* qnmax, double* A, double* Bhr, double* Cg,
+                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s, cudaEvent_t bready);
+void launch_mp_qkeys_all(const double* Bhr, const double* A, const double* Cg, long long N, long long R, int K,
+                         float* keys, cudaStream_t s);
+void launch_mp_qboxes_fact(const unsigned int* perm, const double* Bhr, const double* A, const double* Cg, long long N,
+                           long long R, int K, int ROWS, int QT, const unsigned int* qnmax, float* bmin, float* bmax,
+                           cudaStream_t s);
 // B[r][h] = E_h . Rel_r in FP64 (the pivot-independent part of the factorised keys)
 void launch_mp_hr(const float* E, const float* Rel, long long N, long long R, int d, double* B, cudaStream_t s);
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,

@@ -472,6 +472,7 @@ __global__ void __launch_bounds__(256) mp_ent_kernel(const float* __restrict__ X
                                                      unsigned int* xmax, unsigned int* nonfinite) {
     extern __shared__ __align__(16) double me_smem[];
     constexpr int KP = (K + 1) / 2 * 2;
+    constexpr int KC = KP <= 32 ? KP : 16;  // pivots per pass over the row (registers)
     double* Ps = me_smem;  // [d][KP], converted once per block
     for (int x = threadIdx.x; x < d * KP; x += blockDim.x) {
         const int i = x / KP, k = x - i * KP;
@@ -480,61 +481,75 @@ __global__ void __launch_bounds__(256) mp_ent_kernel(const float* __restrict__ X
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
-    float run_mn = FLT_MAX, run_mx = 0.f, run_x = 0.f;  // lane k: pivot k
+    float run_mn[(K + 31) / 32], run_mx[(K + 31) / 32];  // lane k % 32 of word k / 32: pivot k
+#pragma unroll
+    for (int z = 0; z < (K + 31) / 32; ++z) { run_mn[z] = FLT_MAX; run_mx[z] = 0.f; }
+    float run_x = 0.f;
     bool bad = false;
     const long long nblk = (n + blockDim.x - 1) / blockDim.x;
     for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
         const long long row = blk * blockDim.x + threadIdx.x;
         const bool rv = row < n;
         const float* xr = X + (rv ? row : 0) * d;
-        double acc[KP], xx = 0.0;
+        double xx = 0.0;
 #pragma unroll
-        for (int k = 0; k < KP; ++k) acc[k] = 0.0;
-        auto step = [&](float v, int i) {
-            bad |= !isfinite(v);
-            const double dv = (double)v;
-            xx = fma(dv, dv, xx);
-            const double2* pr = reinterpret_cast<const double2*>(Ps + i * KP);
+        for (int k0 = 0; k0 < KP; k0 += KC) {
+            double acc[KC];
 #pragma unroll
-            for (int k = 0; k < KP; k += 2) {
-                const double2 p2 = pr[k / 2];
-                const double t0 = dv - p2.x, t1 = dv - p2.y;
-                acc[k] = fma(t0, t0, acc[k]);
-                acc[k + 1] = fma(t1, t1, acc[k + 1]);
-            }
-        };
-        if (rv) {
-            if (vec) {
-                for (int i = 0; i < d; i += 4) {
-                    const float4 v = __ldg(reinterpret_cast<const float4*>(xr + i));
-                    step(v.x, i); step(v.y, i + 1); step(v.z, i + 2); step(v.w, i + 3);
+            for (int k = 0; k < KC; ++k) acc[k] = 0.0;
+            auto step = [&](float v, int i) {
+                if (k0 == 0) {
+                    bad |= !isfinite(v);
+                    xx = fma((double)v, (double)v, xx);
                 }
-            } else {
-                for (int i = 0; i < d; ++i) step(__ldg(xr + i), i);
+                const double dv = (double)v;
+                const double2* pr = reinterpret_cast<const double2*>(Ps + i * KP + k0);
+#pragma unroll
+                for (int k = 0; k < KC; k += 2) {
+                    const double2 p2 = pr[k / 2];
+                    const double t0 = dv - p2.x, t1 = dv - p2.y;
+                    acc[k] = fma(t0, t0, acc[k]);
+                    acc[k + 1] = fma(t1, t1, acc[k + 1]);
+                }
+            };
+            if (rv) {
+                if (vec) {
+                    for (int i = 0; i < d; i += 4) {
+                        const float4 v = __ldg(reinterpret_cast<const float4*>(xr + i));
+                        step(v.x, i); step(v.y, i + 1); step(v.z, i + 2); step(v.w, i + 3);
+                    }
+                } else {
+                    for (int i = 0; i < d; ++i) step(__ldg(xr + i), i);
+                }
             }
-        }
-        if (rv && A) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) A[row * K + k] = acc[k];
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const float key = key_sqrt(__double2float_rn(acc[k]));
-            if (rv && keys) keys[row * K + k] = key;
-            const unsigned bits = __float_as_uint(key);
-            const unsigned m = __reduce_min_sync(0xffffffffu, rv ? bits : 0x7f7fffffu);
-            const unsigned z = __reduce_max_sync(0xffffffffu, rv ? bits : 0u);
-            if (lane == k) {
-                run_mn = fminf(run_mn, __uint_as_float(m));
-                run_mx = fmaxf(run_mx, __uint_as_float(z));
+            for (int kk = 0; kk < KC; ++kk) {
+                const int k = k0 + kk;
+                if (k >= K) break;
+                if (rv && A) A[row * K + k] = acc[kk];
+                const float key = key_sqrt(__double2float_rn(acc[kk]));
+                if (rv && keys) keys[row * K + k] = key;
+                const unsigned bits = __float_as_uint(key);
+                const unsigned m = __reduce_min_sync(0xffffffffu, rv ? bits : 0x7f7fffffu);
+                const unsigned z = __reduce_max_sync(0xffffffffu, rv ? bits : 0u);
+                if (lane == (k & 31)) {
+                    run_mn[k >> 5] = fminf(run_mn[k >> 5], __uint_as_float(m));
+                    run_mx[k >> 5] = fmaxf(run_mx[k >> 5], __uint_as_float(z));
+                }
             }
         }
         if (rv) run_x = fmaxf(run_x, __double2float_ru(sqrt(xx) * (1.0 + 0x1p-40)));
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
-    if (minmax && lane < K) {
-        atomicMin(&minmax[2 * lane], __float_as_uint(run_mn));
-        atomicMax(&minmax[2 * lane + 1], __float_as_uint(run_mx));
+    if (minmax) {
+#pragma unroll
+        for (int z = 0; z < (K + 31) / 32; ++z) {
+            const int k = 32 * z + lane;
+            if (k < K) {
+                atomicMin(&minmax[2 * k], __float_as_uint(run_mn[z]));
+                atomicMax(&minmax[2 * k + 1], __float_as_uint(run_mx[z]));
+            }
+        }
     }
     if (xmax) {
         const unsigned z = __reduce_max_sync(0xffffffffu, __float_as_uint(run_x));
@@ -667,60 +682,61 @@ __global__ void mp_rel_terms_kernel(const float* __restrict__ Rel, long long R, 
     }
 }
 
-// Query keys from the factorisation: thread = entity h (its K values A[h][k] in registers),
-// loop over a chunk of relations: D~^2_k = (A[h][k] + (2 B[r][h] + ||r||^2)) - 2 r.p_k, key =
-// sqrtf(fl32(max(D~^2, 0))).  Writes are K contiguous floats per (r, h) row; per (relation,
-// pivot) min / max: warp REDUX, shared-memory atomics per block, one global atomic per block.
+// One L2 query key from the factorisation terms (the only place the formula is written, so
+// the materialised keys, the Hilbert keys and the boxes computed on the fly agree bit for bit).
+__device__ __forceinline__ float mp_key_l2(double a, double b2, double c) {
+    return key_sqrt(__double2float_rn(fmax((a + b2) - c, 0.0)));
+}
+
+// Query keys from the factorisation: thread = entity h (A[h][k] from L2), loop over a chunk of
+// relations: D~^2_k = (A[h][k] + (2 B[r][h] + ||r||^2)) - 2 r.p_k, key = mp_key_l2.  Writes the
+// first KO keys of every (r, h) row (KO = min(K, 4): the Hilbert-order pivots; KO = K: the full
+// keys, only for kgc_inspect), KO contiguous floats per row, and (optionally) per (relation,
+// pivot) key ranges for k < KO: warp REDUX, shared-memory atomics, one global atomic per block.
 constexpr int QK_RCH = 8;  // relations per block
-template <int K>
+template <int K, int KO>
 __global__ void __launch_bounds__(256) mp_qkeys_fact_kernel(const double* __restrict__ B, const double* __restrict__ A,
                                                             const double* __restrict__ Cg, long long N, long long R,
                                                             float* __restrict__ keys, unsigned int* minmax) {
-    __shared__ unsigned int smn[QK_RCH][K], smx[QK_RCH][K];
+    __shared__ unsigned int smn[QK_RCH][KO], smx[QK_RCH][KO];
     __shared__ double cs[QK_RCH][K + 1];
     const long long r0 = (long long)blockIdx.y * QK_RCH;
     const int nr = (int)min((long long)QK_RCH, R - r0);
-    for (int x = threadIdx.x; x < QK_RCH * K; x += blockDim.x) {
-        smn[x / K][x % K] = 0x7f7fffffu;
-        smx[x / K][x % K] = 0u;
+    for (int x = threadIdx.x; x < QK_RCH * KO; x += blockDim.x) {
+        smn[x / KO][x % KO] = 0x7f7fffffu;
+        smx[x / KO][x % KO] = 0u;
     }
     for (int x = threadIdx.x; x < nr * (K + 1); x += blockDim.x) cs[x / (K + 1)][x % (K + 1)] = Cg[r0 * (K + 1) + x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const bool hv = h < N;
-    double a[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) a[k] = hv ? __ldg(A + h * K + k) : 0.0;
     for (int u = 0; u < nr; ++u) {
         const long long r = r0 + u;
         const double b2 = 2.0 * (hv ? __ldg(B + r * N + h) : 0.0) + cs[u][K];
-        float* dst = keys + ((size_t)r * N + h) * K;
+        float* dst = keys + ((size_t)r * N + h) * KO;
 #pragma unroll
-        for (int k0 = 0; k0 < K; k0 += 4) {
+        for (int k0 = 0; k0 < KO; k0 += 4) {
             float kv[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int k = k0 + j;
-                kv[j] = k < K ? key_sqrt(__double2float_rn(fmax((a[k < K ? k : 0] + b2) - cs[u][k < K ? k : 0], 0.0)))
-                              : 0.f;
+                const int k = k0 + j < KO ? k0 + j : 0;
+                kv[j] = (k0 + j < KO && hv) ? mp_key_l2(__ldg(A + h * K + k), b2, cs[u][k]) : 0.f;
             }
             if (hv) {
-                if (K % 4 == 0) {
+                if (KO % 4 == 0) {
                     *reinterpret_cast<float4*>(dst + k0) = make_float4(kv[0], kv[1], kv[2], kv[3]);
                 } else {
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        if (k0 + j < K) dst[k0 + j] = kv[j];
+                        if (k0 + j < KO) dst[k0 + j] = kv[j];
                 }
             }
-            // per (relation, pivot) key range: only the first MP_SORT_PIVOTS pivots are quantised
-            // for the Hilbert order (mp_morton_kernel); nothing else reads the ranges
-            if (k0 < MP_SORT_PIVOTS) {
+            if (minmax && k0 < MP_SORT_PIVOTS) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int k = k0 + j;
-                    if (k < K && k < MP_SORT_PIVOTS) {
+                    if (k < KO && k < MP_SORT_PIVOTS) {
                         const unsigned bits = __float_as_uint(kv[j]);
                         const unsigned m = __reduce_min_sync(0xffffffffu, hv ? bits : 0x7f7fffffu);
                         const unsigned z = __reduce_max_sync(0xffffffffu, hv ? bits : 0u);
@@ -733,13 +749,72 @@ __global__ void __launch_bounds__(256) mp_qkeys_fact_kernel(const double* __rest
             }
         }
     }
+    if (!minmax) return;
     __syncthreads();
-    for (int x = threadIdx.x; x < nr * K; x += blockDim.x) {
-        const int u = x / K, k = x % K;
-        atomicMin(&minmax[((r0 + u) * K + k) * 2], smn[u][k]);
-        atomicMax(&minmax[((r0 + u) * K + k) * 2 + 1], smx[u][k]);
+    for (int x = threadIdx.x; x < nr * KO; x += blockDim.x) {
+        const int u = x / KO, k = x % KO;
+        atomicMin(&minmax[((r0 + u) * KO + k) * 2], smn[u][k]);
+        atomicMax(&minmax[((r0 + u) * KO + k) * 2 + 1], smx[u][k]);
     }
 }
+
+// Query-tile boxes straight from the factorisation terms (no materialised query keys: c5 at 64
+// pivots would need 25.6 GB of them): one warp per query tile, lanes over PIVOTS (lane k holds
+// pivot k, k + 32), rows of the tile one after the other (h = qperm; each row's A[h][.] is one
+// coalesced read).  The key is monotone in D~^2 (fl32 rounding, the clamp at 0 and sqrt are), so
+// the box is the key of the min / max FP64 D~^2 -- two conversions and square roots per (tile,
+// pivot) instead of one per (row, pivot); widened by delta_r (qnmax[r] 2^-23).
+template <int K>
+__global__ void mp_qboxes_fact_kernel(const unsigned int* __restrict__ perm, const double* __restrict__ B,
+                                      const double* __restrict__ A, const double* __restrict__ Cg, long long N,
+                                      long long R, int ROWS, int QT, const unsigned int* __restrict__ qnmax,
+                                      float* __restrict__ bmin, float* __restrict__ bmax) {
+    constexpr int KL = (K + 31) / 32;  // pivots per lane
+    const int lane = threadIdx.x & 31;
+    const long long nt = R * QT;
+    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < nt;
+         w += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const long long r = w / QT, tl = w - r * QT;
+        const long long b = tl * ROWS, e = min(N, b + ROWS);
+        const double* cr = Cg + r * (K + 1);
+        const double rr = __ldg(cr + K);
+        double c[KL], lo[KL], hi[KL];
+#pragma unroll
+        for (int j = 0; j < KL; ++j) {
+            const int k = lane + 32 * j;
+            c[j] = k < K ? __ldg(cr + k) : 0.0;
+            lo[j] = 1e300;
+            hi[j] = -1e300;
+        }
+        const unsigned int* pr = perm + r * N;
+        const double* br = B + r * N;
+#pragma unroll 4
+        for (long long i = b; i < e; ++i) {
+            const long long h = __ldg(pr + i);
+            const double b2 = 2.0 * __ldg(br + h) + rr;
+            const double* ah = A + h * K;
+#pragma unroll
+            for (int j = 0; j < KL; ++j) {
+                const int k = lane + 32 * j;
+                if (k < K) {
+                    const double q2 = (__ldg(ah + k) + b2) - c[j];  // the operation order of mp_key_l2
+                    lo[j] = fmin(lo[j], q2);
+                    hi[j] = fmax(hi[j], q2);
+                }
+            }
+        }
+        const float m = __fmul_ru(__uint_as_float(qnmax[r]), 1.1920928955078125e-07f);  // 2^-23
+#pragma unroll
+        for (int j = 0; j < KL; ++j) {
+            const int k = lane + 32 * j;
+            if (k < K && e > b) {
+                bmin[w * K + k] = __fsub_rd(key_sqrt(__double2float_rn(fmax(lo[j], 0.0))), m);
+                bmax[w * K + k] = __fadd_ru(key_sqrt(__double2float_rn(fmax(hi[j], 0.0))), m);
+            }
+        }
+    }
+}
+
 
 __global__ void mp_init_minmax_kernel(unsigned int* mm, long long n, unsigned int* qnmax, long long nseg) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -828,50 +903,54 @@ __global__ void mp_morton_kernel(const float* __restrict__ keys, const unsigned 
 __global__ void mp_boxes_kernel(const float* __restrict__ keys, const unsigned int* __restrict__ perm, long long nseg,
                                 long long L, int ROWS, int ntile, int K, float* __restrict__ bmin,
                                 float* __restrict__ bmax, const unsigned int* __restrict__ qnmax, int transpose) {
+    constexpr int KC = 16;  // pivots per pass over the tile's rows (registers)
     const int lane = threadIdx.x & 31;
     const long long nt = nseg * ntile;
     for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < nt;
          w += ((long long)gridDim.x * blockDim.x) >> 5) {
         const long long s = w / ntile, tl = w - s * ntile;
         const long long b = tl * ROWS, e = min(L, b + ROWS);
-        float mn[MP_MAX], mx[MP_MAX];
+        for (int k0 = 0; k0 < K; k0 += KC) {
+            float mn[KC], mx[KC];
 #pragma unroll
-        for (int k = 0; k < MP_MAX; ++k) { mn[k] = FLT_MAX; mx[k] = -FLT_MAX; }
-        for (long long i = b + lane; i < e; i += 32) {
-            const float* kr = keys + ((size_t)s * L + perm[s * L + i]) * K;
-            if ((K & 3) == 0) {  // 16-byte rows: one float4 per 4 pivots
+            for (int k = 0; k < KC; ++k) { mn[k] = FLT_MAX; mx[k] = -FLT_MAX; }
+            for (long long i = b + lane; i < e; i += 32) {
+                const float* kr = keys + ((size_t)s * L + perm[s * L + i]) * K + k0;
+                if ((K & 3) == 0) {  // 16-byte rows: one float4 per 4 pivots
 #pragma unroll
-                for (int k = 0; k < MP_MAX; k += 4)
-                    if (k < K) {
-                        const float4 v = __ldg(reinterpret_cast<const float4*>(kr + k));
-                        mn[k] = fminf(mn[k], v.x); mx[k] = fmaxf(mx[k], v.x);
-                        mn[k + 1] = fminf(mn[k + 1], v.y); mx[k + 1] = fmaxf(mx[k + 1], v.y);
-                        mn[k + 2] = fminf(mn[k + 2], v.z); mx[k + 2] = fmaxf(mx[k + 2], v.z);
-                        mn[k + 3] = fminf(mn[k + 3], v.w); mx[k + 3] = fmaxf(mx[k + 3], v.w);
-                    }
-            } else {
+                    for (int k = 0; k < KC; k += 4)
+                        if (k0 + k < K) {
+                            const float4 v = __ldg(reinterpret_cast<const float4*>(kr + k));
+                            mn[k] = fminf(mn[k], v.x); mx[k] = fmaxf(mx[k], v.x);
+                            mn[k + 1] = fminf(mn[k + 1], v.y); mx[k + 1] = fmaxf(mx[k + 1], v.y);
+                            mn[k + 2] = fminf(mn[k + 2], v.z); mx[k + 2] = fmaxf(mx[k + 2], v.z);
+                            mn[k + 3] = fminf(mn[k + 3], v.w); mx[k + 3] = fmaxf(mx[k + 3], v.w);
+                        }
+                } else {
 #pragma unroll
-                for (int k = 0; k < MP_MAX; ++k)
-                    if (k < K) { mn[k] = fminf(mn[k], kr[k]); mx[k] = fmaxf(mx[k], kr[k]); }
+                    for (int k = 0; k < KC; ++k)
+                        if (k0 + k < K) { mn[k] = fminf(mn[k], kr[k]); mx[k] = fmaxf(mx[k], kr[k]); }
+                }
             }
-        }
 #pragma unroll
-        for (int k = 0; k < MP_MAX; ++k) {
-            if (k < K) {
-                float a = mn[k], z = mx[k];
-                for (int o = 16; o > 0; o >>= 1) {
-                    a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
-                    z = fmaxf(z, __shfl_xor_sync(0xffffffffu, z, o));
-                }
-                if (qnmax) {
-                    const float m = __fmul_ru(__uint_as_float(qnmax[s]), 1.1920928955078125e-07f);  // 2^-23
-                    a = __fsub_rd(a, m);
-                    z = __fadd_ru(z, m);
-                }
-                if (lane == 0) {
-                    const long long o = transpose ? k * nt + w : w * K + k;
-                    bmin[o] = a;
-                    bmax[o] = z;
+            for (int kk = 0; kk < KC; ++kk) {
+                const int k = k0 + kk;
+                if (k < K) {
+                    float a = mn[kk], z = mx[kk];
+                    for (int o = 16; o > 0; o >>= 1) {
+                        a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+                        z = fmaxf(z, __shfl_xor_sync(0xffffffffu, z, o));
+                    }
+                    if (qnmax) {
+                        const float m = __fmul_ru(__uint_as_float(qnmax[s]), 1.1920928955078125e-07f);  // 2^-23
+                        a = __fsub_rd(a, m);
+                        z = __fadd_ru(z, m);
+                    }
+                    if (lane == 0) {
+                        const long long o = transpose ? k * nt + w : w * K + k;
+                        bmin[o] = a;
+                        bmax[o] = z;
+                    }
                 }
             }
         }
@@ -906,42 +985,60 @@ __device__ __forceinline__ bool mp_survives(const float* qmn, const float* qmx, 
 }
 
 // One warp per query tile, lanes over tail tiles; the block's 16 query tiles share the tail
-// boxes, staged in shared memory in chunks of MC_CT tail tiles ([pivot][tile]: consecutive lanes
-// read consecutive words) -- the per-lane global loads of the boxes (a dependent L2 round trip
-// per 32 tail tiles) made the 32-pivot test latency-bound.
-constexpr int MC_CT = 128, MC_W = 16;
+// boxes, staged in shared memory in chunks of CT = 4096 / K tail tiles ([pivot][tile]: consecutive
+// lanes read consecutive words), and each warp's query box sits in shared memory too (up to 64
+// pivots) -- the per-lane global loads of the boxes (a dependent L2 round trip per 32 tail tiles)
+// made the many-pivot test latency-bound.
+constexpr int MC_W = 16;
 __global__ void __launch_bounds__(32 * MC_W) mp_count_kernel(const float* __restrict__ qbmin,
                                                              const float* __restrict__ qbmax,
                                                              const float* __restrict__ tbmin,
                                                              const float* __restrict__ tbmax, long long nq, int TT,
                                                              int K, float theta, float relm, int prune, int2* ranges,
                                                              long long* cost, unsigned int* __restrict__ bits) {
-    __shared__ float sbn[MP_MAX][MC_CT], sbx[MP_MAX][MC_CT];
+    extern __shared__ float mc_smem[];
+    const int CT = 4096 / K / 32 * 32;                 // tail tiles per chunk (a multiple of 32)
+    float* sbn = mc_smem;                              // [K][CT]
+    float* sbx = sbn + K * CT;                         // [K][CT]
+    float* sq = sbx + K * CT;                          // [MC_W][2][K] query boxes
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int TW = (TT + 31) >> 5;
+    float* qmn = sq + w * 2 * K;
+    float* qmx = qmn + K;
     for (long long qb = (long long)blockIdx.x * MC_W; qb < nq; qb += (long long)gridDim.x * MC_W) {
         const long long q = qb + w;
         const bool qv = q < nq;
-        float qmn[MP_MAX], qmx[MP_MAX];
-#pragma unroll
-        for (int k = 0; k < MP_MAX; ++k)
-            if (k < K) { qmn[k] = qv ? qbmin[q * K + k] : 0.f; qmx[k] = qv ? qbmax[q * K + k] : 0.f; }
+        for (int k = lane; k < K; k += 32) {
+            qmn[k] = qv ? qbmin[q * K + k] : 0.f;
+            qmx[k] = qv ? qbmax[q * K + k] : 0.f;
+        }
+        __syncwarp();
         int c = 0;
         if (prune) {
-            for (int j0 = 0; j0 < TT; j0 += MC_CT) {
+            for (int j0 = 0; j0 < TT; j0 += CT) {
                 __syncthreads();  // the previous chunk is consumed
-                for (int x = threadIdx.x; x < K * MC_CT; x += blockDim.x) {
-                    const int k = x / MC_CT, jj = x - k * MC_CT;
+                for (int x = threadIdx.x; x < K * CT; x += blockDim.x) {
+                    const int k = x / CT, jj = x - k * CT;
                     const bool in = j0 + jj < TT;
-                    sbn[k][jj] = in ? tbmin[(size_t)k * TT + j0 + jj] : 0.f;
-                    sbx[k][jj] = in ? tbmax[(size_t)k * TT + j0 + jj] : 0.f;
+                    sbn[x] = in ? tbmin[(size_t)k * TT + j0 + jj] : 0.f;
+                    sbx[x] = in ? tbmax[(size_t)k * TT + j0 + jj] : 0.f;
                 }
                 __syncthreads();
                 if (!qv) continue;
-                for (int jj0 = 0; jj0 < MC_CT && j0 + jj0 < TT; jj0 += 32) {
+                for (int jj0 = 0; jj0 < CT && j0 + jj0 < TT; jj0 += 32) {
                     const int jj = jj0 + lane;
-                    const bool ok = j0 + jj < TT && mp_survives<MP_MAX>(qmn, qmx, &sbn[0][jj], &sbx[0][jj], K, theta,
-                                                                       relm, MC_CT);
+                    bool ok = j0 + jj < TT;
+                    // pivots in groups of 8, the lane stops at the first group that fails
+                    for (int k0 = 0; k0 < K && ok; k0 += 8) {
+#pragma unroll
+                        for (int k = k0; k < k0 + 8; ++k) {
+                            if (k < K) {
+                                const float tz = sbx[k * CT + jj], ta = sbn[k * CT + jj];
+                                const float th = theta * (1.0f + 6.103515625e-05f) + relm * (fabsf(qmx[k]) + fabsf(tz));
+                                ok &= !(tz < qmn[k] - th || ta > qmx[k] + th);
+                            }
+                        }
+                    }
                     const unsigned m = __ballot_sync(0xffffffffu, ok);
                     c += __popc(m);
                     if (bits && lane == 0) bits[q * TW + ((j0 + jj0) >> 5)] = m;  // mp_emit expands these
@@ -954,9 +1051,13 @@ __global__ void __launch_bounds__(32 * MC_W) mp_count_kernel(const float* __rest
             ranges[q] = make_int2(0, c - 1);  // positions in this query tile's list
             cost[q] = c;
         }
+        __syncwarp();
     }
 }
 
+// MASKS: expand mp_count's survival masks (the usual case, few registers); else repeat the box
+// tests (masks past 2 GiB).
+template <bool MASKS>
 __global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __restrict__ qbmax,
                                const float* __restrict__ tbmin, const float* __restrict__ tbmax,
                                const long long* __restrict__ cum, const DevCounters* ctr, int TT, int K, float theta,
@@ -965,7 +1066,7 @@ __global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __r
     if (tq0 >= tq1) return;
     const long long base = cum[tq0];
     const int lane = threadIdx.x & 31;
-    if (bits) {  // the survival masks mp_count wrote: expand, no second pass over the boxes
+    if (MASKS) {  // the survival masks mp_count wrote: expand, no second pass over the boxes
         const int TW = (TT + 31) >> 5;
         for (long long q = tq0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); q < tq1;
              q += ((long long)gridDim.x * blockDim.x) >> 5) {
@@ -1411,9 +1512,13 @@ void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, con
     kern<<<1, 1024, smem, s>>>(E, N, d, K, (int)S, p0, P);
 }
 
-// K dispatch for the key kernels: 2..8, 12, 16, 24, 32 pivots (mp_pivots_ok)
-template <class F>
+// K dispatch for the key kernels: 2..8, 12, 16, 24, 32 pivots, and 48, 64 for the L2 path (mp_pivots_ok)
+template <int KMAX = 32, class F>
 static void for_pivots(int K, F&& f) {
+    if constexpr (KMAX >= 48) {
+        if (K == 48) { f(std::integral_constant<int, 48>{}); return; }
+        if (K == 64) { f(std::integral_constant<int, 64>{}); return; }
+    }
     switch (K) {
         case 2: f(std::integral_constant<int, 2>{}); break;
         case 3: f(std::integral_constant<int, 3>{}); break;
@@ -1507,13 +1612,12 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
 // L2 keys by the factorisation (see mp_qkeys_fact_kernel): tails (Et, NT) and queries
 // (E + Rel, N x R), both FP64.  A (N x K doubles) and hmax (one word) are scratch.
 void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long R, const float* Et, long long NT,
-                        int d, int K, const float* P, float* tkeys, unsigned int* tminmax, float* qkeys,
-                        unsigned int* qminmax, unsigned int* qnmax, double* A, double* Bhr, double* Cg,
-                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s, cudaStream_t aux,
-                        cudaEvent_t* ev_fork) {
-    (void)aux;
+                        int d, int K, const float* P, float* tkeys, unsigned int* tminmax, float* qkeys4,
+                        unsigned int* qmm4, unsigned int* qnmax, double* A, double* Bhr, double* Cg,
+                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s, cudaEvent_t bready) {
+    const int KO = K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS;
     mp_init_minmax_kernel<<<grid_for_mp(K, 256), 256, 0, s>>>(tminmax, K, nullptr, 0);
-    mp_init_minmax_kernel<<<grid_for_mp(R * K, 256), 256, 0, s>>>(qminmax, R * K, qnmax, R);
+    mp_init_minmax_kernel<<<grid_for_mp(R * KO, 256), 256, 0, s>>>(qmm4, R * KO, qnmax, R);
     cudaMemsetAsync(hmax, 0, 4, s);
     const size_t esm = (size_t)((K + 1) / 2 * 2) * d * 8;
     auto ent = [&](auto kern, const float* X, long long n, double* a, float* keys, unsigned int* mm, unsigned int* xm) {
@@ -1522,6 +1626,7 @@ void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long
     };
     auto byK = [&](auto k_) {
         constexpr int KK = decltype(k_)::value;
+        constexpr int KOO = KK < MP_SORT_PIVOTS ? KK : MP_SORT_PIVOTS;
         const bool same = Et == E && NT == N;
         if (same) {
             ent(mp_ent_kernel<KK>, E, N, A, tkeys, tminmax, hmax);
@@ -1531,11 +1636,31 @@ void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long
         }
         mp_rel_terms_kernel<<<(unsigned)std::min<long long>(148LL * 4, (R * (KK + 1) + 7) / 8), 256, 0, s>>>(
             Rel, R, d, KK, P, Cg, hmax, qnmax, nonfinite);
-        cudaStreamWaitEvent(s, ev_fork[1], 0);  // B from the aux stream (launch_mp_hr)
+        cudaStreamWaitEvent(s, bready, 0);  // B from the aux stream (launch_mp_hr)
         dim3 gk((unsigned)((N + 255) / 256), (unsigned)((R + QK_RCH - 1) / QK_RCH));
-        mp_qkeys_fact_kernel<KK><<<gk, 256, 0, s>>>(Bhr, A, Cg, N, R, qkeys, qminmax);
+        mp_qkeys_fact_kernel<KK, KOO><<<gk, 256, 0, s>>>(Bhr, A, Cg, N, R, qkeys4, qmm4);
     };
-    for_pivots(K, byK);
+    for_pivots<64>(K, byK);
+}
+
+// The full K query keys per (r, h) (kgc_inspect only: the join itself never materialises them).
+void launch_mp_qkeys_all(const double* Bhr, const double* A, const double* Cg, long long N, long long R, int K,
+                         float* keys, cudaStream_t s) {
+    for_pivots<64>(K, [&](auto k_) {
+        constexpr int KK = decltype(k_)::value;
+        dim3 gk((unsigned)((N + 255) / 256), (unsigned)((R + QK_RCH - 1) / QK_RCH));
+        mp_qkeys_fact_kernel<KK, KK><<<gk, 256, 0, s>>>(Bhr, A, Cg, N, R, keys, nullptr);
+    });
+}
+
+void launch_mp_qboxes_fact(const unsigned int* perm, const double* Bhr, const double* A, const double* Cg, long long N,
+                           long long R, int K, int ROWS, int QT, const unsigned int* qnmax, float* bmin, float* bmax,
+                           cudaStream_t s) {
+    for_pivots<64>(K, [&](auto k_) {
+        constexpr int KK = decltype(k_)::value;
+        mp_qboxes_fact_kernel<KK><<<grid_for_mp(R * QT * 32, 256), 256, 0, s>>>(perm, Bhr, A, Cg, N, R, ROWS, QT, qnmax,
+                                                                              bmin, bmax);
+    });
 }
 
 void launch_mp_hr(const float* E, const float* Rel, long long N, long long R, int d, double* B, cudaStream_t s) {
@@ -1561,16 +1686,20 @@ void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg
 void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,
                      int TT, int K, float theta, float relm, int prune, int2* ranges, long long* cost, unsigned int* bits,
                      cudaStream_t s) {
-    mp_count_kernel<<<grid_for_mp(nq, MC_W, 148LL * 16), 32 * MC_W, 0, s>>>(qbmin, qbmax, tbmin, tbmax, nq, TT, K,
-                                                                          theta, relm, prune, ranges, cost,
-                                                                          prune ? bits : nullptr);
+    const int CT = 4096 / K / 32 * 32;
+    const size_t smem = (size_t)(2 * K * CT + MC_W * 2 * K) * 4;
+    cudaFuncSetAttribute(mp_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    mp_count_kernel<<<grid_for_mp(nq, MC_W, 148LL * 16), 32 * MC_W, smem, s>>>(qbmin, qbmax, tbmin, tbmax, nq, TT, K,
+                                                                             theta, relm, prune, ranges, cost,
+                                                                             prune ? bits : nullptr);
 }
 
 void launch_mp_emit(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax,
                     const long long* cum, const DevCounters* ctr, long long nq, int TT, int K, float theta, float relm,
                     int prune, int* list, const unsigned int* bits, cudaStream_t s) {
-    mp_emit_kernel<<<grid_for_mp(nq * 32, 256), 256, 0, s>>>(qbmin, qbmax, tbmin, tbmax, cum, ctr, TT, K, theta, relm, prune,
-                                                         list, prune ? bits : nullptr);
+    auto kern = (prune && bits) ? mp_emit_kernel<true> : mp_emit_kernel<false>;
+    kern<<<grid_for_mp(nq * 32, 256), 256, 0, s>>>(qbmin, qbmax, tbmin, tbmax, cum, ctr, TT, K, theta, relm, prune, list,
+                                                  prune ? bits : nullptr);
 }
 
 void launch_stage_rows(const float* E, const int* tperm, const float* keys, long long N, int d, int Kpad, int K,

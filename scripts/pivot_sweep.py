@@ -17,7 +17,7 @@ from paper_2307_12059_b200 import kgc  # noqa: E402
 from synth import generate_config  # noqa: E402
 
 name, hit = sys.argv[1], float(sys.argv[2])
-KMAX = 32
+KMAX = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 th = json.loads((ROOT / "configs" / "thresholds.json").read_text())[name][f"L2@{hit:g}"]["theta"]
 E, Rel = generate_config(name)
 N, R, d = E.shape[0], Rel.shape[0], E.shape[1]
@@ -60,7 +60,7 @@ def boxes(sk, rows):
 tp = torch.from_numpy(tperm.astype(np.int64)).cuda()
 tmn, tmx = boxes(kt[tp], BT)
 out = {"config": name, "hit": hit, "lib_tile_pairs": st["tile_pairs_surviving"], "tiles": f"{BQ}x{BT}"}
-Ks = [4, 8, 12, 16, 20, 24, 32]
+Ks = [k for k in (4, 8, 12, 16, 20, 24, 32, 40, 48, 64) if k <= KMAX]
 surv = {K: 0 for K in Ks}
 for r in range(R):
     kq = (A + 2 * HR[:, r:r + 1] - 2 * C[r][None] + rr[r]).clamp_min(0).sqrt()  # [N, 16]
