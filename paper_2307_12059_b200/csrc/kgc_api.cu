@@ -722,18 +722,22 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         const char* kde = kgc_knob("KGC_KD");  // local kd refinement of both orders (experiment knob)
         const bool kd = kde ? atoi(kde) != 0 : false;
         if (kd) launch_kd_refine(P<float>(ctx->mpkt), P<int>(ctx->tperm), 1, NT, K, s);
-        if (norm == 2)  // the Hilbert pivots' keys (the rest are computed on the fly by the boxes)
-            launch_mp_morton(P<float>(ctx->mpk4), P<unsigned>(ctx->mpmm4), R, N, K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS,
-                             bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
-        else
-            launch_mp_morton(P<float>(ctx->mpkq), P<unsigned>(ctx->mpmm_q), R, N, K, bits,
-                             P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
-        LAUNCHED(1);
-        radix_sort_u64_segments(R, N, code_bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
-                                P<unsigned long long>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
-                                ctx->scan_tmp.p, s, &ctx->launches);
-        LAUNCHED(0);
-        CK(cudaMemcpyAsync(ctx->qperm.p, ctx->sv0.p, NR * 4, cudaMemcpyDeviceToDevice, s));
+        // the Hilbert pivots' keys (L2: the first 4 from the factorisation; the rest are computed
+        // on the fly by the boxes; L1: the materialised keys)
+        const float* qk4 = norm == 2 ? P<float>(ctx->mpk4) : P<float>(ctx->mpkq);
+        const unsigned* qmm4 = norm == 2 ? P<unsigned>(ctx->mpmm4) : P<unsigned>(ctx->mpmm_q);
+        const int qks = norm == 2 ? (K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS) : K;
+        if (launch_mp_sort_small(qk4, qmm4, R, N, qks, bits, P<int>(ctx->qperm), s)) {  // short segments (c3)
+            LAUNCHED(1);
+        } else {
+            launch_mp_morton(qk4, qmm4, R, N, qks, bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
+            LAUNCHED(1);
+            radix_sort_u64_segments(R, N, code_bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
+                                    P<unsigned long long>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
+                                    ctx->scan_tmp.p, s, &ctx->launches);
+            LAUNCHED(0);
+            CK(cudaMemcpyAsync(ctx->qperm.p, ctx->sv0.p, NR * 4, cudaMemcpyDeviceToDevice, s));
+        }
         if (kd && norm == 1) launch_kd_refine(P<float>(ctx->mpkq), P<int>(ctx->qperm), R, N, K, s);
         CK(cudaEventRecord(ctx->ev[EV_SORT], s));
         // ---- a4: K-dim tile boxes and the L_inf test of every tile pair

@@ -164,6 +164,8 @@ void launch_mp_qboxes_fact(const unsigned int* perm, const double* Bhr, const do
                            cudaStream_t s);
 // B[r][h] = E_h . Rel_r in FP64 (the pivot-independent part of the factorised keys)
 void launch_mp_hr(const float* E, const float* Rel, long long N, long long R, int d, double* B, cudaStream_t s);
+bool launch_mp_sort_small(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
+                          int* perm, cudaStream_t s);
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
                       unsigned long long* code, unsigned int* idx, cudaStream_t s);
 void launch_kd_refine(const float* keys, int* perm, long long nseg, long long L, int K, cudaStream_t s);

@@ -827,66 +827,169 @@ __global__ void mp_init_minmax_kernel(unsigned int* mm, long long n, unsigned in
 }
 
 // -------------------------------------------------------------- Morton
+// The sort code of one row from its first MP_SORT_PIVOTS keys: quantised to `bits` per pivot over
+// the segment's key range, Hilbert order (Skilling's axes-to-transpose: Gray code + rotations,
+// then the bit interleave) or Morton order.
+__device__ __forceinline__ unsigned long long mp_code(const float* __restrict__ kr, const unsigned int* __restrict__ mm,
+                                                      int K, int bits, int hilbert) {
+    const float scale_max = (float)((1u << bits) - 1);
+    unsigned q[MP_SORT_PIVOTS];
+#pragma unroll
+    for (int k = 0; k < MP_SORT_PIVOTS; ++k) {
+        q[k] = 0;
+        if (k < K) {
+            const float lo = __uint_as_float(mm[k * 2]);
+            const float hi = __uint_as_float(mm[k * 2 + 1]);
+            const float rg = hi - lo;
+            if (rg > 0.f) {
+                float x = (kr[k] - lo) / rg * scale_max;
+                x = fminf(fmaxf(x, 0.f), scale_max);
+                q[k] = (unsigned)x;
+            }
+        }
+    }
+    const int Ks = K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS;  // order by the first pivots only
+    if (hilbert && Ks > 1) {
+        // consecutive Hilbert codes are adjacent cells, so tiles are more compact
+        const unsigned M = 1u << (bits - 1);
+        for (unsigned Q = M; Q > 1; Q >>= 1) {
+            const unsigned P = Q - 1;
+#pragma unroll
+            for (int k = 0; k < MP_SORT_PIVOTS; ++k) {
+                if (k >= Ks) continue;
+                if (q[k] & Q) {
+                    q[0] ^= P;
+                } else {
+                    const unsigned tt = (q[0] ^ q[k]) & P;
+                    q[0] ^= tt;
+                    q[k] ^= tt;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 1; k < MP_SORT_PIVOTS; ++k)
+            if (k < Ks) q[k] ^= q[k - 1];
+        unsigned tt = 0;
+        for (unsigned Q = M; Q > 1; Q >>= 1)
+            if (q[Ks - 1] & Q) tt ^= Q - 1;
+#pragma unroll
+        for (int k = 0; k < MP_SORT_PIVOTS; ++k)
+            if (k < Ks) q[k] ^= tt;
+    }
+    unsigned long long c = 0;
+    for (int b = bits - 1; b >= 0; --b)
+#pragma unroll
+        for (int k = 0; k < MP_SORT_PIVOTS; ++k)
+            if (k < Ks) c = (c << 1) | ((q[k] >> b) & 1u);
+    return c;
+}
+
 __global__ void mp_morton_kernel(const float* __restrict__ keys, const unsigned int* __restrict__ minmax, long long nseg,
                                  long long L, int K, int bits, unsigned long long* __restrict__ code,
                                  unsigned int* __restrict__ idx, int hilbert) {
     const long long n = nseg * L;
-    const float scale_max = (float)((1u << bits) - 1);
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
         const long long s = t / L, i = t - s * L;
-        unsigned q[MP_SORT_PIVOTS];
-#pragma unroll
-        for (int k = 0; k < MP_SORT_PIVOTS; ++k) {
-            q[k] = 0;
-            if (k < K) {
-                const float lo = __uint_as_float(minmax[(s * K + k) * 2]);
-                const float hi = __uint_as_float(minmax[(s * K + k) * 2 + 1]);
-                const float rg = hi - lo;
-                if (rg > 0.f) {
-                    float x = (keys[t * K + k] - lo) / rg * scale_max;
-                    x = fminf(fmaxf(x, 0.f), scale_max);
-                    q[k] = (unsigned)x;
-                }
-            }
-        }
-        const int Ks = K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS;  // order by the first pivots only
-        if (hilbert && Ks > 1) {
-            // Hilbert instead of Morton order: Skilling's axes-to-transpose on the quantised
-            // coordinates (Gray code + rotations), then the same bit interleave gives the Hilbert
-            // index -- consecutive codes are adjacent cells, so tiles are more compact
-            const unsigned M = 1u << (bits - 1);
-            for (unsigned Q = M; Q > 1; Q >>= 1) {
-                const unsigned P = Q - 1;
-#pragma unroll
-                for (int k = 0; k < MP_SORT_PIVOTS; ++k) {
-                    if (k >= Ks) continue;
-                    if (q[k] & Q) {
-                        q[0] ^= P;
-                    } else {
-                        const unsigned tt = (q[0] ^ q[k]) & P;
-                        q[0] ^= tt;
-                        q[k] ^= tt;
-                    }
-                }
-            }
-#pragma unroll
-            for (int k = 1; k < MP_SORT_PIVOTS; ++k)
-                if (k < Ks) q[k] ^= q[k - 1];
-            unsigned tt = 0;
-            for (unsigned Q = M; Q > 1; Q >>= 1)
-                if (q[Ks - 1] & Q) tt ^= Q - 1;
-#pragma unroll
-            for (int k = 0; k < MP_SORT_PIVOTS; ++k)
-                if (k < Ks) q[k] ^= tt;
-        }
-        unsigned long long c = 0;
-        for (int b = bits - 1; b >= 0; --b)
-#pragma unroll
-            for (int k = 0; k < MP_SORT_PIVOTS; ++k)
-                if (k < Ks) c = (c << 1) | ((q[k] >> b) & 1u);
-        code[t] = c;
+        code[t] = mp_code(keys + t * K, minmax + s * K * 2, K, bits, hilbert);
         idx[t] = (unsigned)i;
     }
+}
+
+// Short segments (L <= MS_L): code and stable LSD sort of a whole segment in one CTA's shared
+// memory (32-bit codes and 16-bit row indices, 8-bit digits, per-warp digit ranks by
+// match_any) -- instead of a global code array and 4 x (histogram, scan, scatter) launches.  Same
+// order as the multi-kernel path (stable by code, ties by index).  c3: 1345 segments of 14951.
+constexpr int MS_L = 16384, MS_NT = 512;
+__global__ void __launch_bounds__(MS_NT) mp_sort_small_kernel(const float* __restrict__ keys,
+                                                              const unsigned int* __restrict__ minmax, long long L,
+                                                              int K, int bits, int hilbert, int* __restrict__ perm) {
+    extern __shared__ __align__(16) unsigned int ms_smem[];
+    constexpr int NW = MS_NT / 32;
+    unsigned int* ka = ms_smem;                                        // [L] codes
+    unsigned int* kb = ka + L;                                         // [L]
+    int* hist = reinterpret_cast<int*>(kb + L);                        // [256]
+    int* wcnt = hist + 256;                                            // [NW][257]
+    unsigned short* va = reinterpret_cast<unsigned short*>(wcnt + NW * 257);  // [L] indices
+    unsigned short* vb = va + L;                                       // [L]
+    const long long s = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int Ks = K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS;
+    for (int i = tid; i < L; i += MS_NT) {
+        ka[i] = (unsigned)mp_code(keys + (s * L + i) * K, minmax + s * K * 2, K, bits, hilbert);
+        va[i] = (unsigned short)i;
+    }
+    const int passes = (bits * Ks + 7) / 8;
+    for (int pass = 0; pass < passes; ++pass) {
+        const unsigned int* src = (pass & 1) ? kb : ka;
+        unsigned int* dst = (pass & 1) ? ka : kb;
+        const unsigned short* vs = (pass & 1) ? vb : va;
+        unsigned short* vd = (pass & 1) ? va : vb;
+        const int shift = 8 * pass;
+        if (tid < 256) hist[tid] = 0;
+        __syncthreads();
+        for (int i = tid; i < L; i += MS_NT) atomicAdd(&hist[(src[i] >> shift) & 255u], 1);
+        __syncthreads();
+        if (w == 0) {  // exclusive scan of the 256 bins
+            int v[8], t = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { v[u] = hist[lane * 8 + u]; t += v[u]; }
+            int incl = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int run = incl - t;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { hist[lane * 8 + u] = run; run += v[u]; }
+        }
+        __syncthreads();
+        for (int base = 0; base < L; base += MS_NT) {
+            const int i = base + tid;
+            const bool valid = i < L;
+            const unsigned int x = valid ? src[i] : 0u;
+            const unsigned short xv = valid ? vs[i] : 0;
+            const int dg = valid ? (int)((x >> shift) & 255u) : 256;
+            for (int z = tid; z < NW * 257; z += MS_NT) wcnt[z] = 0;
+            __syncthreads();
+            const unsigned peers = __match_any_sync(0xffffffffu, dg);
+            const int lrank = __popc(peers & lanemask_lt());
+            if (valid && lrank == 0) wcnt[w * 257 + dg] = __popc(peers);
+            __syncthreads();
+            if (tid < 256) {  // per digit: warp offsets in warp order, then advance the running offset
+                int run = hist[tid];
+#pragma unroll
+                for (int ww = 0; ww < NW; ++ww) {
+                    const int c = wcnt[ww * 257 + tid];
+                    wcnt[ww * 257 + tid] = run;
+                    run += c;
+                }
+                hist[tid] = run;
+            }
+            __syncthreads();
+            if (valid) {
+                const int o = wcnt[w * 257 + dg] + lrank;
+                dst[o] = x;
+                vd[o] = xv;
+            }
+            __syncthreads();
+        }
+    }
+    const unsigned short* vf = (passes & 1) ? vb : va;
+    for (int i = tid; i < L; i += MS_NT) perm[s * L + i] = (int)vf[i];
+}
+
+// Sort order of nseg segments of L rows by their code; true when the short-segment kernel did it
+// (perm written), false when the caller must run the global code + radix path.
+bool launch_mp_sort_small(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
+                          int* perm, cudaStream_t s) {
+    if (L > MS_L || L < 1) return false;
+    const char* e = kgc_knob("KGC_HILBERT");
+    const int hilbert = e ? atoi(e) : 1;
+    const size_t smem = (size_t)L * 12 + (256 + (MS_NT / 32) * 257) * 4;
+    cudaFuncSetAttribute(mp_sort_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    mp_sort_small_kernel<<<(unsigned)nseg, MS_NT, smem, s>>>(keys, minmax, L, K, bits, hilbert, perm);
+    return true;
 }
 
 // --------------------------------------------------------------- boxes

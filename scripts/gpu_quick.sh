@@ -1,9 +1,11 @@
 #!/bin/bash
-# quick loop: build, a pytest selection ($PYK), whole-join phases on c4 / c3 / c2 (engine_ab)
+# quick loop: build, a pytest selection ($PYT, $PYK; SKIP_TESTS=1 skips), whole-join phases (engine_ab)
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_q.log 2>&1 || { tail gpurun_out/build_q.log; exit 1; }
-timeout 1200 python -m pytest ${PYT:-tests/test_gpu_gather.py} -m gpu -q -x -p no:cacheprovider ${PYK} 2>&1 | tail -2
-for c in ${CFGS:-"c4 2 1e-05 pivots=32" "c3 2 1e-05 pivots=24" "c2 1 0.0001 pivots=24"}; do
+[ "${SKIP_TESTS:-0}" == "1" ] || timeout 1200 python -m pytest ${PYT:-tests/test_gpu_gather.py} -m gpu -q -x -p no:cacheprovider ${PYK} 2>&1 | tail -2
+# configs: the script's arguments (one quoted "cfg norm hit opts" each), default c4 / c3 / c2
+[ $# -eq 0 ] && set -- "c4 2 1e-05 pivots=64" "c3 2 1e-05 pivots=64" "c2 1 0.0001 pivots=32"
+for c in "$@"; do
   echo "== $c"; timeout 600 python scripts/engine_ab.py $c 2>&1 | grep opts | python -c "
 import sys,json
 for l in sys.stdin:
