@@ -1092,7 +1092,7 @@ __device__ __forceinline__ bool mp_survives(const float* qmn, const float* qmx, 
 // lanes read consecutive words), and each warp's query box sits in shared memory too (up to 64
 // pivots) -- the per-lane global loads of the boxes (a dependent L2 round trip per 32 tail tiles)
 // made the many-pivot test latency-bound.
-constexpr int MC_W = 16;
+constexpr int MC_W = 32;
 __global__ void __launch_bounds__(32 * MC_W) mp_count_kernel(const float* __restrict__ qbmin,
                                                              const float* __restrict__ qbmax,
                                                              const float* __restrict__ tbmin,
@@ -1169,7 +1169,7 @@ __global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __r
     if (tq0 >= tq1) return;
     const long long base = cum[tq0];
     const int lane = threadIdx.x & 31;
-    if (MASKS) {  // the survival masks mp_count wrote: expand, no second pass over the boxes
+    if constexpr (MASKS) {  // the survival masks mp_count wrote: expand, no second pass over the boxes
         const int TW = (TT + 31) >> 5;
         for (long long q = tq0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); q < tq1;
              q += ((long long)gridDim.x * blockDim.x) >> 5) {
@@ -1194,8 +1194,7 @@ __global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __r
                 o += __shfl_sync(0xffffffffu, incl, 31);
             }
         }
-        return;
-    }
+    } else {
     for (long long q = tq0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); q < tq1;
          q += ((long long)gridDim.x * blockDim.x) >> 5) {
         float qmn[MP_MAX], qmx[MP_MAX];
@@ -1211,6 +1210,7 @@ __global__ void mp_emit_kernel(const float* __restrict__ qbmin, const float* __r
             if (ok) list[o + __popc(m & lanemask_lt())] = j;  // ascending j order
             o += __popc(m);
         }
+    }
     }
 }
 
