@@ -47,7 +47,7 @@ enum Phase { EV_START, EV_H2D, EV_KEYS, EV_SORT, EV_RANGES, EV_STAGE, EV_TILES, 
     X(est_hist) X(est_cost) X(mpP) X(mpkt) X(mpkq) X(mpmm_t) X(mpmm_q) X(mpc0) X(mpc1) X(tbmin) X(tbmax) X(qbmin) \
     X(qbmax) X(tile_list) X(tk_sample) X(tk_sel) X(tk_cnt) X(Ts) X(tks) X(gblk) X(granges) X(glist) X(tsc) X(gT2) \
     X(gtst) X(tmapbuf) X(fz) X(frt) X(frn) X(fzero) X(se_w) X(se_a64) X(se_b64) X(se_af) X(se_bf) X(se_zero) \
-    X(acc) X(Eb) X(mpbits) X(se_max) X(mpqn) X(mpA) X(mphx) X(mpB) X(mpC) X(mpk4) X(mpmm4)
+    X(acc) X(Eb) X(mpbits) X(se_max) X(mpqn) X(mpA) X(mphx) X(mpB) X(mpC) X(mpk4) X(mpmm4) X(mpHP)
 
 struct kgc_ctx {
     kgc_options opt{};
@@ -694,10 +694,12 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             CK(ensure(ctx->mpk4, NR * KO * 4));
             CK(ensure(ctx->mpmm4, (size_t)R * KO * 8));
             CK(ensure(ctx->mphx, 16));
+            CK(ensure(ctx->mpHP, (size_t)std::max<long long>(N, NT) * K * 8));
             launch_mp_keys_l2f(E, Rel, N, R, Et, NT, d, K, P<float>(ctx->mpP), P<float>(ctx->mpkt),
                                P<unsigned>(ctx->mpmm_t), P<float>(ctx->mpk4), P<unsigned>(ctx->mpmm4),
                                P<unsigned>(ctx->mpqn), P<double>(ctx->mpA), P<double>(ctx->mpB), P<double>(ctx->mpC),
-                               P<unsigned>(ctx->mphx), &dctr->nonfinite, s, ctx->ev_fork[1]);
+                               P<double>(ctx->mpHP), P<unsigned>(ctx->mphx), &dctr->nonfinite, &dctr->twid, s,
+                               ctx->ev_fork[1]);
             LAUNCHED((Et == E && NT == N) ? 5 : 6);
         } else {
             launch_mp_keys(Et, nullptr, NT, 1, d, norm, K, P<float>(ctx->mpP), P<float>(ctx->mpkt),
@@ -741,8 +743,9 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         if (kd && norm == 1) launch_kd_refine(P<float>(ctx->mpkq), P<int>(ctx->qperm), R, N, K, s);
         CK(cudaEventRecord(ctx->ev[EV_SORT], s));
         // ---- a4: K-dim tile boxes and the L_inf test of every tile pair
+        // tail boxes [k][TT]; L2: widened by the GEMM-form tail-key bound delta_t (DevCounters::twid)
         launch_mp_boxes(P<float>(ctx->mpkt), P<unsigned>(ctx->tperm), 1, NT, BN, TT, K, P<float>(ctx->tbmin),
-                        P<float>(ctx->tbmax), nullptr, s, 1);  // tail boxes [k][TT]
+                        P<float>(ctx->tbmax), norm == 2 ? &dctr->twid : nullptr, s, 1);
         if (norm == 2)
             launch_mp_qboxes_fact(P<unsigned>(ctx->qperm), P<double>(ctx->mpB), P<double>(ctx->mpA), P<double>(ctx->mpC),
                                   N, R, K, bq, QT, P<unsigned>(ctx->mpqn), P<float>(ctx->qbmin), P<float>(ctx->qbmax), s);
@@ -840,8 +843,11 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         CK(cudaMemsetAsync(ctx->gblk.p, 0, (size_t)nq * 8, s));
         CK(cudaMemsetAsync(ctx->nitem.p, 0, (size_t)nq * 4, s));
         CK(cudaMemsetAsync(ctx->item_tiles.p, 0, (size_t)g_max_items * 8, s));
+        // the per-tail test reads single tail keys: with the L2 GEMM-form keys widen theta by delta_t
+        const float gtheta = norm == 2 ? std::nextafter(feps + ldexpf(__uint_as_float_host(h1.c.twid), -23), INFINITY)
+                                       : feps;
         launch_gather_tails(P<float>(ctx->qbmin), P<float>(ctx->qbmax), P<float>(ctx->tks), P<int>(ctx->tile_list),
-                            P<long long>(ctx->cum), P<int2>(ctx->ranges), dctr, NT, BN, K, feps, mp_relm(d), chunk, nq,
+                            P<long long>(ctx->cum), P<int2>(ctx->ranges), dctr, NT, BN, K, gtheta, mp_relm(d), chunk, nq,
                             P<long long>(ctx->gblk), P<int2>(ctx->granges), P<int>(ctx->nitem), P<int>(ctx->glist),
                             gather_tc ? P<float4>(ctx->tsc) : nullptr, gather_tc ? P<float>(ctx->gT2) : nullptr,
                             gather_tc ? P<float2>(ctx->gtst) : nullptr, cyc ? ctx->opt.world : 0, ctx->opt.rank,

@@ -40,7 +40,7 @@ struct DevCounters {
     unsigned long long cand;      // candidates appended by the tile kernels
     unsigned long long res;       // results appended by the verify kernel
     unsigned int nonfinite;       // != 0 if E or Rel holds a non-finite value
-    unsigned int pad0;
+    unsigned int twid;            // L2 K pivots: tail-key bound delta_t 2^23 (float bits, rounded up)
     long long total_cost;         // surviving tile pairs, all shards
     long long my_cost;            // surviving tile pairs, this shard
     int tq_begin, tq_end;         // query-tile range of this shard [begin, end)
@@ -155,8 +155,9 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
 // Cg R x (K + 1) doubles
 void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long R, const float* Et, long long NT,
                         int d, int K, const float* P, float* tkeys, unsigned int* tminmax, float* qkeys4,
-                        unsigned int* qmm4, unsigned int* qnmax, double* A, double* Bhr, double* Cg,
-                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s, cudaEvent_t bready);
+                        unsigned int* qmm4, unsigned int* qnmax, double* A, double* Bhr, double* Cg, double* HP,
+                        unsigned int* hmax, unsigned int* nonfinite, unsigned int* twid, cudaStream_t s,
+                        cudaEvent_t bready);
 void launch_mp_qkeys_all(const double* Bhr, const double* A, const double* Cg, long long N, long long R, int K,
                          float* keys, cudaStream_t s);
 void launch_mp_qboxes_fact(const unsigned int* perm, const double* Bhr, const double* A, const double* Cg, long long N,

@@ -461,25 +461,33 @@ __device__ __forceinline__ float key_sqrt(float x) {
     return y;
 }
 
-// Per entity row x (one thread per row, the pivots in shared memory as FP64, [d][K] so a
-// double2 load serves two pivots): A[x][k] = ||x - p_k||^2 in FP64 from the differences (no
-// cancellation: relative error <= (d + 3) 2^-53; optional), the tail keys sqrtf(fl32(A)) (optional)
-// with their per-pivot min / max, max_x ||x|| rounded up (optional), and the non-finite check of x.
+// Entity terms from the GEMM HP = X P^T (mp_hr_kernel with the pivots as the "relations"):
+// A[x][k] = (||x||^2 + ||p_k||^2) - 2 HP[k][x] in FP64 (one thread per row; ||x||^2 from the row,
+// ||p_k||^2 per block), the tail keys key_sqrt(fl32(max(A, 0))) with their ranges, max ||x|| and the
+// non-finite check.  The expansion cancels: |A~ - A| <= (d + 2) 2^-53 (||x|| + ||p||)^2, so a tail
+// key errs by <= delta_t = sqrt((d + 4) 2^-53) (max ||t|| + max ||p||) absolute -- the tail boxes and
+// the per-tail test are widened by it (mp_rel_terms_kernel writes it to DevCounters::twid); in the
+// query keys the same error is inside delta_r.  Half the FP64 operations of the difference form and
+// a register-blocked GEMM for the K d part (c4, K = 64: 0.47 ms for the difference form).
 template <int K>
-__global__ void __launch_bounds__(256) mp_ent_kernel(const float* __restrict__ X, long long n, int d,
-                                                     const float* __restrict__ P, double* __restrict__ A,
-                                                     float* __restrict__ keys, unsigned int* minmax,
-                                                     unsigned int* xmax, unsigned int* nonfinite) {
-    extern __shared__ __align__(16) double me_smem[];
-    constexpr int KP = (K + 1) / 2 * 2;
-    constexpr int KC = KP <= 32 ? KP : 16;  // pivots per pass over the row (registers)
-    double* Ps = me_smem;  // [d][KP], converted once per block
-    for (int x = threadIdx.x; x < d * KP; x += blockDim.x) {
-        const int i = x / KP, k = x - i * KP;
-        Ps[x] = k < K ? (double)P[k * d + i] : 0.0;
+__global__ void __launch_bounds__(256) mp_ent_gemm_kernel(const float* __restrict__ X, long long n, int d,
+                                                          const float* __restrict__ P, const double* __restrict__ HP,
+                                                          double* __restrict__ A, float* __restrict__ keys,
+                                                          unsigned int* minmax, unsigned int* xmax,
+                                                          unsigned int* nonfinite) {
+    __shared__ double pp[K];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    for (int k = w; k < K; k += NW) {
+        double sp = 0.0;
+        for (int x = lane; x < d; x += 32) {
+            const double v = (double)__ldg(P + k * d + x);
+            sp = fma(v, v, sp);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
+        if (lane == 0) pp[k] = sp;
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31;
     const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
     float run_mn[(K + 31) / 32], run_mx[(K + 31) / 32];  // lane k % 32 of word k / 32: pivot k
 #pragma unroll
@@ -490,45 +498,33 @@ __global__ void __launch_bounds__(256) mp_ent_kernel(const float* __restrict__ X
     for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
         const long long row = blk * blockDim.x + threadIdx.x;
         const bool rv = row < n;
-        const float* xr = X + (rv ? row : 0) * d;
         double xx = 0.0;
-#pragma unroll
-        for (int k0 = 0; k0 < KP; k0 += KC) {
-            double acc[KC];
-#pragma unroll
-            for (int k = 0; k < KC; ++k) acc[k] = 0.0;
-            auto step = [&](float v, int i) {
-                if (k0 == 0) {
+        if (rv) {
+            const float* xr = X + row * d;
+            if (vec) {
+                for (int i = 0; i < d; i += 4) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(xr + i));
+                    bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+                    xx = fma((double)v.x, (double)v.x, xx);
+                    xx = fma((double)v.y, (double)v.y, xx);
+                    xx = fma((double)v.z, (double)v.z, xx);
+                    xx = fma((double)v.w, (double)v.w, xx);
+                }
+            } else {
+                for (int i = 0; i < d; ++i) {
+                    const float v = __ldg(xr + i);
                     bad |= !isfinite(v);
                     xx = fma((double)v, (double)v, xx);
                 }
-                const double dv = (double)v;
-                const double2* pr = reinterpret_cast<const double2*>(Ps + i * KP + k0);
-#pragma unroll
-                for (int k = 0; k < KC; k += 2) {
-                    const double2 p2 = pr[k / 2];
-                    const double t0 = dv - p2.x, t1 = dv - p2.y;
-                    acc[k] = fma(t0, t0, acc[k]);
-                    acc[k + 1] = fma(t1, t1, acc[k + 1]);
-                }
-            };
-            if (rv) {
-                if (vec) {
-                    for (int i = 0; i < d; i += 4) {
-                        const float4 v = __ldg(reinterpret_cast<const float4*>(xr + i));
-                        step(v.x, i); step(v.y, i + 1); step(v.z, i + 2); step(v.w, i + 3);
-                    }
-                } else {
-                    for (int i = 0; i < d; ++i) step(__ldg(xr + i), i);
-                }
             }
-#pragma unroll
-            for (int kk = 0; kk < KC; ++kk) {
-                const int k = k0 + kk;
-                if (k >= K) break;
-                if (rv && A) A[row * K + k] = acc[kk];
-                const float key = key_sqrt(__double2float_rn(acc[kk]));
-                if (rv && keys) keys[row * K + k] = key;
+        }
+#pragma unroll 8
+        for (int k = 0; k < K; ++k) {
+            const double a = rv ? (xx + pp[k]) - 2.0 * __ldg(HP + (size_t)k * n + row) : 0.0;
+            if (rv && A) A[row * K + k] = a;
+            const float key = key_sqrt(__double2float_rn(fmax(a, 0.0)));
+            if (rv && keys) keys[row * K + k] = key;
+            if (minmax) {
                 const unsigned bits = __float_as_uint(key);
                 const unsigned m = __reduce_min_sync(0xffffffffu, rv ? bits : 0x7f7fffffu);
                 const unsigned z = __reduce_max_sync(0xffffffffu, rv ? bits : 0u);
@@ -557,6 +553,7 @@ __global__ void __launch_bounds__(256) mp_ent_kernel(const float* __restrict__ X
     }
 }
 
+
 // B[r][h] = E_h . Rel_r for every (h, r) in FP64 (products of two floats are exact, FP64 sums):
 // the one d-term quantity per query row.  A register-blocked SIMT GEMM (FP64 tensor cores run at
 // the same ~60 FMA/clk/SM on B200): block = 4 warps, tile 128 entities x 32 relations, thread =
@@ -575,19 +572,52 @@ __global__ void __launch_bounds__(128) mp_hr_kernel(const float* __restrict__ E,
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < 8; ++c) acc[a][c] = 0.0;
+    const bool vec = (d & 3) == 0 && ((reinterpret_cast<uintptr_t>(E) | reinterpret_cast<uintptr_t>(Rel)) & 15) == 0;
     for (int k0 = 0; k0 < d; k0 += HR_KC) {
         __syncthreads();
-        // entities: consecutive threads on consecutive rows (conflict-free stores; each row's
-        // 128-byte line is reused from L1 across the chunk's k)
-        for (int x = tid; x < HR_BM * HR_KC; x += 128) {
-            const int i = x % HR_BM, k = x / HR_BM;
-            const long long h = h0 + i;
-            Es[k][i] = (h < N && k0 + k < d) ? (double)__ldg(E + h * d + k0 + k) : 0.0;
-        }
-        for (int x = tid; x < HR_BR * HR_KC; x += 128) {
-            const int i = x % HR_BR, k = x / HR_BR;
-            const long long r = r0 + i;
-            Rs[k][i] = (r < R && k0 + k < d) ? (double)__ldg(Rel + r * d + k0 + k) : 0.0;
+        if (vec) {
+            // thread = entity row (128 rows), its chunk as 8 independent float4 loads in flight
+            // (a dependent-latency loop of 32 scalar loads per thread made the GEMM load-bound);
+            // stores Es[k][row]: consecutive threads, consecutive words
+            const long long h = h0 + tid;
+            float4 v[HR_KC / 4];
+#pragma unroll
+            for (int j = 0; j < HR_KC / 4; ++j) {
+                const int k = k0 + 4 * j;
+                v[j] = (h < N && k < d) ? __ldg(reinterpret_cast<const float4*>(E + h * d + k))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < HR_KC / 4; ++j) {
+                Es[4 * j][tid] = (double)v[j].x;
+                Es[4 * j + 1][tid] = (double)v[j].y;
+                Es[4 * j + 2][tid] = (double)v[j].z;
+                Es[4 * j + 3][tid] = (double)v[j].w;
+            }
+            // relations: 32 rows x 8 float4, two per thread
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int x = tid + 128 * u, i = x >> 3, j = x & 7;
+                const long long r = r0 + i;
+                const int k = k0 + 4 * j;
+                const float4 w4 = (r < R && k < d) ? __ldg(reinterpret_cast<const float4*>(Rel + r * d + k))
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+                Rs[4 * j][i] = (double)w4.x;
+                Rs[4 * j + 1][i] = (double)w4.y;
+                Rs[4 * j + 2][i] = (double)w4.z;
+                Rs[4 * j + 3][i] = (double)w4.w;
+            }
+        } else {
+            for (int x = tid; x < HR_BM * HR_KC; x += 128) {
+                const int i = x % HR_BM, k = x / HR_BM;
+                const long long h = h0 + i;
+                Es[k][i] = (h < N && k0 + k < d) ? (double)__ldg(E + h * d + k0 + k) : 0.0;
+            }
+            for (int x = tid; x < HR_BR * HR_KC; x += 128) {
+                const int i = x % HR_BR, k = x / HR_BR;
+                const long long r = r0 + i;
+                Rs[k][i] = (r < R && k0 + k < d) ? (double)__ldg(Rel + r * d + k0 + k) : 0.0;
+            }
         }
         __syncthreads();
 #pragma unroll 4
@@ -626,7 +656,8 @@ __global__ void __launch_bounds__(128) mp_hr_kernel(const float* __restrict__ E,
 __global__ void mp_rel_terms_kernel(const float* __restrict__ Rel, long long R, int d, int K,
                                     const float* __restrict__ P, double* __restrict__ Cg,
                                     const unsigned int* __restrict__ hmax, unsigned int* qnmax,
-                                    unsigned int* nonfinite) {
+                                    unsigned int* nonfinite, const unsigned int* __restrict__ tmax,
+                                    unsigned int* twid) {
     __shared__ double pmax_s;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
     if (threadIdx.x == 0) pmax_s = 0.0;
@@ -665,6 +696,11 @@ __global__ void mp_rel_terms_kernel(const float* __restrict__ Rel, long long R, 
         // delta_r needs max ||p|| of every pivot: block 0 only (it computed pmax_s), after the
         // terms above are globally visible -- recompute ||r|| here instead of reading Cg
         const double pm = sqrt(pmax_s) * (1.0 + 0x1p-40);
+        if (threadIdx.x == 0 && twid) {  // tail-key bound delta_t of the GEMM-form entity terms
+            const double dt = sqrt((double)(d + 4) * 0x1p-53) * (1.0 + 0x1p-20) *
+                              ((double)__uint_as_float(*tmax) + pm);
+            atomicMax(twid, __float_as_uint(__double2float_ru(dt * 0x1p23)));
+        }
         for (long long r = w; r < R; r += NW) {
             double rr = 0.0;
             for (int x = lane; x < d; x += 32) {
@@ -675,7 +711,7 @@ __global__ void mp_rel_terms_kernel(const float* __restrict__ Rel, long long R, 
             for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
             if (lane == 0) {
                 const double S1 = (double)__uint_as_float(*hmax) + sqrt(rr) * (1.0 + 0x1p-40) + pm;
-                const double delta = sqrt((double)(d + 6) * 0x1p-53) * (1.0 + 0x1p-20) * S1;
+                const double delta = sqrt((double)(d + 8) * 0x1p-53) * (1.0 + 0x1p-20) * S1;
                 atomicMax(&qnmax[r], __float_as_uint(__double2float_ru(delta * 0x1p23)));
             }
         }
@@ -1716,29 +1752,29 @@ void launch_mp_keys(const float* E, const float* Rel, long long N, long long nse
 // (E + Rel, N x R), both FP64.  A (N x K doubles) and hmax (one word) are scratch.
 void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long R, const float* Et, long long NT,
                         int d, int K, const float* P, float* tkeys, unsigned int* tminmax, float* qkeys4,
-                        unsigned int* qmm4, unsigned int* qnmax, double* A, double* Bhr, double* Cg,
-                        unsigned int* hmax, unsigned int* nonfinite, cudaStream_t s, cudaEvent_t bready) {
+                        unsigned int* qmm4, unsigned int* qnmax, double* A, double* Bhr, double* Cg, double* HP,
+                        unsigned int* hmax, unsigned int* nonfinite, unsigned int* twid, cudaStream_t s,
+                        cudaEvent_t bready) {
     const int KO = K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS;
     mp_init_minmax_kernel<<<grid_for_mp(K, 256), 256, 0, s>>>(tminmax, K, nullptr, 0);
     mp_init_minmax_kernel<<<grid_for_mp(R * KO, 256), 256, 0, s>>>(qmm4, R * KO, qnmax, R);
-    cudaMemsetAsync(hmax, 0, 4, s);
-    const size_t esm = (size_t)((K + 1) / 2 * 2) * d * 8;
-    auto ent = [&](auto kern, const float* X, long long n, double* a, float* keys, unsigned int* mm, unsigned int* xm) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
-        kern<<<grid_for_mp(n, 256, 148LL * 2), 256, esm, s>>>(X, n, d, P, a, keys, mm, xm, nonfinite);
-    };
+    cudaMemsetAsync(hmax, 0, 8, s);  // hmax[0] heads, hmax[1] tails
+    cudaMemsetAsync(twid, 0, 4, s);
+    const bool same = Et == E && NT == N;
     auto byK = [&](auto k_) {
         constexpr int KK = decltype(k_)::value;
         constexpr int KOO = KK < MP_SORT_PIVOTS ? KK : MP_SORT_PIVOTS;
-        const bool same = Et == E && NT == N;
-        if (same) {
-            ent(mp_ent_kernel<KK>, E, N, A, tkeys, tminmax, hmax);
-        } else {
-            ent(mp_ent_kernel<KK>, Et, NT, nullptr, tkeys, tminmax, nullptr);
-            ent(mp_ent_kernel<KK>, E, N, A, nullptr, nullptr, hmax);
+        // entity terms: HP = X P^T by the FP64 GEMM, then A, the tail keys and their ranges
+        launch_mp_hr(E, P, N, KK, d, HP, s);
+        mp_ent_gemm_kernel<KK><<<grid_for_mp(N, 256, 148LL * 8), 256, 0, s>>>(
+            E, N, d, P, HP, A, same ? tkeys : nullptr, same ? tminmax : nullptr, hmax, nonfinite);
+        if (!same) {  // tails from another array (tail partition / block join): their own terms
+            launch_mp_hr(Et, P, NT, KK, d, HP, s);
+            mp_ent_gemm_kernel<KK><<<grid_for_mp(NT, 256, 148LL * 8), 256, 0, s>>>(
+                Et, NT, d, P, HP, nullptr, tkeys, tminmax, hmax + 1, nonfinite);
         }
         mp_rel_terms_kernel<<<(unsigned)std::min<long long>(148LL * 4, (R * (KK + 1) + 7) / 8), 256, 0, s>>>(
-            Rel, R, d, KK, P, Cg, hmax, qnmax, nonfinite);
+            Rel, R, d, KK, P, Cg, hmax, qnmax, nonfinite, same ? hmax : hmax + 1, twid);
         cudaStreamWaitEvent(s, bready, 0);  // B from the aux stream (launch_mp_hr)
         dim3 gk((unsigned)((N + 255) / 256), (unsigned)((R + QK_RCH - 1) / QK_RCH));
         mp_qkeys_fact_kernel<KK, KOO><<<gk, 256, 0, s>>>(Bhr, A, Cg, N, R, qkeys4, qmm4);
