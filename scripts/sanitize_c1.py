@@ -20,7 +20,10 @@ from synth import generate_config  # noqa: E402
 RUNS = [(2, dict(l2_engine=1)), (2, dict(l2_engine=2)), (2, dict(l2_engine=3)), (2, dict(l2_engine=1, pivots=8)),
         (2, dict(l2_engine=3, pivots=8)), (2, dict(l2_engine=4, pivots=8)), (2, dict(l2_engine=5)),
         (2, dict(l2_engine=6, pivots=8)), (1, dict(l1_engine=2)), (1, dict(l1_engine=3, pivots=8)),
-        (1, dict(l1_engine=1)), (1, dict(l1_engine=2, pivots=8))]
+        (1, dict(l1_engine=1)), (1, dict(l1_engine=2, pivots=8)),
+        # round 2: many pivots (FP64-factorised L2 keys, on-the-fly boxes, staged tile test, one-CTA sorts)
+        (2, dict(l2_engine=1, pivots=64)), (2, dict(l2_engine=3, pivots=64)), (2, dict(l2_engine=4, pivots=32)),
+        (1, dict(l1_engine=3, pivots=32))]
 
 
 def main():
