@@ -193,11 +193,12 @@ def workload_name(args, cfg):
             f"theta at hit rate {args.hit:g}, {cfg.dist} embeddings ({GENERATOR_VERSION}, seed {cfg.seed})")
 
 
-# Best measured settings per workload: with the FP64-factorised L2 keys (query
-# keys never materialised), 64 pivots cut the surviving tile pairs of c4 / c5 / c3 by 4.7x / 2.9x /
-# 4.8x against 8 (whole join c4 17.4 -> 8.2 ms, c5 1460 -> 527 ms, c3 10.4 (one pivot) -> 7.3 ms);
-# c2 takes 32 (the L1 keys support at most 32); the cyclic split spreads c2's hit-dense relations.
-BEST_PIVOTS = {"c1": 1, "c2": 32, "c3": 64, "c4": 64, "c5": 64}
+# Best measured settings per workload: with the FP64-factorised L2 keys (query keys
+# never materialised) many pivots cut the surviving tile pairs (c4: 4.76% at 8, 1.01% at 64, 0.37% at
+# 96); whole join c4 17.4 (8) -> 8.1 (64) -> 6.9 ms (96), c5 1460 -> 524 -> 443 ms (128), c3 10.4 (one
+# pivot) -> 7.0 ms (64); c2 takes 32 (the L1 keys support at most 32); the cyclic split spreads c2's
+# hit-dense relations.
+BEST_PIVOTS = {"c1": 1, "c2": 32, "c3": 64, "c4": 96, "c5": 128}
 BEST_SPLIT = {"c2": 2}
 DEFAULT_HIT = {"c1": 1e-3, "c2": 1e-4, "c3": 1e-5, "c4": 1e-5, "c5": 1e-6}
 DEFAULT_NORMS = {"c1": "2,1", "c2": "2,1", "c3": "2", "c4": "2", "c5": "2"}
@@ -659,7 +660,7 @@ def main(argv=None):
                     help="diagnostic: on ONE GPU run each of W shards in turn and print the per-shard device times "
                          "(projects the N=W device time; not the official line)")
     ap.add_argument("--pivots", default="auto",
-                    help="1 = the paper's single pivot; 2..8, 12, 16, 24, 32 (48, 64: L2 only) = multi-pivot pruning; "
+                    help="1 = the paper's single pivot; 2..8, 12, 16, 24, 32 (48, 64, 96, 128: L2 only) = multi-pivot pruning; "
                          "auto = best measured per config")
     args = ap.parse_args(argv)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not args.emulate_ranks:

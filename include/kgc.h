@@ -88,12 +88,12 @@ typedef struct {
                               /* per 256-row query tile the tails passing the per-tail K-pivot     */
                               /* test, 256 per block, each CTA gathering its 128 rows with cp.async */
     int32_t chunk_tiles;      /* max tail tiles per work item (load-balance granularity); 0 = auto */
-    int32_t pivots;           /* 0/1 = one pivot (default); 2..8, 12, 16, 24, 32, 48 or */
-                              /* 64 = multi-pivot tile pruning (L_inf over K pivot distances,       */
-                              /* PAPER.md:256; needs d <= 256, prune = 1; otherwise one pivot is    */
-                              /* used); other values: KGC_EINVAL at kgc_create; 48 / 64 with norm 1: */
-                              /* KGC_EINVAL at the join (the L1 keys support 32).  The per-tail test */
-                              /* of the gathered engines uses the first 8 pivots                    */
+    int32_t pivots;           /* 0/1 = one pivot (default); 2..8, 12, 16, 24, 32, 48, */
+                              /* 64, 96 or 128 = multi-pivot tile pruning (L_inf over K pivot       */
+                              /* distances; needs d <= 256, prune = 1; otherwise one  */
+                              /* pivot is used); other values: KGC_EINVAL at kgc_create; more than  */
+                              /* 32 with norm 1: KGC_EINVAL at the join (the L1 keys support 32).   */
+                              /* The per-tail test of the gathered engines uses the first 8 pivots  */
     int64_t result_capacity;  /* initial result-buffer capacity in triplets; 0 = auto (grows)       */
     void*   stream;           /* cudaStream_t to run on; NULL = a stream the context creates       */
     int32_t l1_engine;        /* 0 = auto (3 with multi-pivot pruning, else 2); 1 = FP16x2 SIMT    */

@@ -27,9 +27,11 @@ constexpr int EST_SAMPLES = 256;  // sampled queries per relation, rank-local sp
 constexpr int SIMT_T = 64;       // tile rows (query and tail), FP32 SIMT engines
 constexpr int SORT_IPB = 2048;   // radix-sort items per block (256 threads x 8)
 constexpr int TC_MAX_KPAD = 256; // tensor-core engine supports d <= 256
-constexpr int MP_MAX = 64;       // multi-pivot pruning: at most 64 pivots (2..8, 12, 16, 24, 32; 48, 64 with L2)
+constexpr int MP_MAX = 128;      // multi-pivot pruning: at most 128 pivots (2..8, 12, 16, 24, 32; 48 ... 128 with L2)
 constexpr int MP_G = 8;          // pivots of the per-tail test of the gathered engines (the first 8)
-inline bool mp_pivots_ok(int k) { return k <= 8 || k == 12 || k == 16 || k == 24 || k == 32 || k == 48 || k == 64; }
+inline bool mp_pivots_ok(int k) {
+    return k <= 8 || k == 12 || k == 16 || k == 24 || k == 32 || k == 48 || k == 64 || k == 96 || k == 128;
+}
 constexpr int MP_MAX_L1 = 32;    // the L1 keys (FP32, materialised) support at most 32 pivots
 
 constexpr int MP_MAX_DIM = 256;  // multi-pivot pruning supports d <= 256

@@ -81,23 +81,23 @@ __global__ void __launch_bounds__(1024) pick_pivots_kernel(const float* __restri
     __syncthreads();
     const int sidx = threadIdx.x;
     auto dist_to_piv = [&]() {
-        float s4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains
+        float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent chains (K rounds are serial)
         if (sidx < S) {
             const float* xr = X + sidx * st;
             int k = 0;
-            for (; k + 4 <= d; k += 4) {
+            for (; k + 8 <= d; k += 8) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < 8; ++u) {
                     const float x = xr[k + u] - piv[k + u];
-                    s4[u] = NORM == 1 ? s4[u] + fabsf(x) : fmaf(x, x, s4[u]);
+                    s8[u] = NORM == 1 ? s8[u] + fabsf(x) : fmaf(x, x, s8[u]);
                 }
             }
             for (; k < d; ++k) {
                 const float x = xr[k] - piv[k];
-                s4[0] = NORM == 1 ? s4[0] + fabsf(x) : fmaf(x, x, s4[0]);
+                s8[0] = NORM == 1 ? s8[0] + fabsf(x) : fmaf(x, x, s8[0]);
             }
         }
-        return (s4[0] + s4[1]) + (s4[2] + s4[3]);  // squared for L2 (monotone: fine for argmax)
+        return ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));  // squared for L2
     };
     float mind = sidx < S ? dist_to_piv() : -1.f;
     for (int kk = 1; kk < K; ++kk) {
@@ -110,12 +110,16 @@ __global__ void __launch_bounds__(1024) pick_pivots_kernel(const float* __restri
         }
         if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = best; bi[threadIdx.x >> 5] = besti; }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            float b = -2.f;
-            int ix = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
-                if (bv[w] > b || (bv[w] == b && bi[w] < ix)) { b = bv[w]; ix = bi[w]; }
-            chosen = ix;
+        if (threadIdx.x < 32) {  // warp 0 reduces the per-warp winners (ties: the lower index)
+            const int nw = (int)(blockDim.x >> 5);
+            float b = threadIdx.x < nw ? bv[threadIdx.x] : -2.f;
+            int ix = threadIdx.x < nw ? bi[threadIdx.x] : 0x7fffffff;
+            for (int o = 16; o > 0; o >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, b, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, ix, o);
+                if (ov > b || (ov == b && oi < ix)) { b = ov; ix = oi; }
+            }
+            if (threadIdx.x == 0) chosen = ix;
         }
         __syncthreads();
         float* pk = P + (size_t)kk * d;
@@ -1129,6 +1133,8 @@ __device__ __forceinline__ bool mp_survives(const float* qmn, const float* qmx, 
 // pivots) -- the per-lane global loads of the boxes (a dependent L2 round trip per 32 tail tiles)
 // made the many-pivot test latency-bound.
 constexpr int MC_W = 32;
+// tail tiles per staged chunk: 4096 / K rounded down to 32 (32 KB of boxes; 12288 / K measured slower on c5)
+__host__ __device__ inline int mc_chunk(int K) { return 4096 / K / 32 * 32; }
 __global__ void __launch_bounds__(32 * MC_W) mp_count_kernel(const float* __restrict__ qbmin,
                                                              const float* __restrict__ qbmax,
                                                              const float* __restrict__ tbmin,
@@ -1136,7 +1142,7 @@ __global__ void __launch_bounds__(32 * MC_W) mp_count_kernel(const float* __rest
                                                              int K, float theta, float relm, int prune, int2* ranges,
                                                              long long* cost, unsigned int* __restrict__ bits) {
     extern __shared__ float mc_smem[];
-    const int CT = 4096 / K / 32 * 32;                 // tail tiles per chunk (a multiple of 32)
+    const int CT = mc_chunk(K);                        // tail tiles per chunk (a multiple of 32)
     float* sbn = mc_smem;                              // [K][CT]
     float* sbx = sbn + K * CT;                         // [K][CT]
     float* sq = sbx + K * CT;                          // [MC_W][2][K] query boxes
@@ -1651,12 +1657,14 @@ void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, con
     kern<<<1, 1024, smem, s>>>(E, N, d, K, (int)S, p0, P);
 }
 
-// K dispatch for the key kernels: 2..8, 12, 16, 24, 32 pivots, and 48, 64 for the L2 path (mp_pivots_ok)
+// K dispatch for the key kernels: 2..8, 12, 16, 24, 32 pivots, and 48 ... 128 for the L2 path (mp_pivots_ok)
 template <int KMAX = 32, class F>
 static void for_pivots(int K, F&& f) {
     if constexpr (KMAX >= 48) {
         if (K == 48) { f(std::integral_constant<int, 48>{}); return; }
         if (K == 64) { f(std::integral_constant<int, 64>{}); return; }
+        if (K == 96) { f(std::integral_constant<int, 96>{}); return; }
+        if (K == 128) { f(std::integral_constant<int, 128>{}); return; }
     }
     switch (K) {
         case 2: f(std::integral_constant<int, 2>{}); break;
@@ -1779,13 +1787,13 @@ void launch_mp_keys_l2f(const float* E, const float* Rel, long long N, long long
         dim3 gk((unsigned)((N + 255) / 256), (unsigned)((R + QK_RCH - 1) / QK_RCH));
         mp_qkeys_fact_kernel<KK, KOO><<<gk, 256, 0, s>>>(Bhr, A, Cg, N, R, qkeys4, qmm4);
     };
-    for_pivots<64>(K, byK);
+    for_pivots<128>(K, byK);
 }
 
 // The full K query keys per (r, h) (kgc_inspect only: the join itself never materialises them).
 void launch_mp_qkeys_all(const double* Bhr, const double* A, const double* Cg, long long N, long long R, int K,
                          float* keys, cudaStream_t s) {
-    for_pivots<64>(K, [&](auto k_) {
+    for_pivots<128>(K, [&](auto k_) {
         constexpr int KK = decltype(k_)::value;
         dim3 gk((unsigned)((N + 255) / 256), (unsigned)((R + QK_RCH - 1) / QK_RCH));
         mp_qkeys_fact_kernel<KK, KK><<<gk, 256, 0, s>>>(Bhr, A, Cg, N, R, keys, nullptr);
@@ -1795,7 +1803,7 @@ void launch_mp_qkeys_all(const double* Bhr, const double* A, const double* Cg, l
 void launch_mp_qboxes_fact(const unsigned int* perm, const double* Bhr, const double* A, const double* Cg, long long N,
                            long long R, int K, int ROWS, int QT, const unsigned int* qnmax, float* bmin, float* bmax,
                            cudaStream_t s) {
-    for_pivots<64>(K, [&](auto k_) {
+    for_pivots<128>(K, [&](auto k_) {
         constexpr int KK = decltype(k_)::value;
         mp_qboxes_fact_kernel<KK><<<grid_for_mp(R * QT * 32, 256), 256, 0, s>>>(perm, Bhr, A, Cg, N, R, ROWS, QT, qnmax,
                                                                               bmin, bmax);
@@ -1825,7 +1833,7 @@ void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg
 void launch_mp_count(const float* qbmin, const float* qbmax, const float* tbmin, const float* tbmax, long long nq,
                      int TT, int K, float theta, float relm, int prune, int2* ranges, long long* cost, unsigned int* bits,
                      cudaStream_t s) {
-    const int CT = 4096 / K / 32 * 32;
+    const int CT = mc_chunk(K);
     const size_t smem = (size_t)(2 * K * CT + MC_W * 2 * K) * 4;
     cudaFuncSetAttribute(mp_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     mp_count_kernel<<<grid_for_mp(nq, MC_W, 148LL * 16), 32 * MC_W, smem, s>>>(qbmin, qbmax, tbmin, tbmax, nq, TT, K,

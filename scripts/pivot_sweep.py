@@ -60,7 +60,7 @@ def boxes(sk, rows):
 tp = torch.from_numpy(tperm.astype(np.int64)).cuda()
 tmn, tmx = boxes(kt[tp], BT)
 out = {"config": name, "hit": hit, "lib_tile_pairs": st["tile_pairs_surviving"], "tiles": f"{BQ}x{BT}"}
-Ks = [k for k in (4, 8, 12, 16, 20, 24, 32, 40, 48, 64) if k <= KMAX]
+Ks = [k for k in (4, 8, 12, 16, 20, 24, 32, 40, 48, 64, 96, 128) if k <= KMAX]
 surv = {K: 0 for K in Ks}
 for r in range(R):
     kq = (A + 2 * HR[:, r:r + 1] - 2 * C[r][None] + rr[r]).clamp_min(0).sqrt()  # [N, 16]

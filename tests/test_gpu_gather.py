@@ -339,7 +339,7 @@ def test_tc2_gather_full_size_sampled(cfg, hit, S):
 
 
 @pytest.mark.parametrize("offset", [0.0, 1000.0])
-@pytest.mark.parametrize("K", [3, 8, 16, 32, 64])
+@pytest.mark.parametrize("K", [3, 8, 16, 32, 64, 128])
 def test_l2_factorised_keys_accuracy(offset, K):
     """L2 K-pivot keys come from the FP64 factorisation ||h + r - p||^2 = ||h - p||^2 +
     2 h.r - 2 r.p + ||r||^2 (pivots.cu, mp_qkeys_fact_kernel): each key is within 2^-21
@@ -377,7 +377,7 @@ def test_l2_factorised_keys_accuracy(offset, K):
     check_parity(E, Rel, 2, eps, res)
 
 
-@pytest.mark.parametrize("K", [12, 16, 24, 32, 48, 64])
+@pytest.mark.parametrize("K", [12, 16, 24, 32, 48, 64, 96, 128])
 @pytest.mark.parametrize("norm,opts", [(2, dict(l2_engine=1)), (2, dict(l2_engine=3)), (2, dict(l2_engine=4)),
                                        (1, dict(l1_engine=3)), (1, dict(l1_engine=2))])
 def test_many_pivots_c1_full(K, norm, opts):
@@ -394,7 +394,7 @@ def test_many_pivots_c1_full(K, norm, opts):
     assert st["tile_pairs_surviving"] <= st8["tile_pairs_surviving"]
 
 
-@pytest.mark.parametrize("K", [16, 32, 64])
+@pytest.mark.parametrize("K", [16, 32, 64, 128])
 @pytest.mark.parametrize("N,R,d", [(65, 2, 8), (700, 3, 50), (2049, 3, 33), (513, 2, 256)])
 def test_many_pivots_ragged(K, N, R, d):
     E, Rel = generate(N, R, d, seed=5 * N + d + K)
@@ -406,7 +406,7 @@ def test_many_pivots_ragged(K, N, R, d):
 
 def test_pivot_count_validation():
     from paper_2307_12059_b200 import kgc
-    for bad in (9, 10, 17, 33, 65):
+    for bad in (9, 10, 17, 33, 65, 100, 129):
         with pytest.raises(Exception):
             with kgc.Join(pivots=bad) as j:
                 pass
