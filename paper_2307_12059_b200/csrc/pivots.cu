@@ -522,19 +522,51 @@ __global__ void __launch_bounds__(256) mp_ent_gemm_kernel(const float* __restric
                 }
             }
         }
-#pragma unroll 8
-        for (int k = 0; k < K; ++k) {
-            const double a = rv ? (xx + pp[k]) - 2.0 * __ldg(HP + (size_t)k * n + row) : 0.0;
-            if (rv && A) A[row * K + k] = a;
-            const float key = key_sqrt(__double2float_rn(fmax(a, 0.0)));
-            if (rv && keys) keys[row * K + k] = key;
+        // four pivots at a time: 16-byte stores of A (two double2) and of the keys (float4) -- each
+        // thread's row is K contiguous values, so narrower stores touched a line per lane per pivot
+        constexpr bool V4 = K % 4 == 0;
+#pragma unroll 2
+        for (int k0 = 0; k0 < K; k0 += 4) {
+            double a[4];
+            float key[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = k0 + j;
+                a[j] = (rv && k < K) ? (xx + pp[k]) - 2.0 * __ldg(HP + (size_t)k * n + row) : 0.0;
+                key[j] = key_sqrt(__double2float_rn(fmax(a[j], 0.0)));
+            }
+            if (rv && A) {
+                if (V4) {
+                    reinterpret_cast<double2*>(A + row * K + k0)[0] = make_double2(a[0], a[1]);
+                    reinterpret_cast<double2*>(A + row * K + k0)[1] = make_double2(a[2], a[3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (k0 + j < K) A[row * K + k0 + j] = a[j];
+                }
+            }
+            if (rv && keys) {
+                if (V4) {
+                    *reinterpret_cast<float4*>(keys + row * K + k0) = make_float4(key[0], key[1], key[2], key[3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (k0 + j < K) keys[row * K + k0 + j] = key[j];
+                }
+            }
             if (minmax) {
-                const unsigned bits = __float_as_uint(key);
-                const unsigned m = __reduce_min_sync(0xffffffffu, rv ? bits : 0x7f7fffffu);
-                const unsigned z = __reduce_max_sync(0xffffffffu, rv ? bits : 0u);
-                if (lane == (k & 31)) {
-                    run_mn[k >> 5] = fminf(run_mn[k >> 5], __uint_as_float(m));
-                    run_mx[k >> 5] = fmaxf(run_mx[k >> 5], __uint_as_float(z));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int k = k0 + j;
+                    if (k < K) {
+                        const unsigned bits = __float_as_uint(key[j]);
+                        const unsigned m = __reduce_min_sync(0xffffffffu, rv ? bits : 0x7f7fffffu);
+                        const unsigned z = __reduce_max_sync(0xffffffffu, rv ? bits : 0u);
+                        if (lane == (k & 31)) {
+                            run_mn[k >> 5] = fminf(run_mn[k >> 5], __uint_as_float(m));
+                            run_mx[k >> 5] = fmaxf(run_mx[k >> 5], __uint_as_float(z));
+                        }
+                    }
                 }
             }
         }
