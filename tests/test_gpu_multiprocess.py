@@ -84,7 +84,7 @@ def _run(world, mode, E, Rel, norm, eps, **opts):
 
 
 @pytest.mark.parametrize("norm,opts", [(2, dict()), (2, dict(pivots=8)), (1, dict(pivots=8)), (2, dict(split=2)),
-                                       (2, dict(tail_shard=1))])
+                                       (2, dict(tail_shard=1)), (2, dict(pivots=96)), (2, dict(pivots=64, tail_shard=1))])
 def test_two_process_shards_gathered(norm, opts):
     E, Rel = generate(3000, 5, 40, seed=81)
     eps = theta_for(E, Rel, norm, 2e-3)
@@ -94,7 +94,8 @@ def test_two_process_shards_gathered(norm, opts):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("norm,opts", [(2, dict()), (2, dict(pivots=8)), (1, dict(pivots=8)), (2, dict(l2_engine=3))])
+@pytest.mark.parametrize("norm,opts", [(2, dict()), (2, dict(pivots=8)), (1, dict(pivots=8)), (2, dict(l2_engine=3)),
+                                       (2, dict(pivots=64))])
 def test_partition_ring_join(world, norm, opts):
     N = 4000
     E, Rel = generate(N, 5, 48, seed=82 + world)

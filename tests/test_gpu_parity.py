@@ -454,7 +454,10 @@ def test_cyclic_split_invariance_multipivot(norm, opts, world):
 # ------------------------------------------------- partition-based join (§4.7)
 @pytest.mark.parametrize("norm,opts", [(2, dict()), (2, dict(l2_engine=3)), (2, dict(l2_engine=2)),
                                        (2, dict(pivots=8)), (2, dict(pivots=8, l2_engine=4)), (1, dict()),
-                                       (1, dict(pivots=8)), (1, dict(l1_engine=1))])
+                                       (1, dict(pivots=8)), (1, dict(l1_engine=1)),
+                                       # many pivots: tails from another array (own entity terms, delta_t)
+                                       (2, dict(pivots=64)), (2, dict(pivots=128, l2_engine=3)),
+                                       (2, dict(pivots=32, l2_engine=4)), (1, dict(pivots=32))])
 @pytest.mark.parametrize("world", [2, 3])
 def test_tail_partition_join(norm, opts, world):
     """tail_shard = 1: rank k joins every query against tails [kN/W, (k+1)N/W) only (PAPER.md:419-422);

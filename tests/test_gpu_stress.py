@@ -207,7 +207,8 @@ def test_offset_1000_uniform_multipivot(norm, K):
 
 # ------------------------------------------------------------------ relation batches
 @pytest.mark.parametrize("rb", [1, 3, 7])
-@pytest.mark.parametrize("norm,opts", [(2, dict()), (2, dict(pivots=8)), (1, dict(pivots=8)), (2, dict(l2_engine=5))])
+@pytest.mark.parametrize("norm,opts", [(2, dict()), (2, dict(pivots=8)), (1, dict(pivots=8)), (2, dict(l2_engine=5)),
+                                       (2, dict(pivots=96)), (1, dict(pivots=32))])
 def test_relation_batches_full_parity(rb, norm, opts):
     """relation_batch = rb: the join runs as consecutive relation batches whose results are
     appended; the set equals the one-pass set and the oracle (c1, full)."""
@@ -223,13 +224,14 @@ def test_relation_batches_full_parity(rb, norm, opts):
 
 
 @pytest.mark.parametrize("split,tail_shard", [(0, 0), (1, 0), (2, 0), (0, 1)])
-def test_relation_batches_sharded(split, tail_shard):
+@pytest.mark.parametrize("K", [8, 64])
+def test_relation_batches_sharded(split, tail_shard, K):
     """Every multi-GPU split mode with relation batches: shards disjoint, union = the one-pass set."""
     E, Rel = generate(3000, 7, 40, seed=44)
     eps = theta_for(E, Rel, 2, 2e-3)
-    full, _ = gpu_join(E, Rel, 2, eps, pivots=8)
+    full, _ = gpu_join(E, Rel, 2, eps, pivots=K)
     W = 3
-    parts = [gpu_join(E, Rel, 2, eps, pivots=8, rank=r, world=W, split=split, tail_shard=tail_shard,
+    parts = [gpu_join(E, Rel, 2, eps, pivots=K, rank=r, world=W, split=split, tail_shard=tail_shard,
                       relation_batch=2)[0] for r in range(W)]
     sets = [keyset(p) for p in parts]
     assert sum(len(s) for s in sets) == len(set().union(*sets))
