@@ -713,11 +713,11 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         // ---- a3: Morton-order sorts (tiles compact in pivot space)
         const int bits = 8;  // per pivot, over the first min(K, MP_SORT_PIVOTS) pivots
         launch_mp_morton(P<float>(ctx->mpkt), P<unsigned>(ctx->mpmm_t), 1, NT, K, bits,
-                         P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
+                         P<unsigned>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
         LAUNCHED(1);
-        const int code_bits = bits * (K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS);
-        radix_sort_u64_segments(1, NT, code_bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
-                                P<unsigned long long>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
+        const int code_bits = bits * (K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS);  // <= 32: 32-bit codes
+        radix_sort_u32_segments(1, NT, code_bits, P<unsigned>(ctx->mpc0), P<unsigned>(ctx->sv0),
+                                P<unsigned>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
                                 ctx->scan_tmp.p, s, &ctx->launches);
         LAUNCHED(0);
         CK(cudaMemcpyAsync(ctx->tperm.p, ctx->sv0.p, (size_t)NT * 4, cudaMemcpyDeviceToDevice, s));
@@ -732,10 +732,10 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
         if (launch_mp_sort_small(qk4, qmm4, R, N, qks, bits, P<int>(ctx->qperm), s)) {  // short segments (c3)
             LAUNCHED(1);
         } else {
-            launch_mp_morton(qk4, qmm4, R, N, qks, bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
+            launch_mp_morton(qk4, qmm4, R, N, qks, bits, P<unsigned>(ctx->mpc0), P<unsigned>(ctx->sv0), s);
             LAUNCHED(1);
-            radix_sort_u64_segments(R, N, code_bits, P<unsigned long long>(ctx->mpc0), P<unsigned>(ctx->sv0),
-                                    P<unsigned long long>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
+            radix_sort_u32_segments(R, N, code_bits, P<unsigned>(ctx->mpc0), P<unsigned>(ctx->sv0),
+                                    P<unsigned>(ctx->mpc1), P<unsigned>(ctx->sv1), P<int>(ctx->counts),
                                     ctx->scan_tmp.p, s, &ctx->launches);
             LAUNCHED(0);
             CK(cudaMemcpyAsync(ctx->qperm.p, ctx->sv0.p, NR * 4, cudaMemcpyDeviceToDevice, s));

@@ -147,6 +147,8 @@ void launch_absmax(const float* E, long long nE, const float* Rel, long long nR,
 void radix_sort_u64_segments(long long S, long long L, int bits, unsigned long long* k0, unsigned int* v0,
                              unsigned long long* k1, unsigned int* v1, int* counts, void* scan_tmp, cudaStream_t s,
                              int* launches);
+void radix_sort_u32_segments(long long S, long long L, int bits, unsigned int* k0, unsigned int* v0, unsigned int* k1,
+                             unsigned int* v1, int* counts, void* scan_tmp, cudaStream_t s, int* launches);
 void launch_pick_pivots(const float* E, long long N, int d, int norm, int K, const double* p0, float* P,
                         cudaStream_t s);
 void launch_mp_keys(const float* E, const float* Rel, long long N, long long nseg, int d, int norm, int K,
@@ -170,7 +172,7 @@ void launch_mp_hr(const float* E, const float* Rel, long long N, long long R, in
 bool launch_mp_sort_small(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
                           int* perm, cudaStream_t s);
 void launch_mp_morton(const float* keys, const unsigned int* minmax, long long nseg, long long L, int K, int bits,
-                      unsigned long long* code, unsigned int* idx, cudaStream_t s);
+                      unsigned int* code, unsigned int* idx, cudaStream_t s);
 void launch_kd_refine(const float* keys, int* perm, long long nseg, long long L, int K, cudaStream_t s);
 void launch_mp_boxes(const float* keys, const unsigned int* perm, long long nseg, long long L, int ROWS, int ntile,
                      int K, float* bmin, float* bmax, const unsigned int* qnmax, cudaStream_t s, int transpose = 0);

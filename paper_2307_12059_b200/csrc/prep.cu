@@ -552,11 +552,12 @@ int radix_sort_segments(const float* keys, const unsigned int* minmax, long long
     return 0;
 }
 
-// Stable LSD sort of S segments of L 64-bit keys (already in k0, values =
-// in-segment indices in v0) on the low `bits` bits; sorted values end in v0.
-void radix_sort_u64_segments(long long S, long long L, int bits, unsigned long long* k0, unsigned int* v0,
-                             unsigned long long* k1, unsigned int* v1, int* counts, void* scan_tmp, cudaStream_t s,
-                             int* launches) {
+// Stable LSD sort of S segments of L keys (already in k0, values = in-segment indices in v0) on
+// the low `bits` bits; sorted values end in v0.  32-bit keys for the K-pivot Hilbert codes (4 x 8
+// bits: 8 bytes per item per scatter instead of 12 with 64-bit keys).
+template <class KeyT>
+static void radix_sort_code_segments(long long S, long long L, int bits, KeyT* k0, unsigned int* v0, KeyT* k1,
+                                     unsigned int* v1, int* counts, void* scan_tmp, cudaStream_t s, int* launches) {
     if (S <= 0 || L <= 0) return;
     const int B = (int)((L + SORT_IPB - 1) / SORT_IPB);
     const size_t nc = (size_t)S * 256 * B;
@@ -564,15 +565,24 @@ void radix_sort_u64_segments(long long S, long long L, int bits, unsigned long l
     int passes = (bits + 7) / 8;
     if (passes & 1) ++passes;  // even pass count: the result lands back in (k0, v0)
     for (int pass = 0; pass < passes; ++pass) {
-        const unsigned long long* ki = (pass & 1) ? k1 : k0;
+        const KeyT* ki = (pass & 1) ? k1 : k0;
         const unsigned int* vi = (pass & 1) ? v1 : v0;
-        unsigned long long* ko = (pass & 1) ? k0 : k1;
+        KeyT* ko = (pass & 1) ? k0 : k1;
         unsigned int* vo = (pass & 1) ? v0 : v1;
-        radix_hist_kernel<unsigned long long><<<g, 256, 0, s>>>(ki, L, B, pass * 8, counts);
+        radix_hist_kernel<KeyT><<<g, 256, 0, s>>>(ki, L, B, pass * 8, counts);
         scan_exclusive_i32(counts, counts, nc, scan_tmp, s, launches);
-        radix_scatter_kernel<unsigned long long><<<g, 256, 0, s>>>(ki, vi, ko, vo, counts, L, B, pass * 8);
+        radix_scatter_kernel<KeyT><<<g, 256, 0, s>>>(ki, vi, ko, vo, counts, L, B, pass * 8);
         if (launches) *launches += 2;
     }
+}
+void radix_sort_u64_segments(long long S, long long L, int bits, unsigned long long* k0, unsigned int* v0,
+                             unsigned long long* k1, unsigned int* v1, int* counts, void* scan_tmp, cudaStream_t s,
+                             int* launches) {
+    radix_sort_code_segments(S, L, bits, k0, v0, k1, v1, counts, scan_tmp, s, launches);
+}
+void radix_sort_u32_segments(long long S, long long L, int bits, unsigned int* k0, unsigned int* v0, unsigned int* k1,
+                             unsigned int* v1, int* counts, void* scan_tmp, cudaStream_t s, int* launches) {
+    radix_sort_code_segments(S, L, bits, k0, v0, k1, v1, counts, scan_tmp, s, launches);
 }
 
 // ============================================================== K3: ranges
