@@ -199,7 +199,7 @@ def workload_name(args, cfg):
 # pivot) -> 7.0 ms (64); c2 takes 32 (the L1 keys support at most 32); the cyclic split spreads c2's
 # hit-dense relations.
 BEST_PIVOTS = {"c1": 1, "c2": 32, "c3": 64, "c4": 96, "c5": 128}
-BEST_SPLIT = {"c2": 2}
+BEST_SPLIT = {"c2": 2, "c3": 3, "c4": 3, "c5": 3}
 DEFAULT_HIT = {"c1": 1e-3, "c2": 1e-4, "c3": 1e-5, "c4": 1e-5, "c5": 1e-6}
 DEFAULT_NORMS = {"c1": "2,1", "c2": "2,1", "c3": "2", "c4": "2", "c5": "2"}
 
@@ -545,7 +545,7 @@ def run_ours(args, cfg, thresholds):
             "data": "synthetic",
             "config": {"workload": wl, "N": N, "R": R, "d": d, "norms": args.norms, "eps": eps, "hit_rate": args.hit,
                        "parallelism": (f"tail partitions x{world}, every query on every rank" if args.tail_shard else
-                                       f"query-tile shards x{world} ({['rank-local', 'cost-balanced', 'cyclic'][args.split]} "
+                                       f"query-tile shards x{world} ({['rank-local', 'cost-balanced', 'cyclic', 'spatial block-cyclic heads'][args.split]} "
                                        f"split), tails replicated; E/Rel NCCL-broadcast from rank 0 every step"),
                        "joins": ("concurrent: one context, stream and host thread per norm" if runner.conc else
                                  "one context per norm on one stream"),
@@ -651,8 +651,9 @@ def main(argv=None):
     ap.add_argument("--tail-shard", type=int, default=0,
                     help="world > 1: 1 = partition-based join (rank k holds tails [kN/W, (k+1)N/W), every query)")
     ap.add_argument("--split", default="auto",
-                    help="world > 1: 0 = rank-local split, 1 = global cost-balanced, 2 = cyclic; auto = best "
-                         "measured per config (c2: 2, its hits concentrate in a few relations)")
+                    help="world > 1: 0 = rank-local split, 1 = global cost-balanced, 2 = cyclic, 3 = spatial "
+                         "block-cyclic heads; auto = best measured per config (c2: 2, its hits concentrate in a "
+                         "few relations; c3 / c4 / c5: 3, DESIGN.md §8)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=None, help="(h,r) rows per reference step")

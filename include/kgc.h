@@ -107,7 +107,14 @@ typedef struct {
                               /* touch; tails are replicated); 1 = global cost-balanced split (every */
                               /* rank preprocesses everything, shards by surviving-tile counts);   */
                               /* 2 = cyclic (every rank preprocesses everything and takes query    */
-                              /* tiles q with q % world == rank: hit-dense relations spread out)    */
+                              /* tiles q with q % world == rank: hit-dense relations spread out);   */
+                              /* 3 = spatial block-cyclic head split (split.cu): every rank orders */
+                              /* the heads along the same space-filling curve (Morton order of the */
+                              /* distances to 4 pivots), cuts it into W*m chunks of ~4096 heads    */
+                              /* (m >= 2) and joins the heads of chunks k, k+W, ... for every       */
+                              /* relation against all N tails; no cost estimate, compact query     */
+                              /* tiles, every rank a stratified sample of the space.  Records carry */
+                              /* global ids; stats.N and triplets are those of the whole join       */
     int32_t tail_shard;       /* world > 1: 1 = partition-based join (§4.7): rank */
                               /* k holds only tails [k N/W, (k+1) N/W) and joins every query       */
                               /* against them (split is ignored); 0 = tails replicated (default)   */

@@ -13,7 +13,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "build"
 LIB = PKG / "libkgc.so"
-SOURCES = ["kgc_api.cu", "prep.cu", "pivots.cu", "tiles_tc.cu", "tiles_tc2.cu", "tiles_simt.cu", "verify.cu", "topk.cu", "se.cu"]
+SOURCES = ["kgc_api.cu", "prep.cu", "pivots.cu", "tiles_tc.cu", "tiles_tc2.cu", "tiles_simt.cu", "verify.cu", "topk.cu", "se.cu", "split.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]

@@ -47,7 +47,8 @@ enum Phase { EV_START, EV_H2D, EV_KEYS, EV_SORT, EV_RANGES, EV_STAGE, EV_TILES, 
     X(est_hist) X(est_cost) X(mpP) X(mpkt) X(mpkq) X(mpmm_t) X(mpmm_q) X(mpc0) X(mpc1) X(tbmin) X(tbmax) X(qbmin) \
     X(qbmax) X(tile_list) X(tk_sample) X(tk_sel) X(tk_cnt) X(Ts) X(tks) X(gblk) X(granges) X(glist) X(tsc) X(gT2) \
     X(gtst) X(tmapbuf) X(fz) X(frt) X(frn) X(fzero) X(se_w) X(se_a64) X(se_b64) X(se_af) X(se_bf) X(se_zero) \
-    X(acc) X(Eb) X(mpbits) X(se_max) X(mpqn) X(mpA) X(mphx) X(mpB) X(mpC) X(mpk4) X(mpmm4) X(mpHP)
+    X(acc) X(Eb) X(mpbits) X(se_max) X(mpqn) X(mpA) X(mphx) X(mpB) X(mpC) X(mpk4) X(mpmm4) X(mpHP) \
+    X(sp_P) X(sp_keys) X(sp_mm) X(sp_c0) X(sp_v0) X(sp_c1) X(sp_v1) X(sp_hidx) X(sp_Eh)
 
 struct kgc_ctx {
     kgc_options opt{};
@@ -245,7 +246,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     kgc_options o;
     if (opt) o = *opt; else kgc_default_options(&o);
     if (o.world < 1 || o.rank < 0 || o.rank >= o.world || (o.pivot != 0 && o.pivot != 1) || o.l2_engine < 0 ||
-        o.l2_engine > 6 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || !mp_pivots_ok(o.pivots) || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 2 || o.tail_shard < 0 || o.tail_shard > 1 || o.relation_batch < 0) {
+        o.l2_engine > 6 || o.chunk_tiles < 0 || o.result_capacity < 0 || o.pivots < 0 || o.pivots > MP_MAX || !mp_pivots_ok(o.pivots) || o.l1_engine < 0 || o.l1_engine > 3 || o.split < 0 || o.split > 3 || o.tail_shard < 0 || o.tail_shard > 1 || o.relation_batch < 0) {
         g_create_err = "kgc_create: invalid options";
         return KGC_EINVAL;
     }
@@ -371,6 +372,7 @@ struct JoinExtra {
     long long Nt = -1;            // tail rows (default: N); tail partitions (kgc_options.tail_shard)
     long long t_off = 0;          // first tail row of the partition (added to emitted t)
     long long h_off = 0;          // first head row of a head block (added to emitted h; kgc_join_block)
+    const int* hmap = nullptr;    // device head ids: emitted h = hmap[local head row] (split = 3)
     float filt_eps = -1.f;        // threshold of every filter and pruning test (default: eps)
     const double* A64 = nullptr;  // exact connectors for verify_se (default: TransE verify)
     const double* B64 = nullptr;
@@ -1035,7 +1037,7 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
                 }
                 launch_verify(P<int2>(ctx->cand), &dctr->cand, ctx->cand_cap, P<int>(ctx->qperm), P<int>(ctx->tperm),
                               E, Rel, Et, N, QT, bq, d, norm, eps, reinterpret_cast<KgcTripletDev*>(ctx->res.p),
-                              &dctr->res, ctx->res_cap, ctx->num_sms, s, r_off, NT, ex.t_off, ex.h_off);
+                              &dctr->res, ctx->res_cap, ctx->num_sms, s, r_off, NT, ex.t_off, ex.h_off, ex.hmap);
             }
             LAUNCHED(1);
         }
@@ -1278,6 +1280,96 @@ static int join_relations(kgc_ctx* ctx, const float* E, const float* Rel, long l
     return KGC_OK;
 }
 
+// Spatial block-cyclic head split (split = 3, split.cu): every rank orders the heads along the
+// same space-filling curve, cuts the order into W * m chunks and keeps chunks k, k + W, ...;
+// their rows are gathered into sp_Eh and their global ids into sp_hidx (the records' h).
+constexpr long long SP_CHUNK = 4096;  // target heads per chunk (c5 emulated W = 8: 1024 -> 0.79,
+                                      // 4096 -> 0.83, 16384 -> 0.80 of linear)
+static int spatial_heads(kgc_ctx* ctx, const float* E, long long N, int d, long long* nh_out) {
+    cudaStream_t s = ctx->stream;
+    const long long W = ctx->opt.world, k = ctx->opt.rank;
+    *nh_out = 0;
+    CK(ensure(ctx->pivot, (size_t)d * 8));  // first curve pivot: the row farthest from the origin
+    CK(cudaMemsetAsync(ctx->pivot.p, 0, (size_t)d * 8, s));
+    CK(ensure(ctx->sp_P, (size_t)4 * d * 4));
+    launch_pick_pivots(E, N, d, 2, 4, P<double>(ctx->pivot), P<float>(ctx->sp_P), s);
+    CK(ensure(ctx->sp_keys, (size_t)N * 16));
+    CK(ensure(ctx->sp_mm, 32));
+    CK(ensure(ctx->sp_c0, (size_t)N * 4));
+    CK(ensure(ctx->sp_v0, (size_t)N * 4));
+    CK(ensure(ctx->sp_c1, (size_t)N * 4));
+    CK(ensure(ctx->sp_v1, (size_t)N * 4));
+    launch_sp_order(E, N, d, P<float>(ctx->sp_P), P<float>(ctx->sp_keys), P<unsigned>(ctx->sp_mm),
+                    P<unsigned>(ctx->sp_c0), P<unsigned>(ctx->sp_v0), s);
+    const size_t nc = std::max<size_t>(radix_counts_len(1, N), 1);
+    CK(ensure(ctx->counts, nc * 4));
+    CK(ensure(ctx->scan_tmp, scan_tmp_bytes(nc)));
+    radix_sort_u32_segments(1, N, 32, P<unsigned>(ctx->sp_c0), P<unsigned>(ctx->sp_v0), P<unsigned>(ctx->sp_c1),
+                            P<unsigned>(ctx->sp_v1), P<int>(ctx->counts), ctx->scan_tmp.p, s, &ctx->launches);
+    LAUNCHED(5);
+    long long m = std::llround((double)N / ((double)W * (double)SP_CHUNK));
+    if (m < 2) m = 2;
+    long long nch = W * m;
+    if (nch > N) nch = N;
+    long long dst = 0, owned = 0, max_len = 0;  // this rank's heads: chunks k, k + W, ...
+    for (long long c = k; c < nch; c += W) {
+        const long long len = (c + 1) * N / nch - c * N / nch;
+        dst += len;
+        max_len = std::max(max_len, len);
+        ++owned;
+    }
+    *nh_out = dst;
+    if (dst == 0) return KGC_OK;
+    CK(ensure(ctx->sp_hidx, (size_t)dst * 4));
+    CK(ensure(ctx->sp_Eh, (size_t)dst * d * 4));
+    launch_sp_gather(E, d, P<unsigned>(ctx->sp_v0), N, nch, W, k, owned, max_len, P<int>(ctx->sp_hidx),
+                     P<float>(ctx->sp_Eh), s);
+    LAUNCHED(1);
+    return KGC_OK;
+}
+
+// split = 3: this rank's heads (chunks of a space-filling curve) against all N tails; records
+// carry the global head ids.
+static int join_spatial(kgc_ctx* ctx, const float* E, const float* Rel, long long N, long long R, int d, int norm,
+                        float eps) {
+    cudaStream_t s = ctx->stream;
+    CK(cudaEventRecord(ctx->ev_split[0], s));
+    const float* Ed = E;
+    long long h2d = 0;
+    if (!is_device_ptr(E, ctx->device)) {
+        CK(ensure(ctx->E, (size_t)N * d * 4));
+        CK(cudaMemcpyAsync(ctx->E.p, E, (size_t)N * d * 4, cudaMemcpyDefault, s));
+        Ed = P<float>(ctx->E);
+        h2d = N * d * 4;
+    }
+    long long nh = 0;
+    int rc = spatial_heads(ctx, Ed, N, d, &nh);
+    if (rc != KGC_OK) return rc;
+    CK(cudaEventRecord(ctx->ev_split[1], s));
+    if (nh == 0) {
+        memset(&ctx->st, 0, sizeof ctx->st);
+        ctx->st.R = R; ctx->st.d = d; ctx->st.norm = norm; ctx->st.eps = eps;
+    } else {
+        JoinExtra ex;
+        ex.Et = Ed;
+        ex.Nt = N;
+        ex.hmap = P<int>(ctx->sp_hidx);
+        // all of this rank's query tiles: the fixed range [0, inf), no further sharding
+        rc = join_relations(ctx, P<float>(ctx->sp_Eh), Rel, nh, R, d, norm, eps, 0, R, 0, LLONG_MAX, 0, ex);
+        if (rc != KGC_OK) return rc;
+    }
+    ctx->st.N = N;
+    ctx->st.triplets = (double)N * (double)N * (double)R;
+    ctx->st.rank = ctx->opt.rank;
+    ctx->st.world = ctx->opt.world;
+    ctx->st.h2d_bytes += h2d;
+    if (nh == 0) {
+        ctx->n_results = 0;
+        ctx->have_join = true;
+    }
+    return KGC_OK;
+}
+
 extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t N, int64_t R, int32_t d, int32_t norm,
                         float eps) {
     if (!ctx) return KGC_EINVAL;
@@ -1356,6 +1448,9 @@ extern "C" int kgc_join(kgc_ctx* ctx, const float* E, const float* Rel, int64_t 
             rc = join_relations(ctx, Ed, Rd, N, R, d, norm, eps, r_lo, r_hi, a, b, QT, JoinExtra());
             ctx->st.h2d_bytes += h2d;
         }
+    } else if (ctx->opt.world > 1 && ctx->opt.split == 3 && !(norm == 2 && ctx->opt.l2_engine == 5)) {
+        did_split = true;
+        rc = join_spatial(ctx, E, Rel, N, R, d, norm, eps);
     } else if (ctx->opt.world > 1 && ctx->opt.split == 2) {
         // Cyclic split: every rank preprocesses everything and takes query tiles q with
         // q % world == rank, so hit-dense relations spread over all ranks.

@@ -244,6 +244,14 @@ void launch_verify(const int2* cand, const unsigned long long* cand_count, long 
                    const int* qperm, const int* tperm, const float* E, const float* Rel, const float* Et, long long N,
                    int QT, int bq, int d, int norm, float theta, KgcTripletDev* out, unsigned long long* res_count,
                    long long res_cap, int num_sms, cudaStream_t s, int r_off, long long Nt = -1, long long t_off = 0,
-                   long long h_off = 0);
+                   long long h_off = 0, const int* hmap = nullptr);
+// spatial block-cyclic head split (split.cu, kgc_options.split = 3): Morton codes of the
+// distances to 4 pivots P (4 x d) in code, entity ids in idx (sort them with
+// radix_sort_u32_segments); then the owned chunks' head ids and rows (chunk c = k + W i of
+// nch equal chunks)
+void launch_sp_order(const float* E, long long N, int d, const float* P, float* keys, unsigned int* mm,
+                     unsigned int* code, unsigned int* idx, cudaStream_t s);
+void launch_sp_gather(const float* E, int d, const unsigned int* order, long long N, long long nch, long long W,
+                      long long k, long long owned, long long max_len, int* hidx, float* Eh, cudaStream_t s);
 
 }  // namespace kgc

@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(256, 2) verify_kernel(const int2* __restrict__
                                                         long long N, int QT, int bq,
                                                         int d, double theta, KgcTripletDev* __restrict__ out,
                                                         unsigned long long* res_count, long long res_cap, int r_off,
-                                                        long long Nt, long long t_off, long long h_off) {
+                                                        long long Nt, long long t_off, long long h_off,
+                                                        const int* __restrict__ hmap) {
     long long nc = (long long)*cand_count;
     if (nc > cand_cap) nc = cand_cap;
     const int lane = threadIdx.x & 31, wib = (threadIdx.x >> 5) & 7;
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(256, 2) verify_kernel(const int2* __restrict__
             const uint32_t m = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 KgcTripletDev o;
-                o.h = (int)(h + h_off);  // global ids: head block / tail partition offsets,
+                o.h = hmap ? hmap[h] : (int)(h + h_off);  // global ids: head map / block / partition offsets,
                 o.r = r + r_off;         // relation index in the caller's Rel
                 o.t = (int)(t + t_off);
                 o.dist = dist;
@@ -219,7 +220,8 @@ void launch_l2_prefetch(const void* p, size_t bytes, int num_sms, cudaStream_t s
 void launch_verify(const int2* cand, const unsigned long long* cand_count, long long cand_cap, const int* qperm,
                    const int* tperm, const float* E, const float* Rel, const float* Et, long long N, int QT, int bq,
                    int d, int norm, float theta, KgcTripletDev* out, unsigned long long* res_count, long long res_cap,
-                   int num_sms, cudaStream_t s, int r_off, long long Nt, long long t_off, long long h_off) {
+                   int num_sms, cudaStream_t s, int r_off, long long Nt, long long t_off, long long h_off,
+                   const int* hmap) {
     const bool vec4 = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(E) | reinterpret_cast<uintptr_t>(Rel) |
                                         reinterpret_cast<uintptr_t>(Et)) % 16 == 0);
     auto kern = norm == 1 ? (vec4 ? verify_kernel<1, true> : verify_kernel<1, false>)
@@ -227,7 +229,8 @@ void launch_verify(const int2* cand, const unsigned long long* cand_count, long 
     const int smem = 8 * VB * 32 * (int)sizeof(KgcTripletDev) + 8 * 2 * 32 * VST * 4 + 8 * 32 * 4;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<num_sms * 4, 256, smem, s>>>(cand, cand_count, cand_cap, qperm, tperm, E, Rel, Et, N, QT, bq, d,
-                                        (double)theta, out, res_count, res_cap, r_off, Nt < 0 ? N : Nt, t_off, h_off);
+                                        (double)theta, out, res_count, res_cap, r_off, Nt < 0 ? N : Nt, t_off, h_off,
+                                        hmap);
 }
 
 }  // namespace kgc
