@@ -84,7 +84,8 @@ def _run(world, mode, E, Rel, norm, eps, **opts):
 
 
 @pytest.mark.parametrize("norm,opts", [(2, dict()), (2, dict(pivots=8)), (1, dict(pivots=8)), (2, dict(split=2)),
-                                       (2, dict(tail_shard=1)), (2, dict(pivots=96)), (2, dict(pivots=64, tail_shard=1))])
+                                       (2, dict(tail_shard=1)), (2, dict(pivots=96)), (2, dict(pivots=64, tail_shard=1)),
+                                       (2, dict(split=3, pivots=96)), (1, dict(split=3, pivots=8))])
 def test_two_process_shards_gathered(norm, opts):
     E, Rel = generate(3000, 5, 40, seed=81)
     eps = theta_for(E, Rel, norm, 2e-3)

@@ -82,7 +82,8 @@ def test_pivot_invariance(norm):
     check_parity(E, Rel, norm, eps, b)
 
 
-@pytest.mark.parametrize("world,split", [(2, 0), (3, 0), (5, 0), (8, 0), (2, 1), (3, 1), (5, 1), (2, 2), (3, 2), (8, 2)])
+@pytest.mark.parametrize("world,split", [(2, 0), (3, 0), (5, 0), (8, 0), (2, 1), (3, 1), (5, 1), (2, 2), (3, 2), (8, 2),
+                                         (2, 3), (5, 3), (8, 3)])
 def test_sharding_invariance(world, split):
     """Union of the shards of `world` contexts == the 1-context set, shards disjoint
     (split 0: rank-local preprocessing of a query-tile range; 1: global cost split; 2: cyclic)."""
