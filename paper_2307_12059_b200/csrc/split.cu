@@ -28,35 +28,65 @@ static inline unsigned sp_grid(long long n, int threads, long long cap = 148LL *
 constexpr int SP_K = 4;     // pivots of the space-filling curve
 constexpr int SP_BITS = 8;  // bits per pivot key (32-bit codes)
 
-// warp per entity: the SP_K FP32 distances to the pivots (lanes over k), min / max per pivot
-// as float bits (distances are >= 0, so the unsigned order is the float order)
+// warp per 4 entities: the SP_K FP32 distances to the pivots (lanes over k, float4 loads of the 4
+// rows in flight when d % 4 == 0), min / max per pivot as float bits (distances are >= 0, so the
+// unsigned order is the float order)
+constexpr int SP_R = 4;  // rows per warp step
 __global__ void __launch_bounds__(256) sp_keys_kernel(const float* __restrict__ E, long long N, int d,
                                                       const float* __restrict__ P, float* __restrict__ keys,
                                                       unsigned int* __restrict__ mm) {
     const int lane = threadIdx.x & 31;
     const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(E) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(P) & 15) == 0;
     float mn[SP_K], mx[SP_K];
 #pragma unroll
     for (int j = 0; j < SP_K; ++j) { mn[j] = FLT_MAX; mx[j] = 0.f; }
-    for (long long i = w0; i < N; i += nw) {
-        float acc[SP_K] = {};
-        for (int k = lane; k < d; k += 32) {
-            const float v = E[i * d + k];
+    for (long long i0 = w0 * SP_R; i0 < N; i0 += nw * SP_R) {
+        float acc[SP_R][SP_K] = {};
+        if (vec) {
+            for (int k = 4 * lane; k < d; k += 128) {
+                float4 v[SP_R];
 #pragma unroll
-            for (int j = 0; j < SP_K; ++j) {
-                const float t = v - P[j * d + k];
-                acc[j] = fmaf(t, t, acc[j]);
+                for (int u = 0; u < SP_R; ++u)
+                    v[u] = i0 + u < N ? __ldg(reinterpret_cast<const float4*>(E + (i0 + u) * d + k))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < SP_K; ++j) {
+                    const float4 p = __ldg(reinterpret_cast<const float4*>(P + j * d + k));
+#pragma unroll
+                    for (int u = 0; u < SP_R; ++u) {
+                        const float a = v[u].x - p.x, b = v[u].y - p.y, c = v[u].z - p.z, e = v[u].w - p.w;
+                        acc[u][j] = fmaf(a, a, fmaf(b, b, fmaf(c, c, fmaf(e, e, acc[u][j]))));
+                    }
+                }
+            }
+        } else {
+            for (int k = lane; k < d; k += 32) {
+#pragma unroll
+                for (int u = 0; u < SP_R; ++u) {
+                    const float v = i0 + u < N ? E[(i0 + u) * d + k] : 0.f;
+#pragma unroll
+                    for (int j = 0; j < SP_K; ++j) {
+                        const float t = v - P[j * d + k];
+                        acc[u][j] = fmaf(t, t, acc[u][j]);
+                    }
+                }
             }
         }
 #pragma unroll
-        for (int j = 0; j < SP_K; ++j) {
-            float a = acc[j];
-            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-            a = sqrtf(a);
-            if (lane == j) keys[i * SP_K + j] = a;
-            mn[j] = fminf(mn[j], a);
-            mx[j] = fmaxf(mx[j], a);
+        for (int u = 0; u < SP_R; ++u) {
+            if (i0 + u >= N) break;
+#pragma unroll
+            for (int j = 0; j < SP_K; ++j) {
+                float a = acc[u][j];
+                for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+                a = sqrtf(a);
+                if (lane == j) keys[(i0 + u) * SP_K + j] = a;
+                mn[j] = fminf(mn[j], a);
+                mx[j] = fmaxf(mx[j], a);
+            }
         }
     }
     if (lane < SP_K) {
@@ -121,7 +151,7 @@ __global__ void __launch_bounds__(256) sp_gather_kernel(const float* __restrict_
 void launch_sp_order(const float* E, long long N, int d, const float* P, float* keys, unsigned int* mm,
                      unsigned int* code, unsigned int* idx, cudaStream_t s) {
     sp_init_kernel<<<1, 32, 0, s>>>(mm);
-    sp_keys_kernel<<<sp_grid(N * 32, 256, 148 * 8), 256, 0, s>>>(E, N, d, P, keys, mm);
+    sp_keys_kernel<<<sp_grid((N + SP_R - 1) / SP_R * 32, 256, 148 * 8), 256, 0, s>>>(E, N, d, P, keys, mm);
     sp_code_kernel<<<sp_grid(N, 256), 256, 0, s>>>(keys, N, mm, code, idx);
 }
 
