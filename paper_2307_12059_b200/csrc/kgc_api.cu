@@ -1284,7 +1284,8 @@ static int join_relations(kgc_ctx* ctx, const float* E, const float* Rel, long l
 // same space-filling curve, cuts the order into W * m chunks and keeps chunks k, k + W, ...;
 // their rows are gathered into sp_Eh and their global ids into sp_hidx (the records' h).
 constexpr long long SP_CHUNK = 4096;  // target heads per chunk (c5 emulated W = 8: 1024 -> 0.79,
-                                      // 4096 -> 0.83, 16384 -> 0.80 of linear)
+                                      // 4096 -> 0.84-0.87, 8192 -> 0.87-0.88 but c4 2.90 -> 2.98 ms,
+                                      // 16384 -> 0.80 of linear)
 static int spatial_heads(kgc_ctx* ctx, const float* E, long long N, int d, long long* nh_out) {
     cudaStream_t s = ctx->stream;
     const long long W = ctx->opt.world, k = ctx->opt.rank;
