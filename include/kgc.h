@@ -248,6 +248,17 @@ int64_t kgc_inspect(kgc_ctx* ctx, int32_t what, void* out, int64_t bytes);
 int64_t kgc_shard_range(const int64_t* cum, int64_t n, int64_t total, int32_t rank, int32_t world,
                         int64_t* begin, int64_t* end);
 
+/* Pure host function (no device needed), used by split = 3: the chunks of the
+ * space-filling-curve order of N heads that `rank` of `world` joins.  The order
+ * is cut into nch = min(N, world * m) equal chunks, m = max(2, round(N / (world *
+ * chunk))) (chunk: target heads per chunk; the library uses 4096), chunk c spans
+ * sorted positions [c N / nch, (c + 1) N / nch) and belongs to rank c mod world.
+ * Writes up to `cap` (begin, len) pairs in chunk order and returns the number of
+ * chunks the rank owns (call with cap = 0 to size the arrays), or KGC_EINVAL.
+ * Over all ranks the chunks partition [0, N) exactly. */
+int64_t kgc_spatial_chunks(int64_t N, int32_t world, int32_t rank, int64_t chunk, int64_t* begin, int64_t* len,
+                           int64_t cap);
+
 /* One block of the partition-based join (PAPER.md:419-422 [§4.7]: "divide both
  * datasets into several partitions ... join each pair of partitions"): every
  * (h, r, t) with h in [h_off, h_off + Nh), t in [t_off, t_off + Nt), r in [0, R) and

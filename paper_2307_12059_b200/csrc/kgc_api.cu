@@ -335,6 +335,31 @@ int kgc_set_stream(kgc_ctx* ctx, void* stream) {
     return KGC_OK;
 }
 
+}  // extern "C"
+// split = 3: the curve order is cut into nch = W m equal chunks, m = max(2, round(N / (W chunk)))
+static int64_t sp_nchunks(int64_t N, int64_t world, int64_t chunk) {
+    int64_t m = (int64_t)std::llround((double)N / ((double)world * (double)chunk));
+    if (m < 2) m = 2;
+    return std::min<int64_t>(N, world * m);
+}
+extern "C" {
+
+int64_t kgc_spatial_chunks(int64_t N, int32_t world, int32_t rank, int64_t chunk, int64_t* begin, int64_t* len,
+                           int64_t cap) {
+    if (N < 0 || world < 1 || rank < 0 || rank >= world || chunk < 1 || cap < 0 || (cap > 0 && (!begin || !len)))
+        return KGC_EINVAL;
+    if (N == 0) return 0;
+    const int64_t nch = sp_nchunks(N, world, chunk);
+    int64_t owned = 0;
+    for (int64_t c = rank; c < nch; c += world, ++owned) {
+        if (owned < cap) {
+            begin[owned] = c * N / nch;
+            len[owned] = (c + 1) * N / nch - c * N / nch;
+        }
+    }
+    return owned;
+}
+
 int64_t kgc_shard_range(const int64_t* cum, int64_t n, int64_t total, int32_t rank, int32_t world, int64_t* begin,
                         int64_t* end) {
     if (!cum || !begin || !end || n < 0 || total < 0 || world < 1 || rank < 0 || rank >= world) return KGC_EINVAL;
@@ -1308,17 +1333,16 @@ static int spatial_heads(kgc_ctx* ctx, const float* E, long long N, int d, long 
     radix_sort_u32_segments(1, N, 32, P<unsigned>(ctx->sp_c0), P<unsigned>(ctx->sp_v0), P<unsigned>(ctx->sp_c1),
                             P<unsigned>(ctx->sp_v1), P<int>(ctx->counts), ctx->scan_tmp.p, s, &ctx->launches);
     LAUNCHED(5);
-    long long m = std::llround((double)N / ((double)W * (double)SP_CHUNK));
-    if (m < 2) m = 2;
-    long long nch = W * m;
-    if (nch > N) nch = N;
-    long long dst = 0, owned = 0, max_len = 0;  // this rank's heads: chunks k, k + W, ...
-    for (long long c = k; c < nch; c += W) {
-        const long long len = (c + 1) * N / nch - c * N / nch;
-        dst += len;
-        max_len = std::max(max_len, len);
-        ++owned;
+    // the chunks of this rank (kgc_spatial_chunks: the same rule on the host, tested on the CPU)
+    const long long owned = kgc_spatial_chunks(N, (int32_t)W, (int32_t)k, SP_CHUNK, nullptr, nullptr, 0);
+    std::vector<int64_t> cb((size_t)std::max(owned, 1LL)), cl((size_t)std::max(owned, 1LL));
+    kgc_spatial_chunks(N, (int32_t)W, (int32_t)k, SP_CHUNK, cb.data(), cl.data(), owned);
+    long long dst = 0, max_len = 0;
+    for (long long i = 0; i < owned; ++i) {
+        dst += cl[(size_t)i];
+        max_len = std::max<long long>(max_len, cl[(size_t)i]);
     }
+    const long long nch = sp_nchunks(N, W, SP_CHUNK);
     *nh_out = dst;
     if (dst == 0) return KGC_OK;
     CK(ensure(ctx->sp_hidx, (size_t)dst * 4));

@@ -60,7 +60,7 @@ class kgc_stats_t(ctypes.Structure):
 
 EXPORTS = ["kgc_abi_version", "kgc_default_options", "kgc_create", "kgc_join", "kgc_results", "kgc_stats",
            "kgc_last_error", "kgc_set_stream", "kgc_destroy", "kgc_inspect", "kgc_shard_range", "kgc_topk",
-           "kgc_join_se", "kgc_join_block"]
+           "kgc_join_se", "kgc_join_block", "kgc_spatial_chunks"]
 
 _lib = None
 
@@ -96,6 +96,8 @@ def load_library(path: str | Path | None = None):
     L.kgc_inspect.restype = i64
     L.kgc_shard_range.argtypes = [vp, i64, i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.kgc_shard_range.restype = i64
+    L.kgc_spatial_chunks.argtypes = [i64, i32, i32, i64, vp, vp, i64]
+    L.kgc_spatial_chunks.restype = i64
     L.kgc_topk.argtypes = [vp, vp, vp, i64, i64, i32, i32, i64, i32, vp]
     L.kgc_topk.restype = i64
     L.kgc_join_se.argtypes = [vp, vp, vp, vp, i64, i64, i32, ctypes.c_float]
@@ -227,6 +229,17 @@ def kgc_shard_range(cum, total: int, rank: int, world: int):
     if cost < 0:
         raise KgcError(int(cost), "kgc_shard_range: invalid argument")
     return int(b.value), int(e.value), int(cost)
+
+
+def kgc_spatial_chunks(N: int, world: int, rank: int, chunk: int = 4096):
+    """Pure host function (split = 3): the (begin, len) chunks of the curve order that `rank` joins."""
+    L = load_library()
+    n = L.kgc_spatial_chunks(int(N), int(world), int(rank), int(chunk), None, None, 0)
+    if n < 0:
+        raise KgcError(int(n), "kgc_spatial_chunks: invalid argument")
+    b, ln = np.zeros(max(n, 1), dtype=np.int64), np.zeros(max(n, 1), dtype=np.int64)
+    L.kgc_spatial_chunks(int(N), int(world), int(rank), int(chunk), b.ctypes.data, ln.ctypes.data, n)
+    return b[:n], ln[:n]
 
 
 def kgc_topk(ctx, E, Rel, N: int, R: int, d: int, norm: int, k: int, exclude_self: bool = False, out=None):

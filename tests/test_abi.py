@@ -122,3 +122,40 @@ def test_shard_range_rejects_bad_args():
     from paper_2307_12059_b200 import kgc
     with pytest.raises(kgc.KgcError):
         kgc.kgc_shard_range([0, 1], 2, 3, 2)
+
+
+@pytest.mark.parametrize("N,world,chunk", [(0, 3, 4096), (1, 1, 4096), (5, 8, 4096), (2500, 4, 4096),
+                                           (14951, 8, 4096), (123182, 8, 4096), (1000000, 8, 4096),
+                                           (1000000, 3, 1000), (77777, 5, 8192)])
+def test_spatial_chunks_partition(N, world, chunk):
+    """split = 3 host rule (include/kgc.h): over all ranks the chunks partition [0, N) exactly,
+    every rank owns m or fewer chunks dealt c mod world, chunk sizes differ by at most one, and
+    every rank's head count is within one chunk of N / world."""
+    from paper_2307_12059_b200 import kgc
+    seen = np.zeros(N, dtype=np.int64)
+    heads = []
+    sizes = []
+    for rank in range(world):
+        b, ln = kgc.kgc_spatial_chunks(N, world, rank, chunk)
+        for x, y in zip(b, ln):
+            assert y >= 1
+            seen[x:x + y] += 1
+            sizes.append(int(y))
+        if len(b) > 1:
+            assert np.all(np.diff(b) > 0)          # chunk order
+        heads.append(int(ln.sum()))
+    assert np.all(seen == 1)                        # exact partition
+    if sizes:
+        assert max(sizes) - min(sizes) <= 1
+        assert max(heads) - min(heads) <= max(sizes)
+        m = max(2, round(N / (world * chunk)))
+        assert len(sizes) == min(N, world * m)
+
+
+def test_spatial_chunks_rejects_bad_args():
+    from paper_2307_12059_b200 import kgc
+    for args in [(-1, 2, 0), (10, 0, 0), (10, 2, 2), (10, 2, -1)]:
+        with pytest.raises(kgc.KgcError):
+            kgc.kgc_spatial_chunks(*args)
+    with pytest.raises(kgc.KgcError):
+        kgc.kgc_spatial_chunks(10, 2, 0, chunk=0)
