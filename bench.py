@@ -12,7 +12,9 @@ hit rate 1e-5), the largest BASELINE.json config that fits one GPU's
 single-GPU line (c5 is the 8-GPU config).  The same JSON line also carries
 `extra_workloads`: the c2 L2+L1 step (WN18-shaped, both norms) and the c3
 theta sweep (FB15k-shaped, hit rates 1e-6..1e-3; the analogue of the paper's
-epsilon sweep), each timed the same way.
+epsilon sweep), each timed the same way, and
+`projected_scaling`: every shard of a 2/4/8-rank c4 and c5 join (split 3) in turn
+on this GPU, max shard device time -- a projection, not a multi-GPU measurement.
 
 metric = candidate triplets / s = (N * N * R per join, summed over the joins)
 / device time of the step; whole-job value over all ranks (query tiles are
@@ -534,6 +536,9 @@ def run_ours(args, cfg, thresholds):
                 continue
             extras.append(measure_workload(torch, kgc, dev, stream, name, norms, hit, args.extra_steps, 3,
                                            thresholds, flush))
+    scaling = None
+    if rank == 0 and world == 1 and not args.no_extras and not args.no_scaling:
+        scaling = projected_scaling(torch, kgc, dev, stream, thresholds, flush)
     clocks = clk.summary()
     if rank == 0:
         line = {
@@ -566,6 +571,7 @@ def run_ours(args, cfg, thresholds):
             "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "wall_s_timed_region": wall,
             "extra_workloads": extras,
+            "projected_scaling": scaling,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -622,6 +628,49 @@ def run_emulated_ranks(args, cfg, thresholds):
     return 0
 
 
+def projected_scaling(torch, kgc, dev, stream, thresholds, flush, names=("c4", "c5"), Ws=(2, 4, 8), steps=3):
+    """Projected multi-GPU device times (diagnostic, one GPU): every shard of a W-rank join in turn
+    (the bench's split and pivots per config), max shard device time (CUDA events, L2 flushed before
+    each step) against the one-GPU join; the data path has no collective to leave out."""
+    out = {"method": "each of W shards in turn on this GPU; projected W-GPU time = max shard device time "
+                     "(broadcast / count all-reduce excluded); efficiency = t1 / (W tW)", "workloads": {}}
+
+    def timed(j, Et, Rt, eps):
+        j.run(Et, Rt, 2, eps)
+        ts = []
+        for _ in range(steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            j.run(Et, Rt, 2, eps)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.mean(ts)
+
+    for name in names:
+        hit = DEFAULT_HIT[name]
+        eps = float(thresholds[name][f"L2@{hit:g}"]["theta"])
+        E_h, Rel_h = generate_config(name)
+        Et, Rt = torch.from_numpy(E_h).to(dev), torch.from_numpy(Rel_h).to(dev)
+        piv, split = BEST_PIVOTS.get(name, 1), BEST_SPLIT.get(name, 0)
+        with kgc.Join(device=dev.index, pivots=piv, stream=stream.cuda_stream) as j:
+            t1 = timed(j, Et, Rt, eps)
+        w = {"split": split, "pivots": piv, "hit_rate": hit, "ms": {"1": t1}, "shard_ms": {}, "efficiency": {}}
+        for W in Ws:
+            sh = []
+            for rank in range(W):
+                with kgc.Join(device=dev.index, pivots=piv, rank=rank, world=W, split=split,
+                              stream=stream.cuda_stream) as j:
+                    sh.append(timed(j, Et, Rt, eps))
+            w["ms"][str(W)] = max(sh)
+            w["shard_ms"][str(W)] = sh
+            w["efficiency"][str(W)] = t1 / (W * max(sh))
+        out["workloads"][name] = w
+        del Et, Rt
+    return out
+
+
 def relaunch_distributed(args_argv, n):
     """--gpus N without a launcher: re-execute this script under torch.distributed.run
     (one process per GPU on this node, rendezvous on 127.0.0.1)."""
@@ -647,6 +696,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the c2 step / c3 sweep extra workloads")
     ap.add_argument("--extra-steps", type=int, default=5)
+    ap.add_argument("--no-scaling", action="store_true",
+                    help="skip the projected 2/4/8-GPU shard timings (c4, c5) of the N=1 line")
     ap.add_argument("--sequential", action="store_true", help="run the step's joins one after the other")
     ap.add_argument("--tail-shard", type=int, default=0,
                     help="world > 1: 1 = partition-based join (rank k holds tails [kN/W, (k+1)N/W), every query)")
