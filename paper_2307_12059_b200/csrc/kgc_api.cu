@@ -67,6 +67,8 @@ struct kgc_ctx {
     cudaEvent_t ev_split[2] = {};
     cudaStream_t aux = nullptr;     // fork / join stream for pivot-independent work (the h.r GEMM)
     cudaEvent_t ev_fork[2] = {};
+    cudaEvent_t ev_sp[2] = {};    // split 3: the head order on the aux stream beside the pivot choice
+    bool pivots_ready = false;    // split 3: mpP already holds this join's pivots (launched on stream)
     int launches = 0;
     // geometry of the last join (for kgc_inspect)
     long long N = 0, R = 0;
@@ -290,6 +292,7 @@ int kgc_create(kgc_ctx** out, const kgc_options* opt) {
     for (auto& e : ctx->ev_split) cudaEventCreate(&e);
     cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
     for (auto& e : ctx->ev_fork) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    for (auto& e : ctx->ev_sp) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     cudaSetDevice(prev);
     *out = ctx;
     return KGC_OK;
@@ -307,6 +310,8 @@ void kgc_destroy(kgc_ctx* ctx) {
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_split)
+        if (e) cudaEventDestroy(e);
+    for (auto e : ctx->ev_sp)
         if (e) cudaEventDestroy(e);
     for (auto e : ctx->ev_fork)
         if (e) cudaEventDestroy(e);
@@ -712,8 +717,10 @@ static int join_impl(kgc_ctx* ctx, const float* E_in, const float* Rel_in, long 
             CK(cudaEventRecord(ctx->ev_fork[1], ctx->aux));
             LAUNCHED(1);
         }
-        launch_pick_pivots(Et, NT, d, norm, K, pivot, P<float>(ctx->mpP), s);
-        LAUNCHED(1);
+        if (!ctx->pivots_ready) {  // split 3 launched it already, beside the head order
+            launch_pick_pivots(Et, NT, d, norm, K, pivot, P<float>(ctx->mpP), s);
+            LAUNCHED(1);
+        }
         if (norm == 2) {  // FP64 factorisation: one h.r dot product per query row instead of K distances
             const int KO = K < MP_SORT_PIVOTS ? K : MP_SORT_PIVOTS;
             CK(ensure(ctx->mpA, (size_t)N * K * 8));
@@ -1311,8 +1318,7 @@ static int join_relations(kgc_ctx* ctx, const float* E, const float* Rel, long l
 constexpr long long SP_CHUNK = 4096;  // target heads per chunk (c5 emulated W = 8: 1024 -> 0.79,
                                       // 4096 -> 0.84-0.87, 8192 -> 0.87-0.88 but c4 2.90 -> 2.98 ms,
                                       // 16384 -> 0.80 of linear)
-static int spatial_heads(kgc_ctx* ctx, const float* E, long long N, int d, long long* nh_out) {
-    cudaStream_t s = ctx->stream;
+static int spatial_heads(kgc_ctx* ctx, const float* E, long long N, int d, long long* nh_out, cudaStream_t s) {
     const long long W = ctx->opt.world, k = ctx->opt.rank;
     *nh_out = 0;
     CK(ensure(ctx->pivot, (size_t)d * 8));  // first curve pivot: the row farthest from the origin
@@ -1367,11 +1373,26 @@ static int join_spatial(kgc_ctx* ctx, const float* E, const float* Rel, long lon
         Ed = P<float>(ctx->E);
         h2d = N * d * 4;
     }
+    // The join's own pivot choice (one CTA, tails only) on the stream, the head order (every other
+    // SM) on the aux stream beside it; the join waits for both.
+    const int K = (ctx->opt.pivots >= 2 && ctx->opt.prune && d <= MP_MAX_DIM) ? ctx->opt.pivots : 1;
+    const bool pre = K > 1 && ctx->opt.pivot == 0 && !(norm == 1 && K > MP_MAX_L1);
+    CK(cudaEventRecord(ctx->ev_sp[0], s));  // inputs ready (before the pivot choice: the two overlap)
+    CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_sp[0], 0));
+    if (pre) {
+        CK(ensure(ctx->mpP, (size_t)K * d * 4));
+        launch_pick_pivots(Ed, N, d, norm, K, nullptr, P<float>(ctx->mpP), s);
+        LAUNCHED(1);
+    }
     long long nh = 0;
-    int rc = spatial_heads(ctx, Ed, N, d, &nh);
+    int rc = spatial_heads(ctx, Ed, N, d, &nh, ctx->aux);
     if (rc != KGC_OK) return rc;
-    CK(cudaEventRecord(ctx->ev_split[1], s));
+    CK(cudaEventRecord(ctx->ev_split[1], ctx->aux));
+    CK(cudaEventRecord(ctx->ev_sp[1], ctx->aux));
+    CK(cudaStreamWaitEvent(s, ctx->ev_sp[1], 0));
+    ctx->pivots_ready = pre;
     if (nh == 0) {
+        ctx->pivots_ready = false;
         memset(&ctx->st, 0, sizeof ctx->st);
         ctx->st.R = R; ctx->st.d = d; ctx->st.norm = norm; ctx->st.eps = eps;
     } else {
@@ -1381,6 +1402,7 @@ static int join_spatial(kgc_ctx* ctx, const float* E, const float* Rel, long lon
         ex.hmap = P<int>(ctx->sp_hidx);
         // all of this rank's query tiles: the fixed range [0, inf), no further sharding
         rc = join_relations(ctx, P<float>(ctx->sp_Eh), Rel, nh, R, d, norm, eps, 0, R, 0, LLONG_MAX, 0, ex);
+        ctx->pivots_ready = false;
         if (rc != KGC_OK) return rc;
     }
     ctx->st.N = N;
